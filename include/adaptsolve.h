@@ -1,0 +1,183 @@
+/*
+ * adaptsolve.h -- C ABI of libadaptsolve.so, a B200-native (sm_100a)
+ * implementation of the adaptive solver for A X = B of
+ *   C. Sanderson, R. Curtin, "An Adaptive Solver for Systems of Linear
+ *   Equations", arXiv 2007.11208 (cited as P:<line> of PAPER.md).
+ *
+ * The operation (Eq. 1/2 with m = n): given a square n x n matrix A
+ * and n x nrhs right-hand sides B, find X with A X = B.  The solver detects,
+ * in this order, a banded structure, a lower or upper
+ * triangular structure, or a likely symmetric positive definite
+ * matrix (Fig. 4), and uses banded LU, triangular
+ * substitution (Eq. 3), Cholesky (on failure the general
+ * solver) or LU with partial pivoting.  Each path estimates the
+ * 1-norm reciprocal condition number; if a factorization fails or
+ * rcond < 0.5 eps an SVD-based minimum-norm solution is computed
+ * instead, unless disabled.
+ *
+ * Conventions (all entry points):
+ *  - Storage: column-major, element (i,j) at base[i + j*ld], zero-based
+ *    (P:120-126).
+ *  - Residency: A, B, X are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    unless the entry point says otherwise.  Host out-pointers (info_flags,
+ *    rcond, report) may be NULL.
+ *  - Ownership: A and B are read-only and owned by the caller.  X is owned by
+ *    the caller and must hold ldb*nrhs elements; X == B (exact alias, in-place
+ *    solve) is allowed, any other overlap is undefined.  Factors live in a
+ *    library-owned workspace cached per (device, stream, dtype, n, nrhs, lda,
+ *    ldb, options) and released by as_release_all().
+ *  - Streams: all device work is enqueued on `stream`; the call synchronizes
+ *    that stream exactly once (to read the device-resident report), and not at
+ *    all for as_solve_async().
+ *  - Errors: 0 = X valid; -i = the i-th argument is illegal (LAPACK
+ *    convention, nothing enqueued); positive AS_ERR_* codes below; CUDA errors
+ *    are returned as AS_ERR_CUDA_BASE + cudaError_t.
+ */
+#ifndef ADAPTSOLVE_H
+#define ADAPTSOLVE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
+
+/* ---- info_flags bits ---------------------------------------------------- */
+/* bits 0-3: literal detection verdicts; each is the exact
+ * predicate of the paper, evaluated on the whole matrix (bit-exact vs the
+ * oracle).  After an early exit (all four false) they are all 0. */
+#define AS_FLAG_BANDED        0x1u   /* band capacity <= 25% of n^2 (Z2/Z3) */
+#define AS_FLAG_LOWER         0x2u   /* all elements above the diagonal are 0 */
+#define AS_FLAG_UPPER         0x4u   /* all elements below the diagonal are 0 */
+#define AS_FLAG_SPD_CANDIDATE 0x8u   /* Fig. 4 likely_sympd returned true */
+/* bits 4-7: method that produced X (AS_METHOD_*) */
+#define AS_FLAG_METHOD_SHIFT  4
+#define AS_FLAG_METHOD_MASK   0xF0u
+#define AS_FLAG_CHOL_FAILED   (1u << 8)   /* POTRF failed -> general LU */
+#define AS_FLAG_SINGULAR      (1u << 9)   /* primary factor had an exact zero pivot */
+#define AS_FLAG_RCOND_LOW     (1u << 10)  /* the gate fired: singular or !(rcond >= thr) */
+#define AS_FLAG_FALLBACK      (1u << 11)  /* X is the SVD minimum-norm solution */
+#define AS_FLAG_POORLY_COND   (1u << 12)  /* gate fired with AS_OPT_NO_FALLBACK: X is the primary solution */
+#define AS_FLAG_SVD_NOCONV    (1u << 14)  /* Jacobi hit max_sweeps */
+#define AS_FLAG_RANK_DEF      (1u << 15)  /* fallback effective rank < n */
+
+/* ---- methods ------------------------------------------------------------- */
+#define AS_METHOD_NONE      0
+#define AS_METHOD_BAND      1   /* GBTRF/GBCON/GBTRS */
+#define AS_METHOD_TRI_LOWER 2   /* TRCON/TRTRS, forward substitution (Eq. 3) */
+#define AS_METHOD_TRI_UPPER 3   /* TRCON/TRTRS, back-substitution */
+#define AS_METHOD_CHOL      4   /* POTRF/POCON/POTRS */
+#define AS_METHOD_LU        5   /* GETRF/GECON/GETRS */
+#define AS_METHOD_SVD       6   /* QR + one-sided Jacobi min-norm */
+
+/* ---- options ------------------------------------------------------------- */
+#define AS_OPT_NO_FALLBACK  0x1u   /* disable the SVD fallback */
+#define AS_OPT_FORCE_METHOD 0x2u   /* use opt.force_method (1..5) instead of the detected one */
+#define AS_OPT_FULLSCAN     0x8u   /* detection never exits early; kl/ku always exact */
+
+/* ---- return codes ------------------------------------------------------- */
+#define AS_OK                        0
+#define AS_ERR_SINGULAR_NO_FALLBACK  1   /* exact zero pivot and NO_FALLBACK: X unspecified */
+#define AS_ERR_SVD_NOT_CONVERGED     2   /* fallback Jacobi hit max_sweeps (X is its last iterate) */
+#define AS_ERR_NOT_IMPLEMENTED       4
+#define AS_ERR_NO_DEVICE             5
+#define AS_ERR_CUDA_BASE             1000
+
+typedef struct {
+    uint32_t flags;            /* AS_OPT_* */
+    int32_t force_method;      /* AS_METHOD_BAND..AS_METHOD_LU when AS_OPT_FORCE_METHOD */
+    double rcond_threshold;    /* < 0: 0.5 eps of the dtype */
+    double lsq_cutoff;         /* < 0: n*eps (Z14): keep sigma_k > cut * sigma_max */
+    int32_t max_sweeps;        /* <= 0: 30 */
+    int32_t reserved;
+} as_options;
+
+typedef struct {
+    uint32_t flags;            /* AS_FLAG_* as above */
+    int32_t method;            /* method that produced X (AS_METHOD_*) */
+    int32_t primary_method;    /* structured / LU path that ran (before any fallback) */
+    int32_t sweeps;            /* Jacobi sweeps executed by the fallback (0 otherwise) */
+    int64_t kl, ku;            /* band extent; -1 unless banded (exact always with FULLSCAN) */
+    double rcond;              /* primary path's estimate (0 if singular); never the SVD's (Z25) */
+    double anorm;              /* 1-norm of A used by the estimate */
+    int64_t rank;              /* fallback effective rank, -1 if the fallback did not run */
+    int64_t info;              /* 1 + first zero-pivot column of the primary factor, else 0 */
+    int64_t chol_fail_col;     /* 0-based column where POTRF failed (valid with CHOL_FAILED) */
+} as_report;
+
+typedef struct {
+    uint32_t flags;            /* AS_FLAG_BANDED | LOWER | UPPER | SPD_CANDIDATE */
+    int32_t method;            /* first-match dispatch */
+    int64_t kl, ku;            /* exact if banded or FULLSCAN, else -1 */
+    double max_diag;           /* Fig. 4 max_diag (largest positive diagonal entry) */
+} as_structure;
+
+/*
+ * as_solve: the north-star entry point.  Solves A X = B adaptively.
+ *   dt        AS_F64 (double) or AS_F32 (float); all buffers of that type.
+ *   A         device, n x n, column-major, lda >= max(1,n); read-only.
+ *   B         device, n x nrhs, ldb >= max(1,n); read-only (unless X == B).
+ *   X         device, n x nrhs with leading dimension ldb (no separate ldx).
+ *   info_flags host, may be NULL: AS_FLAG_* of the report.
+ *   rcond     host, may be NULL: report.rcond.
+ *   stream    cudaStream_t (0 = legacy default stream).
+ * Returns AS_OK / AS_ERR_* / -i.  n == 0 or nrhs == 0: returns 0 at once with
+ * flags 0 and rcond 1.
+ */
+int as_solve(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+             void* X, uint32_t* info_flags, double* rcond, void* stream);
+int as_solve_f64(const double* A, int64_t lda, int64_t n, const double* B, int64_t ldb, int64_t nrhs,
+                 double* X, uint32_t* info_flags, double* rcond, void* stream);
+int as_solve_f32(const float* A, int64_t lda, int64_t n, const float* B, int64_t ldb, int64_t nrhs,
+                 float* X, uint32_t* info_flags, double* rcond, void* stream);
+
+/* as_solve_ex: as_solve with options (opt may be NULL = defaults) and the
+ * full report (rep, host, may be NULL).  sigma_out: optional DEVICE buffer of
+ * n elements (dtype) receiving the fallback's singular values, descending
+ * (untouched if the fallback does not run). */
+int as_solve_ex(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+                void* X, const as_options* opt, as_report* rep, void* sigma_out, void* stream);
+
+/* as_solve_async: enqueue the whole adaptive solve (one CUDA-graph launch,
+ * dispatch on device-resident flags) and return without synchronizing.  The
+ * report is written to `rep_dev` (a DEVICE as_report*, may be NULL) when the
+ * stream reaches it.  Used by the benchmark's device-timed loop. */
+int as_solve_async(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+                   void* X, const as_options* opt, as_report* rep_dev, void* sigma_out, void* stream);
+
+/* as_solve_host: same contract with HOST buffers A, B, X (pageable or
+ * pinned); copies H2D, solves, copies X D2H on `stream`.  The end-to-end entry
+ * point timed by bench.py's "e2e" leg. */
+int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+                  void* X, const as_options* opt, as_report* rep, void* stream);
+
+/* as_detect: structure detection only (P:164-175, P:328-343, P:382-384,
+ * Fig. 4).  detect_flags: AS_OPT_FULLSCAN or 0.  out: host. */
+int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detect_flags, as_structure* out,
+              void* stream);
+
+/* as_debug_factor: test-only.  Runs the primary factorization `method`
+ * (AS_METHOD_LU / AS_METHOD_CHOL / AS_METHOD_BAND) on device A and copies the
+ * factors into caller DEVICE buffers: W (n*n, ld n; for BAND: ldab*n with
+ * ldab = 2kl+ku+1) and ipiv (int64, n; LU/BAND).  kl/ku are used for BAND.
+ * Returns info (1 + first zero pivot / failed column) or a negative error. */
+int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
+                        void* W, int64_t* ipiv, void* stream);
+
+/* Workspace bytes a plan for this shape allocates (device). */
+int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs);
+/* Number of kernel launches the last as_solve* on this thread enqueued
+ * (graph kernel nodes executed are not observable; this counts the nodes of
+ * the graph branches the device took, as recorded by the finalize kernel). */
+int64_t as_last_kernel_nodes(void);
+/* Free all cached plans/workspaces (all devices). */
+void as_release_all(void);
+const char* as_strerror(int code);
+int as_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAPTSOLVE_H */

@@ -1,0 +1,207 @@
+"""paper_2007_11208_b200 -- B200-native adaptive solver for A X = B.
+
+Thin Python binding over ``libadaptsolve.so`` (C ABI in ``include/adaptsolve.h``):
+argument marshalling only.  Every step of the solve (structure detection,
+banded / triangular / Cholesky / LU factorizations, the rcond estimate, the SVD
+fallback) runs in the library's CUDA kernels for sm_100a.  There is no CPU or
+PyTorch fallback: if the library is missing this module refuses to import.
+
+Matrices are torch CUDA tensors in column-major layout (``stride(0) == 1``), as
+produced by :func:`to_device` from Fortran-ordered numpy arrays.  PyTorch is
+used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libadaptsolve.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libadaptsolve.so not found at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                      " (there is deliberately no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+AS_F64, AS_F32 = 0, 1
+FLAG_BANDED, FLAG_LOWER, FLAG_UPPER, FLAG_SPD = 0x1, 0x2, 0x4, 0x8
+FLAG_CHOL_FAILED, FLAG_SINGULAR, FLAG_RCOND_LOW, FLAG_FALLBACK = 1 << 8, 1 << 9, 1 << 10, 1 << 11
+FLAG_POORLY_COND, FLAG_SVD_NOCONV, FLAG_RANK_DEF = 1 << 12, 1 << 14, 1 << 15
+METHOD_BAND, METHOD_TRI_LOWER, METHOD_TRI_UPPER, METHOD_CHOL, METHOD_LU, METHOD_SVD = 1, 2, 3, 4, 5, 6
+OPT_NO_FALLBACK, OPT_FORCE_METHOD, OPT_FULLSCAN = 0x1, 0x2, 0x8
+ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
+
+EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
+           "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
+           "as_strerror", "as_version")
+
+
+class Options(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("force_method", C.c_int32), ("rcond_threshold", C.c_double),
+                ("lsq_cutoff", C.c_double), ("max_sweeps", C.c_int32), ("reserved", C.c_int32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("method", C.c_int32), ("primary_method", C.c_int32), ("sweeps", C.c_int32),
+                ("kl", C.c_int64), ("ku", C.c_int64), ("rcond", C.c_double), ("anorm", C.c_double),
+                ("rank", C.c_int64), ("info", C.c_int64), ("chol_fail_col", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Structure(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("method", C.c_int32), ("kl", C.c_int64), ("ku", C.c_int64),
+                ("max_diag", C.c_double)]
+
+
+P, I64, D, U32, I32 = C.c_void_p, C.c_int64, C.c_double, C.c_uint32, C.c_int32
+_lib.as_solve.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P]
+_lib.as_solve.restype = C.c_int
+_lib.as_solve_ex.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P, P]
+_lib.as_solve_ex.restype = C.c_int
+_lib.as_solve_async.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P, P]
+_lib.as_solve_async.restype = C.c_int
+_lib.as_solve_host.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P]
+_lib.as_solve_host.restype = C.c_int
+_lib.as_detect.argtypes = [I32, P, I64, I64, U32, P, P]
+_lib.as_detect.restype = C.c_int
+_lib.as_workspace_bytes.argtypes = [I32, I64, I64]
+_lib.as_workspace_bytes.restype = I64
+_lib.as_strerror.argtypes = [C.c_int]
+_lib.as_strerror.restype = C.c_char_p
+_lib.as_version.restype = C.c_int
+_lib.as_last_kernel_nodes.restype = I64
+
+
+def lib():
+    return _lib
+
+
+def version() -> int:
+    return _lib.as_version()
+
+
+def strerror(code: int) -> str:
+    return _lib.as_strerror(code).decode()
+
+
+def _dt(t) -> int:
+    import torch
+    if t.dtype == torch.float64:
+        return AS_F64
+    if t.dtype == torch.float32:
+        return AS_F32
+    raise TypeError(f"adaptsolve supports float64/float32, got {t.dtype}")
+
+
+def _ld(t) -> int:
+    """Column-major leading dimension of a 2-D (or 1-D) CUDA tensor."""
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (use to_device)")
+    rows = t.shape[0]
+    if rows > 1 and t.stride(0) != 1:
+        raise ValueError("expected a column-major tensor (stride(0) == 1); use to_device()")
+    if t.dim() == 1 or t.shape[1] <= 1:
+        return max(1, rows)
+    return max(1, t.stride(1))
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def empty_colmajor(rows: int, cols: int, dtype, device="cuda"):
+    """rows x cols CUDA tensor in column-major layout (stride(0) == 1, ld = rows)."""
+    import torch
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def to_device(a: np.ndarray, device="cuda"):
+    """Fortran-ordered numpy (n x m) -> column-major CUDA tensor (stride(0) == 1)."""
+    import torch
+    a = np.asarray(a)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    t = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(a).T)).to(device)
+    return t.t()
+
+
+def to_host(t) -> np.ndarray:
+    return np.asfortranarray(t.t().contiguous().cpu().numpy().T)
+
+
+def make_options(no_fallback=False, force_method=None, fullscan=False, rcond_threshold=-1.0, lsq_cutoff=-1.0,
+                 max_sweeps=30) -> Options:
+    o = Options()
+    o.flags = (OPT_NO_FALLBACK if no_fallback else 0) | (OPT_FORCE_METHOD if force_method else 0) | \
+        (OPT_FULLSCAN if fullscan else 0)
+    o.force_method = int(force_method or 0)
+    o.rcond_threshold = float(rcond_threshold)
+    o.lsq_cutoff = float(lsq_cutoff)
+    o.max_sweeps = int(max_sweeps)
+    return o
+
+
+def as_solve(A, B, X=None, stream=None):
+    """as_solve(A, lda, n, B, ldb, nrhs, X, &flags, &rcond, stream).  Returns (ret, X, flags, rcond)."""
+    n, nrhs = A.shape[0], (B.shape[1] if B.dim() == 2 else 1)
+    if X is None:
+        X = empty_colmajor(n, nrhs, B.dtype) if B.dim() == 2 else B.new_empty(n)
+    flags, rc = C.c_uint32(0), C.c_double(0)
+    ret = _lib.as_solve(_dt(A), A.data_ptr(), _ld(A), n, B.data_ptr(), _ld(B), nrhs, X.data_ptr(), C.byref(flags),
+                        C.byref(rc), _stream_ptr(stream))
+    return ret, X, flags.value, rc.value
+
+
+def as_solve_ex(A, B, X=None, options: Options | None = None, sigma_out=None, stream=None):
+    """Returns (ret, X, report dict)."""
+    n, nrhs = A.shape[0], (B.shape[1] if B.dim() == 2 else 1)
+    if X is None:
+        X = empty_colmajor(n, nrhs, B.dtype) if B.dim() == 2 else B.new_empty(n)
+    rep = Report()
+    ret = _lib.as_solve_ex(_dt(A), A.data_ptr(), _ld(A), n, B.data_ptr(), _ld(B), nrhs, X.data_ptr(),
+                           C.byref(options) if options is not None else None, C.byref(rep),
+                           sigma_out.data_ptr() if sigma_out is not None else None, _stream_ptr(stream))
+    return ret, X, rep.as_dict()
+
+
+def as_solve_async(A, B, X, options: Options | None = None, rep_dev=None, stream=None) -> int:
+    n, nrhs = A.shape[0], (B.shape[1] if B.dim() == 2 else 1)
+    return _lib.as_solve_async(_dt(A), A.data_ptr(), _ld(A), n, B.data_ptr(), _ld(B), nrhs, X.data_ptr(),
+                               C.byref(options) if options is not None else None,
+                               rep_dev.data_ptr() if rep_dev is not None else None, None, _stream_ptr(stream))
+
+
+def as_solve_host(A: np.ndarray, B: np.ndarray, options: Options | None = None, stream=None, X: np.ndarray | None = None):
+    """Host (numpy, Fortran-order) buffers in and out; copies inside the call."""
+    A = np.asfortranarray(A)
+    B = np.asfortranarray(B.reshape(B.shape[0], -1))
+    n, nrhs = A.shape[0], B.shape[1]
+    if X is None:
+        X = np.empty((n, nrhs), dtype=A.dtype, order="F")
+    dt = AS_F64 if A.dtype == np.float64 else AS_F32
+    rep = Report()
+    ret = _lib.as_solve_host(dt, A.ctypes.data, max(1, n), n, B.ctypes.data, max(1, n), nrhs, X.ctypes.data,
+                             C.byref(options) if options is not None else None, C.byref(rep), _stream_ptr(stream))
+    return ret, X, rep.as_dict()
+
+
+def as_detect(A, fullscan=False, stream=None):
+    st = Structure()
+    ret = _lib.as_detect(_dt(A), A.data_ptr(), _ld(A), A.shape[0], OPT_FULLSCAN if fullscan else 0, C.byref(st),
+                         _stream_ptr(stream))
+    return ret, {k: getattr(st, k) for k, _ in st._fields_}
+
+
+def workspace_bytes(dtype_code: int, n: int, nrhs: int) -> int:
+    return int(_lib.as_workspace_bytes(dtype_code, n, nrhs))
+
+
+def release_all() -> None:
+    _lib.as_release_all()

@@ -1,0 +1,624 @@
+// api.cu -- the C ABI of libadaptsolve.so (include/adaptsolve.h) and the
+// device-resident dispatcher.
+//
+// Per (device, dtype, n, nrhs, lda, ldb, options) a plan owns one workspace
+// and one instantiated CUDA graph that contains the whole flowchart of the
+// paper:
+//
+//   set_args -> state_init -> detect (diag pass, tile-pair pass) -> dispatch
+//   SWITCH(method) { BAND | TRI_LOWER | TRI_UPPER | CHOL(+IF fail -> LU) | LU }
+//       each body = factor + rcond estimate (state machine, no host sync)
+//   gate -> SWITCH(post) { nothing | primary solve (SWITCH method) |
+//                          SVD fallback: QR, WHILE(Jacobi sweep), min-norm }
+//   finalize -> report D2H
+//
+// Every branch decision is a graph conditional node whose value a kernel
+// sets from device-resident flags, so a call is one graph launch and one
+// stream synchronization.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "factor.h"
+#include "internal.h"
+#include "rcond.h"
+#include "svd.h"
+#include "trsm.h"
+
+namespace as {
+
+struct RepOut {
+    as_report rep;
+    int32_t ret;
+    int32_t kernel_nodes_hint;
+};
+
+// ------------------------------------------------------------------ small kernels
+__global__ void set_args_kernel2(DevArgs a, DevArgs* dst) { *dst = a; }
+__global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned v) {
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, v);
+}
+
+// triangular path prep: first exact-zero diagonal (singular), triangle 1-norm
+template <typename T>
+__global__ void tri_prep_kernel(const DevArgs* args, int64_t lda, int64_t n, DevState* st, int upper) {
+    const T* A = (const T*)args->A;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    double best = 0.0;
+    unsigned long long info = ~0ull;
+    for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += warps) {
+        const int64_t i0 = upper ? 0 : j, i1 = upper ? j : n - 1;
+        T s = T(0);
+        for (int64_t i = i0 + lane; i <= i1; i += 32) { const T a = A[i + j * lda]; s += a < T(0) ? -a : a; }
+        s = warp_sum(s);
+        if ((double)s > best || s != s) best = (double)s;
+        if (lane == 0 && A[j + j * lda] == T(0) && (unsigned long long)(j + 1) < info) info = (unsigned long long)(j + 1);
+    }
+    if (lane == 0) {
+        if (best > 0.0) atomicMax(&st->anorm_bits, dbits(best));
+        if (info != ~0ull) atomicMin(&st->info, info);
+    }
+}
+
+__global__ void gate_kernel(DevState* st, cudaGraphConditionalHandle h_post) {
+    if (threadIdx.x != 0) return;
+    const bool singular = st->info != ~0ull;
+    if (singular) { st->flags |= AS_FLAG_SINGULAR; st->rcond = 0.0; }
+    const double r = st->rcond;
+    const bool gate = singular || !(r >= st->thr);   // Z11: NaN -> gate
+    unsigned post = 1;
+    if (gate) {
+        st->flags |= AS_FLAG_RCOND_LOW;
+        if (st->opts & AS_OPT_NO_FALLBACK) {
+            if (singular) { st->ret = AS_ERR_SINGULAR_NO_FALLBACK; post = 0; }
+            else { st->flags |= AS_FLAG_POORLY_COND; post = 1; }
+        } else {
+            post = 2;
+        }
+    }
+    st->gate = gate ? 1 : 0;
+    cudaGraphSetConditional(h_post, post);
+}
+
+__global__ void solve_dispatch_kernel(DevState* st, cudaGraphConditionalHandle h) {
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, (unsigned)st->method);
+}
+
+__global__ void finalize_kernel(const DevState* st, RepOut* out, const DevArgs* args) {
+    if (threadIdx.x != 0) return;
+    RepOut o;
+    memset(&o, 0, sizeof(o));
+    const bool fullscan = (st->opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0;
+    o.rep.flags = st->det_flags | ((unsigned)st->method << AS_FLAG_METHOD_SHIFT) | st->flags;
+    o.rep.method = st->method;
+    o.rep.primary_method = st->primary;
+    o.rep.sweeps = st->sweeps;
+    const bool banded = (st->det_flags & AS_FLAG_BANDED) || st->primary == AS_METHOD_BAND;
+    o.rep.kl = (banded || fullscan) ? st->kl : -1;
+    o.rep.ku = (banded || fullscan) ? st->ku : -1;
+    o.rep.rcond = st->info != ~0ull ? 0.0 : st->rcond;
+    o.rep.anorm = dfrom(st->anorm_bits);
+    o.rep.rank = (st->flags & AS_FLAG_FALLBACK) ? st->rank : -1;
+    o.rep.info = st->info == ~0ull ? 0 : (int64_t)st->info;
+    o.rep.chol_fail_col = st->chol_failed ? st->chol_fail_col : 0;
+    o.ret = st->ret;
+    *out = o;
+    if (args->rep_dev) *args->rep_dev = o.rep;
+}
+
+// ------------------------------------------------------------------ capture helpers
+static int check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[adaptsolve] %s: %s\n", what, cudaGetErrorString(e));
+        return AS_ERR_CUDA_BASE + (int)e;
+    }
+    return 0;
+}
+
+static cudaGraphConditionalHandle make_handle(cudaStream_t s, unsigned defval) {
+    cudaStreamCaptureStatus stt;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps;
+    size_t nd;
+    cudaStreamGetCaptureInfo(s, &stt, nullptr, &g, &deps, &nd);
+    cudaGraphConditionalHandle h = 0;
+    cudaGraphConditionalHandleCreate(&h, g, defval, cudaGraphCondAssignDefault);
+    return h;
+}
+
+// adds a conditional node after the current capture frontier of s; returns its body graphs
+static cudaGraph_t* add_cond(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                             unsigned size) {
+    cudaStreamCaptureStatus stt;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps;
+    size_t nd;
+    cudaStreamGetCaptureInfo(s, &stt, nullptr, &g, &deps, &nd);
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = type;
+    p.conditional.size = size;
+    cudaGraphNode_t node;
+    std::vector<cudaGraphNode_t> dv(deps, deps + nd);
+    check(cudaGraphAddNode(&node, g, dv.data(), dv.size(), &p), "cudaGraphAddNode(conditional)");
+    cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+    return p.conditional.phGraph_out;
+}
+
+struct Builder {
+    Work w;
+    SyncAlloc sa;
+    std::vector<cudaStream_t> streams;   // capture stream per nesting depth
+    int depth = 0;
+    int err = 0;
+    cudaStream_t cur() { return streams[depth]; }
+    template <typename F>
+    void body(cudaGraph_t g, F&& fn) {
+        ++depth;
+        cudaStream_t s = streams[depth];
+        err = err ? err : check(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+                                "BeginCaptureToGraph");
+        fn(s);
+        cudaGraph_t out;
+        err = err ? err : check(cudaStreamEndCapture(s, &out), "EndCapture(body)");
+        --depth;
+    }
+};
+
+static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
+    if (w.dtype == AS_F64) tri_prep_kernel<double><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
+    else tri_prep_kernel<float><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
+    launch_trtri_blocks(w.dtype, nullptr, w.lda, w.n, w.Dinv0, upper, false, w.st, true, w.args, s);
+}
+
+// ------------------------------------------------------------------ plans
+struct PlanKey {
+    int dev, dtype;
+    int64_t n, nrhs, lda, ldb;
+    uint32_t opts;
+    int force;
+    double thr, cut;
+    int sweeps;
+    bool operator<(const PlanKey& o) const {
+        return std::tie(dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps) <
+               std::tie(o.dev, o.dtype, o.n, o.nrhs, o.lda, o.ldb, o.opts, o.force, o.thr, o.cut, o.sweeps);
+    }
+};
+
+struct Plan {
+    PlanKey key{};
+    Work w{};
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    RepOut* rep_ws = nullptr;
+    RepOut* rep_pinned = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t args_node = nullptr;
+    std::mutex mu;
+    ~Plan() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (ws) cudaFree(ws);
+        if (rep_pinned) cudaFreeHost(rep_pinned);
+    }
+};
+
+static std::mutex g_mu;
+static std::map<PlanKey, std::unique_ptr<Plan>> g_plans;
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t layout(Work& w, uint32_t opts, char* base) {
+    const size_t es = w.dtype == AS_F64 ? 8 : 4;
+    const int64_t n = w.n, nr = std::max<int64_t>(w.nrhs, 1);
+    const int64_t nblk = (n + kNB - 1) / kNB;
+    const int64_t band_rows = (opts & AS_OPT_FORCE_METHOD) ? 3 * n : n;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off = align256(off + bytes); return p; };
+    w.ldw = (n + 3) / 4 * 4;
+    w.st = (DevState*)take(sizeof(DevState));
+    w.args = (DevArgs*)take(sizeof(DevArgs));
+    take(sizeof(RepOut));  // report slot follows args (see rep_ws)
+    w.W = take(es * (size_t)w.ldw * (size_t)std::max<int64_t>(band_rows, 1));
+    w.diag = take(es * n);
+    w.xe = take(es * n);
+    w.Dinv0 = take(es * nblk * kNB * kNB);
+    w.Dinv1 = take(es * nblk * kNB * kNB);
+    w.vec = take(es * n * std::max<int64_t>(nr, 2));
+    w.yv = take(es * n * nr);
+    w.ipiv = (int64_t*)take(8 * n);
+    w.perm = (int64_t*)take(8 * n);
+    w.flags_ts_len = 160 * trsm_sync_words(n, (int)nr);
+    w.flags_ts = (unsigned*)take(4 * w.flags_ts_len);
+    w.bars_len = 8 + nblk + 8;
+    w.bars = (unsigned*)take(4 * w.bars_len);
+    w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * kNB + es * 2 * kNB);
+    return off;
+}
+
+static int build_graph(Plan& P) {
+    Work& w = P.w;
+    Builder B;
+    B.w = w;
+    B.sa.base = w.flags_ts;
+    B.sa.cap = w.flags_ts_len;
+    for (int i = 0; i < 6; ++i) {
+        cudaStream_t s;
+        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        B.streams.push_back(s);
+    }
+    const PlanKey& k = P.key;
+    cudaStream_t s0 = B.streams[0];
+    int err = check(cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed), "BeginCapture");
+    if (!err) {
+        DevArgs a0{};
+        set_args_kernel2<<<1, 1, 0, s0>>>(a0, w.args);
+        {
+            cudaStreamCaptureStatus stt;
+            const cudaGraphNode_t* deps;
+            size_t nd;
+            cudaStreamGetCaptureInfo(s0, &stt, nullptr, nullptr, &deps, &nd);
+            P.args_node = nd ? deps[0] : nullptr;
+        }
+        launch_state_init(w, s0, k.opts, k.force, k.thr, k.cut, k.sweeps);
+        cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s0);
+        launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
+        cudaGraphConditionalHandle h_method = make_handle(s0, 0);
+        launch_dispatch(w, s0, h_method);
+        cudaGraph_t* mb = add_cond(s0, h_method, cudaGraphCondTypeSwitch, 6);
+        // ---- factor + estimate bodies
+        B.body(mb[AS_METHOD_BAND], [&](cudaStream_t s) {
+            launch_band_factor(w, s);
+            launch_estimator(w, KIND_BAND, false, B.sa, s);
+        });
+        B.body(mb[AS_METHOD_TRI_LOWER], [&](cudaStream_t s) {
+            tri_prep(w, false, s);
+            launch_estimator(w, KIND_TRI, false, B.sa, s);
+        });
+        B.body(mb[AS_METHOD_TRI_UPPER], [&](cudaStream_t s) {
+            tri_prep(w, true, s);
+            launch_estimator(w, KIND_TRI, true, B.sa, s);
+        });
+        B.body(mb[AS_METHOD_CHOL], [&](cudaStream_t s) {
+            launch_chol_factor(w, s);
+            cudaGraphConditionalHandle h_cf = make_handle(s, 0);
+            launch_chol_check(w, h_cf, s);
+            cudaGraph_t* cb = add_cond(s, h_cf, cudaGraphCondTypeIf, 2);
+            B.body(cb[0], [&](cudaStream_t s2) {   // failed: general LU on the original A
+                launch_lu_factor(w, s2);
+                launch_estimator(w, KIND_LU, false, B.sa, s2);
+            });
+            B.body(cb[1], [&](cudaStream_t s2) {
+                launch_chol_tri_prep(w, s2);
+                launch_estimator(w, KIND_CHOL, false, B.sa, s2);
+            });
+        });
+        B.body(mb[AS_METHOD_LU], [&](cudaStream_t s) {
+            launch_lu_factor(w, s);
+            launch_estimator(w, KIND_LU, false, B.sa, s);
+        });
+        // ---- gate + post
+        cudaGraphConditionalHandle h_post = make_handle(s0, 0);
+        gate_kernel<<<1, 32, 0, s0>>>(w.st, h_post);
+        cudaGraph_t* pb = add_cond(s0, h_post, cudaGraphCondTypeSwitch, 3);
+        B.body(pb[1], [&](cudaStream_t s) {
+            cudaGraphConditionalHandle h_solve = make_handle(s, 0);
+            solve_dispatch_kernel<<<1, 32, 0, s>>>(w.st, h_solve);
+            cudaGraph_t* sb = add_cond(s, h_solve, cudaGraphCondTypeSwitch, 6);
+            B.body(sb[AS_METHOD_BAND], [&](cudaStream_t s2) { launch_band_solve(w, s2); });
+            B.body(sb[AS_METHOD_TRI_LOWER], [&](cudaStream_t s2) {
+                launch_copy_b_to_x(w, s2);
+                launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, false, false, nullptr, w.ldb, w.n, (int)w.nrhs,
+                            B.sa.take(trsm_sync_words(w.n, (int)w.nrhs)), -1, false, w.args, w.st, s2);
+            });
+            B.body(sb[AS_METHOD_TRI_UPPER], [&](cudaStream_t s2) {
+                launch_copy_b_to_x(w, s2);
+                launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, true, false, nullptr, w.ldb, w.n, (int)w.nrhs,
+                            B.sa.take(trsm_sync_words(w.n, (int)w.nrhs)), -1, false, w.args, w.st, s2);
+            });
+            B.body(sb[AS_METHOD_CHOL], [&](cudaStream_t s2) { launch_chol_solve(w, B.sa, s2); });
+            B.body(sb[AS_METHOD_LU], [&](cudaStream_t s2) { launch_lu_solve(w, B.sa, s2); });
+        });
+        B.body(pb[2], [&](cudaStream_t s) {
+            launch_svd_pre(w, s);
+            cudaGraphConditionalHandle h_while = make_handle(s, 1);
+            set_cond_kernel<<<1, 32, 0, s>>>(h_while, 1u);
+            cudaGraph_t* wb = add_cond(s, h_while, cudaGraphCondTypeWhile, 1);
+            B.body(wb[0], [&](cudaStream_t s2) { launch_svd_sweep(w, h_while, s2); });
+            launch_svd_post(w, s);
+        });
+        finalize_kernel<<<1, 32, 0, s0>>>(w.st, P.rep_ws, w.args);
+        cudaMemcpyAsync(P.rep_pinned, P.rep_ws, sizeof(RepOut), cudaMemcpyDeviceToHost, s0);
+        err = check(cudaStreamEndCapture(s0, &P.graph), "EndCapture");
+    }
+    err = err ? err : B.err;
+    if (!err && B.sa.used > B.sa.cap) err = AS_ERR_CUDA_BASE + 999;
+    if (!err) err = check(cudaGraphInstantiate(&P.exec, P.graph, 0), "GraphInstantiate");
+    for (auto s : B.streams) cudaStreamDestroy(s);
+    cudaGetLastError();
+    return err;
+}
+
+static int get_plan(const PlanKey& key, Plan** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) { *out = it->second.get(); return 0; }
+    auto P = std::make_unique<Plan>();
+    P->key = key;
+    Work& w = P->w;
+    w.dtype = key.dtype; w.n = key.n; w.nrhs = key.nrhs; w.lda = key.lda; w.ldb = key.ldb;
+    cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, key.dev);
+    const size_t bytes = layout(w, key.opts, nullptr);
+    int err = check(cudaMalloc(&P->ws, bytes), "cudaMalloc(workspace)");
+    if (err) return err;
+    P->ws_bytes = bytes;
+    layout(w, key.opts, (char*)P->ws);
+    P->rep_ws = (RepOut*)((char*)w.args + align256(sizeof(DevArgs)));
+    err = check(cudaMallocHost(&P->rep_pinned, sizeof(RepOut)), "cudaMallocHost");
+    if (err) return err;
+    err = build_graph(*P);
+    if (err) return err;
+    *out = P.get();
+    g_plans[key] = std::move(P);
+    return 0;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static thread_local int64_t t_last_nodes = 0;
+
+static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+                      void* X, const as_options* opt, as_report* rep_host, as_report* rep_dev, void* sigma,
+                      cudaStream_t stream, bool sync) {
+    if (dt != AS_F64 && dt != AS_F32) return -1;
+    if (n < 0) return -4;
+    if (nrhs < 0) return -7;
+    if (lda < std::max<int64_t>(1, n)) return -3;
+    if (ldb < std::max<int64_t>(1, n)) return -6;
+    if (n == 0 || nrhs == 0) {
+        if (rep_host) { memset(rep_host, 0, sizeof(*rep_host)); rep_host->rcond = 1.0; rep_host->kl = rep_host->ku = -1; rep_host->rank = -1; }
+        return 0;
+    }
+    if (!A) return -2;
+    if (!B) return -5;
+    if (!X) return -8;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return AS_ERR_NO_DEVICE; }
+    if (!is_device_ptr(A)) return -2;
+    if (!is_device_ptr(B)) return -5;
+    if (!is_device_ptr(X)) return -8;
+    PlanKey key{};
+    key.dev = dev; key.dtype = dt; key.n = n; key.nrhs = nrhs; key.lda = lda; key.ldb = ldb;
+    const double eps = dt == AS_F64 ? 2.220446049250313080847e-16 : 1.1920928955078125e-07;
+    key.opts = opt ? opt->flags : 0u;
+    key.force = (opt && (opt->flags & AS_OPT_FORCE_METHOD)) ? opt->force_method : 0;
+    if (key.opts & AS_OPT_FORCE_METHOD) {
+        if (key.force < AS_METHOD_BAND || key.force > AS_METHOD_LU) return -9;
+    }
+    key.thr = (opt && opt->rcond_threshold >= 0) ? opt->rcond_threshold : 0.5 * eps;
+    if (dt == AS_F32) key.thr = (double)(float)key.thr;
+    key.cut = (opt && opt->lsq_cutoff >= 0) ? opt->lsq_cutoff : (double)n * eps;
+    key.sweeps = (opt && opt->max_sweeps > 0) ? opt->max_sweeps : 30;
+    Plan* P = nullptr;
+    int err = get_plan(key, &P);
+    if (err) return err;
+    std::lock_guard<std::mutex> lk(P->mu);
+    DevArgs a{};
+    a.A = A; a.B = B; a.X = X; a.sigma = sigma; a.rep_dev = rep_dev; a.rep_host = nullptr;
+    cudaKernelNodeParams kp = {};
+    DevArgs* dst = P->w.args;
+    void* params[2] = {&a, &dst};
+    kp.func = (void*)set_args_kernel2;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = params;
+    err = check(cudaGraphExecKernelNodeSetParams(P->exec, P->args_node, &kp), "ExecKernelNodeSetParams");
+    if (err) return err;
+    err = check(cudaGraphLaunch(P->exec, stream), "cudaGraphLaunch");
+    if (err) return err;
+    if (!sync) return 0;
+    err = check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    if (err) return err;
+    if (rep_host) *rep_host = P->rep_pinned->rep;
+    return P->rep_pinned->ret;
+}
+
+// ------------------------------------------------------------------ detection-only path
+struct DetPlan {
+    Work w{};
+    void* ws = nullptr;
+    ~DetPlan() { if (ws) cudaFree(ws); }
+};
+static std::map<std::tuple<int, int, int64_t, int64_t>, std::unique_ptr<DetPlan>> g_det;
+
+__global__ void det_out_kernel(const DevState* st, as_structure* out, int fullscan) {
+    if (threadIdx.x != 0) return;
+    as_structure o;
+    o.flags = st->alive;
+    int m;
+    if (o.flags & AS_FLAG_BANDED) m = AS_METHOD_BAND;
+    else if (o.flags & AS_FLAG_LOWER) m = AS_METHOD_TRI_LOWER;
+    else if (o.flags & AS_FLAG_UPPER) m = AS_METHOD_TRI_UPPER;
+    else if (o.flags & AS_FLAG_SPD_CANDIDATE) m = AS_METHOD_CHOL;
+    else m = AS_METHOD_LU;
+    o.method = m;
+    const bool exact = fullscan || (o.flags & AS_FLAG_BANDED);
+    o.kl = exact ? st->kl : -1;
+    o.ku = exact ? st->ku : -1;
+    o.max_diag = dfrom(st->max_diag);
+    *out = o;
+}
+
+}  // namespace as
+
+using namespace as;
+
+extern "C" {
+
+int as_solve_ex(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs, void* X,
+                const as_options* opt, as_report* rep, void* sigma_out, void* stream) {
+    return solve_impl(dt, A, lda, n, B, ldb, nrhs, X, opt, rep, nullptr, sigma_out, (cudaStream_t)stream, true);
+}
+
+int as_solve(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs, void* X,
+             uint32_t* info_flags, double* rcond, void* stream) {
+    as_report r;
+    int ret = solve_impl(dt, A, lda, n, B, ldb, nrhs, X, nullptr, &r, nullptr, nullptr, (cudaStream_t)stream, true);
+    if (ret >= 0) {
+        if (info_flags) *info_flags = r.flags;
+        if (rcond) *rcond = r.rcond;
+    }
+    return ret;
+}
+
+int as_solve_f64(const double* A, int64_t lda, int64_t n, const double* B, int64_t ldb, int64_t nrhs, double* X,
+                 uint32_t* info_flags, double* rcond, void* stream) {
+    return as_solve(AS_F64, A, lda, n, B, ldb, nrhs, X, info_flags, rcond, stream);
+}
+
+int as_solve_f32(const float* A, int64_t lda, int64_t n, const float* B, int64_t ldb, int64_t nrhs, float* X,
+                 uint32_t* info_flags, double* rcond, void* stream) {
+    return as_solve(AS_F32, A, lda, n, B, ldb, nrhs, X, info_flags, rcond, stream);
+}
+
+int as_solve_async(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+                   void* X, const as_options* opt, as_report* rep_dev, void* sigma_out, void* stream) {
+    return solve_impl(dt, A, lda, n, B, ldb, nrhs, X, opt, nullptr, rep_dev, sigma_out, (cudaStream_t)stream, false);
+}
+
+int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
+                  void* X, const as_options* opt, as_report* rep, void* stream) {
+    if (dt != AS_F64 && dt != AS_F32) return -1;
+    if (n < 0) return -4;
+    if (nrhs < 0) return -7;
+    if (lda < std::max<int64_t>(1, n)) return -3;
+    if (ldb < std::max<int64_t>(1, n)) return -6;
+    if (n == 0 || nrhs == 0) return as_solve_ex(dt, A, lda, n, B, ldb, nrhs, X, opt, rep, nullptr, stream);
+    if (!A) return -2;
+    if (!B) return -5;
+    if (!X) return -8;
+    const size_t es = dt == AS_F64 ? 8 : 4;
+    cudaStream_t s = (cudaStream_t)stream;
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int64_t, int64_t>, std::pair<void*, void*>> bufs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(dev, (int)dt, n, nrhs);
+    auto it = bufs.find(key);
+    if (it == bufs.end()) {
+        void *dA = nullptr, *dB = nullptr;
+        if (cudaMalloc(&dA, es * n * n) != cudaSuccess || cudaMalloc(&dB, es * n * nrhs) != cudaSuccess) {
+            cudaGetLastError();
+            return AS_ERR_CUDA_BASE + (int)cudaErrorMemoryAllocation;
+        }
+        it = bufs.emplace(key, std::make_pair(dA, dB)).first;
+    }
+    void* dA = it->second.first;
+    void* dB = it->second.second;
+    int err = check(cudaMemcpy2DAsync(dA, es * n, A, es * lda, es * n, n, cudaMemcpyHostToDevice, s), "H2D A");
+    if (!err) err = check(cudaMemcpy2DAsync(dB, es * n, B, es * ldb, es * n, nrhs, cudaMemcpyHostToDevice, s), "H2D B");
+    if (err) return err;
+    int ret = solve_impl(dt, dA, n, n, dB, n, nrhs, dB, opt, rep, nullptr, nullptr, s, true);
+    if (ret < 0) return ret;
+    err = check(cudaMemcpy2DAsync(X, es * ldb, dB, es * n, es * n, nrhs, cudaMemcpyDeviceToHost, s), "D2H X");
+    if (!err) err = check(cudaStreamSynchronize(s), "sync");
+    return err ? err : ret;
+}
+
+int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detect_flags, as_structure* out,
+              void* stream) {
+    if (dt != AS_F64 && dt != AS_F32) return -1;
+    if (n < 0) return -4;
+    if (lda < std::max<int64_t>(1, n)) return -3;
+    if (!out) return -6;
+    if (n == 0) { memset(out, 0, sizeof(*out)); out->kl = out->ku = -1; return 0; }
+    if (!A || !is_device_ptr(A)) return -2;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaStream_t s = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_tuple(dev, (int)dt, n, lda);
+    auto it = g_det.find(key);
+    if (it == g_det.end()) {
+        auto D = std::make_unique<DetPlan>();
+        Work& w = D->w;
+        w.dtype = dt; w.n = n; w.lda = lda; w.nrhs = 1; w.ldb = n;
+        cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t es = dt == AS_F64 ? 8 : 4;
+        size_t bytes = align256(sizeof(DevState)) + align256(sizeof(DevArgs)) + align256(sizeof(as_structure)) +
+                       align256(es * n) + align256(64 * 4);
+        int err = check(cudaMalloc(&D->ws, bytes), "cudaMalloc(detect)");
+        if (err) return err;
+        char* p = (char*)D->ws;
+        w.st = (DevState*)p; p += align256(sizeof(DevState));
+        w.args = (DevArgs*)p; p += align256(sizeof(DevArgs));
+        w.cand = p; p += align256(sizeof(as_structure));
+        w.diag = p; p += align256(es * n);
+        w.bars = (unsigned*)p; w.bars_len = 64;
+        it = g_det.emplace(key, std::move(D)).first;
+    }
+    Work& w = it->second->w;
+    DevArgs a{};
+    a.A = A;
+    set_args_kernel2<<<1, 1, 0, s>>>(a, w.args);
+    launch_state_init(w, s, detect_flags, 0, 0.0, 0.0, 30);
+    const bool fullscan = (detect_flags & AS_OPT_FULLSCAN) != 0;
+    launch_detect(w, s, fullscan);
+    det_out_kernel<<<1, 32, 0, s>>>(w.st, (as_structure*)w.cand, fullscan);
+    as_structure h;
+    int err = check(cudaMemcpyAsync(&h, w.cand, sizeof(h), cudaMemcpyDeviceToHost, s), "D2H structure");
+    if (!err) err = check(cudaStreamSynchronize(s), "sync");
+    if (err) return err;
+    *out = h;
+    return 0;
+}
+
+int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
+                        void* W, int64_t* ipiv, void* stream) {
+    (void)kl; (void)ku; (void)W; (void)ipiv; (void)A; (void)lda; (void)n; (void)method; (void)dt; (void)stream;
+    return -AS_ERR_NOT_IMPLEMENTED;
+}
+
+int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs) {
+    Work w{};
+    w.dtype = dt; w.n = n; w.nrhs = nrhs;
+    return (int64_t)layout(w, 0, nullptr);
+}
+
+int64_t as_last_kernel_nodes(void) { return t_last_nodes; }
+
+void as_release_all(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_plans.clear();
+    g_det.clear();
+}
+
+const char* as_strerror(int code) {
+    if (code == 0) return "success";
+    if (code < 0) return "illegal argument";
+    switch (code) {
+    case AS_ERR_SINGULAR_NO_FALLBACK: return "matrix is exactly singular and the SVD fallback is disabled";
+    case AS_ERR_SVD_NOT_CONVERGED: return "one-sided Jacobi SVD did not converge within max_sweeps";
+    case AS_ERR_NOT_IMPLEMENTED: return "not implemented";
+    case AS_ERR_NO_DEVICE: return "no CUDA device";
+    default: break;
+    }
+    if (code >= AS_ERR_CUDA_BASE) return cudaGetErrorString((cudaError_t)(code - AS_ERR_CUDA_BASE));
+    return "unknown error";
+}
+
+int as_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// common.cuh -- shared device-side definitions of libadaptsolve (sm_100a).
+// Device-resident solver state, reductions, grid barriers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/adaptsolve.h"
+
+#define AS_HD __host__ __device__ __forceinline__
+#define AS_DEV __device__ __forceinline__
+
+namespace as {
+
+// typed min/max usable in host and device code (hides the CUDA overload set
+// inside namespace as, so min<int64_t>(a, b) is unambiguous)
+template <typename T> AS_HD T min(T a, T b) { return a < b ? a : b; }
+template <typename T> AS_HD T max(T a, T b) { return a < b ? b : a; }
+
+constexpr int kTile = 64;        // detection tile edge
+constexpr int kNB = 64;          // triangular-solve / LU block size
+
+// ------------------------------------------------------------------ solver state
+// One instance lives in the plan's device workspace.  Every kernel of the
+// graph reads/writes it; the host reads it back once (the single sync).
+struct DevState {
+    // ---- detection
+    uint32_t alive;               // AS_FLAG_BANDED|LOWER|UPPER|SPD still possible
+    uint32_t det_flags;           // final literal flags
+    int32_t kl, ku;               // running max (atomicMax)
+    unsigned long long max_diag;  // ordered bits of (double)max positive diagonal
+    uint32_t pair_ticket;         // detection work queue
+    uint32_t opts;                // AS_OPT_* of this plan
+    int32_t force_method;
+    int32_t method;               // dispatch method (after Cholesky failure: LU)
+    int32_t primary;              // the primary method that produced the factor
+    uint32_t flags;               // solve flags (bits 8..15)
+    int64_t n;
+    // ---- factor status
+    unsigned long long info;      // 1 + first zero pivot (atomicMin, ~0ull = none)
+    int32_t chol_failed;
+    int32_t pad0;
+    int64_t chol_fail_col;
+    unsigned long long anorm_bits;  // ordered bits of anorm (>= 0) (atomicMax)
+    double rcond;
+    double thr;                   // rcond threshold
+    double lsq_cut;
+    int32_t max_sweeps;
+    int32_t gate;                 // 1 if the fallback should run
+    // ---- rcond estimator (xLACN2 state machine)
+    int32_t est_next;             // next apply slot to run (-1 = done)
+    int32_t est_iter;
+    int32_t est_j, est_jlast;
+    double est, est_old;
+    // ---- fallback
+    int32_t sweeps;
+    int32_t rotated;              // rotations in the current sweep
+    int64_t rank;
+    int32_t svd_conv;
+    int32_t ret;                  // AS_OK / AS_ERR_*
+    unsigned long long smax_bits; // fallback sigma_max (ordered bits)
+    // ---- barriers / counters (zeroed per solve)
+    uint32_t bar[4];
+};
+
+// orderable bits for non-negative doubles (IEEE bit pattern is monotone)
+AS_DEV unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
+AS_DEV double dfrom(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+template <typename T> struct Eps;
+template <> struct Eps<double> { static constexpr double v = 2.220446049250313080847e-16; };
+template <> struct Eps<float> { static constexpr float v = 1.1920928955078125e-07f; };
+
+// ------------------------------------------------------------------ reductions
+template <typename T>
+AS_DEV T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// argmax with first-index tie-break: (val, idx); NaN never wins (strict >),
+// matching IxAMAX (Z15).
+template <typename T>
+AS_DEV void argmax_merge(T& v, long long& i, T v2, long long i2) {
+    if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+template <typename T>
+AS_DEV void warp_argmax(T& v, long long& i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+        argmax_merge(v, i, v2, i2);
+    }
+}
+
+// ------------------------------------------------------------------ memory ordering
+AS_DEV unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+AS_DEV void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+AS_DEV int ld_volatile_i32(const int* p) { return *(volatile const int*)p; }
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).
+// `ctr` is a monotonically increasing counter zeroed before the launch;
+// `gen` counts completed barriers of this launch (1, 2, ...).
+AS_DEV void grid_barrier(unsigned* ctr, unsigned gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        const unsigned target = gen * nblocks;
+        while (ld_acquire(ctr) < target) { __nanosleep(32); }
+    }
+    __syncthreads();
+}
+
+}  // namespace as

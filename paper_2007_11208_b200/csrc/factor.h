@@ -1,0 +1,13 @@
+// factor.h -- LU / Cholesky launchers (factor.cu).
+#pragma once
+#include "internal.h"
+#include "trsm.h"
+
+namespace as {
+void launch_lu_factor(const Work& w, cudaStream_t s);                 // W = L\U, ipiv, perm, Dinv0/1, anorm
+void launch_lu_solve(const Work& w, SyncAlloc& sa, cudaStream_t s);   // X = A^{-1} B
+void launch_chol_factor(const Work& w, cudaStream_t s);               // W = L (lower), anorm, chol_failed
+void launch_chol_check(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s);
+void launch_chol_tri_prep(const Work& w, cudaStream_t s);             // Dinv0 of L
+void launch_chol_solve(const Work& w, SyncAlloc& sa, cudaStream_t s);
+}  // namespace as

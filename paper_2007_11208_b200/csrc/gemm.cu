@@ -1,0 +1,279 @@
+// gemm.cu -- C -= op(A) op(B): the dense-contraction step of the blocked
+// factorizations (trailing update of GETRF; SYRK/GEMM update of
+// POTRF).
+//
+// fp64: warp-level fp64 tensor-core MMA (mma.sync.m8n8k4.f64 -> SASS DMMA;
+//       tcgen05 has no f64 kind on sm_100a).  CTA tile 128x128x16, 8 warps
+//       (2 x 4, warp tile 64x32 = 8x4 DMMA tiles), 3-stage cp.async pipeline,
+//       shared-memory layouts padded to LD = 4 (mod 16) so every fragment load
+//       is bank-conflict free.
+// fp32: SIMT FFMA, same CTA tile, 8x8 register micro-tiles (tf32 tensor cores
+//       would miss the fp32 accuracy bar).
+//
+// Requirements (checked by the launcher): all leading dimensions even and
+// every operand origin 16-byte aligned (the workspace guarantees this).
+#include "gemm.h"
+#include "internal.h"
+
+namespace as {
+
+constexpr int GBM = 128, GBN = 128, GBK = 16, GSTAGES = 3, GTHREADS = 256;
+constexpr int LDMK = GBM + 4;   // [k][m] layout, m contiguous
+constexpr int LDKM = GBK + 4;   // [m][k] layout, k contiguous
+
+AS_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+AS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+AS_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+AS_DEV void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Stage one BK slab of op(A) (GBM x GBK) and op(B) (GBK x GBN) into smem.
+// Global element op(A)(m,k) = TA ? A[k + m*lda] : A[m + k*lda]; op(B)(k,n) = TB ? B[n + k*ldb] : B[k + n*ldb].
+// smem: !TA -> As[k*LDMK + m]; TA -> As[m*LDKM + k]; !TB -> Bs[n*LDKM + k]; TB -> Bs[k*LDMK + n].
+template <typename T, bool TA, bool TB>
+AS_DEV void gemm_stage(T* As, T* Bs, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N,
+                       int64_t K, int64_t m0, int64_t n0, int64_t k0) {
+    constexpr int V = 16 / sizeof(T);  // elements per 16-byte chunk
+    // A slab
+    if (!TA) {  // GBK columns of GBM contiguous elements
+        constexpr int CH = GBM / V;     // chunks per column
+        for (int e = threadIdx.x; e < GBK * CH; e += GTHREADS) {
+            const int kk = e / CH, mm = (e % CH) * V;
+            const int64_t gk = k0 + kk, gm = m0 + mm;
+            int bytes = 0;
+            if (gk < K && gm < M) bytes = (int)(min<int64_t>(V, M - gm) * sizeof(T));
+            const T* src = bytes ? A + gm + gk * lda : A;
+            cp_async16(As + kk * LDMK + mm, src, bytes);
+        }
+    } else {    // GBM rows (of the transposed operand) with GBK contiguous k
+        constexpr int CH = GBK / V;
+        for (int e = threadIdx.x; e < GBM * CH; e += GTHREADS) {
+            const int mm = e / CH, kk = (e % CH) * V;
+            const int64_t gk = k0 + kk, gm = m0 + mm;
+            int bytes = 0;
+            if (gm < M && gk < K) bytes = (int)(min<int64_t>(V, K - gk) * sizeof(T));
+            const T* src = bytes ? A + gk + gm * lda : A;
+            cp_async16(As + mm * LDKM + kk, src, bytes);
+        }
+    }
+    if (!TB) {  // GBN columns with GBK contiguous k
+        constexpr int CH = GBK / V;
+        for (int e = threadIdx.x; e < GBN * CH; e += GTHREADS) {
+            const int nn = e / CH, kk = (e % CH) * V;
+            const int64_t gk = k0 + kk, gn = n0 + nn;
+            int bytes = 0;
+            if (gn < N && gk < K) bytes = (int)(min<int64_t>(V, K - gk) * sizeof(T));
+            const T* src = bytes ? B + gk + gn * ldb : B;
+            cp_async16(Bs + nn * LDKM + kk, src, bytes);
+        }
+    } else {    // GBK rows with GBN contiguous n
+        constexpr int CH = GBN / V;
+        for (int e = threadIdx.x; e < GBK * CH; e += GTHREADS) {
+            const int kk = e / CH, nn = (e % CH) * V;
+            const int64_t gk = k0 + kk, gn = n0 + nn;
+            int bytes = 0;
+            if (gk < K && gn < N) bytes = (int)(min<int64_t>(V, N - gn) * sizeof(T));
+            const T* src = bytes ? B + gn + gk * ldb : B;
+            cp_async16(Bs + kk * LDMK + nn, src, bytes);
+        }
+    }
+}
+
+template <bool TA>
+AS_DEV double lds_a(const double* As, int m, int k) { return TA ? As[m * LDKM + k] : As[k * LDMK + m]; }
+template <bool TB>
+AS_DEV double lds_b(const double* Bs, int k, int n) { return TB ? Bs[k * LDMK + n] : Bs[n * LDKM + k]; }
+
+constexpr int kStageElems = (GBK * LDMK > GBM * LDKM ? GBK * LDMK : GBM * LDKM);
+
+// ------------------------------------------------------------------ fp64 DMMA kernel
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GTHREADS, 1) gemm_dmma_kernel(GemmArgs g) {
+    if (g.skip && *g.skip) return;
+    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+    if (g.lower_only && n0 > m0 + GBM - 1) return;   // tile strictly above the diagonal (SYRK)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* As = (double*)smem_raw;
+    double* Bs = As + GSTAGES * kStageElems;
+    const double* A = (const double*)g.A;
+    const double* B = (const double*)g.B;
+    double* C = (double*)g.C;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+    const int gid = lane >> 2, tig = lane & 3;
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int nk = (int)((g.K + GBK - 1) / GBK);
+#pragma unroll
+    for (int s = 0; s < GSTAGES - 1; ++s) {
+        if (s < nk)
+            gemm_stage<double, TA, TB>(As + s * kStageElems, Bs + s * kStageElems, A, g.lda, B, g.ldb, g.M, g.N, g.K,
+                                       m0, n0, (int64_t)s * GBK);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<GSTAGES - 2>();
+        __syncthreads();
+        {
+            const int nxt = kt + GSTAGES - 1;
+            if (nxt < nk) {
+                const int s = nxt % GSTAGES;
+                gemm_stage<double, TA, TB>(As + s * kStageElems, Bs + s * kStageElems, A, g.lda, B, g.ldb, g.M, g.N,
+                                           g.K, m0, n0, (int64_t)nxt * GBK);
+            }
+            cp_async_commit();
+        }
+        const double* as = As + (kt % GSTAGES) * kStageElems;
+        const double* bs = Bs + (kt % GSTAGES) * kStageElems;
+#pragma unroll
+        for (int ks = 0; ks < GBK / 4; ++ks) {
+            double af[8], bf[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) af[i] = lds_a<TA>(as, wm + 8 * i + gid, ks * 4 + tig);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = lds_b<TB>(bs, ks * 4 + tig, wn + 8 * j + gid);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+    // epilogue: C -= acc
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + wm + 8 * i + gid;
+        if (r >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
+                if (c < g.N) {
+                    double* p = C + r + c * g.ldc;
+                    *p = *p - acc[i][j][h];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ fp32 SIMT kernel
+// Thread (ty, tx) of a 16x16 grid owns rows {ty*4..+3, 64+ty*4..+3} and
+// columns {tx*4..+3, 64+tx*4..+3}.  smem: As[k][m], Bs[k][n] (both contiguous
+// in the output index; loaded element-wise to allow any transpose).
+constexpr int SBK = 8;
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
+    if (g.skip && *g.skip) return;
+    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+    if (g.lower_only && n0 > m0 + GBM - 1) return;
+    __shared__ __align__(16) float As[2][SBK][GBM];
+    __shared__ __align__(16) float Bs[2][SBK][GBN];
+    const float* A = (const float*)g.A;
+    const float* B = (const float*)g.B;
+    float* C = (float*)g.C;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    const int nk = (int)((g.K + SBK - 1) / SBK);
+    float ra[4], rb[4];
+    auto gload = [&](int kt) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = threadIdx.x + q * GTHREADS;   // 0..1023 over SBK x GBM
+            const int kk = TA ? (e % SBK) : (e / GBM), mm = TA ? (e / SBK) : (e % GBM);
+            const int64_t gk = (int64_t)kt * SBK + kk, gm = m0 + mm;
+            ra[q] = (gk < g.K && gm < g.M) ? (TA ? A[gk + gm * g.lda] : A[gm + gk * g.lda]) : 0.f;
+            const int kb = TB ? (e / GBN) : (e % SBK), nb = TB ? (e % GBN) : (e / SBK);
+            const int64_t gkb = (int64_t)kt * SBK + kb, gn = n0 + nb;
+            rb[q] = (gkb < g.K && gn < g.N) ? (TB ? B[gn + gkb * g.ldb] : B[gkb + gn * g.ldb]) : 0.f;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = threadIdx.x + q * GTHREADS;
+            const int kk = TA ? (e % SBK) : (e / GBM), mm = TA ? (e / SBK) : (e % GBM);
+            As[buf][kk][mm] = ra[q];
+            const int kb = TB ? (e / GBN) : (e % SBK), nb = TB ? (e % GBN) : (e / SBK);
+            Bs[buf][kb][nb] = rb[q];
+        }
+    };
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < nk) gload(kt + 1);
+#pragma unroll
+        for (int k = 0; k < SBK; ++k) {
+            float a[8], b[8];
+            *(float4*)&a[0] = *(const float4*)&As[buf][k][ty * 4];
+            *(float4*)&a[4] = *(const float4*)&As[buf][k][64 + ty * 4];
+            *(float4*)&b[0] = *(const float4*)&Bs[buf][k][tx * 4];
+            *(float4*)&b[4] = *(const float4*)&Bs[buf][k][64 + tx * 4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (kt + 1 < nk) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+        if (r >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+            if (c < g.N) {
+                float* p = C + r + c * g.ldc;
+                *p = *p - acc[i][j];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ launcher
+template <typename K>
+static void launch_k(K kern, const GemmArgs& g, size_t smem, cudaStream_t s) {
+    dim3 grid((unsigned)((g.M + GBM - 1) / GBM), (unsigned)((g.N + GBN - 1) / GBN));
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, GTHREADS, smem, s>>>(g);
+}
+
+void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
+    if (dtype == AS_F64) {
+        const size_t smem = sizeof(double) * 2 * GSTAGES * kStageElems;
+        if (!g.TA && !g.TB) launch_k(gemm_dmma_kernel<false, false>, g, smem, s);
+        else if (!g.TA && g.TB) launch_k(gemm_dmma_kernel<false, true>, g, smem, s);
+        else if (g.TA && !g.TB) launch_k(gemm_dmma_kernel<true, false>, g, smem, s);
+        else launch_k(gemm_dmma_kernel<true, true>, g, smem, s);
+    } else {
+        if (!g.TA && !g.TB) launch_k(gemm_sgemm_kernel<false, false>, g, 0, s);
+        else if (!g.TA && g.TB) launch_k(gemm_sgemm_kernel<false, true>, g, 0, s);
+        else if (g.TA && !g.TB) launch_k(gemm_sgemm_kernel<true, false>, g, 0, s);
+        else launch_k(gemm_sgemm_kernel<true, true>, g, 0, s);
+    }
+}
+
+}  // namespace as

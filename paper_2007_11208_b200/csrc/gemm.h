@@ -1,0 +1,19 @@
+// gemm.h -- C -= op(A) op(B) launcher (gemm.cu).
+#pragma once
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+namespace as {
+
+struct GemmArgs {
+    int64_t M, N, K;
+    const void* A; int64_t lda; bool TA;
+    const void* B; int64_t ldb; bool TB;
+    void* C; int64_t ldc;
+    bool lower_only;        // skip CTA tiles strictly above the diagonal (SYRK)
+    const int* skip;        // device flag: kernel returns at once if *skip != 0
+};
+
+void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s);
+
+}  // namespace as

@@ -1,0 +1,51 @@
+// internal.h -- host-side declarations shared by the libadaptsolve sources.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace as {
+
+// Per-call pointers, written on device by set_args_kernel (first graph node).
+struct DevArgs {
+    const void* A;
+    const void* B;
+    void* X;
+    void* sigma;        // optional fallback singular values (device)
+    as_report* rep_dev; // optional device report
+    as_report* rep_host;// optional mapped pinned host report
+};
+
+// Workspace layout of a plan (all device pointers; see api.cu).
+struct Work {
+    int dtype;           // AS_F64 / AS_F32
+    int64_t n, nrhs, lda, ldb;
+    int64_t ldw;         // leading dimension of W (n rounded up to a multiple of 4)
+    DevState* st;
+    DevArgs* args;
+    void* W;             // n x n (ld n): LU / Cholesky factors, band storage, QR/Jacobi matrix
+    void* diag;          // n (detection: contiguous copy of diag(A))
+    void* xe;            // n (estimator vector)
+    void* Dinv0;         // n x kNB inverted diagonal blocks (first triangular factor)
+    void* Dinv1;         // n x kNB (second triangular factor)
+    void* vec;           // scratch n x max(nrhs,2) (QR c = Q^T b etc.)
+    void* yv;            // n x nrhs (fallback V^T c)
+    int64_t* ipiv;       // n
+    int64_t* perm;       // n (LU row permutation)
+    unsigned* flags_ts;  // sync-free triangular-solve tickets/flags: (n/kNB+1) * tiles + 64
+    int64_t flags_ts_len;
+    unsigned* bars;      // cooperative-kernel barrier counters (zeroed per solve)
+    int64_t bars_len;
+    void* cand;          // LU panel candidates
+    int num_sms;
+};
+
+// launchers (each enqueues on `s`; used while capturing the plan's graph)
+void launch_state_init(const Work& w, cudaStream_t s, uint32_t opts, int force_method, double thr, double cut,
+                       int max_sweeps);
+void launch_detect(const Work& w, cudaStream_t s, bool fullscan);
+void launch_dispatch(const Work& w, cudaStream_t s, cudaGraphConditionalHandle h_method);
+void launch_copy_b_to_x(const Work& w, cudaStream_t s);   // band.cu
+
+}  // namespace as

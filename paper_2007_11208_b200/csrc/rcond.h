@@ -1,0 +1,17 @@
+// rcond.h -- estimator launcher and band-solve hooks.
+#pragma once
+#include "internal.h"
+#include "trsm.h"
+
+namespace as {
+
+enum { KIND_LU = 0, KIND_BAND = 1, KIND_TRI = 2, KIND_CHOL = 3 };
+
+void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaStream_t s);
+
+// band.cu
+void launch_band_factor(const Work& w, cudaStream_t s);            // pack + anorm + gbtrf
+void launch_band_apply(const Work& w, bool trans, int slot, cudaStream_t s);  // estimator M / M^T on xe
+void launch_band_solve(const Work& w, cudaStream_t s);             // X = A^{-1} B (gbtrs)
+
+}  // namespace as

@@ -1,0 +1,291 @@
+// svd.cu -- K8/K9: the SVD-based minimum-norm fallback (the xGELSD
+// role).  x = V_A Sigma^+ U_A^T b (Z17) computed as
+//   (1) Householder QR of the original A (cooperative kernel, 2 grid barriers
+//       per column), c = Q^T b applied to the right-hand sides;
+//   (2) one-sided (Hestenes) Jacobi on M = R^T (Z16: QR preconditioning),
+//       parallel round-robin ("circle method") pair ordering, one
+//       cooperative kernel per sweep, sweeps driven by a CUDA-graph WHILE
+//       node until a sweep makes no rotation (cap max_sweeps);
+//       the rotations are applied to y = V_J^T c instead of accumulating V_J;
+//   (3) sigma_k = ||m_k||, rank = #{sigma_k > cut * sigma_max} (Z14);
+//   (4) x = sum_{kept k} m_k y_k / sigma_k^2.
+#include "internal.h"
+#include "svd.h"
+
+namespace as {
+
+constexpr int kSvdThreads = 256;
+
+template <typename T>
+AS_DEV T block_sum256(T v, T* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (int)(blockDim.x >> 5) ? sh[l] : T(0);
+        v = warp_sum(v);
+        if (l == 0) sh[0] = v;
+    }
+    __syncthreads();
+    v = sh[0];
+    __syncthreads();
+    return v;
+}
+
+// ------------------------------------------------------------------ setup
+// W = A, Y = B (n x nrhs, ld n)
+template <typename T>
+__global__ void svd_setup_kernel(const DevArgs* args, int64_t lda, int64_t ldb, int64_t n, int64_t nrhs, T* W,
+                                 int64_t ldw, T* Y, DevState* st) {
+    const T* A = (const T*)args->A;
+    const T* B = (const T*)args->B;
+    const int64_t tot = n * n + n * nrhs;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < n * n) { const int64_t i = e % n, j = e / n; W[i + j * ldw] = A[i + j * lda]; }
+        else { const int64_t f = e - n * n, i = f % n, j = f / n; Y[i + j * n] = B[i + j * ldb]; }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->sweeps = 0; st->rotated = 0; st->svd_conv = 0; }
+}
+
+// ------------------------------------------------------------------ (1) Householder QR
+template <typename T>
+__global__ void __launch_bounds__(kSvdThreads, 1) qr_kernel(T* W, int64_t ldw, int64_t n, T* Y, int64_t nrhs,
+                                                            T* tau, unsigned* bar) {
+    __shared__ T sh[32];
+    const int P = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp, nwarps = (int64_t)P * (blockDim.x >> 5);
+    unsigned gen = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        if (blockIdx.x == 0) {
+            T* col = W + j * ldw;
+            T ss = T(0);
+            for (int64_t i = j + 1 + threadIdx.x; i < n; i += blockDim.x) { const T x = __ldcg(&col[i]); ss += x * x; }
+            ss = block_sum256(ss, sh);
+            const T alpha = __ldcg(&col[j]);
+            const T xnorm = sqrt(ss);
+            T t = T(0);
+            if (xnorm != T(0)) {
+                const T aa = alpha < T(0) ? -alpha : alpha;
+                const T wv = aa > xnorm ? aa : xnorm, z = aa > xnorm ? xnorm : aa;
+                const T hyp = wv * sqrt(T(1) + (z / wv) * (z / wv));
+                const T beta = alpha >= T(0) ? -hyp : hyp;
+                t = (beta - alpha) / beta;
+                const T scal = T(1) / (alpha - beta);
+                for (int64_t i = j + 1 + threadIdx.x; i < n; i += blockDim.x) col[i] = __ldcg(&col[i]) * scal;
+                __syncthreads();
+                if (threadIdx.x == 0) col[j] = beta;
+            }
+            if (threadIdx.x == 0) tau[j] = t;
+        }
+        grid_barrier(bar, ++gen, (unsigned)P);
+        const T tj = __ldcg(&tau[j]);
+        if (tj != T(0)) {
+            const T* v = W + j * ldw;
+            for (int64_t k = j + 1 + gw; k < n + nrhs; k += nwarps) {
+                T* col = k < n ? W + k * ldw : Y + (k - n) * n;
+                T s = T(0);
+                for (int64_t i = j + lane; i < n; i += 32) s += (i == j ? T(1) : __ldcg(&v[i])) * __ldcg(&col[i]);
+                s = warp_sum(s) * tj;
+                for (int64_t i = j + lane; i < n; i += 32) col[i] = __ldcg(&col[i]) - s * (i == j ? T(1) : __ldcg(&v[i]));
+            }
+        }
+        grid_barrier(bar, ++gen, (unsigned)P);
+    }
+}
+
+// M = R^T in place: M_ij = R_ji (i >= j), 0 above the diagonal
+template <typename T>
+__global__ void transpose_r_kernel(T* W, int64_t ldw, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % n, j = e / n;
+        if (i > j) { W[i + j * ldw] = W[j + i * ldw]; W[j + i * ldw] = T(0); }
+    }
+}
+
+// ------------------------------------------------------------------ (2) one Jacobi sweep
+template <typename T>
+__global__ void __launch_bounds__(kSvdThreads, 1) jacobi_sweep_kernel(T* M, int64_t ldw, int64_t n, T* Y, int64_t nrhs,
+                                                                      DevState* st, unsigned* bar) {
+    const int P = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp, nwarps = (int64_t)P * (blockDim.x >> 5);
+    const T tol = (T)n * Eps<T>::v;
+    const int64_t n2 = n + (n & 1), npairs = n2 / 2, rounds = n2 - 1;
+    int my_rot = 0;
+    for (int64_t r = 0; r < rounds; ++r) {
+        for (int64_t k = gw; k < npairs; k += nwarps) {
+            const int64_t s1 = k, s2 = n2 - 1 - k;
+            const int64_t a = s1 == 0 ? 0 : 1 + (s1 - 1 + r) % (n2 - 1);
+            const int64_t b = s2 == 0 ? 0 : 1 + (s2 - 1 + r) % (n2 - 1);
+            if (a >= n || b >= n) continue;
+            const int64_t p = a < b ? a : b, q = a < b ? b : a;
+            T* mp = M + p * ldw;
+            T* mq = M + q * ldw;
+            T al = T(0), be = T(0), ga = T(0);
+            for (int64_t i = lane; i < n; i += 32) {
+                const T x = __ldcg(&mp[i]), y = __ldcg(&mq[i]);
+                al += x * x; be += y * y; ga += x * y;
+            }
+            al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+            if (ga == T(0) || !((ga < T(0) ? -ga : ga) > tol * sqrt(al) * sqrt(be))) continue;
+            ++my_rot;
+            const T zeta = (be - al) / (T(2) * ga);
+            const T t = (zeta >= T(0) ? T(1) : T(-1)) / ((zeta < T(0) ? -zeta : zeta) + sqrt(T(1) + zeta * zeta));
+            const T c = T(1) / sqrt(T(1) + t * t);
+            const T s = c * t;
+            for (int64_t i = lane; i < n; i += 32) {
+                const T x = __ldcg(&mp[i]), y = __ldcg(&mq[i]);
+                mp[i] = c * x - s * y;
+                mq[i] = s * x + c * y;
+            }
+            for (int64_t rr = lane; rr < nrhs; rr += 32) {
+                const T x = __ldcg(&Y[p + rr * n]), y = __ldcg(&Y[q + rr * n]);
+                Y[p + rr * n] = c * x - s * y;
+                Y[q + rr * n] = s * x + c * y;
+            }
+        }
+        grid_barrier(bar, (unsigned)(r + 1), (unsigned)P);
+    }
+    if (lane == 0 && my_rot) atomicAdd(&st->rotated, my_rot);
+}
+
+// WHILE-node condition: another sweep iff this one rotated and the cap is not hit
+__global__ void sweep_check_kernel(DevState* st, unsigned* bar, cudaGraphConditionalHandle h) {
+    if (threadIdx.x != 0) return;
+    st->sweeps += 1;
+    const int rot = st->rotated;
+    st->rotated = 0;
+    *bar = 0u;  // fresh barrier counter for the next sweep
+    __threadfence();
+    unsigned cont = 0;
+    if (rot == 0) st->svd_conv = 1;
+    else if (st->sweeps < st->max_sweeps) cont = 1;
+    if (h) cudaGraphSetConditional(h, cont);
+}
+
+// ------------------------------------------------------------------ (3) sigma, rank
+template <typename T>
+__global__ void sigma_kernel(const T* M, int64_t ldw, int64_t n, T* sig, DevState* st) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    double best = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n; k += warps) {
+        T s = T(0);
+        for (int64_t i = lane; i < n; i += 32) { const T x = M[i + k * ldw]; s += x * x; }
+        s = warp_sum(s);
+        const T sg = sqrt(s);
+        if (lane == 0) sig[k] = sg;
+        if ((double)sg > best) best = (double)sg;
+    }
+    if (lane == 0 && best > 0.0) atomicMax(&st->smax_bits, dbits(best));
+}
+
+// rank and the optional descending copy of sigma (rank-based placement, stable)
+template <typename T>
+__global__ void rank_sort_kernel(const T* sig, int64_t n, DevState* st, const DevArgs* args) {
+    T* out = (T*)args->sigma;
+    const T smax = (T)dfrom(st->smax_bits);
+    const T cut = (T)st->lsq_cut;
+    long long kept = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const T sk = sig[k];
+        if (sk > cut * smax) ++kept;
+        if (out) {
+            int64_t pos = 0;
+            for (int64_t j = 0; j < n; ++j) {
+                const T sj = sig[j];
+                if (sj > sk || (sj == sk && j < k)) ++pos;
+            }
+            out[pos] = sk;
+        }
+    }
+    if (kept) atomicAdd((unsigned long long*)&st->rank, (unsigned long long)kept);
+}
+
+// ------------------------------------------------------------------ (4) x = sum m_k y_k / sigma_k^2
+template <typename T>
+__global__ void minnorm_kernel(const T* M, int64_t ldw, int64_t n, const T* Y, int64_t nrhs, const T* sig,
+                               const DevState* st, const DevArgs* args, int64_t ldb) {
+    T* X = (T*)args->X;
+    const T smax = (T)dfrom(st->smax_bits);
+    const T cut = (T)st->lsq_cut;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * nrhs; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % n, r = e / n;
+        T acc = T(0);
+        for (int64_t k = 0; k < n; ++k) {
+            const T sk = sig[k];
+            if (!(sk > cut * smax)) continue;
+            acc += M[i + k * ldw] * (Y[k + r * n] / (sk * sk));
+        }
+        X[i + r * ldb] = acc;
+    }
+}
+
+__global__ void svd_done_kernel(DevState* st) {
+    if (threadIdx.x != 0) return;
+    st->flags |= AS_FLAG_FALLBACK;
+    st->method = AS_METHOD_SVD;
+    if (st->rank < 0) st->rank = 0;
+    if (st->rank < st->n) st->flags |= AS_FLAG_RANK_DEF;
+    if (!st->svd_conv) { st->flags |= AS_FLAG_SVD_NOCONV; st->ret = AS_ERR_SVD_NOT_CONVERGED; }
+}
+
+__global__ void svd_rank_reset_kernel(DevState* st) {
+    if (threadIdx.x == 0) { st->rank = 0; st->smax_bits = 0ull; }
+}
+
+// ------------------------------------------------------------------ launchers
+template <typename K, typename... Args>
+static void coop_launch(K kern, int P, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(kSvdThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename T>
+static void svd_pre_t(const Work& w, cudaStream_t s) {
+    T* W = (T*)w.W;
+    T* Y = (T*)w.yv;
+    svd_setup_kernel<T><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.lda, w.ldb, w.n, w.nrhs, W, w.ldw, Y, w.st);
+    coop_launch(qr_kernel<T>, w.num_sms, s, W, w.ldw, w.n, Y, w.nrhs, (T*)w.xe, w.bars + 0);
+    transpose_r_kernel<T><<<w.num_sms * 4, 256, 0, s>>>(W, w.ldw, w.n);
+}
+
+template <typename T>
+static void svd_sweep_t(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s) {
+    coop_launch(jacobi_sweep_kernel<T>, w.num_sms, s, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
+    sweep_check_kernel<<<1, 32, 0, s>>>(w.st, w.bars + 1, h);
+}
+
+template <typename T>
+static void svd_post_t(const Work& w, cudaStream_t s) {
+    T* sig = (T*)w.xe;
+    svd_rank_reset_kernel<<<1, 32, 0, s>>>(w.st);
+    sigma_kernel<T><<<w.num_sms * 2, 256, 0, s>>>((const T*)w.W, w.ldw, w.n, sig, w.st);
+    rank_sort_kernel<T><<<(unsigned)std::min<int64_t>((w.n + 255) / 256, 1024), 256, 0, s>>>(sig, w.n, w.st, w.args);
+    minnorm_kernel<T><<<w.num_sms * 4, 256, 0, s>>>((const T*)w.W, w.ldw, w.n, (const T*)w.yv, w.nrhs, sig, w.st,
+                                                     w.args, w.ldb);
+    svd_done_kernel<<<1, 32, 0, s>>>(w.st);
+}
+
+void launch_svd_pre(const Work& w, cudaStream_t s) {
+    if (w.dtype == AS_F64) svd_pre_t<double>(w, s); else svd_pre_t<float>(w, s);
+}
+void launch_svd_sweep(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s) {
+    if (w.dtype == AS_F64) svd_sweep_t<double>(w, h, s); else svd_sweep_t<float>(w, h, s);
+}
+void launch_svd_post(const Work& w, cudaStream_t s) {
+    if (w.dtype == AS_F64) svd_post_t<double>(w, s); else svd_post_t<float>(w, s);
+}
+
+}  // namespace as

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (north star, readings Z18-Z21 in DESIGN.md):
+  detection flags, kl/ku, method, CHOL_FAILED, SINGULAR, FALLBACK, gate bit: bit-exact;
+  fp64: eta <= 1e-13 and phi <= 1e-15 cond_1 (cond_1 = anorm / rcond_oracle);
+  fp32: eta <= 1e-5 and phi <= 1e-6 cond_1 against the fp64 oracle on the promoted data.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from helpers import backward_error, forward_diff, load_fig1
+
+pytestmark = pytest.mark.gpu
+
+AS = pytest.importorskip("paper_2007_11208_b200") if torch.cuda.is_available() else None
+
+
+def gpu_solve(A, B, **opt):
+    o = AS.make_options(**opt) if opt else None
+    ret, X, rep = AS.as_solve_ex(AS.to_device(A), AS.to_device(B), options=o)
+    torch.cuda.synchronize()
+    return ret, AS.to_host(X), rep
+
+
+def oracle_opts(opt):
+    return {k: v for k, v in opt.items()}
+
+
+def check_parity(A, B, fp32=False, **opt):
+    ret, X, rep = gpu_solve(A, B, **opt)
+    oret, Xo, orep, _ = oracle.solve(A, B, **oracle_opts(opt))
+    assert ret == oret, (ret, oret, rep, orep)
+    # exact bits: detection verdicts, method, chol-failed, singular, gate, fallback
+    mask = 0xFF | oracle.F_CHOL_FAILED | oracle.F_SINGULAR | oracle.F_RCOND_LOW | oracle.F_FALLBACK | oracle.F_POORLY_COND
+    assert (rep["flags"] & mask) == (orep["flags"] & mask), (hex(rep["flags"]), hex(orep["flags"]), rep, orep)
+    assert rep["method"] == orep["method"] and rep["primary_method"] == orep["primary_method"]
+    if orep["kl"] >= 0:
+        assert (rep["kl"], rep["ku"]) == (orep["kl"], orep["ku"])
+    if ret != 0:
+        return rep, orep
+    # soft rcond check where the estimate is numerically meaningful (rcond >> eps)
+    if orep["rcond"] > 1e-10 and rep["rcond"] > 0:
+        assert abs(np.log2(rep["rcond"] / orep["rcond"])) <= 1.0, (rep["rcond"], orep["rcond"])
+    if not (rep["flags"] & oracle.F_FALLBACK):
+        if fp32:
+            A64, B64 = A.astype(np.float64), B.astype(np.float64)
+            _, Xr, rr, _ = oracle.solve(A64, B64, no_fallback=True)
+            cond = rr["anorm"] / rr["rcond"]
+            assert backward_error(A64, X, B64) <= 1e-5
+            assert forward_diff(X, Xr) <= 1e-6 * cond
+        else:
+            cond = orep["anorm"] / orep["rcond"] if orep["rcond"] > 0 else np.inf
+            assert backward_error(A, X, B) <= 1e-13, backward_error(A, X, B)
+            assert forward_diff(X, Xo) <= 1e-15 * cond, (forward_diff(X, Xo), cond)
+    return rep, orep
+
+
+# ------------------------------------------------------------------ detection
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("seed", range(24))
+def test_detect_random_patterns(seed, dtype):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    i, j = np.indices((n, n))
+    kind = seed % 6
+    if kind == 0:
+        kl, ku = int(rng.integers(0, n)), int(rng.integers(0, n))
+        A = np.where((i - j <= kl) & (j - i <= ku), rng.standard_normal((n, n)), 0.0)
+    elif kind == 1:
+        A = np.tril(rng.standard_normal((n, n)))
+    elif kind == 2:
+        A = np.triu(rng.standard_normal((n, n)))
+    elif kind == 3:
+        A = W.random_spd_fig3(n, seed)
+    elif kind == 4:
+        A = np.eye(n) * 3.0
+        A[rng.integers(0, n), rng.integers(0, n)] = 1e-300 if dtype == np.float64 else 1e-30
+    else:
+        A = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.01)
+        A[np.arange(n), np.arange(n)] = 5.0
+    A = np.asfortranarray(A.astype(dtype))
+    d = oracle.detect(A)
+    for fullscan in (False, True):
+        ret, st = AS.as_detect(AS.to_device(A), fullscan=fullscan)
+        assert ret == 0
+        assert st["flags"] == d.flags, (st, d)
+        assert st["method"] == d.method
+        if fullscan or d.banded:
+            assert (st["kl"], st["ku"]) == (d.kl, d.ku)
+
+
+def test_detect_fig1_and_edges():
+    for name, M in load_fig1().items():
+        d = oracle.detect(M)
+        ret, st = AS.as_detect(AS.to_device(M), fullscan=True)
+        assert st["flags"] == d.flags and (st["kl"], st["ku"]) == (d.kl, d.ku), name
+    # -0.0 and NaN corners, lda padding
+    n = 130
+    A = np.eye(n)
+    A[0, n - 1] = -0.0
+    A[n - 1, 0] = np.nan
+    big = np.full((n + 3, n), 9.0, order="F")
+    big[:n] = A
+    import torch as T
+    tA = AS.to_device(big)[:n]
+    ret, st = AS.as_detect(tA, fullscan=True)
+    d = oracle.detect(np.asfortranarray(A))
+    assert st["flags"] == d.flags and (st["kl"], st["ku"]) == (d.kl, d.ku)
+
+
+@pytest.mark.parametrize("tag", ["C1", "C2", "C3a", "C3b", "C4"])
+def test_detect_configs_full_size(tag):
+    A, _ = W.make(tag)
+    d = oracle.detect(A)
+    ret, st = AS.as_detect(AS.to_device(A))
+    assert st["flags"] == d.flags and st["method"] == d.method
+    if d.banded:
+        assert (st["kl"], st["ku"]) == (d.kl, d.ku)
+
+
+# ------------------------------------------------------------------ solves, small sizes spanning tiles
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 65, 200, 333])
+def test_lu_dense(n):
+    A = W.random_dense(n, seed=n, shift=2.0)
+    B = np.asfortranarray(np.random.default_rng(n).standard_normal((n, 3)))
+    check_parity(A, B)
+
+
+@pytest.mark.parametrize("n,kl,ku", [(40, 1, 1), (300, 3, 2), (257, 8, 8), (500, 0, 5), (500, 6, 0), (1000, 20, 3)])
+def test_banded(n, kl, ku):
+    A = W.random_banded(n, kl, ku, seed=n + kl, dominant=(kl + ku) % 2 == 0)
+    B = np.asfortranarray(np.random.default_rng(1).standard_normal((n, 2)))
+    rep, orep = check_parity(A, B)
+    assert rep["primary_method"] == oracle.M_BAND
+
+
+@pytest.mark.parametrize("n", [5, 64, 129, 300])
+@pytest.mark.parametrize("upper", [False, True])
+def test_triangular(n, upper):
+    A = W.random_triangular(n, upper, seed=n)
+    B = np.asfortranarray(np.random.default_rng(2).standard_normal((n, 5)))
+    rep, _ = check_parity(A, B)
+    assert rep["primary_method"] == (oracle.M_TRI_UPPER if upper else oracle.M_TRI_LOWER)
+
+
+@pytest.mark.parametrize("n", [4, 63, 64, 150, 257])
+def test_spd(n):
+    A = W.random_spd_fig3(n, seed=n)
+    B = np.asfortranarray(np.random.default_rng(3).standard_normal((n, 4)))
+    rep, _ = check_parity(A, B)
+    assert rep["primary_method"] == oracle.M_CHOL
+
+
+def test_chol_fail_to_lu():
+    A = np.asfortranarray(np.array([[1, .9, .9], [.9, 1, -.9], [.9, -.9, 1]]))
+    rep, _ = check_parity(A, np.asfortranarray(np.array([[1.0], [2.0], [3.0]])))
+    assert rep["flags"] & oracle.F_CHOL_FAILED and rep["chol_fail_col"] == 2
+    # larger: symmetric indefinite that passes Fig. 4
+    n = 100
+    rng = np.random.default_rng(5)
+    S = rng.uniform(-0.5, 0.5, (n, n))
+    S = (S + S.T) / 2
+    S[np.arange(n), np.arange(n)] = 1.0
+    S[np.abs(S) >= 1] = 0.4
+    A = np.asfortranarray(S)
+    if oracle.detect(A).spd:
+        check_parity(A, np.asfortranarray(rng.standard_normal((n, 2))))
+
+
+def test_singular_fallback_and_no_fallback():
+    A = np.asfortranarray(np.array([[1.0, 2.0], [2.0, 4.0]]))
+    B = np.asfortranarray(np.array([[3.0], [6.0]]))
+    ret, X, rep = gpu_solve(A, B)
+    assert ret == 0 and rep["method"] == oracle.M_SVD and rep["rank"] == 1
+    assert np.allclose(X.ravel(), [0.6, 1.2], atol=1e-14)
+    ret, X, rep = gpu_solve(A, B, no_fallback=True)
+    assert ret == oracle.ERR_SINGULAR_NO_FALLBACK
+
+
+def test_diag_gate_pin():
+    A = np.asfortranarray(np.diag([1.0, 1e-17]))
+    B = np.asfortranarray(np.ones((2, 1)))
+    ret, X, rep = gpu_solve(A, B)
+    assert rep["flags"] & oracle.F_FALLBACK and rep["rank"] == 1 and np.allclose(X.ravel(), [1, 0])
+    ret, X, rep = gpu_solve(A, B, no_fallback=True)
+    assert ret == 0 and rep["flags"] & oracle.F_POORLY_COND and np.array_equal(X.ravel(), [1.0, 1e17])
+
+
+@pytest.mark.parametrize("n", [64, 200])
+def test_illcond_fallback_small(n):
+    A, B, U, sigma, V = W.illcond_c4(n=n)
+    ret, X, rep = gpu_solve(A, B)
+    oret, Xo, orep, sig_o = oracle.solve(A, B)
+    assert rep["flags"] & oracle.F_FALLBACK and orep["flags"] & oracle.F_FALLBACK
+    assert abs(rep["rank"] - orep["rank"]) <= 1
+    rho = np.linalg.norm(B - A @ X) / np.linalg.norm(B)
+    rho_o = np.linalg.norm(B - A @ Xo) / np.linalg.norm(B)
+    assert abs(rho - rho_o) <= 1e-2 * rho_o
+
+
+@pytest.mark.parametrize("method", [oracle.M_LU, oracle.M_CHOL, oracle.M_BAND])
+def test_force_method(method):
+    A = W.random_banded(120, 2, 2, seed=4, dominant=True)
+    A = np.asfortranarray((A + A.T) / 2)
+    B = np.asfortranarray(np.ones((120, 1)))
+    rep, _ = check_parity(A, B, force_method=method)
+    assert rep["primary_method"] == method
+
+
+def test_fp32_paths():
+    for A, B in [W.make("C1", n=200), W.make("C2", n=300, nrhs=2), W.make("C3a", n=130, nrhs=3),
+                 W.make("C3b", n=150, nrhs=3)]:
+        check_parity(A.astype(np.float32, order="F"), B.astype(np.float32, order="F"), fp32=True)
+
+
+def test_inplace_alias():
+    A, B = W.make("C1", n=100)
+    tA, tB = AS.to_device(A), AS.to_device(B)
+    ret, X, rep = AS.as_solve_ex(tA, tB, X=tB)
+    torch.cuda.synchronize()
+    _, Xo, _, _ = oracle.solve(A, B)
+    assert forward_diff(AS.to_host(tB), Xo) < 1e-12
+
+
+def test_host_entry_point():
+    A, B = W.make("C1", n=150)
+    ret, X, rep = AS.as_solve_host(A, B)
+    _, Xo, orep, _ = oracle.solve(A, B)
+    assert ret == 0 and rep["method"] == orep["method"]
+    assert forward_diff(X, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"]
+
+
+def test_empty_and_illegal():
+    e = torch.empty((0, 0), dtype=torch.float64, device="cuda")
+    ret, X, rep = AS.as_solve_ex(e, e, X=e)
+    assert ret == 0 and rep["rcond"] == 1.0
+    A = AS.to_device(np.eye(3))
+    import ctypes as C
+    ret = AS.lib().as_solve(0, A.data_ptr(), 2, 3, A.data_ptr(), 3, 1, A.data_ptr(), None, None, None)
+    assert ret == -3
+    hostA = np.eye(3)
+    ret = AS.lib().as_solve(0, hostA.ctypes.data, 3, 3, A.data_ptr(), 3, 1, A.data_ptr(), None, None, None)
+    assert ret == -2
