@@ -166,6 +166,26 @@ int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detec
 int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
                         void* W, int64_t* ipiv, void* stream);
 
+/* Benchmark instrumentation.  When enabled, plans built afterwards record
+ * CUDA events (graph event-record nodes) around the top-level stages of the
+ * solve; as_last_stage_ms() returns the device-timed durations (ms) of the
+ * last synchronous call on this thread: [0] detection (diag + tile-pair
+ * pass + dispatch), [1] the method body (factor + rcond estimate),
+ * [2] gate + post (primary solve or SVD fallback), [3] whole graph.
+ * Returns 0, or -1 if the last plan was not instrumented. */
+void as_set_instrumentation(int enable);
+int as_last_stage_ms(double* out4);
+
+/* Execution mode of plans built afterwards: 0 (default) = one CUDA graph with
+ * device-side conditional nodes, one host sync per call; 1 = eager profiling
+ * mode: the same kernels launched directly, branch decisions read back by the
+ * host (several syncs; for kernel-by-kernel ncu launch lists only). */
+void as_set_exec_mode(int eager);
+
+/* Roofline denominator probe (benchmark only, not part of a solve): fp64
+ * tensor-core (DMMA) throughput in TFLOP/s of a register-resident MMA loop. */
+double as_measure_fp64_peak(int iters, void* stream);
+
 /* Workspace bytes a plan for this shape allocates (device). */
 int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs);
 /* Number of kernel launches the last as_solve* on this thread enqueued

@@ -36,7 +36,8 @@ ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
 
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
            "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
-           "as_strerror", "as_version")
+           "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
+           "as_set_exec_mode")
 
 
 class Options(C.Structure):
@@ -197,6 +198,46 @@ def as_detect(A, fullscan=False, stream=None):
     ret = _lib.as_detect(_dt(A), A.data_ptr(), _ld(A), A.shape[0], OPT_FULLSCAN if fullscan else 0, C.byref(st),
                          _stream_ptr(stream))
     return ret, {k: getattr(st, k) for k, _ in st._fields_}
+
+
+_lib.as_set_instrumentation.argtypes = [C.c_int]
+_lib.as_last_stage_ms.argtypes = [P]
+_lib.as_last_stage_ms.restype = C.c_int
+
+
+_lib.as_measure_fp64_peak.argtypes = [C.c_int, P]
+_lib.as_measure_fp64_peak.restype = C.c_double
+
+
+def measure_fp64_peak(iters: int = 20000, stream=None) -> float:
+    """fp64 DMMA TFLOP/s of a register-resident loop (roofline denominator)."""
+    return float(_lib.as_measure_fp64_peak(int(iters), _stream_ptr(stream)))
+
+
+_lib.as_set_exec_mode.argtypes = [C.c_int]
+
+
+def set_exec_mode(eager: bool) -> None:
+    """eager=True: plans built afterwards launch kernels directly (profiling mode)."""
+    _lib.as_set_exec_mode(1 if eager else 0)
+
+
+def set_instrumentation(enable: bool) -> None:
+    """Plans built afterwards record CUDA events around the solve's top-level stages."""
+    _lib.as_set_instrumentation(1 if enable else 0)
+
+
+def last_stage_ms():
+    """Device-timed [detect, factor+estimate, gate+solve/fallback, total] ms of the last call (or None)."""
+    out = (C.c_double * 4)()
+    if _lib.as_last_stage_ms(out) != 0:
+        return None
+    return list(out)
+
+
+def last_kernel_nodes() -> int:
+    """Kernel launches (graph kernel nodes) the last synchronous call executed."""
+    return int(_lib.as_last_kernel_nodes())
 
 
 def workspace_bytes(dtype_code: int, n: int, nrhs: int) -> int:

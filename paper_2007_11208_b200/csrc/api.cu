@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "factor.h"
+#include "gemm.h"
 #include "internal.h"
 #include "rcond.h"
 #include "svd.h"
@@ -82,7 +83,8 @@ __global__ void gate_kernel(DevState* st, cudaGraphConditionalHandle h_post) {
         }
     }
     st->gate = gate ? 1 : 0;
-    cudaGraphSetConditional(h_post, post);
+    st->post = (int)post;
+    if (h_post) cudaGraphSetConditional(h_post, post);
 }
 
 __global__ void solve_dispatch_kernel(DevState* st, cudaGraphConditionalHandle h) {
@@ -119,6 +121,8 @@ static int check(cudaError_t e, const char* what) {
     }
     return 0;
 }
+
+static int64_t count_kernels(cudaGraph_t g);
 
 static cudaGraphConditionalHandle make_handle(cudaStream_t s, unsigned defval) {
     cudaStreamCaptureStatus stt;
@@ -177,6 +181,35 @@ static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
     launch_trtri_blocks(w.dtype, nullptr, w.lda, w.n, w.Dinv0, upper, false, w.st, true, w.args, s);
 }
 
+// ------------------------------------------------------------------ branch bodies (shared by graph and eager modes)
+constexpr int kCholOk = 100;
+
+static void body_factor(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
+    switch (m) {
+    case AS_METHOD_BAND: launch_band_factor(w, s); launch_estimator(w, KIND_BAND, false, sa, s); break;
+    case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); launch_estimator(w, KIND_TRI, false, sa, s); break;
+    case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); launch_estimator(w, KIND_TRI, true, sa, s); break;
+    case AS_METHOD_LU: launch_lu_factor(w, s); launch_estimator(w, KIND_LU, false, sa, s); break;
+    case kCholOk: launch_chol_tri_prep(w, s); launch_estimator(w, KIND_CHOL, false, sa, s); break;
+    default: break;
+    }
+}
+
+static void body_solve(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
+    switch (m) {
+    case AS_METHOD_BAND: launch_band_solve(w, s); break;
+    case AS_METHOD_TRI_LOWER:
+    case AS_METHOD_TRI_UPPER:
+        launch_copy_b_to_x(w, s);
+        launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, m == AS_METHOD_TRI_UPPER, false, nullptr, w.ldb, w.n,
+                    (int)w.nrhs, sa.take(trsm_sync_words(w.n, (int)w.nrhs)), -1, false, w.args, w.st, s);
+        break;
+    case AS_METHOD_CHOL: launch_chol_solve(w, sa, s); break;
+    case AS_METHOD_LU: launch_lu_solve(w, sa, s); break;
+    default: break;
+    }
+}
+
 // ------------------------------------------------------------------ plans
 struct PlanKey {
     int dev, dtype;
@@ -185,11 +218,16 @@ struct PlanKey {
     int force;
     double thr, cut;
     int sweeps;
+    int instrumented;
+    int eager;
     bool operator<(const PlanKey& o) const {
-        return std::tie(dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps) <
-               std::tie(o.dev, o.dtype, o.n, o.nrhs, o.lda, o.ldb, o.opts, o.force, o.thr, o.cut, o.sweeps);
+        return std::tie(dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps, instrumented, eager) <
+               std::tie(o.dev, o.dtype, o.n, o.nrhs, o.lda, o.ldb, o.opts, o.force, o.thr, o.cut, o.sweeps,
+                        o.instrumented, o.eager);
     }
 };
+static int g_instrument = 0;
+static int g_eager = 0;
 
 struct Plan {
     PlanKey key{};
@@ -201,8 +239,13 @@ struct Plan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t args_node = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // kernel-node counts per branch (for the launch count a call executes)
+    int64_t nodes_top = 0, nodes_method[8] = {}, nodes_chol_lu = 0, nodes_chol_ok = 0;
+    int64_t nodes_solve_hdr = 0, nodes_solve[8] = {}, nodes_fallback = 0, nodes_sweep = 0;
     std::mutex mu;
     ~Plan() {
+        for (auto e : ev) if (e) cudaEventDestroy(e);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (ws) cudaFree(ws);
@@ -256,6 +299,9 @@ static int build_graph(Plan& P) {
     }
     const PlanKey& k = P.key;
     cudaStream_t s0 = B.streams[0];
+    cudaGraph_t g_cb0 = nullptr, g_cb1 = nullptr, g_wb = nullptr, g_sb[6] = {};
+    cudaGraph_t* mb = nullptr;
+    cudaGraph_t* pb = nullptr;
     int err = check(cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed), "BeginCapture");
     if (!err) {
         DevArgs a0{};
@@ -269,74 +315,61 @@ static int build_graph(Plan& P) {
         }
         launch_state_init(w, s0, k.opts, k.force, k.thr, k.cut, k.sweeps);
         cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s0);
+        if (k.instrumented) cudaEventRecordWithFlags(P.ev[0], s0, cudaEventRecordExternal);
         launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
         cudaGraphConditionalHandle h_method = make_handle(s0, 0);
         launch_dispatch(w, s0, h_method);
-        cudaGraph_t* mb = add_cond(s0, h_method, cudaGraphCondTypeSwitch, 6);
+        if (k.instrumented) cudaEventRecordWithFlags(P.ev[1], s0, cudaEventRecordExternal);
+        mb = add_cond(s0, h_method, cudaGraphCondTypeSwitch, 6);
         // ---- factor + estimate bodies
-        B.body(mb[AS_METHOD_BAND], [&](cudaStream_t s) {
-            launch_band_factor(w, s);
-            launch_estimator(w, KIND_BAND, false, B.sa, s);
-        });
-        B.body(mb[AS_METHOD_TRI_LOWER], [&](cudaStream_t s) {
-            tri_prep(w, false, s);
-            launch_estimator(w, KIND_TRI, false, B.sa, s);
-        });
-        B.body(mb[AS_METHOD_TRI_UPPER], [&](cudaStream_t s) {
-            tri_prep(w, true, s);
-            launch_estimator(w, KIND_TRI, true, B.sa, s);
-        });
+        for (int m : {AS_METHOD_BAND, AS_METHOD_TRI_LOWER, AS_METHOD_TRI_UPPER, AS_METHOD_LU})
+            B.body(mb[m], [&](cudaStream_t s) { body_factor(w, m, B.sa, s); });
         B.body(mb[AS_METHOD_CHOL], [&](cudaStream_t s) {
             launch_chol_factor(w, s);
             cudaGraphConditionalHandle h_cf = make_handle(s, 0);
             launch_chol_check(w, h_cf, s);
             cudaGraph_t* cb = add_cond(s, h_cf, cudaGraphCondTypeIf, 2);
-            B.body(cb[0], [&](cudaStream_t s2) {   // failed: general LU on the original A
-                launch_lu_factor(w, s2);
-                launch_estimator(w, KIND_LU, false, B.sa, s2);
-            });
-            B.body(cb[1], [&](cudaStream_t s2) {
-                launch_chol_tri_prep(w, s2);
-                launch_estimator(w, KIND_CHOL, false, B.sa, s2);
-            });
-        });
-        B.body(mb[AS_METHOD_LU], [&](cudaStream_t s) {
-            launch_lu_factor(w, s);
-            launch_estimator(w, KIND_LU, false, B.sa, s);
+            g_cb0 = cb[0]; g_cb1 = cb[1];
+            // failed: general LU on the original A
+            B.body(cb[0], [&](cudaStream_t s2) { body_factor(w, AS_METHOD_LU, B.sa, s2); });
+            B.body(cb[1], [&](cudaStream_t s2) { body_factor(w, kCholOk, B.sa, s2); });
         });
         // ---- gate + post
+        if (k.instrumented) cudaEventRecordWithFlags(P.ev[2], s0, cudaEventRecordExternal);
         cudaGraphConditionalHandle h_post = make_handle(s0, 0);
         gate_kernel<<<1, 32, 0, s0>>>(w.st, h_post);
-        cudaGraph_t* pb = add_cond(s0, h_post, cudaGraphCondTypeSwitch, 3);
+        pb = add_cond(s0, h_post, cudaGraphCondTypeSwitch, 3);
         B.body(pb[1], [&](cudaStream_t s) {
             cudaGraphConditionalHandle h_solve = make_handle(s, 0);
             solve_dispatch_kernel<<<1, 32, 0, s>>>(w.st, h_solve);
             cudaGraph_t* sb = add_cond(s, h_solve, cudaGraphCondTypeSwitch, 6);
-            B.body(sb[AS_METHOD_BAND], [&](cudaStream_t s2) { launch_band_solve(w, s2); });
-            B.body(sb[AS_METHOD_TRI_LOWER], [&](cudaStream_t s2) {
-                launch_copy_b_to_x(w, s2);
-                launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, false, false, nullptr, w.ldb, w.n, (int)w.nrhs,
-                            B.sa.take(trsm_sync_words(w.n, (int)w.nrhs)), -1, false, w.args, w.st, s2);
-            });
-            B.body(sb[AS_METHOD_TRI_UPPER], [&](cudaStream_t s2) {
-                launch_copy_b_to_x(w, s2);
-                launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, true, false, nullptr, w.ldb, w.n, (int)w.nrhs,
-                            B.sa.take(trsm_sync_words(w.n, (int)w.nrhs)), -1, false, w.args, w.st, s2);
-            });
-            B.body(sb[AS_METHOD_CHOL], [&](cudaStream_t s2) { launch_chol_solve(w, B.sa, s2); });
-            B.body(sb[AS_METHOD_LU], [&](cudaStream_t s2) { launch_lu_solve(w, B.sa, s2); });
+            for (int m = 0; m < 6; ++m) g_sb[m] = sb[m];
+            for (int m = AS_METHOD_BAND; m <= AS_METHOD_LU; ++m)
+                B.body(sb[m], [&](cudaStream_t s2) { body_solve(w, m, B.sa, s2); });
         });
         B.body(pb[2], [&](cudaStream_t s) {
             launch_svd_pre(w, s);
             cudaGraphConditionalHandle h_while = make_handle(s, 1);
             set_cond_kernel<<<1, 32, 0, s>>>(h_while, 1u);
             cudaGraph_t* wb = add_cond(s, h_while, cudaGraphCondTypeWhile, 1);
+            g_wb = wb[0];
             B.body(wb[0], [&](cudaStream_t s2) { launch_svd_sweep(w, h_while, s2); });
             launch_svd_post(w, s);
         });
+        if (k.instrumented) cudaEventRecordWithFlags(P.ev[3], s0, cudaEventRecordExternal);
         finalize_kernel<<<1, 32, 0, s0>>>(w.st, P.rep_ws, w.args);
         cudaMemcpyAsync(P.rep_pinned, P.rep_ws, sizeof(RepOut), cudaMemcpyDeviceToHost, s0);
         err = check(cudaStreamEndCapture(s0, &P.graph), "EndCapture");
+        if (!err) {
+            P.nodes_top = count_kernels(P.graph);
+            for (int m = 1; m < 6; ++m) P.nodes_method[m] = count_kernels(mb[m]);
+            P.nodes_chol_lu = g_cb0 ? count_kernels(g_cb0) : 0;
+            P.nodes_chol_ok = g_cb1 ? count_kernels(g_cb1) : 0;
+            P.nodes_solve_hdr = count_kernels(pb[1]);
+            for (int m = 1; m < 6; ++m) P.nodes_solve[m] = g_sb[m] ? count_kernels(g_sb[m]) : 0;
+            P.nodes_fallback = count_kernels(pb[2]);
+            P.nodes_sweep = g_wb ? count_kernels(g_wb) : 0;
+        }
     }
     err = err ? err : B.err;
     if (!err && B.sa.used > B.sa.cap) err = AS_ERR_CUDA_BASE + 999;
@@ -363,11 +396,65 @@ static int get_plan(const PlanKey& key, Plan** out) {
     P->rep_ws = (RepOut*)((char*)w.args + align256(sizeof(DevArgs)));
     err = check(cudaMallocHost(&P->rep_pinned, sizeof(RepOut)), "cudaMallocHost");
     if (err) return err;
-    err = build_graph(*P);
+    if (key.instrumented)
+        for (auto& e : P->ev) cudaEventCreate(&e);
+    err = key.eager ? 0 : build_graph(*P);
     if (err) return err;
     *out = P.get();
     g_plans[key] = std::move(P);
     return 0;
+}
+
+// Eager mode (profiling / debugging): the same kernels launched directly on the
+// stream with the branch decisions read back by the host.  Graph kernel nodes
+// under conditional nodes cannot be profiled kernel-by-kernel by ncu; this mode
+// gives the per-kernel launch list of the identical kernels.
+static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
+    Work& w = P.w;
+    const PlanKey& k = P.key;
+    SyncAlloc sa;
+    sa.base = w.flags_ts;
+    sa.cap = w.flags_ts_len;
+    DevState h;
+    auto rd = [&]() {
+        cudaMemcpyAsync(&h, w.st, sizeof(DevState), cudaMemcpyDeviceToHost, s);
+        return check(cudaStreamSynchronize(s), "eager sync");
+    };
+    set_args_kernel2<<<1, 1, 0, s>>>(a, w.args);
+    launch_state_init(w, s, k.opts, k.force, k.thr, k.cut, k.sweeps);
+    cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s);
+    if (k.instrumented) cudaEventRecord(P.ev[0], s);
+    launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
+    launch_dispatch(w, s, 0);
+    if (k.instrumented) cudaEventRecord(P.ev[1], s);
+    int err = rd();
+    if (err) return err;
+    if (h.method == AS_METHOD_CHOL) {
+        launch_chol_factor(w, s);
+        launch_chol_check(w, 0, s);
+        if ((err = rd())) return err;
+        body_factor(w, h.chol_failed ? AS_METHOD_LU : kCholOk, sa, s);
+    } else {
+        body_factor(w, h.method, sa, s);
+    }
+    if (k.instrumented) cudaEventRecord(P.ev[2], s);
+    gate_kernel<<<1, 32, 0, s>>>(w.st, 0);
+    if ((err = rd())) return err;
+    if (h.post == 1) {
+        body_solve(w, h.method, sa, s);
+    } else if (h.post == 2) {
+        launch_svd_pre(w, s);
+        for (;;) {
+            launch_svd_sweep(w, 0, s);
+            if ((err = rd())) return err;
+            if (h.svd_conv || h.sweeps >= h.max_sweeps) break;
+        }
+        launch_svd_post(w, s);
+    }
+    if (k.instrumented) cudaEventRecord(P.ev[3], s);
+    finalize_kernel<<<1, 32, 0, s>>>(w.st, P.rep_ws, w.args);
+    cudaMemcpyAsync(P.rep_pinned, P.rep_ws, sizeof(RepOut), cudaMemcpyDeviceToHost, s);
+    return check(cudaGetLastError(), "eager launch");
 }
 
 static bool is_device_ptr(const void* p) {
@@ -377,6 +464,22 @@ static bool is_device_ptr(const void* p) {
 }
 
 static thread_local int64_t t_last_nodes = 0;
+static thread_local Plan* t_last_plan = nullptr;
+
+// kernel nodes of a graph; recursing into conditional bodies per `pick`
+static int64_t count_kernels(cudaGraph_t g) {
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    int64_t c = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t == cudaGraphNodeTypeKernel) ++c;
+    }
+    return c;
+}
 
 static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
                       void* X, const as_options* opt, as_report* rep_host, as_report* rep_dev, void* sigma,
@@ -410,6 +513,8 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     if (dt == AS_F32) key.thr = (double)(float)key.thr;
     key.cut = (opt && opt->lsq_cutoff >= 0) ? opt->lsq_cutoff : (double)n * eps;
     key.sweeps = (opt && opt->max_sweeps > 0) ? opt->max_sweeps : 30;
+    key.instrumented = g_instrument;
+    key.eager = g_eager;
     Plan* P = nullptr;
     int err = get_plan(key, &P);
     if (err) return err;
@@ -417,6 +522,15 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     DevArgs a{};
     a.A = A; a.B = B; a.X = X; a.sigma = sigma; a.rep_dev = rep_dev; a.rep_host = nullptr;
     cudaKernelNodeParams kp = {};
+    if (key.eager) {
+        err = run_eager(*P, a, stream);
+        if (err) return err;
+        t_last_plan = P;
+        if (!sync) return 0;
+        if ((err = check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"))) return err;
+        if (rep_host) *rep_host = P->rep_pinned->rep;
+        return P->rep_pinned->ret;
+    }
     DevArgs* dst = P->w.args;
     void* params[2] = {&a, &dst};
     kp.func = (void*)set_args_kernel2;
@@ -427,10 +541,20 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     if (err) return err;
     err = check(cudaGraphLaunch(P->exec, stream), "cudaGraphLaunch");
     if (err) return err;
+    t_last_plan = P;
     if (!sync) return 0;
     err = check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     if (err) return err;
     if (rep_host) *rep_host = P->rep_pinned->rep;
+    {
+        const as_report& r = P->rep_pinned->rep;
+        int64_t c = P->nodes_top + P->nodes_method[r.primary_method & 7];
+        if (r.flags & AS_FLAG_CHOL_FAILED) c += P->nodes_method[AS_METHOD_CHOL] + P->nodes_chol_lu;
+        else if (r.primary_method == AS_METHOD_CHOL) c += P->nodes_chol_ok;
+        if (r.flags & AS_FLAG_FALLBACK) c += P->nodes_fallback + (int64_t)r.sweeps * P->nodes_sweep;
+        else if (!(P->rep_pinned->ret)) c += P->nodes_solve_hdr + P->nodes_solve[r.primary_method & 7];
+        t_last_nodes = c;
+    }
     return P->rep_pinned->ret;
 }
 
@@ -598,6 +722,28 @@ int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs) {
 }
 
 int64_t as_last_kernel_nodes(void) { return t_last_nodes; }
+
+void as_set_instrumentation(int enable) { g_instrument = enable ? 1 : 0; }
+
+void as_set_exec_mode(int eager) { g_eager = eager ? 1 : 0; }
+
+double as_measure_fp64_peak(int iters, void* stream) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return measure_fp64_peak(sms, iters, (cudaStream_t)stream);
+}
+
+int as_last_stage_ms(double* out4) {
+    Plan* P = t_last_plan;
+    if (!P || !P->key.instrumented || !out4) return -1;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]); out4[0] = ms;
+    cudaEventElapsedTime(&ms, P->ev[1], P->ev[2]); out4[1] = ms;
+    cudaEventElapsedTime(&ms, P->ev[2], P->ev[3]); out4[2] = ms;
+    cudaEventElapsedTime(&ms, P->ev[0], P->ev[3]); out4[3] = ms;
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
 
 void as_release_all(void) {
     std::lock_guard<std::mutex> lk(g_mu);

@@ -45,7 +45,9 @@ struct DevState {
     double thr;                   // rcond threshold
     double lsq_cut;
     int32_t max_sweeps;
-    int32_t gate;                 // 1 if the fallback should run
+    int32_t gate;                 // 1 if the gate fired (singular or rcond below threshold)
+    int32_t post;                 // 0 nothing, 1 primary solve, 2 SVD fallback
+    int32_t pad1;
     // ---- rcond estimator (xLACN2 state machine)
     int32_t est_next;             // next apply slot to run (-1 = done)
     int32_t est_iter;

@@ -252,6 +252,45 @@ __global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
     }
 }
 
+// ------------------------------------------------------------------ fp64 tensor peak probe
+// Register-resident DMMA loop (16 independent accumulator chains per warp) used
+// by the benchmark to measure the fp64 tensor-core roofline denominator.
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+    double acc[16][2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * blockIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dmma884(acc[i][0], acc[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.678) out[0] = s;  // keep the work alive
+}
+
+double measure_fp64_peak(int num_sms, int iters, cudaStream_t s) {
+    double* d = nullptr;
+    cudaMalloc(&d, 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = num_sms * 4;
+    dmma_peak_kernel<<<blocks, 256, 0, s>>>(d, 16);  // warm-up
+    cudaEventRecord(e0, s);
+    dmma_peak_kernel<<<blocks, 256, 0, s>>>(d, iters);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    const double flops = 2.0 * 256.0 * 16.0 * (double)iters * (double)blocks * 8.0;  // 8 warps, 16 mma, 256 FMA
+    return flops / (ms * 1e-3) / 1e12;
+}
+
 // ------------------------------------------------------------------ launcher
 template <typename K>
 static void launch_k(K kern, const GemmArgs& g, size_t smem, cudaStream_t s) {

@@ -16,4 +16,7 @@ struct GemmArgs {
 
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s);
 
+// fp64 tensor-core (DMMA) throughput in TFLOP/s from a register-resident loop
+double measure_fp64_peak(int num_sms, int iters, cudaStream_t s);
+
 }  // namespace as
