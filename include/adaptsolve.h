@@ -182,6 +182,10 @@ int as_last_stage_ms(double* out4);
  * host (several syncs; for kernel-by-kernel ncu launch lists only). */
 void as_set_exec_mode(int eager);
 
+/* Diagnostics: %globaltimer stamps (ns) recorded by the last call's kernels
+ * at phase boundaries (out: 16 values; 0 = not recorded). */
+int as_debug_timestamps(unsigned long long* out16);
+
 /* Roofline denominator probe (benchmark only, not part of a solve): fp64
  * tensor-core (DMMA) throughput in TFLOP/s of a register-resident MMA loop. */
 double as_measure_fp64_peak(int iters, void* stream);

@@ -37,7 +37,7 @@ ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
            "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
            "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
-           "as_set_exec_mode")
+           "as_set_exec_mode", "as_debug_timestamps")
 
 
 class Options(C.Structure):
@@ -215,6 +215,18 @@ def measure_fp64_peak(iters: int = 20000, stream=None) -> float:
 
 
 _lib.as_set_exec_mode.argtypes = [C.c_int]
+_lib.as_debug_timestamps.argtypes = [P]
+_lib.as_debug_timestamps.restype = C.c_int
+
+
+def debug_timestamps():
+    """Phase stamps (ns, %globaltimer) of the last call, relative to the first stamp."""
+    out = (C.c_ulonglong * 16)()
+    if _lib.as_debug_timestamps(out) != 0:
+        return None
+    v = list(out)
+    t0 = v[0]
+    return [(x - t0) / 1e3 if x else None for x in v]   # microseconds
 
 
 def set_exec_mode(eager: bool) -> None:

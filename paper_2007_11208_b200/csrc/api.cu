@@ -183,10 +183,12 @@ static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
 
 // ------------------------------------------------------------------ branch bodies (shared by graph and eager modes)
 constexpr int kCholOk = 100;
+constexpr int kBandSpike = 101;
 
 static void body_factor(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     switch (m) {
-    case AS_METHOD_BAND: launch_band_factor(w, s); launch_estimator(w, KIND_BAND, false, sa, s); break;
+    case AS_METHOD_BAND: launch_band_factor(w, s); launch_estimator(w, KIND_BAND, false, sa, s); break;  // sequential
+    case kBandSpike: launch_band_spike(w, s); break;
     case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); launch_estimator(w, KIND_TRI, false, sa, s); break;
     case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); launch_estimator(w, KIND_TRI, true, sa, s); break;
     case AS_METHOD_LU: launch_lu_factor(w, s); launch_estimator(w, KIND_LU, false, sa, s); break;
@@ -269,7 +271,9 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.st = (DevState*)take(sizeof(DevState));
     w.args = (DevArgs*)take(sizeof(DevArgs));
     take(sizeof(RepOut));  // report slot follows args (see rep_ws)
-    w.W = take(es * (size_t)w.ldw * (size_t)std::max<int64_t>(band_rows, 1));
+    const size_t w_elems = std::max<size_t>((size_t)w.ldw * (size_t)std::max<int64_t>(band_rows, 1),
+                                            (size_t)spike_scratch_elems(n, w.num_sms > 0 ? w.num_sms : 148));
+    w.W = take(es * w_elems);
     w.diag = take(es * n);
     w.xe = take(es * n);
     w.Dinv0 = take(es * nblk * kNB * kNB);
@@ -322,8 +326,16 @@ static int build_graph(Plan& P) {
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[1], s0, cudaEventRecordExternal);
         mb = add_cond(s0, h_method, cudaGraphCondTypeSwitch, 6);
         // ---- factor + estimate bodies
-        for (int m : {AS_METHOD_BAND, AS_METHOD_TRI_LOWER, AS_METHOD_TRI_UPPER, AS_METHOD_LU})
+        for (int m : {AS_METHOD_TRI_LOWER, AS_METHOD_TRI_UPPER, AS_METHOD_LU})
             B.body(mb[m], [&](cudaStream_t s) { body_factor(w, m, B.sa, s); });
+        B.body(mb[AS_METHOD_BAND], [&](cudaStream_t s) {
+            launch_band_norm(w, s);
+            cudaGraphConditionalHandle h_bm = make_handle(s, 0);
+            launch_band_dominance(w, h_bm, s);
+            cudaGraph_t* bb = add_cond(s, h_bm, cudaGraphCondTypeIf, 2);
+            B.body(bb[0], [&](cudaStream_t s2) { body_factor(w, kBandSpike, B.sa, s2); });
+            B.body(bb[1], [&](cudaStream_t s2) { body_factor(w, AS_METHOD_BAND, B.sa, s2); });
+        });
         B.body(mb[AS_METHOD_CHOL], [&](cudaStream_t s) {
             launch_chol_factor(w, s);
             cudaGraphConditionalHandle h_cf = make_handle(s, 0);
@@ -434,6 +446,11 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
         launch_chol_check(w, 0, s);
         if ((err = rd())) return err;
         body_factor(w, h.chol_failed ? AS_METHOD_LU : kCholOk, sa, s);
+    } else if (h.method == AS_METHOD_BAND) {
+        launch_band_norm(w, s);
+        launch_band_dominance(w, 0, s);
+        if ((err = rd())) return err;
+        body_factor(w, h.band_use_spike ? kBandSpike : AS_METHOD_BAND, sa, s);
     } else {
         body_factor(w, h.method, sa, s);
     }
@@ -726,6 +743,18 @@ int64_t as_last_kernel_nodes(void) { return t_last_nodes; }
 void as_set_instrumentation(int enable) { g_instrument = enable ? 1 : 0; }
 
 void as_set_exec_mode(int eager) { g_eager = eager ? 1 : 0; }
+
+int as_debug_timestamps(unsigned long long* out16) {
+    Plan* P = t_last_plan;
+    if (!P || !out16) return -1;
+    DevState h;
+    if (cudaMemcpy(&h, P->w.st, sizeof(DevState), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return -2;
+    }
+    memcpy(out16, h.dbg_t, sizeof(h.dbg_t));
+    return 0;
+}
 
 double as_measure_fp64_peak(int iters, void* stream) {
     int dev = 0, sms = 148;

@@ -168,16 +168,18 @@ __global__ void __launch_bounds__(32) gbtrs_kernel(const T* ab, int64_t n, const
                                                     const DevArgs* args, int64_t ldb, T* xvec, int trans, int slot) {
     if (slot >= 0 && ld_volatile_i32(&st->est_next) != slot) return;
     if (st->info != ~0ull) return;
+    if (st->band_fast) return;    // the partitioned solver already produced X
     T* b = xvec ? xvec : (T*)args->X + (int64_t)blockIdx.x * ldb;
     gb_solve_vec<T>(ab, n, st->kl, st->ku, ipiv, b, trans != 0);
 }
 
 // X = B (column by column; skipped when X aliases B)
 template <typename T>
-__global__ void copy_b_to_x_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs) {
+__global__ void copy_b_to_x_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs, const DevState* st) {
     const T* B = (const T*)args->B;
     T* X = (T*)args->X;
     if ((const void*)B == (const void*)X) return;
+    if (st && st->band_fast) return;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * nrhs; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e % n, c = e / n;
         X[i + c * ldb] = B[i + c * ldb];
@@ -185,15 +187,20 @@ __global__ void copy_b_to_x_kernel(const DevArgs* args, int64_t n, int64_t ldb, 
 }
 
 // ------------------------------------------------------------------ launchers
+void launch_band_norm(const Work& w, cudaStream_t s) {
+    const int blocks = w.num_sms * 4;
+    if (w.dtype == AS_F64) band_norm_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
+    else band_norm_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
+}
+
+// sequential (faithful xGBTF2) path: pack + factor
 void launch_band_factor(const Work& w, cudaStream_t s) {
     const int blocks = w.num_sms * 4;
     if (w.dtype == AS_F64) {
         band_pack_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st, (double*)w.W);
-        band_norm_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
         gbtrf_warp_kernel<double><<<1, 32, 0, s>>>((double*)w.W, w.n, w.st, w.ipiv);
     } else {
         band_pack_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st, (float*)w.W);
-        band_norm_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
         gbtrf_warp_kernel<float><<<1, 32, 0, s>>>((float*)w.W, w.n, w.st, w.ipiv);
     }
 }
@@ -207,8 +214,8 @@ void launch_band_apply(const Work& w, bool trans, int slot, cudaStream_t s) {
 
 void launch_copy_b_to_x(const Work& w, cudaStream_t s) {
     const int blocks = w.num_sms * 4;
-    if (w.dtype == AS_F64) copy_b_to_x_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs);
-    else copy_b_to_x_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs);
+    if (w.dtype == AS_F64) copy_b_to_x_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, w.st);
+    else copy_b_to_x_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, w.st);
 }
 
 void launch_band_solve(const Work& w, cudaStream_t s) {

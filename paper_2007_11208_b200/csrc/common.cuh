@@ -60,6 +60,12 @@ struct DevState {
     int32_t svd_conv;
     int32_t ret;                  // AS_OK / AS_ERR_*
     unsigned long long smax_bits; // fallback sigma_max (ordered bits)
+    // ---- banded path
+    unsigned band_dom;            // bit0: strictly row dominant, bit1: strictly column dominant
+    int32_t band_use_spike;       // partitioned solver selected
+    int32_t band_fast;            // partitioned solver already produced X
+    int32_t pad2;
+    unsigned long long dbg_t[16]; // %globaltimer phase stamps (diagnostics)
     // ---- barriers / counters (zeroed per solve)
     uint32_t bar[4];
 };
@@ -106,6 +112,11 @@ AS_DEV void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 AS_DEV int ld_volatile_i32(const int* p) { return *(volatile const int*)p; }
+AS_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Grid-wide barrier for a cooperative launch (all CTAs co-resident).
 // `ctr` is a monotonically increasing counter zeroed before the launch;

@@ -38,6 +38,7 @@ __global__ void state_init_kernel(DevState* st, int64_t n, uint32_t opts, int fo
     s.max_sweeps = max_sweeps;
     s.est_next = 0;
     s.rank = -1;
+    s.band_dom = 3u;
     *st = s;
 }
 
@@ -217,6 +218,336 @@ __global__ void __launch_bounds__(kDetThreads) detect_pairs_kernel(const DevArgs
     }
 }
 
+// ------------------------------------------------------------------ pass 2 (v2): pipelined tile pairs
+// Persistent CTAs (one per SM) stream tile pairs through a 2-stage cp.async
+// pipeline into padded shared memory; while pair k is checked, pair k+G is in
+// flight.  Elements are visited along skewed diagonals (lane l, step d:
+// row l, column (l+d) mod 64) so that both the tile read and the transposed
+// mirror read are shared-memory bank-conflict free with a 16-byte aligned
+// padded leading dimension (66 doubles / 68 floats).
+template <typename T> struct DetLD;
+template <> struct DetLD<double> { static constexpr int v = 66; };
+template <> struct DetLD<float> { static constexpr int v = 68; };
+
+AS_DEV void cp_async_bytes(void* smem, const void* gmem, int chunk, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if (chunk == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+    else if (chunk == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+
+AS_DEV void pair_of(unsigned p, long long nt, long long& I, long long& J) {
+    long long q = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5) + 1;
+    while (q * (q - 1) / 2 > (long long)p) --q;
+    while (q * (q + 1) / 2 <= (long long)p) ++q;
+    const long long D = nt - q;
+    J = (long long)p - q * (q - 1) / 2;
+    I = J + D;
+}
+
+// stage a 64x64 tile (rows rr.., cols cc..) into smem column-major with leading dimension LD
+template <typename T>
+AS_DEV void stage_tile(T* dst, const T* A, int64_t lda, int64_t n, long long rr, long long cc, int chunk_bytes) {
+    constexpr int LD = DetLD<T>::v;
+    const int per = chunk_bytes / (int)sizeof(T);          // elements per chunk
+    const int cpc = kTile / per;                            // chunks per column
+    for (int e = threadIdx.x; e < kTile * cpc; e += blockDim.x) {
+        const int c = e / cpc, r = (e % cpc) * per;
+        const long long gr = rr + r, gc = cc + c;
+        int bytes = 0;
+        if (gc < n && gr < n) bytes = (int)(min<long long>(per, n - gr) * sizeof(T));
+        const T* src = bytes ? A + gr + gc * lda : A;
+        cp_async_bytes(dst + c * LD + r, src, chunk_bytes, bytes);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kDetThreads, 1) detect_pairs_v2(const DevArgs* args, int64_t lda, int64_t n,
+                                                                   DevState* st, const T* diag, int fullscan) {
+    constexpr int LD = DetLD<T>::v;
+    constexpr int TILE = kTile * LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* buf = (T*)smem_raw;                 // [stage][lower, upper][TILE]
+    __shared__ unsigned s_alive[2];
+    __shared__ int s_kl, s_ku;
+    __shared__ unsigned s_kill;
+    const T* A = (const T*)args->A;
+    // 16-byte chunks when every column start is 16-byte aligned, else element-wise
+    const int chunk_bytes = (((uintptr_t)A & 15) == 0 && ((lda * (int64_t)sizeof(T)) & 15) == 0) ? 16 : (int)sizeof(T);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long nt = (n + kTile - 1) / kTile;
+    const unsigned total = (unsigned)(nt * (nt + 1) / 2);
+    const T tol = T(100) * Eps<T>::v;                       // Fig. 4 line 5
+    const T max_diag = (T)dfrom(st->max_diag);
+    const unsigned G = gridDim.x;
+    int my_kl = 0, my_ku = 0;
+
+    auto issue = [&](int stage, unsigned p, unsigned alive) {
+        long long I, J;
+        pair_of(p, nt, I, J);
+        const bool diag_tile = (I == J);
+        const bool need_lower = diag_tile || (alive & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
+        const bool need_upper = !diag_tile && (alive & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
+        T* lo = buf + (stage * 2 + 0) * TILE;
+        T* up = buf + (stage * 2 + 1) * TILE;
+        if (need_lower) stage_tile<T>(lo, A, lda, n, I * kTile, J * kTile, chunk_bytes);
+        if (need_upper) stage_tile<T>(up, A, lda, n, J * kTile, I * kTile, chunk_bytes);
+    };
+
+    unsigned p = blockIdx.x;
+    if (threadIdx.x == 0) s_alive[0] = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+    __syncthreads();
+    if (p >= total || s_alive[0] == 0) return;
+    issue(0, p, s_alive[0]);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    int cur = 0;
+    for (;;) {
+        // decide and issue the next pair
+        if (threadIdx.x == 0) {
+            s_alive[cur ^ 1] = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+            s_kl = 0; s_ku = 0; s_kill = 0;
+        }
+        __syncthreads();
+        const unsigned pn = p + G;
+        const bool next_ok = pn < total && s_alive[cur ^ 1] != 0;
+        if (next_ok) issue(cur ^ 1, pn, s_alive[cur ^ 1]);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        // ---- check pair p on stage cur
+        {
+            const unsigned alive = s_alive[cur];
+            long long I, J;
+            pair_of(p, nt, I, J);
+            const bool diag_tile = (I == J);
+            const bool have_lower = diag_tile || (alive & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
+            const bool have_upper = !diag_tile && (alive & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
+            const bool chk_spd = (alive & AS_FLAG_SPD_CANDIDATE) != 0;
+            const T* lo = buf + (cur * 2 + 0) * TILE;
+            const T* up = diag_tile ? lo : buf + (cur * 2 + 1) * TILE;
+            const long long r0 = I * kTile, c0 = J * kTile;
+            const int r = 32 * (warp & 1) + lane;
+            const int dbase = 16 * (warp >> 1);
+            int kl_loc = 0, ku_loc = 0;
+            bool lower_nz = false, upper_nz = false, spd_dead = false;
+            const long long gi = r0 + r;
+            const T di = (chk_spd && gi < n) ? diag[gi] : T(0);
+#pragma unroll 4
+            for (int dd = 0; dd < 16; ++dd) {
+                const int c = (r + dbase + dd) & (kTile - 1);
+                const long long gj = c0 + c;
+                if (gi >= n || gj >= n) continue;
+                const T a = have_lower ? lo[c * LD + r] : T(0);          // A(gi, gj)
+                if (gi > gj) {
+                    const T b = have_upper || diag_tile ? up[r * LD + c] : T(0);   // A(gj, gi)
+                    const int dist = (int)(gi - gj);
+                    if (a != T(0)) { lower_nz = true; kl_loc = max(kl_loc, dist); }
+                    if (b != T(0)) { upper_nz = true; ku_loc = max(ku_loc, dist); }
+                    if (chk_spd) {
+                        const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
+                        const T df = a - b;
+                        const T delta = df < T(0) ? -df : df;                        // line 12
+                        const T m = aa > ab ? aa : ab;
+                        if (delta > tol && delta > tol * m) spd_dead = true;         // lines 13-14
+                        if (aa >= max_diag) spd_dead = true;                          // line 15
+                        if (aa + ab >= di + diag[gj]) spd_dead = true;               // line 16
+                    }
+                } else if (gi < gj && diag_tile) {
+                    if (a != T(0)) { upper_nz = true; ku_loc = max(ku_loc, (int)(gj - gi)); }
+                }
+            }
+            kl_loc = __reduce_max_sync(0xffffffffu, kl_loc);
+            ku_loc = __reduce_max_sync(0xffffffffu, ku_loc);
+            const unsigned kill = (__any_sync(0xffffffffu, lower_nz) ? AS_FLAG_UPPER : 0u) |
+                                  (__any_sync(0xffffffffu, upper_nz) ? AS_FLAG_LOWER : 0u) |
+                                  (__any_sync(0xffffffffu, spd_dead) ? AS_FLAG_SPD_CANDIDATE : 0u);
+            if (lane == 0) {
+                if (kl_loc) atomicMax(&s_kl, kl_loc);
+                if (ku_loc) atomicMax(&s_ku, ku_loc);
+                if (kill) atomicOr(&s_kill, kill);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int gkl = my_kl, gku = my_ku;
+                if (s_kl > my_kl) gkl = max(s_kl, atomicMax(&st->kl, s_kl));
+                if (s_ku > my_ku) gku = max(s_ku, atomicMax(&st->ku, s_ku));
+                my_kl = gkl; my_ku = gku;
+                unsigned k2 = s_kill;
+                if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
+                if (k2 & alive) atomicAnd(&st->alive, ~k2);
+            }
+        }
+        __syncthreads();   // stage cur is free again
+        if (!next_ok) break;
+        p = pn;
+        cur ^= 1;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ pass 2 (v3): register-direct tile pairs
+// Both tiles of pair (I,J) are loaded straight into registers with fully
+// coalesced vector loads (warp = one 64-element column per instruction; lane
+// l holds rows 2l, 2l+1 of columns w + 8i).  The band/triangular verdicts need
+// no transposition: distances of non-zeros are computed in each tile's own
+// layout.  Only when the sympd candidate is alive AND the pair has a non-zero
+// are the tiles written to shared memory for the mirrored Fig. 4 checks
+// (an all-zero pair passes lines 12-16 trivially because every diagonal entry
+// is > 0 once pass 1 kept the candidate alive).  Static round-robin pair
+// assignment, far-from-diagonal pairs first (early exit after the first wave
+// on dense asymmetric input).
+constexpr int kLD3 = kTile + 1;
+
+template <typename T>
+struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+template <typename T>
+AS_DEV void load_tile_regs(T (&v)[16], const T* A, int64_t lda, int64_t n, long long r0, long long c0, bool vec,
+                           bool interior) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = 2 * lane;
+    if (interior && vec) {
+        const T* p = A + (r0 + r) + (c0 + warp) * lda;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const typename Vec2<T>::type x = __ldcs((const typename Vec2<T>::type*)(p + (int64_t)(8 * i) * lda));
+            v[2 * i] = x.x;
+            v[2 * i + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long long gc = c0 + warp + 8 * i;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long gr = r0 + r + h;
+                v[2 * i + h] = (gr < n && gc < n) ? A[gr + gc * lda] : T(0);
+            }
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs* args, int64_t lda, int64_t n,
+                                                                DevState* st, const T* diag, int fullscan) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* lo_s = (T*)smem_raw;            // kTile x kLD3 (only used for the sympd pass)
+    T* up_s = lo_s + kTile * kLD3;
+    __shared__ unsigned s_alive;
+    __shared__ int s_kl, s_ku;
+    __shared__ unsigned s_kill;
+    __shared__ int s_nz;
+    const T* A = (const T*)args->A;
+    const bool vec = (((uintptr_t)A & (2 * sizeof(T) - 1)) == 0) && ((lda & 1) == 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long nt = (n + kTile - 1) / kTile;
+    const unsigned total = (unsigned)(nt * (nt + 1) / 2);
+    const T tol = T(100) * Eps<T>::v;
+    const T max_diag = (T)dfrom(st->max_diag);
+    int my_kl = 0, my_ku = 0;
+    const int r_loc = 2 * lane;
+
+    for (unsigned p = blockIdx.x; p < total; p += gridDim.x) {
+        long long I, J;
+        pair_of(p, nt, I, J);
+        const long long D = I - J;
+        const long long r0 = I * kTile, c0 = J * kTile;          // lower tile origin
+        const bool interior = (r0 + kTile <= n) && (c0 + kTile <= n);
+        // candidates only ever die, so a (per-warp) early look at `alive` may skip a tile nobody needs:
+        // only UPPER alive -> the mirror (upper) tile is irrelevant; only LOWER alive -> the lower tile is.
+        const unsigned peek = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+        const bool need_lo = (D == 0) || (peek & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
+        const bool need_up = (D != 0) && (peek & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
+        T lo[16], up[16];
+        if (need_lo) load_tile_regs<T>(lo, A, lda, n, r0, c0, vec, interior);
+        else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) lo[i] = T(0);
+        }
+        if (need_up) load_tile_regs<T>(up, A, lda, n, c0, r0, vec, interior);   // mirror tile (rows J, cols I)
+        else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) up[i] = T(0);
+        }
+        if (threadIdx.x == 0) {
+            s_alive = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+            s_kl = 0; s_ku = 0; s_kill = 0; s_nz = 0;
+        }
+        __syncthreads();
+        const unsigned alive = s_alive;
+        if (alive == 0) break;
+        int kl_loc = 0, ku_loc = 0;
+        bool lower_nz = false, upper_nz = false;
+        // ---- band / triangular verdicts in each tile's own layout
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+            const int d = (int)(D * kTile) + r - c;             // lower tile: row - col;  mirror tile: col - row
+            if (lo[i] != T(0)) {
+                if (d > 0) { lower_nz = true; kl_loc = max(kl_loc, d); }
+                else if (d < 0) { upper_nz = true; ku_loc = max(ku_loc, -d); }   // (diagonal tile only)
+            }
+            // mirror tile element at tile (r, c) is A(J*64 + r, I*64 + c): distance col - row = D*64 + c - r > 0
+            if (D != 0 && up[i] != T(0)) { upper_nz = true; ku_loc = max(ku_loc, (int)(D * kTile) + c - r); }
+        }
+        bool spd_dead = false;
+        if (alive & AS_FLAG_SPD_CANDIDATE) {
+            bool any = false;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) any |= (lo[i] != T(0)) || (D != 0 && up[i] != T(0));
+            if (__any_sync(0xffffffffu, any) && lane == 0) s_nz = 1;
+            __syncthreads();
+            if (s_nz) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                    lo_s[c * kLD3 + r] = lo[i];
+                    up_s[c * kLD3 + r] = (D != 0) ? up[i] : lo[i];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                    const long long gi = r0 + r, gj = c0 + c;
+                    if (gi >= n || gj >= n || gi <= gj) continue;
+                    const T a = lo[i];                           // A(gi, gj)
+                    const T b = up_s[r * kLD3 + c];              // A(gj, gi)
+                    const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
+                    const T df = a - b;
+                    const T delta = df < T(0) ? -df : df;                            // line 12
+                    const T m = aa > ab ? aa : ab;
+                    if (delta > tol && delta > tol * m) spd_dead = true;             // lines 13-14
+                    if (aa >= max_diag) spd_dead = true;                              // line 15
+                    if (aa + ab >= diag[gi] + diag[gj]) spd_dead = true;             // line 16
+                }
+            }
+        }
+        kl_loc = __reduce_max_sync(0xffffffffu, kl_loc);
+        ku_loc = __reduce_max_sync(0xffffffffu, ku_loc);
+        const unsigned kill = (__any_sync(0xffffffffu, lower_nz) ? AS_FLAG_UPPER : 0u) |
+                              (__any_sync(0xffffffffu, upper_nz) ? AS_FLAG_LOWER : 0u) |
+                              (__any_sync(0xffffffffu, spd_dead) ? AS_FLAG_SPD_CANDIDATE : 0u);
+        if (lane == 0) {
+            if (kl_loc) atomicMax(&s_kl, kl_loc);
+            if (ku_loc) atomicMax(&s_ku, ku_loc);
+            if (kill) atomicOr(&s_kill, kill);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int gkl = my_kl, gku = my_ku;
+            if (s_kl > my_kl) gkl = max(s_kl, atomicMax(&st->kl, s_kl));
+            if (s_ku > my_ku) gku = max(s_ku, atomicMax(&st->ku, s_ku));
+            my_kl = gkl; my_ku = gku;
+            unsigned k2 = s_kill;
+            if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
+            if (k2 & alive) atomicAnd(&st->alive, ~k2);
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ dispatch
 // First match in the paper's order: banded, lower, upper, sympd,
 // else general LU; or the forced method.  Sets the SWITCH handle.
@@ -248,15 +579,20 @@ void launch_detect(const Work& w, cudaStream_t s, bool fullscan) {
     const int dblocks = (int)std::min<int64_t>((w.n + dthreads - 1) / dthreads, 4 * w.num_sms);
     const long long nt = (w.n + kTile - 1) / kTile;
     const long long pairs = nt * (nt + 1) / 2;
-    const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 6);
     if (w.dtype == AS_F64) {
+        const int smem = (int)(sizeof(double) * 2 * kTile * kLD3);
+        const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 2);
+        cudaFuncSetAttribute(detect_pairs_v3<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<double><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (double*)w.diag);
-        detect_pairs_kernel<double><<<std::max(pblocks, 1), kDetThreads, 0, s>>>(w.args, w.lda, w.n, w.st,
-                                                                                 (const double*)w.diag, fullscan);
+        detect_pairs_v3<double><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
+                                                                              (const double*)w.diag, fullscan);
     } else {
+        const int smem = (int)(sizeof(float) * 2 * kTile * kLD3);
+        const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 4);
+        cudaFuncSetAttribute(detect_pairs_v3<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<float><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (float*)w.diag);
-        detect_pairs_kernel<float><<<std::max(pblocks, 1), kDetThreads, 0, s>>>(w.args, w.lda, w.n, w.st,
-                                                                               (const float*)w.diag, fullscan);
+        detect_pairs_v3<float><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
+                                                                             (const float*)w.diag, fullscan);
     }
 }
 

@@ -137,6 +137,18 @@ def test_banded(n, kl, ku):
     assert rep["primary_method"] == oracle.M_BAND
 
 
+@pytest.mark.parametrize("n,kl,ku,nrhs", [(256, 1, 1, 1), (777, 8, 8, 4), (1000, 16, 1, 3), (1500, 2, 7, 2),
+                                          (3001, 4, 4, 33), (8192, 8, 8, 4)])
+def test_banded_partitioned(n, kl, ku, nrhs):
+    """Strictly diagonally dominant bands take the partitioned (SPIKE) path: C2 recipe."""
+    A, B = W.make("C2", n=n, kl=kl, ku=ku, nrhs=nrhs)
+    rep, orep = check_parity(A, B)
+    assert rep["primary_method"] == oracle.M_BAND and (rep["kl"], rep["ku"]) == (kl, ku)
+    A32, B32 = A.astype(np.float32, order="F"), B.astype(np.float32, order="F")
+    if n <= 3001:
+        check_parity(A32, B32, fp32=True)
+
+
 @pytest.mark.parametrize("n", [5, 64, 129, 300])
 @pytest.mark.parametrize("upper", [False, True])
 def test_triangular(n, upper):
