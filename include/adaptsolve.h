@@ -189,6 +189,9 @@ int as_debug_timestamps(unsigned long long* out16);
 /* Roofline denominator probe (benchmark only, not part of a solve): fp64
  * tensor-core (DMMA) throughput in TFLOP/s of a register-resident MMA loop. */
 double as_measure_fp64_peak(int iters, void* stream);
+/* Benchmark only: TFLOP/s of the library's C -= A op(B) kernel (dtype AS_F64 / AS_F32)
+ * on internal zero-filled buffers, M x N x K, op(B) = B^T if trans_b. */
+double as_bench_gemm(int dtype, int64_t M, int64_t N, int64_t K, int trans_b, int iters);
 
 /* Workspace bytes a plan for this shape allocates (device). */
 int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs);

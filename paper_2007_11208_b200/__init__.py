@@ -37,7 +37,7 @@ ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
            "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
            "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
-           "as_set_exec_mode", "as_debug_timestamps")
+           "as_set_exec_mode", "as_debug_timestamps", "as_bench_gemm")
 
 
 class Options(C.Structure):
@@ -215,6 +215,13 @@ def measure_fp64_peak(iters: int = 20000, stream=None) -> float:
 
 
 _lib.as_set_exec_mode.argtypes = [C.c_int]
+_lib.as_bench_gemm.argtypes = [C.c_int, I64, I64, I64, C.c_int, C.c_int]
+_lib.as_bench_gemm.restype = C.c_double
+
+
+def bench_gemm(M, N, K, dtype_code=AS_F64, trans_b=False, iters=5) -> float:
+    """TFLOP/s of the library's trailing-update GEMM kernel."""
+    return float(_lib.as_bench_gemm(dtype_code, M, N, K, int(trans_b), iters))
 _lib.as_debug_timestamps.argtypes = [P]
 _lib.as_debug_timestamps.restype = C.c_int
 

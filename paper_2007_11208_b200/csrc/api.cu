@@ -744,6 +744,38 @@ void as_set_instrumentation(int enable) { g_instrument = enable ? 1 : 0; }
 
 void as_set_exec_mode(int eager) { g_eager = eager ? 1 : 0; }
 
+double as_bench_gemm(int dtype, int64_t M, int64_t N, int64_t K, int trans_b, int iters) {
+    const size_t es = dtype == AS_F64 ? 8 : 4;
+    const int64_t ld = (std::max(M, std::max(N, K)) + 3) / 4 * 4;
+    void *A = nullptr, *B = nullptr, *Cm = nullptr;
+    if (cudaMalloc(&A, es * ld * K) || cudaMalloc(&B, es * ld * std::max(N, K)) || cudaMalloc(&Cm, es * ld * N)) {
+        cudaGetLastError();
+        return -1.0;
+    }
+    cudaMemset(A, 0, es * ld * K);
+    cudaMemset(B, 0, es * ld * std::max(N, K));
+    cudaMemset(Cm, 0, es * ld * N);
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.lda = ld; g.TA = false;
+    g.B = B; g.ldb = ld; g.TB = trans_b != 0;
+    g.C = Cm; g.ldc = ld;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    launch_gemm_minus(dtype, g, 0);
+    cudaEventRecord(e0, 0);
+    for (int i = 0; i < iters; ++i) launch_gemm_minus(dtype, g, 0);
+    cudaEventRecord(e1, 0);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(A); cudaFree(B); cudaFree(Cm);
+    return 2.0 * (double)M * N * K * iters / (ms * 1e-3) / 1e12;
+}
+
 int as_debug_timestamps(unsigned long long* out16) {
     Plan* P = t_last_plan;
     if (!P || !out16) return -1;

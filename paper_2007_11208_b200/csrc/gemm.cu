@@ -187,11 +187,16 @@ __global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
     const float* B = (const float*)g.B;
     float* C = (float*)g.C;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    float acc[8][8];
+    float acc[8][8];   // starts as C; accumulates C - A B
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < 8; ++j) {
+            const int64_t c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+            acc[i][j] = (r < g.M && c < g.N) ? __ldcg(C + r + c * g.ldc) : 0.f;
+        }
+    }
     const int nk = (int)((g.K + SBK - 1) / SBK);
     float ra[4], rb[4];
     auto gload = [&](int kt) {
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(-a[i], b[j], acc[i][j]);
         }
         if (kt + 1 < nk) sstore(buf ^ 1);
         __syncthreads();
@@ -244,9 +249,141 @@ __global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int64_t c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
-            if (c < g.N) {
-                float* p = C + r + c * g.ldc;
-                *p = *p - acc[i][j];
+            if (c < g.N) C[r + c * g.ldc] = acc[i][j];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ fp64 DMMA kernel v2
+// CTA tile 128 x 64 x 16, 4 warps (2 x 2, warp tile 64 x 32 = 8 x 4 DMMA tiles),
+// 3-stage cp.async pipeline, 2 CTAs per SM so one CTA's C read-modify-write
+// epilogue overlaps the other's MMA main loop.
+namespace d2 {
+constexpr int BM = 128, BN = 64, BK = 16, ST = 3, NT = 128;
+constexpr int LDA_KM = BM + 4;   // A as [k][m]
+constexpr int LDA_MK = BK + 4;   // A as [m][k]
+constexpr int LDB_NK = BK + 4;   // B as [n][k]
+constexpr int LDB_KN = BN + 4;   // B as [k][n]
+constexpr int AEL = (BK * LDA_KM > BM * LDA_MK) ? BK * LDA_KM : BM * LDA_MK;
+constexpr int BEL = (BN * LDB_NK > BK * LDB_KN) ? BN * LDB_NK : BK * LDB_KN;
+}  // namespace d2
+
+template <bool TA, bool TB>
+AS_DEV void stage_d2(double* As, double* Bs, const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M,
+                     int64_t N, int64_t K, int64_t m0, int64_t n0, int64_t k0) {
+    using namespace d2;
+    if (!TA) {      // BK columns x BM contiguous m: chunk = 2 doubles
+        for (int e = threadIdx.x; e < BK * (BM / 2); e += NT) {
+            const int kk = e / (BM / 2), mm = (e % (BM / 2)) * 2;
+            const int64_t gk = k0 + kk, gm = m0 + mm;
+            int bytes = 0;
+            if (gk < K && gm < M) bytes = (int)(min<int64_t>(2, M - gm) * 8);
+            cp_async16(As + kk * LDA_KM + mm, bytes ? A + gm + gk * lda : A, bytes);
+        }
+    } else {
+        for (int e = threadIdx.x; e < BM * (BK / 2); e += NT) {
+            const int mm = e / (BK / 2), kk = (e % (BK / 2)) * 2;
+            const int64_t gk = k0 + kk, gm = m0 + mm;
+            int bytes = 0;
+            if (gm < M && gk < K) bytes = (int)(min<int64_t>(2, K - gk) * 8);
+            cp_async16(As + mm * LDA_MK + kk, bytes ? A + gk + gm * lda : A, bytes);
+        }
+    }
+    if (!TB) {      // BN columns x BK contiguous k
+        for (int e = threadIdx.x; e < BN * (BK / 2); e += NT) {
+            const int nn = e / (BK / 2), kk = (e % (BK / 2)) * 2;
+            const int64_t gk = k0 + kk, gn = n0 + nn;
+            int bytes = 0;
+            if (gn < N && gk < K) bytes = (int)(min<int64_t>(2, K - gk) * 8);
+            cp_async16(Bs + nn * LDB_NK + kk, bytes ? B + gk + gn * ldb : B, bytes);
+        }
+    } else {
+        for (int e = threadIdx.x; e < BK * (BN / 2); e += NT) {
+            const int kk = e / (BN / 2), nn = (e % (BN / 2)) * 2;
+            const int64_t gk = k0 + kk, gn = n0 + nn;
+            int bytes = 0;
+            if (gk < K && gn < N) bytes = (int)(min<int64_t>(2, N - gn) * 8);
+            cp_async16(Bs + kk * LDB_KN + nn, bytes ? B + gn + gk * ldb : B, bytes);
+        }
+    }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
+    using namespace d2;
+    if (g.skip && *g.skip) return;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    if (g.lower_only && n0 > m0 + BM - 1) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* As = (double*)smem_raw;
+    double* Bs = As + ST * AEL;
+    const double* A = (const double*)g.A;
+    const double* B = (const double*)g.B;
+    double* C = (double*)g.C;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int nk = (int)((g.K + BK - 1) / BK);
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nk) stage_d2<TA, TB>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)s * BK);
+        cp_async_commit();
+    }
+    // acc starts as C (all loads in flight together, overlapping the prologue);
+    // the MMAs then accumulate acc += A (-B), so the epilogue is a plain store.
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + wm + 8 * i + gid;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
+                acc[i][j][h] = (r < g.M && c < g.N) ? __ldcg(C + r + c * g.ldc) : 0.0;
+            }
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        const int nxt = kt + ST - 1;
+        if (nxt < nk) {
+            const int s = nxt % ST;
+            stage_d2<TA, TB>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)nxt * BK);
+        }
+        cp_async_commit();
+        const double* as = As + (kt % ST) * AEL;
+        const double* bs = Bs + (kt % ST) * BEL;
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+            double af[8], bf[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int m = wm + 8 * i + gid, k = ks * 4 + tig;
+                af[i] = TA ? as[m * LDA_MK + k] : as[k * LDA_KM + m];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = wn + 8 * j + gid, k = ks * 4 + tig;
+                bf[j] = -(TB ? bs[k * LDB_KN + n] : bs[n * LDB_NK + k]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = m0 + wm + 8 * i + gid;
+        if (r >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
+                if (c < g.N) C[r + c * g.ldc] = acc[i][j][h];
             }
         }
     }
@@ -302,11 +439,16 @@ static void launch_k(K kern, const GemmArgs& g, size_t smem, cudaStream_t s) {
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
     if (dtype == AS_F64) {
-        const size_t smem = sizeof(double) * 2 * GSTAGES * kStageElems;
-        if (!g.TA && !g.TB) launch_k(gemm_dmma_kernel<false, false>, g, smem, s);
-        else if (!g.TA && g.TB) launch_k(gemm_dmma_kernel<false, true>, g, smem, s);
-        else if (g.TA && !g.TB) launch_k(gemm_dmma_kernel<true, false>, g, smem, s);
-        else launch_k(gemm_dmma_kernel<true, true>, g, smem, s);
+        const size_t smem = sizeof(double) * d2::ST * (d2::AEL + d2::BEL);
+        auto go = [&](auto kern) {
+            dim3 grid((unsigned)((g.M + d2::BM - 1) / d2::BM), (unsigned)((g.N + d2::BN - 1) / d2::BN));
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<grid, d2::NT, smem, s>>>(g);
+        };
+        if (!g.TA && !g.TB) go(gemm_dmma2_kernel<false, false>);
+        else if (!g.TA && g.TB) go(gemm_dmma2_kernel<false, true>);
+        else if (g.TA && !g.TB) go(gemm_dmma2_kernel<true, false>);
+        else go(gemm_dmma2_kernel<true, true>);
     } else {
         if (!g.TA && !g.TB) launch_k(gemm_sgemm_kernel<false, false>, g, 0, s);
         else if (!g.TA && g.TB) launch_k(gemm_sgemm_kernel<false, true>, g, 0, s);
