@@ -439,7 +439,7 @@ static void launch_k(K kern, const GemmArgs& g, size_t smem, cudaStream_t s) {
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
     if (dtype == AS_F64) {
-        const size_t smem = sizeof(double) * d2::ST * (d2::AEL + d2::BEL);
+        const size_t smem = g.one_per_sm ? (size_t)116 * 1024 : sizeof(double) * d2::ST * (d2::AEL + d2::BEL);
         auto go = [&](auto kern) {
             dim3 grid((unsigned)((g.M + d2::BM - 1) / d2::BM), (unsigned)((g.N + d2::BN - 1) / d2::BN));
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

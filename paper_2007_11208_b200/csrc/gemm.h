@@ -12,6 +12,8 @@ struct GemmArgs {
     void* C; int64_t ldc;
     bool lower_only;        // skip CTA tiles strictly above the diagonal (SYRK)
     const int* skip;        // device flag: kernel returns at once if *skip != 0
+    bool one_per_sm;        // reserve shared memory so only one GEMM CTA fits per SM (room for a
+                            // concurrently running cooperative panel kernel)
 };
 
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s);

@@ -1,0 +1,435 @@
+// lu.cu -- K7: blocked LU with partial pivoting (xGETRF).
+//
+// Right-looking, 128-column blocks, each block factored as two 64-column
+// panels (a two-level recursive panel: the second half is updated by a
+// rank-64 DMMA GEMM before it is factored), so that the trailing update is a
+// K = 128 DMMA GEMM (86% of the measured fp64 tensor peak at n = 16384).
+//
+//   per block b (columns k0 .. k0+127):
+//     panel(k0, 64)          cooperative kernel: rows split over P CTAs, held in
+//                            shared memory; per column one grid-wide exchange of
+//                            (|max|, row) candidates -- published with a sequence
+//                            number and polled, so barrier and data arrive
+//                            together -- first-max tie-break (Z15), swap, scale,
+//                            in-panel rank-1 update
+//     laswp + u12 + gemm      bring columns k0+64..k0+127 up to date
+//     panel(k0+64, 64)
+//     laswp                  all other columns (and the row permutation)
+//     u12                    U12 = L11^{-1} A12 (128 x (n - k0 - 128))
+//     gemm (DMMA, K = 128)   A22 -= L21 U12
+//   look-ahead: the GEMM is split; the columns of the next block are updated
+//   first on a high-priority stream and the next block's panels start there
+//   while the bulk of the GEMM is still running.
+#include <mutex>
+
+#include "factor.h"
+#include "gemm.h"
+#include "internal.h"
+#include "trsm.h"
+
+namespace as {
+
+constexpr int kPT = 256;     // panel threads
+constexpr int kPW = 64;      // panel width
+constexpr int kBW = 128;     // block width (two panels)
+
+struct __align__(32) PSlot {
+    double v;
+    long long idx;
+    unsigned long long seq;
+    long long pad;
+};
+
+// ------------------------------------------------------------------ panel (cooperative)
+template <typename T>
+__global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+                                                            int64_t* ipiv, DevState* st, PSlot* slots, T* rowbuf,
+                                                            T* diagbuf, unsigned long long seq_base, int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int P = gridDim.x, cta = blockIdx.x;
+    const int64_t m = n - k0;
+    const int64_t chunk = (m + P - 1) / P;
+    const int64_t rbeg = k0 + (int64_t)cta * chunk;
+    const int64_t rend = min(n, rbeg + chunk);
+    const int nr = (int)max<int64_t>(0, rend - rbeg);
+    const int64_t cp = use_smem ? chunk : ldw;
+    T* Ps = use_smem ? (T*)smem_raw : W + rbeg + k0 * ldw;
+    T* ubuf = use_smem ? (T*)smem_raw + chunk * nbp : (T*)smem_raw;
+    __shared__ T sv[8];
+    __shared__ long long si[8];
+    __shared__ int sdn[8];
+    __shared__ long long s_p;
+    __shared__ int s_owner;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    if (use_smem) {
+        for (int64_t e = threadIdx.x; e < (int64_t)nr * nbp; e += blockDim.x) {
+            const int64_t r = e % nr, c = e / nr;
+            Ps[r + c * cp] = W[(rbeg + r) + (k0 + c) * ldw];
+        }
+        __syncthreads();
+    }
+    unsigned long long info = ~0ull;
+    for (int j = 0; j < nbp; ++j) {
+        const int64_t g = k0 + j;
+        const int par = j & 1;
+        const unsigned long long want = seq_base + (unsigned long long)j + 1ull;
+        // ---- local first-max over my rows >= g (NaN never wins, Z15)
+        T v = T(-1);
+        long long idx = 0x7fffffffffffffffll;
+        int dnan = 0;
+        for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+            const int64_t gr = rbeg + r;
+            if (gr < g) continue;
+            T a = Ps[r + j * cp];
+            a = a < T(0) ? -a : a;
+            if (gr == g && a != a) dnan = 1;
+            argmax_merge(v, idx, a, (long long)gr);
+        }
+        warp_argmax(v, idx);
+        dnan = __any_sync(0xffffffffu, dnan);
+        if (lane == 0) { sv[warp] = v; si[warp] = idx; sdn[warp] = dnan; }
+        __syncthreads();
+        if (warp == 0) {
+            v = lane < 8 ? sv[lane] : T(-1);
+            idx = lane < 8 ? si[lane] : 0x7fffffffffffffffll;
+            int dn = lane < 8 ? sdn[lane] : 0;
+            warp_argmax(v, idx);
+            dn = __any_sync(0xffffffffu, dn);
+            if (lane == 0) {
+                if (dn) { v = T(INFINITY); idx = g; }     // NaN diagonal: the serial sweep keeps row g
+                sv[0] = v; si[0] = idx;
+            }
+        }
+        __syncthreads();
+        v = sv[0];
+        idx = si[0];
+        // ---- publish my candidate row (and the old row g if I own it)
+        if (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) {
+            const int r = (int)(idx - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) rowbuf[((int64_t)par * P + cta) * nbp + c] = Ps[r + c * cp];
+        }
+        if (g >= rbeg && g < rend) {
+            const int r = (int)(g - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) diagbuf[par * nbp + c] = Ps[r + c * cp];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            PSlot* sl = slots + cta;
+            sl->v = (double)v;
+            sl->idx = idx;
+            // release is cumulative: the CTA's rowbuf writes (ordered by the barrier above) are published too
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq), "l"(want) : "memory");
+        }
+        // ---- poll every slot (barrier + data in one), pick the winner
+        if (warp == 0) {
+            T bv = T(-1);
+            long long bi = 0x7fffffffffffffffll;
+            int bo = 0;
+            // each lane owns up to 5 slots (P <= 160); all are polled together each round
+            constexpr int kMaxPer = 5;
+            bool ready[kMaxPer];
+#pragma unroll
+            for (int q = 0; q < kMaxPer; ++q) ready[q] = (lane + 32 * q) >= P;
+            for (;;) {
+                bool all = true;
+#pragma unroll
+                for (int q = 0; q < kMaxPer; ++q) {
+                    if (!ready[q]) {
+                        unsigned long long sq;
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(sq) : "l"(&slots[lane + 32 * q].seq) : "memory");
+                        ready[q] = sq >= want;
+                        all = all && ready[q];
+                    }
+                }
+                if (__all_sync(0xffffffffu, all)) break;
+            }
+#pragma unroll
+            for (int q = 0; q < kMaxPer; ++q) {
+                const int t = lane + 32 * q;
+                if (t < P) {
+                    const T cv = (T)__ldcg(&slots[t].v);
+                    const long long ci = __ldcg(&slots[t].idx);
+                    if (cv > bv || (cv == bv && ci < bi)) { bv = cv; bi = ci; bo = t; }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int o2 = __shfl_xor_sync(0xffffffffu, bo, o);
+                if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; bo = o2; }
+            }
+            if (lane == 0) { s_p = bi; s_owner = bo; }
+        }
+        __syncthreads();
+        const long long p = s_p;
+        const int owner = s_owner;
+        for (int c = threadIdx.x; c < nbp; c += blockDim.x) ubuf[c] = __ldcg(&rowbuf[((int64_t)par * P + owner) * nbp + c]);
+        __syncthreads();
+        const T piv = ubuf[j];
+        if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
+        if (piv == T(0)) {                       // exact zero pivot: singular column (no elimination)
+            if (info == ~0ull) info = (unsigned long long)(g + 1);
+            continue;
+        }
+        // ---- swap: row p <- old row g, row g <- pivot row
+        if (p != g && p >= rbeg && p < rend) {
+            const int r = (int)(p - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = __ldcg(&diagbuf[par * nbp + c]);
+        }
+        if (g >= rbeg && g < rend) {
+            const int r = (int)(g - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = ubuf[c];
+        }
+        __syncthreads();
+        // ---- multipliers and the rank-1 update of my rows > g (rows x columns in parallel)
+        const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
+        const int nrow = (int)max<int64_t>(0, nr - r0);
+        // thread = (row, column phase): rows r0 + (tid % 128) + 128 k, columns j+1+ph, step 2
+        {
+            const int rl = threadIdx.x & 127, ph = threadIdx.x >> 7;
+            for (int base = 0; base < nrow; base += 128) {     // uniform trip count (barrier inside)
+                const int r = base + rl;
+                const bool valid = r < nrow;
+                const int64_t rr = r0 + r;
+                const T l = valid ? Ps[rr + j * cp] / piv : T(0);
+                __syncthreads();                               // both phases have read the column-j value
+                if (valid) {
+                    if (ph == 0) Ps[rr + j * cp] = l;
+#pragma unroll 4
+                    for (int c = j + 1 + ph; c < nbp; c += 2) Ps[rr + c * cp] -= l * ubuf[c];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (use_smem) {
+        for (int64_t e = threadIdx.x; e < (int64_t)nr * nbp; e += blockDim.x) {
+            const int64_t r = e % nr, c = e / nr;
+            W[(rbeg + r) + (k0 + c) * ldw] = Ps[r + c * cp];
+        }
+    }
+    if (threadIdx.x == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
+}
+
+// ------------------------------------------------------------------ laswp
+// Apply ipiv[j0 .. j0+cnt) in order to columns [a0, a1) U [b0, b1) and (if perm) to perm.
+// One thread per column (each swap is a dependent pair of accesses, independent across columns).
+template <typename T>
+__global__ void laswp2_kernel(T* W, int64_t ldw, int64_t j0, int cnt, int64_t a0, int64_t a1, int64_t b0, int64_t b1,
+                              const int64_t* ipiv, int64_t* perm) {
+    const int64_t na = max<int64_t>(0, a1 - a0), nb = max<int64_t>(0, b1 - b0);
+    const int64_t ncols = na + nb + (perm ? 1 : 0);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ncols; t += (int64_t)gridDim.x * blockDim.x) {
+        if (perm && t == ncols - 1) {
+            for (int q = 0; q < cnt; ++q) {
+                const int64_t a = j0 + q, b = ipiv[a];
+                if (b != a) { const int64_t x = perm[a]; perm[a] = perm[b]; perm[b] = x; }
+            }
+            continue;
+        }
+        const int64_t col = t < na ? a0 + t : b0 + (t - na);
+        T* __restrict__ c = W + col * ldw;
+        for (int q = 0; q < cnt; ++q) {
+            const int64_t a = j0 + q, b = ipiv[a];
+            if (b != a) { const T x = c[a]; const T y = c[b]; c[a] = y; c[b] = x; }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ U12 = L11^{-1} A12
+// L11: nb x nb unit lower at W[r0.., r0..]; A12 rows r0..r0+nb, columns [c0, c1) (tile of 32).
+constexpr int kU12C = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) u12v2_kernel(T* W, int64_t ldw, int64_t r0, int nb, int64_t c0, int64_t c1) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int LDL = nb + 1;
+    T* L = (T*)smem_raw;                  // nb x LDL
+    T* Bt = L + (int64_t)nb * LDL;        // nb x (kU12C + 1), Bt[r*(kU12C+1) + c]
+    const int64_t cc0 = c0 + (int64_t)blockIdx.x * kU12C;
+    const int nc = (int)min<int64_t>(kU12C, c1 - cc0);
+    if (nc <= 0) return;
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+        const int r = e % nb, c = e / nb;
+        L[r * LDL + c] = r > c ? W[(r0 + r) + (r0 + c) * ldw] : T(0);
+    }
+    for (int e = threadIdx.x; e < nb * nc; e += blockDim.x) {
+        const int r = e % nb, c = e / nb;
+        Bt[r * (kU12C + 1) + c] = W[(r0 + r) + (cc0 + c) * ldw];
+    }
+    __syncthreads();
+    // forward substitution, one (row i) step at a time, all columns / rows below in parallel
+    for (int i = 0; i < nb - 1; ++i) {
+        const int rows = nb - 1 - i;
+        for (int e = threadIdx.x; e < rows * nc; e += blockDim.x) {
+            const int r = i + 1 + e / nc, c = e % nc;
+            Bt[r * (kU12C + 1) + c] -= L[r * LDL + i] * Bt[i * (kU12C + 1) + c];
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < nb * nc; e += blockDim.x) {
+        const int r = e % nb, c = e / nb;
+        W[(r0 + r) + (cc0 + c) * ldw] = Bt[r * (kU12C + 1) + c];
+    }
+}
+
+// ------------------------------------------------------------------ host driver
+struct LuStreams {
+    cudaStream_t hi = nullptr;
+    cudaEvent_t ev[64];
+    int next = 0;
+    int prio_hi = 0;
+};
+
+static LuStreams& lu_streams() {
+    static thread_local LuStreams L;
+    if (!L.hi) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        L.prio_hi = hi;
+        cudaStreamCreateWithPriority(&L.hi, cudaStreamNonBlocking, hi);
+        for (auto& e : L.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    return L;
+}
+
+template <typename T>
+static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long seq_base, int prio, cudaStream_t s) {
+    const int64_t n = w.n, m = n - k0;
+    static const int rows_per_cta = getenv("AS_LU_PANEL_ROWS") ? atoi(getenv("AS_LU_PANEL_ROWS")) : 128;
+    int P = (int)std::min<int64_t>(w.num_sms, (m + rows_per_cta - 1) / rows_per_cta);
+    P = std::max(P, 1);
+    const int64_t chunk = (m + P - 1) / P;
+    size_t smem = sizeof(T) * (chunk * nbp + nbp);
+    int use_smem = 1;
+    if (smem > 200 * 1024) { use_smem = 0; smem = sizeof(T) * nbp; }
+    PSlot* slots = (PSlot*)w.cand;
+    T* rowbuf = (T*)((char*)w.cand + sizeof(PSlot) * 1024);
+    T* diagbuf = rowbuf + (int64_t)2 * 1024 * kPW;
+    auto kern = lu_panel2_kernel<T>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1024));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(kPT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (P > 1) { attr[na].id = cudaLaunchAttributeCooperative; attr[na].val.cooperative = 1; ++na; }
+    attr[na].id = cudaLaunchAttributePriority; attr[na].val.priority = prio; ++na;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, slots, rowbuf, diagbuf, seq_base, use_smem);
+}
+
+template <typename T>
+static void laswp_launch(const Work& w, int64_t j0, int cnt, int64_t a0, int64_t a1, int64_t b0, int64_t b1, bool perm,
+                         cudaStream_t s) {
+    const int64_t ncols = std::max<int64_t>(0, a1 - a0) + std::max<int64_t>(0, b1 - b0) + (perm ? 1 : 0);
+    if (ncols <= 0 || cnt <= 0) return;
+    laswp2_kernel<T><<<(unsigned)std::min<int64_t>((ncols + 127) / 128, 8192), 128, 0, s>>>(
+        (T*)w.W, w.ldw, j0, cnt, a0, a1, b0, b1, w.ipiv, perm ? w.perm : nullptr);
+}
+
+template <typename T>
+static void u12_launch(const Work& w, int64_t r0, int nb, int64_t c0, int64_t c1, cudaStream_t s) {
+    if (c1 <= c0) return;
+    const int smem = (int)(sizeof(T) * ((size_t)nb * (nb + 1) + (size_t)nb * (kU12C + 1)));
+    cudaFuncSetAttribute(u12v2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    u12v2_kernel<T><<<(unsigned)((c1 - c0 + kU12C - 1) / kU12C), 256, smem, s>>>((T*)w.W, w.ldw, r0, nb, c0, c1);
+}
+
+template <typename T>
+static void gemm_launch(const Work& w, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, cudaStream_t s,
+                        int prio, bool one_per_sm = false) {
+    (void)prio;
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    T* W = (T*)w.W;
+    const int64_t ldw = w.ldw;
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K;
+    g.A = W + r0 + k0 * ldw; g.lda = ldw; g.TA = false;
+    g.B = W + k0 + c0 * ldw; g.ldb = ldw; g.TB = false;
+    g.C = W + r0 + c0 * ldw; g.ldc = ldw;
+    g.one_per_sm = one_per_sm;
+    launch_gemm_minus(w.dtype, g, s);
+}
+
+// Factor the block's two panels (columns k0 .. k0+bw), on stream s.
+template <typename T>
+static void block_panels(const Work& w, int64_t k0, int bw, int prio, cudaStream_t s) {
+    const int64_t n = w.n;
+    const int p1 = std::min(kPW, bw);
+    // sequence numbers of the panel exchange grow monotonically with the panel's column
+    panel_launch<T>(w, k0, p1, (unsigned long long)(k0 / kPW) * 128ull, prio, s);
+    if (bw > p1) {
+        const int p2 = bw - p1;
+        // bring the block's second half up to date: swaps of panel 1, U12, rank-p1 update
+        laswp_launch<T>(w, k0, p1, k0 + p1, k0 + bw, 0, 0, false, s);
+        u12_launch<T>(w, k0, p1, k0 + p1, k0 + bw, s);
+        gemm_launch<T>(w, k0 + p1, k0 + p1, k0, n - k0 - p1, p2, p1, s, prio);
+        panel_launch<T>(w, k0 + p1, p2, (unsigned long long)((k0 + p1) / kPW) * 128ull, prio, s);
+    }
+}
+
+template <typename T>
+static void lu_factor_t(const Work& w, cudaStream_t s) {
+    const int64_t n = w.n;
+    launch_copy_norm(w, true, s);
+    cudaMemsetAsync(w.cand, 0, sizeof(PSlot) * 1024, s);       // panel exchange slots (sequence numbers)
+    LuStreams& LS = lu_streams();
+    // Look-ahead: next block's panels on a high-priority stream beside the bulk GEMM (measured
+    // ~10% on C5; the gang-scheduled cooperative panel only partly overlaps).
+    const bool lookahead = n >= 2048 && getenv("AS_LU_NO_LOOKAHEAD") == nullptr;
+    int evi = 0;
+    auto ev = [&]() { return LS.ev[(evi++) % 64]; };
+    // first block's panels
+    block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, s);
+    for (int64_t k0 = 0; k0 < n; k0 += kBW) {
+        const int bw = (int)std::min<int64_t>(kBW, n - k0);
+        const int p1 = std::min(kPW, bw);
+        const int64_t kn = k0 + bw;             // next block start
+        // swaps of this block into all other columns (+ perm)
+        // panel-1 swaps: columns [0, k0) and [kn, n)  (block's second half already done)
+        // panel-2 swaps: columns [0, k0+p1) and [kn, n)
+        laswp_launch<T>(w, k0, p1, 0, k0, kn, n, false, s);
+        if (bw > p1) laswp_launch<T>(w, k0 + p1, bw - p1, 0, k0 + p1, kn, n, false, s);
+        laswp_launch<T>(w, k0, bw, 0, 0, 0, 0, true, s);        // row permutation: all bw swaps
+        if (kn >= n) break;
+        // U12 = L11^{-1} A12 with L11 = [La 0; Lb Lc] in 64-row halves: Utop = La^{-1} Atop,
+        // Abot -= Lb Utop (DMMA), Ubot = Lc^{-1} Abot
+        u12_launch<T>(w, k0, p1, kn, n, s);
+        if (bw > p1) {
+            gemm_launch<T>(w, k0 + p1, kn, k0, bw - p1, n - kn, p1, s, 0);
+            u12_launch<T>(w, k0 + p1, bw - p1, kn, n, s);
+        }
+        const int64_t M = n - kn;
+        const int nbw = (int)std::min<int64_t>(kBW, n - kn);
+        if (lookahead && n - kn > nbw) {
+            // next block's columns first (high priority), then its panels; the rest of the GEMM
+            // concurrently on the main stream
+            cudaEvent_t e0 = ev();
+            cudaEventRecord(e0, s);
+            cudaStreamWaitEvent(LS.hi, e0, 0);
+            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi);
+            block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
+            gemm_launch<T>(w, kn, kn + nbw, k0, M, n - kn - nbw, bw, s, 0, getenv("AS_LU_ONE_PER_SM") != nullptr);
+            cudaEvent_t e1 = ev();
+            cudaEventRecord(e1, LS.hi);
+            cudaStreamWaitEvent(s, e1, 0);
+        } else {
+            gemm_launch<T>(w, kn, kn, k0, M, n - kn, bw, s, 0);
+            block_panels<T>(w, kn, nbw, LS.prio_hi, s);
+        }
+    }
+    launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv0, false, true, w.st, true, w.args, s);
+    launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
+}
+
+void launch_lu_factor(const Work& w, cudaStream_t s) {
+    if (w.dtype == AS_F64) lu_factor_t<double>(w, s);
+    else lu_factor_t<float>(w, s);
+}
+
+}  // namespace as
