@@ -112,10 +112,12 @@ __global__ void __launch_bounds__(256) potf2_kernel(T* W, int64_t ldw, int64_t n
         if (threadIdx.x == 0) a[j + j * LD] = ljj;
         for (int i = j + 1 + threadIdx.x; i < nbp; i += blockDim.x) a[i + j * LD] = a[i + j * LD] / ljj;
         __syncthreads();
-        const int rem = nbp - j - 1;
-        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-            const int i = j + 1 + e % rem, k = j + 1 + e / rem;
-            if (i >= k) a[i + k * LD] -= a[i + j * LD] * a[k + j * LD];
+        {   // thread = (row i, column phase); trailing lower triangle update
+            const int i = threadIdx.x & (kNB - 1), ph = threadIdx.x / kNB, nph = blockDim.x / kNB;
+            if (i > j && i < nbp) {
+                const T lij = a[i + j * LD];
+                for (int k = j + 1 + ph; k <= i; k += nph) a[i + k * LD] -= lij * a[k + j * LD];
+            }
         }
         __syncthreads();
     }
@@ -156,10 +158,12 @@ __global__ void __launch_bounds__(256) l21_kernel(T* W, int64_t ldw, int64_t n, 
     for (int c = 0; c < nbp; ++c) {
         for (int r = threadIdx.x; r < nr; r += blockDim.x) X[r + c * LD] = X[r + c * LD] / L[c + c * LD];
         __syncthreads();
-        const int rem = nbp - c - 1;
-        for (int e = threadIdx.x; e < nr * rem; e += blockDim.x) {
-            const int r = e % nr, cc = c + 1 + e / nr;
-            X[r + cc * LD] -= X[r + c * LD] * L[cc + c * LD];
+        {   // thread = (row r, column phase)
+            const int r = threadIdx.x & (kNB - 1), ph = threadIdx.x / kNB, nph = blockDim.x / kNB;
+            if (r < nr) {
+                const T xr = X[r + c * LD];
+                for (int cc = c + 1 + ph; cc < nbp; cc += nph) X[r + cc * LD] -= xr * L[cc + c * LD];
+            }
         }
         __syncthreads();
     }

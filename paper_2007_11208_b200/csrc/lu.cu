@@ -260,13 +260,15 @@ __global__ void __launch_bounds__(256) u12v2_kernel(T* W, int64_t ldw, int64_t r
     }
     __syncthreads();
     // forward substitution, one (row i) step at a time, all columns / rows below in parallel
-    for (int i = 0; i < nb - 1; ++i) {
-        const int rows = nb - 1 - i;
-        for (int e = threadIdx.x; e < rows * nc; e += blockDim.x) {
-            const int r = i + 1 + e / nc, c = e % nc;
-            Bt[r * (kU12C + 1) + c] -= L[r * LDL + i] * Bt[i * (kU12C + 1) + c];
+    {
+        const int c = threadIdx.x & (kU12C - 1), r0 = threadIdx.x / kU12C, nr = blockDim.x / kU12C;
+        for (int i = 0; i < nb - 1; ++i) {
+            if (c < nc) {
+                const T bi = Bt[i * (kU12C + 1) + c];
+                for (int r = i + 1 + r0; r < nb; r += nr) Bt[r * (kU12C + 1) + c] -= L[r * LDL + i] * bi;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     for (int e = threadIdx.x; e < nb * nc; e += blockDim.x) {
         const int r = e % nb, c = e / nb;

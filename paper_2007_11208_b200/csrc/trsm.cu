@@ -94,29 +94,40 @@ struct TsArgs {
 };
 
 // acc[i][c] (partial over k-quarter q) for row i = tid % 64, q = tid / 64
-template <typename T, bool TRANSB>
-AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T (&part)[kTsR], int R) {
+template <typename T, bool TRANSB, int RT>
+AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T (&part)[RT], int R) {
     const int i = threadIdx.x % kNB, q = threadIdx.x / kNB;
 #pragma unroll
-    for (int c = 0; c < kTsR; ++c) part[c] = T(0);
+    for (int c = 0; c < RT; ++c) part[c] = T(0);
 #pragma unroll 4
     for (int kk = 0; kk < kNB / 4; ++kk) {
         const int k = q * (kNB / 4) + kk;
         const T m = TRANSB ? Ms[k + i * kLDT] : Ms[i + k * kLDT];
 #pragma unroll
-        for (int c = 0; c < kTsR; ++c)
+        for (int c = 0; c < RT; ++c)
             if (c < R) part[c] += m * Xs[k + c * kLDT];
     }
 }
 
-template <typename T, bool UPPER, bool TRANS>
+template <typename T>
+AS_DEV void cp_async_elem(T* smem, const T* gmem, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    if (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(ok ? 4 : 0) : "memory");
+}
+
+template <typename T, bool UPPER, bool TRANS, int RT>
 __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const DevArgs* args, const DevState* st) {
     if (p.slot >= 0 && ld_volatile_i32(&st->est_next) != p.slot) return;
     if (p.skip_if_singular && st->info != ~0ull) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* Ms = (T*)smem_raw;                       // kNB x kLDT: T block / Dinv block
-    T* Xs = Ms + kNB * kLDT;                    // kNB x kLDT (R columns used): X_j tile
-    T* Red = Xs + kNB * kLDT;                   // 4 x kNB x kTsR partials
+    T* Mb0 = (T*)smem_raw;                      // kNB x kLDT: T block (double buffered: Mb0, Mb1)
+    T* Mb1 = Mb0 + kNB * kLDT;
+    T* Xs = Mb1 + kNB * kLDT;                   // kNB x kLDT (R columns used): X_j tile
+    T* Red = Xs + kNB * kLDT;                   // 4 x kNB x RT partials
+    T* Ds = Red + 4 * kNB * RT;                 // kNB x kLDT: Dinv_b (prefetched off the critical path)
     __shared__ unsigned s_ticket;
 
     const T* A = (const T*)(p.A ? p.A : args->A);
@@ -135,83 +146,85 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     const int64_t ob = (int64_t)b * kNB;
     const int nbr = (int)min<int64_t>(kNB, n - ob);
     const int c0 = rt * kTsR;
-    const int R = min(kTsR, p.nrhs - c0);
+    const int R = min(RT, p.nrhs - c0);
     const int i = threadIdx.x % kNB, q = threadIdx.x / kNB;
 
+    // async staging of op(T)_{b j} (no-trans: A[b rows, j cols]; trans: A[j rows, b cols])
+    auto stage = [&](T* dst, int sp) {
+        const int j = FWD ? sp : nblk - 1 - sp;
+        const int64_t oj = (int64_t)j * kNB;
+        const int nbj = (int)min<int64_t>(kNB, n - oj);
+        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+            const int r = e % kNB, c = e / kNB;
+            const bool ok = TRANS ? (r < nbj && c < nbr) : (r < nbr && c < nbj);
+            const T* src = !ok ? A : TRANS ? A + (oj + r) + (ob + c) * p.lda : A + (ob + r) + (oj + c) * p.lda;
+            cp_async_elem(dst + r + c * kLDT, src, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (s > 0) stage(Mb0, 0);
+    {   // Dinv_b prefetch
+        const T* D = Dinv + (int64_t)b * kNB * kNB;
+        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) Ds[(e % kNB) + (e / kNB) * kLDT] = D[e];
+    }
     // acc = B_b (only q == 0 threads keep it)
-    T acc[kTsR];
+    T acc[RT];
 #pragma unroll
-    for (int c = 0; c < kTsR; ++c) acc[c] = (q == 0 && c < R && i < nbr) ? X[(ob + i) + (c0 + c) * p.ldx] : T(0);
+    for (int c = 0; c < RT; ++c) acc[c] = (q == 0 && c < R && i < nbr) ? X[(ob + i) + (c0 + c) * p.ldx] : T(0);
 
-    T part[kTsR];
+    T part[RT];
     for (int sp = 0; sp < s; ++sp) {
         const int j = FWD ? sp : nblk - 1 - sp;
         const int64_t oj = (int64_t)j * kNB;
         const int nbj = (int)min<int64_t>(kNB, n - oj);
-        // stage op(T)_{bj}: no-trans: A[b rows, j cols]; trans: A[j rows, b cols] (transposed in product)
-        __syncthreads();
-        if (!TRANS) {
-            for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-                const int r = e % kNB, c = e / kNB;
-                Ms[r + c * kLDT] = (r < nbr && c < nbj) ? A[(ob + r) + (oj + c) * p.lda] : T(0);
-            }
-        } else {
-            for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-                const int r = e % kNB, c = e / kNB;   // r: row within A block (j rows), c: col (b cols)
-                Ms[r + c * kLDT] = (r < nbj && c < nbr) ? A[(oj + r) + (ob + c) * p.lda] : T(0);
-            }
-        }
+        T* Ms = (sp & 1) ? Mb1 : Mb0;
+        if (sp + 1 < s) stage((sp & 1) ? Mb0 : Mb1, sp + 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
         // wait for X_j (tile rt)
         if (threadIdx.x == 0) {
             const unsigned* f = &p.sync[1 + j * ntiles + rt];
             while (ld_acquire(f) == 0u) { __nanosleep(20); }
         }
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        for (int e = threadIdx.x; e < kNB * kTsR; e += blockDim.x) {
+        for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
             const int r = e % kNB, c = e / kNB;
             Xs[r + c * kLDT] = (r < nbj && c < R) ? __ldcg(&X[(oj + r) + (c0 + c) * p.ldx]) : T(0);
         }
         __syncthreads();
-        if (!TRANS) block_product<T, false>(Ms, Xs, part, R);
-        else block_product<T, true>(Ms, Xs, part, R);
+        if (!TRANS) block_product<T, false, RT>(Ms, Xs, part, R);
+        else block_product<T, true, RT>(Ms, Xs, part, R);
 #pragma unroll
-        for (int c = 0; c < kTsR; ++c) Red[(q * kTsR + c) * kNB + i] = part[c];
+        for (int c = 0; c < RT; ++c) Red[(q * RT + c) * kNB + i] = part[c];
         __syncthreads();
         if (q == 0) {
 #pragma unroll
-            for (int c = 0; c < kTsR; ++c)
-                acc[c] -= (Red[(0 * kTsR + c) * kNB + i] + Red[(1 * kTsR + c) * kNB + i]) +
-                          (Red[(2 * kTsR + c) * kNB + i] + Red[(3 * kTsR + c) * kNB + i]);
+            for (int c = 0; c < RT; ++c)
+                acc[c] -= (Red[(0 * RT + c) * kNB + i] + Red[(1 * RT + c) * kNB + i]) +
+                          (Red[(2 * RT + c) * kNB + i] + Red[(3 * RT + c) * kNB + i]);
         }
     }
     // X_b = Dinv_b * acc  (trans: Dinv_b^T)
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    {
-        const T* D = Dinv + (int64_t)b * kNB * kNB;
-        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-            const int r = e % kNB, c = e / kNB;
-            Ms[r + c * kLDT] = D[r + c * kNB];
-        }
-        if (q == 0) {
+    if (q == 0) {
 #pragma unroll
-            for (int c = 0; c < kTsR; ++c) Xs[i + c * kLDT] = acc[c];
-        }
+        for (int c = 0; c < RT; ++c) Xs[i + c * kLDT] = acc[c];
     }
     __syncthreads();
-    if (!TRANS) block_product<T, false>(Ms, Xs, part, R);
-    else block_product<T, true>(Ms, Xs, part, R);
+    if (!TRANS) block_product<T, false, RT>(Ds, Xs, part, R);
+    else block_product<T, true, RT>(Ds, Xs, part, R);
 #pragma unroll
-    for (int c = 0; c < kTsR; ++c) Red[(q * kTsR + c) * kNB + i] = part[c];
+    for (int c = 0; c < RT; ++c) Red[(q * RT + c) * kNB + i] = part[c];
     __syncthreads();
     if (q == 0 && i < nbr) {
 #pragma unroll
-        for (int c = 0; c < kTsR; ++c)
+        for (int c = 0; c < RT; ++c)
             if (c < R)
-                X[(ob + i) + (c0 + c) * p.ldx] = (Red[(0 * kTsR + c) * kNB + i] + Red[(1 * kTsR + c) * kNB + i]) +
-                                                 (Red[(2 * kTsR + c) * kNB + i] + Red[(3 * kTsR + c) * kNB + i]);
+                X[(ob + i) + (c0 + c) * p.ldx] = (Red[(0 * RT + c) * kNB + i] + Red[(1 * RT + c) * kNB + i]) +
+                                                 (Red[(2 * RT + c) * kNB + i] + Red[(3 * RT + c) * kNB + i]);
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();   // release is cumulative over the CTA's X stores ordered by this barrier
     if (threadIdx.x == 0) st_release(&p.sync[1 + b * ntiles + rt], 1u);
 }
 
@@ -252,17 +265,22 @@ static void trsm_dispatch(const TsArgs& p, bool upper, bool trans, const DevArgs
                           cudaStream_t s) {
     const int nblk = (int)((p.n + kNB - 1) / kNB);
     const int ntiles = (p.nrhs + kTsR - 1) / kTsR;
-    const size_t smem = sizeof(T) * (2 * kNB * kLDT + 4 * kNB * kTsR);
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern, int rt) {
+        const size_t smem = sizeof(T) * (4 * kNB * kLDT + 4 * kNB * rt);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk * ntiles, kTsThreads, smem, s>>>(p, args, st);
     };
+    auto by_r = [&](auto k1, auto k4, auto k16) {
+        if (p.nrhs == 1) go(k1, 1);
+        else if (p.nrhs <= 4) go(k4, 4);
+        else go(k16, kTsR);
+    };
     if (upper) {
-        if (trans) go(trsm_sf_kernel<T, true, true>);
-        else go(trsm_sf_kernel<T, true, false>);
+        if (trans) by_r(trsm_sf_kernel<T, true, true, 1>, trsm_sf_kernel<T, true, true, 4>, trsm_sf_kernel<T, true, true, kTsR>);
+        else by_r(trsm_sf_kernel<T, true, false, 1>, trsm_sf_kernel<T, true, false, 4>, trsm_sf_kernel<T, true, false, kTsR>);
     } else {
-        if (trans) go(trsm_sf_kernel<T, false, true>);
-        else go(trsm_sf_kernel<T, false, false>);
+        if (trans) by_r(trsm_sf_kernel<T, false, true, 1>, trsm_sf_kernel<T, false, true, 4>, trsm_sf_kernel<T, false, true, kTsR>);
+        else by_r(trsm_sf_kernel<T, false, false, 1>, trsm_sf_kernel<T, false, false, 4>, trsm_sf_kernel<T, false, false, kTsR>);
     }
 }
 
