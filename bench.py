@@ -188,6 +188,22 @@ def cpu_baseline(tag: str, A, B, budget_s: float = 12.0):
             "sample": f"{sample}, {reps} solve(s) in {dt:.1f} s"}
 
 
+# ------------------------------------------------------------------ multi-rank aggregation
+def aggregate_time(t_ms: float, dist=None, device=None) -> float:
+    """Max over ranks of this rank's timed-region duration (replicas: the job ends with the slowest)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return t_ms
+    import torch
+    t = torch.tensor([t_ms], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(world: int, steps: int, t_max_ms: float) -> float:
+    """Whole-job solves/s: every rank solves `steps` independent systems in t_max."""
+    return world * steps / (t_max_ms * 1e-3)
+
+
 # ------------------------------------------------------------------ main (CUDA arm)
 def main():
     ap = argparse.ArgumentParser()
@@ -263,13 +279,9 @@ def main():
     if dist:
         dist.barrier()
     clocks = clock.stop()
-    t_ms = float(np.sum(step_ms))
-    if dist:
-        t = torch.tensor([t_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
+    t_ms = aggregate_time(float(np.sum(step_ms)), dist, device="cuda")
     ms_per_step = t_ms / args.steps
-    value = world * args.steps / (t_ms * 1e-3)
+    value = job_throughput(world, args.steps, t_ms)
     stage /= args.steps
     rep = reports[-1]
 

@@ -152,6 +152,98 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_sweep_kernel(T* M, int6
     if (lane == 0 && my_rot) atomicAdd(&st->rotated, my_rot);
 }
 
+// ------------------------------------------------------------------ (2') one block-Jacobi sweep
+// Columns are grouped in blocks of BS; a round-robin tournament over the NB blocks pairs them,
+// each CTA stages its two blocks (2*BS columns of M and the matching rows of Y) in shared
+// memory and rotates every pair among its 2*BS columns (a local round-robin), then writes
+// them back.  One sweep = NB-1 block rounds, each ending in one grid barrier (instead of
+// n-1 rounds of single pairs); every pair (p, q) meets at least once per sweep.
+template <typename T, int BS>
+__global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M, int64_t ldw, int64_t n, T* Y,
+                                                                            int64_t nrhs, DevState* st, unsigned* bar) {
+    constexpr int C2 = 2 * BS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Ms = (T*)smem_raw;                  // C2 columns x n
+    T* Ys = Ms + (int64_t)C2 * n;          // C2 rows x nrhs
+    __shared__ int s_gc[C2];
+    const int P = gridDim.x, k = blockIdx.x;
+    const int NB = 2 * P;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const T tol = (T)n * Eps<T>::v;
+    int my_rot = 0;
+    for (int r = 0; r < NB - 1; ++r) {
+        const int s1 = k, s2 = NB - 1 - k;
+        const int ba = s1 == 0 ? 0 : 1 + (s1 - 1 + r) % (NB - 1);
+        const int bb = s2 == 0 ? 0 : 1 + (s2 - 1 + r) % (NB - 1);
+        if (threadIdx.x < C2) {
+            const int blk = threadIdx.x < BS ? ba : bb;
+            const int64_t gc = (int64_t)blk * BS + (threadIdx.x % BS);
+            s_gc[threadIdx.x] = gc < n ? (int)gc : -1;
+        }
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < (int64_t)C2 * n; e += blockDim.x) {
+            const int c = (int)(e / n);
+            const int64_t i = e % n;
+            const int gc = s_gc[c];
+            Ms[e] = gc >= 0 ? __ldcg(&M[i + (int64_t)gc * ldw]) : T(0);
+        }
+        for (int64_t e = threadIdx.x; e < (int64_t)C2 * nrhs; e += blockDim.x) {
+            const int c = (int)(e % C2);
+            const int64_t rr = e / C2;
+            const int gc = s_gc[c];
+            Ys[c + rr * C2] = gc >= 0 ? __ldcg(&Y[gc + rr * n]) : T(0);
+        }
+        __syncthreads();
+        // local round-robin over C2 columns: C2-1 sub-rounds of BS disjoint pairs, one warp per pair
+        for (int sr = 0; sr < C2 - 1; ++sr) {
+            for (int u = warp; u < BS; u += (int)(blockDim.x >> 5)) {
+                const int t1 = u, t2 = C2 - 1 - u;
+                const int la = t1 == 0 ? 0 : 1 + (t1 - 1 + sr) % (C2 - 1);
+                const int lb = t2 == 0 ? 0 : 1 + (t2 - 1 + sr) % (C2 - 1);
+                int lp = la, lq = lb;
+                if (s_gc[lp] < 0 || s_gc[lq] < 0) continue;
+                if (s_gc[lp] > s_gc[lq]) { lp = lb; lq = la; }   // p < q by global column index
+                T* mp = Ms + (int64_t)lp * n;
+                T* mq = Ms + (int64_t)lq * n;
+                T al = T(0), be = T(0), ga = T(0);
+                for (int64_t i = lane; i < n; i += 32) { const T x = mp[i], y = mq[i]; al += x * x; be += y * y; ga += x * y; }
+                al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+                if (ga == T(0) || !((ga < T(0) ? -ga : ga) > tol * sqrt(al) * sqrt(be))) continue;
+                ++my_rot;
+                const T zeta = (be - al) / (T(2) * ga);
+                const T t = (zeta >= T(0) ? T(1) : T(-1)) / ((zeta < T(0) ? -zeta : zeta) + sqrt(T(1) + zeta * zeta));
+                const T c = T(1) / sqrt(T(1) + t * t);
+                const T sn = c * t;
+                for (int64_t i = lane; i < n; i += 32) {
+                    const T x = mp[i], y = mq[i];
+                    mp[i] = c * x - sn * y;
+                    mq[i] = sn * x + c * y;
+                }
+                for (int64_t rr = lane; rr < nrhs; rr += 32) {
+                    const T x = Ys[lp + rr * C2], y = Ys[lq + rr * C2];
+                    Ys[lp + rr * C2] = c * x - sn * y;
+                    Ys[lq + rr * C2] = sn * x + c * y;
+                }
+            }
+            __syncthreads();
+        }
+        for (int64_t e = threadIdx.x; e < (int64_t)C2 * n; e += blockDim.x) {
+            const int c = (int)(e / n);
+            const int64_t i = e % n;
+            const int gc = s_gc[c];
+            if (gc >= 0) M[i + (int64_t)gc * ldw] = Ms[e];
+        }
+        for (int64_t e = threadIdx.x; e < (int64_t)C2 * nrhs; e += blockDim.x) {
+            const int c = (int)(e % C2);
+            const int64_t rr = e / C2;
+            const int gc = s_gc[c];
+            if (gc >= 0) Y[gc + rr * n] = Ys[c + rr * C2];
+        }
+        grid_barrier(bar, (unsigned)(r + 1), (unsigned)P);
+    }
+    if (lane == 0 && my_rot) atomicAdd(&st->rotated, my_rot);
+}
+
 // WHILE-node condition: another sweep iff this one rotated and the cap is not hit
 __global__ void sweep_check_kernel(DevState* st, unsigned* bar, cudaGraphConditionalHandle h) {
     if (threadIdx.x != 0) return;
@@ -263,7 +355,30 @@ static void svd_pre_t(const Work& w, cudaStream_t s) {
 
 template <typename T>
 static void svd_sweep_t(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s) {
-    coop_launch(jacobi_sweep_kernel<T>, w.num_sms, s, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
+    constexpr int BS = 4;
+    const int64_t nb = (w.n + BS - 1) / BS;
+    const int P = (int)((nb + 1) / 2);                     // NB = 2P blocks (one may be a dummy)
+    const size_t smem = sizeof(T) * ((size_t)2 * BS * w.n + (size_t)2 * BS * std::max<int64_t>(w.nrhs, 1));
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (P >= 2 && P <= w.num_sms && smem <= (size_t)optin) {
+        auto kern = jacobi_block_sweep_kernel<T, BS>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(P);
+        cfg.blockDim = dim3(kSvdThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
+    } else {
+        coop_launch(jacobi_sweep_kernel<T>, w.num_sms, s, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
+    }
     sweep_check_kernel<<<1, 32, 0, s>>>(w.st, w.bars + 1, h);
 }
 
