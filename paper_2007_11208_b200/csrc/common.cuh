@@ -124,10 +124,11 @@ AS_DEV unsigned long long gtimer() {
 AS_DEV void grid_barrier(unsigned* ctr, unsigned gen, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
+        // arrive with release semantics (cumulative over the CTA's writes ordered by the barrier),
+        // then spin with acquire loads (no sleep: the barrier is on every critical path)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
         const unsigned target = gen * nblocks;
-        while (ld_acquire(ctr) < target) { __nanosleep(32); }
+        while (ld_acquire(ctr) < target) { }
     }
     __syncthreads();
 }

@@ -181,17 +181,15 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             s_gc[threadIdx.x] = gc < n ? (int)gc : -1;
         }
         __syncthreads();
-        for (int64_t e = threadIdx.x; e < (int64_t)C2 * n; e += blockDim.x) {
-            const int c = (int)(e / n);
-            const int64_t i = e % n;
+        for (int c = 0; c < C2; ++c) {             // (no runtime 64-bit divisions in the staging loops)
             const int gc = s_gc[c];
-            Ms[e] = gc >= 0 ? __ldcg(&M[i + (int64_t)gc * ldw]) : T(0);
+            T* dst = Ms + (int64_t)c * n;
+            const T* src = M + (int64_t)(gc >= 0 ? gc : 0) * ldw;
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = gc >= 0 ? __ldcg(&src[i]) : T(0);
         }
-        for (int64_t e = threadIdx.x; e < (int64_t)C2 * nrhs; e += blockDim.x) {
-            const int c = (int)(e % C2);
-            const int64_t rr = e / C2;
+        for (int c = 0; c < C2; ++c) {
             const int gc = s_gc[c];
-            Ys[c + rr * C2] = gc >= 0 ? __ldcg(&Y[gc + rr * n]) : T(0);
+            for (int64_t rr = threadIdx.x; rr < nrhs; rr += blockDim.x) Ys[c + rr * C2] = gc >= 0 ? __ldcg(&Y[gc + rr * n]) : T(0);
         }
         __syncthreads();
         // local round-robin over C2 columns: C2-1 sub-rounds of BS disjoint pairs, one warp per pair
@@ -227,17 +225,13 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             }
             __syncthreads();
         }
-        for (int64_t e = threadIdx.x; e < (int64_t)C2 * n; e += blockDim.x) {
-            const int c = (int)(e / n);
-            const int64_t i = e % n;
+        for (int c = 0; c < C2; ++c) {
             const int gc = s_gc[c];
-            if (gc >= 0) M[i + (int64_t)gc * ldw] = Ms[e];
-        }
-        for (int64_t e = threadIdx.x; e < (int64_t)C2 * nrhs; e += blockDim.x) {
-            const int c = (int)(e % C2);
-            const int64_t rr = e / C2;
-            const int gc = s_gc[c];
-            if (gc >= 0) Y[gc + rr * n] = Ys[c + rr * C2];
+            if (gc < 0) continue;
+            const T* src = Ms + (int64_t)c * n;
+            T* dst = M + (int64_t)gc * ldw;
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+            for (int64_t rr = threadIdx.x; rr < nrhs; rr += blockDim.x) Y[gc + rr * n] = Ys[c + rr * C2];
         }
         grid_barrier(bar, (unsigned)(r + 1), (unsigned)P);
     }
