@@ -226,12 +226,14 @@ _lib.as_debug_timestamps.argtypes = [P]
 _lib.as_debug_timestamps.restype = C.c_int
 
 
-def debug_timestamps():
+def debug_timestamps(raw: bool = False):
     """Phase stamps (ns, %globaltimer) of the last call, relative to the first stamp."""
     out = (C.c_ulonglong * 16)()
     if _lib.as_debug_timestamps(out) != 0:
         return None
     v = list(out)
+    if raw:
+        return v
     t0 = v[0]
     return [(x - t0) / 1e3 if x else None for x in v]   # microseconds
 

@@ -188,7 +188,9 @@ constexpr int kBandSpike = 101;
 static void body_factor(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     switch (m) {
     case AS_METHOD_BAND: launch_band_factor(w, s); launch_estimator(w, KIND_BAND, false, sa, s); break;  // sequential
-    case kBandSpike: launch_band_spike(w, s); break;
+    case kBandSpike + 0: case kBandSpike + 1: case kBandSpike + 2: case kBandSpike + 3:
+        launch_band_spike(w, m - kBandSpike, s);
+        break;
     case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); launch_estimator(w, KIND_TRI, false, sa, s); break;
     case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); launch_estimator(w, KIND_TRI, true, sa, s); break;
     case AS_METHOD_LU: launch_lu_factor(w, s); launch_estimator(w, KIND_LU, false, sa, s); break;
@@ -332,9 +334,11 @@ static int build_graph(Plan& P) {
             launch_band_norm(w, s);
             cudaGraphConditionalHandle h_bm = make_handle(s, 0);
             launch_band_dominance(w, h_bm, s);
-            cudaGraph_t* bb = add_cond(s, h_bm, cudaGraphCondTypeIf, 2);
-            B.body(bb[0], [&](cudaStream_t s2) { body_factor(w, kBandSpike, B.sa, s2); });
-            B.body(bb[1], [&](cudaStream_t s2) { body_factor(w, AS_METHOD_BAND, B.sa, s2); });
+            // SWITCH: 0 sequential GBTRF path, 1 + c partitioned path with K class 2^c
+            cudaGraph_t* bb = add_cond(s, h_bm, cudaGraphCondTypeSwitch, 5);
+            B.body(bb[0], [&](cudaStream_t s2) { body_factor(w, AS_METHOD_BAND, B.sa, s2); });
+            for (int c = 0; c < 4; ++c)
+                B.body(bb[1 + c], [&](cudaStream_t s2) { body_factor(w, kBandSpike + c, B.sa, s2); });
         });
         B.body(mb[AS_METHOD_CHOL], [&](cudaStream_t s) {
             launch_chol_factor(w, s);
@@ -450,7 +454,7 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
         launch_band_norm(w, s);
         launch_band_dominance(w, 0, s);
         if ((err = rd())) return err;
-        body_factor(w, h.band_use_spike ? kBandSpike : AS_METHOD_BAND, sa, s);
+        body_factor(w, h.band_use_spike ? kBandSpike + h.band_use_spike - 1 : AS_METHOD_BAND, sa, s);
     } else {
         body_factor(w, h.method, sa, s);
     }

@@ -17,8 +17,8 @@
 // factor, the xLACN2 estimate of ||A^{-1}||_1 (state machine with distributed
 // reductions), and the primary solve X = A^{-1} B -- runs in ONE cooperative
 // kernel of p + 2 CTAs; phases are separated by grid barriers.  Bandwidths are
-// padded to a K class (1, 2, 4, 8, 16) >= max(kl, ku); one variant per class is
-// captured and all but the matching one exit at once.
+// padded to a K class (1, 2, 4, 8) >= max(kl, ku); a SWITCH node (value set by
+// band_mode_kernel) launches the matching variant only.
 #include "internal.h"
 #include "rcond.h"
 
@@ -26,7 +26,7 @@ namespace as {
 
 constexpr int kSpThreads = 256;
 constexpr int kSpR = 8;    // RHS columns per partition-solve chunk (one thread per column)
-constexpr int kRedR = 4;   // RHS columns per reduced-solve chunk
+constexpr int kRedR = 8;   // RHS columns per reduced-solve chunk (the serial chains: 32/K columns per warp)
 
 struct SpikeArgs {
     const DevArgs* args;
@@ -56,78 +56,81 @@ struct SpLayout {
 // ------------------------------------------------------------------ partition-level chains
 // LU rows: LU[r*LDR + k], k = col - row + K; the diagonal slot holds 1/u_jj (reciprocal pivot).
 // Solve A_i y = r (trans=0) or A_i^T y = r (trans=1) in place on v[0..m) (stride vs), one thread.
-// Only the newest window value is on the dependency chain of each step.
-// sum_{q=1..K-1} c[q] * w[q] as a balanced tree (off the step's dependency chain)
-template <typename T, int K>
-AS_DEV T tail_dot(const T (&c)[K], const T (&w)[K]) {
-    T p[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) p[q] = q == 0 ? T(0) : c[q] * w[q];
-#pragma unroll
-    for (int h = 1; h < K; h *= 2)
-#pragma unroll
-        for (int q = 0; q + h < K; q += 2 * h) p[q] += p[q + h];
-    return p[0];
-}
-
-// LU rows (pitch LDR = 2K+2, odd lane stride for the warp factor loop), zero pad rows
-// -K..-1 and m..m+K-1 so the transposed sweeps load unconditionally.
-template <typename T, int K>
-AS_DEV void part_solve(const T* __restrict__ LU, int m, T* __restrict__ v, int vs, bool trans, int first_nz) {
+// LU rows (pitch LDR = 2K+2), zero pad rows -K..-1 and m..m+K-1; LU[j][K] = 1/u_jj.
+// LC rows hold the factor's columns: LC[j][q] = L(j+1+q, j), LC[j][K+1+q] = U(j-1-q, j).
+//
+// One substitution sweep, column-oriented: once s_j is known it is folded into the pending
+// right-hand sides of the next K rows of the sweep (acc[0..K-1]), so the dependency chain per
+// row is one FMA (+ one multiply by 1/u) and the K updates are independent.  CASE: 0 unit L
+// (forward, LC), 1 U (backward, LC), 2 U^T (forward, LU rows), 3 unit L^T (backward, LU rows).
+// The right-hand sides entering the window are read kChunk rows ahead.
+constexpr int kChunk = 8;
+template <typename T, int K, int CASE>
+AS_DEV void sweep_row(const T* __restrict__ LU, const T* __restrict__ LC, int j, T (&acc)[K], T enter,
+                      T* __restrict__ v, int vs) {
     constexpr int LDR = 2 * K + 2;
-    T win[K], cf[K];
+    T c[K];
 #pragma unroll
-    for (int q = 0; q < K; ++q) win[q] = T(0);
-    if (!trans) {
-#pragma unroll 4
-        for (int j = first_nz; j < m; ++j) {            // unit L: L(j, j-1-q) = LU[j][K-1-q]
-            const T* row = LU + j * LDR;
+    for (int q = 0; q < K; ++q) {
+        if (CASE == 0) c[q] = LC[j * LDR + q];               // L(j+1+q, j)
+        if (CASE == 1) c[q] = LC[j * LDR + K + 1 + q];       // U(j-1-q, j)
+        if (CASE == 2) c[q] = LU[j * LDR + K + 1 + q];       // U(j, j+1+q)
+        if (CASE == 3) c[q] = LU[j * LDR + K - 1 - q];       // L(j, j-1-q)
+    }
+    T s = acc[0];
+    if (CASE == 1 || CASE == 2) s *= LU[j * LDR + K];
+    v[j * vs] = s;
 #pragma unroll
-            for (int q = 0; q < K; ++q) cf[q] = row[K - 1 - q];
-            const T s = (v[j * vs] - tail_dot<T, K>(cf, win)) - cf[0] * win[0];
+    for (int q = 0; q + 1 < K; ++q) acc[q] = acc[q + 1] - c[q] * s;
+    acc[K - 1] = enter - c[K - 1] * s;
+}
+template <typename T, int K, int CASE>
+AS_DEV void sweep(const T* __restrict__ LU, const T* __restrict__ LC, int jb, int je, T* __restrict__ v, int vs) {
+    constexpr bool FWD = (CASE == 0 || CASE == 2);
+    const int cnt = je - jb;
+    T acc[K];
 #pragma unroll
-            for (int q = K - 1; q > 0; --q) win[q] = win[q - 1];
-            win[0] = s;
-            v[j * vs] = s;
+    for (int q = 0; q < K; ++q) acc[q] = q < cnt ? v[(FWD ? jb + q : je - 1 - q) * vs] : T(0);
+    int t = 0;
+    for (; t + kChunk <= cnt; t += kChunk) {
+        T vv[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            const int te = t + u + K;
+            vv[u] = te < cnt ? v[(FWD ? jb + te : je - 1 - te) * vs] : T(0);
         }
 #pragma unroll
-        for (int q = 0; q < K; ++q) win[q] = T(0);
-#pragma unroll 4
-        for (int j = m - 1; j >= 0; --j) {              // U: U(j, j+1+q) = LU[j][K+1+q]; LU[j][K] = 1/u_jj
-            const T* row = LU + j * LDR;
-#pragma unroll
-            for (int q = 0; q < K; ++q) cf[q] = row[K + 1 + q];
-            const T s = ((v[j * vs] - tail_dot<T, K>(cf, win)) - cf[0] * win[0]) * row[K];
-#pragma unroll
-            for (int q = K - 1; q > 0; --q) win[q] = win[q - 1];
-            win[0] = s;
-            v[j * vs] = s;
-        }
-    } else {
-#pragma unroll 4
-        for (int j = first_nz; j < m; ++j) {            // U^T: U(j-1-q, j) = LU[j-1-q][K+1+q]
-#pragma unroll
-            for (int q = 0; q < K; ++q) cf[q] = LU[(j - 1 - q) * LDR + K + 1 + q];
-            const T s = ((v[j * vs] - tail_dot<T, K>(cf, win)) - cf[0] * win[0]) * LU[j * LDR + K];
-#pragma unroll
-            for (int q = K - 1; q > 0; --q) win[q] = win[q - 1];
-            win[0] = s;
-            v[j * vs] = s;
-        }
-#pragma unroll
-        for (int q = 0; q < K; ++q) win[q] = T(0);
-#pragma unroll 4
-        for (int j = m - 1; j >= 0; --j) {              // L^T (unit): L(j+1+q, j) = LU[j+1+q][K-1-q]
-#pragma unroll
-            for (int q = 0; q < K; ++q) cf[q] = LU[(j + 1 + q) * LDR + K - 1 - q];
-            const T s = (v[j * vs] - tail_dot<T, K>(cf, win)) - cf[0] * win[0];
-#pragma unroll
-            for (int q = K - 1; q > 0; --q) win[q] = win[q - 1];
-            win[0] = s;
-            v[j * vs] = s;
-        }
+        for (int u = 0; u < kChunk; ++u) sweep_row<T, K, CASE>(LU, LC, FWD ? jb + t + u : je - 1 - t - u, acc, vv[u], v, vs);
+    }
+    for (; t < cnt; ++t) {
+        const int te = t + K;
+        const T ent = te < cnt ? v[(FWD ? jb + te : je - 1 - te) * vs] : T(0);
+        sweep_row<T, K, CASE>(LU, LC, FWD ? jb + t : je - 1 - t, acc, ent, v, vs);
     }
 }
+template <typename T, int K>
+AS_DEV void part_solve(const T* __restrict__ LU, const T* __restrict__ LC, int m, T* __restrict__ v, int vs, bool trans,
+                       int first_nz) {
+    if (!trans) {
+        sweep<T, K, 0>(LU, LC, first_nz, m, v, vs);    // L y = r (rows before first_nz are zero)
+        sweep<T, K, 1>(LU, LC, 0, m, v, vs);           // U x = y
+    } else {
+        sweep<T, K, 2>(LU, LC, first_nz, m, v, vs);    // U^T y = r
+        sweep<T, K, 3>(LU, LC, 0, m, v, vs);           // L^T x = y
+    }
+}
+
+// Reciprocal on the factor's dependency chain: MUFU approximation + two Newton steps
+// (~55 cycles against ~127 for the IEEE division; within 1 ulp, not correctly rounded).
+AS_DEV double recip(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+AS_DEV float recip(float x) { return 1.0f / x; }
 
 // Warp-level in-place Gauss-Jordan inverse of an S x S row-major matrix (S <= 32, no
 // pivoting: the reduced pivots of a strictly dominant band matrix are dominant).
@@ -143,7 +146,7 @@ AS_DEV void warp_gj_inverse(T* M) {
 #pragma unroll
     for (int k = 0; k < S; ++k) {
         const T piv = __shfl_sync(0xffffffffu, col[k], k);
-        const T inv = T(1) / piv;
+        const T inv = recip(piv);
         const T pk = col[k] * inv;          // normalized pivot-row entry of my column
         T f[S];
 #pragma unroll
@@ -157,9 +160,30 @@ AS_DEV void warp_gj_inverse(T* M) {
     __syncwarp();
 }
 
+// Latency-batched element loop: each thread issues U independent loads before any of its
+// stores, so a loop over global/L2 data costs ~tot / (U * blockDim) memory latencies instead of
+// tot / blockDim (the kernel is latency-bound: one CTA per partition, little data per CTA).
+template <int U, typename T, class Ld, class St>
+AS_DEV void batched(int tot, Ld ld, St stf) {
+    for (int e0 = 0; e0 < tot; e0 += U * (int)blockDim.x) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+            v[u] = e < tot ? ld(e) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+            if (e < tot) stf(e, v[u]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ the kernel
 template <typename T, int K>
 __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) {
+    constexpr int kCPW = (32 / K < kRedR) ? 32 / K : kRedR;   // reduced-chain columns per warp
     constexpr int BW = 2 * K + 2, S = 2 * K;     // BW: LU row pitch (odd lane stride 2K+1 in the factor loop)
     {   // exactly one K-class variant runs (uniform exit for all CTAs of the others)
         const int km = max(a.st->kl, a.st->ku);
@@ -181,6 +205,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
     const SpLayout<K> L(P);
     __shared__ T red_s[32];
     __shared__ long long redi_s[32];
+    __shared__ T zsh[2 * K * kSpR];            // interface values a partition needs (solve correction)
     unsigned gen = 0;
     auto gbar = [&]() { grid_barrier(a.bar, ++gen, (unsigned)gridDim.x); };
 
@@ -188,6 +213,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
     T* LU = (T*)smem_raw + (int64_t)K * BW;     // rows -K .. a.m+K-1, pitch BW
     T* SP = LU + (int64_t)(a.m + K) * BW;       // [4][K][a.m]: V, W (A), V', W' (A^T)
     T* G = SP + (int64_t)4 * K * a.m;           // a.m x kSpR
+    T* LC = G + (int64_t)a.m * kSpR;            // a.m rows, pitch BW: the factor's columns (sweeps)
     // smem carve-up: reduced CTAs  [i][Lr(K x S) | Dinv(S x S) | Fv(K x K)] then h, y
     constexpr int RSZ = 7 * K * K;
     T* RM = (T*)smem_raw;
@@ -197,22 +223,37 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
 
 #define STAMP(k) do { if (cta == 0 && threadIdx.x == 0) st->dbg_t[k] = gtimer(); } while (0)
     STAMP(0);
+    if (cta == 0 && threadIdx.x == 0) st->dbg_t[13] = clock64();
     // ---------------- F1: load the partition band and factor it (no pivoting)
     if (is_part) {
-        for (int e = threadIdx.x; e < (a.m + 2 * K) * BW; e += blockDim.x) {
-            const int r = e / BW - K, k = e % BW;            // rows -K..a.m+K-1 (pads are zero)
-            const int64_t gr = o + r, gc = gr + (k - K);
-            T v = T(0);
-            if (r >= 0 && r < m && gc >= o && gc < o + m && gc - gr <= ku && gr - gc <= kl) v = A[gr + gc * lda];
-            LU[(int64_t)r * BW + k] = v;
+        {   // zero rows -K..a.m+K-1 (pads, out-of-band slots), then the band column by column:
+            // e = (column c, slot k) with k fastest reads a contiguous run of rows of column c
+            T* LU0 = LU - (int64_t)K * BW;
+            for (int e = threadIdx.x; e < (a.m + 2 * K) * BW; e += blockDim.x) LU0[e] = T(0);
+            __syncthreads();
+            batched<8, T>(
+                m * BW,
+                [&](int e) -> T {
+                    const int c = e / BW, k = e - c * BW, r = c + K - k;
+                    const bool ok = k <= 2 * K && r >= 0 && r < m && k - K <= ku && K - k <= kl;
+                    return ok ? A[(o + r) + (o + c) * lda] : T(0);
+                },
+                [&](int e, T v) {
+                    const int c = e / BW, k = e - c * BW, r = c + K - k;
+                    if (k <= 2 * K && r >= 0 && r < m) LU[r * BW + k] = v;
+                });
         }
         __syncthreads();
+        if (cta == 0 && threadIdx.x == 0) st->dbg_t[15] = gtimer();
         if (threadIdx.x < 32) {
+            // lane r (1..K) owns row j+r of the active window: multiplier + its K updates.  Entries
+            // outside the band / partition are zero in LU, so padding kl, ku to K adds zero work.
+            // (A register-resident window with shuffle broadcasts measured 2.5x slower per step:
+            // the step is instruction-issue bound for a single warp.)
             const int lane = threadIdx.x;
-            // lane r (1..K) owns row j+r of the active window: multiplier + its K updates
             for (int j = 0; j < m; ++j) {
                 const T* prow = LU + j * BW + K;               // prow[c] = U(j, j+c)
-                const T inv = T(1) / prow[0];
+                const T inv = recip(prow[0]);
                 if (lane >= 1 && lane <= K && j + lane < m) {
                     T* row = LU + (j + lane) * BW + K - lane;  // row[c] = A(j+lane, j+c)
                     T rv[K + 1], pv[K + 1];
@@ -221,8 +262,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                     const T l = rv[0] * inv;
                     row[0] = l;
 #pragma unroll
-                    for (int c = 1; c <= K; ++c)
-                        if (j + c < m) row[c] = rv[c] - l * pv[c];
+                    for (int c = 1; c <= K; ++c) row[c] = rv[c] - l * pv[c];
                 }
                 __syncwarp();
                 if (lane == 0) LU[j * BW + K] = inv;   // keep the reciprocal pivot
@@ -231,7 +271,15 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
         }
         __syncthreads();
 
+        // column copies of L and U for the column-oriented sweeps
+        for (int e = threadIdx.x; e < m * 2 * K; e += blockDim.x) {
+            const int j = e / (2 * K), qq = e - j * 2 * K;
+            if (qq < K) LC[j * BW + qq] = LU[(j + 1 + qq) * BW + K - 1 - qq];
+            else { const int q = qq - K; LC[j * BW + K + 1 + q] = LU[(j - 1 - q) * BW + K + 1 + q]; }
+        }
+        __syncthreads();
         STAMP(1);
+        if (cta == 0 && threadIdx.x == 0) st->dbg_t[14] = clock64();
         // ---------------- F2: spikes (kind 0 V, 1 W for A; 2 V', 3 W' for A^T), column q
         for (int e = threadIdx.x; e < 4 * K * a.m; e += blockDim.x) SP[e] = T(0);
         __syncthreads();
@@ -266,7 +314,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                 }
                 nz = true;
             }
-            if (nz) part_solve<T, K>(LU, m, v, 1, kind >= 2, first);
+            if (nz) part_solve<T, K>(LU, LC, m, v, 1, kind >= 2, first);
         }
         __syncthreads();
         // tips: [dir][i][w][rr][q], w: 0 Vtop, 1 Vbot, 2 Wtop, 3 Wbot
@@ -294,16 +342,21 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
     //   Slots per interface: [0] X [1] Y [2] Si [3] Wb [4] Vt->N [5] Q [6] M  (K x K, row-major).
     if (!is_part && P > 1) {
         const T* tp = scr + L.tips + (int64_t)rdir * P * 4 * K * K;
-        for (int e = threadIdx.x; e < (P - 1) * K * K; e += blockDim.x) {
-            const int i = e / (K * K), q = e % (K * K);
-            T* R7 = RM + (int64_t)i * RSZ;
-            const T* ti = tp + (int64_t)i * 4 * K * K;
-            const T* tn = tp + (int64_t)(i + 1) * 4 * K * K;
-            R7[0 * K * K + q] = __ldcg(&ti[1 * K * K + q]);
-            R7[1 * K * K + q] = __ldcg(&tn[2 * K * K + q]);
-            R7[3 * K * K + q] = __ldcg(&ti[3 * K * K + q]);
-            R7[4 * K * K + q] = __ldcg(&tn[0 * K * K + q]);
-        }
+        // e = (interface i, part w4, entry q): slot 0 X <- Vbot_i, 1 Y <- Wtop_{i+1}, 3 Wb <- Wbot_i,
+        // 4 Vt <- Vtop_{i+1}
+        batched<16, T>(
+            (P - 1) * 4 * K * K,
+            [&](int e) -> T {
+                const int i = e / (4 * K * K), w4 = (e / (K * K)) & 3, q = e % (K * K);
+                const int blk = (w4 == 1 || w4 == 3) ? i + 1 : i;
+                const int tw = w4 == 0 ? 1 : w4 == 1 ? 2 : w4 == 2 ? 3 : 0;
+                return __ldcg(&tp[((int64_t)blk * 4 + tw) * K * K + q]);
+            },
+            [&](int e, T v) {
+                const int i = e / (4 * K * K), w4 = (e / (K * K)) & 3, q = e % (K * K);
+                const int slot = w4 == 0 ? 0 : w4 == 1 ? 1 : w4 == 2 ? 3 : 4;
+                RM[(int64_t)i * RSZ + slot * K * K + q] = v;
+            });
         __syncthreads();
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         // C = A B (+ C if acc), K x K, one warp
@@ -363,7 +416,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
 #define STAMP1(k) do { if (nsolve == 0 && cta == 0 && threadIdx.x == 0) st->dbg_t[k] = gtimer(); } while (0)
     auto solve = [&](int dir, int R) {
         if (is_part) {
-            if (threadIdx.x < R) part_solve<T, K>(LU, m, G + threadIdx.x, kSpR, dir == 1, 0);
+            if (threadIdx.x < R) part_solve<T, K>(LU, LC, m, G + threadIdx.x, kSpR, dir == 1, 0);
             __syncthreads();
             for (int e = threadIdx.x; e < 2 * K * R; e += blockDim.x) {
                 const int rr = e / R, c = e % R;
@@ -378,10 +431,13 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
             const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
             for (int c0 = 0; c0 < R; c0 += kRedR) {
                 const int Rr = min(kRedR, R - c0);
-                for (int e = threadIdx.x; e < P * 2 * K * Rr; e += blockDim.x) {
-                    const int c = e % Rr, rr = (e / Rr) % (2 * K), i = e / (Rr * 2 * K);
-                    RH[((int64_t)i * 2 * K + rr) * kRedR + c] = __ldcg(&scr[L.gt + ((int64_t)i * 2 * K + rr) * kSpR + c0 + c]);
-                }
+                batched<16, T>(
+                    P * 2 * K * Rr,
+                    [&](int e) -> T {
+                        const int c = e % Rr, ir = e / Rr;      // ir = i * 2K + rr
+                        return __ldcg(&scr[L.gt + (int64_t)ir * kSpR + c0 + c]);
+                    },
+                    [&](int e, T v) { const int c = e % Rr, ir = e / Rr; RH[(int64_t)ir * kRedR + c] = v; });
                 __syncthreads();
                 // vectors [k][c], stride kRedR; gb_i = RH[i][K..2K), gt_{i+1} = RH[i+1][0..K)
                 auto GB = [&](int i) { return RH + ((int64_t)i * 2 * K + K) * kRedR; };
@@ -409,16 +465,17 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                 }
                 __syncthreads();
                 // B: a_i = c_i - M_i a_{i-1}   (serial, registers + shuffles)
-                if (warp == 0) {
-                    const bool act = lane < K * Rr;
-                    const int r = act ? lane / Rr : 0, c = act ? lane % Rr : 0;
+                if (warp * kCPW < Rr) {                 // column group of this warp
+                    const int cb = warp * kCPW, Rw = min(kCPW, Rr - cb);
+                    const bool act = lane < K * Rw;
+                    const int r = act ? lane / Rw : 0, cl = act ? lane % Rw : 0, c = cb + cl;
                     T ap = act ? CA[r * kRedR + c] : T(0);
                     for (int i = 1; i <= P - 2; ++i) {
                         const T* Mi = RM + (int64_t)i * RSZ + 6 * K * K;
                         T s = T(0);
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
-                            const T ak = __shfl_sync(0xffffffffu, ap, k * Rr + c);
+                            const T ak = __shfl_sync(0xffffffffu, ap, k * Rw + cl);
                             s += (act ? Mi[r * K + k] : T(0)) * ak;
                         }
                         T* ci = CA + (int64_t)i * K * kRedR;
@@ -450,16 +507,17 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                 }
                 __syncthreads();
                 // D: b_i = d_i - N_i b_{i+1}   (serial)
-                if (warp == 0) {
-                    const bool act = lane < K * Rr;
-                    const int r = act ? lane / Rr : 0, c = act ? lane % Rr : 0;
+                if (warp * kCPW < Rr) {
+                    const int cb = warp * kCPW, Rw = min(kCPW, Rr - cb);
+                    const bool act = lane < K * Rw;
+                    const int r = act ? lane / Rw : 0, cl = act ? lane % Rw : 0, c = cb + cl;
                     T bp = act ? DB[(int64_t)(P - 2) * K * kRedR + r * kRedR + c] : T(0);
                     for (int i = P - 3; i >= 0; --i) {
                         const T* Ni = RM + (int64_t)i * RSZ + 4 * K * K;
                         T s = T(0);
 #pragma unroll
                         for (int k = 0; k < K; ++k) {
-                            const T bk = __shfl_sync(0xffffffffu, bp, k * Rr + c);
+                            const T bk = __shfl_sync(0xffffffffu, bp, k * Rw + cl);
                             s += (act ? Ni[r * K + k] : T(0)) * bk;
                         }
                         T* di = DB + (int64_t)i * K * kRedR;
@@ -491,21 +549,23 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
             // x_i = g_i - V_i t_{i+1} - W_i b_{i-1};  t_{i+1} = z_i[K:S], b_{i-1} = z_{i-1}[0:K]
             const T* V = SP + (int64_t)(dir * 2 + 0) * K * a.m;
             const T* Wsp = SP + (int64_t)(dir * 2 + 1) * K * a.m;
-            T* zt = RT;   // not used by partition CTAs; small local copy of the needed z values
-            (void)zt;
+            // zsh[q][c]: q < K: t_{i+1}[q] = z_i[K+q];  q >= K: b_{i-1}[q-K] = z_{i-1}[q-K]
+            batched<4, T>(
+                2 * K * R,
+                [&](int e) -> T {
+                    const int q = e / R, c = e - q * R;
+                    if (q < K) return cta < P - 1 ? __ldcg(&scr[L.zz + ((int64_t)cta * S + K + q) * kSpR + c]) : T(0);
+                    return cta > 0 ? __ldcg(&scr[L.zz + ((int64_t)(cta - 1) * S + q - K) * kSpR + c]) : T(0);
+                },
+                [&](int e, T v) { zsh[e] = v; });
+            __syncthreads();
             for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
-                const int r = e / R, c = e % R;
+                const int r = e / R, c = e - r * R;
                 T v = G[r * kSpR + c];
-                if (cta < P - 1) {
-#pragma unroll 4
-                    for (int q = 0; q < K; ++q)
-                        v -= V[(int64_t)q * a.m + r] * __ldcg(&scr[L.zz + ((int64_t)cta * S + K + q) * kSpR + c]);
-                }
-                if (cta > 0) {
-#pragma unroll 4
-                    for (int q = 0; q < K; ++q)
-                        v -= Wsp[(int64_t)q * a.m + r] * __ldcg(&scr[L.zz + ((int64_t)(cta - 1) * S + q) * kSpR + c]);
-                }
+#pragma unroll
+                for (int q = 0; q < K; ++q) v -= V[(int64_t)q * a.m + r] * zsh[q * R + c];
+#pragma unroll
+                for (int q = 0; q < K; ++q) v -= Wsp[(int64_t)q * a.m + r] * zsh[(K + q) * R + c];
                 G[r * kSpR + c] = v;
             }
             __syncthreads();
@@ -521,6 +581,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
     const int64_t nn = n;
     auto block_sum = [&](T v) -> T {   // result valid on thread 0
         v = warp_sum(v);
+        __syncthreads();               // red_s may still be read by a previous reduction
         if ((threadIdx.x & 31) == 0) red_s[threadIdx.x >> 5] = v;
         __syncthreads();
         T r = T(0);
@@ -528,14 +589,21 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
         __syncthreads();
         return r;
     };
+    // sum of the P partition partials, the same fixed tree in every CTA (so every thread of the
+    // grid takes the same estimator branch): one L2 round trip, then a block reduction
     auto all_sum = [&](int slot) -> T {
-        T s = T(0);
-        for (int i = 0; i < P; ++i) s += __ldcg(&part[i * 8 + slot]);
-        return s;
+        T v = (int)threadIdx.x < P ? __ldcg(&part[threadIdx.x * 8 + slot]) : T(0);
+        v = warp_sum(v);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red_s[threadIdx.x >> 5] = v;
+        __syncthreads();
+        T r = T(0);
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red_s[w];
+        return r;
     };
-    auto asum_local = [&]() -> T {
+    auto asum_local = [&](int col) -> T {
         T s = T(0);
-        for (int r = threadIdx.x; r < m; r += blockDim.x) { const T v = G[r * kSpR]; s += v < T(0) ? -v : v; }
+        for (int r = threadIdx.x; r < m; r += blockDim.x) { const T v = G[r * kSpR + col]; s += v < T(0) ? -v : v; }
         return block_sum(s);
     };
     auto set_G_col0 = [&](auto f) {
@@ -553,6 +621,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                 xe[o + r] = G[r * kSpR];      // publish z for the x[jlast] comparison
             }
             warp_argmax(v, idx);
+            __syncthreads();
             if ((threadIdx.x & 31) == 0) { red_s[threadIdx.x >> 5] = v; redi_s[threadIdx.x >> 5] = idx; }
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -566,17 +635,48 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
         gbar();
         T bv = T(-1);
         long long bi = 0x7fffffffffffffffll;
-        for (int i = 0; i < P; ++i) argmax_merge(bv, bi, __ldcg(&part[i * 8 + 2]), (long long)(double)__ldcg(&part[i * 8 + 3]));
+        if ((int)threadIdx.x < P) { bv = __ldcg(&part[threadIdx.x * 8 + 2]); bi = (long long)(double)__ldcg(&part[threadIdx.x * 8 + 3]); }
+        warp_argmax(bv, bi);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) { red_s[threadIdx.x >> 5] = bv; redi_s[threadIdx.x >> 5] = bi; }
+        __syncthreads();
+        bv = T(-1);
+        bi = 0x7fffffffffffffffll;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) argmax_merge(bv, bi, red_s[w], redi_s[w]);
         return bi == 0x7fffffffffffffffll ? 0 : bi;
     };
 
     STAMP(5);
     double est = 0.0;
+    const T* Bm = (const T*)a.args->B;
+    T* X = (T*)a.args->X;
+    // The first solve carries every application of M = A^{-1} that does not depend on the
+    // estimator's iteration: the start vector e/n (col 0), xLACN2's closing alternating-sign
+    // probe (col 1), and the primary solve X = A^{-1} B (cols 2.., speculative: the gate may
+    // still replace it; the spike path is not selected for X == B).
+    const int R0 = (int)min<int64_t>(a.nrhs, kSpR - 2);
     {
-        if (is_part) set_G_col0([&](int64_t) { return T(1) / (T)nn; });
-        solve(0, 1);                                         // y = M (e/n)
-        T s = is_part ? asum_local() : T(0);
-        if (is_part && threadIdx.x == 0) part[cta * 8 + 0] = s;
+        if (is_part) {
+            for (int r = threadIdx.x; r < m; r += blockDim.x) {
+                const int64_t i = o + r;
+                const T sg = (i & 1) ? T(-1) : T(1);
+                G[r * kSpR + 0] = T(1) / (T)nn;
+                G[r * kSpR + 1] = sg * (T(1) + (T)i / (T)(nn - 1));
+            }
+            batched<8, T>(
+                m * R0, [&](int e) -> T { const int c = e / m, r = e - c * m; return Bm[(o + r) + c * a.ldb]; },
+                [&](int e, T v) { const int c = e / m, r = e - c * m; G[r * kSpR + 2 + c] = v; });
+            __syncthreads();
+        }
+        solve(0, 2 + R0);                                    // y = M (e/n), alt probe, X = M B
+        T s = T(0), s3 = T(0);
+        if (is_part) {
+            for (int c = 0; c < R0; ++c)
+                for (int r = threadIdx.x; r < m; r += blockDim.x) X[(o + r) + c * a.ldb] = G[r * kSpR + 2 + c];
+            s = asum_local(0);
+            s3 = asum_local(1);
+            if (threadIdx.x == 0) { part[cta * 8 + 0] = s; part[cta * 8 + 4] = s3; }
+        }
         gbar();
         est = (double)all_sum(0);
         if (is_part)
@@ -590,7 +690,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
             int diff = 0;
             T s2 = T(0);
             if (is_part) {
-                s2 = asum_local();
+                s2 = asum_local(0);
                 for (int r = threadIdx.x; r < m; r += blockDim.x) {
                     const T v = G[r * kSpR];
                     const T sg = v >= T(0) ? T(1) : T(-1);
@@ -615,14 +715,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
             if (zjl != azj && iter < 5) { ++iter; continue; }
             break;
         }
-        // alternating-sign probe
-        if (is_part) set_G_col0([&](int64_t i) { const T sg = (i & 1) ? T(-1) : T(1); return sg * (T(1) + (T)i / (T)(nn - 1)); });
-        solve(0, 1);
-        T s3 = is_part ? asum_local() : T(0);
-        if (is_part && threadIdx.x == 0) part[cta * 8 + 4] = s3;
-        gbar();
-        T tot = T(0);
-        for (int i = 0; i < P; ++i) tot += __ldcg(&part[i * 8 + 4]);
+        // alternating-sign probe (applied in the first solve, column 1)
+        const T tot = all_sum(4);
         const T temp = T(2) * (tot / (T)(3 * nn));
         if (temp > (T)est) est = (double)temp;
     }
@@ -638,16 +732,15 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
 
     STAMP(6);
     // ---------------- primary solve X = A^{-1} B (speculative: the gate may still replace it)
-    const T* Bm = (const T*)a.args->B;
-    T* X = (T*)a.args->X;
-    for (int64_t c0 = 0; c0 < a.nrhs; c0 += kSpR) {
+    // remaining right-hand sides (each CTA reads and writes only its own rows of B and X)
+    for (int64_t c0 = R0; c0 < a.nrhs; c0 += kSpR) {
         const int R = (int)min<int64_t>(kSpR, a.nrhs - c0);
-        if (is_part)
-            for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
-                const int r = e % m, c = e / m;
-                G[r * kSpR + c] = Bm[(o + r) + (c0 + c) * a.ldb];
-            }
-        gbar();   // every partition has read its B rows before anyone writes X (X may alias B)
+        if (is_part) {
+            batched<8, T>(
+                m * R, [&](int e) -> T { const int c = e / m, r = e - c * m; return Bm[(o + r) + (c0 + c) * a.ldb]; },
+                [&](int e, T v) { const int c = e / m, r = e - c * m; G[r * kSpR + c] = v; });
+            __syncthreads();
+        }
         solve(0, R);
         if (is_part)
             for (int e = threadIdx.x; e < m * R; e += blockDim.x) {
@@ -686,22 +779,25 @@ __global__ void band_dominance_kernel(const DevArgs* args, int64_t lda, int64_t 
 }
 
 // feasible_mask bit c: the K = 2^c variant was captured (fits in shared memory, enough SMs)
-__global__ void band_mode_kernel(DevState* st, cudaGraphConditionalHandle h, int feasible_mask) {
+__global__ void band_mode_kernel(const DevArgs* args, DevState* st, cudaGraphConditionalHandle h, int feasible_mask) {
     if (threadIdx.x != 0) return;
+    // the spike kernel writes X speculatively before the gate: not for an in-place solve (X == B),
+    // whose fallback still needs B
     const int km = max(st->kl, st->ku);
     const int cbit = km <= 1 ? 0 : km <= 2 ? 1 : km <= 4 ? 2 : km <= 8 ? 3 : 4;
     const int use = (st->band_dom != 0) && st->kl + st->ku > 0 && km <= 16 && ((feasible_mask >> cbit) & 1) &&
-                    st->primary == AS_METHOD_BAND;
+                    st->primary == AS_METHOD_BAND &&
+                    (const void*)args->X != args->B;
     st->band_fast = 0;
-    st->band_use_spike = use;
-    if (h) cudaGraphSetConditional(h, use ? 1u : 0u);
+    st->band_use_spike = use ? 1 + cbit : 0;      // 1 + K class index (SWITCH value; 0 = sequential)
+    if (h) cudaGraphSetConditional(h, use ? (unsigned)(1 + cbit) : 0u);
 }
 
 // ------------------------------------------------------------------ host side
 template <typename T, int K>
 static size_t part_smem(int M) {
     constexpr int BW = 2 * K + 2;
-    return sizeof(T) * ((size_t)(M + 2 * K) * BW + (size_t)4 * K * M + (size_t)M * kSpR) + 64;
+    return sizeof(T) * ((size_t)(M + 2 * K) * BW + (size_t)4 * K * M + (size_t)M * kSpR + (size_t)M * BW) + 64;
 }
 template <typename T, int K>
 static size_t red_smem(int P) {
@@ -772,13 +868,23 @@ static int feasible_mask_t(int64_t n, int num_sms) {
     return mask;
 }
 
-void launch_band_spike(const Work& w, cudaStream_t s) {
+void launch_band_spike(const Work& w, int cls, cudaStream_t s) {
     if (w.dtype == AS_F64) {
-        launch_spike_k<double, 1>(w, s); launch_spike_k<double, 2>(w, s); launch_spike_k<double, 4>(w, s);
-        launch_spike_k<double, 8>(w, s);
+        switch (cls) {
+        case 0: launch_spike_k<double, 1>(w, s); break;
+        case 1: launch_spike_k<double, 2>(w, s); break;
+        case 2: launch_spike_k<double, 4>(w, s); break;
+        case 3: launch_spike_k<double, 8>(w, s); break;
+        default: break;
+        }
     } else {
-        launch_spike_k<float, 1>(w, s); launch_spike_k<float, 2>(w, s); launch_spike_k<float, 4>(w, s);
-        launch_spike_k<float, 8>(w, s);
+        switch (cls) {
+        case 0: launch_spike_k<float, 1>(w, s); break;
+        case 1: launch_spike_k<float, 2>(w, s); break;
+        case 2: launch_spike_k<float, 4>(w, s); break;
+        case 3: launch_spike_k<float, 8>(w, s); break;
+        default: break;
+        }
     }
 }
 
@@ -787,7 +893,7 @@ void launch_band_dominance(const Work& w, cudaGraphConditionalHandle h, cudaStre
     const int mask = w.dtype == AS_F64 ? feasible_mask_t<double>(w.n, w.num_sms) : feasible_mask_t<float>(w.n, w.num_sms);
     if (w.dtype == AS_F64) band_dominance_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
     else band_dominance_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
-    band_mode_kernel<<<1, 32, 0, s>>>(w.st, h, mask);
+    band_mode_kernel<<<1, 32, 0, s>>>(w.args, w.st, h, mask);
 }
 
 int64_t spike_scratch_elems(int64_t n, int num_sms) {

@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            PSlot* sl = slots + cta;
+            // slots are double-buffered by column parity like rowbuf: a CTA one column ahead must
+            // not overwrite a candidate another CTA has not read yet
+            PSlot* sl = slots + par * 512 + cta;
             sl->v = (double)v;
             sl->idx = idx;
             // release is cumulative: the CTA's rowbuf writes (ordered by the barrier above) are published too
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
                 for (int q = 0; q < kMaxPer; ++q) {
                     if (!ready[q]) {
                         unsigned long long sq;
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(sq) : "l"(&slots[lane + 32 * q].seq) : "memory");
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(sq) : "l"(&slots[par * 512 + lane + 32 * q].seq) : "memory");
                         ready[q] = sq >= want;
                         all = all && ready[q];
                     }
@@ -148,8 +150,8 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
             for (int q = 0; q < kMaxPer; ++q) {
                 const int t = lane + 32 * q;
                 if (t < P) {
-                    const T cv = (T)__ldcg(&slots[t].v);
-                    const long long ci = __ldcg(&slots[t].idx);
+                    const T cv = (T)__ldcg(&slots[par * 512 + t].v);
+                    const long long ci = __ldcg(&slots[par * 512 + t].idx);
                     if (cv > bv || (cv == bv && ci < bi)) { bv = cv; bi = ci; bo = t; }
                 }
             }

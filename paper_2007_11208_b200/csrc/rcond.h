@@ -17,7 +17,7 @@ void launch_band_solve(const Work& w, cudaStream_t s);             // X = A^{-1}
 
 // band_spike.cu: partitioned path for strictly diagonally dominant band matrices
 void launch_band_dominance(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s);  // sets band_use_spike
-void launch_band_spike(const Work& w, cudaStream_t s);             // factor + estimate + X in one kernel
+void launch_band_spike(const Work& w, int cls, cudaStream_t s);    // K class 2^cls: factor + estimate + X in one kernel
 int64_t spike_scratch_elems(int64_t n, int num_sms);
 
 }  // namespace as
