@@ -133,4 +133,24 @@ AS_DEV void grid_barrier(unsigned* ctr, unsigned gen, unsigned nblocks) {
     __syncthreads();
 }
 
+// Latency-batched element loop: each thread issues U independent loads before any of its
+// stores, so a loop over global/L2 data costs ~tot / (U * blockDim) memory latencies instead of
+// tot / blockDim (the kernel is latency-bound: one CTA per partition, little data per CTA).
+template <int U, typename T, class Ld, class St>
+AS_DEV void batched(int tot, Ld ld, St stf) {
+    for (int e0 = 0; e0 < tot; e0 += U * (int)blockDim.x) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+            v[u] = e < tot ? ld(e) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+            if (e < tot) stf(e, v[u]);
+        }
+    }
+}
+
 }  // namespace as

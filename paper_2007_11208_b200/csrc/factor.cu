@@ -20,6 +20,7 @@
 #include "gemm.h"
 #include "internal.h"
 #include "trsm.h"
+#include "blk64.cuh"
 
 namespace as {
 
@@ -92,31 +93,49 @@ void launch_lu_solve(const Work& w, SyncAlloc& sa, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ Cholesky
+// POTF2 of one kNB x kNB diagonal block in shared memory, plus its inverse.
+// Factor: right-looking with the scaling deferred (a_ik -= a_ij a_kj / d_j, then column j is
+// divided by sqrt(d_j) at the end) so every column step needs a single barrier; the first
+// !(d_j > 0) stops it (Z23).  The inverse L11^{-1} (lower, column-major ld kNB) goes to the
+// block's Dinv slot: the substitutions of POTRS / POCON use it, and L21 = A21 L11^{-T}
+// becomes a small product instead of a second column sweep.
+constexpr int kChLD = kNB + 1;
 template <typename T>
-__global__ void __launch_bounds__(256) potf2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp, DevState* st) {
+__global__ void __launch_bounds__(256) potf2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp, DevState* st,
+                                                    T* Dinv) {
     if (st->chol_failed) return;
-    constexpr int LD = kNB + 1;
-    __shared__ T a[kNB * LD];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* a = (T*)smem_raw;           // kNB x kChLD, lower triangle
+    T* x = a + kNB * kChLD;        // kNB x kChLD, L^{-1}
     __shared__ int s_fail;
-    for (int e = threadIdx.x; e < nbp * nbp; e += blockDim.x) {
-        const int r = e % nbp, c = e / nbp;
-        a[r + c * LD] = (r >= c) ? W[(k0 + r) + (k0 + c) * ldw] : T(0);
+    batched<8, T>(
+        nbp * nbp,
+        [&](int e) -> T { const int r = e % nbp, c = e / nbp; return r >= c ? W[(k0 + r) + (k0 + c) * ldw] : T(0); },
+        [&](int e, T v) { const int r = e % nbp, c = e / nbp; a[r + c * kChLD] = v; });
+    for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+        const int r = e % kNB, c = e / kNB;
+        x[r + c * kChLD] = (r == c) ? T(1) : T(0);
     }
     if (threadIdx.x == 0) s_fail = -1;
     __syncthreads();
+    const int i = threadIdx.x & (kNB - 1), ph = threadIdx.x / kNB;  // 256 threads: 4 phases
+    // thread (row i, phase ph) owns columns k = ph + 4 m of its row: loads first, then stores,
+    // so a step is one smem round trip instead of one per column
     for (int j = 0; j < nbp; ++j) {
-        const T d = a[j + j * LD];
-        if (!(d > T(0))) { if (threadIdx.x == 0) s_fail = j; break; }
-        const T ljj = sqrt(d);
-        __syncthreads();
-        if (threadIdx.x == 0) a[j + j * LD] = ljj;
-        for (int i = j + 1 + threadIdx.x; i < nbp; i += blockDim.x) a[i + j * LD] = a[i + j * LD] / ljj;
-        __syncthreads();
-        {   // thread = (row i, column phase); trailing lower triangle update
-            const int i = threadIdx.x & (kNB - 1), ph = threadIdx.x / kNB, nph = blockDim.x / kNB;
-            if (i > j && i < nbp) {
-                const T lij = a[i + j * LD];
-                for (int k = j + 1 + ph; k <= i; k += nph) a[i + k * LD] -= lij * a[k + j * LD];
+        const T d = a[j + j * kChLD];
+        if (!(d > T(0))) { if (threadIdx.x == 0) s_fail = j; break; }   // uniform
+        if (i > j && i < nbp) {
+            const T aij = a[i + j * kChLD] / d;
+            T va[kNB / 4], vb[kNB / 4];
+#pragma unroll
+            for (int m = 0; m < kNB / 4; ++m) {
+                const int k = j + 1 + ph + 4 * m;
+                if (k <= i) { va[m] = a[i + k * kChLD]; vb[m] = a[k + j * kChLD]; }
+            }
+#pragma unroll
+            for (int m = 0; m < kNB / 4; ++m) {
+                const int k = j + 1 + ph + 4 * m;
+                if (k <= i) a[i + k * kChLD] = va[m] - aij * vb[m];
             }
         }
         __syncthreads();
@@ -129,47 +148,82 @@ __global__ void __launch_bounds__(256) potf2_kernel(T* W, int64_t ldw, int64_t n
         }
         return;
     }
+    __shared__ T sq[kNB];
+    if (threadIdx.x < nbp) sq[threadIdx.x] = sqrt(a[threadIdx.x + threadIdx.x * kChLD]);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+        const int r = e % kNB, c = e / kNB;
+        if (r >= nbp || c >= nbp) a[r + c * kChLD] = (r == c) ? T(1) : T(0);   // identity pad
+        else if (r > c) a[r + c * kChLD] /= sq[c];
+        else if (r == c) a[r + c * kChLD] = sq[c];
+    }
+    __syncthreads();
+    // X = L^{-1} (lower, non-unit): diagonal 16 x 16 blocks by substitution, the rest by
+    // block diagonals (blk64.cuh)
+    block_trinv64<T, false>(a, x, x + kNB * kChLD);
+    T* D = Dinv + (k0 / kNB) * (int64_t)kNB * kNB;
+    for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+        const int r = e % kNB, c = e / kNB;
+        T v;
+        if (r < nbp && c < nbp) v = x[r + c * kChLD];
+        else v = (r == c) ? T(1) : T(0);
+        D[r + c * kNB] = v;
+    }
     for (int e = threadIdx.x; e < nbp * nbp; e += blockDim.x) {
         const int r = e % nbp, c = e / nbp;
-        if (r >= c) W[(k0 + r) + (k0 + c) * ldw] = a[r + c * LD];
+        if (r >= c) W[(k0 + r) + (k0 + c) * ldw] = a[r + c * kChLD];
     }
 }
 
-// L21 = A21 L11^{-T}: each CTA solves kNB rows  x L11^T = a  (column sweep)
+// L21 = A21 L11^{-T} = A21 (Dinv block)^T: each CTA multiplies one kNB-row block in place.
+// 256 threads, 4 x 4 register tile each; As[k][r], Ls[k][c] = Linv(c, k).
+constexpr int kL21LD = kNB + 4;
 template <typename T>
-__global__ void __launch_bounds__(256) l21_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const DevState* st) {
+__global__ void __launch_bounds__(256) l21_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const DevState* st,
+                                                  const T* Dinv) {
     if (st->chol_failed) return;
-    constexpr int LD = kNB + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* L = (T*)smem_raw;         // kNB x LD
-    T* X = L + kNB * LD;         // X[r + c*LD]: row r of this CTA's block, column c
+    T* As = (T*)smem_raw;             // kNB x kL21LD
+    T* Ls = As + kNB * kL21LD;        // kNB x kL21LD
     const int64_t r0 = k0 + nbp + (int64_t)blockIdx.x * kNB;
     const int nr = (int)min<int64_t>(kNB, n - r0);
     if (nr <= 0) return;
-    for (int e = threadIdx.x; e < nbp * nbp; e += blockDim.x) {
-        const int r = e % nbp, c = e / nbp;
-        L[r + c * LD] = (r >= c) ? W[(k0 + r) + (k0 + c) * ldw] : T(0);
-    }
-    for (int e = threadIdx.x; e < nr * nbp; e += blockDim.x) {
-        const int r = e % nr, c = e / nr;
-        X[r + c * LD] = W[(r0 + r) + (k0 + c) * ldw];
-    }
-    __syncthreads();
-    for (int c = 0; c < nbp; ++c) {
-        for (int r = threadIdx.x; r < nr; r += blockDim.x) X[r + c * LD] = X[r + c * LD] / L[c + c * LD];
-        __syncthreads();
-        {   // thread = (row r, column phase)
-            const int r = threadIdx.x & (kNB - 1), ph = threadIdx.x / kNB, nph = blockDim.x / kNB;
-            if (r < nr) {
-                const T xr = X[r + c * LD];
-                for (int cc = c + 1 + ph; cc < nbp; cc += nph) X[r + cc * LD] -= xr * L[cc + c * LD];
+    const T* Li = Dinv + (k0 / kNB) * (int64_t)kNB * kNB;
+    batched<8, T>(
+        2 * kNB * kNB,
+        [&](int e) -> T {
+            if (e < kNB * kNB) {
+                const int r = e % kNB, k = e / kNB;
+                return (r < nr && k < nbp) ? W[(r0 + r) + (k0 + k) * ldw] : T(0);
             }
-        }
-        __syncthreads();
+            const int f = e - kNB * kNB;
+            return Li[f];                     // Linv(c, k) at c + k * kNB
+        },
+        [&](int e, T v) {
+            if (e < kNB * kNB) { const int r = e % kNB, k = e / kNB; As[k * kL21LD + r] = v; }
+            else { const int f = e - kNB * kNB, c = f % kNB, k = f / kNB; Ls[k * kL21LD + c] = v; }
+        });
+    __syncthreads();
+    const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
+    T acc[4][4] = {};
+    for (int k = 0; k < nbp; ++k) {
+        T av[4], bv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { av[q] = As[k * kL21LD + 4 * tr + q]; bv[q] = Ls[k * kL21LD + 4 * tc + q]; }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[p][q] += av[p] * bv[q];
     }
-    for (int e = threadIdx.x; e < nr * nbp; e += blockDim.x) {
-        const int r = e % nr, c = e / nr;
-        W[(r0 + r) + (k0 + c) * ldw] = X[r + c * LD];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int c = 4 * tc + q;
+        if (c >= nbp) continue;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int r = 4 * tr + p;
+            if (r < nr) W[(r0 + r) + (k0 + c) * ldw] = acc[p][q];
+        }
     }
 }
 
@@ -177,15 +231,18 @@ template <typename T>
 static void chol_factor_t(const Work& w, cudaStream_t s) {
     const int64_t n = w.n, ldw = w.ldw;
     T* W = (T*)w.W;
+    T* Dinv = (T*)w.Dinv0;
     copy_norm_kernel<T><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.lda, n, W, ldw, w.st, nullptr);
+    const int sm1 = (int)(sizeof(T) * (2 * kNB * kChLD + 3 * 256));
+    const int sm2 = (int)(sizeof(T) * 2 * kNB * kL21LD);
+    cudaFuncSetAttribute(potf2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+    cudaFuncSetAttribute(l21_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
     for (int64_t k0 = 0; k0 < n; k0 += kNB) {
         const int nbp = (int)std::min<int64_t>(kNB, n - k0);
-        potf2_kernel<T><<<1, 256, 0, s>>>(W, ldw, n, k0, nbp, w.st);
+        potf2_kernel<T><<<1, 256, sm1, s>>>(W, ldw, n, k0, nbp, w.st, Dinv);
         const int64_t rest = n - k0 - nbp;
         if (rest > 0) {
-            const int sm2 = (int)(sizeof(T) * 2 * kNB * (kNB + 1));
-            cudaFuncSetAttribute(l21_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-            l21_kernel<T><<<(unsigned)((rest + kNB - 1) / kNB), 256, sm2, s>>>(W, ldw, n, k0, nbp, w.st);
+            l21_kernel<T><<<(unsigned)((rest + kNB - 1) / kNB), 256, sm2, s>>>(W, ldw, n, k0, nbp, w.st, Dinv);
             GemmArgs g{};
             g.M = rest; g.N = rest; g.K = nbp;
             g.A = W + (k0 + nbp) + k0 * ldw; g.lda = ldw; g.TA = false;
@@ -221,7 +278,7 @@ void launch_chol_check(const Work& w, cudaGraphConditionalHandle h, cudaStream_t
 }
 
 void launch_chol_tri_prep(const Work& w, cudaStream_t s) {
-    launch_trtri_blocks(w.dtype, w.W, w.ldw, w.n, w.Dinv0, false, false, w.st, true, w.args, s);
+    (void)w; (void)s;   // potf2_kernel already wrote the inverse diagonal blocks of L to Dinv0
 }
 
 void launch_chol_solve(const Work& w, SyncAlloc& sa, cudaStream_t s) {

@@ -25,6 +25,7 @@
 #include "factor.h"
 #include "gemm.h"
 #include "internal.h"
+#include "blk64.cuh"
 #include "trsm.h"
 
 namespace as {
@@ -216,65 +217,133 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
 }
 
 // ------------------------------------------------------------------ laswp
-// Apply ipiv[j0 .. j0+cnt) in order to columns [a0, a1) U [b0, b1) and (if perm) to perm.
-// One thread per column (each swap is a dependent pair of accesses, independent across columns).
+// Apply the interchanges ipiv[j0 .. j0+cnt) (in order) to columns [a0, a1) U [b0, b1) and, if
+// perm != nullptr, to perm.  The cnt swaps compose into one permutation of the row set
+// S = [j0, j0+cnt) U {ipiv targets}: every CTA first tracks the final position of each row of S
+// through the swap sequence (one thread per row, in parallel), then one warp per column gathers
+// all moved values and scatters them to their final rows -- independent accesses instead of
+// cnt dependent swaps per column (column-major rows are 8-byte strided accesses either way).
+constexpr int kSwapMax = 2 * kBW;
 template <typename T>
-__global__ void laswp2_kernel(T* W, int64_t ldw, int64_t j0, int cnt, int64_t a0, int64_t a1, int64_t b0, int64_t b1,
-                              const int64_t* ipiv, int64_t* perm) {
+__global__ void __launch_bounds__(256) laswp3_kernel(T* W, int64_t ldw, int64_t j0, int cnt, int64_t a0, int64_t a1,
+                                                     int64_t b0, int64_t b1, const int64_t* ipiv, int64_t* perm) {
+    __shared__ int64_t piv[kBW];
+    __shared__ int64_t dst[kSwapMax], src[kSwapMax];
+    __shared__ int s_np;
+    if (threadIdx.x == 0) s_np = 0;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) piv[q] = ipiv[j0 + q];
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * cnt; t += blockDim.x) {
+        int64_t x;
+        if (t < cnt) x = j0 + t;
+        else {
+            x = piv[t - cnt];
+            if (x < j0 + cnt) continue;                       // already tracked as a block row
+            bool first = true;                                // one thread per distinct external row
+            for (int q = 0; q < t - cnt; ++q) first = first && (piv[q] != x);
+            if (!first) continue;
+        }
+        int64_t pos = x;
+        for (int q = 0; q < cnt; ++q) {
+            const int64_t r = j0 + q, tq = piv[q];
+            if (pos == r) pos = tq;
+            else if (pos == tq) pos = r;
+        }
+        if (pos != x) {
+            const int k = atomicAdd(&s_np, 1);
+            dst[k] = pos;
+            src[k] = x;
+        }
+    }
+    __syncthreads();
+    const int np = s_np;
+    const int lane = threadIdx.x & 31;
     const int64_t na = max<int64_t>(0, a1 - a0), nb = max<int64_t>(0, b1 - b0);
     const int64_t ncols = na + nb + (perm ? 1 : 0);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ncols; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    constexpr int kPer = kSwapMax / 32;
+    for (int64_t t = wid; t < ncols; t += nw) {
         if (perm && t == ncols - 1) {
-            for (int q = 0; q < cnt; ++q) {
-                const int64_t a = j0 + q, b = ipiv[a];
-                if (b != a) { const int64_t x = perm[a]; perm[a] = perm[b]; perm[b] = x; }
-            }
+            int64_t v[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) { const int k = lane + 32 * u; if (k < np) v[u] = perm[src[k]]; }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) { const int k = lane + 32 * u; if (k < np) perm[dst[k]] = v[u]; }
             continue;
         }
         const int64_t col = t < na ? a0 + t : b0 + (t - na);
-        T* __restrict__ c = W + col * ldw;
-        for (int q = 0; q < cnt; ++q) {
-            const int64_t a = j0 + q, b = ipiv[a];
-            if (b != a) { const T x = c[a]; const T y = c[b]; c[a] = y; c[b] = x; }
-        }
+        T* c = W + col * ldw;
+        T v[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) { const int k = lane + 32 * u; if (k < np) v[u] = c[src[k]]; }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) { const int k = lane + 32 * u; if (k < np) c[dst[k]] = v[u]; }
     }
 }
 
-// ------------------------------------------------------------------ U12 = L11^{-1} A12
-// L11: nb x nb unit lower at W[r0.., r0..]; A12 rows r0..r0+nb, columns [c0, c1) (tile of 32).
-constexpr int kU12C = 32;
+// ------------------------------------------------------------------ L11^{-1}, U12 = L11^{-1} A12
+// Inverse of the panel's unit-lower diagonal block (rows / columns k0 .. k0+nbp) into its Dinv0
+// slot: the U12 product below and the final GETRS / GECON forward substitutions use it.  Later
+// interchanges only move rows below the panel, so the block is final once the panel is.
 template <typename T>
-__global__ void __launch_bounds__(256) u12v2_kernel(T* W, int64_t ldw, int64_t r0, int nb, int64_t c0, int64_t c1) {
+__global__ void __launch_bounds__(256) lu_linv_kernel(const T* W, int64_t ldw, int64_t k0, int nbp, T* Dinv) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int LDL = nb + 1;
-    T* L = (T*)smem_raw;                  // nb x LDL
-    T* Bt = L + (int64_t)nb * LDL;        // nb x (kU12C + 1), Bt[r*(kU12C+1) + c]
-    const int64_t cc0 = c0 + (int64_t)blockIdx.x * kU12C;
-    const int nc = (int)min<int64_t>(kU12C, c1 - cc0);
-    if (nc <= 0) return;
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-        const int r = e % nb, c = e / nb;
-        L[r * LDL + c] = r > c ? W[(r0 + r) + (r0 + c) * ldw] : T(0);
-    }
-    for (int e = threadIdx.x; e < nb * nc; e += blockDim.x) {
-        const int r = e % nb, c = e / nb;
-        Bt[r * (kU12C + 1) + c] = W[(r0 + r) + (cc0 + c) * ldw];
-    }
+    T* L = (T*)smem_raw;
+    T* X = L + kB64 * kB64LD;
+    T* tmp = X + kB64 * kB64LD;
+    batched<8, T>(
+        kB64 * kB64,
+        [&](int e) -> T {
+            const int r = e & 63, c = e >> 6;
+            return (r > c && r < nbp) ? W[(k0 + r) + (k0 + c) * ldw] : T(0);
+        },
+        [&](int e, T v) { L[(e & 63) + (e >> 6) * kB64LD] = v; });
     __syncthreads();
-    // forward substitution, one (row i) step at a time, all columns / rows below in parallel
-    {
-        const int c = threadIdx.x & (kU12C - 1), r0 = threadIdx.x / kU12C, nr = blockDim.x / kU12C;
-        for (int i = 0; i < nb - 1; ++i) {
-            if (c < nc) {
-                const T bi = Bt[i * (kU12C + 1) + c];
-                for (int r = i + 1 + r0; r < nb; r += nr) Bt[r * (kU12C + 1) + c] -= L[r * LDL + i] * bi;
-            }
-            __syncthreads();
+    block_trinv64<T, true>(L, X, tmp);
+    T* D = Dinv + (k0 / kB64) * (int64_t)kB64 * kB64;
+    for (int e = threadIdx.x; e < kB64 * kB64; e += blockDim.x) D[e] = X[(e & 63) + (e >> 6) * kB64LD];
+}
+
+// U12 = L11^{-1} A12 in place: one CTA per 64-column tile of rows r0 .. r0+nb, as the product
+// Dinv0(block) x tile (4 x 4 register tiles).
+constexpr int kU12LD = kB64 + 4;
+template <typename T>
+__global__ void __launch_bounds__(256) u12v3_kernel(T* W, int64_t ldw, int64_t r0, int nb, int64_t c0, int64_t c1,
+                                                    const T* Dinv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Ls = (T*)smem_raw;            // Ls[k][r] = Linv(r, k)
+    T* Bs = Ls + kB64 * kU12LD;      // Bs[k][c] = A12(k, c)
+    const int64_t cc0 = c0 + (int64_t)blockIdx.x * kB64;
+    const int nc = (int)min<int64_t>(kB64, c1 - cc0);
+    if (nc <= 0) return;
+    const T* D = Dinv + (r0 / kB64) * (int64_t)kB64 * kB64;
+    batched<8, T>(
+        2 * kB64 * kB64,
+        [&](int e) -> T {
+            if (e < kB64 * kB64) return D[e];
+            const int f = e - kB64 * kB64, k = f & 63, c = f >> 6;
+            return (k < nb && c < nc) ? W[(r0 + k) + (cc0 + c) * ldw] : T(0);
+        },
+        [&](int e, T v) {
+            if (e < kB64 * kB64) Ls[(e >> 6) * kU12LD + (e & 63)] = v;
+            else { const int f = e - kB64 * kB64; Bs[(f & 63) * kU12LD + (f >> 6)] = v; }
+        });
+    __syncthreads();
+    T acc[4][4];
+    tile_mul64<T>(Ls, kU12LD, Bs, kU12LD, nb, acc);
+    const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int c = 4 * tc + q;
+        if (c >= nc) continue;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int r = 4 * tr + p;
+            if (r < nb) W[(r0 + r) + (cc0 + c) * ldw] = acc[p][q];
         }
-    }
-    for (int e = threadIdx.x; e < nb * nc; e += blockDim.x) {
-        const int r = e % nb, c = e / nb;
-        W[(r0 + r) + (cc0 + c) * ldw] = Bt[r * (kU12C + 1) + c];
     }
 }
 
@@ -332,16 +401,24 @@ static void laswp_launch(const Work& w, int64_t j0, int cnt, int64_t a0, int64_t
                          cudaStream_t s) {
     const int64_t ncols = std::max<int64_t>(0, a1 - a0) + std::max<int64_t>(0, b1 - b0) + (perm ? 1 : 0);
     if (ncols <= 0 || cnt <= 0) return;
-    laswp2_kernel<T><<<(unsigned)std::min<int64_t>((ncols + 127) / 128, 8192), 128, 0, s>>>(
+    laswp3_kernel<T><<<(unsigned)std::min<int64_t>((ncols + 7) / 8, (int64_t)w.num_sms * 4), 256, 0, s>>>(
         (T*)w.W, w.ldw, j0, cnt, a0, a1, b0, b1, w.ipiv, perm ? w.perm : nullptr);
+}
+
+template <typename T>
+static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
+    const int smem = (int)(sizeof(T) * (2 * kB64 * kB64LD + 3 * 256));
+    cudaFuncSetAttribute(lu_linv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    lu_linv_kernel<T><<<1, 256, smem, s>>>((const T*)w.W, w.ldw, k0, nbp, (T*)w.Dinv0);
 }
 
 template <typename T>
 static void u12_launch(const Work& w, int64_t r0, int nb, int64_t c0, int64_t c1, cudaStream_t s) {
     if (c1 <= c0) return;
-    const int smem = (int)(sizeof(T) * ((size_t)nb * (nb + 1) + (size_t)nb * (kU12C + 1)));
-    cudaFuncSetAttribute(u12v2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    u12v2_kernel<T><<<(unsigned)((c1 - c0 + kU12C - 1) / kU12C), 256, smem, s>>>((T*)w.W, w.ldw, r0, nb, c0, c1);
+    const int smem = (int)(sizeof(T) * 2 * kB64 * kU12LD);
+    cudaFuncSetAttribute(u12v3_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    u12v3_kernel<T><<<(unsigned)((c1 - c0 + kB64 - 1) / kB64), 256, smem, s>>>((T*)w.W, w.ldw, r0, nb, c0, c1,
+                                                                             (const T*)w.Dinv0);
 }
 
 template <typename T>
@@ -367,6 +444,7 @@ static void block_panels(const Work& w, int64_t k0, int bw, int prio, cudaStream
     const int p1 = std::min(kPW, bw);
     // sequence numbers of the panel exchange grow monotonically with the panel's column
     panel_launch<T>(w, k0, p1, (unsigned long long)(k0 / kPW) * 128ull, prio, s);
+    linv_launch<T>(w, k0, p1, s);
     if (bw > p1) {
         const int p2 = bw - p1;
         // bring the block's second half up to date: swaps of panel 1, U12, rank-p1 update
@@ -374,6 +452,7 @@ static void block_panels(const Work& w, int64_t k0, int bw, int prio, cudaStream
         u12_launch<T>(w, k0, p1, k0 + p1, k0 + bw, s);
         gemm_launch<T>(w, k0 + p1, k0 + p1, k0, n - k0 - p1, p2, p1, s, prio);
         panel_launch<T>(w, k0 + p1, p2, (unsigned long long)((k0 + p1) / kPW) * 128ull, prio, s);
+        linv_launch<T>(w, k0 + p1, p2, s);
     }
 }
 
@@ -427,7 +506,7 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
             block_panels<T>(w, kn, nbw, LS.prio_hi, s);
         }
     }
-    launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv0, false, true, w.st, true, w.args, s);
+    // Dinv0 (unit-L diagonal block inverses) was written panel by panel
     launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
 }
 
