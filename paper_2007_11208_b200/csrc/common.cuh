@@ -108,6 +108,19 @@ AS_DEV unsigned ld_acquire(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// relaxed gpu-scope load (served by L2, no L1 invalidation per poll); pair a successful poll
+// with fence_acq_rel() before reading the data it guards
+AS_DEV unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+AS_DEV unsigned long long ld_relaxed64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+AS_DEV void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 AS_DEV void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -128,7 +141,8 @@ AS_DEV void grid_barrier(unsigned* ctr, unsigned gen, unsigned nblocks) {
         // then spin with acquire loads (no sleep: the barrier is on every critical path)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
         const unsigned target = gen * nblocks;
-        while (ld_acquire(ctr) < target) { }
+        while (ld_relaxed(ctr) < target) { }
+        fence_acq_rel();
     }
     __syncthreads();
 }

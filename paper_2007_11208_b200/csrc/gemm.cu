@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
 // 3-stage cp.async pipeline, 2 CTAs per SM so one CTA's C read-modify-write
 // epilogue overlaps the other's MMA main loop.
 namespace d2 {
-constexpr int BM = 128, BN = 64, BK = 16, ST = 3, NT = 128;
+constexpr int BM = 128, BN = 64, BK = 16, ST = 2, NT = 128;
 constexpr int LDA_KM = BM + 4;   // A as [k][m]
 constexpr int LDA_MK = BK + 4;   // A as [m][k]
 constexpr int LDB_NK = BK + 4;   // B as [n][k]

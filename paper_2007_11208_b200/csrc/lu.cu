@@ -42,6 +42,48 @@ struct __align__(32) PSlot {
 };
 
 // ------------------------------------------------------------------ panel (cooperative)
+// Rows of the panel are split over the P CTAs (shared memory when they fit).  Per column j:
+// every CTA publishes its local first-max candidate row (and the owner of row g the old row g)
+// and a sequence-numbered slot; all CTAs poll the P slots (barrier and data in one), read the
+// winning row, swap, form the multipliers and update column j+1 first, so that column j+1's
+// candidate can be published before the bulk of the rank-1 update -- the other CTAs' exchange
+// latency then overlaps this CTA's update.
+template <typename T>
+AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, int64_t g, int col, T& v, long long& idx,
+                               T* sv, long long* si, int* sdn) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = T(-1);
+    idx = 0x7fffffffffffffffll;
+    int dnan = 0;
+    for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+        const int64_t gr = rbeg + r;
+        if (gr < g) continue;
+        T a = Ps[r + col * cp];
+        a = a < T(0) ? -a : a;
+        if (gr == g && a != a) dnan = 1;
+        argmax_merge(v, idx, a, (long long)gr);
+    }
+    warp_argmax(v, idx);
+    dnan = __any_sync(0xffffffffu, dnan);
+    if (lane == 0) { sv[warp] = v; si[warp] = idx; sdn[warp] = dnan; }
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < 8 ? sv[lane] : T(-1);
+        idx = lane < 8 ? si[lane] : 0x7fffffffffffffffll;
+        int dn = lane < 8 ? sdn[lane] : 0;
+        warp_argmax(v, idx);
+        dn = __any_sync(0xffffffffu, dn);
+        if (lane == 0) {
+            if (dn) { v = T(INFINITY); idx = g; }     // NaN diagonal: the serial sweep keeps row g
+            sv[0] = v; si[0] = idx;
+        }
+    }
+    __syncthreads();
+    v = sv[0];
+    idx = si[0];
+    __syncthreads();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
                                                             int64_t* ipiv, DevState* st, PSlot* slots, T* rowbuf,
@@ -64,48 +106,15 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     if (use_smem) {
-        for (int64_t e = threadIdx.x; e < (int64_t)nr * nbp; e += blockDim.x) {
-            const int64_t r = e % nr, c = e / nr;
-            Ps[r + c * cp] = W[(rbeg + r) + (k0 + c) * ldw];
-        }
+        batched<8, T>(
+            nr * nbp, [&](int e) -> T { const int c = e / nr, r = e - c * nr; return W[(rbeg + r) + (k0 + c) * ldw]; },
+            [&](int e, T v) { const int c = e / nr, r = e - c * nr; Ps[r + c * cp] = v; });
         __syncthreads();
     }
-    unsigned long long info = ~0ull;
-    for (int j = 0; j < nbp; ++j) {
+    // publish the candidate for column j: (v, idx) of this CTA, its row, and the old row g
+    auto publish = [&](int j, T v, long long idx) {
         const int64_t g = k0 + j;
         const int par = j & 1;
-        const unsigned long long want = seq_base + (unsigned long long)j + 1ull;
-        // ---- local first-max over my rows >= g (NaN never wins, Z15)
-        T v = T(-1);
-        long long idx = 0x7fffffffffffffffll;
-        int dnan = 0;
-        for (int r = threadIdx.x; r < nr; r += blockDim.x) {
-            const int64_t gr = rbeg + r;
-            if (gr < g) continue;
-            T a = Ps[r + j * cp];
-            a = a < T(0) ? -a : a;
-            if (gr == g && a != a) dnan = 1;
-            argmax_merge(v, idx, a, (long long)gr);
-        }
-        warp_argmax(v, idx);
-        dnan = __any_sync(0xffffffffu, dnan);
-        if (lane == 0) { sv[warp] = v; si[warp] = idx; sdn[warp] = dnan; }
-        __syncthreads();
-        if (warp == 0) {
-            v = lane < 8 ? sv[lane] : T(-1);
-            idx = lane < 8 ? si[lane] : 0x7fffffffffffffffll;
-            int dn = lane < 8 ? sdn[lane] : 0;
-            warp_argmax(v, idx);
-            dn = __any_sync(0xffffffffu, dn);
-            if (lane == 0) {
-                if (dn) { v = T(INFINITY); idx = g; }     // NaN diagonal: the serial sweep keeps row g
-                sv[0] = v; si[0] = idx;
-            }
-        }
-        __syncthreads();
-        v = sv[0];
-        idx = si[0];
-        // ---- publish my candidate row (and the old row g if I own it)
         if (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) {
             const int r = (int)(idx - rbeg);
             for (int c = threadIdx.x; c < nbp; c += blockDim.x) rowbuf[((int64_t)par * P + cta) * nbp + c] = Ps[r + c * cp];
@@ -122,8 +131,20 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
             sl->v = (double)v;
             sl->idx = idx;
             // release is cumulative: the CTA's rowbuf writes (ordered by the barrier above) are published too
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq), "l"(want) : "memory");
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq), "l"(seq_base + (unsigned long long)j + 1ull) : "memory");
         }
+    };
+    {
+        T v;
+        long long idx;
+        panel_local_argmax(Ps, cp, nr, rbeg, k0, 0, v, idx, sv, si, sdn);
+        publish(0, v, idx);
+    }
+    unsigned long long info = ~0ull;
+    for (int j = 0; j < nbp; ++j) {
+        const int64_t g = k0 + j;
+        const int par = j & 1;
+        const unsigned long long want = seq_base + (unsigned long long)j + 1ull;
         // ---- poll every slot (barrier + data in one), pick the winner
         if (warp == 0) {
             T bv = T(-1);
@@ -139,14 +160,14 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
 #pragma unroll
                 for (int q = 0; q < kMaxPer; ++q) {
                     if (!ready[q]) {
-                        unsigned long long sq;
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(sq) : "l"(&slots[par * 512 + lane + 32 * q].seq) : "memory");
+                        const unsigned long long sq = ld_relaxed64(&slots[par * 512 + lane + 32 * q].seq);
                         ready[q] = sq >= want;
                         all = all && ready[q];
                     }
                 }
                 if (__all_sync(0xffffffffu, all)) break;
             }
+            fence_acq_rel();   // the slots' data (and the rows they guard) after the flags
 #pragma unroll
             for (int q = 0; q < kMaxPer; ++q) {
                 const int t = lane + 32 * q;
@@ -168,48 +189,71 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         __syncthreads();
         const long long p = s_p;
         const int owner = s_owner;
-        for (int c = threadIdx.x; c < nbp; c += blockDim.x) ubuf[c] = __ldcg(&rowbuf[((int64_t)par * P + owner) * nbp + c]);
+        const bool own_p = p != g && p >= rbeg && p < rend;
+        // the pivot row into ubuf; the owner of p takes the old row g (both loads in flight together)
+        T* dst_p = own_p ? Ps + (p - rbeg) : nullptr;
+        for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
+            const T u = __ldcg(&rowbuf[((int64_t)par * P + owner) * nbp + c]);
+            const T dg = own_p ? __ldcg(&diagbuf[par * nbp + c]) : T(0);
+            ubuf[c] = u;
+            if (own_p) dst_p[c * cp] = dg;
+        }
         __syncthreads();
         const T piv = ubuf[j];
         if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
-        if (piv == T(0)) {                       // exact zero pivot: singular column (no elimination)
+        const bool elim = piv != T(0);
+        if (!elim) {                             // exact zero pivot: singular column (no swap, no elimination)
             if (info == ~0ull) info = (unsigned long long)(g + 1);
-            continue;
-        }
-        // ---- swap: row p <- old row g, row g <- pivot row
-        if (p != g && p >= rbeg && p < rend) {
-            const int r = (int)(p - rbeg);
-            for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = __ldcg(&diagbuf[par * nbp + c]);
-        }
-        if (g >= rbeg && g < rend) {
+            if (own_p)                           // undo: row p keeps its own values
+                for (int c = threadIdx.x; c < nbp; c += blockDim.x) dst_p[c * cp] = ubuf[c];
+        } else if (g >= rbeg && g < rend) {
             const int r = (int)(g - rbeg);
             for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = ubuf[c];
         }
         __syncthreads();
-        // ---- multipliers and the rank-1 update of my rows > g (rows x columns in parallel)
         const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
-        const int nrow = (int)max<int64_t>(0, nr - r0);
-        // thread = (row, column phase): rows r0 + (tid % 128) + 128 k, columns j+1+ph, step 2
-        {
+        // ---- multipliers and column j+1 of my rows > g
+        if (elim) {
+            const T u1 = (j + 1 < nbp) ? ubuf[j + 1] : T(0);
+            for (int r = (int)r0 + threadIdx.x; r < nr; r += blockDim.x) {
+                const T l = Ps[r + j * cp] / piv;
+                Ps[r + j * cp] = l;
+                if (j + 1 < nbp) Ps[r + (j + 1) * cp] -= l * u1;
+            }
+        }
+        __syncthreads();
+        if (j + 1 >= nbp) break;
+        // ---- column j+1's candidate: finish its row (and row g+1) first, publish, then the bulk
+        T v;
+        long long idx;
+        panel_local_argmax(Ps, cp, nr, rbeg, g + 1, j + 1, v, idx, sv, si, sdn);
+        const int rc = (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) ? (int)(idx - rbeg) : -1;
+        const int rg = (g + 1 >= rbeg && g + 1 < rend) ? (int)(g + 1 - rbeg) : -1;
+        if (elim) {
+            for (int c = j + 2 + threadIdx.x; c < nbp; c += blockDim.x) {
+                if (rc >= 0) Ps[rc + c * cp] -= Ps[rc + j * cp] * ubuf[c];
+                if (rg >= 0 && rg != rc) Ps[rg + c * cp] -= Ps[rg + j * cp] * ubuf[c];
+            }
+        }
+        __syncthreads();
+        publish(j + 1, v, idx);
+        // ---- bulk rank-1 update of the remaining rows, columns j+2.. (thread = row, column phase)
+        if (elim) {
+            const int nrow = (int)max<int64_t>(0, nr - r0);
             const int rl = threadIdx.x & 127, ph = threadIdx.x >> 7;
-            for (int base = 0; base < nrow; base += 128) {     // uniform trip count (barrier inside)
-                const int r = base + rl;
-                const bool valid = r < nrow;
-                const int64_t rr = r0 + r;
-                const T l = valid ? Ps[rr + j * cp] / piv : T(0);
-                __syncthreads();                               // both phases have read the column-j value
-                if (valid) {
-                    if (ph == 0) Ps[rr + j * cp] = l;
+            for (int rr = rl; rr < nrow; rr += 128) {
+                const int r = (int)r0 + rr;
+                if (r == rc || r == rg) continue;
+                const T l = Ps[r + j * cp];
 #pragma unroll 4
-                    for (int c = j + 1 + ph; c < nbp; c += 2) Ps[rr + c * cp] -= l * ubuf[c];
-                }
+                for (int c = j + 2 + ph; c < nbp; c += 2) Ps[r + c * cp] -= l * ubuf[c];
             }
         }
         __syncthreads();
     }
     if (use_smem) {
-        for (int64_t e = threadIdx.x; e < (int64_t)nr * nbp; e += blockDim.x) {
-            const int64_t r = e % nr, c = e / nr;
+        for (int e = threadIdx.x; e < nr * nbp; e += blockDim.x) {
+            const int c = e / nr, r = e - c * nr;
             W[(rbeg + r) + (k0 + c) * ldw] = Ps[r + c * cp];
         }
     }

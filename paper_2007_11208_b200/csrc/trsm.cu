@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         // wait for X_j (tile rt)
         if (threadIdx.x == 0) {
             const unsigned* f = &p.sync[1 + j * ntiles + rt];
-            while (ld_acquire(f) == 0u) { __nanosleep(20); }
+            while (ld_acquire(f) == 0u) { __nanosleep(20); }   // (relaxed poll + fence measured slower here)
         }
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
