@@ -461,6 +461,16 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
         const bool need_lo = (D == 0) || (peek & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
         const bool need_up = (D != 0) && (peek & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
         T lo[16], up[16];
+        // Fig. 4 line 16 needs diag(gi), diag(gj) of every checked element: issue those loads with
+        // the tiles' (2 rows, 8 columns per thread) instead of after the mirror exchange
+        T drow[2], dcol[8];
+        const bool spd_peek = (peek & AS_FLAG_SPD_CANDIDATE) != 0;
+        if (spd_peek) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) drow[h] = (r0 + r_loc + h < n) ? diag[r0 + r_loc + h] : T(0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dcol[k] = (c0 + warp + 8 * k < n) ? diag[c0 + warp + 8 * k] : T(0);
+        }
         if (need_lo) load_tile_regs<T>(lo, A, lda, n, r0, c0, vec, interior);
         else {
 #pragma unroll
@@ -493,7 +503,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
             if (D != 0 && up[i] != T(0)) { upper_nz = true; ku_loc = max(ku_loc, (int)(D * kTile) + c - r); }
         }
         bool spd_dead = false;
-        if (alive & AS_FLAG_SPD_CANDIDATE) {
+        if (alive & AS_FLAG_SPD_CANDIDATE) {   // uniform (barriers inside)
             bool any = false;
 #pragma unroll
             for (int i = 0; i < 16; ++i) any |= (lo[i] != T(0)) || (D != 0 && up[i] != T(0));
@@ -511,7 +521,8 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
                 for (int i = 0; i < 16; ++i) {
                     const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
                     const long long gi = r0 + r, gj = c0 + c;
-                    if (gi >= n || gj >= n || gi <= gj) continue;
+                    // (a thread whose early peek already saw SPD dead has no diag values: nothing to decide)
+                    if (gi >= n || gj >= n || gi <= gj || !spd_peek) continue;
                     const T a = lo[i];                           // A(gi, gj)
                     const T b = up_s[r * kLD3 + c];              // A(gj, gi)
                     const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
@@ -520,7 +531,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
                     const T m = aa > ab ? aa : ab;
                     if (delta > tol && delta > tol * m) spd_dead = true;             // lines 13-14
                     if (aa >= max_diag) spd_dead = true;                              // line 15
-                    if (aa + ab >= diag[gi] + diag[gj]) spd_dead = true;             // line 16
+                    if (aa + ab >= drow[i & 1] + dcol[i >> 1]) spd_dead = true;      // line 16
                 }
             }
         }
