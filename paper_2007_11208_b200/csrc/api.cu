@@ -656,28 +656,34 @@ int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void
     const size_t es = dt == AS_F64 ? 8 : 4;
     cudaStream_t s = (cudaStream_t)stream;
     static std::mutex mu;
-    static std::map<std::tuple<int, int, int64_t, int64_t>, std::pair<void*, void*>> bufs;
+    // device staging for A, B and X (X separate from B: an in-place solve would exclude the
+    // speculative partitioned band path)
+    static std::map<std::tuple<int, int, int64_t, int64_t>, std::tuple<void*, void*, void*>> bufs;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
     auto key = std::make_tuple(dev, (int)dt, n, nrhs);
     auto it = bufs.find(key);
     if (it == bufs.end()) {
-        void *dA = nullptr, *dB = nullptr;
-        if (cudaMalloc(&dA, es * n * n) != cudaSuccess || cudaMalloc(&dB, es * n * nrhs) != cudaSuccess) {
+        void *dA = nullptr, *dB = nullptr, *dX = nullptr;
+        if (cudaMalloc(&dA, es * n * n) != cudaSuccess || cudaMalloc(&dB, es * n * nrhs) != cudaSuccess ||
+            cudaMalloc(&dX, es * n * nrhs) != cudaSuccess) {
             cudaGetLastError();
+            if (dA) cudaFree(dA);
+            if (dB) cudaFree(dB);
             return AS_ERR_CUDA_BASE + (int)cudaErrorMemoryAllocation;
         }
-        it = bufs.emplace(key, std::make_pair(dA, dB)).first;
+        it = bufs.emplace(key, std::make_tuple(dA, dB, dX)).first;
     }
-    void* dA = it->second.first;
-    void* dB = it->second.second;
+    void* dA = std::get<0>(it->second);
+    void* dB = std::get<1>(it->second);
+    void* dX = std::get<2>(it->second);
     int err = check(cudaMemcpy2DAsync(dA, es * n, A, es * lda, es * n, n, cudaMemcpyHostToDevice, s), "H2D A");
     if (!err) err = check(cudaMemcpy2DAsync(dB, es * n, B, es * ldb, es * n, nrhs, cudaMemcpyHostToDevice, s), "H2D B");
     if (err) return err;
-    int ret = solve_impl(dt, dA, n, n, dB, n, nrhs, dB, opt, rep, nullptr, nullptr, s, true);
+    int ret = solve_impl(dt, dA, n, n, dB, n, nrhs, dX, opt, rep, nullptr, nullptr, s, true);
     if (ret < 0) return ret;
-    err = check(cudaMemcpy2DAsync(X, es * ldb, dB, es * n, es * n, nrhs, cudaMemcpyDeviceToHost, s), "D2H X");
+    err = check(cudaMemcpy2DAsync(X, es * ldb, dX, es * n, es * n, nrhs, cudaMemcpyDeviceToHost, s), "D2H X");
     if (!err) err = check(cudaStreamSynchronize(s), "sync");
     return err ? err : ret;
 }
