@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
 
 #define STAMP(k) do { if (cta == 0 && threadIdx.x == 0) st->dbg_t[k] = gtimer(); } while (0)
     STAMP(0);
-    if (cta == 0 && threadIdx.x == 0) st->dbg_t[13] = clock64();
     // ---------------- F1: load the partition band and factor it (no pivoting)
     if (is_part) {
         {   // zero rows -K..a.m+K-1 (pads, out-of-band slots), then the band column by column:
@@ -224,7 +223,6 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                 });
         }
         __syncthreads();
-        if (cta == 0 && threadIdx.x == 0) st->dbg_t[15] = gtimer();
         if (threadIdx.x < 32) {
             // lane r (1..K) owns row j+r of the active window: multiplier + its K updates.  Entries
             // outside the band / partition are zero in LU, so padding kl, ku to K adds zero work.
@@ -259,7 +257,6 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
         }
         __syncthreads();
         STAMP(1);
-        if (cta == 0 && threadIdx.x == 0) st->dbg_t[14] = clock64();
         // ---------------- F2: spikes (kind 0 V, 1 W for A; 2 V', 3 W' for A^T), column q
         for (int e = threadIdx.x; e < 4 * K * a.m; e += blockDim.x) SP[e] = T(0);
         __syncthreads();
@@ -425,106 +422,177 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
                 T* CA = RY;                                             // (P-1) x K x kRedR
                 T* UU = RY + (int64_t)(P - 1) * K * kRedR;
                 T* DB = RY + (int64_t)2 * (P - 1) * K * kRedR;
-                T* tw = RT + (int64_t)warp * K * kRedR;
-                // out = x - M y   (K x Rr), one warp
-                auto wmv = [&](T* out, const T* x, const T* M, const T* y) {
-                    for (int e = lane; e < K * Rr; e += 32) {
-                        const int r = e / Rr, c = e % Rr;
-                        T s = T(0);
-#pragma unroll
-                        for (int k = 0; k < K; ++k) s += M[r * K + k] * y[k * kRedR + c];
-                        out[r * kRedR + c] = x[r * kRedR + c] - s;
+                // Parallel phases: every (interface i, row r, column c) entry is one thread's K-term
+                // dot product; a phase is a few block-wide passes separated by barriers.
+                // pass(out, x, M, y): out_i = x_i - M_i y_i for i in [i0, P-2]   (K x Rr each)
+                const int ne = K * Rr;
+                auto pass = [&](int i0, auto&& fn) {
+                    for (int e = threadIdx.x; e < (P - 1 - i0) * ne; e += blockDim.x) {
+                        const int i = i0 + e / ne, f = e % ne, r = f / Rr, c = f - (f / Rr) * Rr;
+                        fn(i, r, c);
                     }
-                    __syncwarp();
                 };
-                // A: c_i = gb_i - Q_i (gt_{i+1} - Y_i gb_i)
-                for (int i = warp; i <= P - 2; i += nw) {
+                auto dotM = [&](const T* M, const T* y, int r, int c) -> T {   // (M y)(r, c), tree sum
+                    T pr[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) pr[k] = M[r * K + k] * y[k * kRedR + c];
+#pragma unroll
+                    for (int h = 1; h < K; h *= 2)
+#pragma unroll
+                        for (int k = 0; k + h < K; k += 2 * h) pr[k] += pr[k + h];
+                    return pr[0];
+                };
+#define RSTAMP(k) do { if (nsolve == 2 && rdir == 0 && threadIdx.x == 0) st->dbg_t[k] = gtimer(); } while (0)
+                RSTAMP(11);
+                RSTAMP(13);
+                // A: c_i = gb_i - Q_i (gt_{i+1} - Y_i gb_i)      (UU: temporary)
+                pass(0, [&](int i, int r, int c) {
                     const T* R7 = RM + (int64_t)i * RSZ;
-                    wmv(tw, GT(i), R7 + 1 * K * K, GB(i));
-                    wmv(CA + (int64_t)i * K * kRedR, GB(i), R7 + 5 * K * K, tw);
-                }
+                    UU[(int64_t)i * K * kRedR + r * kRedR + c] = GT(i)[r * kRedR + c] - dotM(R7 + 1 * K * K, GB(i), r, c);
+                });
                 __syncthreads();
-                // B: a_i = c_i - M_i a_{i-1}   (serial, registers + shuffles)
-                if (warp * kCPW < Rr) {                 // column group of this warp
+                pass(0, [&](int i, int r, int c) {
+                    const T* R7 = RM + (int64_t)i * RSZ;
+                    CA[(int64_t)i * K * kRedR + r * kRedR + c] =
+                        GB(i)[r * kRedR + c] - dotM(R7 + 5 * K * K, UU + (int64_t)i * K * kRedR, r, c);
+                });
+                __syncthreads();
+                // serial chain  v_i = w_i - C_i v_{i -/+ 1}  (registers + shuffles; the next step's
+                // coefficients and right-hand side are loaded while the current step waits)
+                // one right-hand side: warp 0, lane = (row r = lane / 4, quarter q = lane % 4) holds
+                // columns 2q, 2q+1 of C_i's row r; a step is 2 products, a 2-level xor reduction and
+                // two shuffles that hand v_i to the lanes of the next step
+                auto chain1 = [&](T* V, int slot, bool fwd) {
+                    static_assert(K == 8 || K < 8, "");
+                    if (warp != 0) return;
+                    constexpr int KP = (K + 3) / 4;                    // columns per lane (K = 8: 2)
+                    const int r = lane >> 2, q = lane & 3;
+                    const bool act = r < K;
+                    const int i_first = fwd ? 0 : P - 2, i_last = fwd ? P - 2 : 0, step = fwd ? 1 : -1;
+                    T vpr[KP];
+                    const T v0 = (act && q == 0) ? V[(int64_t)i_first * K * kRedR + r * kRedR] : T(0);
+#pragma unroll
+                    for (int u = 0; u < KP; ++u) {
+                        const int k = q * KP + u;
+                        vpr[u] = __shfl_sync(0xffffffffu, v0, (k < K ? k : 0) * 4);
+                        if (k >= K) vpr[u] = T(0);
+                    }
+                    if (i_first == i_last) return;
+                    int i = i_first + step;
+                    auto ldc = [&](int ii, T (&mc)[KP], T& wc) {
+#pragma unroll
+                        for (int u = 0; u < KP; ++u) {
+                            const int k = q * KP + u;
+                            mc[u] = (act && k < K) ? RM[(int64_t)ii * RSZ + slot * K * K + r * K + k] : T(0);
+                        }
+                        wc = act ? V[(int64_t)ii * K * kRedR + r * kRedR] : T(0);
+                    };
+                    T mc[KP], wc;
+                    ldc(i, mc, wc);
+                    for (;;) {
+                        const bool more = i != i_last;
+                        const int inx = more ? i + step : i;
+                        T mn[KP], wn;
+                        ldc(inx, mn, wn);
+                        T pr = T(0);
+#pragma unroll
+                        for (int u = 0; u < KP; ++u) pr += mc[u] * vpr[u];
+                        pr += __shfl_xor_sync(0xffffffffu, pr, 1);
+                        pr += __shfl_xor_sync(0xffffffffu, pr, 2);
+                        const T v = wc - pr;
+                        if (act && q == 0) V[(int64_t)i * K * kRedR + r * kRedR] = v;
+#pragma unroll
+                        for (int u = 0; u < KP; ++u) {
+                            const int k = q * KP + u;
+                            const T t = __shfl_sync(0xffffffffu, v, (k < K ? k : 0) * 4);
+                            vpr[u] = k < K ? t : T(0);
+                        }
+                        if (!more) break;
+                        i = inx;
+#pragma unroll
+                        for (int u = 0; u < KP; ++u) mc[u] = mn[u];
+                        wc = wn;
+                    }
+                };
+                auto chain = [&](T* V, int slot, bool fwd) {
+                    if (Rr == 1) { chain1(V, slot, fwd); return; }
+                    if (warp * kCPW >= Rr) return;                       // column group of this warp
                     const int cb = warp * kCPW, Rw = min(kCPW, Rr - cb);
                     const bool act = lane < K * Rw;
                     const int r = act ? lane / Rw : 0, cl = act ? lane % Rw : 0, c = cb + cl;
-                    T ap = act ? CA[r * kRedR + c] : T(0);
-                    for (int i = 1; i <= P - 2; ++i) {
-                        const T* Mi = RM + (int64_t)i * RSZ + 6 * K * K;
-                        T s = T(0);
+                    const int i_first = fwd ? 0 : P - 2, i_last = fwd ? P - 2 : 0, step = fwd ? 1 : -1;
+                    T vp = act ? V[(int64_t)i_first * K * kRedR + r * kRedR + c] : T(0);
+                    if (i_first == i_last) return;
+                    int i = i_first + step;
+                    T mc[K], wc;
 #pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            const T ak = __shfl_sync(0xffffffffu, ap, k * Rw + cl);
-                            s += (act ? Mi[r * K + k] : T(0)) * ak;
-                        }
-                        T* ci = CA + (int64_t)i * K * kRedR;
-                        const T v = act ? ci[r * kRedR + c] - s : T(0);
-                        if (act) ci[r * kRedR + c] = v;
-                        ap = v;
+                    for (int k = 0; k < K; ++k) mc[k] = act ? RM[(int64_t)i * RSZ + slot * K * K + r * K + k] : T(0);
+                    wc = act ? V[(int64_t)i * K * kRedR + r * kRedR + c] : T(0);
+                    for (;;) {
+                        const bool more = i != i_last;
+                        const int inx = more ? i + step : i;
+                        T mn[K], wn;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) mn[k] = act ? RM[(int64_t)inx * RSZ + slot * K * K + r * K + k] : T(0);
+                        wn = act ? V[(int64_t)inx * K * kRedR + r * kRedR + c] : T(0);
+                        T pr[K];
+#pragma unroll
+                        for (int k = 0; k < K; ++k) pr[k] = mc[k] * __shfl_sync(0xffffffffu, vp, k * Rw + cl);
+#pragma unroll
+                        for (int h = 1; h < K; h *= 2)
+#pragma unroll
+                            for (int k = 0; k + h < K; k += 2 * h) pr[k] += pr[k + h];
+                        vp = wc - pr[0];
+                        if (act) V[(int64_t)i * K * kRedR + r * kRedR + c] = vp;
+                        if (!more) break;
+                        i = inx;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) mc[k] = mn[k];
+                        wc = wn;
                     }
-                }
+                };
+                // B: a_i = c_i - M_i a_{i-1}
+                chain(CA, 6, true);
                 __syncthreads();
-                // C: u_i = gb_i - Wb_i a_{i-1};  d_i = Si_i (gt_{i+1} - Y_i u_i)
-                for (int i = warp; i <= P - 2; i += nw) {
+                RSTAMP(14);
+                // C: u_i = gb_i - Wb_i a_{i-1};  d_i = Si_i (gt_{i+1} - Y_i u_i)   (CA reused as temporary
+                //    after the first pass)
+                pass(0, [&](int i, int r, int c) {
                     const T* R7 = RM + (int64_t)i * RSZ;
-                    T* ui = UU + (int64_t)i * K * kRedR;
-                    if (i > 0) wmv(ui, GB(i), R7 + 3 * K * K, CA + (int64_t)(i - 1) * K * kRedR);
-                    else {
-                        for (int e = lane; e < K * Rr; e += 32) { const int r = e / Rr, c = e % Rr; ui[r * kRedR + c] = GB(0)[r * kRedR + c]; }
-                        __syncwarp();
-                    }
-                    wmv(tw, GT(i), R7 + 1 * K * K, ui);
-                    T* di = DB + (int64_t)i * K * kRedR;
-                    for (int e = lane; e < K * Rr; e += 32) {
-                        const int r = e / Rr, c = e % Rr;
-                        T s = T(0);
-#pragma unroll
-                        for (int k = 0; k < K; ++k) s += R7[2 * K * K + r * K + k] * tw[k * kRedR + c];
-                        di[r * kRedR + c] = s;
-                    }
-                    __syncwarp();
-                }
+                    const T g = GB(i)[r * kRedR + c];
+                    UU[(int64_t)i * K * kRedR + r * kRedR + c] =
+                        i > 0 ? g - dotM(R7 + 3 * K * K, CA + (int64_t)(i - 1) * K * kRedR, r, c) : g;
+                });
                 __syncthreads();
-                // D: b_i = d_i - N_i b_{i+1}   (serial)
-                if (warp * kCPW < Rr) {
-                    const int cb = warp * kCPW, Rw = min(kCPW, Rr - cb);
-                    const bool act = lane < K * Rw;
-                    const int r = act ? lane / Rw : 0, cl = act ? lane % Rw : 0, c = cb + cl;
-                    T bp = act ? DB[(int64_t)(P - 2) * K * kRedR + r * kRedR + c] : T(0);
-                    for (int i = P - 3; i >= 0; --i) {
-                        const T* Ni = RM + (int64_t)i * RSZ + 4 * K * K;
-                        T s = T(0);
-#pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            const T bk = __shfl_sync(0xffffffffu, bp, k * Rw + cl);
-                            s += (act ? Ni[r * K + k] : T(0)) * bk;
-                        }
-                        T* di = DB + (int64_t)i * K * kRedR;
-                        const T v = act ? di[r * kRedR + c] - s : T(0);
-                        if (act) di[r * kRedR + c] = v;
-                        bp = v;
-                    }
-                }
+                pass(0, [&](int i, int r, int c) {
+                    const T* R7 = RM + (int64_t)i * RSZ;
+                    CA[(int64_t)i * K * kRedR + r * kRedR + c] =
+                        GT(i)[r * kRedR + c] - dotM(R7 + 1 * K * K, UU + (int64_t)i * K * kRedR, r, c);
+                });
                 __syncthreads();
+                pass(0, [&](int i, int r, int c) {
+                    const T* R7 = RM + (int64_t)i * RSZ;
+                    DB[(int64_t)i * K * kRedR + r * kRedR + c] = dotM(R7 + 2 * K * K, CA + (int64_t)i * K * kRedR, r, c);
+                });
+                __syncthreads();
+                // D: b_i = d_i - N_i b_{i+1}
+                chain(DB, 4, false);
+                __syncthreads();
+                RSTAMP(15);
                 // E: a_i = u_i - X_i b_i;  z_i = [a_i; b_i]
-                for (int i = warp; i <= P - 2; i += nw) {
+                pass(0, [&](int i, int r, int c) {
                     const T* R7 = RM + (int64_t)i * RSZ;
                     const T* bi = DB + (int64_t)i * K * kRedR;
-                    wmv(tw, UU + (int64_t)i * K * kRedR, R7, bi);
-                    for (int e = lane; e < K * Rr; e += 32) {
-                        const int r = e / Rr, c = e % Rr;
-                        scr[L.zz + ((int64_t)i * S + r) * kSpR + c0 + c] = tw[r * kRedR + c];
-                        scr[L.zz + ((int64_t)i * S + K + r) * kSpR + c0 + c] = bi[r * kRedR + c];
-                    }
-                    __syncwarp();
-                }
+                    scr[L.zz + ((int64_t)i * S + r) * kSpR + c0 + c] =
+                        UU[(int64_t)i * K * kRedR + r * kRedR + c] - dotM(R7, bi, r, c);
+                    scr[L.zz + ((int64_t)i * S + K + r) * kSpR + c0 + c] = bi[r * kRedR + c];
+                });
                 __syncthreads();
+                RSTAMP(12);
             }
             if (nsolve == 0 && threadIdx.x == 0) st->dbg_t[10] = gtimer();
         }
         gbar();
-        STAMP1(11);
         if (is_part) {
             // x_i = g_i - V_i t_{i+1} - W_i b_{i-1};  t_{i+1} = z_i[K:S], b_{i-1} = z_{i-1}[0:K]
             const T* V = SP + (int64_t)(dir * 2 + 0) * K * a.m;
@@ -550,7 +618,6 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
             }
             __syncthreads();
         }
-        STAMP1(12);
         ++nsolve;
     };
 

@@ -32,6 +32,3 @@ for i in range(a.calls):
 ts = AS.debug_timestamps()
 if ts and ts[0] is not None:
     print("stamps_us", [round(x, 1) if x is not None else None for x in ts])
-    raw = AS.debug_timestamps(raw=True)
-    print("raw", raw[13:16], "clock MHz(F1):", (raw[14] - raw[13]) / max(1, raw[1] - raw[0]) * 1e3,
-          "F1 load us:", (raw[15] - raw[0]) / 1e3, "F1 loop us:", (raw[1] - raw[15]) / 1e3)
