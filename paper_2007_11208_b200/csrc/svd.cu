@@ -34,6 +34,14 @@ AS_DEV T block_sum256(T v, T* sh) {
     return v;
 }
 
+// 1/sqrt(x): hardware approximation + two Newton steps (within ~1 ulp; x >= 1 here)
+AS_DEV double rsqrt_nr(double x) {
+    double y = rsqrt(x);
+    y = y * (1.5 - 0.5 * x * y * y);
+    return y * (1.5 - 0.5 * x * y * y);
+}
+AS_DEV float rsqrt_nr(float x) { return 1.0f / sqrtf(x); }
+
 // ------------------------------------------------------------------ setup
 // W = A, Y = B (n x nrhs, ld n)
 template <typename T>
@@ -171,7 +179,10 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const T tol = (T)n * Eps<T>::v;
     int my_rot = 0;
+    const bool stamp = (k == 0 && threadIdx.x == 0 && st->sweeps == 0);
+#define JSTAMP(q) do { if (stamp && r == 5) st->dbg_t[q] = gtimer(); } while (0)
     for (int r = 0; r < NB - 1; ++r) {
+        JSTAMP(0);
         const int s1 = k, s2 = NB - 1 - k;
         const int ba = s1 == 0 ? 0 : 1 + (s1 - 1 + r) % (NB - 1);
         const int bb = s2 == 0 ? 0 : 1 + (s2 - 1 + r) % (NB - 1);
@@ -181,17 +192,23 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             s_gc[threadIdx.x] = gc < n ? (int)gc : -1;
         }
         __syncthreads();
-        for (int c = 0; c < C2; ++c) {             // (no runtime 64-bit divisions in the staging loops)
-            const int gc = s_gc[c];
-            T* dst = Ms + (int64_t)c * n;
-            const T* src = M + (int64_t)(gc >= 0 ? gc : 0) * ldw;
-            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = gc >= 0 ? __ldcg(&src[i]) : T(0);
+        {   // stage the C2 columns: all of a thread's loads in flight together (latency-batched)
+            const int nn = (int)n;
+            batched<32, T>(
+                C2 * nn,
+                [&](int e) -> T {
+                    const int c = e / nn, i = e - c * nn;
+                    const int gc = s_gc[c];
+                    return gc >= 0 ? __ldcg(&M[(int64_t)gc * ldw + i]) : T(0);
+                },
+                [&](int e, T v) { Ms[e] = v; });
         }
         for (int c = 0; c < C2; ++c) {
             const int gc = s_gc[c];
             for (int64_t rr = threadIdx.x; rr < nrhs; rr += blockDim.x) Ys[c + rr * C2] = gc >= 0 ? __ldcg(&Y[gc + rr * n]) : T(0);
         }
         __syncthreads();
+        JSTAMP(1);
         // local round-robin over C2 columns: C2-1 sub-rounds of BS disjoint pairs, one warp per pair
         for (int sr = 0; sr < C2 - 1; ++sr) {
             for (int u = warp; u < BS; u += (int)(blockDim.x >> 5)) {
@@ -203,19 +220,40 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
                 if (s_gc[lp] > s_gc[lq]) { lp = lb; lq = la; }   // p < q by global column index
                 T* mp = Ms + (int64_t)lp * n;
                 T* mq = Ms + (int64_t)lq * n;
-                T al = T(0), be = T(0), ga = T(0);
-                for (int64_t i = lane; i < n; i += 32) { const T x = mp[i], y = mq[i]; al += x * x; be += y * y; ga += x * y; }
+                // alpha, beta, gamma with 4 independent partial sums per lane (the FMA chains are
+                // the latency of the pair; n is a multiple of 4 here or the tail is zero-padded)
+                const int nn = (int)n;
+                T al4[4] = {}, be4[4] = {}, ga4[4] = {};
+                for (int i0 = lane; i0 < nn; i0 += 128) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + 32 * u;
+                        if (i < nn) { const T x = mp[i], y = mq[i]; al4[u] += x * x; be4[u] += y * y; ga4[u] += x * y; }
+                    }
+                }
+                T al = (al4[0] + al4[1]) + (al4[2] + al4[3]);
+                T be = (be4[0] + be4[1]) + (be4[2] + be4[3]);
+                T ga = (ga4[0] + ga4[1]) + (ga4[2] + ga4[3]);
                 al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-                if (ga == T(0) || !((ga < T(0) ? -ga : ga) > tol * sqrt(al) * sqrt(be))) continue;
+                // rotation skipped when |gamma| <= tol sqrt(alpha beta) (Z14 reading)
+                const T sa = sqrt(al), sb = sqrt(be);
+                if (ga == T(0) || !((ga < T(0) ? -ga : ga) > tol * sa * sb)) continue;
                 ++my_rot;
                 const T zeta = (be - al) / (T(2) * ga);
-                const T t = (zeta >= T(0) ? T(1) : T(-1)) / ((zeta < T(0) ? -zeta : zeta) + sqrt(T(1) + zeta * zeta));
-                const T c = T(1) / sqrt(T(1) + t * t);
+                const T az = zeta < T(0) ? -zeta : zeta;
+                const T t = (zeta >= T(0) ? T(1) : T(-1)) / (az + sqrt(T(1) + zeta * zeta));
+                const T c = rsqrt_nr(T(1) + t * t);
                 const T sn = c * t;
-                for (int64_t i = lane; i < n; i += 32) {
-                    const T x = mp[i], y = mq[i];
-                    mp[i] = c * x - sn * y;
-                    mq[i] = sn * x + c * y;
+                for (int i0 = lane; i0 < nn; i0 += 128) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + 32 * u;
+                        if (i < nn) {
+                            const T x = mp[i], y = mq[i];
+                            mp[i] = c * x - sn * y;
+                            mq[i] = sn * x + c * y;
+                        }
+                    }
                 }
                 for (int64_t rr = lane; rr < nrhs; rr += 32) {
                     const T x = Ys[lp + rr * C2], y = Ys[lq + rr * C2];
@@ -225,6 +263,7 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             }
             __syncthreads();
         }
+        JSTAMP(2);
         for (int c = 0; c < C2; ++c) {
             const int gc = s_gc[c];
             if (gc < 0) continue;
@@ -233,8 +272,11 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
             for (int64_t rr = threadIdx.x; rr < nrhs; rr += blockDim.x) Y[gc + rr * n] = Ys[c + rr * C2];
         }
+        JSTAMP(3);
         grid_barrier(bar, (unsigned)(r + 1), (unsigned)P);
+        JSTAMP(4);
     }
+#undef JSTAMP
     if (lane == 0 && my_rot) atomicAdd(&st->rotated, my_rot);
 }
 
@@ -347,9 +389,8 @@ static void svd_pre_t(const Work& w, cudaStream_t s) {
     transpose_r_kernel<T><<<w.num_sms * 4, 256, 0, s>>>(W, w.ldw, w.n);
 }
 
-template <typename T>
-static void svd_sweep_t(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s) {
-    constexpr int BS = 4;
+template <typename T, int BS>
+static bool launch_block_sweep(const Work& w, cudaStream_t s) {
     const int64_t nb = (w.n + BS - 1) / BS;
     const int P = (int)((nb + 1) / 2);                     // NB = 2P blocks (one may be a dummy)
     const size_t smem = sizeof(T) * ((size_t)2 * BS * w.n + (size_t)2 * BS * std::max<int64_t>(w.nrhs, 1));
@@ -370,9 +411,19 @@ static void svd_sweep_t(const Work& w, cudaGraphConditionalHandle h, cudaStream_
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
-    } else {
-        coop_launch(jacobi_sweep_kernel<T>, w.num_sms, s, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
+        return true;
     }
+    return false;
+}
+
+// one sweep: column blocks of 4 (8 columns per CTA) when they fit in shared memory and on the
+// SMs, else the per-pair kernel
+template <typename T>
+static void svd_sweep_t(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s) {
+    // (blocks of 8 measured slower: the pair updates are shared-memory bandwidth bound and only
+    //  half as many CTAs take part)
+    if (!launch_block_sweep<T, 4>(w, s))
+        coop_launch(jacobi_sweep_kernel<T>, w.num_sms, s, (T*)w.W, w.ldw, w.n, (T*)w.yv, w.nrhs, w.st, w.bars + 1);
     sweep_check_kernel<<<1, 32, 0, s>>>(w.st, w.bars + 1, h);
 }
 
