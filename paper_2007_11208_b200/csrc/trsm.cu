@@ -21,7 +21,7 @@
 namespace as {
 
 constexpr int kTsThreads = 256;
-constexpr int kTsR = 16;          // max RHS columns per CTA tile
+constexpr int kTsR = 32;          // max RHS columns per CTA tile
 constexpr int kLDT = kNB + 1;     // padded smem leading dimension
 
 // ------------------------------------------------------------------ diagonal block inverse
@@ -93,19 +93,32 @@ struct TsArgs {
     int skip_if_singular;
 };
 
-// acc[i][c] (partial over k-quarter q) for row i = tid % 64, q = tid / 64
+// One 64 x 64 block times a 64 x RT tile.  RT == 1: thread (row i, k-quarter q) -> part[0]
+// (the four quarters are summed through shared memory).  RT >= 4: thread (row i, column
+// group g) owns columns g, g+4, ... over the full k range -> part[0 .. RT/4).
+constexpr int kLDX = kNB + 1;
+template <int RT> struct TsPer { static constexpr int v = RT == 1 ? 1 : RT / 4; };
 template <typename T, bool TRANSB, int RT>
-AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T (&part)[RT], int R) {
-    const int i = threadIdx.x % kNB, q = threadIdx.x / kNB;
+AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T (&part)[TsPer<RT>::v], int R) {
+    const int i = threadIdx.x % kNB, g = threadIdx.x / kNB;
+    constexpr int PER = TsPer<RT>::v;
 #pragma unroll
-    for (int c = 0; c < RT; ++c) part[c] = T(0);
+    for (int u = 0; u < PER; ++u) part[u] = T(0);
+    if (RT == 1) {
 #pragma unroll 4
-    for (int kk = 0; kk < kNB / 4; ++kk) {
-        const int k = q * (kNB / 4) + kk;
-        const T m = TRANSB ? Ms[k + i * kLDT] : Ms[i + k * kLDT];
+        for (int kk = 0; kk < kNB / 4; ++kk) {
+            const int k = g * (kNB / 4) + kk;
+            const T m = TRANSB ? Ms[k + i * kLDT] : Ms[i + k * kLDT];
+            part[0] += m * Xs[k];
+        }
+    } else {
+#pragma unroll 4
+        for (int k = 0; k < kNB; ++k) {
+            const T m = TRANSB ? Ms[k + i * kLDT] : Ms[i + k * kLDT];
 #pragma unroll
-        for (int c = 0; c < RT; ++c)
-            if (c < R) part[c] += m * Xs[k + c * kLDT];
+            for (int u = 0; u < PER; ++u)
+                if (g + 4 * u < R) part[u] += m * Xs[k + (g + 4 * u) * kLDX];
+        }
     }
 }
 
@@ -118,16 +131,24 @@ AS_DEV void cp_async_elem(T* smem, const T* gmem, bool ok) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(ok ? 4 : 0) : "memory");
 }
 
+// Shared memory: two T-block buffers (the second one receives Dinv_b during the last step, off
+// the critical path), the X_j tile, and for RT == 1 the k-quarter partials: <= 83 KB, so two
+// or three CTAs fit per SM and every block of an n <= 16384 solve is resident at once.
+template <typename T, int RT>
+constexpr size_t ts_smem() {
+    return sizeof(T) * (2 * kNB * kLDT + (size_t)kLDX * RT + (RT == 1 ? 4 * kNB : 0));
+}
+
 template <typename T, bool UPPER, bool TRANS, int RT>
 __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const DevArgs* args, const DevState* st) {
     if (p.slot >= 0 && ld_volatile_i32(&st->est_next) != p.slot) return;
     if (p.skip_if_singular && st->info != ~0ull) return;
+    constexpr int PER = TsPer<RT>::v;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* Mb0 = (T*)smem_raw;                      // kNB x kLDT: T block (double buffered: Mb0, Mb1)
     T* Mb1 = Mb0 + kNB * kLDT;
-    T* Xs = Mb1 + kNB * kLDT;                   // kNB x kLDT (R columns used): X_j tile
-    T* Red = Xs + kNB * kLDT;                   // 4 x kNB x RT partials
-    T* Ds = Red + 4 * kNB * RT;                 // kNB x kLDT: Dinv_b (prefetched off the critical path)
+    T* Xs = Mb1 + kNB * kLDT;                   // kLDX x RT: X_j tile (column c at c * kLDX)
+    T* Red = Xs + kLDX * RT;                    // RT == 1: 4 x kNB partials
     __shared__ unsigned s_ticket;
 
     const T* A = (const T*)(p.A ? p.A : args->A);
@@ -135,7 +156,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     const T* Dinv = (const T*)p.Dinv;
     const int64_t n = p.n;
     const int nblk = (int)((n + kNB - 1) / kNB);
-    const int ntiles = (p.nrhs + kTsR - 1) / kTsR;
+    const int ntiles = (p.nrhs + RT - 1) / RT;
     constexpr bool FWD = (!UPPER && !TRANS) || (UPPER && TRANS);
 
     if (threadIdx.x == 0) s_ticket = atomicAdd(&p.sync[0], 1u);
@@ -145,9 +166,9 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     const int b = FWD ? s : nblk - 1 - s;
     const int64_t ob = (int64_t)b * kNB;
     const int nbr = (int)min<int64_t>(kNB, n - ob);
-    const int c0 = rt * kTsR;
+    const int c0 = rt * RT;
     const int R = min(RT, p.nrhs - c0);
-    const int i = threadIdx.x % kNB, q = threadIdx.x / kNB;
+    const int i = threadIdx.x % kNB, g = threadIdx.x / kNB;
 
     // async staging of op(T)_{b j} (no-trans: A[b rows, j cols]; trans: A[j rows, b cols])
     auto stage = [&](T* dst, int sp) {
@@ -162,24 +183,30 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (s > 0) stage(Mb0, 0);
-    {   // Dinv_b prefetch
+    auto stage_dinv = [&](T* dst) {
         const T* D = Dinv + (int64_t)b * kNB * kNB;
-        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) Ds[(e % kNB) + (e / kNB) * kLDT] = D[e];
-    }
-    // acc = B_b (only q == 0 threads keep it)
-    T acc[RT];
+        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) cp_async_elem(dst + (e % kNB) + (e / kNB) * kLDT, D + e, true);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    T* Ds = (s & 1) ? Mb1 : Mb0;               // the buffer step s would use (free after step s-1)
+    if (s > 0) stage(Mb0, 0);
+    else stage_dinv(Ds);
+    // acc = B_b for my (row, columns)
+    T acc[PER];
 #pragma unroll
-    for (int c = 0; c < RT; ++c) acc[c] = (q == 0 && c < R && i < nbr) ? X[(ob + i) + (c0 + c) * p.ldx] : T(0);
+    for (int u = 0; u < PER; ++u) {
+        const int c = RT == 1 ? 0 : g + 4 * u;
+        acc[u] = ((RT > 1 || g == 0) && c < R && i < nbr) ? X[(ob + i) + (c0 + c) * p.ldx] : T(0);
+    }
 
-    T part[RT];
+    T part[PER];
     for (int sp = 0; sp < s; ++sp) {
         const int j = FWD ? sp : nblk - 1 - sp;
         const int64_t oj = (int64_t)j * kNB;
         const int nbj = (int)min<int64_t>(kNB, n - oj);
         T* Ms = (sp & 1) ? Mb1 : Mb0;
         if (sp + 1 < s) stage((sp & 1) ? Mb0 : Mb1, sp + 1);
-        else asm volatile("cp.async.commit_group;" ::: "memory");
+        else stage_dinv(Ds);                    // last step: Dinv_b into the free buffer
         // wait for X_j (tile rt)
         if (threadIdx.x == 0) {
             const unsigned* f = &p.sync[1 + j * ntiles + rt];
@@ -189,40 +216,40 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         __syncthreads();
         for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
             const int r = e % kNB, c = e / kNB;
-            Xs[r + c * kLDT] = (r < nbj && c < R) ? __ldcg(&X[(oj + r) + (c0 + c) * p.ldx]) : T(0);
+            Xs[r + c * kLDX] = (r < nbj && c < R) ? __ldcg(&X[(oj + r) + (c0 + c) * p.ldx]) : T(0);
         }
         __syncthreads();
-        if (!TRANS) block_product<T, false, RT>(Ms, Xs, part, R);
-        else block_product<T, true, RT>(Ms, Xs, part, R);
+        block_product<T, TRANS, RT>(Ms, Xs, part, R);
+        if (RT == 1) {
+            Red[g * kNB + i] = part[0];
+            __syncthreads();
+            if (g == 0) acc[0] -= (Red[i] + Red[kNB + i]) + (Red[2 * kNB + i] + Red[3 * kNB + i]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < RT; ++c) Red[(q * RT + c) * kNB + i] = part[c];
-        __syncthreads();
-        if (q == 0) {
-#pragma unroll
-            for (int c = 0; c < RT; ++c)
-                acc[c] -= (Red[(0 * RT + c) * kNB + i] + Red[(1 * RT + c) * kNB + i]) +
-                          (Red[(2 * RT + c) * kNB + i] + Red[(3 * RT + c) * kNB + i]);
+            for (int u = 0; u < PER; ++u) acc[u] -= part[u];
+            __syncthreads();                    // Ms / Xs reused by the next step
         }
     }
     // X_b = Dinv_b * acc  (trans: Dinv_b^T)
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    if (q == 0) {
 #pragma unroll
-        for (int c = 0; c < RT; ++c) Xs[i + c * kLDT] = acc[c];
+    for (int u = 0; u < PER; ++u) {
+        const int c = RT == 1 ? 0 : g + 4 * u;
+        if (RT > 1 || g == 0) Xs[i + c * kLDX] = acc[u];
     }
     __syncthreads();
-    if (!TRANS) block_product<T, false, RT>(Ds, Xs, part, R);
-    else block_product<T, true, RT>(Ds, Xs, part, R);
+    block_product<T, TRANS, RT>(Ds, Xs, part, R);
+    if (RT == 1) {
+        Red[g * kNB + i] = part[0];
+        __syncthreads();
+        if (g == 0 && i < nbr) X[(ob + i) + c0 * p.ldx] = (Red[i] + Red[kNB + i]) + (Red[2 * kNB + i] + Red[3 * kNB + i]);
+    } else if (i < nbr) {
 #pragma unroll
-    for (int c = 0; c < RT; ++c) Red[(q * RT + c) * kNB + i] = part[c];
-    __syncthreads();
-    if (q == 0 && i < nbr) {
-#pragma unroll
-        for (int c = 0; c < RT; ++c)
-            if (c < R)
-                X[(ob + i) + (c0 + c) * p.ldx] = (Red[(0 * RT + c) * kNB + i] + Red[(1 * RT + c) * kNB + i]) +
-                                                 (Red[(2 * RT + c) * kNB + i] + Red[(3 * RT + c) * kNB + i]);
+        for (int u = 0; u < PER; ++u) {
+            const int c = g + 4 * u;
+            if (c < R) X[(ob + i) + (c0 + c) * p.ldx] = part[u];
+        }
     }
     __syncthreads();   // release is cumulative over the CTA's X stores ordered by this barrier
     if (threadIdx.x == 0) st_release(&p.sync[1 + b * ntiles + rt], 1u);
@@ -264,24 +291,27 @@ template <typename T>
 static void trsm_dispatch(const TsArgs& p, bool upper, bool trans, const DevArgs* args, const DevState* st,
                           cudaStream_t s) {
     const int nblk = (int)((p.n + kNB - 1) / kNB);
-    const int ntiles = (p.nrhs + kTsR - 1) / kTsR;
-    auto go = [&](auto kern, int rt) {
-        const size_t smem = sizeof(T) * (4 * kNB * kLDT + 4 * kNB * rt);
+    auto go = [&](auto kern, int rt, size_t smem) {
+        const int ntiles = (p.nrhs + rt - 1) / rt;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk * ntiles, kTsThreads, smem, s>>>(p, args, st);
     };
-    auto by_r = [&](auto k1, auto k4, auto k16) {
-        if (p.nrhs == 1) go(k1, 1);
-        else if (p.nrhs <= 4) go(k4, 4);
-        else go(k16, kTsR);
+    auto by_r = [&](auto k1, auto k4, auto k16, auto k32) {
+        if (p.nrhs == 1) go(k1, 1, ts_smem<T, 1>());
+        else if (p.nrhs <= 4) go(k4, 4, ts_smem<T, 4>());
+        else if (p.nrhs <= 16) go(k16, 16, ts_smem<T, 16>());
+        else go(k32, kTsR, ts_smem<T, kTsR>());
     };
+#define AS_TS(U, TR) trsm_sf_kernel<T, U, TR, 1>, trsm_sf_kernel<T, U, TR, 4>, trsm_sf_kernel<T, U, TR, 16>, \
+                     trsm_sf_kernel<T, U, TR, kTsR>
     if (upper) {
-        if (trans) by_r(trsm_sf_kernel<T, true, true, 1>, trsm_sf_kernel<T, true, true, 4>, trsm_sf_kernel<T, true, true, kTsR>);
-        else by_r(trsm_sf_kernel<T, true, false, 1>, trsm_sf_kernel<T, true, false, 4>, trsm_sf_kernel<T, true, false, kTsR>);
+        if (trans) by_r(AS_TS(true, true));
+        else by_r(AS_TS(true, false));
     } else {
-        if (trans) by_r(trsm_sf_kernel<T, false, true, 1>, trsm_sf_kernel<T, false, true, 4>, trsm_sf_kernel<T, false, true, kTsR>);
-        else by_r(trsm_sf_kernel<T, false, false, 1>, trsm_sf_kernel<T, false, false, 4>, trsm_sf_kernel<T, false, false, kTsR>);
+        if (trans) by_r(AS_TS(false, true));
+        else by_r(AS_TS(false, false));
     }
+#undef AS_TS
 }
 
 void launch_trsm(int dtype, const void* A, int64_t lda, const void* Dinv, bool upper, bool trans, void* X,
