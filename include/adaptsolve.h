@@ -186,6 +186,13 @@ void as_set_exec_mode(int eager);
  * at phase boundaries (out: 16 values; 0 = not recorded). */
 int as_debug_timestamps(unsigned long long* out16);
 
+/* Diagnostics (only with the environment variable AS_LU_TRACE set when the library loads):
+ * per 128-column LU block k, slots 4k+0 trailing GEMM (main stream), 4k+1 panel 1, 4k+2 panel 2,
+ * 4k+3 look-ahead GEMM; tmin = first CTA start, tmax = last CTA end (%globaltimer ns) of the last
+ * factorization.  Host arrays of `cap` entries.  Returns the number of slots written, or -1 when
+ * tracing is off. */
+int as_debug_lu_trace(unsigned long long* tmin, unsigned long long* tmax, int cap);
+
 /* Roofline denominator probe (benchmark only, not part of a solve): fp64
  * tensor-core (DMMA) throughput in TFLOP/s of a register-resident MMA loop. */
 double as_measure_fp64_peak(int iters, void* stream);

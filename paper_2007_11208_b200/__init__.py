@@ -37,7 +37,7 @@ ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
            "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
            "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
-           "as_set_exec_mode", "as_debug_timestamps", "as_bench_gemm")
+           "as_set_exec_mode", "as_debug_timestamps", "as_debug_lu_trace", "as_bench_gemm")
 
 
 class Options(C.Structure):
@@ -224,6 +224,27 @@ def bench_gemm(M, N, K, dtype_code=AS_F64, trans_b=False, iters=5) -> float:
     return float(_lib.as_bench_gemm(dtype_code, M, N, K, int(trans_b), iters))
 _lib.as_debug_timestamps.argtypes = [P]
 _lib.as_debug_timestamps.restype = C.c_int
+_lib.as_debug_lu_trace.argtypes = [P, P, C.c_int]
+_lib.as_debug_lu_trace.restype = C.c_int
+
+
+def debug_lu_trace():
+    """[(kind, block, start_us, end_us)] of the last LU factorization (AS_LU_TRACE=1), or None."""
+    cap = 2048
+    lo, hi = (C.c_ulonglong * cap)(), (C.c_ulonglong * cap)()
+    cnt = _lib.as_debug_lu_trace(lo, hi, cap)
+    if cnt <= 0:
+        return None
+    starts = [lo[i] for i in range(cnt) if lo[i] != 0xFFFFFFFFFFFFFFFF]
+    if not starts:
+        return None
+    t0 = min(starts)
+    kinds = ["gemm", "panel1", "panel2", "gemm_la"]
+    out = []
+    for i in range(cnt):
+        if lo[i] != 0xFFFFFFFFFFFFFFFF and hi[i]:
+            out.append((kinds[i % 4], i // 4, (lo[i] - t0) / 1e3, (hi[i] - t0) / 1e3))
+    return out
 
 
 def debug_timestamps(raw: bool = False):

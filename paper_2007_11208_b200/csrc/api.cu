@@ -288,7 +288,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.flags_ts = (unsigned*)take(4 * w.flags_ts_len);
     w.bars_len = 8 + nblk + 8;
     w.bars = (unsigned*)take(4 * w.bars_len);
-    w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * kNB + es * 2 * kNB);
+    w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * 128 + es * 2 * 128);   // LU panel slots, rowbuf, diagbuf (128-wide)
     return off;
 }
 
@@ -784,6 +784,11 @@ double as_bench_gemm(int dtype, int64_t M, int64_t N, int64_t K, int trans_b, in
     cudaEventDestroy(e1);
     cudaFree(A); cudaFree(B); cudaFree(Cm);
     return 2.0 * (double)M * N * K * iters / (ms * 1e-3) / 1e12;
+}
+
+int as_debug_lu_trace(unsigned long long* tmin, unsigned long long* tmax, int cap) {
+    if (!tmin || !tmax || cap <= 0) return -1;
+    return as::lu_trace_copy(tmin, tmax, cap);
 }
 
 int as_debug_timestamps(unsigned long long* out16) {

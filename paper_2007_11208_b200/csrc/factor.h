@@ -5,6 +5,7 @@
 
 namespace as {
 void launch_copy_norm(const Work& w, bool with_perm, cudaStream_t s); // W = A, anorm (+ perm = id)
+int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap);  // lu.cu diagnostics
 void launch_lu_factor(const Work& w, cudaStream_t s);                 // lu.cu                 // W = L\U, ipiv, perm, Dinv0/1, anorm
 void launch_lu_solve(const Work& w, SyncAlloc& sa, cudaStream_t s);   // X = A^{-1} B
 void launch_chol_factor(const Work& w, cudaStream_t s);               // W = L (lower), anorm, chol_failed

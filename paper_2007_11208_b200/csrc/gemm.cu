@@ -312,6 +312,7 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     using namespace d2;
     if (g.skip && *g.skip) return;
+    if (g.trace_min && threadIdx.x == 0) atomicMin(g.trace_min, gtimer());
     const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
     if (g.lower_only && n0 > m0 + BM - 1) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
             }
         }
     }
+    if (g.trace_max && threadIdx.x == 0) atomicMax(g.trace_max, gtimer());
 }
 
 // ------------------------------------------------------------------ fp64 tensor peak probe

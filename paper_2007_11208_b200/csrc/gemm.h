@@ -14,6 +14,8 @@ struct GemmArgs {
     const int* skip;        // device flag: kernel returns at once if *skip != 0
     bool one_per_sm;        // reserve shared memory so only one GEMM CTA fits per SM (room for a
                             // concurrently running cooperative panel kernel)
+    unsigned long long* trace_min = nullptr;   // diagnostics: first CTA start / last CTA end
+    unsigned long long* trace_max = nullptr;   // (%globaltimer, AS_LU_TRACE only)
 };
 
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s);

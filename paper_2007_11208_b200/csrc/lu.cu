@@ -31,8 +31,30 @@
 namespace as {
 
 constexpr int kPT = 256;     // panel threads
-constexpr int kPW = 64;      // panel width
-constexpr int kBW = 128;     // block width (two panels)
+constexpr int kPW = 128;     // panel width (= block width: one cooperative panel per block, so the
+                             // look-ahead chain is panel + L11 inverse only)
+constexpr int kBW = 128;     // block width
+constexpr int kHalf = 64;    // U12 and Dinv work in 64-row halves of a block
+
+// ---- diagnostics: per-block timeline of the factorization (AS_LU_TRACE=1; %globaltimer)
+// slots per 128-column block k: 0 main-stream trailing GEMM, 1 panel 1, 2 panel 2, 3 look-ahead GEMM
+constexpr int kTraceBlocks = 512;
+struct LuTrace {
+    unsigned long long* tmin = nullptr;   // [4 * kTraceBlocks] first start
+    unsigned long long* tmax = nullptr;   // [4 * kTraceBlocks] last end
+};
+static LuTrace& lu_trace() {
+    static LuTrace t;
+    static bool init = false;
+    if (!init) {
+        init = true;
+        if (getenv("AS_LU_TRACE")) {
+            cudaMalloc(&t.tmin, sizeof(unsigned long long) * 4 * kTraceBlocks);
+            cudaMalloc(&t.tmax, sizeof(unsigned long long) * 4 * kTraceBlocks);
+        }
+    }
+    return t;
+}
 
 struct __align__(32) PSlot {
     double v;
@@ -87,8 +109,10 @@ AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, in
 template <typename T>
 __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
                                                             int64_t* ipiv, DevState* st, PSlot* slots, T* rowbuf,
-                                                            T* diagbuf, unsigned long long seq_base, int use_smem) {
+                                                            T* diagbuf, unsigned long long seq_base, int use_smem,
+                                                            unsigned long long* tr_min, unsigned long long* tr_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
     const int P = gridDim.x, cta = blockIdx.x;
     const int64_t m = n - k0;
     const int64_t chunk = (m + P - 1) / P;
@@ -258,6 +282,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         }
     }
     if (threadIdx.x == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
+    if (tr_max && threadIdx.x == 0) atomicMax(tr_max, gtimer());
 }
 
 // ------------------------------------------------------------------ laswp
@@ -333,7 +358,11 @@ __global__ void __launch_bounds__(256) laswp3_kernel(T* W, int64_t ldw, int64_t 
 // slot: the U12 product below and the final GETRS / GECON forward substitutions use it.  Later
 // interchanges only move rows below the panel, so the block is final once the panel is.
 template <typename T>
-__global__ void __launch_bounds__(256) lu_linv_kernel(const T* W, int64_t ldw, int64_t k0, int nbp, T* Dinv) {
+__global__ void __launch_bounds__(256) lu_linv_kernel(const T* W, int64_t ldw, int64_t k0b, int nbpb, T* Dinv) {
+    // CTA h inverts the diagonal 64 x 64 block of rows k0b + 64 h .. of the panel
+    const int64_t k0 = k0b + (int64_t)blockIdx.x * kB64;
+    const int nbp = min(kB64, nbpb - (int)blockIdx.x * kB64);
+    if (nbp <= 0) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* L = (T*)smem_raw;
     T* X = L + kB64 * kB64LD;
@@ -394,6 +423,7 @@ __global__ void __launch_bounds__(256) u12v3_kernel(T* W, int64_t ldw, int64_t r
 // ------------------------------------------------------------------ host driver
 struct LuStreams {
     cudaStream_t hi = nullptr;
+    cudaStream_t side = nullptr;   // interchanges into the finished L columns (off the critical path)
     cudaEvent_t ev[64];
     int next = 0;
     int prio_hi = 0;
@@ -406,6 +436,7 @@ static LuStreams& lu_streams() {
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         L.prio_hi = hi;
         cudaStreamCreateWithPriority(&L.hi, cudaStreamNonBlocking, hi);
+        cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, lo);
         for (auto& e : L.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     }
     return L;
@@ -437,7 +468,12 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
     attr[na].id = cudaLaunchAttributePriority; attr[na].val.priority = prio; ++na;
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, slots, rowbuf, diagbuf, seq_base, use_smem);
+    LuTrace& tr = lu_trace();
+    const int slot = (int)(k0 / kBW) * 4 + ((k0 % kBW) ? 2 : 1);
+    unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
+    unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
+    cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, slots, rowbuf, diagbuf, seq_base, use_smem,
+                       tmn, tmx);
 }
 
 template <typename T>
@@ -453,7 +489,7 @@ template <typename T>
 static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
     const int smem = (int)(sizeof(T) * (2 * kB64 * kB64LD + 3 * 256));
     cudaFuncSetAttribute(lu_linv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    lu_linv_kernel<T><<<1, 256, smem, s>>>((const T*)w.W, w.ldw, k0, nbp, (T*)w.Dinv0);
+    lu_linv_kernel<T><<<(nbp + kB64 - 1) / kB64, 256, smem, s>>>((const T*)w.W, w.ldw, k0, nbp, (T*)w.Dinv0);
 }
 
 template <typename T>
@@ -467,7 +503,7 @@ static void u12_launch(const Work& w, int64_t r0, int nb, int64_t c0, int64_t c1
 
 template <typename T>
 static void gemm_launch(const Work& w, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, cudaStream_t s,
-                        int prio, bool one_per_sm = false) {
+                        int prio, bool one_per_sm = false, int trace_slot = -1) {
     (void)prio;
     if (M <= 0 || N <= 0 || K <= 0) return;
     T* W = (T*)w.W;
@@ -478,6 +514,11 @@ static void gemm_launch(const Work& w, int64_t r0, int64_t c0, int64_t k0, int64
     g.B = W + k0 + c0 * ldw; g.ldb = ldw; g.TB = false;
     g.C = W + r0 + c0 * ldw; g.ldc = ldw;
     g.one_per_sm = one_per_sm;
+    LuTrace& tr = lu_trace();
+    if (tr.tmin && trace_slot >= 0 && trace_slot < 4 * kTraceBlocks) {
+        g.trace_min = tr.tmin + trace_slot;
+        g.trace_max = tr.tmax + trace_slot;
+    }
     launch_gemm_minus(w.dtype, g, s);
 }
 
@@ -487,7 +528,7 @@ static void block_panels(const Work& w, int64_t k0, int bw, int prio, cudaStream
     const int64_t n = w.n;
     const int p1 = std::min(kPW, bw);
     // sequence numbers of the panel exchange grow monotonically with the panel's column
-    panel_launch<T>(w, k0, p1, (unsigned long long)(k0 / kPW) * 128ull, prio, s);
+    panel_launch<T>(w, k0, p1, (unsigned long long)(k0 / kPW) * 256ull, prio, s);
     linv_launch<T>(w, k0, p1, s);
     if (bw > p1) {
         const int p2 = bw - p1;
@@ -495,7 +536,7 @@ static void block_panels(const Work& w, int64_t k0, int bw, int prio, cudaStream
         laswp_launch<T>(w, k0, p1, k0 + p1, k0 + bw, 0, 0, false, s);
         u12_launch<T>(w, k0, p1, k0 + p1, k0 + bw, s);
         gemm_launch<T>(w, k0 + p1, k0 + p1, k0, n - k0 - p1, p2, p1, s, prio);
-        panel_launch<T>(w, k0 + p1, p2, (unsigned long long)((k0 + p1) / kPW) * 128ull, prio, s);
+        panel_launch<T>(w, k0 + p1, p2, (unsigned long long)((k0 + p1) / kPW) * 256ull, prio, s);
         linv_launch<T>(w, k0 + p1, p2, s);
     }
 }
@@ -505,24 +546,35 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
     const int64_t n = w.n;
     launch_copy_norm(w, true, s);
     cudaMemsetAsync(w.cand, 0, sizeof(PSlot) * 1024, s);       // panel exchange slots (sequence numbers)
+    if (lu_trace().tmin) {
+        cudaMemsetAsync(lu_trace().tmin, 0xFF, sizeof(unsigned long long) * 4 * kTraceBlocks, s);
+        cudaMemsetAsync(lu_trace().tmax, 0, sizeof(unsigned long long) * 4 * kTraceBlocks, s);
+    }
     LuStreams& LS = lu_streams();
     // Look-ahead: next block's panels on a high-priority stream beside the bulk GEMM (measured
     // ~10% on C5; the gang-scheduled cooperative panel only partly overlaps).
     const bool lookahead = n >= 2048 && getenv("AS_LU_NO_LOOKAHEAD") == nullptr;
     int evi = 0;
     auto ev = [&]() { return LS.ev[(evi++) % 64]; };
+    bool side_used = false;
     // first block's panels
     block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, s);
     for (int64_t k0 = 0; k0 < n; k0 += kBW) {
         const int bw = (int)std::min<int64_t>(kBW, n - k0);
-        const int p1 = std::min(kPW, bw);
+        const int p1 = std::min(kHalf, bw);
         const int64_t kn = k0 + bw;             // next block start
-        // swaps of this block into all other columns (+ perm)
-        // panel-1 swaps: columns [0, k0) and [kn, n)  (block's second half already done)
-        // panel-2 swaps: columns [0, k0+p1) and [kn, n)
-        laswp_launch<T>(w, k0, p1, 0, k0, kn, n, false, s);
-        if (bw > p1) laswp_launch<T>(w, k0 + p1, bw - p1, 0, k0 + p1, kn, n, false, s);
-        laswp_launch<T>(w, k0, bw, 0, 0, 0, 0, true, s);        // row permutation: all bw swaps
+        // the block's interchanges into all other columns (the panel already swapped its own):
+        // the finished L columns [0, k0) on the side stream (nothing reads them before the
+        // solve; the side stream keeps the blocks' order), the trailing columns [kn, n) and
+        // the row permutation on the critical path
+        if (k0 > 0) {
+            cudaEvent_t el = ev();
+            cudaEventRecord(el, s);
+            cudaStreamWaitEvent(LS.side, el, 0);
+            laswp_launch<T>(w, k0, bw, 0, k0, 0, 0, false, LS.side);
+            side_used = true;
+        }
+        laswp_launch<T>(w, k0, bw, kn, n, 0, 0, true, s);       // + row permutation
         if (kn >= n) break;
         // U12 = L11^{-1} A12 with L11 = [La 0; Lb Lc] in 64-row halves: Utop = La^{-1} Atop,
         // Abot -= Lb Utop (DMMA), Ubot = Lc^{-1} Abot
@@ -539,9 +591,10 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
             cudaEvent_t e0 = ev();
             cudaEventRecord(e0, s);
             cudaStreamWaitEvent(LS.hi, e0, 0);
-            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi);
+            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
             block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
-            gemm_launch<T>(w, kn, kn + nbw, k0, M, n - kn - nbw, bw, s, 0, getenv("AS_LU_ONE_PER_SM") != nullptr);
+            gemm_launch<T>(w, kn, kn + nbw, k0, M, n - kn - nbw, bw, s, 0, getenv("AS_LU_ONE_PER_SM") != nullptr,
+                           (int)(k0 / kBW) * 4 + 0);
             cudaEvent_t e1 = ev();
             cudaEventRecord(e1, LS.hi);
             cudaStreamWaitEvent(s, e1, 0);
@@ -550,8 +603,24 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
             block_panels<T>(w, kn, nbw, LS.prio_hi, s);
         }
     }
+    if (side_used) {
+        cudaEvent_t ej = ev();
+        cudaEventRecord(ej, LS.side);
+        cudaStreamWaitEvent(s, ej, 0);
+    }
     // Dinv0 (unit-L diagonal block inverses) was written panel by panel
     launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
+}
+
+// host copy of the last factorization's trace (diagnostics); returns the slot count or -1
+int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap) {
+    LuTrace& tr = lu_trace();
+    if (!tr.tmin) return -1;
+    const int cnt = std::min(cap, 4 * kTraceBlocks);
+    cudaDeviceSynchronize();
+    cudaMemcpy(out_min, tr.tmin, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
+    cudaMemcpy(out_max, tr.tmax, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
+    return cnt;
 }
 
 void launch_lu_factor(const Work& w, cudaStream_t s) {
