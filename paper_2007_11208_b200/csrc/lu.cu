@@ -420,6 +420,126 @@ __global__ void __launch_bounds__(256) u12v3_kernel(T* W, int64_t ldw, int64_t r
     }
 }
 
+// ------------------------------------------------------------------ fused interchanges + U12
+// For the trailing columns [c0, c1) of block k0 (bw <= 128 rows, one CTA per 32 columns):
+//   1. the block's bw interchanges, composed into a permutation of S = block rows U targets
+//      (each row of S tracked through the swap sequence in parallel, as in laswp3);
+//   2. every moved value gathered from its source row before any is written;
+//   3. U12 = L11^{-1} A12 on the new block rows with L11 = [La 0; Lb Lc] in 64-row halves:
+//      Utop = La^{-1} Atop, Abot -= Lb Utop, Ubot = Lc^{-1} Abot (La^{-1}, Lc^{-1}: Dinv0).
+// This replaces laswp + u12 + gemm + u12 on the critical path between two panels.
+constexpr int kSUC = 32;
+constexpr int kSULD = kBW + 1;           // column stride of the column-major row buffers
+template <typename T>
+__global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_t k0, int bw, int64_t c0, int64_t c1,
+                                                      const int64_t* ipiv, const T* Dinv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* AiT = (T*)smem_raw;               // La^{-1} column-major (element (r, k) at r + 64 k)
+    T* LbT = AiT + kB64 * kB64;          // Lb
+    T* CiT = LbT + kB64 * kB64;          // Lc^{-1}
+    T* Bn = CiT + kB64 * kB64;           // [kSUC][kSULD]: column c of the block rows after the interchanges
+    T* Ex = Bn + kSUC * kSULD;           // [kSUC][kSULD]: values for the rows leaving the block
+    __shared__ int64_t piv[kBW];
+    __shared__ int64_t srow[2 * kBW];    // source rows: block positions 0..bw-1, then leaving rows
+    __shared__ int64_t edst[kBW];
+    __shared__ int s_ne;
+    const int64_t cc0 = c0 + (int64_t)blockIdx.x * kSUC;
+    const int nc = (int)min<int64_t>(kSUC, c1 - cc0);
+    if (nc <= 0) return;
+    const int p1 = min(kB64, bw), p2 = bw - p1;
+    if (threadIdx.x == 0) s_ne = 0;
+    for (int q = threadIdx.x; q < bw; q += blockDim.x) piv[q] = ipiv[k0 + q];
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * bw; t += blockDim.x) {
+        int64_t x;
+        if (t < bw) x = k0 + t;
+        else {
+            x = piv[t - bw];
+            if (x < k0 + bw) continue;
+            bool first = true;
+            for (int q = 0; q < t - bw; ++q) first = first && (piv[q] != x);
+            if (!first) continue;
+        }
+        int64_t pos = x;
+        for (int q = 0; q < bw; ++q) {
+            const int64_t r = k0 + q, tq = piv[q];
+            if (pos == r) pos = tq;
+            else if (pos == tq) pos = r;
+        }
+        if (pos < k0 + bw) srow[pos - k0] = x;
+        else { const int e = atomicAdd(&s_ne, 1); edst[e] = pos; srow[bw + e] = x; }
+    }
+    for (int e = threadIdx.x; e < kSUC * kSULD; e += blockDim.x) Bn[e] = T(0);   // short blocks / columns
+    __syncthreads();
+    const int ne = s_ne, R = bw + ne;
+    // every source value before any store: consecutive threads read consecutive (mostly
+    // contiguous) source rows of one column; then the triangular blocks (contiguous copies)
+    batched<16, T>(
+        R * nc + 3 * kB64 * kB64,
+        [&](int e) -> T {
+            if (e < R * nc) {
+                const int c = e / R, row = e - c * R;
+                return W[srow[row] + (cc0 + c) * ldw];
+            }
+            const int f = e - R * nc, which = f >> 12, g = f & 4095, r = g & 63, k = g >> 6;
+            if (which == 0) return Dinv[(k0 / kB64) * (int64_t)kB64 * kB64 + g];
+            if (p2 <= 0) return T(0);
+            if (which == 1) return (r < p2) ? W[(k0 + kB64 + r) + (k0 + k) * ldw] : T(0);
+            return Dinv[(k0 / kB64 + 1) * (int64_t)kB64 * kB64 + g];
+        },
+        [&](int e, T v) {
+            if (e < R * nc) {
+                const int c = e / R, row = e - c * R;
+                if (row < bw) Bn[c * kSULD + row] = v;
+                else Ex[c * kSULD + row - bw] = v;
+            } else {
+                AiT[e - R * nc] = v;                       // AiT, LbT, CiT are contiguous
+            }
+        });
+    __syncthreads();
+    // rows leaving the block
+    for (int e = threadIdx.x; e < ne * nc; e += blockDim.x) {
+        const int c = e / ne, row = e - c * ne;
+        W[edst[row] + (cc0 + c) * ldw] = Ex[c * kSULD + row];
+    }
+    // thread = (row r, 8-column group g)
+    const int r = threadIdx.x & 63, g = threadIdx.x >> 6;
+    auto prod = [&](const T* M, int roff, T (&acc)[8]) {   // acc = M(r, :) * Bn[roff + :, g*8 ..]
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = T(0);
+#pragma unroll 4
+        for (int k = 0; k < kB64; ++k) {
+            const T m = M[r + k * kB64];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] += m * Bn[(g * 8 + u) * kSULD + roff + k];
+        }
+    };
+    T acc[8];
+    prod(AiT, 0, acc);                                     // Utop = La^{-1} Atop
+    __syncthreads();
+    if (r < p1)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) Bn[(g * 8 + u) * kSULD + r] = acc[u];
+    __syncthreads();
+    if (p2 > 0) {
+        prod(LbT, 0, acc);                                 // Abot -= Lb Utop
+        if (r < p2)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) Bn[(g * 8 + u) * kSULD + kB64 + r] -= acc[u];
+        __syncthreads();
+        prod(CiT, kB64, acc);                              // Ubot = Lc^{-1} Abot
+        __syncthreads();
+        if (r < p2)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) Bn[(g * 8 + u) * kSULD + kB64 + r] = acc[u];
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < bw * nc; e += blockDim.x) {
+        const int c = e / bw, row = e - c * bw;
+        W[(k0 + row) + (cc0 + c) * ldw] = Bn[c * kSULD + row];
+    }
+}
+
 // ------------------------------------------------------------------ host driver
 struct LuStreams {
     cudaStream_t hi = nullptr;
@@ -502,6 +622,15 @@ static void u12_launch(const Work& w, int64_t r0, int nb, int64_t c0, int64_t c1
 }
 
 template <typename T>
+static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s) {
+    if (c1 <= c0) return;
+    const int smem = (int)(sizeof(T) * (2 * kSUC * kSULD + 3 * kB64 * kB64));
+    cudaFuncSetAttribute(swap_u12_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    swap_u12_kernel<T><<<(unsigned)((c1 - c0 + kSUC - 1) / kSUC), 256, smem, s>>>((T*)w.W, w.ldw, k0, bw, c0, c1, w.ipiv,
+                                                                                 (const T*)w.Dinv0);
+}
+
+template <typename T>
 static void gemm_launch(const Work& w, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, cudaStream_t s,
                         int prio, bool one_per_sm = false, int trace_slot = -1) {
     (void)prio;
@@ -567,22 +696,17 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         // the finished L columns [0, k0) on the side stream (nothing reads them before the
         // solve; the side stream keeps the blocks' order), the trailing columns [kn, n) and
         // the row permutation on the critical path
-        if (k0 > 0) {
+        {
             cudaEvent_t el = ev();
             cudaEventRecord(el, s);
             cudaStreamWaitEvent(LS.side, el, 0);
-            laswp_launch<T>(w, k0, bw, 0, k0, 0, 0, false, LS.side);
+            laswp_launch<T>(w, k0, bw, 0, k0, 0, 0, true, LS.side);   // L columns + row permutation
             side_used = true;
         }
-        laswp_launch<T>(w, k0, bw, kn, n, 0, 0, true, s);       // + row permutation
         if (kn >= n) break;
-        // U12 = L11^{-1} A12 with L11 = [La 0; Lb Lc] in 64-row halves: Utop = La^{-1} Atop,
-        // Abot -= Lb Utop (DMMA), Ubot = Lc^{-1} Abot
-        u12_launch<T>(w, k0, p1, kn, n, s);
-        if (bw > p1) {
-            gemm_launch<T>(w, k0 + p1, kn, k0, bw - p1, n - kn, p1, s, 0);
-            u12_launch<T>(w, k0 + p1, bw - p1, kn, n, s);
-        }
+        // trailing columns: interchanges + U12 = L11^{-1} A12 in one kernel
+        (void)p1;
+        swap_u12_launch<T>(w, k0, bw, kn, n, s);
         const int64_t M = n - kn;
         const int nbw = (int)std::min<int64_t>(kBW, n - kn);
         if (lookahead && n - kn > nbw) {

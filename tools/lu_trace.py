@@ -24,8 +24,15 @@ for k in sorted(blocks):
     if g: tot_g += g[1] - g[0]
     for p in (p1, p2):
         if p: tot_p += p[1] - p[0]
-    if k % 8 == 0 or k > max(blocks) - 4:
+    show = os.environ.get("SHOW")
+    if (show and int(show.split(",")[0]) <= k <= int(show.split(",")[1])) or (not show and (k % 8 == 0 or k > max(blocks) - 4)):
         fmt = lambda x: f"{x[0]:9.1f}-{x[1]:9.1f} ({x[1]-x[0]:7.1f})" if x else " " * 29
         print(f"blk {k:3d} gemm {fmt(g)} | p1 {fmt(p1)} | p2 {fmt(p2)} | la {fmt(la)}")
+gaps = []
+for k in sorted(blocks):
+    if k + 1 in blocks and "gemm" in blocks[k] and "gemm" in blocks[k + 1]:
+        gaps.append(blocks[k + 1]["gemm"][0] - blocks[k]["gemm"][1])
+if gaps:
+    print(f"gap GEMM_k end -> GEMM_k+1 start: mean {sum(gaps)/len(gaps):.1f} us, total {sum(gaps):.1f} us")
 end = max(e for _, _, _, e in tr)
 print(f"span {end:.1f} us, sum(main gemm) {tot_g:.1f} us, sum(panels) {tot_p:.1f} us")
