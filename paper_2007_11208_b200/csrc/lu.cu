@@ -25,6 +25,7 @@
 #include "factor.h"
 #include "gemm.h"
 #include "internal.h"
+#include <cooperative_groups.h>
 #include "blk64.cuh"
 #include "trsm.h"
 
@@ -283,6 +284,157 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
     }
     if (threadIdx.x == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
     if (tr_max && threadIdx.x == 0) atomicMax(tr_max, gtimer());
+}
+
+// ------------------------------------------------------------------ panel (one thread-block cluster)
+// Same algorithm as lu_panel2_kernel for panels whose rows fit in the shared memory of at most
+// kClMax CTAs: the per-column candidate exchange goes through distributed shared memory with
+// one cluster barrier per column instead of sequence-numbered global slots (several L2 round
+// trips per column).  Candidate rows / old row g are double-buffered by column parity: a CTA
+// rewrites a parity buffer only after the next column's barrier, i.e. after every CTA read it.
+namespace cg = cooperative_groups;
+constexpr int kClMax = 8;
+template <typename T>
+__global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+                                                              int64_t* ipiv, DevState* st) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int P = gridDim.x, cta = blockIdx.x;          // the grid is one cluster
+    const int64_t m = n - k0;
+    const int64_t chunk = (m + P - 1) / P;
+    const int64_t rbeg = k0 + (int64_t)cta * chunk;
+    const int64_t rend = min(n, rbeg + chunk);
+    const int nr = (int)max<int64_t>(0, rend - rbeg);
+    const int64_t cp = chunk;
+    T* Ps = (T*)smem_raw;                                // chunk x nbp, column-major
+    T* ubuf = Ps + chunk * nbp;                          // pivot row
+    T* candb = ubuf + nbp;                               // [2][nbp] my candidate row
+    T* diagb = candb + 2 * nbp;                          // [2][nbp] old row g (owner of g)
+    __shared__ T s_cv[2];
+    __shared__ long long s_ci[2];
+    __shared__ T sv[8];
+    __shared__ long long si[8];
+    __shared__ int sdn[8];
+    __shared__ long long s_p;
+    __shared__ int s_owner;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    batched<8, T>(
+        nr * nbp, [&](int e) -> T { const int c = e / nr, r = e - c * nr; return W[(rbeg + r) + (k0 + c) * ldw]; },
+        [&](int e, T v) { const int c = e / nr, r = e - c * nr; Ps[r + c * cp] = v; });
+    __syncthreads();
+    auto publish = [&](int j, T v, long long idx) {
+        const int64_t g = k0 + j;
+        const int par = j & 1;
+        if (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) {
+            const int r = (int)(idx - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) candb[par * nbp + c] = Ps[r + c * cp];
+        }
+        if (g >= rbeg && g < rend) {
+            const int r = (int)(g - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) diagb[par * nbp + c] = Ps[r + c * cp];
+        }
+        if (threadIdx.x == 0) { s_cv[par] = v; s_ci[par] = idx; }
+    };
+    {
+        T v;
+        long long idx;
+        panel_local_argmax(Ps, cp, nr, rbeg, k0, 0, v, idx, sv, si, sdn);
+        publish(0, v, idx);
+    }
+    unsigned long long info = ~0ull;
+    for (int j = 0; j < nbp; ++j) {
+        const int64_t g = k0 + j;
+        const int par = j & 1;
+        cl.sync();                                       // every candidate of column j is visible
+        if (warp == 0) {
+            T bv = T(-1);
+            long long bi = 0x7fffffffffffffffll;
+            int bo = 0;
+            if (lane < P) {
+                bv = *cl.map_shared_rank(&s_cv[par], lane);
+                bi = *cl.map_shared_rank(&s_ci[par], lane);
+                bo = lane;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int o2 = __shfl_xor_sync(0xffffffffu, bo, o);
+                if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; bo = o2; }
+            }
+            if (lane == 0) { s_p = bi; s_owner = bo; }
+        }
+        __syncthreads();
+        const long long p = s_p;
+        const int owner = s_owner;
+        const int gown = (int)((g - k0) / chunk);
+        const bool own_p = p != g && p >= rbeg && p < rend;
+        const T* rc = cl.map_shared_rank(candb + par * nbp, owner);
+        const T* rd = cl.map_shared_rank(diagb + par * nbp, gown);
+        T* dst_p = own_p ? Ps + (p - rbeg) : nullptr;
+        for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
+            const T u = rc[c];
+            const T dg = own_p ? rd[c] : T(0);
+            ubuf[c] = u;
+            if (own_p) dst_p[c * cp] = dg;
+        }
+        __syncthreads();
+        const T piv = ubuf[j];
+        if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
+        const bool elim = piv != T(0);
+        if (!elim) {
+            if (info == ~0ull) info = (unsigned long long)(g + 1);
+            if (own_p)
+                for (int c = threadIdx.x; c < nbp; c += blockDim.x) dst_p[c * cp] = ubuf[c];
+        } else if (g >= rbeg && g < rend) {
+            const int r = (int)(g - rbeg);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = ubuf[c];
+        }
+        __syncthreads();
+        const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
+        if (elim) {
+            const T u1 = (j + 1 < nbp) ? ubuf[j + 1] : T(0);
+            for (int r = (int)r0 + threadIdx.x; r < nr; r += blockDim.x) {
+                const T l = Ps[r + j * cp] / piv;
+                Ps[r + j * cp] = l;
+                if (j + 1 < nbp) Ps[r + (j + 1) * cp] -= l * u1;
+            }
+        }
+        __syncthreads();
+        if (j + 1 >= nbp) break;
+        T v;
+        long long idx;
+        panel_local_argmax(Ps, cp, nr, rbeg, g + 1, j + 1, v, idx, sv, si, sdn);
+        const int rcn = (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) ? (int)(idx - rbeg) : -1;
+        const int rg = (g + 1 >= rbeg && g + 1 < rend) ? (int)(g + 1 - rbeg) : -1;
+        if (elim) {
+            for (int c = j + 2 + threadIdx.x; c < nbp; c += blockDim.x) {
+                if (rcn >= 0) Ps[rcn + c * cp] -= Ps[rcn + j * cp] * ubuf[c];
+                if (rg >= 0 && rg != rcn) Ps[rg + c * cp] -= Ps[rg + j * cp] * ubuf[c];
+            }
+        }
+        __syncthreads();
+        publish(j + 1, v, idx);
+        if (elim) {
+            const int nrow = (int)max<int64_t>(0, nr - r0);
+            const int rl = threadIdx.x & 127, ph = threadIdx.x >> 7;
+            for (int rr = rl; rr < nrow; rr += 128) {
+                const int r = (int)r0 + rr;
+                if (r == rcn || r == rg) continue;
+                const T l = Ps[r + j * cp];
+#pragma unroll 4
+                for (int c = j + 2 + ph; c < nbp; c += 2) Ps[r + c * cp] -= l * ubuf[c];
+            }
+        }
+        __syncthreads();
+    }
+    cl.sync();                                           // no CTA exits while others may read its buffers
+    for (int e = threadIdx.x; e < nr * nbp; e += blockDim.x) {
+        const int c = e / nr, r = e - c * nr;
+        W[(rbeg + r) + (k0 + c) * ldw] = Ps[r + c * cp];
+    }
+    if (threadIdx.x == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
 }
 
 // ------------------------------------------------------------------ laswp
@@ -568,6 +720,30 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
     static const int rows_per_cta = getenv("AS_LU_PANEL_ROWS") ? atoi(getenv("AS_LU_PANEL_ROWS")) : 128;
     int P = (int)std::min<int64_t>(w.num_sms, (m + rows_per_cta - 1) / rows_per_cta);
     P = std::max(P, 1);
+    if (getenv("AS_LU_NO_CLUSTER") == nullptr) {
+        // cluster panel when the rows fit in <= kClMax CTAs' shared memory (~200 KB each)
+        int pc = 1;
+        while (pc < kClMax && (size_t)((m + pc - 1) / pc) * nbp * sizeof(T) > 192 * 1024) pc *= 2;
+        const int64_t ch = (m + pc - 1) / pc;
+        const size_t smc = sizeof(T) * ((size_t)ch * nbp + 5 * (size_t)nbp);
+        if (smc <= 200 * 1024) {
+            auto kc = lu_panel_cl_kernel<T>;
+            cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(pc);
+            cfg.blockDim = dim3(kPT);
+            cfg.dynamicSmemBytes = smc;
+            cfg.stream = s;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = pc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributePriority; at[1].val.priority = prio;
+            cfg.attrs = at;
+            cfg.numAttrs = 2;
+            if (cudaLaunchKernelEx(&cfg, kc, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st) == cudaSuccess) return;
+            cudaGetLastError();
+        }
+    }
     const int64_t chunk = (m + P - 1) / P;
     size_t smem = sizeof(T) * (chunk * nbp + nbp);
     int use_smem = 1;
