@@ -76,6 +76,10 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
 #define AS_OPT_NO_FALLBACK  0x1u   /* disable the SVD fallback */
 #define AS_OPT_FORCE_METHOD 0x2u   /* use opt.force_method (1..5) instead of the detected one */
 #define AS_OPT_FULLSCAN     0x8u   /* detection never exits early; kl/ku always exact */
+#define AS_OPT_SKIP_DETECT  0x10u  /* with AS_OPT_FORCE_METHOD (LU, CHOL, TRI_*): no structure detection at all --
+                                      the "standard solver" of the paper's comparison; report bits
+                                      0..3 are 0.  Illegal (-9) without FORCE_METHOD or with AS_METHOD_BAND,
+                                      which needs the detected kl/ku. */
 
 /* ---- return codes ------------------------------------------------------- */
 #define AS_OK                        0
@@ -191,6 +195,16 @@ int as_debug_timestamps(unsigned long long* out16);
  * 4k+3 look-ahead GEMM; tmin = first CTA start, tmax = last CTA end (%globaltimer ns) of the last
  * factorization.  Host arrays of `cap` entries.  Returns the number of slots written, or -1 when
  * tracing is off. */
+/* Diagnostics (not part of the solve path): average device time in microseconds of one panel
+ * factorization of the column block k0 .. k0+nbp of the n x n column-major matrix W (device,
+ * leading dimension ldw), restored from the device copy Wsrc before each of `iters` launches (the
+ * first launch is not averaged when iters > 1).  kind 0: LU register/cluster panel,
+ * 1: LU cooperative panel, 2: Cholesky cluster panel, 3: Cholesky POTF2 + L21.
+ * dbg: ablation bits of the LU register panel (1 skip interchanges on other columns, 2 skip the
+ * deferred update, 8 skip the column loop) -- timing studies only, results are then wrong.
+ * Returns < 0 on an illegal argument or a CUDA error (-error code). */
+double as_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
+                           int iters, int dbg);
 int as_debug_lu_trace(unsigned long long* tmin, unsigned long long* tmax, int cap);
 
 /* Roofline denominator probe (benchmark only, not part of a solve): fp64

@@ -32,12 +32,14 @@ FLAG_CHOL_FAILED, FLAG_SINGULAR, FLAG_RCOND_LOW, FLAG_FALLBACK = 1 << 8, 1 << 9,
 FLAG_POORLY_COND, FLAG_SVD_NOCONV, FLAG_RANK_DEF = 1 << 12, 1 << 14, 1 << 15
 METHOD_BAND, METHOD_TRI_LOWER, METHOD_TRI_UPPER, METHOD_CHOL, METHOD_LU, METHOD_SVD = 1, 2, 3, 4, 5, 6
 OPT_NO_FALLBACK, OPT_FORCE_METHOD, OPT_FULLSCAN = 0x1, 0x2, 0x8
+OPT_SKIP_DETECT = 0x10
 ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
 
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
            "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
            "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
-           "as_set_exec_mode", "as_debug_timestamps", "as_debug_lu_trace", "as_bench_gemm")
+           "as_set_exec_mode", "as_debug_timestamps", "as_debug_lu_trace", "as_bench_gemm",
+           "as_debug_panel_time")
 
 
 class Options(C.Structure):
@@ -138,10 +140,10 @@ def to_host(t) -> np.ndarray:
 
 
 def make_options(no_fallback=False, force_method=None, fullscan=False, rcond_threshold=-1.0, lsq_cutoff=-1.0,
-                 max_sweeps=30) -> Options:
+                 max_sweeps=30, skip_detect=False) -> Options:
     o = Options()
     o.flags = (OPT_NO_FALLBACK if no_fallback else 0) | (OPT_FORCE_METHOD if force_method else 0) | \
-        (OPT_FULLSCAN if fullscan else 0)
+        (OPT_FULLSCAN if fullscan else 0) | (OPT_SKIP_DETECT if skip_detect else 0)
     o.force_method = int(force_method or 0)
     o.rcond_threshold = float(rcond_threshold)
     o.lsq_cutoff = float(lsq_cutoff)
@@ -224,6 +226,20 @@ def bench_gemm(M, N, K, dtype_code=AS_F64, trans_b=False, iters=5) -> float:
     return float(_lib.as_bench_gemm(dtype_code, M, N, K, int(trans_b), iters))
 _lib.as_debug_timestamps.argtypes = [P]
 _lib.as_debug_timestamps.restype = C.c_int
+_lib.as_debug_panel_time.argtypes = [C.c_int, C.c_int, P, C.c_int64, C.c_int64, C.c_int64, C.c_int, P, C.c_int, C.c_int]
+_lib.as_debug_panel_time.restype = C.c_double
+
+
+def debug_panel_time(W, k0, nbp, kind=0, iters=5, dbg=0):
+    """Average device time (us) of one panel factorization of the column-major device matrix W
+    (kind 0/1: LU register / cooperative panel, 2/3: Cholesky cluster panel / POTF2 + L21)."""
+    n = W.shape[0]
+    Wc = W.clone()
+    src = W.clone()
+    return _lib.as_debug_panel_time(_dt(W), kind, Wc.data_ptr(), W.stride(1), n, k0, nbp, src.data_ptr(),
+                                    iters, dbg)
+
+
 _lib.as_debug_lu_trace.argtypes = [P, P, C.c_int]
 _lib.as_debug_lu_trace.restype = C.c_int
 

@@ -45,8 +45,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
         return OUT
     os.makedirs(BUILD, exist_ok=True)
+    # a source is recompiled when it, or any header, is newer than its object
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + [hdr]
+    newest_hdr = max(os.path.getmtime(h) for h in hdrs)
+
+    def need(src: str) -> bool:
+        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        if force or verbose or not os.path.exists(obj):
+            return True
+        return os.path.getmtime(obj) < max(newest_hdr, os.path.getmtime(os.path.join(CSRC, src)))
+
+    def one(src: str) -> str:
+        return _compile(src, verbose) if need(src) else os.path.join(BUILD, src.replace(".cu", ".o"))
+
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
+        objs = list(ex.map(one, sources()))
     tmp = OUT + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-lcuda"]
     r = subprocess.run(cmd, capture_output=True, text=True)

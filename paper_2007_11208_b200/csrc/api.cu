@@ -206,7 +206,7 @@ static void body_solve(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     case AS_METHOD_TRI_UPPER:
         launch_copy_b_to_x(w, s);
         launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, m == AS_METHOD_TRI_UPPER, false, nullptr, w.ldb, w.n,
-                    (int)w.nrhs, sa.take(trsm_sync_words(w.n, (int)w.nrhs)), -1, false, w.args, w.st, s);
+                    (int)w.nrhs, sa, -1, false, w.args, w.st, s);
         break;
     case AS_METHOD_CHOL: launch_chol_solve(w, sa, s); break;
     case AS_METHOD_LU: launch_lu_solve(w, sa, s); break;
@@ -286,6 +286,8 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.perm = (int64_t*)take(8 * n);
     w.flags_ts_len = 160 * trsm_sync_words(n, (int)nr);
     w.flags_ts = (unsigned*)take(4 * w.flags_ts_len);
+    w.ll_len = 100 * trsm_ll_words(n, 1) + 10 * trsm_ll_words(n, (int)nr);
+    w.ll = (unsigned long long*)take(8 * w.ll_len);
     w.bars_len = 8 + nblk + 8;
     w.bars = (unsigned*)take(4 * w.bars_len);
     w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * 128 + es * 2 * 128);   // LU panel slots, rowbuf, diagbuf (128-wide)
@@ -298,6 +300,8 @@ static int build_graph(Plan& P) {
     B.w = w;
     B.sa.base = w.flags_ts;
     B.sa.cap = w.flags_ts_len;
+    B.sa.llbase = w.ll;
+    B.sa.llcap = w.ll_len;
     for (int i = 0; i < 6; ++i) {
         cudaStream_t s;
         cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
@@ -322,7 +326,7 @@ static int build_graph(Plan& P) {
         launch_state_init(w, s0, k.opts, k.force, k.thr, k.cut, k.sweeps);
         cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s0);
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[0], s0, cudaEventRecordExternal);
-        launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
+        if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
         cudaGraphConditionalHandle h_method = make_handle(s0, 0);
         launch_dispatch(w, s0, h_method);
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[1], s0, cudaEventRecordExternal);
@@ -388,7 +392,7 @@ static int build_graph(Plan& P) {
         }
     }
     err = err ? err : B.err;
-    if (!err && B.sa.used > B.sa.cap) err = AS_ERR_CUDA_BASE + 999;
+    if (!err && (B.sa.used > B.sa.cap || B.sa.llpeak > B.sa.llcap)) err = AS_ERR_CUDA_BASE + 999;
     if (!err) err = check(cudaGraphInstantiate(&P.exec, P.graph, 0), "GraphInstantiate");
     for (auto s : B.streams) cudaStreamDestroy(s);
     cudaGetLastError();
@@ -409,6 +413,8 @@ static int get_plan(const PlanKey& key, Plan** out) {
     if (err) return err;
     P->ws_bytes = bytes;
     layout(w, key.opts, (char*)P->ws);
+    err = check(cudaMemset(P->ws, 0, bytes), "cudaMemset(workspace)");   // epoch 0, exchange words untagged
+    if (err) return err;
     P->rep_ws = (RepOut*)((char*)w.args + align256(sizeof(DevArgs)));
     err = check(cudaMallocHost(&P->rep_pinned, sizeof(RepOut)), "cudaMallocHost");
     if (err) return err;
@@ -431,6 +437,8 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
     SyncAlloc sa;
     sa.base = w.flags_ts;
     sa.cap = w.flags_ts_len;
+    sa.llbase = w.ll;
+    sa.llcap = w.ll_len;
     DevState h;
     auto rd = [&]() {
         cudaMemcpyAsync(&h, w.st, sizeof(DevState), cudaMemcpyDeviceToHost, s);
@@ -440,7 +448,7 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
     launch_state_init(w, s, k.opts, k.force, k.thr, k.cut, k.sweeps);
     cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s);
     if (k.instrumented) cudaEventRecord(P.ev[0], s);
-    launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
+    if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
     launch_dispatch(w, s, 0);
     if (k.instrumented) cudaEventRecord(P.ev[1], s);
     int err = rd();
@@ -530,6 +538,7 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     if (key.opts & AS_OPT_FORCE_METHOD) {
         if (key.force < AS_METHOD_BAND || key.force > AS_METHOD_LU) return -9;
     }
+    if ((key.opts & AS_OPT_SKIP_DETECT) && (!(key.opts & AS_OPT_FORCE_METHOD) || key.force == AS_METHOD_BAND)) return -9;
     key.thr = (opt && opt->rcond_threshold >= 0) ? opt->rcond_threshold : 0.5 * eps;
     if (dt == AS_F32) key.thr = (double)(float)key.thr;
     key.cut = (opt && opt->lsq_cutoff >= 0) ? opt->lsq_cutoff : (double)n * eps;
@@ -784,6 +793,13 @@ double as_bench_gemm(int dtype, int64_t M, int64_t N, int64_t K, int trans_b, in
     cudaEventDestroy(e1);
     cudaFree(A); cudaFree(B); cudaFree(Cm);
     return 2.0 * (double)M * N * K * iters / (ms * 1e-3) / 1e12;
+}
+
+double as_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
+                           int iters, int dbg) {
+    if (!W || !Wsrc || n <= 0 || k0 < 0 || k0 >= n || nbp <= 0 || ldw < n || iters <= 0) return -1.0;
+    if (kind <= 1) return as::lu_debug_panel_time(dtype, kind, W, ldw, n, k0, nbp, Wsrc, iters, dbg);
+    return as::chol_debug_panel_time(dtype, kind - 2, W, ldw, n, k0, nbp, Wsrc, iters);
 }
 
 int as_debug_lu_trace(unsigned long long* tmin, unsigned long long* tmax, int cap) {

@@ -68,6 +68,8 @@ struct DevState {
     unsigned long long dbg_t[16]; // %globaltimer phase stamps (diagnostics)
     // ---- barriers / counters (zeroed per solve)
     uint32_t bar[4];
+    uint32_t epoch;               // solve counter (kept across solves): tags the triangular-solve exchange words
+    uint32_t pad3;
 };
 
 // orderable bits for non-negative doubles (IEEE bit pattern is monotone)

@@ -24,7 +24,9 @@ __global__ void set_args_kernel(DevArgs a, DevArgs* dst) { *dst = a; }
 __global__ void state_init_kernel(DevState* st, int64_t n, uint32_t opts, int force_method, double thr, double cut,
                                   int max_sweeps) {
     if (threadIdx.x != 0) return;
+    const uint32_t ep = st->epoch + 1u;      // the workspace is zeroed at plan creation
     DevState s = {};
+    s.epoch = ep == 0u ? 1u : ep;
     s.alive = AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE;
     s.kl = 0; s.ku = 0;
     s.max_diag = 0ull;
@@ -564,7 +566,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
 // else general LU; or the forced method.  Sets the SWITCH handle.
 __global__ void dispatch_kernel(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
     if (threadIdx.x != 0) return;
-    const unsigned f = st->alive;
+    const unsigned f = (st->opts & AS_OPT_SKIP_DETECT) ? 0u : st->alive;   // detection skipped: no verdicts
     st->det_flags = f;
     int m;
     if (st->opts & AS_OPT_FORCE_METHOD) m = st->force_method;

@@ -35,6 +35,8 @@ struct Work {
     int64_t* perm;       // n (LU row permutation)
     unsigned* flags_ts;  // sync-free triangular-solve tickets/flags: (n/kNB+1) * tiles + 64
     int64_t flags_ts_len;
+    unsigned long long* ll;   // triangular-solve exchange words (epoch-tagged, zeroed once)
+    int64_t ll_len;
     unsigned* bars;      // cooperative-kernel barrier counters (zeroed per solve)
     int64_t bars_len;
     void* cand;          // LU panel candidates

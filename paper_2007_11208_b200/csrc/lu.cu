@@ -20,6 +20,9 @@
 //   look-ahead: the GEMM is split; the columns of the next block are updated
 //   first on a high-priority stream and the next block's panels start there
 //   while the bulk of the GEMM is still running.
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "factor.h"
@@ -437,6 +440,392 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
     if (threadIdx.x == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
 }
 
+// ------------------------------------------------------------------ panel (leaf-blocked, one cluster)
+// The panel's m rows are split over the P <= 16 CTAs of one thread-block cluster, RPT <= 4 rows per
+// thread (row tid + 256 i of the CTA's chunk).  The panel's columns are factored in leaves of
+// kLW = 16 columns held in REGISTERS (compile-time column index: the column loop is unrolled); the
+// rest of the panel stays in global memory (L2) and receives one deferred rank-16 update per leaf.
+// Per column:
+//   every CTA pushes its first-max candidate (|value|, row, the row's 16 leaf values) -- and the
+//   owner of row g its old row g -- into every CTA's shared memory (remote DSMEM stores), one
+//   cluster barrier, every thread picks the winner from local shared memory (first-max tie-break,
+//   Z15), the owners of g and p swap the two rows, the rank-1 update runs in registers together
+//   with the next column's candidate search, one CTA barrier for the candidate reduction.
+// Per leaf: the leaf's interchanges composed into one permutation of <= 32 rows and applied to
+// the panel's other columns; U12 = L11^{-1} A12 for the leaf's pivot rows; A22 -= L21 U12 for the
+// rows below.  The result (W rows interchanged within the panel, ipiv) is the unblocked column
+// sweep's up to rounding.
+constexpr int kLfMaxP = 16;
+constexpr int kLW = 16;
+constexpr int kURW = kPW - kLW + 16;  // + padding: vector reads past the last column
+
+template <typename T, int RPT>
+__global__ void __launch_bounds__(kPT, 1) lu_panel_reg_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+                                                               int64_t* ipiv, DevState* st, unsigned long long* tr_min,
+                                                               unsigned long long* tr_max, int dbg) {
+    cg::cluster_group cl = cg::this_cluster();
+    if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
+    const int P = (int)cl.num_blocks(), cta = (int)cl.block_rank();
+    const int64_t m = n - k0;
+    const int64_t chunk = (m + P - 1) / P;
+    const int64_t rbeg = k0 + (int64_t)cta * chunk;
+    const int64_t rend = min(n, rbeg + chunk);
+    __shared__ T crow[2][kLfMaxP][kLW];      // pushed candidate rows (leaf values)
+    __shared__ T grow[2][kLW];               // pushed old row g
+    __shared__ T cval[2][kLfMaxP];
+    __shared__ int cidx[2][kLfMaxP];
+    __shared__ T Ub[kLW][kLW];               // pivot rows of the leaf (L11 \ U11)
+    __shared__ T stg[2][kLW];                // staging of the rows this CTA pushes
+    __shared__ T U12[kLW][kURW];
+    __shared__ T red_v[8];
+    __shared__ int red_i[8];
+    __shared__ int red_dn[8];
+    __shared__ int64_t s_piv[kPW];
+    __shared__ int64_t s_src[2 * kLW], s_dst[2 * kLW];
+    __shared__ int s_np;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kNone = 0x7fffffff;        // row positions fit in int (n <= 2^31 - 1)
+    int gr[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) gr[i] = (rbeg + tid + (int64_t)kPT * i < rend) ? (int)(rbeg + tid + (int64_t)kPT * i) : -1;
+    T a[RPT][kLW];
+
+    auto cbar = [&]() {
+        if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        else __syncthreads();
+    };
+    // CTA-wide first-max over this thread's partial (bv, bi, dn); NaN at row gd keeps gd
+    auto merge = [](T& v, int& i, T v2, int i2) { if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; } };
+    auto reduce = [&](T bv, int bi, int dn, int gd, T& v, int& idx) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            merge(bv, bi, v2, i2);
+        }
+        dn = __any_sync(0xffffffffu, dn);
+        if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; red_dn[warp] = dn; }
+        __syncthreads();
+        // every warp merges the 8 partials as a 3-level shuffle tree (lanes 0..7)
+        v = red_v[lane & 7];
+        idx = red_i[lane & 7];
+        int d = red_dn[lane & 7];
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            const T v2 = __shfl_xor_sync(0xffffffffu, v, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+            merge(v, idx, v2, i2);
+            d |= __shfl_xor_sync(0xffffffffu, d, o);
+        }
+        if (d) { v = T(INFINITY); idx = gd; }
+    };
+
+    unsigned long long info = ~0ull;
+    // diagnostics (dbg & 256): clock64 phase totals of CTA 0 / thread 0 into st->dbg_t
+    const bool prof = (dbg & 256) && cta == 0 && tid == 0;
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64();
+#define PH(k) do { if (prof) { const long long t_ = clock64(); ph[k] += t_ - tp; tp = t_; } } while (0)
+    for (int c0 = 0; c0 < nbp; c0 += kLW) {
+        const int w = min(kLW, nbp - c0);
+        const int g0 = (int)(k0 + c0);
+        // leaf columns of my active rows (positions >= g0) into registers
+#pragma unroll
+        for (int c = 0; c < kLW; ++c)
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                a[i][c] = (gr[i] >= g0 && c < w) ? W[gr[i] + (k0 + c0 + c) * ldw] : T(0);
+        T v;
+        int idx;
+        {
+            T bv = T(-1);
+            int bi = kNone;
+            int dn = 0;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                if (gr[i] >= g0) {
+                    T x = a[i][0];
+                    x = x < T(0) ? -x : x;
+                    if (gr[i] == g0 && x != x) dn = 1;
+                    merge(bv, bi, x, gr[i]);
+                }
+            reduce(bv, bi, dn, g0, v, idx);
+        }
+        // Column loop, NOT unrolled (an unrolled leaf is ~200 KB of code: instruction-cache bound).
+        // Each row is kept ROTATED in registers: at step jj, a[i][k] holds leaf column (jj + k) mod 16,
+        // so the current column is always a[i][0] and every register index is a compile-time
+        // constant; the finished column rotates to the end (after 16 steps the order is restored).
+        for (int jj = 0; jj < (dbg & 8 ? 0 : w); ++jj) {
+            {
+                const int c = c0 + jj;
+                const int g = (int)(k0 + c);
+                const int par = c & 1;
+                // ---- push: candidate (value, index, leaf row), and the owner of g its row g.  The
+                // rows are staged in this CTA's shared memory by their owner thread, then the lanes
+                // of its warp push them to every CTA (warp-uniform branches: other warps skip)
+                if (tid < P) {
+                    T* rv = cl.map_shared_rank(&cval[par][0], tid);
+                    int* ri = cl.map_shared_rank(&cidx[par][0], tid);
+                    rv[cta] = v;
+                    ri[cta] = idx;
+                }
+                {
+                    const int64_t oc = (idx != kNone && idx >= rbeg && idx < rend) ? idx - rbeg : -1;
+                    const int64_t og = (g >= rbeg && g < rend) ? g - rbeg : -1;
+                    const int wc = oc >= 0 ? (int)((oc & (kPT - 1)) >> 5) : -1;
+                    const int wg = og >= 0 ? (int)((og & (kPT - 1)) >> 5) : -1;
+                    if (warp == wc || warp == wg) {
+                        if (oc >= 0 && tid == (int)(oc & (kPT - 1))) {
+                            const int ic = (int)(oc >> 8);
+#pragma unroll
+                            for (int i = 0; i < RPT; ++i)
+                                if (i == ic)
+#pragma unroll
+                                    for (int k = 0; k < kLW; ++k) stg[0][(jj + k) & (kLW - 1)] = a[i][k];
+                        }
+                        if (og >= 0 && tid == (int)(og & (kPT - 1))) {
+                            const int ig = (int)(og >> 8);
+#pragma unroll
+                            for (int i = 0; i < RPT; ++i)
+                                if (i == ig)
+#pragma unroll
+                                    for (int k = 0; k < kLW; ++k) stg[1][(jj + k) & (kLW - 1)] = a[i][k];
+                        }
+                        __syncwarp();
+                        if (warp == wc)
+                            for (int e = lane; e < P * kLW; e += 32) {
+                                T* rr = cl.map_shared_rank(&crow[par][cta][0], e / kLW);
+                                rr[e % kLW] = stg[0][e % kLW];
+                            }
+                        if (warp == wg)
+                            for (int e = lane; e < P * kLW; e += 32) {
+                                T* rg = cl.map_shared_rank(&grow[par][0], e / kLW);
+                                rg[e % kLW] = stg[1][e % kLW];
+                            }
+                    }
+                }
+                PH(0);
+                cbar();
+                PH(1);
+                // ---- winner from local shared memory
+                T bv = T(-1);
+                int bi = kNone;
+                int bo = 0;
+                for (int q = 0; q < P; ++q) {
+                    const T cv = cval[par][q];
+                    const int ci = cidx[par][q];
+                    if (cv > bv || (cv == bv && ci < bi)) { bv = cv; bi = ci; bo = q; }
+                }
+                const int p = bi;
+                const T* ub = &crow[par][bo][0];
+                const T piv = ub[jj];
+                const bool elim = piv != T(0);
+                if (tid < kLW) Ub[jj][tid] = ub[tid];
+                if (tid == 0) s_piv[c] = (p == kNone) ? g : p;
+                if (!elim) {
+                    if (info == ~0ull) info = (unsigned long long)(g + 1);
+                } else if (p != g) {
+                    const int64_t og = (g >= rbeg && g < rend) ? g - rbeg : -1;
+                    const int64_t op = (p >= rbeg && p < rend) ? p - rbeg : -1;
+                    if ((og >= 0 && warp == (int)((og & (kPT - 1)) >> 5)) || (op >= 0 && warp == (int)((op & (kPT - 1)) >> 5))) {
+#pragma unroll
+                        for (int i = 0; i < RPT; ++i) {
+                            if (gr[i] == g) {
+#pragma unroll
+                                for (int k = 0; k < kLW; ++k) a[i][k] = ub[(jj + k) & (kLW - 1)];
+                            } else if (gr[i] == p) {
+#pragma unroll
+                                for (int k = 0; k < kLW; ++k) a[i][k] = grow[par][(jj + k) & (kLW - 1)];
+                            }
+                        }
+                    }
+                }
+                PH(2);
+                // ---- multipliers, rank-1 update (registers), rotation, next column's candidate
+                T u[kLW];                                    // u[k] = pivot row at column jj + k
+#pragma unroll
+                for (int k = 1; k < kLW; ++k) u[k] = ub[(jj + k) & (kLW - 1)];
+                const int nlive = kLW - jj;                  // a[.][k] for k < nlive are leaf columns >= jj
+                T nb = T(-1);
+                int ni = kNone;
+                int dn = 0;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    T x0 = a[i][0];
+                    if (gr[i] > g && elim && !(dbg & 16)) {
+                        const T l = x0 / piv;
+                        x0 = l;
+#pragma unroll
+                        for (int k = 1; k < kLW; ++k)
+                            if (k < nlive) a[i][k] -= l * u[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < kLW - 1; ++k) a[i][k] = a[i][k + 1];
+                    a[i][kLW - 1] = x0;
+                    if (gr[i] > g) {
+                        T x = a[i][0];
+                        x = x < T(0) ? -x : x;
+                        if (gr[i] == g + 1 && x != x) dn = 1;
+                        merge(nb, ni, x, gr[i]);
+                    }
+                }
+                PH(3);
+                if (jj + 1 < w) {
+                    if (dbg & 64) { v = nb; idx = ni; __syncthreads(); }
+                    else reduce(nb, ni, dn, g + 1, v, idx);
+                }
+                PH(4);
+            }
+        }
+        // short leaf (w < 16): finish the rotation so that a[.][c] is leaf column c again
+        if (w < kLW && !(dbg & 8))
+            for (int r = w; r < kLW; ++r)
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const T x0 = a[i][0];
+#pragma unroll
+                    for (int k = 0; k < kLW - 1; ++k) a[i][k] = a[i][k + 1];
+                    a[i][kLW - 1] = x0;
+                }
+        // ---- leaf end: write back, pivots, the leaf's interchanges on the panel's other columns
+#pragma unroll
+        for (int c = 0; c < kLW; ++c)
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                if (gr[i] >= g0 && c < w) W[gr[i] + (k0 + c0 + c) * ldw] = a[i][c];
+        if (cta == 0 && tid < w) ipiv[g0 + tid] = s_piv[c0 + tid];
+        if (tid == 0) s_np = 0;
+        __syncthreads();
+        if (tid < 2 * w) {
+            const int t = tid;
+            int64_t x = 0;
+            bool go = true;
+            if (t < w) x = g0 + t;
+            else {
+                x = s_piv[c0 + t - w];
+                if (x < g0 + w) go = false;
+                for (int q = 0; q < t - w && go; ++q) go = s_piv[c0 + q] != x;
+            }
+            if (go) {
+                int64_t pos = x;
+                for (int q = 0; q < w; ++q) {
+                    const int64_t r = g0 + q, tq = s_piv[c0 + q];
+                    if (pos == r) pos = tq;
+                    else if (pos == tq) pos = r;
+                }
+                if (pos != x) {
+                    const int k = atomicAdd(&s_np, 1);
+                    s_dst[k] = pos;
+                    s_src[k] = x;
+                }
+            }
+        }
+        __syncthreads();
+        {
+            // one warp per column, up to 16 columns per warp with every gather issued before any
+            // scatter (one memory latency instead of one per column)
+            const int np = s_np;   // <= 32: one value per lane
+            const int nother = nbp - w;
+            const int64_t src = lane < np ? s_src[lane] : 0, dst = lane < np ? s_dst[lane] : 0;
+            constexpr int kCW = 16;
+            const int nw = P * (kPT / 32), w0 = cta * (kPT / 32) + warp;
+            for (int t0 = 0; t0 < (dbg & 1 ? 0 : nother); t0 += nw * kCW) {
+                T vv[kCW];
+#pragma unroll
+                for (int u = 0; u < kCW; ++u) {
+                    const int t = t0 + w0 + u * nw;
+                    const int col = t < c0 ? t : t + w;
+                    vv[u] = (lane < np && t < nother) ? W[src + (k0 + col) * ldw] : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < kCW; ++u) {
+                    const int t = t0 + w0 + u * nw;
+                    const int col = t < c0 ? t : t + w;
+                    if (lane < np && t < nother) W[dst + (k0 + col) * ldw] = vv[u];
+                }
+            }
+        }
+        PH(5);
+        cbar();
+        // ---- deferred update of the rest of the panel
+        if (c0 + w < nbp && !(dbg & 2)) {
+            const int c1 = c0 + w, rw = nbp - c1;
+            batched<8, T>(
+                kLW * rw, [&](int e) -> T { const int k = e % kLW, cc = e / kLW; return __ldcg(&W[(g0 + k) + (k0 + c1 + cc) * ldw]); },
+                [&](int e, T v) { const int k = e % kLW, cc = e / kLW; U12[k][cc] = v; });
+            __syncthreads();
+            // U12 = L11^{-1} A12 (unit lower L11 = Ub), one column per thread, unrolled in registers
+            for (int cc = tid; cc < rw; cc += kPT) {
+#pragma unroll 1
+                for (int k = 1; k < kLW; ++k) {
+                    T s = U12[k][cc];
+#pragma unroll
+                    for (int i2 = 0; i2 < kLW; ++i2)
+                        if (i2 < k) s -= Ub[k][i2] * U12[i2][cc];
+                    U12[k][cc] = s;
+                }
+            }
+            __syncthreads();
+            for (int e = tid; e < kLW * rw; e += kPT) {
+                const int k = e % kLW, cc = e / kLW;
+                const int64_t grow_k = g0 + k;
+                if (grow_k >= rbeg && grow_k < rend) W[grow_k + (k0 + c1 + cc) * ldw] = U12[k][cc];
+            }
+            // A22 -= L21 U12 on my rows below the leaf (L21 in registers)
+            // batches of kQ columns with a two-batch-deep prefetch (the loads of batches b+1 and b+2
+            // are in flight while batch b computes: this loop is bound by global latency otherwise);
+            // per k one vector read of U12[k][cb .. cb+kQ) feeds kQ x RPT FMAs
+            constexpr int kQ = RPT >= 4 ? 4 : RPT >= 2 ? 8 : 16;
+            const int lim = g0 + w;
+            T nx[2][RPT][kQ];
+            auto load = [&](int buf, int cb) {
+#pragma unroll
+                for (int q = 0; q < kQ; ++q)
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i)
+                        nx[buf][i][q] = (gr[i] >= lim && cb + q < rw) ? W[gr[i] + (k0 + c1 + cb + q) * ldw] : T(0);
+            };
+            load(0, 0);
+            if (kQ < rw) load(1, kQ);
+            int buf = 0;
+            for (int cb = 0; cb < rw; cb += kQ) {
+                T acc[RPT][kQ];
+#pragma unroll
+                for (int q = 0; q < kQ; ++q)
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) acc[i][q] = buf ? nx[1][i][q] : nx[0][i][q];
+                if (cb + 2 * kQ < rw) {
+                    if (buf) load(1, cb + 2 * kQ);
+                    else load(0, cb + 2 * kQ);
+                }
+#pragma unroll
+                for (int k = 0; k < kLW; ++k) {
+                    T u[kQ];
+#pragma unroll
+                    for (int q = 0; q < kQ; ++q) u[q] = U12[k][cb + q];     // padded row: no bound check
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+                        for (int q = 0; q < kQ; ++q) acc[i][q] -= a[i][k] * u[q];
+                }
+#pragma unroll
+                for (int q = 0; q < kQ; ++q)
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i)
+                        if (gr[i] >= lim && cb + q < rw) W[gr[i] + (k0 + c1 + cb + q) * ldw] = acc[i][q];
+                buf ^= 1;
+            }
+            __syncthreads();
+        }
+    }
+    PH(6);
+#undef PH
+    if (prof)
+        for (int q = 0; q < 8; ++q) st->dbg_t[q] = (unsigned long long)ph[q];
+    if (tid == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
+    if (tr_max && tid == 0) atomicMax(tr_max, gtimer());
+}
+
 // ------------------------------------------------------------------ laswp
 // Apply the interchanges ipiv[j0 .. j0+cnt) (in order) to columns [a0, a1) U [b0, b1) and, if
 // perm != nullptr, to perm.  The cnt swaps compose into one permutation of the row set
@@ -714,9 +1103,66 @@ static LuStreams& lu_streams() {
     return L;
 }
 
+static int g_panel_dbg = 0;   // diagnostics: ablation mask of the register panel (lu_debug_panel_time)
+
+// Cluster size and rows per thread of the register panel: one CTA up to 1024 rows, then up to
+// 16 CTAs of <= 1024 rows (4 per thread); larger panels use the cooperative kernel.
+template <typename T>
+static bool leaf_panel_launch(const Work& w, int64_t k0, int nbp, int prio, cudaStream_t s) {
+    const int64_t n = w.n, m = n - k0;
+    static const int rpt_env = getenv("AS_LU_LEAF_RPT") ? atoi(getenv("AS_LU_LEAF_RPT")) : 4;
+    static int pmax = kLfMaxP;
+    if (nbp > kPW) return false;
+    for (;;) {
+        const int64_t cap = (int64_t)kPT * rpt_env;
+        int P = 1;
+        while (P < pmax && (m + P - 1) / P > cap) P *= 2;
+        const int64_t chunk = (m + P - 1) / P;
+        const int rpt = (int)((chunk + kPT - 1) / kPT);
+        if (rpt > 4) return false;
+        void* kern = rpt <= 1 ? (void*)lu_panel_reg_kernel<T, 1> : rpt <= 2 ? (void*)lu_panel_reg_kernel<T, 2>
+                                                                              : (void*)lu_panel_reg_kernel<T, 4>;
+        if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(P);
+        cfg.blockDim = dim3(kPT);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = s;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributePriority; at[1].val.priority = prio;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        LuTrace& tr = lu_trace();
+        const int slot = (int)(k0 / kBW) * 4 + ((k0 % kBW) ? 2 : 1);
+        unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
+        unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
+        // the cluster shape must be schedulable (checked outside the stream: a failing launch
+        // would invalidate a graph capture)
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0) {
+            T* Wp = (T*)w.W;
+            int64_t ldw = w.ldw;
+            int64_t* ip = w.ipiv;
+            DevState* stp = w.st;
+            int dbg = g_panel_dbg;
+            void* args[] = {&Wp, &ldw, (void*)&n, &k0, &nbp, &ip, &stp, &tmn, &tmx, &dbg};
+            const cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
+            if (e == cudaSuccess) return true;
+        }
+        cudaGetLastError();
+        if (pmax <= 1) return false;
+        pmax /= 2;                          // e.g. 16-CTA clusters not available: retry with 8
+    }
+}
+
 template <typename T>
 static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long seq_base, int prio, cudaStream_t s) {
     const int64_t n = w.n, m = n - k0;
+    // register/cluster panel: opt-in (AS_LU_PANEL=reg) until it beats the cooperative panel
+    static const bool use_reg = getenv("AS_LU_PANEL") && strcmp(getenv("AS_LU_PANEL"), "reg") == 0;
+    if (use_reg && getenv("AS_LU_PANEL_OLD") == nullptr && leaf_panel_launch<T>(w, k0, nbp, prio, s)) return;
     static const int rows_per_cta = getenv("AS_LU_PANEL_ROWS") ? atoi(getenv("AS_LU_PANEL_ROWS")) : 128;
     int P = (int)std::min<int64_t>(w.num_sms, (m + rows_per_cta - 1) / rows_per_cta);
     P = std::max(P, 1);
@@ -921,6 +1367,64 @@ int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int 
     cudaMemcpy(out_min, tr.tmin, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
     cudaMemcpy(out_max, tr.tmax, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
     return cnt;
+}
+
+// Diagnostics: average time (us) of one panel factorization of W (restored from Wsrc before each
+// launch).  kind 0: the launch the factorization would make; kind 1: the cooperative panel.
+double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
+                           int iters, int dbg) {
+    Work w{};
+    w.dtype = dtype; w.n = n; w.ldw = ldw; w.W = W;
+    cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaMalloc(&w.ipiv, 8 * n);
+    cudaMalloc(&w.st, sizeof(DevState));
+    cudaMalloc(&w.cand, 16 * 2 * 1024 + 8 * 2 * 1024 * 128 + 8 * 2 * 128);
+    cudaMemset(w.st, 0, sizeof(DevState));
+    cudaMemset(&w.st->info, 0xFF, 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    g_panel_dbg = dbg;
+    const size_t es = dtype == AS_F64 ? 8 : 4;
+    double tot = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        cudaMemcpy(W, Wsrc, es * ldw * n, cudaMemcpyDeviceToDevice);
+        cudaMemset(w.cand, 0, 16 * 2 * 1024);
+        cudaEventRecord(e0, 0);
+        if (dtype == AS_F64) {
+            if (kind != 0 || !leaf_panel_launch<double>(w, k0, nbp, 0, 0)) {
+                setenv("AS_LU_PANEL_OLD", "1", 1);
+                panel_launch<double>(w, k0, nbp, 0, 0, 0);
+                unsetenv("AS_LU_PANEL_OLD");
+            }
+        } else {
+            if (kind != 0 || !leaf_panel_launch<float>(w, k0, nbp, 0, 0)) {
+                setenv("AS_LU_PANEL_OLD", "1", 1);
+                panel_launch<float>(w, k0, nbp, 0, 0, 0);
+                unsetenv("AS_LU_PANEL_OLD");
+            }
+        }
+        cudaEventRecord(e1, 0);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it > 0 || iters == 1) tot += ms;
+    }
+    g_panel_dbg = 0;
+    if (dbg & 256) {
+        unsigned long long ph[16];
+        cudaMemcpy(ph, w.st->dbg_t, sizeof(ph), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "panel phases (cycles, CTA 0): push %llu cbar %llu winner+swap %llu update %llu reduce %llu "
+                        "leafend %llu deferred %llu\n", ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(w.ipiv);
+    cudaFree(w.st);
+    cudaFree(w.cand);
+    if (err != cudaSuccess) return -(double)err;
+    return 1000.0 * tot / (iters > 1 ? iters - 1 : 1);
 }
 
 void launch_lu_factor(const Work& w, cudaStream_t s) {

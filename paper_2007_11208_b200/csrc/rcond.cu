@@ -197,7 +197,7 @@ void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaSt
     for (int slot = 0; slot < kEstSlots; ++slot) {
         const bool trans = (slot & 1) != 0;
         auto tr = [&](const void* A, int64_t lda, const void* Dinv, bool up, bool t) {
-            launch_trsm(dt, A, lda, Dinv, up, t, w.xe, n, n, 1, sa.take(trsm_sync_words(n, 1)), slot, true, w.args,
+            launch_trsm(dt, A, lda, Dinv, up, t, w.xe, n, n, 1, sa, slot, true, w.args,
                         w.st, s);
         };
         switch (kind) {

@@ -17,16 +17,19 @@
 // parameters; "forward" order = (lower && !trans) || (upper && trans).
 #include "internal.h"
 #include "trsm.h"
+#include "blk64.cuh"
 
 namespace as {
 
 constexpr int kTsThreads = 256;
-constexpr int kTsR = 32;          // max RHS columns per CTA tile
+constexpr int kTsR = 8;           // max RHS columns per CTA tile (more, narrower tiles: shorter per-CTA chains)
 constexpr int kLDT = kNB + 1;     // padded smem leading dimension
 
 // ------------------------------------------------------------------ diagonal block inverse
 // Dinv block b (kNB x kNB, column-major, ld kNB) = inverse of the b-th diagonal
-// block of the stored triangle; padded with identity beyond n.
+// block of the stored triangle; padded with identity beyond n.  Upper blocks are
+// inverted as (U^T)^{-1} transposed, so both cases run block_trinv64 (16 x 16
+// substitutions + block diagonals) instead of 64 dependent column steps.
 template <typename T, bool UPPER, bool UNIT>
 __global__ void __launch_bounds__(kTsThreads) trtri_blocks_kernel(const T* __restrict__ A_, int64_t lda, int64_t n,
                                                                    T* __restrict__ Dinv, const DevState* st,
@@ -34,51 +37,34 @@ __global__ void __launch_bounds__(kTsThreads) trtri_blocks_kernel(const T* __res
     if (skip_if_singular && st->info != ~0ull) return;
     const T* A = A_ ? A_ : (const T*)args->A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* Ts = (T*)smem_raw;          // kNB x kLDT
-    T* Is = Ts + kNB * kLDT;       // kNB x kLDT
+    T* Ls = (T*)smem_raw;               // kB64 x kB64LD: the block as a lower triangle
+    T* Xs = Ls + kB64 * kB64LD;         // its inverse
+    T* tmp = Xs + kB64 * kB64LD;        // 3 * 256 scratch
     const int b = blockIdx.x;
     const int64_t o = (int64_t)b * kNB;
     const int nb = (int)min<int64_t>(kNB, n - o);
-    for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-        const int r = e % kNB, c = e / kNB;
-        T v = T(0);
-        if (r < nb && c < nb) {
-            const bool in_tri = UPPER ? (r <= c) : (r >= c);
-            if (in_tri) v = A[(o + r) + (o + c) * lda];
-            if (r == c && UNIT) v = T(1);
-        } else if (r == c) {
-            v = T(1);
-        }
-        Ts[r + c * kLDT] = v;
-    }
-    __syncthreads();
-    // column c of the inverse solves T x = e_c; threads split columns x 4 row-phases
-    // (simple and exact enough: one thread per column, sequential substitution)
-    if (threadIdx.x < kNB) {
-        const int c = threadIdx.x;
-        if (!UPPER) {
-            for (int r = 0; r < kNB; ++r) {
-                T s = (r == c) ? T(1) : T(0);
-                if (r > c) {
-                    for (int k = c; k < r; ++k) s -= Ts[r + k * kLDT] * Is[k + c * kLDT];
-                }
-                Is[r + c * kLDT] = (r < c) ? T(0) : s / Ts[r + r * kLDT];
+    batched<8, T>(
+        kNB * kNB,
+        [&](int e) -> T {
+            const int r = e % kNB, c = e / kNB;      // element (r, c) of the stored block
+            if (r < nb && c < nb) {
+                if (r == c) return UNIT ? T(1) : A[(o + r) + (o + c) * lda];
+                const bool in_tri = UPPER ? (r < c) : (r > c);
+                return in_tri ? A[(o + r) + (o + c) * lda] : T(0);
             }
-        } else {
-            for (int r = kNB - 1; r >= 0; --r) {
-                T s = (r == c) ? T(1) : T(0);
-                if (r < c) {
-                    for (int k = r + 1; k <= c; ++k) s -= Ts[r + k * kLDT] * Is[k + c * kLDT];
-                }
-                Is[r + c * kLDT] = (r > c) ? T(0) : s / Ts[r + r * kLDT];
-            }
-        }
-    }
+            return r == c ? T(1) : T(0);
+        },
+        [&](int e, T v) {
+            const int r = e % kNB, c = e / kNB;
+            if (UPPER) Ls[c + r * kB64LD] = v;       // transpose: U^T is lower
+            else Ls[r + c * kB64LD] = v;
+        });
     __syncthreads();
+    block_trinv64<T, UNIT>(Ls, Xs, tmp);
     T* D = Dinv + (int64_t)b * kNB * kNB;
     for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
         const int r = e % kNB, c = e / kNB;
-        D[r + c * kNB] = Is[r + c * kLDT];
+        D[r + c * kNB] = UPPER ? Xs[c + r * kB64LD] : Xs[r + c * kB64LD];
     }
 }
 
@@ -88,10 +74,39 @@ struct TsArgs {
     const void* Dinv;
     void* X; int64_t ldx;            // in/out (nullptr: args->X with ldx)
     int64_t n; int nrhs;
-    unsigned* sync;                  // [0] = ticket, [1..] = flags (nblk * ntiles), zeroed per solve
+    unsigned* sync;                  // [0] = ticket, zeroed per solve
+    unsigned long long* ll;          // published X blocks, every word tagged with the solve epoch
     int slot;                        // estimator slot gate (-1: none)
     int skip_if_singular;
 };
+
+// Published X blocks ("LL" words, the tag travels with the data, so one load is both the
+// readiness test and the data): element (i, c) of block b, tile rt at word
+// ((b * ntiles + rt) * RT + c) * kNB + i; fp64 values as two words {lo32 | epoch << 32,
+// hi32 | epoch << 32} (each 8-byte word is written and read as one access), fp32 as one.
+template <typename T> struct LLw { static constexpr int v = sizeof(T) / 4; };
+AS_DEV void ll_put(unsigned long long* w, double x, unsigned ep) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned long long hi = ((unsigned long long)ep << 32);
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(w), "l"(hi | (b & 0xffffffffull)), "l"(hi | (b >> 32))
+                 : "memory");
+}
+AS_DEV void ll_put(unsigned long long* w, float x, unsigned ep) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(w),
+                 "l"(((unsigned long long)ep << 32) | (unsigned long long)__float_as_uint(x)) : "memory");
+}
+AS_DEV bool ll_get(const unsigned long long* w, unsigned ep, double& x) {
+    unsigned long long a, b;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(w) : "memory");
+    x = __longlong_as_double((long long)(((b & 0xffffffffull) << 32) | (a & 0xffffffffull)));
+    return (unsigned)(a >> 32) == ep && (unsigned)(b >> 32) == ep;
+}
+AS_DEV bool ll_get(const unsigned long long* w, unsigned ep, float& x) {
+    unsigned long long a;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(a) : "l"(w) : "memory");
+    x = __uint_as_float((unsigned)(a & 0xffffffffull));
+    return (unsigned)(a >> 32) == ep;
+}
 
 // One 64 x 64 block times a 64 x RT tile.  RT == 1: thread (row i, k-quarter q) -> part[0]
 // (the four quarters are summed through shared memory).  RT >= 4: thread (row i, column
@@ -159,6 +174,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     const int ntiles = (p.nrhs + RT - 1) / RT;
     constexpr bool FWD = (!UPPER && !TRANS) || (UPPER && TRANS);
 
+    const unsigned ep = st->epoch;
     if (threadIdx.x == 0) s_ticket = atomicAdd(&p.sync[0], 1u);
     __syncthreads();
     const unsigned t = s_ticket;
@@ -207,17 +223,18 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         T* Ms = (sp & 1) ? Mb1 : Mb0;
         if (sp + 1 < s) stage((sp & 1) ? Mb0 : Mb1, sp + 1);
         else stage_dinv(Ds);                    // last step: Dinv_b into the free buffer
-        // wait for X_j (tile rt)
-        if (threadIdx.x == 0) {
-            const unsigned* f = &p.sync[1 + j * ntiles + rt];
-            while (ld_acquire(f) == 0u) { __nanosleep(20); }   // (relaxed poll + fence measured slower here)
+        // X_j (tile rt): each thread spins on its own tagged words until the producer's epoch shows
+        (void)oj; (void)nbj;
+        {
+            const unsigned long long* src = p.ll + ((int64_t)(j * ntiles + rt) * RT) * kNB * LLw<T>::v;
+            for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
+                const int r = e % kNB, c = e / kNB;
+                T x;
+                while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x)) {}
+                Xs[r + c * kLDX] = x;
+            }
         }
         asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-        for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
-            const int r = e % kNB, c = e / kNB;
-            Xs[r + c * kLDX] = (r < nbj && c < R) ? __ldcg(&X[(oj + r) + (c0 + c) * p.ldx]) : T(0);
-        }
         __syncthreads();
         block_product<T, TRANS, RT>(Ms, Xs, part, R);
         if (RT == 1) {
@@ -240,33 +257,46 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     }
     __syncthreads();
     block_product<T, TRANS, RT>(Ds, Xs, part, R);
+    unsigned long long* dst = p.ll + ((int64_t)(b * ntiles + rt) * RT) * kNB * LLw<T>::v;
     if (RT == 1) {
         Red[g * kNB + i] = part[0];
         __syncthreads();
-        if (g == 0 && i < nbr) X[(ob + i) + c0 * p.ldx] = (Red[i] + Red[kNB + i]) + (Red[2 * kNB + i] + Red[3 * kNB + i]);
-    } else if (i < nbr) {
+        if (g == 0) {
+            const T x = (Red[i] + Red[kNB + i]) + (Red[2 * kNB + i] + Red[3 * kNB + i]);
+            ll_put(dst + (int64_t)i * LLw<T>::v, i < nbr ? x : T(0), ep);
+            if (i < nbr) X[(ob + i) + c0 * p.ldx] = x;
+        }
+    } else {
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int c = g + 4 * u;
-            if (c < R) X[(ob + i) + (c0 + c) * p.ldx] = part[u];
+            const T x = (i < nbr && c < R) ? part[u] : T(0);
+            ll_put(dst + (int64_t)(c * kNB + i) * LLw<T>::v, x, ep);
+            if (i < nbr && c < R) X[(ob + i) + (c0 + c) * p.ldx] = x;
         }
     }
-    __syncthreads();   // release is cumulative over the CTA's X stores ordered by this barrier
-    if (threadIdx.x == 0) st_release(&p.sync[1 + b * ntiles + rt], 1u);
 }
 
 // ------------------------------------------------------------------ launchers
 int64_t trsm_sync_words(int64_t n, int nrhs) {
+    (void)n; (void)nrhs;
+    return 2;
+}
+
+static int ts_rt(int nrhs) { return nrhs == 1 ? 1 : nrhs <= 4 ? 4 : kTsR; }
+
+int64_t trsm_ll_words(int64_t n, int nrhs) {
     const int64_t nblk = (n + kNB - 1) / kNB;
-    const int64_t ntiles = (nrhs + kTsR - 1) / kTsR;
-    return 1 + nblk * ntiles;
+    const int rt = ts_rt(nrhs);
+    const int64_t ntiles = (nrhs + rt - 1) / rt;
+    return nblk * ntiles * rt * kNB * 2;      // 2 words per element covers fp64
 }
 
 template <typename T>
 static void trtri_dispatch(const T* A, int64_t lda, int64_t n, T* Dinv, bool upper, bool unit, const DevState* st,
                            bool skip, const DevArgs* args, cudaStream_t s) {
     const int nblk = (int)((n + kNB - 1) / kNB);
-    const int smem = (int)(sizeof(T) * 2 * kNB * kLDT);
+    const int smem = (int)(sizeof(T) * (2 * kB64 * kB64LD + 3 * 256));
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         kern<<<nblk, kTsThreads, smem, s>>>(A, lda, n, Dinv, st, skip, args);
@@ -296,14 +326,12 @@ static void trsm_dispatch(const TsArgs& p, bool upper, bool trans, const DevArgs
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk * ntiles, kTsThreads, smem, s>>>(p, args, st);
     };
-    auto by_r = [&](auto k1, auto k4, auto k16, auto k32) {
+    auto by_r = [&](auto k1, auto k4, auto k8) {
         if (p.nrhs == 1) go(k1, 1, ts_smem<T, 1>());
         else if (p.nrhs <= 4) go(k4, 4, ts_smem<T, 4>());
-        else if (p.nrhs <= 16) go(k16, 16, ts_smem<T, 16>());
-        else go(k32, kTsR, ts_smem<T, kTsR>());
+        else go(k8, kTsR, ts_smem<T, kTsR>());
     };
-#define AS_TS(U, TR) trsm_sf_kernel<T, U, TR, 1>, trsm_sf_kernel<T, U, TR, 4>, trsm_sf_kernel<T, U, TR, 16>, \
-                     trsm_sf_kernel<T, U, TR, kTsR>
+#define AS_TS(U, TR) trsm_sf_kernel<T, U, TR, 1>, trsm_sf_kernel<T, U, TR, 4>, trsm_sf_kernel<T, U, TR, kTsR>
     if (upper) {
         if (trans) by_r(AS_TS(true, true));
         else by_r(AS_TS(true, false));
@@ -315,9 +343,10 @@ static void trsm_dispatch(const TsArgs& p, bool upper, bool trans, const DevArgs
 }
 
 void launch_trsm(int dtype, const void* A, int64_t lda, const void* Dinv, bool upper, bool trans, void* X,
-                 int64_t ldx, int64_t n, int nrhs, unsigned* sync, int slot, bool skip_if_singular,
+                 int64_t ldx, int64_t n, int nrhs, SyncAlloc& sa, int slot, bool skip_if_singular,
                  const DevArgs* args, const DevState* st, cudaStream_t s) {
-    TsArgs p{A, lda, Dinv, X, ldx, n, nrhs, sync, slot, skip_if_singular ? 1 : 0};
+    TsArgs p{A, lda, Dinv, X, ldx, n, nrhs, sa.take(trsm_sync_words(n, nrhs)), sa.take_ll(trsm_ll_words(n, nrhs)), slot,
+             skip_if_singular ? 1 : 0};
     if (n <= 0 || nrhs <= 0) return;
     if (dtype == AS_F64) trsm_dispatch<double>(p, upper, trans, args, st, s);
     else trsm_dispatch<float>(p, upper, trans, args, st, s);

@@ -122,7 +122,7 @@ def test_detect_configs_full_size(tag):
 
 
 # ------------------------------------------------------------------ solves, small sizes spanning tiles
-@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 65, 200, 333])
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 65, 200, 333, 700, 1100])
 def test_lu_dense(n):
     A = W.random_dense(n, seed=n, shift=2.0)
     B = np.asfortranarray(np.random.default_rng(n).standard_normal((n, 3)))
@@ -158,7 +158,7 @@ def test_triangular(n, upper):
     assert rep["primary_method"] == (oracle.M_TRI_UPPER if upper else oracle.M_TRI_LOWER)
 
 
-@pytest.mark.parametrize("n", [4, 63, 64, 150, 257])
+@pytest.mark.parametrize("n", [4, 63, 64, 150, 257, 1000, 2100])
 def test_spd(n):
     A = W.random_spd_fig3(n, seed=n)
     B = np.asfortranarray(np.random.default_rng(3).standard_normal((n, 4)))
