@@ -441,28 +441,59 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
 }
 
 // ------------------------------------------------------------------ panel (leaf-blocked, one cluster)
-// The panel's m rows are split over the P <= 16 CTAs of one thread-block cluster, RPT <= 4 rows per
-// thread (row tid + 256 i of the CTA's chunk).  The panel's columns are factored in leaves of
-// kLW = 16 columns held in REGISTERS (compile-time column index: the column loop is unrolled); the
-// rest of the panel stays in global memory (L2) and receives one deferred rank-16 update per leaf.
-// Per column:
-//   every CTA pushes its first-max candidate (|value|, row, the row's 16 leaf values) -- and the
-//   owner of row g its old row g -- into every CTA's shared memory (remote DSMEM stores), one
-//   cluster barrier, every thread picks the winner from local shared memory (first-max tie-break,
-//   Z15), the owners of g and p swap the two rows, the rank-1 update runs in registers together
-//   with the next column's candidate search, one CTA barrier for the candidate reduction.
-// Per leaf: the leaf's interchanges composed into one permutation of <= 32 rows and applied to
+// The panel's m rows are split over the P <= 16 CTAs of one thread-block cluster, RPT rows per
+// thread (row tid + 256 i of the CTA's chunk).  The columns are factored in leaves of KLW columns
+// held in REGISTERS (RPT x KLW = 64 values per thread); the rest of the panel stays in global
+// memory (L2) and receives one deferred rank-KLW update per leaf.  Rows are kept ROTATED: at leaf
+// step jj, a[i][k] holds leaf column (jj + k) mod KLW, so the current column is a[i][0], every
+// register index is a compile-time constant and the column loop stays compact (not unrolled).
+// Per column (first-max tie-break, Z15; a NaN diagonal keeps its row, as the serial sweep does):
+//   warp argmax = fmax shuffle + ballot + integer min-reduction of the row index; the winning
+//   lane stores its (rotated) row, the owner of row g its row g; ONE CTA barrier; every thread
+//   merges the 8 warp results.  P > 1: each CTA's winner (value, index, row) -- and row g from
+//   its owner -- is pushed into every CTA with st.async, which completes the receiver's mbarrier
+//   transaction count: data and signal arrive together, no cluster barrier, no fence.
+//   Then: swap of rows g and p (their owners), multipliers, rank-1 update in registers.
+// Per leaf: the leaf's interchanges composed into one permutation of <= 2 KLW rows and applied to
 // the panel's other columns; U12 = L11^{-1} A12 for the leaf's pivot rows; A22 -= L21 U12 for the
-// rows below.  The result (W rows interchanged within the panel, ipiv) is the unblocked column
-// sweep's up to rounding.
+// rows below.  Result (rows interchanged within the panel, ipiv): the unblocked column sweep's up
+// to rounding.
 constexpr int kLfMaxP = 16;
-constexpr int kLW = 16;
-constexpr int kURW = kPW - kLW + 16;  // + padding: vector reads past the last column
 
-template <typename T, int RPT>
-__global__ void __launch_bounds__(kPT, 1) lu_panel_reg_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
-                                                               int64_t* ipiv, DevState* st, unsigned long long* tr_min,
-                                                               unsigned long long* tr_max, int dbg) {
+template <typename T, int KLW>
+struct LeafSmem {
+    T rowbuf[2][1][KLW];                 // the CTA winner's row (rotated)
+    T gbuf[2][KLW];                      // row g (rotated), CTA-local
+    T crow[2][kLfMaxP][KLW];             // cluster: every CTA's candidate row
+    T cgrow[2][KLW];                     // cluster: row g
+    T Ub[KLW][KLW];                      // pivot rows of the leaf, natural column order
+    T U12[KLW][kPW - KLW + 16];          // + padding: vector reads past the last column
+    unsigned long long cvi[2][kLfMaxP][2];   // cluster: (value bits, index) per CTA
+    unsigned long long mbar[2];
+    T wval[2][kPT / 32];
+    int widx[2][kPT / 32];
+    int64_t s_piv[kPW];
+    int64_t s_src[2 * KLW], s_dst[2 * KLW];
+    int s_np;
+};
+
+template <typename T> AS_DEV unsigned long long t_bits(T v);
+template <> AS_DEV unsigned long long t_bits<double>(double v) { return (unsigned long long)__double_as_longlong(v); }
+template <> AS_DEV unsigned long long t_bits<float>(float v) { return (unsigned long long)__float_as_uint(v); }
+template <typename T> AS_DEV T t_from(unsigned long long b);
+template <> AS_DEV double t_from<double>(unsigned long long b) { return __longlong_as_double((long long)b); }
+template <> AS_DEV float t_from<float>(unsigned long long b) { return __uint_as_float((unsigned)b); }
+template <typename T>
+AS_DEV void push_elem(const T* local_dst, unsigned rank, T v, unsigned rbar) {
+    const unsigned ra = mapa_u32(smem_u32(local_dst), rank);
+    if (sizeof(T) == 8) st_async_b64(ra, t_bits<T>(v), rbar);
+    else st_async_b32(ra, (unsigned)t_bits<T>(v), rbar);
+}
+
+template <typename T, int RPT, int KLW>
+__global__ void __launch_bounds__(kPT, 1) lu_panel_fast_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+                                                                int64_t* ipiv, DevState* st, unsigned long long* tr_min,
+                                                                unsigned long long* tr_max, int dbg) {
     cg::cluster_group cl = cg::this_cluster();
     if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
     const int P = (int)cl.num_blocks(), cta = (int)cl.block_rank();
@@ -470,231 +501,196 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_reg_kernel(T* W, int64_t ldw,
     const int64_t chunk = (m + P - 1) / P;
     const int64_t rbeg = k0 + (int64_t)cta * chunk;
     const int64_t rend = min(n, rbeg + chunk);
-    __shared__ T crow[2][kLfMaxP][kLW];      // pushed candidate rows (leaf values)
-    __shared__ T grow[2][kLW];               // pushed old row g
-    __shared__ T cval[2][kLfMaxP];
-    __shared__ int cidx[2][kLfMaxP];
-    __shared__ T Ub[kLW][kLW];               // pivot rows of the leaf (L11 \ U11)
-    __shared__ T stg[2][kLW];                // staging of the rows this CTA pushes
-    __shared__ T U12[kLW][kURW];
-    __shared__ T red_v[8];
-    __shared__ int red_i[8];
-    __shared__ int red_dn[8];
-    __shared__ int64_t s_piv[kPW];
-    __shared__ int64_t s_src[2 * kLW], s_dst[2 * kLW];
-    __shared__ int s_np;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LeafSmem<T, KLW>& S = *reinterpret_cast<LeafSmem<T, KLW>*>(smem_raw);
+    constexpr int URW = kPW - KLW + 16;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kNone = 0x7fffffff;        // row positions fit in int (n <= 2^31 - 1)
     int gr[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) gr[i] = (rbeg + tid + (int64_t)kPT * i < rend) ? (int)(rbeg + tid + (int64_t)kPT * i) : -1;
-    T a[RPT][kLW];
-
+    T a[RPT][KLW];
     auto cbar = [&]() {
         if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         else __syncthreads();
     };
-    // CTA-wide first-max over this thread's partial (bv, bi, dn); NaN at row gd keeps gd
-    auto merge = [](T& v, int& i, T v2, int i2) { if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; } };
-    auto reduce = [&](T bv, int bi, int dn, int gd, T& v, int& idx) {
+    if (P > 1) {
+        if (tid == 0) { mbar_init(&S.mbar[0], 1); mbar_init(&S.mbar[1], 1); mbar_fence_init_cluster(); }
+        cbar();
+    }
+    // local first-max over my rows at positions >= gmin for the current (rotated) column
+    auto local_cand = [&](int gmin, T& lv, int& li) {
+        lv = T(-1);
+        li = kNone;
+        bool dn = false;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-            merge(bv, bi, v2, i2);
+        for (int i = 0; i < RPT; ++i) {
+            if (gr[i] >= gmin) {
+                T x = a[i][0];
+                x = x < T(0) ? -x : x;
+                if (gr[i] == gmin && x != x) dn = true;
+                if (x > lv) { lv = x; li = gr[i]; }      // rows increase with i: strict > keeps the first
+            }
         }
-        dn = __any_sync(0xffffffffu, dn);
-        if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; red_dn[warp] = dn; }
-        __syncthreads();
-        // every warp merges the 8 partials as a 3-level shuffle tree (lanes 0..7)
-        v = red_v[lane & 7];
-        idx = red_i[lane & 7];
-        int d = red_dn[lane & 7];
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-            const T v2 = __shfl_xor_sync(0xffffffffu, v, o);
-            const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
-            merge(v, idx, v2, i2);
-            d |= __shfl_xor_sync(0xffffffffu, d, o);
-        }
-        if (d) { v = T(INFINITY); idx = gd; }
+        if (dn) { lv = T(INFINITY); li = gmin; }
     };
 
     unsigned long long info = ~0ull;
-    // diagnostics (dbg & 256): clock64 phase totals of CTA 0 / thread 0 into st->dbg_t
-    const bool prof = (dbg & 256) && cta == 0 && tid == 0;
-    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long tp = clock64();
-#define PH(k) do { if (prof) { const long long t_ = clock64(); ph[k] += t_ - tp; tp = t_; } } while (0)
-    for (int c0 = 0; c0 < nbp; c0 += kLW) {
-        const int w = min(kLW, nbp - c0);
+    int uses = 0;                             // columns processed (mbarrier phase bookkeeping)
+    for (int c0 = 0; c0 < nbp; c0 += KLW) {
+        const int w = min(KLW, nbp - c0);
         const int g0 = (int)(k0 + c0);
-        // leaf columns of my active rows (positions >= g0) into registers
 #pragma unroll
-        for (int c = 0; c < kLW; ++c)
+        for (int c = 0; c < KLW; ++c)
 #pragma unroll
             for (int i = 0; i < RPT; ++i)
                 a[i][c] = (gr[i] >= g0 && c < w) ? W[gr[i] + (k0 + c0 + c) * ldw] : T(0);
-        T v;
-        int idx;
-        {
-            T bv = T(-1);
-            int bi = kNone;
-            int dn = 0;
+        T lv;
+        int li;
+        local_cand(g0, lv, li);
+        if ((dbg & 8) && tid < w) S.s_piv[c0 + tid] = g0 + tid;   // ablation: no interchanges
+        for (int jj = 0; jj < (dbg & 8 ? 0 : w); ++jj, ++uses) {
+            const int c = c0 + jj;
+            const int g = (int)(k0 + c);
+            const int par = uses & 1;
+            // ---- warp argmax: value by fmax shuffles, index by ballot + min-reduction
+            T wm = lv;
 #pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                if (gr[i] >= g0) {
-                    T x = a[i][0];
-                    x = x < T(0) ? -x : x;
-                    if (gr[i] == g0 && x != x) dn = 1;
-                    merge(bv, bi, x, gr[i]);
-                }
-            reduce(bv, bi, dn, g0, v, idx);
-        }
-        // Column loop, NOT unrolled (an unrolled leaf is ~200 KB of code: instruction-cache bound).
-        // Each row is kept ROTATED in registers: at step jj, a[i][k] holds leaf column (jj + k) mod 16,
-        // so the current column is always a[i][0] and every register index is a compile-time
-        // constant; the finished column rotates to the end (after 16 steps the order is restored).
-        for (int jj = 0; jj < (dbg & 8 ? 0 : w); ++jj) {
-            {
-                const int c = c0 + jj;
-                const int g = (int)(k0 + c);
-                const int par = c & 1;
-                // ---- push: candidate (value, index, leaf row), and the owner of g its row g.  The
-                // rows are staged in this CTA's shared memory by their owner thread, then the lanes
-                // of its warp push them to every CTA (warp-uniform branches: other warps skip)
-                if (tid < P) {
-                    T* rv = cl.map_shared_rank(&cval[par][0], tid);
-                    int* ri = cl.map_shared_rank(&cidx[par][0], tid);
-                    rv[cta] = v;
-                    ri[cta] = idx;
-                }
-                {
-                    const int64_t oc = (idx != kNone && idx >= rbeg && idx < rend) ? idx - rbeg : -1;
-                    const int64_t og = (g >= rbeg && g < rend) ? g - rbeg : -1;
-                    const int wc = oc >= 0 ? (int)((oc & (kPT - 1)) >> 5) : -1;
-                    const int wg = og >= 0 ? (int)((og & (kPT - 1)) >> 5) : -1;
-                    if (warp == wc || warp == wg) {
-                        if (oc >= 0 && tid == (int)(oc & (kPT - 1))) {
-                            const int ic = (int)(oc >> 8);
+            for (int o = 16; o > 0; o >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+            const unsigned wi = __reduce_min_sync(0xffffffffu, (lv == wm && li != kNone) ? (unsigned)li : (unsigned)kNone);
+            if (lane == 0) { S.wval[par][warp] = wi == (unsigned)kNone ? T(-1) : wm; S.widx[par][warp] = (int)wi; }
+            __syncthreads();
+            // ---- CTA winner (every thread); its owner stores the row, the owner of g row g
+            // (warp-uniform branches: only the owners' warps execute the row copies)
+            T cv = T(-1);
+            int ci = kNone;
 #pragma unroll
-                            for (int i = 0; i < RPT; ++i)
-                                if (i == ic)
-#pragma unroll
-                                    for (int k = 0; k < kLW; ++k) stg[0][(jj + k) & (kLW - 1)] = a[i][k];
-                        }
-                        if (og >= 0 && tid == (int)(og & (kPT - 1))) {
-                            const int ig = (int)(og >> 8);
-#pragma unroll
-                            for (int i = 0; i < RPT; ++i)
-                                if (i == ig)
-#pragma unroll
-                                    for (int k = 0; k < kLW; ++k) stg[1][(jj + k) & (kLW - 1)] = a[i][k];
-                        }
-                        __syncwarp();
-                        if (warp == wc)
-                            for (int e = lane; e < P * kLW; e += 32) {
-                                T* rr = cl.map_shared_rank(&crow[par][cta][0], e / kLW);
-                                rr[e % kLW] = stg[0][e % kLW];
-                            }
-                        if (warp == wg)
-                            for (int e = lane; e < P * kLW; e += 32) {
-                                T* rg = cl.map_shared_rank(&grow[par][0], e / kLW);
-                                rg[e % kLW] = stg[1][e % kLW];
-                            }
-                    }
-                }
-                PH(0);
-                cbar();
-                PH(1);
-                // ---- winner from local shared memory
-                T bv = T(-1);
-                int bi = kNone;
-                int bo = 0;
-                for (int q = 0; q < P; ++q) {
-                    const T cv = cval[par][q];
-                    const int ci = cidx[par][q];
-                    if (cv > bv || (cv == bv && ci < bi)) { bv = cv; bi = ci; bo = q; }
-                }
-                const int p = bi;
-                const T* ub = &crow[par][bo][0];
-                const T piv = ub[jj];
-                const bool elim = piv != T(0);
-                if (tid < kLW) Ub[jj][tid] = ub[tid];
-                if (tid == 0) s_piv[c] = (p == kNone) ? g : p;
-                if (!elim) {
-                    if (info == ~0ull) info = (unsigned long long)(g + 1);
-                } else if (p != g) {
-                    const int64_t og = (g >= rbeg && g < rend) ? g - rbeg : -1;
-                    const int64_t op = (p >= rbeg && p < rend) ? p - rbeg : -1;
-                    if ((og >= 0 && warp == (int)((og & (kPT - 1)) >> 5)) || (op >= 0 && warp == (int)((op & (kPT - 1)) >> 5))) {
-#pragma unroll
-                        for (int i = 0; i < RPT; ++i) {
-                            if (gr[i] == g) {
-#pragma unroll
-                                for (int k = 0; k < kLW; ++k) a[i][k] = ub[(jj + k) & (kLW - 1)];
-                            } else if (gr[i] == p) {
-#pragma unroll
-                                for (int k = 0; k < kLW; ++k) a[i][k] = grow[par][(jj + k) & (kLW - 1)];
-                            }
-                        }
-                    }
-                }
-                PH(2);
-                // ---- multipliers, rank-1 update (registers), rotation, next column's candidate
-                T u[kLW];                                    // u[k] = pivot row at column jj + k
-#pragma unroll
-                for (int k = 1; k < kLW; ++k) u[k] = ub[(jj + k) & (kLW - 1)];
-                const int nlive = kLW - jj;                  // a[.][k] for k < nlive are leaf columns >= jj
-                T nb = T(-1);
-                int ni = kNone;
-                int dn = 0;
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                    T x0 = a[i][0];
-                    if (gr[i] > g && elim && !(dbg & 16)) {
-                        const T l = x0 / piv;
-                        x0 = l;
-#pragma unroll
-                        for (int k = 1; k < kLW; ++k)
-                            if (k < nlive) a[i][k] -= l * u[k];
-                    }
-#pragma unroll
-                    for (int k = 0; k < kLW - 1; ++k) a[i][k] = a[i][k + 1];
-                    a[i][kLW - 1] = x0;
-                    if (gr[i] > g) {
-                        T x = a[i][0];
-                        x = x < T(0) ? -x : x;
-                        if (gr[i] == g + 1 && x != x) dn = 1;
-                        merge(nb, ni, x, gr[i]);
-                    }
-                }
-                PH(3);
-                if (jj + 1 < w) {
-                    if (dbg & 64) { v = nb; idx = ni; __syncthreads(); }
-                    else reduce(nb, ni, dn, g + 1, v, idx);
-                }
-                PH(4);
+            for (int q = 0; q < kPT / 32; ++q) {
+                const T v = S.wval[par][q];
+                const int ix = S.widx[par][q];
+                if (v > cv || (v == cv && ix < ci)) { cv = v; ci = ix; }
             }
+            const int cw = 0;
+            {
+                const int wc = (ci != kNone) ? (int)(((int64_t)ci - rbeg) & (kPT - 1)) >> 5 : -1;
+                const int wg = (g >= rbeg && g < rend) ? (int)(((int64_t)g - rbeg) & (kPT - 1)) >> 5 : -1;
+                if (warp == wc) {
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i)
+                        if (gr[i] == ci)
+#pragma unroll
+                            for (int k = 0; k < KLW; ++k) S.rowbuf[par][0][k] = a[i][k];
+                }
+                if (warp == wg) {
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i)
+                        if (gr[i] == g)
+#pragma unroll
+                            for (int k = 0; k < KLW; ++k) S.gbuf[par][k] = a[i][k];
+                }
+            }
+            __syncthreads();
+            int p = ci;
+            const T* prow = &S.rowbuf[par][cw][0];
+            const T* grw = &S.gbuf[par][0];
+            if (P > 1) {
+                // ---- cluster exchange: push (value, index, row) and row g into every CTA
+                const unsigned bar_l = smem_u32(&S.mbar[par]);
+                if (warp == 0) {
+                    for (int e = lane; e < P * (KLW + 2); e += 32) {
+                        const int q = e / (KLW + 2), k = e - q * (KLW + 2);
+                        const unsigned rb = mapa_u32(bar_l, q);
+                        if (k < KLW) push_elem<T>(&S.crow[par][cta][k], q, S.rowbuf[par][cw][k], rb);
+                        else if (k == KLW) st_async_b64(mapa_u32(smem_u32(&S.cvi[par][cta][0]), q), t_bits<double>((double)cv), rb);
+                        else st_async_b64(mapa_u32(smem_u32(&S.cvi[par][cta][1]), q), (unsigned long long)(unsigned)ci, rb);
+                    }
+                } else if (warp == 1 && g >= rbeg && g < rend) {
+                    for (int e = lane; e < P * KLW; e += 32) {
+                        const int q = e / KLW, k = e - q * KLW;
+                        push_elem<T>(&S.cgrow[par][k], q, S.gbuf[par][k], mapa_u32(bar_l, q));
+                    }
+                }
+                if (tid == 0) mbar_arrive_expect_tx(&S.mbar[par], (unsigned)(P * (KLW * sizeof(T) + 16) + KLW * sizeof(T)));
+                const unsigned ph = (unsigned)((uses >> 1) & 1);
+                while (!mbar_try_wait_cluster(&S.mbar[par], ph)) {}
+                T bv = T(-1);
+                int bi = kNone, bo = 0;
+                for (int q = 0; q < P; ++q) {
+                    const T v = (T)t_from<double>(S.cvi[par][q][0]);
+                    const int ix = (int)(unsigned)S.cvi[par][q][1];
+                    if (v > bv || (v == bv && ix < bi)) { bv = v; bi = ix; bo = q; }
+                }
+                p = bi;
+                prow = &S.crow[par][bo][0];
+                grw = &S.cgrow[par][0];
+            }
+            const T piv = prow[0];
+            const bool elim = piv != T(0);
+            if (tid < KLW) S.Ub[jj][(jj + tid) % KLW] = prow[tid];
+            if (tid == 0) S.s_piv[c] = (p == kNone) ? g : p;
+            if (!elim) {
+                if (info == ~0ull) info = (unsigned long long)(g + 1);
+            } else if (p != g) {
+                const int wg = (g >= rbeg && g < rend) ? (int)(((int64_t)g - rbeg) & (kPT - 1)) >> 5 : -1;
+                const int wp = (p >= rbeg && p < rend) ? (int)(((int64_t)p - rbeg) & (kPT - 1)) >> 5 : -1;
+                if (warp == wg || warp == wp) {
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        if (gr[i] == g) {
+#pragma unroll
+                            for (int k = 0; k < KLW; ++k) a[i][k] = prow[k];
+                        } else if (gr[i] == p) {
+#pragma unroll
+                            for (int k = 0; k < KLW; ++k) a[i][k] = grw[k];
+                        }
+                    }
+                }
+            }
+            // ---- multipliers, rank-1 update (registers), rotation, next column's local candidate
+            const int nlive = KLW - jj;
+            T l[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const bool below = gr[i] > g && elim;
+                l[i] = below ? a[i][0] / piv : T(0);
+                if (below) a[i][0] = l[i];
+            }
+#pragma unroll
+            for (int k = 1; k < KLW; ++k) {
+                if (k < nlive) {
+                    const T uk = prow[k];
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) a[i][k] -= l[i] * uk;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const T x0 = a[i][0];
+#pragma unroll
+                for (int k = 0; k < KLW - 1; ++k) a[i][k] = a[i][k + 1];
+                a[i][KLW - 1] = x0;
+            }
+            local_cand(g + 1, lv, li);
         }
-        // short leaf (w < 16): finish the rotation so that a[.][c] is leaf column c again
-        if (w < kLW && !(dbg & 8))
-            for (int r = w; r < kLW; ++r)
+        // short leaf: finish the rotation so that a[.][c] is leaf column c again
+        if (w < KLW && !(dbg & 8))
+            for (int r = w; r < KLW; ++r)
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) {
                     const T x0 = a[i][0];
 #pragma unroll
-                    for (int k = 0; k < kLW - 1; ++k) a[i][k] = a[i][k + 1];
-                    a[i][kLW - 1] = x0;
+                    for (int k = 0; k < KLW - 1; ++k) a[i][k] = a[i][k + 1];
+                    a[i][KLW - 1] = x0;
                 }
         // ---- leaf end: write back, pivots, the leaf's interchanges on the panel's other columns
 #pragma unroll
-        for (int c = 0; c < kLW; ++c)
+        for (int cc = 0; cc < KLW; ++cc)
 #pragma unroll
             for (int i = 0; i < RPT; ++i)
-                if (gr[i] >= g0 && c < w) W[gr[i] + (k0 + c0 + c) * ldw] = a[i][c];
-        if (cta == 0 && tid < w) ipiv[g0 + tid] = s_piv[c0 + tid];
-        if (tid == 0) s_np = 0;
+                if (gr[i] >= g0 && cc < w) W[gr[i] + (k0 + c0 + cc) * ldw] = a[i][cc];
+        __syncthreads();
+        if (cta == 0 && tid < w) ipiv[g0 + tid] = S.s_piv[c0 + tid];
+        if (tid == 0) S.s_np = 0;
         __syncthreads();
         if (tid < 2 * w) {
             const int t = tid;
@@ -702,126 +698,124 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_reg_kernel(T* W, int64_t ldw,
             bool go = true;
             if (t < w) x = g0 + t;
             else {
-                x = s_piv[c0 + t - w];
+                x = S.s_piv[c0 + t - w];
                 if (x < g0 + w) go = false;
-                for (int q = 0; q < t - w && go; ++q) go = s_piv[c0 + q] != x;
+                for (int q = 0; q < t - w && go; ++q) go = S.s_piv[c0 + q] != x;
             }
             if (go) {
                 int64_t pos = x;
                 for (int q = 0; q < w; ++q) {
-                    const int64_t r = g0 + q, tq = s_piv[c0 + q];
+                    const int64_t r = g0 + q, tq = S.s_piv[c0 + q];
                     if (pos == r) pos = tq;
                     else if (pos == tq) pos = r;
                 }
                 if (pos != x) {
-                    const int k = atomicAdd(&s_np, 1);
-                    s_dst[k] = pos;
-                    s_src[k] = x;
+                    const int k = atomicAdd(&S.s_np, 1);
+                    S.s_dst[k] = pos;
+                    S.s_src[k] = x;
                 }
             }
         }
         __syncthreads();
         {
-            // one warp per column, up to 16 columns per warp with every gather issued before any
-            // scatter (one memory latency instead of one per column)
-            const int np = s_np;   // <= 32: one value per lane
+            // a warp per column, every gather issued before any scatter; <= 2 KLW moved rows
+            const int np = S.s_np;
             const int nother = nbp - w;
-            const int64_t src = lane < np ? s_src[lane] : 0, dst = lane < np ? s_dst[lane] : 0;
-            constexpr int kCW = 16;
+            constexpr int kPer = (2 * KLW + 31) / 32;
+            int64_t src[kPer], dst[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int k = lane + 32 * u;
+                src[u] = k < np ? S.s_src[k] : 0;
+                dst[u] = k < np ? S.s_dst[k] : 0;
+            }
+            constexpr int kCW = kPer > 2 ? 4 : 8;
             const int nw = P * (kPT / 32), w0 = cta * (kPT / 32) + warp;
             for (int t0 = 0; t0 < (dbg & 1 ? 0 : nother); t0 += nw * kCW) {
-                T vv[kCW];
+                T vv[kCW][kPer];
 #pragma unroll
-                for (int u = 0; u < kCW; ++u) {
-                    const int t = t0 + w0 + u * nw;
+                for (int uu = 0; uu < kCW; ++uu) {
+                    const int t = t0 + w0 + uu * nw;
                     const int col = t < c0 ? t : t + w;
-                    vv[u] = (lane < np && t < nother) ? W[src + (k0 + col) * ldw] : T(0);
+#pragma unroll
+                    for (int u = 0; u < kPer; ++u)
+                        vv[uu][u] = (lane + 32 * u < np && t < nother) ? W[src[u] + (k0 + col) * ldw] : T(0);
                 }
 #pragma unroll
-                for (int u = 0; u < kCW; ++u) {
-                    const int t = t0 + w0 + u * nw;
+                for (int uu = 0; uu < kCW; ++uu) {
+                    const int t = t0 + w0 + uu * nw;
                     const int col = t < c0 ? t : t + w;
-                    if (lane < np && t < nother) W[dst + (k0 + col) * ldw] = vv[u];
+#pragma unroll
+                    for (int u = 0; u < kPer; ++u)
+                        if (lane + 32 * u < np && t < nother) W[dst[u] + (k0 + col) * ldw] = vv[uu][u];
                 }
             }
         }
-        PH(5);
         cbar();
         // ---- deferred update of the rest of the panel
         if (c0 + w < nbp && !(dbg & 2)) {
             const int c1 = c0 + w, rw = nbp - c1;
             batched<8, T>(
-                kLW * rw, [&](int e) -> T { const int k = e % kLW, cc = e / kLW; return __ldcg(&W[(g0 + k) + (k0 + c1 + cc) * ldw]); },
-                [&](int e, T v) { const int k = e % kLW, cc = e / kLW; U12[k][cc] = v; });
+                KLW * rw, [&](int e) -> T { const int k = e % KLW, cc = e / KLW; return __ldcg(&W[(g0 + k) + (k0 + c1 + cc) * ldw]); },
+                [&](int e, T v) { const int k = e % KLW, cc = e / KLW; S.U12[k][cc] = v; });
             __syncthreads();
-            // U12 = L11^{-1} A12 (unit lower L11 = Ub), one column per thread, unrolled in registers
-            for (int cc = tid; cc < rw; cc += kPT) {
-#pragma unroll 1
-                for (int k = 1; k < kLW; ++k) {
-                    T s = U12[k][cc];
-#pragma unroll
-                    for (int i2 = 0; i2 < kLW; ++i2)
-                        if (i2 < k) s -= Ub[k][i2] * U12[i2][cc];
-                    U12[k][cc] = s;
+            // U12 = L11^{-1} A12 (unit lower L11 = Ub) in column-oriented (axpy) form: step k
+            // updates rows k+1.. of every column in parallel (a per-column serial sweep would be a
+            // chain of KLW^2/2 dependent shared-memory loads)
+            for (int k = 0; k + 1 < KLW; ++k) {
+                const int nrow = KLW - 1 - k;
+                for (int e = tid; e < nrow * rw; e += kPT) {
+                    const int i2 = k + 1 + e % nrow, cc = e / nrow;
+                    S.U12[i2][cc] -= S.Ub[i2][k] * S.U12[k][cc];
                 }
+                __syncthreads();
             }
-            __syncthreads();
-            for (int e = tid; e < kLW * rw; e += kPT) {
-                const int k = e % kLW, cc = e / kLW;
-                const int64_t grow_k = g0 + k;
-                if (grow_k >= rbeg && grow_k < rend) W[grow_k + (k0 + c1 + cc) * ldw] = U12[k][cc];
+            for (int e = tid; e < KLW * rw; e += kPT) {
+                const int k = e % KLW, cc = e / KLW;
+                const int64_t rk = g0 + k;
+                if (rk >= rbeg && rk < rend) W[rk + (k0 + c1 + cc) * ldw] = S.U12[k][cc];
             }
-            // A22 -= L21 U12 on my rows below the leaf (L21 in registers)
-            // batches of kQ columns with a two-batch-deep prefetch (the loads of batches b+1 and b+2
-            // are in flight while batch b computes: this loop is bound by global latency otherwise);
-            // per k one vector read of U12[k][cb .. cb+kQ) feeds kQ x RPT FMAs
-            constexpr int kQ = RPT >= 4 ? 4 : RPT >= 2 ? 8 : 16;
+            // A22 -= L21 U12 on my rows below the leaf (L21 = the leaf values in registers); batches
+            // of kQ columns with the next batch's loads in flight
+            constexpr int kQ = RPT >= 4 ? 2 : RPT >= 2 ? 4 : 4;
             const int lim = g0 + w;
-            T nx[2][RPT][kQ];
-            auto load = [&](int buf, int cb) {
+            T nx[RPT][kQ];
+            auto load = [&](int cb) {
 #pragma unroll
                 for (int q = 0; q < kQ; ++q)
 #pragma unroll
                     for (int i = 0; i < RPT; ++i)
-                        nx[buf][i][q] = (gr[i] >= lim && cb + q < rw) ? W[gr[i] + (k0 + c1 + cb + q) * ldw] : T(0);
+                        nx[i][q] = (gr[i] >= lim && cb + q < rw) ? W[gr[i] + (k0 + c1 + cb + q) * ldw] : T(0);
             };
-            load(0, 0);
-            if (kQ < rw) load(1, kQ);
-            int buf = 0;
+            load(0);
             for (int cb = 0; cb < rw; cb += kQ) {
                 T acc[RPT][kQ];
 #pragma unroll
                 for (int q = 0; q < kQ; ++q)
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i) acc[i][q] = buf ? nx[1][i][q] : nx[0][i][q];
-                if (cb + 2 * kQ < rw) {
-                    if (buf) load(1, cb + 2 * kQ);
-                    else load(0, cb + 2 * kQ);
-                }
+                    for (int i = 0; i < RPT; ++i) acc[i][q] = nx[i][q];
+                if (cb + kQ < rw) load(cb + kQ);
 #pragma unroll
-                for (int k = 0; k < kLW; ++k) {
-                    T u[kQ];
+                for (int k = 0; k < KLW; ++k) {
+                    T uu[kQ];
 #pragma unroll
-                    for (int q = 0; q < kQ; ++q) u[q] = U12[k][cb + q];     // padded row: no bound check
+                    for (int q = 0; q < kQ; ++q) uu[q] = S.U12[k][cb + q];
 #pragma unroll
                     for (int i = 0; i < RPT; ++i)
 #pragma unroll
-                        for (int q = 0; q < kQ; ++q) acc[i][q] -= a[i][k] * u[q];
+                        for (int q = 0; q < kQ; ++q) acc[i][q] -= a[i][k] * uu[q];
                 }
 #pragma unroll
                 for (int q = 0; q < kQ; ++q)
 #pragma unroll
                     for (int i = 0; i < RPT; ++i)
                         if (gr[i] >= lim && cb + q < rw) W[gr[i] + (k0 + c1 + cb + q) * ldw] = acc[i][q];
-                buf ^= 1;
             }
             __syncthreads();
         }
     }
-    PH(6);
-#undef PH
-    if (prof)
-        for (int q = 0; q < 8; ++q) st->dbg_t[q] = (unsigned long long)ph[q];
+    (void)URW;
+    if (P > 1) cbar();                       // no CTA leaves while remote stores may target it
     if (tid == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
     if (tr_max && tid == 0) atomicMax(tr_max, gtimer());
 }
@@ -1105,28 +1099,32 @@ static LuStreams& lu_streams() {
 
 static int g_panel_dbg = 0;   // diagnostics: ablation mask of the register panel (lu_debug_panel_time)
 
-// Cluster size and rows per thread of the register panel: one CTA up to 1024 rows, then up to
-// 16 CTAs of <= 1024 rows (4 per thread); larger panels use the cooperative kernel.
+// Cluster size and rows per thread of the fast panel: one CTA up to 1024 rows (RPT = 1, 2, 4
+// with leaves of 64, 32, 16 columns), then up to 16 CTAs of <= 1024 rows; larger panels use the
+// cooperative kernel.
 template <typename T>
 static bool leaf_panel_launch(const Work& w, int64_t k0, int nbp, int prio, cudaStream_t s) {
     const int64_t n = w.n, m = n - k0;
-    static const int rpt_env = getenv("AS_LU_LEAF_RPT") ? atoi(getenv("AS_LU_LEAF_RPT")) : 4;
+    static const int rows_env = getenv("AS_LU_LEAF_ROWS") ? atoi(getenv("AS_LU_LEAF_ROWS")) : 1024;
     static int pmax = kLfMaxP;
     if (nbp > kPW) return false;
     for (;;) {
-        const int64_t cap = (int64_t)kPT * rpt_env;
         int P = 1;
-        while (P < pmax && (m + P - 1) / P > cap) P *= 2;
+        while (P < pmax && (m + P - 1) / P > rows_env) P *= 2;
         const int64_t chunk = (m + P - 1) / P;
         const int rpt = (int)((chunk + kPT - 1) / kPT);
         if (rpt > 4) return false;
-        void* kern = rpt <= 1 ? (void*)lu_panel_reg_kernel<T, 1> : rpt <= 2 ? (void*)lu_panel_reg_kernel<T, 2>
-                                                                              : (void*)lu_panel_reg_kernel<T, 4>;
+        void* kern;
+        size_t smem;
+        if (rpt <= 1) { kern = (void*)lu_panel_fast_kernel<T, 1, 64>; smem = sizeof(LeafSmem<T, 64>); }
+        else if (rpt <= 2) { kern = (void*)lu_panel_fast_kernel<T, 2, 32>; smem = sizeof(LeafSmem<T, 32>); }
+        else { kern = (void*)lu_panel_fast_kernel<T, 4, 16>; smem = sizeof(LeafSmem<T, 16>); }
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(P);
         cfg.blockDim = dim3(kPT);
-        cfg.dynamicSmemBytes = 0;
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;

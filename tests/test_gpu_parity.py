@@ -222,6 +222,27 @@ def test_force_method(method):
     assert rep["primary_method"] == method
 
 
+@pytest.mark.parametrize("method", [oracle.M_LU, oracle.M_CHOL, oracle.M_TRI_LOWER])
+def test_skip_detect_standard_solver(method):
+    """AS_OPT_SKIP_DETECT (the paper's "standard solver"): no detection verdicts, the forced
+    method's X matches the oracle's forced solve; illegal without FORCE_METHOD or with BAND."""
+    A = W.random_triangular(150, False, seed=3) if method == oracle.M_TRI_LOWER else W.random_spd_fig3(150, seed=3)
+    B = np.asfortranarray(np.random.default_rng(3).standard_normal((150, 2)))
+    o = AS.make_options(force_method=method, skip_detect=True)
+    ret, X, rep = AS.as_solve_ex(AS.to_device(A), AS.to_device(B), options=o)
+    torch.cuda.synchronize()
+    assert ret == 0 and rep["primary_method"] == method and (rep["flags"] & 0xF) == 0
+    oret, Xo, orep, _ = oracle.solve(A, B, force_method=method)
+    assert oret == 0
+    Xg = AS.to_host(X)
+    assert backward_error(A, Xg, B) <= 1e-13
+    assert forward_diff(Xg, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"]
+    bad = AS.make_options(skip_detect=True)
+    assert AS.as_solve_ex(AS.to_device(A), AS.to_device(B), options=bad)[0] == -9
+    bad = AS.make_options(force_method=oracle.M_BAND, skip_detect=True)
+    assert AS.as_solve_ex(AS.to_device(A), AS.to_device(B), options=bad)[0] == -9
+
+
 def test_fp32_paths():
     for A, B in [W.make("C1", n=200), W.make("C2", n=300, nrhs=2), W.make("C3a", n=130, nrhs=3),
                  W.make("C3b", n=150, nrhs=3)]:

@@ -12,8 +12,8 @@ dt = torch.float64
 for m in ms:
     A = torch.randn(m, m, generator=g, device="cuda", dtype=dt).t().contiguous().t()
     row = [f"LU m={m:6d}"]
-    for kind, dbg, tag in [(0, 0, "reg"), (0, 2, "nodefer"), (0, 8, "nocols"), (0, 2 | 16, "nodefer-noupd"),
-                           (0, 2 | 64, "nodefer-noreduce"), (0, 2 | 16 | 64, "nodefer-noupd-nored"), (1, 0, "coop")]:
+    for kind, dbg, tag in [(0, 0, "fast"), (0, 1, "noswap"), (0, 2, "nodefer"), (0, 8, "nocols"), (0, 11, "empty"),
+                           (1, 0, "coop")]:
         t = AS.debug_panel_time(A, 0, min(128, m), kind=kind, iters=4, dbg=dbg)
         torch.cuda.synchronize()
         row.append(f"{tag} {t:8.1f}")
