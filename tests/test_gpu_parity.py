@@ -129,7 +129,7 @@ def test_lu_dense(n):
     check_parity(A, B)
 
 
-@pytest.mark.parametrize("n,kl,ku", [(40, 1, 1), (300, 3, 2), (257, 8, 8), (500, 0, 5), (500, 6, 0), (1000, 20, 3)])
+@pytest.mark.parametrize("n,kl,ku", [(40, 1, 1), (300, 3, 2), (257, 8, 8), (500, 0, 5), (500, 6, 0), (1000, 20, 3), (300, 30, 25), (3000, 2, 2)])
 def test_banded(n, kl, ku):
     A = W.random_banded(n, kl, ku, seed=n + kl, dominant=(kl + ku) % 2 == 0)
     B = np.asfortranarray(np.random.default_rng(1).standard_normal((n, 2)))
