@@ -1159,8 +1159,15 @@ template <typename T>
 static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long seq_base, int prio, cudaStream_t s) {
     const int64_t n = w.n, m = n - k0;
     // register/cluster panel: opt-in (AS_LU_PANEL=reg) until it beats the cooperative panel
-    static const bool use_reg = getenv("AS_LU_PANEL") && strcmp(getenv("AS_LU_PANEL"), "reg") == 0;
-    if (use_reg && getenv("AS_LU_PANEL_OLD") == nullptr && leaf_panel_launch<T>(w, k0, nbp, prio, s)) return;
+    // Panel policy.  The cluster panel occupies <= 16 SMs but is slower per column than the
+    // cooperative panel (which occupies ~m/128 SMs); measured on C5 (n = 16384) the cooperative
+    // panel everywhere wins (196 ms) over the cluster panel for m >= 12288 / 10240 / 8192
+    // (209 / 218 / 227 ms), so the cluster panel is opt-in: AS_LU_PANEL=reg (everywhere) or
+    // AS_LU_FAST_MIN_M=<m> (where the panel has >= m rows).
+    static const char* pol = getenv("AS_LU_PANEL");
+    static const int64_t fast_min_m = getenv("AS_LU_FAST_MIN_M") ? atoll(getenv("AS_LU_FAST_MIN_M")) : (int64_t)1 << 62;
+    const bool want_fast = pol && strcmp(pol, "reg") == 0 ? true : (pol && strcmp(pol, "coop") == 0) ? false : m >= fast_min_m;
+    if (want_fast && getenv("AS_LU_PANEL_OLD") == nullptr && leaf_panel_launch<T>(w, k0, nbp, prio, s)) return;
     static const int rows_per_cta = getenv("AS_LU_PANEL_ROWS") ? atoi(getenv("AS_LU_PANEL_ROWS")) : 128;
     int P = (int)std::min<int64_t>(w.num_sms, (m + rows_per_cta - 1) / rows_per_cta);
     P = std::max(P, 1);
