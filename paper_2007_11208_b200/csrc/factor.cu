@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) l21_kernel(T* W, int64_t ldw, int64_t n, 
     const int nr = (int)min<int64_t>(kNB, n - r0);
     if (nr <= 0) return;
     const T* Li = Dinv + (k0 / kNB) * (int64_t)kNB * kNB;
-    batched<8, T>(
+    batched<16, T>(
         2 * kNB * kNB,
         [&](int e) -> T {
             if (e < kNB * kNB) {

@@ -77,9 +77,12 @@ struct __align__(32) PSlot {
 template <typename T>
 AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, int64_t g, int col, T& v, long long& idx,
                                T* sv, long long* si, int* sdn) {
+    // first max |a(r, col)| over local rows at positions >= g; NaN never wins, a NaN at row g keeps
+    // g (the serial sweep's semantics).  Warp level: fmax shuffles + ballot + integer min of the
+    // row; CTA level: every warp merges the 8 warp results the same way (one barrier).
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    v = T(-1);
-    idx = 0x7fffffffffffffffll;
+    T bv = T(-1);
+    unsigned br = 0xffffffffu;
     int dnan = 0;
     for (int r = threadIdx.x; r < nr; r += blockDim.x) {
         const int64_t gr = rbeg + r;
@@ -87,27 +90,65 @@ AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, in
         T a = Ps[r + col * cp];
         a = a < T(0) ? -a : a;
         if (gr == g && a != a) dnan = 1;
-        argmax_merge(v, idx, a, (long long)gr);
+        if (a > bv) { bv = a; br = (unsigned)r; }     // rows increase: strict > keeps the first
     }
-    warp_argmax(v, idx);
+    T wm = bv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    const unsigned wr = __reduce_min_sync(0xffffffffu, (bv == wm && br != 0xffffffffu) ? br : 0xffffffffu);
     dnan = __any_sync(0xffffffffu, dnan);
-    if (lane == 0) { sv[warp] = v; si[warp] = idx; sdn[warp] = dnan; }
+    if (lane == 0) { sv[warp] = (wr == 0xffffffffu) ? T(-1) : wm; si[warp] = (long long)wr; sdn[warp] = dnan; }
     __syncthreads();
-    if (warp == 0) {
-        v = lane < 8 ? sv[lane] : T(-1);
-        idx = lane < 8 ? si[lane] : 0x7fffffffffffffffll;
-        int dn = lane < 8 ? sdn[lane] : 0;
-        warp_argmax(v, idx);
-        dn = __any_sync(0xffffffffu, dn);
-        if (lane == 0) {
-            if (dn) { v = T(INFINITY); idx = g; }     // NaN diagonal: the serial sweep keeps row g
-            sv[0] = v; si[0] = idx;
+    const int nw = (int)(blockDim.x >> 5);
+    const T v8 = (lane & 7) < nw ? sv[lane & 7] : T(-1);
+    const unsigned r8 = (lane & 7) < nw ? (unsigned)si[lane & 7] : 0xffffffffu;
+    const int d8 = (lane & 7) < nw ? sdn[lane & 7] : 0;
+    T m8 = v8;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) m8 = fmax(m8, __shfl_xor_sync(0xffffffffu, m8, o));
+    const unsigned rmin = __reduce_min_sync(0xffffffffu, (v8 == m8 && r8 != 0xffffffffu) ? r8 : 0xffffffffu);
+    const int dn = __any_sync(0xffffffffu, d8);
+    v = (rmin == 0xffffffffu) ? T(-1) : m8;
+    idx = (rmin == 0xffffffffu) ? 0x7fffffffffffffffll : (long long)(rbeg + rmin);
+    if (dn) { v = T(INFINITY); idx = g; }
+}
+
+// Bulk rank-1 update of the panel rows r0 .. nr-1 (local), columns j+2 .. nbp-1:
+// a(r, c) -= a(r, j) * u(c), rows skip0 / skip1 excluded.  Thread tile: 4 rows (lane + 32 i) x
+// columns cg + 8 q (warp = column group), 4 columns per batch with every load before the stores
+// (one u load feeds 4 rows; Ps and u are both shared memory: unbatched code would serialise).
+template <typename T>
+AS_DEV void panel_bulk_update(T* __restrict__ Ps, int64_t cp, const T* __restrict__ u, int r0, int nr, int j, int nbp,
+                              int skip0, int skip1) {
+    const int lane = threadIdx.x & 31, cgp = threadIdx.x >> 5, ncg = (int)(blockDim.x >> 5);
+    for (int rb = r0; rb < nr; rb += 128) {
+        int rr[4];
+        T l[4];
+        bool ok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            rr[i] = rb + lane + 32 * i;
+            ok[i] = rr[i] < nr && rr[i] != skip0 && rr[i] != skip1;
+            l[i] = ok[i] ? Ps[rr[i] + j * cp] : T(0);
+        }
+        for (int c0 = j + 2 + cgp; c0 < nbp; c0 += 4 * ncg) {
+            T uv[4], av[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = c0 + q * ncg;
+                uv[q] = c < nbp ? u[c] : T(0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) av[q][i] = (ok[i] && c < nbp) ? Ps[rr[i] + c * cp] : T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = c0 + q * ncg;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (ok[i] && c < nbp) Ps[rr[i] + c * cp] = av[q][i] - l[i] * uv[q];
+            }
         }
     }
-    __syncthreads();
-    v = sv[0];
-    idx = si[0];
-    __syncthreads();
 }
 
 template <typename T>
@@ -123,9 +164,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
     const int64_t rbeg = k0 + (int64_t)cta * chunk;
     const int64_t rend = min(n, rbeg + chunk);
     const int nr = (int)max<int64_t>(0, rend - rbeg);
-    const int64_t cp = use_smem ? chunk : ldw;
+    // odd column stride: row accesses (pivot / candidate rows, stride cp) are bank-conflict free
+    const int64_t cp = use_smem ? (chunk | 1) : ldw;
     T* Ps = use_smem ? (T*)smem_raw : W + rbeg + k0 * ldw;
-    T* ubuf = use_smem ? (T*)smem_raw + chunk * nbp : (T*)smem_raw;
+    T* ubuf = use_smem ? (T*)smem_raw + cp * nbp : (T*)smem_raw;
     __shared__ T sv[8];
     __shared__ long long si[8];
     __shared__ int sdn[8];
@@ -266,17 +308,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         __syncthreads();
         publish(j + 1, v, idx);
         // ---- bulk rank-1 update of the remaining rows, columns j+2.. (thread = row, column phase)
-        if (elim) {
-            const int nrow = (int)max<int64_t>(0, nr - r0);
-            const int rl = threadIdx.x & 127, ph = threadIdx.x >> 7;
-            for (int rr = rl; rr < nrow; rr += 128) {
-                const int r = (int)r0 + rr;
-                if (r == rc || r == rg) continue;
-                const T l = Ps[r + j * cp];
-#pragma unroll 4
-                for (int c = j + 2 + ph; c < nbp; c += 2) Ps[r + c * cp] -= l * ubuf[c];
-            }
-        }
+        if (elim) panel_bulk_update<T>(Ps, cp, ubuf, (int)r0, nr, j, nbp, rc, rg);
         __syncthreads();
     }
     if (use_smem) {
@@ -299,8 +331,13 @@ namespace cg = cooperative_groups;
 constexpr int kClMax = 8;
 template <typename T>
 __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
-                                                              int64_t* ipiv, DevState* st) {
+                                                              int64_t* ipiv, DevState* st, int prof_on) {
     cg::cluster_group cl = cg::this_cluster();
+    // diagnostics (prof_on): clock64 phase totals of CTA 0 / thread 0 into st->dbg_t
+    const bool prof = prof_on && blockIdx.x == 0 && threadIdx.x == 0;
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = clock64();
+#define PHC(q) do { if (prof) { const long long t_ = clock64(); ph[q] += t_ - tp; tp = t_; } } while (0)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int P = gridDim.x, cta = blockIdx.x;          // the grid is one cluster
     const int64_t m = n - k0;
@@ -308,9 +345,9 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
     const int64_t rbeg = k0 + (int64_t)cta * chunk;
     const int64_t rend = min(n, rbeg + chunk);
     const int nr = (int)max<int64_t>(0, rend - rbeg);
-    const int64_t cp = chunk;
+    const int64_t cp = chunk | 1;                        // odd stride: conflict-free row accesses
     T* Ps = (T*)smem_raw;                                // chunk x nbp, column-major
-    T* ubuf = Ps + chunk * nbp;                          // pivot row
+    T* ubuf = Ps + cp * nbp;                             // pivot row
     T* candb = ubuf + nbp;                               // [2][nbp] my candidate row
     T* diagb = candb + 2 * nbp;                          // [2][nbp] old row g (owner of g)
     __shared__ T s_cv[2];
@@ -349,7 +386,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
     for (int j = 0; j < nbp; ++j) {
         const int64_t g = k0 + j;
         const int par = j & 1;
-        cl.sync();                                       // every candidate of column j is visible
+        PHC(0);
+        if (P > 1) cl.sync();                            // every candidate of column j is visible
+        else __syncthreads();
+        PHC(1);
         if (warp == 0) {
             T bv = T(-1);
             long long bi = 0x7fffffffffffffffll;
@@ -383,6 +423,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
             if (own_p) dst_p[c * cp] = dg;
         }
         __syncthreads();
+        PHC(2);
         const T piv = ubuf[j];
         if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
         const bool elim = piv != T(0);
@@ -405,10 +446,12 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
             }
         }
         __syncthreads();
+        PHC(3);
         if (j + 1 >= nbp) break;
         T v;
         long long idx;
         panel_local_argmax(Ps, cp, nr, rbeg, g + 1, j + 1, v, idx, sv, si, sdn);
+        PHC(4);
         const int rcn = (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) ? (int)(idx - rbeg) : -1;
         const int rg = (g + 1 >= rbeg && g + 1 < rend) ? (int)(g + 1 - rbeg) : -1;
         if (elim) {
@@ -419,19 +462,14 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
         }
         __syncthreads();
         publish(j + 1, v, idx);
-        if (elim) {
-            const int nrow = (int)max<int64_t>(0, nr - r0);
-            const int rl = threadIdx.x & 127, ph = threadIdx.x >> 7;
-            for (int rr = rl; rr < nrow; rr += 128) {
-                const int r = (int)r0 + rr;
-                if (r == rcn || r == rg) continue;
-                const T l = Ps[r + j * cp];
-#pragma unroll 4
-                for (int c = j + 2 + ph; c < nbp; c += 2) Ps[r + c * cp] -= l * ubuf[c];
-            }
-        }
+        PHC(5);
+        if (elim) panel_bulk_update<T>(Ps, cp, ubuf, (int)r0, nr, j, nbp, rcn, rg);
         __syncthreads();
     }
+    PHC(6);
+#undef PHC
+    if (prof)
+        for (int q = 0; q < 8; ++q) st->dbg_t[q] = (unsigned long long)ph[q];
     cl.sync();                                           // no CTA exits while others may read its buffers
     for (int e = threadIdx.x; e < nr * nbp; e += blockDim.x) {
         const int c = e / nr, r = e - c * nr;
@@ -467,7 +505,8 @@ struct LeafSmem {
     T crow[2][kLfMaxP][KLW];             // cluster: every CTA's candidate row
     T cgrow[2][KLW];                     // cluster: row g
     T Ub[KLW][KLW];                      // pivot rows of the leaf, natural column order
-    T U12[KLW][kPW - KLW + 16];          // + padding: vector reads past the last column
+    T U12[KLW][kPW - KLW + 17];          // + padding (vector reads past the last column); odd row
+                                         // stride: column accesses are bank-conflict free
     unsigned long long cvi[2][kLfMaxP][2];   // cluster: (value bits, index) per CTA
     unsigned long long mbar[2];
     T wval[2][kPT / 32];
@@ -503,7 +542,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_fast_kernel(T* W, int64_t ldw
     const int64_t rend = min(n, rbeg + chunk);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LeafSmem<T, KLW>& S = *reinterpret_cast<LeafSmem<T, KLW>*>(smem_raw);
-    constexpr int URW = kPW - KLW + 16;
+    constexpr int URW = kPW - KLW + 17;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kNone = 0x7fffffff;        // row positions fit in int (n <= 2^31 - 1)
     int gr[RPT];
@@ -1176,7 +1215,7 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
         int pc = 1;
         while (pc < kClMax && (size_t)((m + pc - 1) / pc) * nbp * sizeof(T) > 192 * 1024) pc *= 2;
         const int64_t ch = (m + pc - 1) / pc;
-        const size_t smc = sizeof(T) * ((size_t)ch * nbp + 5 * (size_t)nbp);
+        const size_t smc = sizeof(T) * ((size_t)(ch | 1) * nbp + 5 * (size_t)nbp);
         if (smc <= 200 * 1024) {
             auto kc = lu_panel_cl_kernel<T>;
             cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
@@ -1191,12 +1230,13 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
             at[1].id = cudaLaunchAttributePriority; at[1].val.priority = prio;
             cfg.attrs = at;
             cfg.numAttrs = 2;
-            if (cudaLaunchKernelEx(&cfg, kc, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st) == cudaSuccess) return;
+            if (cudaLaunchKernelEx(&cfg, kc, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, (g_panel_dbg & 256) ? 1 : 0) == cudaSuccess)
+                return;
             cudaGetLastError();
         }
     }
     const int64_t chunk = (m + P - 1) / P;
-    size_t smem = sizeof(T) * (chunk * nbp + nbp);
+    size_t smem = sizeof(T) * ((chunk | 1) * nbp + nbp);
     int use_smem = 1;
     if (smem > 200 * 1024) { use_smem = 0; smem = sizeof(T) * nbp; }
     PSlot* slots = (PSlot*)w.cand;
@@ -1419,8 +1459,8 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
     if (dbg & 256) {
         unsigned long long ph[16];
         cudaMemcpy(ph, w.st->dbg_t, sizeof(ph), cudaMemcpyDeviceToHost);
-        fprintf(stderr, "panel phases (cycles, CTA 0): push %llu cbar %llu winner+swap %llu update %llu reduce %llu "
-                        "leafend %llu deferred %llu\n", ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
+        fprintf(stderr, "panel phases (cycles, CTA 0, kind %d): %llu %llu %llu %llu %llu %llu %llu\n", kind, ph[0], ph[1],
+                ph[2], ph[3], ph[4], ph[5], ph[6]);
     }
     const cudaError_t err = cudaGetLastError();
     cudaEventDestroy(e0);
