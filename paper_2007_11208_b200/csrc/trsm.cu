@@ -85,6 +85,9 @@ struct TsArgs {
 // ((b * ntiles + rt) * RT + c) * kNB + i; fp64 values as two words {lo32 | epoch << 32,
 // hi32 | epoch << 32} (each 8-byte word is written and read as one access), fp32 as one.
 template <typename T> struct LLw { static constexpr int v = sizeof(T) / 4; };
+// back-off between polls of a not-yet-published word: hundreds of spinning CTAs otherwise keep
+// L2 busy with volatile loads and slow the producers down
+constexpr unsigned ts_backoff_ns = 64;
 AS_DEV void ll_put(unsigned long long* w, double x, unsigned ep) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(x);
     const unsigned long long hi = ((unsigned long long)ep << 32);
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
             for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
                 const int r = e % kNB, c = e / kNB;
                 T x;
-                while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x)) {}
+                while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x)) __nanosleep(ts_backoff_ns);
                 Xs[r + c * kLDX] = x;
             }
         }
