@@ -294,6 +294,24 @@ def main():
         launches += AS.last_kernel_nodes()
         reports.append(rep)
     torch.cuda.synchronize()
+    blocking_ms = float(np.sum(step_ms)) / args.steps
+    # Device throughput (inputs larger than L2): the same K public-API solves issued back to back
+    # with as_solve_async (one graph launch each, no host sync between them), bracketed by a
+    # barrier + synchronize; the host-side enqueue of call k+1 overlaps the GPU work of call k.
+    # With L2 flushes between steps (small inputs) the blocking per-call loop above is the number.
+    if flush is None and not args.eager:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(args.steps):
+            r = AS.as_solve_async(dA, dB, X, options=opts, stream=stream)
+            assert r == 0, AS.strerror(r)
+        eb.record(stream)
+        eb.synchronize()
+        torch.cuda.synchronize()
+        step_ms = [ea.elapsed_time(eb) / args.steps] * args.steps
     if dist:
         dist.barrier()
     clocks = clock.stop()
@@ -372,6 +390,10 @@ def main():
             "config": {"workload": f"{tag}: {info['desc']}", "n": info["n"], "nrhs": info["nrhs"],
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps (256 MB write)",
+                       "timing": ("K back-to-back as_solve_async calls between two synchronizes (device throughput)"
+                                  if flush is None and not args.eager else
+                                  "per-call CUDA events around blocking as_solve_ex (host launch + sync included)"),
+                       "ms_per_call_blocking": blocking_ms,
                        "method": rep["method"], "flags": hex(rep["flags"]), "rcond": rep["rcond"]},
             "gflops": gflops, "roofline": roof, **extra, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks, "fp64_dmma_peak_tflops": fp64_peak}
