@@ -94,10 +94,37 @@ __global__ void __launch_bounds__(kSvdThreads, 1) qr_kernel(T* W, int64_t ldw, i
             const T* v = W + j * ldw;
             for (int64_t k = j + 1 + gw; k < n + nrhs; k += nwarps) {
                 T* col = k < n ? W + k * ldw : Y + (k - n) * n;
+                // 8 loads in flight per iteration (a lane-serial loop was bound by one L2 latency per
+                // 32 rows); the lane's sum keeps the serial order i = j+lane, j+lane+32, ... (the C4
+                // least-squares residual is sensitive to the rounding of the reflector products)
                 T s = T(0);
-                for (int64_t i = j + lane; i < n; i += 32) s += (i == j ? T(1) : __ldcg(&v[i])) * __ldcg(&col[i]);
+                for (int64_t i0 = j + lane; i0 < n; i0 += 128) {
+                    T vv[4], cv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t i = i0 + 32 * u;
+                        vv[u] = i < n ? (i == j ? T(1) : __ldcg(&v[i])) : T(0);
+                        cv[u] = i < n ? __ldcg(&col[i]) : T(0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (i0 + 32 * u < n) s += vv[u] * cv[u];
+                }
                 s = warp_sum(s) * tj;
-                for (int64_t i = j + lane; i < n; i += 32) col[i] = __ldcg(&col[i]) - s * (i == j ? T(1) : __ldcg(&v[i]));
+                for (int64_t i0 = j + lane; i0 < n; i0 += 128) {
+                    T vv[4], cv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t i = i0 + 32 * u;
+                        vv[u] = i < n ? (i == j ? T(1) : __ldcg(&v[i])) : T(0);
+                        cv[u] = i < n ? __ldcg(&col[i]) : T(0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t i = i0 + 32 * u;
+                        if (i < n) col[i] = cv[u] - s * vv[u];
+                    }
+                }
             }
         }
         grid_barrier(bar, ++gen, (unsigned)P);
@@ -192,73 +219,110 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             s_gc[threadIdx.x] = gc < n ? (int)gc : -1;
         }
         __syncthreads();
-        {   // stage the C2 columns: all of a thread's loads in flight together (latency-batched)
+        {   // stage the C2 columns: per thread C2 x 4 independent loads in flight (no index division)
             const int nn = (int)n;
-            batched<32, T>(
-                C2 * nn,
-                [&](int e) -> T {
-                    const int c = e / nn, i = e - c * nn;
+            for (int i0 = 0; i0 < nn; i0 += 4 * (int)blockDim.x) {
+                T v[C2][4];
+#pragma unroll
+                for (int c = 0; c < C2; ++c) {
                     const int gc = s_gc[c];
-                    return gc >= 0 ? __ldcg(&M[(int64_t)gc * ldw + i]) : T(0);
-                },
-                [&](int e, T v) { Ms[e] = v; });
+                    const T* col = M + (int64_t)(gc >= 0 ? gc : 0) * ldw;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int i = i0 + (int)threadIdx.x + k * (int)blockDim.x;
+                        v[c][k] = (gc >= 0 && i < nn) ? __ldcg(col + i) : T(0);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < C2; ++c)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int i = i0 + (int)threadIdx.x + k * (int)blockDim.x;
+                        if (i < nn) Ms[(int64_t)c * n + i] = v[c][k];
+                    }
+            }
         }
-        for (int c = 0; c < C2; ++c) {
-            const int gc = s_gc[c];
-            for (int64_t rr = threadIdx.x; rr < nrhs; rr += blockDim.x) Ys[c + rr * C2] = gc >= 0 ? __ldcg(&Y[gc + rr * n]) : T(0);
+        {   // the C2 rows of Y: element-parallel (a column-outer loop with one active thread for one
+            // right-hand side serialised C2 global latencies per round)
+            const int nr = (int)nrhs;
+            batched<8, T>(
+                C2 * nr,
+                [&](int e) -> T {
+                    const int rr = e / C2, c = e - rr * C2;
+                    const int gc = s_gc[c];
+                    return gc >= 0 ? __ldcg(&Y[gc + (int64_t)rr * n]) : T(0);
+                },
+                [&](int e, T v) { Ys[e] = v; });          // Ys[c + rr * C2] = Ys[e]
         }
         __syncthreads();
         JSTAMP(1);
-        // local round-robin over C2 columns: C2-1 sub-rounds of BS disjoint pairs, one warp per pair
+        // local round-robin over C2 columns: C2-1 sub-rounds of BS disjoint pairs; each pair is
+        // handled by G = 8 / BS warps, each covering a contiguous slice of the n rows: slice partial
+        // sums meet in shared memory (one barrier), every warp of the pair forms the same rotation
+        // and applies it to its own slice
+        constexpr int G = (kSvdThreads / 32) / BS > 0 ? (kSvdThreads / 32) / BS : 1;
+        __shared__ T s_part[BS][G][3];
+        const int nn = (int)n;
+        const int u_pair = warp % BS, gsl = warp / BS;                   // pair, slice of this warp
+        const int slice = (nn + G - 1) / G;
+        const int i_lo = gsl * slice, i_hi = min(nn, i_lo + slice);
         for (int sr = 0; sr < C2 - 1; ++sr) {
-            for (int u = warp; u < BS; u += (int)(blockDim.x >> 5)) {
-                const int t1 = u, t2 = C2 - 1 - u;
-                const int la = t1 == 0 ? 0 : 1 + (t1 - 1 + sr) % (C2 - 1);
-                const int lb = t2 == 0 ? 0 : 1 + (t2 - 1 + sr) % (C2 - 1);
-                int lp = la, lq = lb;
-                if (s_gc[lp] < 0 || s_gc[lq] < 0) continue;
-                if (s_gc[lp] > s_gc[lq]) { lp = lb; lq = la; }   // p < q by global column index
-                T* mp = Ms + (int64_t)lp * n;
-                T* mq = Ms + (int64_t)lq * n;
-                // alpha, beta, gamma with 4 independent partial sums per lane (the FMA chains are
-                // the latency of the pair; n is a multiple of 4 here or the tail is zero-padded)
-                const int nn = (int)n;
+            const int t1 = u_pair, t2 = C2 - 1 - u_pair;
+            const int la = t1 == 0 ? 0 : 1 + (t1 - 1 + sr) % (C2 - 1);
+            const int lb = t2 == 0 ? 0 : 1 + (t2 - 1 + sr) % (C2 - 1);
+            int lp = la, lq = lb;
+            const bool live = gsl < G && s_gc[lp] >= 0 && s_gc[lq] >= 0;
+            if (live && s_gc[lp] > s_gc[lq]) { lp = lb; lq = la; }   // p < q by global column index
+            T* mp = Ms + (int64_t)lp * n;
+            T* mq = Ms + (int64_t)lq * n;
+            if (live) {
+                // alpha, beta, gamma over this warp's slice, 4 independent partial sums per lane
                 T al4[4] = {}, be4[4] = {}, ga4[4] = {};
-                for (int i0 = lane; i0 < nn; i0 += 128) {
+                for (int i0 = i_lo + lane; i0 < i_hi; i0 += 128) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int i = i0 + 32 * u;
-                        if (i < nn) { const T x = mp[i], y = mq[i]; al4[u] += x * x; be4[u] += y * y; ga4[u] += x * y; }
+                        if (i < i_hi) { const T x = mp[i], y = mq[i]; al4[u] += x * x; be4[u] += y * y; ga4[u] += x * y; }
                     }
                 }
                 T al = (al4[0] + al4[1]) + (al4[2] + al4[3]);
                 T be = (be4[0] + be4[1]) + (be4[2] + be4[3]);
                 T ga = (ga4[0] + ga4[1]) + (ga4[2] + ga4[3]);
                 al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+                if (lane == 0) { s_part[u_pair][gsl][0] = al; s_part[u_pair][gsl][1] = be; s_part[u_pair][gsl][2] = ga; }
+            }
+            __syncthreads();
+            if (live) {
+                T al = T(0), be = T(0), ga = T(0);
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) { al += s_part[u_pair][gg][0]; be += s_part[u_pair][gg][1]; ga += s_part[u_pair][gg][2]; }
                 // rotation skipped when |gamma| <= tol sqrt(alpha beta) (Z14 reading)
                 const T sa = sqrt(al), sb = sqrt(be);
-                if (ga == T(0) || !((ga < T(0) ? -ga : ga) > tol * sa * sb)) continue;
-                ++my_rot;
-                const T zeta = (be - al) / (T(2) * ga);
-                const T az = zeta < T(0) ? -zeta : zeta;
-                const T t = (zeta >= T(0) ? T(1) : T(-1)) / (az + sqrt(T(1) + zeta * zeta));
-                const T c = rsqrt_nr(T(1) + t * t);
-                const T sn = c * t;
-                for (int i0 = lane; i0 < nn; i0 += 128) {
+                const bool rot = !(ga == T(0) || !((ga < T(0) ? -ga : ga) > tol * sa * sb));
+                if (rot) {
+                    if (gsl == 0) ++my_rot;
+                    const T zeta = (be - al) / (T(2) * ga);
+                    const T az = zeta < T(0) ? -zeta : zeta;
+                    const T t = (zeta >= T(0) ? T(1) : T(-1)) / (az + sqrt(T(1) + zeta * zeta));
+                    const T c = rsqrt_nr(T(1) + t * t);
+                    const T sn = c * t;
+                    for (int i0 = i_lo + lane; i0 < i_hi; i0 += 128) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int i = i0 + 32 * u;
-                        if (i < nn) {
-                            const T x = mp[i], y = mq[i];
-                            mp[i] = c * x - sn * y;
-                            mq[i] = sn * x + c * y;
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = i0 + 32 * u;
+                            if (i < i_hi) {
+                                const T x = mp[i], y = mq[i];
+                                mp[i] = c * x - sn * y;
+                                mq[i] = sn * x + c * y;
+                            }
                         }
                     }
-                }
-                for (int64_t rr = lane; rr < nrhs; rr += 32) {
-                    const T x = Ys[lp + rr * C2], y = Ys[lq + rr * C2];
-                    Ys[lp + rr * C2] = c * x - sn * y;
-                    Ys[lq + rr * C2] = sn * x + c * y;
+                    if (gsl == 0)
+                        for (int64_t rr = lane; rr < nrhs; rr += 32) {
+                            const T x = Ys[lp + rr * C2], y = Ys[lq + rr * C2];
+                            Ys[lp + rr * C2] = c * x - sn * y;
+                            Ys[lq + rr * C2] = sn * x + c * y;
+                        }
                 }
             }
             __syncthreads();
@@ -270,7 +334,11 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
             const T* src = Ms + (int64_t)c * n;
             T* dst = M + (int64_t)gc * ldw;
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-            for (int64_t rr = threadIdx.x; rr < nrhs; rr += blockDim.x) Y[gc + rr * n] = Ys[c + rr * C2];
+        }
+        for (int e = threadIdx.x; e < C2 * (int)nrhs; e += blockDim.x) {
+            const int rr = e / C2, c = e - rr * C2;
+            const int gc = s_gc[c];
+            if (gc >= 0) Y[gc + (int64_t)rr * n] = Ys[e];
         }
         JSTAMP(3);
         grid_barrier(bar, (unsigned)(r + 1), (unsigned)P);
