@@ -266,10 +266,21 @@ __global__ void __launch_bounds__(kSvdThreads, 1) jacobi_block_sweep_kernel(T* M
         const int u_pair = warp % BS, gsl = warp / BS;                   // pair, slice of this warp
         const int slice = (nn + G - 1) / G;
         const int i_lo = gsl * slice, i_hi = min(nn, i_lo + slice);
-        for (int sr = 0; sr < C2 - 1; ++sr) {
-            const int t1 = u_pair, t2 = C2 - 1 - u_pair;
-            const int la = t1 == 0 ? 0 : 1 + (t1 - 1 + sr) % (C2 - 1);
-            const int lb = t2 == 0 ? 0 : 1 + (t2 - 1 + sr) % (C2 - 1);
+        // round 0 (every block takes part once per round): all C2(C2-1)/2 pairs of the two blocks
+        // (a local round-robin); later rounds: only the BS^2 cross pairs (A_u, B_(u+sr) mod BS) --
+        // every pair of columns still meets once per sweep, without re-rotating the intra-block
+        // pairs in every round
+        const int nsub = (r == 0) ? C2 - 1 : BS;
+        for (int sr = 0; sr < nsub; ++sr) {
+            int la, lb;
+            if (r == 0) {
+                const int t1 = u_pair, t2 = C2 - 1 - u_pair;
+                la = t1 == 0 ? 0 : 1 + (t1 - 1 + sr) % (C2 - 1);
+                lb = t2 == 0 ? 0 : 1 + (t2 - 1 + sr) % (C2 - 1);
+            } else {
+                la = u_pair;
+                lb = BS + (u_pair + sr) % BS;
+            }
             int lp = la, lq = lb;
             const bool live = gsl < G && s_gc[lp] >= 0 && s_gc[lq] >= 0;
             if (live && s_gc[lp] > s_gc[lq]) { lp = lb; lq = la; }   // p < q by global column index
