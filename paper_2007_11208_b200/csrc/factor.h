@@ -9,6 +9,7 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
                            int iters, int dbg);
 double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
                              int iters);
+unsigned long long* debug_trace_buf(int which);   // lu.cu diagnostics (AS_LU_TRACE)
 int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap);  // lu.cu diagnostics
 void launch_lu_factor(const Work& w, cudaStream_t s);                 // lu.cu                 // W = L\U, ipiv, perm, Dinv0/1, anorm
 void launch_lu_solve(const Work& w, SyncAlloc& sa, cudaStream_t s);   // X = A^{-1} B

@@ -1403,6 +1403,12 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
     launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
 }
 
+// trace buffers for other kernels' diagnostics (triangular solves), nullptr unless AS_LU_TRACE
+unsigned long long* debug_trace_buf(int which) {
+    LuTrace& tr = lu_trace();
+    return which == 0 ? tr.tmin : tr.tmax;
+}
+
 // host copy of the last factorization's trace (diagnostics); returns the slot count or -1
 int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap) {
     LuTrace& tr = lu_trace();

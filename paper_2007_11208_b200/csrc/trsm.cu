@@ -15,9 +15,13 @@
 //
 // The stored triangle (upper/lower), transpose and unit diagonal are template
 // parameters; "forward" order = (lower && !trans) || (upper && trans).
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.h"
 #include "trsm.h"
 #include "blk64.cuh"
+#include "factor.h"
 
 namespace as {
 
@@ -78,6 +82,8 @@ struct TsArgs {
     unsigned long long* ll;          // published X blocks, every word tagged with the solve epoch
     int slot;                        // estimator slot gate (-1: none)
     int skip_if_singular;
+    unsigned long long* tr_start;    // diagnostics (AS_LU_TRACE, multi-RHS solves): per-ticket %globaltimer
+    unsigned long long* tr_end;
 };
 
 // Published X blocks ("LL" words, the tag travels with the data, so one load is both the
@@ -116,12 +122,41 @@ AS_DEV bool ll_get(const unsigned long long* w, unsigned ep, float& x) {
 // group g) owns columns g, g+4, ... over the full k range -> part[0 .. RT/4).
 constexpr int kLDX = kNB + 1;
 template <int RT> struct TsPer { static constexpr int v = RT == 1 ? 1 : RT / 4; };
+// RT = 4, 8: thread (row i, k-quarter g) accumulates ALL RT columns over its 16 k values (every
+// block element is read once from shared memory, RT independent FMA chains), then the four
+// quarters are summed through Red (4 x RT x kNB) -> part[] for columns g, g+4, ...  (one barrier).
+// (A (row, column-group) split reads every block element RT/4... 4 times and was shared-memory
+// bandwidth bound: 2.8 us per 64 x 64 x 8 product with three CTAs per SM.)
 template <typename T, bool TRANSB, int RT>
-AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T (&part)[TsPer<RT>::v], int R) {
+AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T (&part)[TsPer<RT>::v], int R,
+                          T* __restrict__ Red) {
     const int i = threadIdx.x % kNB, g = threadIdx.x / kNB;
     constexpr int PER = TsPer<RT>::v;
 #pragma unroll
     for (int u = 0; u < PER; ++u) part[u] = T(0);
+    if (RT > 1 && RT <= 8) {
+        T a[RT];
+#pragma unroll
+        for (int c = 0; c < RT; ++c) a[c] = T(0);
+#pragma unroll 4
+        for (int kk = 0; kk < kNB / 4; ++kk) {
+            const int k = g * (kNB / 4) + kk;
+            const T m = TRANSB ? Ms[k + i * kLDT] : Ms[i + k * kLDT];
+#pragma unroll
+            for (int c = 0; c < RT; ++c) a[c] += m * Xs[k + c * kLDX];
+        }
+#pragma unroll
+        for (int c = 0; c < RT; ++c) Red[(g * RT + c) * kNB + i] = a[c];
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int c = g + 4 * u;
+            if (c < R)
+                part[u] = (Red[(0 * RT + c) * kNB + i] + Red[(1 * RT + c) * kNB + i]) +
+                          (Red[(2 * RT + c) * kNB + i] + Red[(3 * RT + c) * kNB + i]);
+        }
+        return;
+    }
     if (RT == 1) {
 #pragma unroll 4
         for (int kk = 0; kk < kNB / 4; ++kk) {
@@ -154,7 +189,7 @@ AS_DEV void cp_async_elem(T* smem, const T* gmem, bool ok) {
 // or three CTAs fit per SM and every block of an n <= 16384 solve is resident at once.
 template <typename T, int RT>
 constexpr size_t ts_smem() {
-    return sizeof(T) * (2 * kNB * kLDT + (size_t)kLDX * RT + (RT == 1 ? 4 * kNB : 0));
+    return sizeof(T) * (2 * kNB * kLDT + (size_t)kLDX * RT + (RT == 1 ? 4 * kNB : RT <= 8 ? (size_t)4 * RT * kNB : 0));
 }
 
 template <typename T, bool UPPER, bool TRANS, int RT>
@@ -181,6 +216,10 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     if (threadIdx.x == 0) s_ticket = atomicAdd(&p.sync[0], 1u);
     __syncthreads();
     const unsigned t = s_ticket;
+    if (p.tr_start && threadIdx.x == 0 && t < 2048) p.tr_start[t] = gtimer();
+    // diagnostics: phase stamps of the (step 32, tile 0) CTA into tr_end[1024 + k]
+    const bool probe = p.tr_end && threadIdx.x == 0 && t == 32u * (unsigned)((p.nrhs + RT - 1) / RT);
+#define TSP(k) do { if (probe) p.tr_end[1024 + (k)] = gtimer(); } while (0)
     const int s = (int)(t / ntiles), rt = (int)(t % ntiles);
     const int b = FWD ? s : nblk - 1 - s;
     const int64_t ob = (int64_t)b * kNB;
@@ -228,6 +267,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         else stage_dinv(Ds);                    // last step: Dinv_b into the free buffer
         // X_j (tile rt): each thread spins on its own tagged words until the producer's epoch shows
         (void)oj; (void)nbj;
+        if (sp + 1 == s) TSP(0);
         {
             const unsigned long long* src = p.ll + ((int64_t)(j * ntiles + rt) * RT) * kNB * LLw<T>::v;
             for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
@@ -237,9 +277,11 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
                 Xs[r + c * kLDX] = x;
             }
         }
+        if (sp + 1 == s) TSP(1);
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        block_product<T, TRANS, RT>(Ms, Xs, part, R);
+        if (sp + 1 == s) TSP(2);
+        block_product<T, TRANS, RT>(Ms, Xs, part, R, Red);
         if (RT == 1) {
             Red[g * kNB + i] = part[0];
             __syncthreads();
@@ -251,15 +293,17 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         }
     }
     // X_b = Dinv_b * acc  (trans: Dinv_b^T)
+    TSP(3);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    TSP(4);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
         const int c = RT == 1 ? 0 : g + 4 * u;
         if (RT > 1 || g == 0) Xs[i + c * kLDX] = acc[u];
     }
     __syncthreads();
-    block_product<T, TRANS, RT>(Ds, Xs, part, R);
+    block_product<T, TRANS, RT>(Ds, Xs, part, R, Red);
     unsigned long long* dst = p.ll + ((int64_t)(b * ntiles + rt) * RT) * kNB * LLw<T>::v;
     if (RT == 1) {
         Red[g * kNB + i] = part[0];
@@ -278,6 +322,9 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
             if (i < nbr && c < R) X[(ob + i) + (c0 + c) * p.ldx] = x;
         }
     }
+    TSP(5);
+#undef TSP
+    if (p.tr_end && threadIdx.x == 0 && t < 2048) p.tr_end[t] = gtimer();
 }
 
 // ------------------------------------------------------------------ launchers
@@ -286,7 +333,12 @@ int64_t trsm_sync_words(int64_t n, int nrhs) {
     return 2;
 }
 
-static int ts_rt(int nrhs) { return nrhs == 1 ? 1 : nrhs <= 4 ? 4 : kTsR; }
+// RHS tile width: 1, 4, or the wide tile (AS_TS_RT = 8 / 16 / 32 for experiments)
+static int ts_wide() {
+    static const int v = getenv("AS_TS_RT") ? atoi(getenv("AS_TS_RT")) : kTsR;
+    return (v == 16 || v == 32) ? v : 8;
+}
+static int ts_rt(int nrhs) { return nrhs == 1 ? 1 : nrhs <= 4 ? 4 : ts_wide(); }
 
 int64_t trsm_ll_words(int64_t n, int nrhs) {
     const int64_t nblk = (n + kNB - 1) / kNB;
@@ -326,15 +378,21 @@ static void trsm_dispatch(const TsArgs& p, bool upper, bool trans, const DevArgs
     const int nblk = (int)((p.n + kNB - 1) / kNB);
     auto go = [&](auto kern, int rt, size_t smem) {
         const int ntiles = (p.nrhs + rt - 1) / rt;
+        // experiment knob: AS_TS_CTAS_PER_SM=k pads shared memory so at most k CTAs share an SM
+        static const int per_sm = getenv("AS_TS_CTAS_PER_SM") ? atoi(getenv("AS_TS_CTAS_PER_SM")) : 0;
+        if (per_sm > 0 && rt > 1) smem = std::max<size_t>(smem, (size_t)(220 * 1024) / per_sm);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk * ntiles, kTsThreads, smem, s>>>(p, args, st);
     };
-    auto by_r = [&](auto k1, auto k4, auto k8) {
+    auto by_r = [&](auto k1, auto k4, auto k8, auto k16, auto k32) {
         if (p.nrhs == 1) go(k1, 1, ts_smem<T, 1>());
         else if (p.nrhs <= 4) go(k4, 4, ts_smem<T, 4>());
-        else go(k8, kTsR, ts_smem<T, kTsR>());
+        else if (ts_wide() == 16) go(k16, 16, ts_smem<T, 16>());
+        else if (ts_wide() == 32) go(k32, 32, ts_smem<T, 32>());
+        else go(k8, 8, ts_smem<T, 8>());
     };
-#define AS_TS(U, TR) trsm_sf_kernel<T, U, TR, 1>, trsm_sf_kernel<T, U, TR, 4>, trsm_sf_kernel<T, U, TR, kTsR>
+#define AS_TS(U, TR) trsm_sf_kernel<T, U, TR, 1>, trsm_sf_kernel<T, U, TR, 4>, trsm_sf_kernel<T, U, TR, 8>, \
+                     trsm_sf_kernel<T, U, TR, 16>, trsm_sf_kernel<T, U, TR, 32>
     if (upper) {
         if (trans) by_r(AS_TS(true, true));
         else by_r(AS_TS(true, false));
@@ -349,7 +407,8 @@ void launch_trsm(int dtype, const void* A, int64_t lda, const void* Dinv, bool u
                  int64_t ldx, int64_t n, int nrhs, SyncAlloc& sa, int slot, bool skip_if_singular,
                  const DevArgs* args, const DevState* st, cudaStream_t s) {
     TsArgs p{A, lda, Dinv, X, ldx, n, nrhs, sa.take(trsm_sync_words(n, nrhs)), sa.take_ll(trsm_ll_words(n, nrhs)), slot,
-             skip_if_singular ? 1 : 0};
+             skip_if_singular ? 1 : 0, nullptr, nullptr};
+    if (nrhs > 1) { p.tr_start = debug_trace_buf(0); p.tr_end = debug_trace_buf(1); }
     if (n <= 0 || nrhs <= 0) return;
     if (dtype == AS_F64) trsm_dispatch<double>(p, upper, trans, args, st, s);
     else trsm_dispatch<float>(p, upper, trans, args, st, s);
