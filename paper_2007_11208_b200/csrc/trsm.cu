@@ -408,7 +408,8 @@ void launch_trsm(int dtype, const void* A, int64_t lda, const void* Dinv, bool u
                  const DevArgs* args, const DevState* st, cudaStream_t s) {
     TsArgs p{A, lda, Dinv, X, ldx, n, nrhs, sa.take(trsm_sync_words(n, nrhs)), sa.take_ll(trsm_ll_words(n, nrhs)), slot,
              skip_if_singular ? 1 : 0, nullptr, nullptr};
-    if (nrhs > 1) { p.tr_start = debug_trace_buf(0); p.tr_end = debug_trace_buf(1); }
+    p.tr_start = debug_trace_buf(0);   // diagnostics only (nullptr unless AS_LU_TRACE)
+    p.tr_end = debug_trace_buf(1);
     if (n <= 0 || nrhs <= 0) return;
     if (dtype == AS_F64) trsm_dispatch<double>(p, upper, trans, args, st, s);
     else trsm_dispatch<float>(p, upper, trans, args, st, s);

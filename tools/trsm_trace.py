@@ -10,7 +10,8 @@ import paper_2007_11208_b200 as AS  # noqa: E402
 import workloads as W  # noqa: E402
 tag = sys.argv[1] if len(sys.argv) > 1 else "C3b"
 tiles = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-A, B = W.make(tag)
+nrhs = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+A, B = W.make(tag, nrhs=nrhs) if nrhs else W.make(tag)
 dA, dB = AS.to_device(A), AS.to_device(B)
 for _ in range(2):
     AS.as_solve_ex(dA, dB)
