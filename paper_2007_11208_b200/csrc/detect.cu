@@ -450,6 +450,9 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
     const T max_diag = (T)dfrom(st->max_diag);
     int my_kl = 0, my_ku = 0;
     const int r_loc = 2 * lane;
+    // candidates only die, so the alive mask seen at the previous pair's barrier is a safe
+    // (conservative) guide for which tiles to load: no L2 round trip before the loads
+    unsigned known = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
 
     for (unsigned p = blockIdx.x; p < total; p += gridDim.x) {
         long long I, J;
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
         const bool interior = (r0 + kTile <= n) && (c0 + kTile <= n);
         // candidates only ever die, so a (per-warp) early look at `alive` may skip a tile nobody needs:
         // only UPPER alive -> the mirror (upper) tile is irrelevant; only LOWER alive -> the lower tile is.
-        const unsigned peek = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+        const unsigned peek = known;
         const bool need_lo = (D == 0) || (peek & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
         const bool need_up = (D != 0) && (peek & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
         T lo[16], up[16];
@@ -489,6 +492,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
         }
         __syncthreads();
         const unsigned alive = s_alive;
+        known = alive;
         if (alive == 0) break;
         int kl_loc = 0, ku_loc = 0;
         bool lower_nz = false, upper_nz = false;
