@@ -496,7 +496,12 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
         if (alive == 0) break;
         int kl_loc = 0, ku_loc = 0;
         bool lower_nz = false, upper_nz = false;
-        // ---- band / triangular verdicts in each tile's own layout
+        // ---- band / triangular verdicts in each tile's own layout (only triangular candidates
+        // left and an off-diagonal pair: distances are irrelevant, a non-zero anywhere decides)
+        if (D != 0 && !(alive & (AS_FLAG_BANDED | AS_FLAG_SPD_CANDIDATE))) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) { lower_nz |= lo[i] != T(0); upper_nz |= up[i] != T(0); }
+        } else
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
