@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
             for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
                 const int r = e % kNB, c = e / kNB;
                 T x;
-                while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x)) __nanosleep(ts_backoff_ns);
+                while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x))
+                    if (RT > 1) __nanosleep(ts_backoff_ns);   // single RHS: few pollers, latency first
                 Xs[r + c * kLDX] = x;
             }
         }
