@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <type_traits>
 #include <memory>
 #include <mutex>
 #include <tuple>
@@ -181,6 +182,49 @@ static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
     launch_trtri_blocks(w.dtype, nullptr, w.lda, w.n, w.Dinv0, upper, false, w.st, true, w.args, s);
 }
 
+// Z = [B | e/n | alt] (ld n): the triangular path solves the primary system together with the two
+// estimator applications that do not depend on its iteration (the start vector and the closing
+// alternating-sign probe of xLACN2, Z13b/Z24) -- one sweep instead of three.
+template <typename T>
+__global__ void tri_rhs_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs, T* Z) {
+    const T* B = (const T*)args->B;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * (nrhs + 2); e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % n, c = e / n;
+        T v;
+        if (c < nrhs) v = B[i + c * ldb];
+        else if (c == nrhs) v = T(1) / (T)n;
+        else v = ((i & 1) ? T(-1) : T(1)) * (T(1) + (T)i / (T)(n > 1 ? n - 1 : 1));
+        Z[e] = v;
+    }
+}
+// xe = M (e/n) from Z (the estimator's first result), or X = M B (the primary solution, after the gate)
+template <typename T>
+__global__ void tri_take_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs, const T* Z, T* xe, int which) {
+    T* X = (T*)args->X;
+    const int64_t tot = which == 0 ? n : n * nrhs;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        if (which == 0) xe[e] = Z[e + nrhs * n];
+        else { const int64_t i = e % n, c = e / n; X[i + c * ldb] = Z[e]; }
+    }
+}
+static void tri_fused_solve(const Work& w, bool upper, SyncAlloc& sa, cudaStream_t s) {
+    const int blocks = w.num_sms * 4;
+    auto go = [&](auto* Z) {
+        using T = std::remove_pointer_t<decltype(Z)>;
+        tri_rhs_kernel<T><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, Z);
+        launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, upper, false, Z, w.n, w.n, (int)w.nrhs + 2, sa, -1, true, w.args,
+                    w.st, s);
+        tri_take_kernel<T><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, Z, (T*)w.xe, 0);
+        launch_estimator(w, KIND_TRI, upper, sa, s, Z + (w.nrhs + 1) * w.n);
+    };
+    if (w.dtype == AS_F64) go((double*)w.zx);
+    else go((float*)w.zx);
+}
+static void tri_take_x(const Work& w, cudaStream_t s) {
+    if (w.dtype == AS_F64) tri_take_kernel<double><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, (const double*)w.zx, nullptr, 1);
+    else tri_take_kernel<float><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, (const float*)w.zx, nullptr, 1);
+}
+
 // ------------------------------------------------------------------ branch bodies (shared by graph and eager modes)
 constexpr int kCholOk = 100;
 constexpr int kBandSpike = 101;
@@ -191,8 +235,8 @@ static void body_factor(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     case kBandSpike + 0: case kBandSpike + 1: case kBandSpike + 2: case kBandSpike + 3:
         launch_band_spike(w, m - kBandSpike, s);
         break;
-    case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); launch_estimator(w, KIND_TRI, false, sa, s); break;
-    case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); launch_estimator(w, KIND_TRI, true, sa, s); break;
+    case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); tri_fused_solve(w, false, sa, s); break;
+    case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); tri_fused_solve(w, true, sa, s); break;
     case AS_METHOD_LU: launch_lu_factor(w, s); launch_estimator(w, KIND_LU, false, sa, s); break;
     case kCholOk: launch_chol_tri_prep(w, s); launch_estimator(w, KIND_CHOL, false, sa, s); break;
     default: break;
@@ -204,9 +248,7 @@ static void body_solve(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     case AS_METHOD_BAND: launch_band_solve(w, s); break;
     case AS_METHOD_TRI_LOWER:
     case AS_METHOD_TRI_UPPER:
-        launch_copy_b_to_x(w, s);
-        launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, m == AS_METHOD_TRI_UPPER, false, nullptr, w.ldb, w.n,
-                    (int)w.nrhs, sa, -1, false, w.args, w.st, s);
+        tri_take_x(w, s);          // solved with the estimator's first application (tri_fused_solve)
         break;
     case AS_METHOD_CHOL: launch_chol_solve(w, sa, s); break;
     case AS_METHOD_LU: launch_lu_solve(w, sa, s); break;
@@ -282,6 +324,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.Dinv1 = take(es * nblk * kNB * kNB);
     w.vec = take(es * n * std::max<int64_t>(nr, 2));
     w.yv = take(es * n * nr);
+    w.zx = take(es * n * (nr + 2));
     w.ipiv = (int64_t*)take(8 * n);
     w.perm = (int64_t*)take(8 * n);
     w.flags_ts_len = 160 * trsm_sync_words(n, (int)nr);

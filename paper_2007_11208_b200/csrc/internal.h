@@ -31,6 +31,7 @@ struct Work {
     void* Dinv1;         // n x kNB (second triangular factor)
     void* vec;           // scratch n x max(nrhs,2) (QR c = Q^T b etc.)
     void* yv;            // n x nrhs (fallback V^T c)
+    void* zx;            // n x (nrhs + 2): triangular path's fused solve [B | e/n | alt] (ld n)
     int64_t* ipiv;       // n
     int64_t* perm;       // n (LU row permutation)
     unsigned* flags_ts;  // sync-free triangular-solve tickets/flags: (n/kNB+1) * tiles + 64

@@ -66,9 +66,10 @@ AS_DEV void set_alt(T* x, int64_t n) {
 
 // x = e/n, est_next = 0 (or done if the factor was singular / n == 0)
 template <typename T>
-__global__ void est_begin_kernel(DevState* st, T* x, int64_t n) {
+__global__ void est_begin_kernel(DevState* st, T* x, int64_t n, int init_x) {
     const bool singular = st->info != ~0ull;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = T(1) / (T)n;
+    if (init_x)
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = T(1) / (T)n;
     if (threadIdx.x == 0) {
         st->est_next = singular ? -1 : 0;
         st->est = 0.0;
@@ -80,13 +81,29 @@ __global__ void est_begin_kernel(DevState* st, T* x, int64_t n) {
 
 // After apply slot `slot` ran on x (only if est_next == slot).
 // xs holds the stored sign vector (isgn) as +-1.
+// altres != nullptr: M applied to the closing alternating-sign probe was computed up front (fused
+// into the primary solve): the probe's estimate temp = 2 ||M alt||_1 / (3n) is taken at once
+// instead of requesting one more application.
 template <typename T>
-__global__ void __launch_bounds__(kEstThreads) est_step_kernel(DevState* st, T* x, T* xs, int64_t n, int slot) {
+__global__ void __launch_bounds__(kEstThreads) est_step_kernel(DevState* st, T* x, T* xs, int64_t n, int slot,
+                                                               const T* altres) {
     if (ld_volatile_i32(&st->est_next) != slot) return;
     __shared__ T sh[32];
     __shared__ T shv[32];
     __shared__ long long shi[32];
     __shared__ int s_flag;
+    // the closing probe from the precomputed M alt (block-uniform call): est = max(est_now, temp)
+    auto alt_now = [&](T est_now) {
+        T sa = T(0);
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sa += altres[i] < T(0) ? -altres[i] : altres[i];
+        sa = block_sum(sa, sh);
+        if (threadIdx.x == 0) {
+            const T temp = T(2) * (sa / (T)(3 * n));
+            st->est = (double)(temp > est_now ? temp : est_now);
+            st->est_iter = -1;
+            st->est_next = -1;
+        }
+    };
     if (slot == 0) {
         if (n == 1) {
             if (threadIdx.x == 0) {
@@ -140,7 +157,10 @@ __global__ void __launch_bounds__(kEstThreads) est_step_kernel(DevState* st, T* 
         const bool differ = s_flag != 0;
         __syncthreads();
         const bool go_alt = !differ || (s <= estold);
-        if (go_alt) {
+        if (go_alt && altres) {
+            if (threadIdx.x == 0) st->est_old = (double)estold;
+            alt_now(s);
+        } else if (go_alt) {
             set_alt(x, n);
             if (threadIdx.x == 0) { st->est = (double)s; st->est_old = (double)estold; st->est_iter = -1; st->est_next = slot + 2; }
         } else {
@@ -164,6 +184,9 @@ __global__ void __launch_bounds__(kEstThreads) est_step_kernel(DevState* st, T* 
         if (xjl != xj && iter < 5) {
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == j) ? T(1) : T(0);
             if (threadIdx.x == 0) { st->est_jlast = jlast; st->est_j = (int)j; st->est_iter = iter + 1; st->est_next = slot + 1; }
+        } else if (altres) {
+            if (threadIdx.x == 0) { st->est_jlast = jlast; st->est_j = (int)j; }
+            alt_now((T)st->est);
         } else {
             set_alt(x, n);
             if (threadIdx.x == 0) { st->est_jlast = jlast; st->est_j = (int)j; st->est_iter = -1; st->est_next = slot + 1; }
@@ -187,15 +210,22 @@ __global__ void est_finish_kernel(DevState* st) {
 // kind: KIND_LU (W = L\U, Dinv0 = inv blocks of unit L, Dinv1 = of U),
 //       KIND_TRI (args->A triangle, Dinv0), KIND_CHOL (W = L, Dinv0),
 //       KIND_BAND (band solves, see band.cu).
-void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaStream_t s) {
+void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaStream_t s, const void* altres) {
     const int dt = w.dtype;
     const int64_t n = w.n;
     const int64_t ldw = w.ldw;  // W leading dimension
-    if (dt == AS_F64) est_begin_kernel<double><<<1, kEstThreads, 0, s>>>(w.st, (double*)w.xe, n);
-    else est_begin_kernel<float><<<1, kEstThreads, 0, s>>>(w.st, (float*)w.xe, n);
+    // altres != nullptr: xe already holds M (e/n) and altres M alt (fused into the primary solve)
+    const int init_x = altres ? 0 : 1;
+    if (dt == AS_F64) est_begin_kernel<double><<<1, kEstThreads, 0, s>>>(w.st, (double*)w.xe, n, init_x);
+    else est_begin_kernel<float><<<1, kEstThreads, 0, s>>>(w.st, (float*)w.xe, n, init_x);
     void* xs = (char*)w.vec;  // sign vector scratch (n elements)
     for (int slot = 0; slot < kEstSlots; ++slot) {
         const bool trans = (slot & 1) != 0;
+        if (altres && slot == 0) {                 // first application already done
+            if (dt == AS_F64) est_step_kernel<double><<<1, kEstThreads, 0, s>>>(w.st, (double*)w.xe, (double*)xs, n, 0, (const double*)altres);
+            else est_step_kernel<float><<<1, kEstThreads, 0, s>>>(w.st, (float*)w.xe, (float*)xs, n, 0, (const float*)altres);
+            continue;
+        }
         auto tr = [&](const void* A, int64_t lda, const void* Dinv, bool up, bool t) {
             launch_trsm(dt, A, lda, Dinv, up, t, w.xe, n, n, 1, sa, slot, true, w.args,
                         w.st, s);
@@ -216,8 +246,8 @@ void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaSt
             launch_band_apply(w, trans, slot, s);
             break;
         }
-        if (dt == AS_F64) est_step_kernel<double><<<1, kEstThreads, 0, s>>>(w.st, (double*)w.xe, (double*)xs, n, slot);
-        else est_step_kernel<float><<<1, kEstThreads, 0, s>>>(w.st, (float*)w.xe, (float*)xs, n, slot);
+        if (dt == AS_F64) est_step_kernel<double><<<1, kEstThreads, 0, s>>>(w.st, (double*)w.xe, (double*)xs, n, slot, (const double*)altres);
+        else est_step_kernel<float><<<1, kEstThreads, 0, s>>>(w.st, (float*)w.xe, (float*)xs, n, slot, (const float*)altres);
     }
     if (dt == AS_F64) est_finish_kernel<double><<<1, 32, 0, s>>>(w.st);
     else est_finish_kernel<float><<<1, 32, 0, s>>>(w.st);

@@ -7,7 +7,7 @@ namespace as {
 
 enum { KIND_LU = 0, KIND_BAND = 1, KIND_TRI = 2, KIND_CHOL = 3 };
 
-void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaStream_t s);
+void launch_estimator(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaStream_t s, const void* altres = nullptr);
 
 // band.cu
 void launch_band_norm(const Work& w, cudaStream_t s);              // anorm of the band
