@@ -186,12 +186,12 @@ static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
 // estimator applications that do not depend on its iteration (the start vector and the closing
 // alternating-sign probe of xLACN2, Z13b/Z24) -- one sweep instead of three.
 template <typename T>
-__global__ void tri_rhs_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs, T* Z) {
+__global__ void tri_rhs_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs, T* Z, const int64_t* perm) {
     const T* B = (const T*)args->B;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * (nrhs + 2); e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e % n, c = e / n;
         T v;
-        if (c < nrhs) v = B[i + c * ldb];
+        if (c < nrhs) v = B[(perm ? perm[i] : i) + c * ldb];      // LU: the rows of P B
         else if (c == nrhs) v = T(1) / (T)n;
         else v = ((i & 1) ? T(-1) : T(1)) * (T(1) + (T)i / (T)(n > 1 ? n - 1 : 1));
         Z[e] = v;
@@ -207,15 +207,25 @@ __global__ void tri_take_kernel(const DevArgs* args, int64_t n, int64_t ldb, int
         else { const int64_t i = e % n, c = e / n; X[i + c * ldb] = Z[e]; }
     }
 }
-static void tri_fused_solve(const Work& w, bool upper, SyncAlloc& sa, cudaStream_t s) {
+// kind KIND_TRI (the caller's triangle), KIND_CHOL (L then L^T), KIND_LU (P B; unit L then U; the
+// estimator's columns without interchanges, as xGECON applies inv(U) inv(L), Z13b)
+static void fused_solve(const Work& w, int kind, bool upper, SyncAlloc& sa, cudaStream_t s) {
     const int blocks = w.num_sms * 4;
+    const int nz = (int)w.nrhs + 2;
     auto go = [&](auto* Z) {
         using T = std::remove_pointer_t<decltype(Z)>;
-        tri_rhs_kernel<T><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, Z);
-        launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, upper, false, Z, w.n, w.n, (int)w.nrhs + 2, sa, -1, true, w.args,
-                    w.st, s);
+        tri_rhs_kernel<T><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, Z, kind == KIND_LU ? w.perm : nullptr);
+        if (kind == KIND_TRI) {
+            launch_trsm(w.dtype, nullptr, w.lda, w.Dinv0, upper, false, Z, w.n, w.n, nz, sa, -1, true, w.args, w.st, s);
+        } else if (kind == KIND_CHOL) {
+            launch_trsm(w.dtype, w.W, w.ldw, w.Dinv0, false, false, Z, w.n, w.n, nz, sa, -1, true, w.args, w.st, s);
+            launch_trsm(w.dtype, w.W, w.ldw, w.Dinv0, false, true, Z, w.n, w.n, nz, sa, -1, true, w.args, w.st, s);
+        } else {
+            launch_trsm(w.dtype, w.W, w.ldw, w.Dinv0, false, false, Z, w.n, w.n, nz, sa, -1, true, w.args, w.st, s);
+            launch_trsm(w.dtype, w.W, w.ldw, w.Dinv1, true, false, Z, w.n, w.n, nz, sa, -1, true, w.args, w.st, s);
+        }
         tri_take_kernel<T><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, Z, (T*)w.xe, 0);
-        launch_estimator(w, KIND_TRI, upper, sa, s, Z + (w.nrhs + 1) * w.n);
+        launch_estimator(w, kind, upper, sa, s, Z + (w.nrhs + 1) * w.n);
     };
     if (w.dtype == AS_F64) go((double*)w.zx);
     else go((float*)w.zx);
@@ -235,10 +245,12 @@ static void body_factor(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     case kBandSpike + 0: case kBandSpike + 1: case kBandSpike + 2: case kBandSpike + 3:
         launch_band_spike(w, m - kBandSpike, s);
         break;
-    case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); tri_fused_solve(w, false, sa, s); break;
-    case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); tri_fused_solve(w, true, sa, s); break;
-    case AS_METHOD_LU: launch_lu_factor(w, s); launch_estimator(w, KIND_LU, false, sa, s); break;
-    case kCholOk: launch_chol_tri_prep(w, s); launch_estimator(w, KIND_CHOL, false, sa, s); break;
+    // the primary solve runs with the estimator's first application (the gate may still send the
+    // call to the fallback, which then overwrites X; X itself is written only after the gate)
+    case AS_METHOD_TRI_LOWER: tri_prep(w, false, s); fused_solve(w, KIND_TRI, false, sa, s); break;
+    case AS_METHOD_TRI_UPPER: tri_prep(w, true, s); fused_solve(w, KIND_TRI, true, sa, s); break;
+    case AS_METHOD_LU: launch_lu_factor(w, s); fused_solve(w, KIND_LU, false, sa, s); break;
+    case kCholOk: launch_chol_tri_prep(w, s); fused_solve(w, KIND_CHOL, false, sa, s); break;
     default: break;
     }
 }
@@ -248,10 +260,10 @@ static void body_solve(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
     case AS_METHOD_BAND: launch_band_solve(w, s); break;
     case AS_METHOD_TRI_LOWER:
     case AS_METHOD_TRI_UPPER:
-        tri_take_x(w, s);          // solved with the estimator's first application (tri_fused_solve)
+        tri_take_x(w, s);          // solved with the estimator's first application (fused_solve)
         break;
-    case AS_METHOD_CHOL: launch_chol_solve(w, sa, s); break;
-    case AS_METHOD_LU: launch_lu_solve(w, sa, s); break;
+    case AS_METHOD_CHOL:
+    case AS_METHOD_LU: tri_take_x(w, s); break;   // solved in fused_solve
     default: break;
     }
 }
@@ -329,7 +341,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.perm = (int64_t*)take(8 * n);
     w.flags_ts_len = 160 * trsm_sync_words(n, (int)nr);
     w.flags_ts = (unsigned*)take(4 * w.flags_ts_len);
-    w.ll_len = 100 * trsm_ll_words(n, 1) + 10 * trsm_ll_words(n, (int)nr);
+    w.ll_len = 100 * trsm_ll_words(n, 1) + 10 * trsm_ll_words(n, (int)nr + 2);   // + the fused solves' 2 columns
     w.ll = (unsigned long long*)take(8 * w.ll_len);
     w.bars_len = 8 + nblk + 8;
     w.bars = (unsigned*)take(4 * w.bars_len);

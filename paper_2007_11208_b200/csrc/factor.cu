@@ -64,38 +64,6 @@ void launch_copy_norm(const Work& w, bool with_perm, cudaStream_t s) {
                                                               with_perm ? w.perm : nullptr);
 }
 
-// X[i,:] = B[perm[i], :]  (through scratch when X aliases B)
-template <typename T>
-__global__ void gather_rows_kernel(const DevArgs* args, int64_t n, int64_t ldb, int64_t nrhs, const int64_t* perm,
-                                   T* scratch, int phase) {
-    const T* B = (const T*)args->B;
-    T* X = (T*)args->X;
-    const bool alias = (const void*)B == (const void*)X;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * nrhs; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e % n, c = e / n;
-        if (phase == 0) {
-            if (alias) scratch[i + c * n] = B[i + c * ldb];
-        } else {
-            X[i + c * ldb] = alias ? scratch[perm[i] + c * n] : B[perm[i] + c * ldb];
-        }
-    }
-}
-
-void launch_lu_solve(const Work& w, SyncAlloc& sa, cudaStream_t s) {
-    const int blocks = w.num_sms * 4;
-    if (w.dtype == AS_F64) {
-        gather_rows_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, w.perm, (double*)w.vec, 0);
-        gather_rows_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, w.perm, (double*)w.vec, 1);
-    } else {
-        gather_rows_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, w.perm, (float*)w.vec, 0);
-        gather_rows_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.n, w.ldb, w.nrhs, w.perm, (float*)w.vec, 1);
-    }
-    launch_trsm(w.dtype, w.W, w.ldw, w.Dinv0, false, false, nullptr, w.ldb, w.n, (int)w.nrhs,
-                sa, -1, false, w.args, w.st, s);
-    launch_trsm(w.dtype, w.W, w.ldw, w.Dinv1, true, false, nullptr, w.ldb, w.n, (int)w.nrhs,
-                sa, -1, false, w.args, w.st, s);
-}
-
 // ------------------------------------------------------------------ Cholesky
 // POTF2 of one kNB x kNB diagonal block in shared memory, plus its inverse.
 // Factor: right-looking with the scaling deferred (a_ik -= a_ij a_kj / d_j, then column j is
@@ -513,14 +481,6 @@ void launch_chol_check(const Work& w, cudaGraphConditionalHandle h, cudaStream_t
 
 void launch_chol_tri_prep(const Work& w, cudaStream_t s) {
     (void)w; (void)s;   // potf2_kernel already wrote the inverse diagonal blocks of L to Dinv0
-}
-
-void launch_chol_solve(const Work& w, SyncAlloc& sa, cudaStream_t s) {
-    launch_copy_b_to_x(w, s);
-    launch_trsm(w.dtype, w.W, w.ldw, w.Dinv0, false, false, nullptr, w.ldb, w.n, (int)w.nrhs,
-                sa, -1, false, w.args, w.st, s);
-    launch_trsm(w.dtype, w.W, w.ldw, w.Dinv0, false, true, nullptr, w.ldb, w.n, (int)w.nrhs,
-                sa, -1, false, w.args, w.st, s);
 }
 
 }  // namespace as

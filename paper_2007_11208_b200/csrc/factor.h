@@ -11,10 +11,8 @@ double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t 
                              int iters);
 unsigned long long* debug_trace_buf(int which);   // lu.cu diagnostics (AS_LU_TRACE)
 int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap);  // lu.cu diagnostics
-void launch_lu_factor(const Work& w, cudaStream_t s);                 // lu.cu                 // W = L\U, ipiv, perm, Dinv0/1, anorm
-void launch_lu_solve(const Work& w, SyncAlloc& sa, cudaStream_t s);   // X = A^{-1} B
+void launch_lu_factor(const Work& w, cudaStream_t s);                 // lu.cu: W = L\U, ipiv, perm, Dinv0/1, anorm
 void launch_chol_factor(const Work& w, cudaStream_t s);               // W = L (lower), anorm, chol_failed
 void launch_chol_check(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s);
 void launch_chol_tri_prep(const Work& w, cudaStream_t s);             // Dinv0 of L
-void launch_chol_solve(const Work& w, SyncAlloc& sa, cudaStream_t s);
 }  // namespace as
