@@ -954,46 +954,6 @@ __global__ void __launch_bounds__(256) lu_linv_kernel(const T* W, int64_t ldw, i
     for (int e = threadIdx.x; e < kB64 * kB64; e += blockDim.x) D[e] = X[(e & 63) + (e >> 6) * kB64LD];
 }
 
-// U12 = L11^{-1} A12 in place: one CTA per 64-column tile of rows r0 .. r0+nb, as the product
-// Dinv0(block) x tile (4 x 4 register tiles).
-constexpr int kU12LD = kB64 + 4;
-template <typename T>
-__global__ void __launch_bounds__(256) u12v3_kernel(T* W, int64_t ldw, int64_t r0, int nb, int64_t c0, int64_t c1,
-                                                    const T* Dinv) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* Ls = (T*)smem_raw;            // Ls[k][r] = Linv(r, k)
-    T* Bs = Ls + kB64 * kU12LD;      // Bs[k][c] = A12(k, c)
-    const int64_t cc0 = c0 + (int64_t)blockIdx.x * kB64;
-    const int nc = (int)min<int64_t>(kB64, c1 - cc0);
-    if (nc <= 0) return;
-    const T* D = Dinv + (r0 / kB64) * (int64_t)kB64 * kB64;
-    batched<8, T>(
-        2 * kB64 * kB64,
-        [&](int e) -> T {
-            if (e < kB64 * kB64) return D[e];
-            const int f = e - kB64 * kB64, k = f & 63, c = f >> 6;
-            return (k < nb && c < nc) ? W[(r0 + k) + (cc0 + c) * ldw] : T(0);
-        },
-        [&](int e, T v) {
-            if (e < kB64 * kB64) Ls[(e >> 6) * kU12LD + (e & 63)] = v;
-            else { const int f = e - kB64 * kB64; Bs[(f & 63) * kU12LD + (f >> 6)] = v; }
-        });
-    __syncthreads();
-    T acc[4][4];
-    tile_mul64<T>(Ls, kU12LD, Bs, kU12LD, nb, acc);
-    const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int c = 4 * tc + q;
-        if (c >= nc) continue;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const int r = 4 * tr + p;
-            if (r < nb) W[(r0 + r) + (cc0 + c) * ldw] = acc[p][q];
-        }
-    }
-}
-
 // ------------------------------------------------------------------ fused interchanges + U12
 // For the trailing columns [c0, c1) of block k0 (bw <= 128 rows, one CTA per 32 columns):
 //   1. the block's bw interchanges, composed into a permutation of S = block rows U targets
@@ -1280,15 +1240,6 @@ static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
 }
 
 template <typename T>
-static void u12_launch(const Work& w, int64_t r0, int nb, int64_t c0, int64_t c1, cudaStream_t s) {
-    if (c1 <= c0) return;
-    const int smem = (int)(sizeof(T) * 2 * kB64 * kU12LD);
-    cudaFuncSetAttribute(u12v3_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    u12v3_kernel<T><<<(unsigned)((c1 - c0 + kB64 - 1) / kB64), 256, smem, s>>>((T*)w.W, w.ldw, r0, nb, c0, c1,
-                                                                             (const T*)w.Dinv0);
-}
-
-template <typename T>
 static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s) {
     if (c1 <= c0) return;
     const int smem = (int)(sizeof(T) * (2 * kSUC * kSULD + 3 * kB64 * kB64));
@@ -1322,19 +1273,11 @@ static void gemm_launch(const Work& w, int64_t r0, int64_t c0, int64_t k0, int64
 template <typename T>
 static void block_panels(const Work& w, int64_t k0, int bw, int prio, cudaStream_t s) {
     const int64_t n = w.n;
-    const int p1 = std::min(kPW, bw);
-    // sequence numbers of the panel exchange grow monotonically with the panel's column
-    panel_launch<T>(w, k0, p1, (unsigned long long)(k0 / kPW) * 256ull, prio, s);
-    linv_launch<T>(w, k0, p1, s);
-    if (bw > p1) {
-        const int p2 = bw - p1;
-        // bring the block's second half up to date: swaps of panel 1, U12, rank-p1 update
-        laswp_launch<T>(w, k0, p1, k0 + p1, k0 + bw, 0, 0, false, s);
-        u12_launch<T>(w, k0, p1, k0 + p1, k0 + bw, s);
-        gemm_launch<T>(w, k0 + p1, k0 + p1, k0, n - k0 - p1, p2, p1, s, prio);
-        panel_launch<T>(w, k0 + p1, p2, (unsigned long long)((k0 + p1) / kPW) * 256ull, prio, s);
-        linv_launch<T>(w, k0 + p1, p2, s);
-    }
+    (void)n;
+    // one panel per block (kPW == kBW); sequence numbers of the panel exchange grow with the block
+    static_assert(kPW == kBW, "block_panels factors a block as one panel");
+    panel_launch<T>(w, k0, bw, (unsigned long long)(k0 / kPW) * 256ull, prio, s);
+    linv_launch<T>(w, k0, bw, s);
 }
 
 template <typename T>
