@@ -12,6 +12,8 @@
 //
 // Requirements (checked by the launcher): all leading dimensions even and
 // every operand origin 16-byte aligned (the workspace guarantees this).
+#include <cstdlib>
+
 #include "gemm.h"
 #include "internal.h"
 
@@ -254,6 +256,122 @@ __global__ void __launch_bounds__(GTHREADS) gemm_sgemm_kernel(GemmArgs g) {
     }
 }
 
+// ------------------------------------------------------------------ fp32 SIMT kernel v2 (NN)
+// C -= A B with A (M x K) and B (K x N) column-major, the LU trailing update's shape.  CTA tile
+// 128 x 128 x 16, 256 threads, 8 x 8 register tile per thread (rows ty*4.. and 64+ty*4.., columns
+// tx*4.. and 64+tx*4..: every operand read is an LDS.128), 16-byte global loads, the next k-tile's
+// loads issued before the current tile's 1024 FFMAs per thread (double-buffered shared memory).
+// A tile: As[k][m] straight from the m-contiguous columns; B tile: Bs[k][n] through registers
+// (4 consecutive k of one column per LDG.128, stored as 4 conflict-free row writes).
+namespace s2 {
+constexpr int BM = 128, BN = 128, BK = 16, NT = 256;
+constexpr int LDA = BM + 4, LDB = BN + 4;
+}
+__global__ void __launch_bounds__(s2::NT, 2) gemm_sgemm_nn_kernel(GemmArgs g) {
+    using namespace s2;
+    if (g.skip && *g.skip) return;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    if (g.lower_only && n0 > m0 + BM - 1) return;
+    __shared__ __align__(16) float As[2][BK][LDA];
+    __shared__ __align__(16) float Bs[2][BK][LDB];
+    const float* A = (const float*)g.A;
+    const float* B = (const float*)g.B;
+    float* C = (float*)g.C;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const bool full = (m0 + BM <= g.M) && (n0 + BN <= g.N);
+    const int nk = (int)((g.K + BK - 1) / BK);
+    float4 ra[2], rb[2];
+    // thread e (0..511 over 2 loads): A chunk (k = e / 32, m = 4 (e % 32)); B chunk (n = e % 128, k = 4 (e / 128))
+    auto gload = [&](int kt) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = threadIdx.x + q * NT;
+            const int ka = e >> 5, ma = (e & 31) * 4;
+            const int64_t gk = (int64_t)kt * BK + ka, gm = m0 + ma;
+            if (gk < g.K && gm + 3 < g.M) ra[q] = __ldg((const float4*)(A + gm + gk * g.lda));
+            else {
+                float t[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) t[u] = (gk < g.K && gm + u < g.M) ? A[gm + u + gk * g.lda] : 0.f;
+                ra[q] = make_float4(t[0], t[1], t[2], t[3]);
+            }
+            const int nb = e & 127, kb = (e >> 7) * 4;
+            const int64_t gkb = (int64_t)kt * BK + kb, gn = n0 + nb;
+            if (gn < g.N && gkb + 3 < g.K) rb[q] = __ldg((const float4*)(B + gkb + gn * g.ldb));
+            else {
+                float t[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) t[u] = (gn < g.N && gkb + u < g.K) ? B[gkb + u + gn * g.ldb] : 0.f;
+                rb[q] = make_float4(t[0], t[1], t[2], t[3]);
+            }
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = threadIdx.x + q * NT;
+            *(float4*)&As[buf][e >> 5][(e & 31) * 4] = ra[q];
+            const int nb = e & 127, kb = (e >> 7) * 4;
+            Bs[buf][kb + 0][nb] = rb[q].x;
+            Bs[buf][kb + 1][nb] = rb[q].y;
+            Bs[buf][kb + 2][nb] = rb[q].z;
+            Bs[buf][kb + 3][nb] = rb[q].w;
+        }
+    };
+    gload(0);                      // the first tile's loads in flight together with C's
+    float acc[8][8];   // starts as C; accumulates C - A B
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int64_t c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t r = m0 + ty * 4 + 64 * h;
+            if (full) {
+                const float4 v = __ldcg((const float4*)(C + r + c * g.ldc));
+                acc[4 * h + 0][j] = v.x; acc[4 * h + 1][j] = v.y; acc[4 * h + 2][j] = v.z; acc[4 * h + 3][j] = v.w;
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[4 * h + q][j] = (r + q < g.M && c < g.N) ? __ldcg(C + r + q + c * g.ldc) : 0.f;
+            }
+        }
+    }
+    sstore(0);
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < nk) gload(kt + 1);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            float a[8], b[8];
+            *(float4*)&a[0] = *(const float4*)&As[buf][k][ty * 4];
+            *(float4*)&a[4] = *(const float4*)&As[buf][k][64 + ty * 4];
+            *(float4*)&b[0] = *(const float4*)&Bs[buf][k][tx * 4];
+            *(float4*)&b[4] = *(const float4*)&Bs[buf][k][64 + tx * 4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(-a[i], b[j], acc[i][j]);
+        }
+        if (kt + 1 < nk) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int64_t c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t r = m0 + ty * 4 + 64 * h;
+            if (full) {
+                *(float4*)(C + r + c * g.ldc) = make_float4(acc[4 * h][j], acc[4 * h + 1][j], acc[4 * h + 2][j], acc[4 * h + 3][j]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (r + q < g.M && c < g.N) C[r + q + c * g.ldc] = acc[4 * h + q][j];
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ fp64 DMMA kernel v2
 // CTA tile 128 x 64 x 16, 4 warps (2 x 2, warp tile 64 x 32 = 8 x 4 DMMA tiles),
 // 3-stage cp.async pipeline, 2 CTAs per SM so one CTA's C read-modify-write
@@ -452,7 +570,13 @@ void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
         else if (g.TA && !g.TB) go(gemm_dmma2_kernel<true, false>);
         else go(gemm_dmma2_kernel<true, true>);
     } else {
-        if (!g.TA && !g.TB) launch_k(gemm_sgemm_kernel<false, false>, g, 0, s);
+        // NN with 16-byte aligned operands (the LU trailing update): the v2 kernel
+        const bool al = (((uintptr_t)g.A | (uintptr_t)g.B | (uintptr_t)g.C) & 15) == 0 && g.lda % 4 == 0 &&
+                        g.ldb % 4 == 0 && g.ldc % 4 == 0;
+        if (!g.TA && !g.TB && al && getenv("AS_SGEMM_V1") == nullptr) {
+            dim3 grid((unsigned)((g.M + s2::BM - 1) / s2::BM), (unsigned)((g.N + s2::BN - 1) / s2::BN));
+            gemm_sgemm_nn_kernel<<<grid, s2::NT, 0, s>>>(g);
+        } else if (!g.TA && !g.TB) launch_k(gemm_sgemm_kernel<false, false>, g, 0, s);
         else if (!g.TA && g.TB) launch_k(gemm_sgemm_kernel<false, true>, g, 0, s);
         else if (g.TA && !g.TB) launch_k(gemm_sgemm_kernel<true, false>, g, 0, s);
         else launch_k(gemm_sgemm_kernel<true, true>, g, 0, s);
