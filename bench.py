@@ -79,6 +79,15 @@ def load_traffic():
         return {}
 
 
+def clocks_peak_ghz() -> float:
+    """Max SM clock (GHz) from MEASURED_PEAKS.json (1.965 on this pool's B200s)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("sm_max_mhz", 1965.0)) / 1e3
+    except (OSError, ValueError):
+        return 1.965
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -351,6 +360,14 @@ def main():
         ach = info["detect_bytes"] / (stage[0] * 1e-3) / 1e9
         roof.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                      "traffic": None, "algorithmic_bytes": info["detect_bytes"], "peak_source": hbm_src})
+    elif info.get("factor_flops") and dom == 1 and tag == "C5f":
+        # fp32 runs on the SIMT FFMA pipe (tf32 tensor cores would miss the fp32 accuracy bar):
+        # plain ALU arithmetic against the unit-count peak
+        ffma_peak = 148 * 128 * 2 * clocks_peak_ghz() / 1e3
+        ach = info["factor_flops"] / (stage[1] * 1e-3) / 1e12
+        roof.update({"bound": "alu", "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s",
+                     "frac": ach / ffma_peak, "traffic": None, "algorithmic_flops": info["factor_flops"],
+                     "peak_source": "FP32 FFMA unit count: 148 SMs x 128 lanes x 2 flop x max SM clock"})
     elif info.get("factor_flops") and dom == 1:
         ach = info["factor_flops"] / (stage[1] * 1e-3) / 1e12
         roof.update({"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
