@@ -409,8 +409,11 @@ void launch_trsm(int dtype, const void* A, int64_t lda, const void* Dinv, bool u
                  const DevArgs* args, const DevState* st, cudaStream_t s) {
     TsArgs p{A, lda, Dinv, X, ldx, n, nrhs, sa.take(trsm_sync_words(n, nrhs)), sa.take_ll(trsm_ll_words(n, nrhs)), slot,
              skip_if_singular ? 1 : 0, nullptr, nullptr};
-    p.tr_start = debug_trace_buf(0);   // diagnostics only (nullptr unless AS_LU_TRACE)
-    p.tr_end = debug_trace_buf(1);
+    // diagnostics only: the per-CTA timeline shares the LU trace buffers (AS_LU_TRACE) and is taken
+    // only with AS_TS_TRACE as well (tools/trsm_trace.py), so that the LU timeline stays intact
+    static const bool ts_trace = getenv("AS_TS_TRACE") != nullptr;
+    p.tr_start = ts_trace ? debug_trace_buf(0) : nullptr;
+    p.tr_end = ts_trace ? debug_trace_buf(1) : nullptr;
     if (n <= 0 || nrhs <= 0) return;
     if (dtype == AS_F64) trsm_dispatch<double>(p, upper, trans, args, st, s);
     else trsm_dispatch<float>(p, upper, trans, args, st, s);

@@ -2,7 +2,7 @@
 #   bench lines for every config, the reference arm, the eager ncu launch list of the default
 #   bench command, and one ncu --set full capture per dominant kernel.
 set -x
-O=gpurun_out/r01e
+O=gpurun_out/r01f
 mkdir -p $O
 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?"
 for c in C1 C3a C3b C4 C5 C5f; do

@@ -1,9 +1,10 @@
-"""Per-CTA timeline of the multi-RHS triangular solve of one C3b / C3a solve (AS_LU_TRACE=1):
+"""Per-CTA timeline of the multi-RHS triangular solve of one C3b / C3a solve (AS_LU_TRACE=1 AS_TS_TRACE=1):
 ticket t = step s * tiles + tile; prints, per block step, the tile-0 CTA's start / end (us)."""
 import ctypes as C
 import os
 import sys
 os.environ["AS_LU_TRACE"] = "1"
+os.environ["AS_TS_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 import paper_2007_11208_b200 as AS  # noqa: E402
