@@ -201,7 +201,8 @@ int as_debug_timestamps(unsigned long long* out16);
  * first launch is not averaged when iters > 1).  kind 0: LU register/cluster panel,
  * 1: LU cooperative panel, 2: Cholesky cluster panel, 3: Cholesky POTF2 + L21.
  * dbg: ablation bits of the LU register panel (1 skip interchanges on other columns, 2 skip the
- * deferred update, 8 skip the column loop) -- timing studies only, results are then wrong.
+ * deferred update, 8 skip the column loop) -- timing studies only, results are then wrong;
+ * kind 3: 2 = POTF2 only (no L21), 4 = restore only the panel columns (L2 stays warm).
  * Returns < 0 on an illegal argument or a CUDA error (-error code). */
 double as_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
                            int iters, int dbg);

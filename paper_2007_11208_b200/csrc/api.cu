@@ -854,7 +854,7 @@ double as_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
                            int iters, int dbg) {
     if (!W || !Wsrc || n <= 0 || k0 < 0 || k0 >= n || nbp <= 0 || ldw < n || iters <= 0) return -1.0;
     if (kind <= 1) return as::lu_debug_panel_time(dtype, kind, W, ldw, n, k0, nbp, Wsrc, iters, dbg);
-    return as::chol_debug_panel_time(dtype, kind - 2, W, ldw, n, k0, nbp, Wsrc, iters);
+    return as::chol_debug_panel_time(dtype, kind - 2, W, ldw, n, k0, nbp, Wsrc, iters, dbg);
 }
 
 int as_debug_lu_trace(unsigned long long* tmin, unsigned long long* tmax, int cap) {

@@ -414,7 +414,7 @@ static void chol_factor_t(const Work& w, cudaStream_t s) {
 // Diagnostics: average time (us) of one Cholesky panel of W (restored from Wsrc before each
 // launch).  kind 0: the cluster panel; kind 1: POTF2 + L21 (the fallback kernels).
 double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
-                             int iters) {
+                             int iters, int dbg) {
     Work w{};
     w.dtype = dtype; w.n = n; w.ldw = ldw; w.W = W;
     cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, 0);
@@ -426,7 +426,9 @@ double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t 
     const size_t es = dtype == AS_F64 ? 8 : 4;
     double tot = 0.0;
     for (int it = 0; it < iters; ++it) {
-        cudaMemcpy(W, Wsrc, es * ldw * n, cudaMemcpyDeviceToDevice);
+        // dbg 4: restore only the panel's columns (no L2 flush between launches)
+        if (dbg & 4) cudaMemcpy((char*)W + es * ldw * k0, (const char*)Wsrc + es * ldw * k0, es * ldw * nbp, cudaMemcpyDeviceToDevice);
+        else cudaMemcpy(W, Wsrc, es * ldw * n, cudaMemcpyDeviceToDevice);
         cudaMemset(w.st, 0, sizeof(DevState));
         cudaEventRecord(e0, 0);
         auto run = [&](auto tag) {
@@ -438,7 +440,7 @@ double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t 
             cudaFuncSetAttribute(l21_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
             potf2_kernel<T><<<1, 256, sm1, 0>>>((T*)W, ldw, n, k0, nbp, w.st, (T*)w.Dinv0);
             const int64_t rest = n - k0 - nbp;
-            if (rest > 0) l21_kernel<T><<<(unsigned)((rest + kNB - 1) / kNB), 256, sm2, 0>>>((T*)W, ldw, n, k0, nbp, w.st, (T*)w.Dinv0);
+            if (rest > 0 && !(dbg & 2)) l21_kernel<T><<<(unsigned)((rest + kNB - 1) / kNB), 256, sm2, 0>>>((T*)W, ldw, n, k0, nbp, w.st, (T*)w.Dinv0);
         };
         if (dtype == AS_F64) run(double{});
         else run(float{});

@@ -8,7 +8,7 @@ void launch_copy_norm(const Work& w, bool with_perm, cudaStream_t s); // W = A, 
 double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
                            int iters, int dbg);
 double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
-                             int iters);
+                             int iters, int dbg);
 unsigned long long* debug_trace_buf(int which);   // lu.cu diagnostics (AS_LU_TRACE)
 int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap);  // lu.cu diagnostics
 void launch_lu_factor(const Work& w, cudaStream_t s);                 // lu.cu: W = L\U, ipiv, perm, Dinv0/1, anorm
