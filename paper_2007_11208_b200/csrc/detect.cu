@@ -498,7 +498,9 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
         bool lower_nz = false, upper_nz = false;
         // ---- band / triangular verdicts in each tile's own layout (only triangular candidates
         // left and an off-diagonal pair: distances are irrelevant, a non-zero anywhere decides)
-        if (D != 0 && !(alive & (AS_FLAG_BANDED | AS_FLAG_SPD_CANDIDATE))) {
+        // (nothing but the sympd candidate left: no band / triangular work at all)
+        if (!(alive & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_UPPER))) {
+        } else if (D != 0 && !(alive & AS_FLAG_BANDED)) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) { lower_nz |= lo[i] != T(0); upper_nz |= up[i] != T(0); }
         } else
@@ -528,6 +530,19 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
                     up_s[c * kLD3 + r] = (D != 0) ? up[i] : lo[i];
                 }
                 __syncthreads();
+                if (interior && D > 0 && spd_peek) {
+                    // strictly below the diagonal and inside the matrix: no index checks;
+                    // lines 13-14: delta > tol and delta > tol max(|a|, |b|), the max split into
+                    // two compares (tol > 0: tol max(x, y) = max(tol x, tol y) exactly)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                        const T a = lo[i], b = up_s[r * kLD3 + c];
+                        const T aa = fabs(a), ab = fabs(b), delta = fabs(a - b);
+                        spd_dead |= ((delta > tol) & (delta > tol * aa) & (delta > tol * ab)) | (aa >= max_diag) |
+                                    (aa + ab >= drow[i & 1] + dcol[i >> 1]);
+                    }
+                } else
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
