@@ -111,6 +111,41 @@ def test_detect_fig1_and_edges():
     assert st["flags"] == d.flags and (st["kl"], st["ku"]) == (d.kl, d.ku)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", ["asym", "asym_small_rel", "asym_tiny_abs", "maxdiag", "diag_sum", "none"])
+def test_detect_fig4_interior_pair(case, dtype):
+    # Fig. 4 lines 12-16 decided on one element pair inside an interior below-diagonal tile pair
+    # (rows 192..255, cols 64..127 of n = 300): the kernel's index-check-free path must agree
+    # with the oracle on each condition, including the two halves of lines 13-14.
+    n, i, j = 300, 200, 70
+    A = np.diag(np.full(n, 10.0))
+    a = b = 0.5
+    if case == "asym":
+        b = 0.5 * (1 + 1e-3)                           # delta > tol and > tol m: dies
+    elif case == "asym_small_rel":
+        a = 1e3                                        # one ulp apart: delta > tol, < tol m: alive
+        b = float(np.nextafter(dtype(a), dtype(np.inf)))
+        A[i, i] = A[j, j] = 1e4
+    elif case == "asym_tiny_abs":
+        a, b = 1e-20, 2e-20                            # delta < tol: alive
+    elif case == "maxdiag":
+        a = b = 10.0                                   # |a| >= max diag: dies
+    elif case == "diag_sum":
+        A[i, i] = A[j, j] = 1.0
+        a = b = 1.0                                    # |a| + |b| >= d_i + d_j: dies
+    A[i, j], A[j, i] = a, b
+    A = np.asfortranarray(A.astype(dtype))
+    d = oracle.detect(A)
+    for fullscan in (False, True):
+        ret, st = AS.as_detect(AS.to_device(A), fullscan=fullscan)
+        assert ret == 0
+        assert st["flags"] == d.flags, (case, st, d)
+    if case in ("none", "asym_tiny_abs", "asym_small_rel"):
+        assert d.flags & oracle.SPD
+    else:
+        assert not d.flags & oracle.SPD
+
+
 @pytest.mark.parametrize("tag", ["C1", "C2", "C3a", "C3b", "C4"])
 def test_detect_configs_full_size(tag):
     A, _ = W.make(tag)
