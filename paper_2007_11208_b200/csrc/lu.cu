@@ -1074,6 +1074,192 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
     }
 }
 
+// ------------------------------------------------------------------ small n: one-cluster LU
+// xGETRF for n <= kSmN (C1) in ONE launch: a cluster of P = ceil(n/64) CTAs, CTA c owns the
+// column block [64c, 64c+64) with thread r holding row r of it in registers for the whole
+// factorization.  Per panel b (the paper's blocked GETRF order):
+//   owner CTA b   its block to shared memory, then column by column (xGETF2): first-max |.|
+//                 pivot search (warp shuffles + one CTA barrier), the row interchange (one
+//                 element per thread, second barrier), multipliers, rank-1 update with the
+//                 pivot row as a broadcast read; the block stays in shared memory (L_b is read
+//                 by the later CTAs over DSMEM, the write-out reads it at the end);
+//   cluster barrier
+//   CTAs c > b    apply panel b's 64 interchanges to their rows (one permutation through shared
+//                 memory), copy their own row of L_b from the owner, then the 64 rank-1 steps
+//                 (= U12 = L11^{-1} A12 and A22 -= L21 U12, one CTA barrier per step).
+// At the end every CTA applies the interchanges of later panels while writing its rows to W
+// (LAPACK's convention: all interchanges applied to all columns), CTA 0 writes the row
+// permutation.  No grid-wide exchange, no intermediate launches: C1's factorization was ~0.7 ms
+// of panel launches with one cross-CTA exchange per column.
+constexpr int kSmN = 256;        // rows = threads
+constexpr int kSmC = 64;         // columns per CTA
+template <typename T>
+__global__ void __launch_bounds__(kSmN, 1) lu_small_kernel(T* W, int64_t ldw, int n, int64_t* ipiv, int64_t* perm,
+                                                           DevState* st) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Lb = (T*)smem_raw;                           // [kSmC][kSmN]: L_b copy (update) / own block (owner)
+    T* ub = Lb + kSmC * kSmN;                       // [2][kSmC] pivot row
+    T* xb = ub + 2 * kSmC;                          // [2][kSmC] displaced row
+    __shared__ T s_v[2][kSmN / 32];
+    __shared__ int s_i[2][kSmN / 32];
+    __shared__ int s_piv[kSmC];                     // this CTA's pivots (read by later CTAs)
+    __shared__ int s_pb[kSmC];                      // pivots of the panel being applied
+    __shared__ int s_all[kSmN];                     // all pivots (write-out)
+    const int c = (int)cl.block_rank(), P = (int)cl.num_blocks();
+    const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+    const int cb = kSmC * c, nc = min(kSmC, n - cb);
+    const bool row_ok = r < n;
+    T a[kSmC];
+#pragma unroll
+    for (int k = 0; k < kSmC; ++k) a[k] = (row_ok && k < nc) ? W[r + (int64_t)(cb + k) * ldw] : T(0);
+    unsigned long long info = ~0ull;
+
+    for (int b = 0; b < P; ++b) {
+        if (b == c) {
+            // ---- xGETF2 on the own block, in shared memory (thread r = row r; the pivot row is a
+            // broadcast read, the interchange one element per thread)
+#pragma unroll
+            for (int k = 0; k < kSmC; ++k) Lb[r + k * kSmN] = a[k];
+            __syncthreads();
+            for (int j = 0; j < nc; ++j) {
+                const int g = cb + j, par = j & 1;
+                T v = T(-1);
+                int ri = 0x7fffffff;
+                if (r >= g && row_ok) {
+                    const T aj = Lb[r + j * kSmN];
+                    const T x = aj < T(0) ? -aj : aj;
+                    if (x == x) { v = x; ri = r; }           // NaN never wins (Z15: first max)
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const T v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int r2 = __shfl_xor_sync(0xffffffffu, ri, o);
+                    if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; }
+                }
+                if (lane == 0) { s_v[par][warp] = v; s_i[par][warp] = ri; }
+                __syncthreads();
+                v = s_v[par][0]; ri = s_i[par][0];
+#pragma unroll
+                for (int w2 = 1; w2 < kSmN / 32; ++w2) {
+                    const T v2 = s_v[par][w2];
+                    const int r2 = s_i[par][w2];
+                    if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; }
+                }
+                const int p = (ri == 0x7fffffff) ? g : ri;
+                if (p != g && r < kSmC) {
+                    const T t = Lb[g + r * kSmN];
+                    Lb[g + r * kSmN] = Lb[p + r * kSmN];
+                    Lb[p + r * kSmN] = t;
+                }
+                if (r == 0) { s_piv[j] = p; ipiv[g] = p; }
+                __syncthreads();
+                const T piv = Lb[g + j * kSmN];
+                if (piv == T(0)) {
+                    if (info == ~0ull) info = (unsigned long long)(g + 1);   // exact zero pivot: singular
+                } else if (r > g && row_ok) {
+                    const T l = Lb[r + j * kSmN] / piv;
+                    Lb[r + j * kSmN] = l;
+                    for (int k = j + 1; k < nc; ++k) Lb[r + k * kSmN] -= l * Lb[g + k * kSmN];
+                }
+            }
+        }
+        cl.sync();                                   // panel b (pivots + L_b) visible to the cluster
+        if (c > b) {
+            // ---- panel b's interchanges as one permutation of this block's rows
+            const int* pr = cl.map_shared_rank(s_piv, b);
+            if (r < kSmC) s_pb[r] = pr[r];
+            __syncthreads();
+            const int g0 = kSmC * b;
+            int dest = r;
+            for (int k = 0; k < kSmC; ++k) {
+                const int g = g0 + k, p = s_pb[k];
+                if (dest == g) dest = p;
+                else if (dest == p) dest = g;
+            }
+#pragma unroll
+            for (int k = 0; k < kSmC; ++k) Lb[dest + k * kSmN] = a[k];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < kSmC; ++k) a[k] = Lb[r + k * kSmN];
+            __syncthreads();
+            // ---- my row of L_b (rows are in their final order now)
+            const T* Lr = cl.map_shared_rank(Lb, b);
+            if (r > g0 && row_ok)
+#pragma unroll 16
+                for (int k = 0; k < kSmC; ++k) Lb[r + k * kSmN] = Lr[r + k * kSmN];
+            // ---- 64 rank-1 steps: row g0 + k of this block is final after step k - 1
+            if (r == g0) {
+#pragma unroll
+                for (int k = 0; k < kSmC; ++k) ub[k] = a[k];
+            }
+            __syncthreads();
+            for (int k = 0; k < kSmC; ++k) {
+                const int g = g0 + k, par = k & 1;
+                const T* u = ub + par * kSmC;
+                if (r > g && row_ok) {
+                    const T l = Lb[r + k * kSmN];
+#pragma unroll
+                    for (int q = 0; q < kSmC; ++q) a[q] -= l * u[q];
+                    if (r == g + 1 && k + 1 < kSmC) {
+                        T* un = ub + (par ^ 1) * kSmC;
+#pragma unroll
+                        for (int q = 0; q < kSmC; ++q) un[q] = a[q];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    // ---- write-out with the later panels' interchanges applied, the row permutation
+    for (int q = r; q < n; q += kSmN) s_all[q] = (int)__ldcg(ipiv + q);
+    __syncthreads();
+    if (row_ok) {
+        int dest = r;
+        for (int g = kSmC * (c + 1); g < n; ++g) {
+            const int p = s_all[g];
+            if (dest == g) dest = p;
+            else if (dest == p) dest = g;
+        }
+        for (int k = 0; k < nc; ++k) W[dest + (int64_t)(cb + k) * ldw] = Lb[r + k * kSmN];
+        if (c == 0) {
+            int d2 = r;
+            for (int g = 0; g < n; ++g) {
+                const int p = s_all[g];
+                if (d2 == g) d2 = p;
+                else if (d2 == p) d2 = g;
+            }
+            perm[d2] = r;
+        }
+    }
+    if (r == 0 && info != ~0ull) atomicMin(&st->info, info);
+    cl.sync();                                       // no CTA exits while its shared memory may be read
+}
+
+template <typename T>
+static bool small_lu_launch(const Work& w, cudaStream_t s) {
+    const int n = (int)w.n;
+    const int P = (n + kSmC - 1) / kSmC;
+    const size_t smem = sizeof(T) * ((size_t)kSmC * kSmN + 4 * kSmC);
+    auto kern = lu_small_kernel<T>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(kSmN);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, w.ipiv, w.perm, w.st);
+    if (e == cudaSuccess) return true;
+    cudaGetLastError();
+    return false;
+}
+
 // ------------------------------------------------------------------ host driver
 struct LuStreams {
     cudaStream_t hi = nullptr;
@@ -1284,6 +1470,12 @@ template <typename T>
 static void lu_factor_t(const Work& w, cudaStream_t s) {
     const int64_t n = w.n;
     launch_copy_norm(w, true, s);
+    static const bool small_off = getenv("AS_LU_SMALL_OFF") != nullptr;
+    if (n <= kSmN && !small_off && small_lu_launch<T>(w, s)) {
+        linv_launch<T>(w, 0, (int)n, s);                        // Dinv0: unit-L diagonal block inverses
+        launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
+        return;
+    }
     cudaMemsetAsync(w.cand, 0, sizeof(PSlot) * 1024, s);       // panel exchange slots (sequence numbers)
     if (lu_trace().tmin) {
         cudaMemsetAsync(lu_trace().tmin, 0xFF, sizeof(unsigned long long) * 4 * kTraceBlocks, s);

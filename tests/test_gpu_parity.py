@@ -164,6 +164,41 @@ def test_lu_dense(n):
     check_parity(A, B)
 
 
+@pytest.mark.parametrize("n", [63, 128, 129, 191, 192, 255, 256])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_lu_small_cluster(n, fp32):
+    """n <= 256 takes the one-cluster LU (64 columns per CTA, rows in registers): every CTA-count
+    boundary and ragged last block, no diagonal shift (real pivoting), fp64 and fp32."""
+    A = W.random_dense(n, seed=100 + n)
+    B = np.asfortranarray(np.random.default_rng(n).standard_normal((n, 2)))
+    if fp32:
+        check_parity(A.astype(np.float32, order="F"), B.astype(np.float32, order="F"), fp32=True)
+    else:
+        rep, _ = check_parity(A, B)
+        assert rep["primary_method"] == oracle.M_LU
+
+
+@pytest.mark.parametrize("n,zcol", [(200, 70), (256, 255), (130, 0)])
+def test_lu_small_zero_pivot(n, zcol):
+    """An exactly zero column gives an exact zero pivot (singular): SINGULAR and the
+    SVD fallback bit-exact against the oracle; with NO_FALLBACK the singular error code."""
+    A = W.random_dense(n, seed=7 + n)
+    A[:, zcol] = 0.0
+    B = np.asfortranarray(np.random.default_rng(n).standard_normal((n, 1)))
+    rep, orep = check_parity(A, B)
+    assert rep["flags"] & oracle.F_SINGULAR
+    check_parity(A, B, no_fallback=True)
+
+
+def test_lu_small_ties():
+    """Entries in {-1, 0, 1}: many exactly tied pivot candidates (first-max rule, Z15)."""
+    n = 250
+    A = np.asfortranarray(np.random.default_rng(11).integers(-1, 2, (n, n)).astype(np.float64))
+    A[np.arange(n), np.arange(n)] += 0.5
+    B = np.asfortranarray(np.random.default_rng(12).standard_normal((n, 3)))
+    check_parity(A, B)
+
+
 @pytest.mark.parametrize("n,kl,ku", [(40, 1, 1), (300, 3, 2), (257, 8, 8), (500, 0, 5), (500, 6, 0), (1000, 20, 3), (300, 30, 25), (3000, 2, 2)])
 def test_banded(n, kl, ku):
     A = W.random_banded(n, kl, ku, seed=n + kl, dominant=(kl + ku) % 2 == 0)
