@@ -1073,103 +1073,67 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
         W[(k0 + row) + (cc0 + c) * ldw] = Bn[c * kSULD + row];
     }
 }
-
 // ------------------------------------------------------------------ small n: one-cluster LU
 // xGETRF for n <= kSmN (C1) in ONE launch: a cluster of P = ceil(n/64) CTAs, CTA c owns the
-// column block [64c, 64c+64) with thread r holding row r of it in registers for the whole
-// factorization.  Per panel b (the paper's blocked GETRF order):
-//   owner CTA b   its block to shared memory, then column by column (xGETF2): first-max |.|
-//                 pivot search (warp shuffles + one CTA barrier), the row interchange (one
-//                 element per thread, second barrier), multipliers, rank-1 update with the
-//                 pivot row as a broadcast read; the block stays in shared memory (L_b is read
-//                 by the later CTAs over DSMEM, the write-out reads it at the end);
+// column block [64c, 64c+64).  512 threads: thread (r, h) = row r, columns 32h .. 32h+31 of the
+// block.  Per panel b (the paper's blocked GETRF order):
+//   owner CTA b   its block in shared memory, factored 8 columns at a time (xGETF2 inside the
+//                 group: first-max |.| pivot search by warp shuffles + one CTA barrier, the row
+//                 interchange, multipliers and rank-1 steps on the group's columns held in
+//                 registers; then the group's U12 rows by a column-parallel unit-lower solve and
+//                 a rank-8 update of the rest of the block, pivot rows as broadcast reads); the
+//                 block stays in shared memory (L_b is read by the later CTAs over DSMEM);
 //   cluster barrier
-//   CTAs c > b    apply panel b's 64 interchanges to their rows (one permutation through shared
-//                 memory), copy their own row of L_b from the owner, then the 64 rank-1 steps
-//                 (= U12 = L11^{-1} A12 and A22 -= L21 U12, one CTA barrier per step).
+//   CTAs c > b    rows in registers: panel b's 64 interchanges as one permutation through shared
+//                 memory, their own row of L_b copied from the owner, then the 64 rank-1 steps
+//                 (= U12 = L11^{-1} A12 and A22 -= L21 U12, one CTA barrier per step, the next
+//                 pivot row published by its owner thread as soon as it is final).
 // At the end every CTA applies the interchanges of later panels while writing its rows to W
 // (LAPACK's convention: all interchanges applied to all columns), CTA 0 writes the row
 // permutation.  No grid-wide exchange, no intermediate launches: C1's factorization was ~0.7 ms
 // of panel launches with one cross-CTA exchange per column.
-constexpr int kSmN = 256;        // rows = threads
+constexpr int kSmN = 256;        // rows
+constexpr int kSmT = 512;        // threads: two per row
 constexpr int kSmC = 64;         // columns per CTA
+constexpr int kSmH = 32;         // columns per thread in the update phase
 template <typename T>
-__global__ void __launch_bounds__(kSmN, 1) lu_small_kernel(T* W, int64_t ldw, int n, int64_t* ipiv, int64_t* perm,
-                                                           DevState* st) {
+__global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, int n, int64_t* ipiv, int64_t* perm,
+                                                           DevState* st, int prof) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* Lb = (T*)smem_raw;                           // [kSmC][kSmN]: L_b copy (update) / own block (owner)
-    T* ub = Lb + kSmC * kSmN;                       // [2][kSmC] pivot row
-    T* xb = ub + 2 * kSmC;                          // [2][kSmC] displaced row
-    __shared__ T s_v[2][kSmN / 32];
-    __shared__ int s_i[2][kSmN / 32];
+    T* ub = Lb + kSmC * kSmN;                       // [2][kSmC] pivot row (update phase)
+    T* xb = ub + 2 * kSmC;                          // [2][8][8] candidate rows, [2][8] row g (group columns)
+    __shared__ T s_v[2][kSmT / 32];
+    __shared__ int s_i[2][kSmT / 32];
     __shared__ int s_piv[kSmC];                     // this CTA's pivots (read by later CTAs)
     __shared__ int s_pb[kSmC];                      // pivots of the panel being applied
     __shared__ int s_all[kSmN];                     // all pivots (write-out)
     const int c = (int)cl.block_rank(), P = (int)cl.num_blocks();
-    const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = tid & (kSmN - 1), h = tid >> 8, hc = kSmH * h;
     const int cb = kSmC * c, nc = min(kSmC, n - cb);
     const bool row_ok = r < n;
-    T a[kSmC];
+#define SMPROF(slot)                                                                   \
+    if (prof == 2 && tid == 0 && c == 1) {                                             \
+        unsigned long long t_;                                                         \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+        st->dbg_t[slot] = t_;                                                          \
+    }
+    T a[kSmH];
 #pragma unroll
-    for (int k = 0; k < kSmC; ++k) a[k] = (row_ok && k < nc) ? W[r + (int64_t)(cb + k) * ldw] : T(0);
+    for (int i = 0; i < kSmH; ++i) a[i] = (row_ok && hc + i < nc) ? W[r + (int64_t)(cb + hc + i) * ldw] : T(0);
     unsigned long long info = ~0ull;
 
-    for (int b = 0; b < P; ++b) {
-        if (b == c) {
-            // ---- xGETF2 on the own block, in shared memory (thread r = row r; the pivot row is a
-            // broadcast read, the interchange one element per thread)
-#pragma unroll
-            for (int k = 0; k < kSmC; ++k) Lb[r + k * kSmN] = a[k];
-            __syncthreads();
-            for (int j = 0; j < nc; ++j) {
-                const int g = cb + j, par = j & 1;
-                T v = T(-1);
-                int ri = 0x7fffffff;
-                if (r >= g && row_ok) {
-                    const T aj = Lb[r + j * kSmN];
-                    const T x = aj < T(0) ? -aj : aj;
-                    if (x == x) { v = x; ri = r; }           // NaN never wins (Z15: first max)
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const T v2 = __shfl_xor_sync(0xffffffffu, v, o);
-                    const int r2 = __shfl_xor_sync(0xffffffffu, ri, o);
-                    if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; }
-                }
-                if (lane == 0) { s_v[par][warp] = v; s_i[par][warp] = ri; }
-                __syncthreads();
-                v = s_v[par][0]; ri = s_i[par][0];
-#pragma unroll
-                for (int w2 = 1; w2 < kSmN / 32; ++w2) {
-                    const T v2 = s_v[par][w2];
-                    const int r2 = s_i[par][w2];
-                    if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; }
-                }
-                const int p = (ri == 0x7fffffff) ? g : ri;
-                if (p != g && r < kSmC) {
-                    const T t = Lb[g + r * kSmN];
-                    Lb[g + r * kSmN] = Lb[p + r * kSmN];
-                    Lb[p + r * kSmN] = t;
-                }
-                if (r == 0) { s_piv[j] = p; ipiv[g] = p; }
-                __syncthreads();
-                const T piv = Lb[g + j * kSmN];
-                if (piv == T(0)) {
-                    if (info == ~0ull) info = (unsigned long long)(g + 1);   // exact zero pivot: singular
-                } else if (r > g && row_ok) {
-                    const T l = Lb[r + j * kSmN] / piv;
-                    Lb[r + j * kSmN] = l;
-                    for (int k = j + 1; k < nc; ++k) Lb[r + k * kSmN] -= l * Lb[g + k * kSmN];
-                }
-            }
-        }
+    // (the three phases as separate loops: the row registers are dead after the owner phase)
+    for (int b = 0; b < c; ++b) {
         cl.sync();                                   // panel b (pivots + L_b) visible to the cluster
-        if (c > b) {
+        {
             // ---- panel b's interchanges as one permutation of this block's rows
+            SMPROF(0);
             const int* pr = cl.map_shared_rank(s_piv, b);
-            if (r < kSmC) s_pb[r] = pr[r];
+            if (tid < kSmC) s_pb[tid] = pr[tid];
             __syncthreads();
             const int g0 = kSmC * b;
             int dest = r;
@@ -1179,41 +1143,202 @@ __global__ void __launch_bounds__(kSmN, 1) lu_small_kernel(T* W, int64_t ldw, in
                 else if (dest == p) dest = g;
             }
 #pragma unroll
-            for (int k = 0; k < kSmC; ++k) Lb[dest + k * kSmN] = a[k];
+            for (int i = 0; i < kSmH; ++i) Lb[dest + (hc + i) * kSmN] = a[i];
             __syncthreads();
 #pragma unroll
-            for (int k = 0; k < kSmC; ++k) a[k] = Lb[r + k * kSmN];
+            for (int i = 0; i < kSmH; ++i) a[i] = Lb[r + (hc + i) * kSmN];
             __syncthreads();
-            // ---- my row of L_b (rows are in their final order now)
+            SMPROF(1);
+            // ---- rows of L_b (final order now): thread (r, h) copies columns hc .. hc+31
             const T* Lr = cl.map_shared_rank(Lb, b);
-            if (r > g0 && row_ok)
-#pragma unroll 16
-                for (int k = 0; k < kSmC; ++k) Lb[r + k * kSmN] = Lr[r + k * kSmN];
+            if (r > g0 && row_ok) {
+                // all remote loads of a batch before its stores (Lb and Lr may alias as far as the
+                // compiler knows: element-wise copies serialise one DSMEM round trip per element)
+#pragma unroll
+                for (int i0 = 0; i0 < kSmH; i0 += 16) {
+                    T tmp[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) tmp[i] = Lr[r + (hc + i0 + i) * kSmN];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) Lb[r + (hc + i0 + i) * kSmN] = tmp[i];
+                }
+            }
             // ---- 64 rank-1 steps: row g0 + k of this block is final after step k - 1
             if (r == g0) {
 #pragma unroll
-                for (int k = 0; k < kSmC; ++k) ub[k] = a[k];
+                for (int i = 0; i < kSmH; ++i) ub[hc + i] = a[i];
             }
             __syncthreads();
+            SMPROF(2);
             for (int k = 0; k < kSmC; ++k) {
                 const int g = g0 + k, par = k & 1;
-                const T* u = ub + par * kSmC;
+                const T* u = ub + par * kSmC + hc;
                 if (r > g && row_ok) {
                     const T l = Lb[r + k * kSmN];
 #pragma unroll
-                    for (int q = 0; q < kSmC; ++q) a[q] -= l * u[q];
+                    for (int i = 0; i < kSmH; ++i) a[i] -= l * u[i];
                     if (r == g + 1 && k + 1 < kSmC) {
-                        T* un = ub + (par ^ 1) * kSmC;
+                        T* un = ub + (par ^ 1) * kSmC + hc;
 #pragma unroll
-                        for (int q = 0; q < kSmC; ++q) un[q] = a[q];
+                        for (int i = 0; i < kSmH; ++i) un[i] = a[i];
                     }
                 }
                 __syncthreads();
             }
         }
+        if (prof == 1 && tid == 0 && c < 4 && b < 4) {   // diagnostics: %globaltimer at the end of step b
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            st->dbg_t[4 * c + b] = t;
+        }
+    }
+    {
+        const int b = c;
+        {
+#pragma unroll
+            for (int i = 0; i < kSmH; ++i) Lb[r + (hc + i) * kSmN] = a[i];
+            __syncthreads();
+            SMPROF(3);
+            for (int j0 = 0; j0 < nc; j0 += 8) {
+                if (j0 == 8) SMPROF(4);
+                T q[8];
+                if (h == 0) {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) q[t] = (j0 + t < nc) ? Lb[r + (j0 + t) * kSmN] : T(0);
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int j = j0 + t;
+                    if (j >= nc) break;
+                    const int g = cb + j, par = j & 1;
+                    T v = T(-1);
+                    int ri = 0x7fffffff;
+                    if (h == 0 && r >= g && row_ok) {
+                        const T x = q[t] < T(0) ? -q[t] : q[t];
+                        if (x == x) { v = x; ri = r; }       // NaN never wins (Z15: first max)
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const T v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                        const int r2 = __shfl_xor_sync(0xffffffffu, ri, o);
+                        if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; }
+                    }
+                    // one barrier per column: the warp winner publishes its group row with its
+                    // candidate, row g publishes itself (the displaced row when p != g)
+                    T* CR = xb + par * 64;                      // [8 warps][8]: candidate rows
+                    T* Yr = xb + 128 + par * 8;                 // row g, group columns
+                    if (h == 0 && ri == r) {
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2) CR[warp * 8 + s2] = q[s2];
+                    }
+                    if (h == 0 && r == g) {
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2) Yr[s2] = q[s2];
+                    }
+                    if (lane == 0) { s_v[par][warp] = v; s_i[par][warp] = ri; }
+                    __syncthreads();
+                    v = s_v[par][0]; ri = s_i[par][0];
+                    int wb = 0;
+#pragma unroll
+                    for (int w2 = 1; w2 < kSmN / 32; ++w2) {   // (warps of h = 1 hold no candidates)
+                        const T v2 = s_v[par][w2];
+                        const int r2 = s_i[par][w2];
+                        if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; wb = w2; }
+                    }
+                    const int p = (ri == 0x7fffffff) ? g : ri;
+                    const T* X = (ri == 0x7fffffff) ? Yr : CR + wb * 8;   // pivot row, group columns
+                    if (p != g && tid < kSmC && (tid < j0 || tid >= j0 + 8)) {   // the other columns, in shared memory
+                        const T tt = Lb[g + tid * kSmN];
+                        Lb[g + tid * kSmN] = Lb[p + tid * kSmN];
+                        Lb[p + tid * kSmN] = tt;
+                    }
+                    if (tid == 0) { s_piv[j] = p; ipiv[g] = p; }
+                    if (h == 0) {
+                        if (p != g) {
+                            if (r == g) {
+#pragma unroll
+                                for (int s2 = 0; s2 < 8; ++s2) q[s2] = X[s2];
+                            } else if (r == p) {
+#pragma unroll
+                                for (int s2 = 0; s2 < 8; ++s2) q[s2] = Yr[s2];
+                            }
+                        }
+                        const T pv = X[t];
+                        if (pv == T(0)) {
+                            if (info == ~0ull) info = (unsigned long long)(g + 1);   // exact zero pivot: singular
+                        } else if (r > g && row_ok) {
+                            const T l = q[t] / pv;
+                            q[t] = l;
+#pragma unroll
+                            for (int s2 = t + 1; s2 < 8; ++s2) q[s2] -= l * X[s2];
+                        }
+                    }
+                }
+                if (h == 0) {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        if (j0 + t < nc) Lb[r + (j0 + t) * kSmN] = q[t];
+                }
+                if (j0 == 8) SMPROF(5);
+                const int j1 = min(j0 + 8, nc);
+                if (j1 >= nc) break;
+                __syncthreads();
+                if (j0 == 8) SMPROF(6);
+                // U12 rows g0 .. g0+7 of columns j1..nc-1: unit-lower solve, one thread per column
+                const int g0 = cb + j0;
+                if (tid >= j1 && tid < nc) {
+                    T u[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        T x = Lb[(g0 + t) + tid * kSmN];
+#pragma unroll
+                        for (int s2 = 0; s2 < t; ++s2) x -= Lb[(g0 + t) + (j0 + s2) * kSmN] * u[s2];
+                        u[t] = x;
+                        Lb[(g0 + t) + tid * kSmN] = x;
+                    }
+                }
+                __syncthreads();
+                if (j0 == 8) SMPROF(7);
+                // rank-8 update of the rows below the group; thread (r, h) takes 4-column chunks
+                // j1 + 4h, j1 + 4h + 8, ... (four independent accumulations per chunk)
+                if (r >= g0 + 8 && row_ok) {
+                    T lq[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) lq[t] = Lb[r + (j0 + t) * kSmN];
+                    for (int k = j1 + 4 * h; k < nc; k += 8) {
+                        T x[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) x[i] = Lb[r + (k + i) * kSmN];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) x[i] -= lq[t] * Lb[(g0 + t) + (k + i) * kSmN];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (k + i < nc) Lb[r + (k + i) * kSmN] = x[i];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        SMPROF(8);
+        cl.sync();                                   // panel c visible to the cluster
+        if (prof == 1 && tid == 0 && c < 4 && b < 4) {   // diagnostics: %globaltimer at the end of step b
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            st->dbg_t[4 * c + b] = t;
+        }
+    }
+    for (int b = c + 1; b < P; ++b) {
+        cl.sync();
+        if (prof == 1 && tid == 0 && c < 4 && b < 4) {   // diagnostics: %globaltimer at the end of step b
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            st->dbg_t[4 * c + b] = t;
+        }
     }
     // ---- write-out with the later panels' interchanges applied, the row permutation
-    for (int q = r; q < n; q += kSmN) s_all[q] = (int)__ldcg(ipiv + q);
+    for (int q = tid; q < n; q += kSmT) s_all[q] = (int)__ldcg(ipiv + q);
     __syncthreads();
     if (row_ok) {
         int dest = r;
@@ -1222,8 +1347,9 @@ __global__ void __launch_bounds__(kSmN, 1) lu_small_kernel(T* W, int64_t ldw, in
             if (dest == g) dest = p;
             else if (dest == p) dest = g;
         }
-        for (int k = 0; k < nc; ++k) W[dest + (int64_t)(cb + k) * ldw] = Lb[r + k * kSmN];
-        if (c == 0) {
+        for (int i = 0; i < kSmH; ++i)
+            if (hc + i < nc) W[dest + (int64_t)(cb + hc + i) * ldw] = Lb[r + (hc + i) * kSmN];
+        if (c == 0 && h == 0) {
             int d2 = r;
             for (int g = 0; g < n; ++g) {
                 const int p = s_all[g];
@@ -1233,20 +1359,21 @@ __global__ void __launch_bounds__(kSmN, 1) lu_small_kernel(T* W, int64_t ldw, in
             perm[d2] = r;
         }
     }
-    if (r == 0 && info != ~0ull) atomicMin(&st->info, info);
+    if (tid == 0 && info != ~0ull) atomicMin(&st->info, info);
     cl.sync();                                       // no CTA exits while its shared memory may be read
+#undef SMPROF
 }
 
 template <typename T>
 static bool small_lu_launch(const Work& w, cudaStream_t s) {
     const int n = (int)w.n;
     const int P = (n + kSmC - 1) / kSmC;
-    const size_t smem = sizeof(T) * ((size_t)kSmC * kSmN + 4 * kSmC);
+    const size_t smem = sizeof(T) * ((size_t)kSmC * kSmN + 5 * kSmC);
     auto kern = lu_small_kernel<T>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P);
-    cfg.blockDim = dim3(kSmN);
+    cfg.blockDim = dim3(kSmT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -1254,7 +1381,8 @@ static bool small_lu_launch(const Work& w, cudaStream_t s) {
     at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, w.ipiv, w.perm, w.st);
+    static const int prof = getenv("AS_LU_SMALL_PROF") ? atoi(getenv("AS_LU_SMALL_PROF")) : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, w.ipiv, w.perm, w.st, prof);
     if (e == cudaSuccess) return true;
     cudaGetLastError();
     return false;
