@@ -162,11 +162,20 @@ int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void
 int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detect_flags, as_structure* out,
               void* stream);
 
-/* as_debug_factor: test-only.  Runs the primary factorization `method`
- * (AS_METHOD_LU / AS_METHOD_CHOL / AS_METHOD_BAND) on device A and copies the
- * factors into caller DEVICE buffers: W (n*n, ld n; for BAND: ldab*n with
- * ldab = 2kl+ku+1) and ipiv (int64, n; LU/BAND).  kl/ku are used for BAND.
- * Returns info (1 + first zero pivot / failed column) or a negative error. */
+/* as_debug_factor: test-only (T3 reconstruction tests; never used by the
+ * solve or the bench).  Runs the primary factorization `method` alone, with
+ * the launchers the solve uses (AS_METHOD_LU: xGETRF, P:505-515;
+ * AS_METHOD_CHOL: xPOTRF), on device A (read-only, ld lda) and
+ * copies the factors into caller DEVICE buffers: W (n*n, ld n; LU: L\U with
+ * unit-diagonal L, every interchange applied to every column; CHOL: L in the
+ * lower triangle, the strict upper triangle unspecified) and, for LU, ipiv
+ * (int64, n, 0-based: row j was interchanged with row ipiv[j], in order
+ * j = 0..n-1).  kl/ku are unused.  Enqueued on `stream`, which it
+ * synchronises once.  Returns 0, info > 0 (LU: 1 + first exact zero pivot;
+ * CHOL: 1 + first column with a non-positive or NaN pivot), or a negative
+ * error: -1 dt, -3 A, -4 lda, -5 n <= 0, -8 W, -9 ipiv (not device pointers),
+ * -AS_ERR_NOT_IMPLEMENTED for AS_METHOD_BAND (the band factors are checked
+ * through the solve parity tests). */
 int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
                         void* W, int64_t* ipiv, void* stream);
 

@@ -202,6 +202,22 @@ def as_detect(A, fullscan=False, stream=None):
     return ret, {k: getattr(st, k) for k, _ in st._fields_}
 
 
+_lib.as_debug_factor.argtypes = [I32, I32, P, I64, I64, I64, I64, P, P, P]
+_lib.as_debug_factor.restype = I64
+
+
+def as_debug_factor(A, method: int, stream=None):
+    """Test-only: the primary factorization alone (LU: W = L\\U and 0-based ipiv; Cholesky: L in the
+    lower triangle).  Returns (info, W, ipiv) with W column-major n x n on A's device."""
+    import torch
+    n = A.shape[0]
+    Wt = empty_colmajor(n, n, A.dtype, device=A.device)
+    ipiv = torch.empty(n, dtype=torch.int64, device=A.device)
+    info = _lib.as_debug_factor(_dt(A), method, A.data_ptr(), _ld(A), n, 0, 0, Wt.data_ptr(), ipiv.data_ptr(),
+                                _stream_ptr(stream))
+    return int(info), Wt, ipiv
+
+
 _lib.as_set_instrumentation.argtypes = [C.c_int]
 _lib.as_last_stage_ms.argtypes = [P]
 _lib.as_last_stage_ms.restype = C.c_int

@@ -800,10 +800,46 @@ int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detec
     return 0;
 }
 
+// Test-only: the primary factorization alone (the same launchers the solve uses), eagerly on a
+// private workspace, factors copied out for the PA = LU / L L^T = A reconstruction tests.
 int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
                         void* W, int64_t* ipiv, void* stream) {
-    (void)kl; (void)ku; (void)W; (void)ipiv; (void)A; (void)lda; (void)n; (void)method; (void)dt; (void)stream;
-    return -AS_ERR_NOT_IMPLEMENTED;
+    (void)kl; (void)ku;
+    if (dt != AS_F64 && dt != AS_F32) return -1;
+    if (method != AS_METHOD_LU && method != AS_METHOD_CHOL) return -(int64_t)AS_ERR_NOT_IMPLEMENTED;
+    if (n <= 0) return -5;
+    if (lda < n) return -4;
+    if (!A || !is_device_ptr(A)) return -3;
+    if (!W || !is_device_ptr(W)) return -8;
+    if (method == AS_METHOD_LU && (!ipiv || !is_device_ptr(ipiv))) return -9;
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return AS_ERR_NO_DEVICE; }
+    Work w{};
+    w.dtype = dt; w.n = n; w.nrhs = 1; w.lda = lda; w.ldb = n;
+    cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t bytes = layout(w, 0, nullptr);
+    void* ws = nullptr;
+    int err = check(cudaMalloc(&ws, bytes), "cudaMalloc(debug workspace)");
+    if (err) return err;
+    layout(w, 0, (char*)ws);
+    cudaMemsetAsync(ws, 0, bytes, s);
+    DevArgs a{};
+    a.A = A;
+    set_args_kernel2<<<1, 1, 0, s>>>(a, w.args);
+    launch_state_init(w, s, 0u, 0, 0.0, 0.0, 30);
+    if (method == AS_METHOD_LU) launch_lu_factor(w, s);
+    else launch_chol_factor(w, s);
+    const size_t es = dt == AS_F64 ? 8 : 4;
+    cudaMemcpy2DAsync(W, es * n, w.W, es * w.ldw, es * n, n, cudaMemcpyDeviceToDevice, s);
+    if (method == AS_METHOD_LU) cudaMemcpyAsync(ipiv, w.ipiv, 8 * n, cudaMemcpyDeviceToDevice, s);
+    DevState h;
+    cudaMemcpyAsync(&h, w.st, sizeof(DevState), cudaMemcpyDeviceToHost, s);
+    err = check(cudaStreamSynchronize(s), "debug factor");
+    cudaFree(ws);
+    if (err) return err;
+    if (method == AS_METHOD_LU) return h.info == ~0ull ? 0 : (int64_t)h.info;
+    return h.chol_failed ? h.chol_fail_col + 1 : 0;
 }
 
 int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs) {

@@ -399,3 +399,69 @@ def test_config_c5_full_size(tag):
     assert eta <= (1e-13 if tag == "C5" else 1e-5), eta
     if tag == "C5":
         assert not rep["flags"] & oracle.F_FALLBACK and rep["rcond"] > 1e-10
+
+
+# ------------------------------------------------------------------ T3: factor reconstruction (as_debug_factor)
+def _perm_from_ipiv(ipiv):
+    perm = np.arange(len(ipiv))
+    for j, p in enumerate(ipiv):
+        perm[[j, p]] = perm[[p, j]]
+    return perm
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 200, 256, 257, 700])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_debug_factor_lu_reconstruction(n, fp32):
+    """P A = L U from the GPU factors (xGETRF): both LU paths (one-cluster n <= 256, blocked
+    above), |L| <= 1 (partial pivoting), first pivot equal to the oracle's (exact first-max rule, Z15),
+    and the oracle's factors reconstruct to the same bound."""
+    A = W.random_dense(n, seed=300 + n)
+    if fp32:
+        A = A.astype(np.float32, order="F")
+    eps = np.finfo(A.dtype).eps
+    info, Wd, ipiv = AS.as_debug_factor(AS.to_device(A), oracle.M_LU)
+    torch.cuda.synchronize()
+    assert info == 0
+    F = AS.to_host(Wd).astype(np.float64)
+    piv = ipiv.cpu().numpy()
+    assert np.all((piv >= np.arange(n)) & (piv < n))
+    L = np.tril(F, -1) + np.eye(n)
+    U = np.triu(F)
+    A64 = A.astype(np.float64)
+    R = A64[_perm_from_ipiv(piv)] - L @ U
+    bound = 4 * n * eps * np.abs(A64).max() * max(1.0, np.abs(U).max() / np.abs(A64).max())
+    assert np.abs(R).max() <= 10 * bound, (np.abs(R).max(), bound)
+    assert np.abs(L).max() <= 1.0
+    Wo, ipo, oinfo = oracle.getrf(A)
+    assert oinfo == 0 and piv[0] == ipo[0]
+    assert (piv == ipo).mean() >= 0.95
+
+
+def test_debug_factor_lu_zero_column():
+    """An exactly zero column j: info = j + 1 (first zero pivot), as the oracle's getrf."""
+    n = 150
+    A = W.random_dense(n, seed=9)
+    A[:, 40] = 0.0
+    info, _, _ = AS.as_debug_factor(AS.to_device(A), oracle.M_LU)
+    _, _, oinfo = oracle.getrf(A)
+    assert info == oinfo == 41
+
+
+@pytest.mark.parametrize("n", [3, 64, 300, 1000])
+def test_debug_factor_cholesky_reconstruction(n):
+    """L L^T = A from the GPU Cholesky factor (xPOTRF) and the non-positive-pivot column of an
+    indefinite matrix equal to the oracle's."""
+    A = W.random_spd_fig3(n, seed=n)
+    info, Wd, _ = AS.as_debug_factor(AS.to_device(A), oracle.M_CHOL)
+    torch.cuda.synchronize()
+    assert info == 0
+    L = np.tril(AS.to_host(Wd))
+    eps = np.finfo(np.float64).eps
+    assert np.abs(L @ L.T - A).max() <= 8 * n * eps * np.abs(A).max()
+    Lo, oinfo = oracle.potrf(A)
+    assert oinfo == 0 and np.abs(L - Lo).max() <= 1e3 * n * eps * np.abs(Lo).max()
+    B = A.copy(order="F")
+    B[n // 2, n // 2] = -1.0
+    info, _, _ = AS.as_debug_factor(AS.to_device(B), oracle.M_CHOL)
+    _, oinfo = oracle.potrf(B)
+    assert info == oinfo and info > 0
