@@ -1082,10 +1082,11 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
 //                 interchange, multipliers and rank-1 steps on the group's columns held in
 //                 registers; then the group's U12 rows by a column-parallel unit-lower solve and
 //                 a rank-8 update of the rest of the block, pivot rows as broadcast reads); the
-//                 block stays in shared memory (L_b is read by the later CTAs over DSMEM);
+//                 block stays in shared memory and goes to W for the later CTAs;
 //   cluster barrier
 //   CTAs c > b    rows in registers: panel b's 64 interchanges as one permutation through shared
-//                 memory, their own row of L_b copied from the owner, then the 64 rank-1 steps
+//                 memory, their own row of L_b read from W (the owner writes its block there
+//                 before the cluster barrier; pivots come over DSMEM), then the 64 rank-1 steps
 //                 (= U12 = L11^{-1} A12 and A22 -= L21 U12, one CTA barrier per step, the next
 //                 pivot row published by its owner thread as soon as it is final).
 // At the end every CTA applies the interchanges of later panels while writing its rows to W
@@ -1150,15 +1151,14 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
             __syncthreads();
             SMPROF(1);
             // ---- rows of L_b (final order now): thread (r, h) copies columns hc .. hc+31
-            const T* Lr = cl.map_shared_rank(Lb, b);
+            const T* Lr = W + (int64_t)kSmC * b * ldw;        // owner b's block, written before its barrier
             if (r > g0 && row_ok) {
-                // all remote loads of a batch before its stores (Lb and Lr may alias as far as the
-                // compiler knows: element-wise copies serialise one DSMEM round trip per element)
+                // all loads of a batch before its stores
 #pragma unroll
                 for (int i0 = 0; i0 < kSmH; i0 += 16) {
                     T tmp[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) tmp[i] = Lr[r + (hc + i0 + i) * kSmN];
+                    for (int i = 0; i < 16; ++i) tmp[i] = __ldcg(Lr + r + (int64_t)(hc + i0 + i) * ldw);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) Lb[r + (hc + i0 + i) * kSmN] = tmp[i];
                 }
@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
                         Lb[g + tid * kSmN] = Lb[p + tid * kSmN];
                         Lb[p + tid * kSmN] = tt;
                     }
-                    if (tid == 0) { s_piv[j] = p; ipiv[g] = p; }
+                    if (tid == 0) s_piv[j] = p;                 // (ipiv is written after the block)
                     if (h == 0) {
                         if (p != g) {
                             if (r == g) {
@@ -1322,6 +1322,13 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
             }
         }
         SMPROF(8);
+        // the factored block to W for the later CTAs (read through L2: DSMEM reads of one owner by
+        // all later CTAs share the owner's shared-memory port, ~20 B/clk, measured 9.6 us per panel)
+        __syncthreads();
+        if (tid < nc) ipiv[cb + tid] = s_piv[tid];
+        if (c + 1 < P && row_ok)
+            for (int i = 0; i < kSmH; ++i)
+                if (hc + i < nc) W[r + (int64_t)(cb + hc + i) * ldw] = Lb[r + (hc + i) * kSmN];
         cl.sync();                                   // panel c visible to the cluster
         if (prof == 1 && tid == 0 && c < 4 && b < 4) {   // diagnostics: %globaltimer at the end of step b
             unsigned long long t;
