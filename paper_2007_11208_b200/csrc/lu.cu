@@ -1086,13 +1086,23 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
 //   cluster barrier
 //   CTAs c > b    rows in registers: panel b's 64 interchanges as one permutation through shared
 //                 memory, their own row of L_b read from W (the owner writes its block there
-//                 before the cluster barrier; pivots come over DSMEM), then the 64 rank-1 steps
-//                 (= U12 = L11^{-1} A12 and A22 -= L21 U12, one CTA barrier per step, the next
-//                 pivot row published by its owner thread as soon as it is final).
+//                 before the cluster barrier; pivots come over DSMEM), then 8 groups of 8 rows:
+//                 U12 rows by a column-parallel unit-lower solve, rank-8 update of the rows below
+//                 (U12 = L11^{-1} A12, A22 -= L21 U12; two CTA barriers per group).
 // At the end every CTA applies the interchanges of later panels while writing its rows to W
 // (LAPACK's convention: all interchanges applied to all columns), CTA 0 writes the row
 // permutation.  No grid-wide exchange, no intermediate launches: C1's factorization was ~0.7 ms
 // of panel launches with one cross-CTA exchange per column.
+template <typename T> AS_DEV void cand_key(T x, unsigned& hi, unsigned& lo);
+template <> AS_DEV void cand_key<double>(double x, unsigned& hi, unsigned& lo) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);   // x >= +0: bits are monotone
+    hi = (unsigned)(b >> 32) + 1u;
+    lo = (unsigned)b;
+}
+template <> AS_DEV void cand_key<float>(float x, unsigned& hi, unsigned& lo) {
+    hi = __float_as_uint(x) + 1u;
+    lo = 0u;
+}
 constexpr int kSmN = 256;        // rows
 constexpr int kSmT = 512;        // threads: two per row
 constexpr int kSmC = 64;         // columns per CTA
@@ -1105,9 +1115,9 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* Lb = (T*)smem_raw;                           // [kSmC][kSmN]: L_b copy (update) / own block (owner)
     T* ub = Lb + kSmC * kSmN;                       // [2][kSmC] pivot row (update phase)
-    T* xb = ub + 2 * kSmC;                          // [2][8][8] candidate rows, [2][8] row g (group columns)
-    __shared__ T s_v[2][kSmT / 32];
-    __shared__ int s_i[2][kSmT / 32];
+    T* xb = ub + 2 * kSmC;                          // [2][8][8] candidate rows, [2][8] row g (group columns),
+                                                    // then at xb + 272: [2][8][kSmC] U12 rows of the update groups
+    __shared__ unsigned s_kh[2][kSmN / 32], s_kl[2][kSmN / 32], s_ki[2][kSmN / 32];   // warp argmax keys
     __shared__ int s_piv[kSmC];                     // this CTA's pivots (read by later CTAs)
     __shared__ int s_pb[kSmC];                      // pivots of the panel being applied
     __shared__ int s_all[kSmN];                     // all pivots (write-out)
@@ -1163,28 +1173,45 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
                     for (int i = 0; i < 16; ++i) Lb[r + (hc + i0 + i) * kSmN] = tmp[i];
                 }
             }
-            // ---- 64 rank-1 steps: row g0 + k of this block is final after step k - 1
-            if (r == g0) {
-#pragma unroll
-                for (int i = 0; i < kSmH; ++i) ub[hc + i] = a[i];
-            }
-            __syncthreads();
+            // ---- 8 groups of 8 rows: the group's U12 rows by a column-parallel unit-lower solve
+            // (staged in shared memory), then a rank-8 update of the rows below (two barriers per
+            // group instead of one per row)
             SMPROF(2);
-            for (int k = 0; k < kSmC; ++k) {
-                const int g = g0 + k, par = k & 1;
-                const T* u = ub + par * kSmC + hc;
-                if (r > g && row_ok) {
-                    const T l = Lb[r + k * kSmN];
+            for (int k0 = 0; k0 < kSmC; k0 += 8) {
+                const int gg = g0 + k0;
+                T* U8 = xb + 272 + ((k0 >> 3) & 1) * (8 * kSmC);   // [8][kSmC], double-buffered
+                const bool in_grp = r >= gg && r < gg + 8;
+                if (in_grp) {
 #pragma unroll
-                    for (int i = 0; i < kSmH; ++i) a[i] -= l * u[i];
-                    if (r == g + 1 && k + 1 < kSmC) {
-                        T* un = ub + (par ^ 1) * kSmC + hc;
+                    for (int i = 0; i < kSmH; ++i) U8[(r - gg) * kSmC + hc + i] = a[i];
+                }
+                __syncthreads();
+                if (tid < kSmC) {
+                    T u[8];
 #pragma unroll
-                        for (int i = 0; i < kSmH; ++i) un[i] = a[i];
+                    for (int t = 0; t < 8; ++t) {
+                        T x = U8[t * kSmC + tid];
+#pragma unroll
+                        for (int s2 = 0; s2 < t; ++s2) x -= Lb[(gg + t) + (k0 + s2) * kSmN] * u[s2];
+                        u[t] = x;
+                        U8[t * kSmC + tid] = x;
                     }
                 }
                 __syncthreads();
+                if (in_grp) {
+#pragma unroll
+                    for (int i = 0; i < kSmH; ++i) a[i] = U8[(r - gg) * kSmC + hc + i];
+                } else if (r >= gg + 8 && row_ok) {
+                    T lq[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) lq[t] = Lb[r + (k0 + t) * kSmN];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+#pragma unroll
+                        for (int i = 0; i < kSmH; ++i) a[i] -= lq[t] * U8[t * kSmC + hc + i];
+                }
             }
+            __syncthreads();
         }
         if (prof == 1 && tid == 0 && c < 4 && b < 4) {   // diagnostics: %globaltimer at the end of step b
             unsigned long long t;
@@ -1211,23 +1238,25 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
                     const int j = j0 + t;
                     if (j >= nc) break;
                     const int g = cb + j, par = j & 1;
-                    T v = T(-1);
-                    int ri = 0x7fffffff;
+                    // first-max argmax (Z15) by integer warp reductions on an order-preserving key of
+                    // |a| (hi word + 1, lo word; 0 = no candidate), then the smallest row among the
+                    // maxima; NaN never wins
+                    unsigned kh = 0u, kl = 0u;
                     if (h == 0 && r >= g && row_ok) {
-                        const T x = q[t] < T(0) ? -q[t] : q[t];
-                        if (x == x) { v = x; ri = r; }       // NaN never wins (Z15: first max)
+                        T x = q[t] < T(0) ? -q[t] : q[t];
+                        if (x == x) {
+                            if (x == T(0)) x = T(0);                // -0 -> +0
+                            cand_key(x, kh, kl);
+                        }
                     }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const T v2 = __shfl_xor_sync(0xffffffffu, v, o);
-                        const int r2 = __shfl_xor_sync(0xffffffffu, ri, o);
-                        if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; }
-                    }
+                    unsigned mh = __reduce_max_sync(0xffffffffu, kh);
+                    unsigned ml = __reduce_max_sync(0xffffffffu, kh == mh ? kl : 0u);
+                    unsigned mi = __reduce_min_sync(0xffffffffu, (mh != 0u && kh == mh && kl == ml) ? (unsigned)r : 0x7fffffffu);
                     // one barrier per column: the warp winner publishes its group row with its
                     // candidate, row g publishes itself (the displaced row when p != g)
                     T* CR = xb + par * 64;                      // [8 warps][8]: candidate rows
                     T* Yr = xb + 128 + par * 8;                 // row g, group columns
-                    if (h == 0 && ri == r) {
+                    if (h == 0 && mi == (unsigned)r) {
 #pragma unroll
                         for (int s2 = 0; s2 < 8; ++s2) CR[warp * 8 + s2] = q[s2];
                     }
@@ -1235,16 +1264,16 @@ __global__ void __launch_bounds__(kSmT, 1) lu_small_kernel(T* W, int64_t ldw, in
 #pragma unroll
                         for (int s2 = 0; s2 < 8; ++s2) Yr[s2] = q[s2];
                     }
-                    if (lane == 0) { s_v[par][warp] = v; s_i[par][warp] = ri; }
+                    if (lane == 0 && h == 0) { s_kh[par][warp] = mh; s_kl[par][warp] = ml; s_ki[par][warp] = mi; }
                     __syncthreads();
-                    v = s_v[par][0]; ri = s_i[par][0];
-                    int wb = 0;
-#pragma unroll
-                    for (int w2 = 1; w2 < kSmN / 32; ++w2) {   // (warps of h = 1 hold no candidates)
-                        const T v2 = s_v[par][w2];
-                        const int r2 = s_i[par][w2];
-                        if (v2 > v || (v2 == v && r2 < ri)) { v = v2; ri = r2; wb = w2; }
-                    }
+                    kh = lane < kSmN / 32 ? s_kh[par][lane] : 0u;
+                    kl = lane < kSmN / 32 ? s_kl[par][lane] : 0u;
+                    const unsigned ki = lane < kSmN / 32 ? s_ki[par][lane] : 0x7fffffffu;
+                    mh = __reduce_max_sync(0xffffffffu, kh);
+                    ml = __reduce_max_sync(0xffffffffu, kh == mh ? kl : 0u);
+                    mi = __reduce_min_sync(0xffffffffu, (mh != 0u && kh == mh && kl == ml) ? ki : 0x7fffffffu);
+                    const int ri = (int)mi;
+                    const int wb = ri >> 5;                     // rows of the h = 0 warps: r = tid
                     const int p = (ri == 0x7fffffff) ? g : ri;
                     const T* X = (ri == 0x7fffffff) ? Yr : CR + wb * 8;   // pivot row, group columns
                     if (p != g && tid < kSmC && (tid < j0 || tid >= j0 + 8)) {   // the other columns, in shared memory
@@ -1375,7 +1404,7 @@ template <typename T>
 static bool small_lu_launch(const Work& w, cudaStream_t s) {
     const int n = (int)w.n;
     const int P = (n + kSmC - 1) / kSmC;
-    const size_t smem = sizeof(T) * ((size_t)kSmC * kSmN + 5 * kSmC);
+    const size_t smem = sizeof(T) * ((size_t)kSmC * kSmN + 2 * kSmC + 272 + 2 * 8 * kSmC);
     auto kern = lu_small_kernel<T>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
