@@ -67,6 +67,20 @@ struct __align__(32) PSlot {
     long long pad;
 };
 
+// Order-preserving integer key of a candidate |a| >= +0 (0 is reserved for "no candidate"): the
+// first-max argmax becomes three integer warp reductions (max high word, max low word among the
+// high maxima, min row among the full maxima).
+template <typename T> AS_DEV void cand_key(T x, unsigned& hi, unsigned& lo);
+template <> AS_DEV void cand_key<double>(double x, unsigned& hi, unsigned& lo) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);   // x >= +0: bits are monotone
+    hi = (unsigned)(b >> 32) + 1u;
+    lo = (unsigned)b;
+}
+template <> AS_DEV void cand_key<float>(float x, unsigned& hi, unsigned& lo) {
+    hi = __float_as_uint(x) + 1u;
+    lo = 0u;
+}
+
 // ------------------------------------------------------------------ panel (cooperative)
 // Rows of the panel are split over the P CTAs (shared memory when they fit).  Per column j:
 // every CTA publishes its local first-max candidate row (and the owner of row g the old row g)
@@ -92,10 +106,12 @@ AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, in
         if (gr == g && a != a) dnan = 1;
         if (a > bv) { bv = a; br = (unsigned)r; }     // rows increase: strict > keeps the first
     }
-    T wm = bv;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-    const unsigned wr = __reduce_min_sync(0xffffffffu, (bv == wm && br != 0xffffffffu) ? br : 0xffffffffu);
+    unsigned kh = 0u, kl = 0u;
+    if (br != 0xffffffffu) cand_key<T>(bv == T(0) ? T(0) : bv, kh, kl);   // (-0 -> +0)
+    unsigned mh = __reduce_max_sync(0xffffffffu, kh);
+    unsigned ml = __reduce_max_sync(0xffffffffu, kh == mh ? kl : 0u);
+    const unsigned wr = __reduce_min_sync(0xffffffffu, (mh != 0u && kh == mh && kl == ml) ? br : 0xffffffffu);
+    const T wm = __shfl_sync(0xffffffffu, bv, (int)(__ffs(__ballot_sync(0xffffffffu, br == wr && wr != 0xffffffffu)) - 1) & 31);
     dnan = __any_sync(0xffffffffu, dnan);
     if (lane == 0) { sv[warp] = (wr == 0xffffffffu) ? T(-1) : wm; si[warp] = (long long)wr; sdn[warp] = dnan; }
     __syncthreads();
@@ -103,10 +119,12 @@ AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, in
     const T v8 = (lane & 7) < nw ? sv[lane & 7] : T(-1);
     const unsigned r8 = (lane & 7) < nw ? (unsigned)si[lane & 7] : 0xffffffffu;
     const int d8 = (lane & 7) < nw ? sdn[lane & 7] : 0;
-    T m8 = v8;
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) m8 = fmax(m8, __shfl_xor_sync(0xffffffffu, m8, o));
-    const unsigned rmin = __reduce_min_sync(0xffffffffu, (v8 == m8 && r8 != 0xffffffffu) ? r8 : 0xffffffffu);
+    kh = 0u; kl = 0u;
+    if (r8 != 0xffffffffu) cand_key<T>(v8, kh, kl);
+    mh = __reduce_max_sync(0xffffffffu, kh);
+    ml = __reduce_max_sync(0xffffffffu, kh == mh ? kl : 0u);
+    const unsigned rmin = __reduce_min_sync(0xffffffffu, (mh != 0u && kh == mh && kl == ml) ? r8 : 0xffffffffu);
+    const T m8 = __shfl_sync(0xffffffffu, v8, (int)(__ffs(__ballot_sync(0xffffffffu, r8 == rmin && rmin != 0xffffffffu)) - 1) & 31);
     const int dn = __any_sync(0xffffffffu, d8);
     v = (rmin == 0xffffffffu) ? T(-1) : m8;
     idx = (rmin == 0xffffffffu) ? 0x7fffffffffffffffll : (long long)(rbeg + rmin);
@@ -1093,16 +1111,6 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
 // (LAPACK's convention: all interchanges applied to all columns), CTA 0 writes the row
 // permutation.  No grid-wide exchange, no intermediate launches: C1's factorization was ~0.7 ms
 // of panel launches with one cross-CTA exchange per column.
-template <typename T> AS_DEV void cand_key(T x, unsigned& hi, unsigned& lo);
-template <> AS_DEV void cand_key<double>(double x, unsigned& hi, unsigned& lo) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(x);   // x >= +0: bits are monotone
-    hi = (unsigned)(b >> 32) + 1u;
-    lo = (unsigned)b;
-}
-template <> AS_DEV void cand_key<float>(float x, unsigned& hi, unsigned& lo) {
-    hi = __float_as_uint(x) + 1u;
-    lo = 0u;
-}
 constexpr int kSmN = 256;        // rows
 constexpr int kSmT = 512;        // threads: two per row
 constexpr int kSmC = 64;         // columns per CTA
