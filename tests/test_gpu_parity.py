@@ -465,3 +465,21 @@ def test_debug_factor_cholesky_reconstruction(n):
     info, _, _ = AS.as_debug_factor(AS.to_device(B), oracle.M_CHOL)
     _, oinfo = oracle.potrf(B)
     assert info == oinfo and info > 0
+
+
+@pytest.mark.parametrize("n", [200, 300])
+def test_lu_padded_lda(n):
+    """lda > n (a row-padded view): both LU paths read A through lda and W through its own ld."""
+    A = W.random_dense(n, seed=40 + n)
+    B = np.asfortranarray(np.random.default_rng(n).standard_normal((n, 2)))
+    big = np.full((n + 5, n), 7.0, order="F")
+    big[:n] = A
+    dA = AS.to_device(big)[:n]
+    assert dA.stride(1) == n + 5
+    ret, X, rep = AS.as_solve_ex(dA, AS.to_device(B))
+    torch.cuda.synchronize()
+    assert ret == 0 and rep["primary_method"] == oracle.M_LU
+    _, Xo, orep, _ = oracle.solve(A, B)
+    Xg = AS.to_host(X)
+    assert backward_error(A, Xg, B) <= 1e-13
+    assert forward_diff(Xg, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"]
