@@ -44,6 +44,63 @@ __global__ void state_init_kernel(DevState* st, int64_t n, uint32_t opts, int fo
     *st = s;
 }
 
+AS_DEV bool band_density_ok(long long n, long long kl, long long ku);
+
+// The far corner tile pair, (rows n-64.., cols 0..63) and its mirror, checked ahead of the pair
+// pass with every verdict that needs no diagonal value: non-zeros (UPPER / LOWER, kl / ku and the
+// 25% band rule) and Fig. 4 lines 12-14 (asymmetry).  The same per-element predicates the pair
+// pass evaluates (Z8: order cannot change the verdict), so a dense or triangular matrix enters the
+// pair pass with its dead candidates already known -- the first wave then reads one tile per pair
+// instead of two (C3b: 86 -> 67 MB).
+template <typename T>
+__device__ void corner_pair(const T* A, int64_t lda, int64_t n, DevState* st) {
+    __shared__ T mir[kTile * (kTile + 1)];
+    const int64_t i0 = n - kTile;                          // lower tile rows i0.., columns 0..63
+    constexpr int kPer = kTile * kTile / 256;              // blockDim.x == 256 (launch_detect)
+    T mv[kPer], av[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {                       // every load of both tiles issued at once
+        const int e = threadIdx.x + 256 * k, r = e & (kTile - 1), c = e >> 6;
+        mv[k] = A[r + (i0 + c) * lda];                     // mirror tile element A(r, i0 + c)
+        av[k] = A[(i0 + r) + (int64_t)c * lda];            // lower tile element A(i0 + r, c)
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int e = threadIdx.x + 256 * k, r = e & (kTile - 1), c = e >> 6;
+        mir[c * (kTile + 1) + r] = mv[k];
+    }
+    __syncthreads();
+    const T tol = T(100) * Eps<T>::v;                      // Fig. 4 line 5
+    int kl = 0, ku = 0;
+    bool lnz = false, unz = false, asym = false;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int e = threadIdx.x + 256 * k, r = e & (kTile - 1), c = e >> 6;
+        const T a = av[k];                                 // A(i0 + r, c), strictly below the diagonal
+        const T b = mir[r * (kTile + 1) + c];              // A(c, i0 + r)
+        const int dist = (int)(i0 + r - c);
+        if (a != T(0)) { lnz = true; kl = max(kl, dist); }
+        if (b != T(0)) { unz = true; ku = max(ku, dist); }
+        const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
+        const T df = a - b;
+        const T delta = df < T(0) ? -df : df;              // line 12
+        const T m = aa > ab ? aa : ab;
+        if (delta > tol && delta > tol * m) asym = true;   // lines 13-14
+    }
+    kl = __reduce_max_sync(0xffffffffu, kl);
+    ku = __reduce_max_sync(0xffffffffu, ku);
+    const unsigned kill = (__any_sync(0xffffffffu, lnz) ? AS_FLAG_UPPER : 0u) |
+                          (__any_sync(0xffffffffu, unz) ? AS_FLAG_LOWER : 0u) |
+                          (__any_sync(0xffffffffu, asym) ? AS_FLAG_SPD_CANDIDATE : 0u);
+    if ((threadIdx.x & 31) == 0) {
+        int gkl = kl ? max(kl, atomicMax(&st->kl, kl)) : 0;
+        int gku = ku ? max(ku, atomicMax(&st->ku, ku)) : 0;
+        unsigned k2 = kill;
+        if ((kl || ku) && !band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
+        if (k2) atomicAnd(&st->alive, ~k2);
+    }
+}
+
 // ------------------------------------------------------------------ pass 1: diagonal
 // Fig. 4 lines 7-9: any A_jj <= 0 kills SPD; max_diag = max A_jj over A_jj > 0.
 // Also gathers diag(A) contiguously for the pair pass (line 16).
@@ -63,6 +120,7 @@ __global__ void detect_diag_kernel(const DevArgs* args, int64_t lda, int64_t n, 
     __shared__ int skill;
     if (threadIdx.x == 0) skill = 0;
     __syncthreads();
+    if (blockIdx.x == 0 && blockDim.x == 256 && n >= 2 * kTile) corner_pair<T>(A, lda, n, st);
     for (int o = 16; o > 0; o >>= 1) local = fmax(local, __shfl_xor_sync(0xffffffffu, local, o));
     if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = local;
     if (kill) skill = 1;
@@ -455,6 +513,44 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
     unsigned known = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
 
     for (unsigned p = blockIdx.x; p < total; p += gridDim.x) {
+        if (!fullscan && (known == AS_FLAG_UPPER || known == AS_FLAG_LOWER)) {
+            // ---- only one triangular candidate left: one tile per pair decides (UPPER: the lower
+            // tile must be zero; LOWER: the mirror tile), so the next pair's tile is loaded into
+            // the second register buffer before the current one is checked (loads stay in flight)
+            const bool up_only = known == AS_FLAG_UPPER;
+            auto load = [&](unsigned q, T (&v)[16]) {
+                long long I2, J2;
+                pair_of(q, nt, I2, J2);
+                const bool inter = (I2 * kTile + kTile <= n) && (J2 * kTile + kTile <= n);
+                if (up_only) load_tile_regs<T>(v, A, lda, n, I2 * kTile, J2 * kTile, vec, inter);
+                else load_tile_regs<T>(v, A, lda, n, J2 * kTile, I2 * kTile, vec, inter);
+            };
+            T cur[16], nxt[16];
+            load(p, cur);
+            for (;;) {
+                const unsigned pn = p + gridDim.x;
+                const bool has_next = pn < total;
+                if (has_next) load(pn, nxt);
+                if (threadIdx.x == 0) s_alive = *(volatile unsigned*)&st->alive;
+                long long I, J;
+                pair_of(p, nt, I, J);
+                bool nz = false;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                    // diagonal tile: only the strict lower (UPPER candidate) / strict upper part counts
+                    nz |= cur[i] != T(0) && (I != J || (up_only ? r > c : c > r));
+                }
+                if (__syncthreads_or(nz)) {
+                    if (threadIdx.x == 0) atomicAnd(&st->alive, ~known);
+                    return;
+                }
+                if (s_alive == 0u || !has_next) return;
+                p = pn;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+            }
+        }
         long long I, J;
         pair_of(p, nt, I, J);
         const long long D = I - J;
