@@ -25,7 +25,9 @@
  *    the caller and must hold ldb*nrhs elements; X == B (exact alias, in-place
  *    solve) is allowed, any other overlap is undefined.  Factors live in a
  *    library-owned workspace cached per (device, stream, dtype, n, nrhs, lda,
- *    ldb, options) and released by as_release_all().
+ *    ldb, options) and released by as_release_all().  Calls on different
+ *    streams therefore never share a workspace; calls on one stream are
+ *    ordered by the stream.
  *  - Streams: all device work is enqueued on `stream`; the call synchronizes
  *    that stream exactly once (to read the device-resident report), and not at
  *    all for as_solve_async().
@@ -60,6 +62,11 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
 #define AS_FLAG_RCOND_LOW     (1u << 10)  /* the gate fired: singular or !(rcond >= thr) */
 #define AS_FLAG_FALLBACK      (1u << 11)  /* X is the SVD minimum-norm solution */
 #define AS_FLAG_POORLY_COND   (1u << 12)  /* gate fired with AS_OPT_NO_FALLBACK: X is the primary solution */
+#define AS_FLAG_NONFINITE     (1u << 13)  /* a NaN/Inf was seen: in A or B under AS_OPT_CHECK_FINITE (the call
+                                             returns AS_ERR_NONFINITE before any factorization), or in the
+                                             fallback's singular values (non-finite input reached the SVD, whose
+                                             minimum-norm solution is then undefined: AS_ERR_NONFINITE).
+                                             (robustness to floating-point limits), Z28/Z29 */
 #define AS_FLAG_SVD_NOCONV    (1u << 14)  /* Jacobi hit max_sweeps */
 #define AS_FLAG_RANK_DEF      (1u << 15)  /* fallback effective rank < n */
 
@@ -75,6 +82,9 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
 /* ---- options ------------------------------------------------------------- */
 #define AS_OPT_NO_FALLBACK  0x1u   /* disable the SVD fallback */
 #define AS_OPT_FORCE_METHOD 0x2u   /* use opt.force_method (1..5) instead of the detected one */
+#define AS_OPT_CHECK_FINITE 0x4u   /* reject NaN/Inf in A or B (AS_ERR_NONFINITE, flag AS_FLAG_NONFINITE, X untouched):
+                                      the detection pass then reads every element of A (no early exit) and B is
+                                      scanned once; off by default (the paper is silent on non-finite input, Z28) */
 #define AS_OPT_FULLSCAN     0x8u   /* detection never exits early; kl/ku always exact */
 #define AS_OPT_SKIP_DETECT  0x10u  /* with AS_OPT_FORCE_METHOD (LU, CHOL, TRI_*): no structure detection at all --
                                       the "standard solver" of the paper's comparison; report bits
@@ -85,6 +95,8 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
 #define AS_OK                        0
 #define AS_ERR_SINGULAR_NO_FALLBACK  1   /* exact zero pivot and NO_FALLBACK: X unspecified */
 #define AS_ERR_SVD_NOT_CONVERGED     2   /* fallback Jacobi hit max_sweeps (X is its last iterate) */
+#define AS_ERR_NONFINITE             3   /* NaN/Inf input (AS_OPT_CHECK_FINITE) or non-finite singular values in the
+                                            fallback: X unspecified, flags carry AS_FLAG_NONFINITE */
 #define AS_ERR_NOT_IMPLEMENTED       4
 #define AS_ERR_NO_DEVICE             5
 #define AS_ERR_CUDA_BASE             1000
@@ -116,6 +128,8 @@ typedef struct {
     int32_t method;            /* first-match dispatch */
     int64_t kl, ku;            /* exact if banded or FULLSCAN, else -1 */
     double max_diag;           /* Fig. 4 max_diag (largest positive diagonal entry) */
+    int32_t nonfinite_seen;    /* 1 if A holds a NaN/Inf (only evaluated with AS_OPT_CHECK_FINITE, else 0) */
+    int32_t reserved;
 } as_structure;
 
 /*
@@ -158,10 +172,15 @@ int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void
                   void* X, const as_options* opt, as_report* rep, void* stream);
 
 /* as_detect: structure detection only (P:164-175, P:328-343, P:382-384,
- * Fig. 4).  detect_flags: AS_OPT_FULLSCAN or 0.  out: host. */
+ * Fig. 4).  detect_flags: AS_OPT_FULLSCAN and/or AS_OPT_CHECK_FINITE (which
+ * implies a full scan and fills out->nonfinite_seen), or 0.  out: host. */
 int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detect_flags, as_structure* out,
               void* stream);
 
+/* ---- test-only / diagnostic exports: only in libadaptsolve_debug.so, the same
+ * sources built with -DAS_DEBUG (SURVEY 8(b) "Test-only exports").  Never used by
+ * the solve, the benchmark or smoke(). */
+#ifdef AS_DEBUG
 /* as_debug_factor: test-only (T3 reconstruction tests; never used by the
  * solve or the bench).  Runs the primary factorization `method` alone, with
  * the launchers the solve uses (AS_METHOD_LU: xGETRF, P:505-515;
@@ -178,22 +197,6 @@ int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detec
  * through the solve parity tests). */
 int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
                         void* W, int64_t* ipiv, void* stream);
-
-/* Benchmark instrumentation.  When enabled, plans built afterwards record
- * CUDA events (graph event-record nodes) around the top-level stages of the
- * solve; as_last_stage_ms() returns the device-timed durations (ms) of the
- * last synchronous call on this thread: [0] detection (diag + tile-pair
- * pass + dispatch), [1] the method body (factor + rcond estimate),
- * [2] gate + post (primary solve or SVD fallback), [3] whole graph.
- * Returns 0, or -1 if the last plan was not instrumented. */
-void as_set_instrumentation(int enable);
-int as_last_stage_ms(double* out4);
-
-/* Execution mode of plans built afterwards: 0 (default) = one CUDA graph with
- * device-side conditional nodes, one host sync per call; 1 = eager profiling
- * mode: the same kernels launched directly, branch decisions read back by the
- * host (several syncs; for kernel-by-kernel ncu launch lists only). */
-void as_set_exec_mode(int eager);
 
 /* Diagnostics: %globaltimer stamps (ns) recorded by the last call's kernels
  * at phase boundaries (out: 16 values; 0 = not recorded). */
@@ -217,6 +220,24 @@ double as_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
                            int iters, int dbg);
 int as_debug_lu_trace(unsigned long long* tmin, unsigned long long* tmax, int cap);
 
+#endif /* AS_DEBUG */
+
+/* Benchmark instrumentation.  When enabled, plans built afterwards record
+ * CUDA events (graph event-record nodes) around the top-level stages of the
+ * solve; as_last_stage_ms() returns the device-timed durations (ms) of the
+ * last synchronous call on this thread: [0] detection (diag + tile-pair
+ * pass + dispatch), [1] the method body (factor + rcond estimate),
+ * [2] gate + post (primary solve or SVD fallback), [3] whole graph.
+ * Returns 0, or -1 if the last plan was not instrumented. */
+void as_set_instrumentation(int enable);
+int as_last_stage_ms(double* out4);
+
+/* Execution mode of plans built afterwards: 0 (default) = one CUDA graph with
+ * device-side conditional nodes, one host sync per call; 1 = eager profiling
+ * mode: the same kernels launched directly, branch decisions read back by the
+ * host (several syncs; for kernel-by-kernel ncu launch lists only). */
+void as_set_exec_mode(int eager);
+
 /* Roofline denominator probe (benchmark only, not part of a solve): fp64
  * tensor-core (DMMA) throughput in TFLOP/s of a register-resident MMA loop. */
 double as_measure_fp64_peak(int iters, void* stream);
@@ -224,8 +245,10 @@ double as_measure_fp64_peak(int iters, void* stream);
  * on internal zero-filled buffers, M x N x K, op(B) = B^T if trans_b. */
 double as_bench_gemm(int dtype, int64_t M, int64_t N, int64_t K, int trans_b, int iters);
 
-/* Workspace bytes a plan for this shape allocates (device). */
-int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs);
+/* Workspace bytes (device) a plan for this shape and these AS_OPT_* option
+ * flags allocates (FORCE_METHOD reserves room for a forced band factor of
+ * any width).  Returns -1 on an illegal argument (dt, n < 0, nrhs < 0). */
+int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs, uint32_t opts);
 /* Number of kernel launches the last as_solve* on this thread enqueued
  * (graph kernel nodes executed are not observable; this counts the nodes of
  * the graph branches the device took, as recorded by the finalize kernel). */

@@ -27,6 +27,9 @@ F_CHOL_FAILED, F_SINGULAR, F_RCOND_LOW, F_FALLBACK = 1 << 8, 1 << 9, 1 << 10, 1 
 F_POORLY_COND, F_NONFINITE, F_SVD_NOCONV, F_RANK_DEF = 1 << 12, 1 << 13, 1 << 14, 1 << 15
 M_BAND, M_TRI_LOWER, M_TRI_UPPER, M_CHOL, M_LU, M_SVD = 1, 2, 3, 4, 5, 6
 OPT_NO_FALLBACK, OPT_FORCE_METHOD, OPT_FULLSCAN = 0x1, 0x2, 0x8
+OPT_CHECK_FINITE = 0x4
+ERR_NONFINITE = 3
+F_NONFINITE = 1 << 13
 ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
 
 
@@ -36,8 +39,9 @@ def build(force: bool = False) -> str:
     if not force and os.path.exists(_SO) and all(os.path.getmtime(_SO) >= os.path.getmtime(s) for s in src):
         return _SO
     cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
-           "-Wall", "-Wno-unused-function", "-o", _SO, os.path.join(_HERE, "oracle.c"), "-lm"]
+           "-Wall", "-Wno-unused-function", "-o", _SO + ".tmp", os.path.join(_HERE, "oracle.c"), "-lm"]
     subprocess.check_call(cmd)
+    os.replace(_SO + ".tmp", _SO)    # a running process keeps its mapped copy
     return _SO
 
 
@@ -274,7 +278,7 @@ def lsq_svd(A, B, cut=None, max_sweeps=30):
 
 # ---------------------------------------------------------------- solve
 def solve(A, B, *, no_fallback=False, force_method=None, fullscan=False, rcond_threshold=-1.0,
-          lsq_cutoff=-1.0, max_sweeps=30):
+          lsq_cutoff=-1.0, max_sweeps=30, check_finite=False):
     """The adaptive solve (oracle_impl.h: or_solve).  Returns (ret, X, report dict, sigma)."""
     A = _fortran(A)
     B = _fortran(B).astype(A.dtype, copy=False)
@@ -283,7 +287,7 @@ def solve(A, B, *, no_fallback=False, force_method=None, fullscan=False, rcond_t
     sig = np.zeros(max(n, 1), dtype=A.dtype)
     o = Options()
     o.flags = (OPT_NO_FALLBACK if no_fallback else 0) | (OPT_FORCE_METHOD if force_method else 0) | \
-        (OPT_FULLSCAN if fullscan else 0)
+        (OPT_FULLSCAN if fullscan else 0) | (OPT_CHECK_FINITE if check_finite else 0)
     o.force_method = int(force_method or 0)
     o.rcond_threshold = rcond_threshold
     o.lsq_cutoff = lsq_cutoff

@@ -32,10 +32,12 @@
 /* options */
 #define OR_OPT_NO_FALLBACK  0x1u
 #define OR_OPT_FORCE_METHOD 0x2u
+#define OR_OPT_CHECK_FINITE 0x4u
 #define OR_OPT_FULLSCAN     0x8u
 /* errors */
 #define OR_ERR_SINGULAR_NO_FALLBACK 1
 #define OR_ERR_SVD_NOT_CONVERGED    2
+#define OR_ERR_NONFINITE            3
 
 typedef struct {
     uint32_t flags;       /* OR_BANDED | OR_LOWER | OR_UPPER | OR_SPD (literal, each evaluated) */

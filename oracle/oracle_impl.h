@@ -106,6 +106,17 @@ static int FN(band_density_ok)(int64_t n, int64_t kl, int64_t ku)
     return 4u * cnt <= un * un;
 }
 
+/* Every element of the m x n column-major array finite?  Z28:
+ * SPEC S:91 / S:409 reject NaN/Inf input at solve entry; the paper asks for
+ * robustness to floating-point limits.  isfinite() of C99. */
+static int FN(all_finite)(const T* A, int64_t lda, int64_t m, int64_t n)
+{
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i)
+            if (!isfinite(A[i + j * lda])) return 0;
+    return 1;
+}
+
 /* ------------------------------------------------------------------ */
 /* Norms                                                               */
 /* ------------------------------------------------------------------ */
@@ -509,7 +520,8 @@ static int FN(jacobi)(T* M, int64_t ld, int64_t n, T* V, int max_sweeps, int* co
  * descending (stable).  Returns the rank (number kept); *sweeps_out and
  * *conv_out report the Jacobi iteration. */
 static int64_t FN(lsq_svd)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, int64_t nrhs,
-                           T* X, int64_t ldx, T cut, int max_sweeps, T* sigma_out, int* sweeps_out, int* conv_out)
+                           T* X, int64_t ldx, T cut, int max_sweeps, T* sigma_out, int* sweeps_out, int* conv_out,
+                           int* nonfinite_out)
 {
     T* W = (T*)malloc(sizeof(T) * (size_t)(n * n));
     T* C = (T*)malloc(sizeof(T) * (size_t)(n * (nrhs > 0 ? nrhs : 1)));
@@ -526,12 +538,15 @@ static int64_t FN(lsq_svd)(const T* A, int64_t lda, int64_t n, const T* B, int64
     int conv = 0;
     int sweeps = FN(jacobi)(M, n, n, V, max_sweeps, &conv);
     /* (3) sigma_k = ||m_k||_2, sorted descending (stable insertion sort) */
+    int nonfinite = 0;
     for (int64_t k = 0; k < n; ++k) {
         T s = (T)0;
         for (int64_t i = 0; i < n; ++i) s += M[i + k * n] * M[i + k * n];
         sig[k] = SQRT(s);
         order[k] = k;
+        if (!isfinite(sig[k])) nonfinite = 1;   /* Z29: non-finite input reached the SVD */
     }
+    if (nonfinite_out) *nonfinite_out = nonfinite;
     for (int64_t a = 1; a < n; ++a) {
         int64_t key = order[a]; int64_t b = a - 1;
         while (b >= 0 && sig[order[b]] < sig[key]) { order[b + 1] = order[b]; --b; }
@@ -607,7 +622,7 @@ void FN(or_geqr)(T* W, int64_t ld, int64_t n, T* C, int64_t ldc, int64_t nrhs) {
 int FN(or_jacobi)(T* M, int64_t ld, int64_t n, T* V, int max_sweeps, int* conv) { return FN(jacobi)(M, ld, n, V, max_sweeps, conv); }
 int64_t FN(or_lsq_svd)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, int64_t nrhs, T* X, int64_t ldx,
                        double cut, int max_sweeps, T* sigma_out, int* sweeps_out, int* conv_out)
-{ return FN(lsq_svd)(A, lda, n, B, ldb, nrhs, X, ldx, (T)cut, max_sweeps, sigma_out, sweeps_out, conv_out); }
+{ return FN(lsq_svd)(A, lda, n, B, ldb, nrhs, X, ldx, (T)cut, max_sweeps, sigma_out, sweeps_out, conv_out, NULL); }
 
 /* The adaptive solve, the paper's flowchart (Fig. 2
  * caption P:237-243) as read in Z9-Z11, Z24, Z25:
@@ -640,6 +655,14 @@ int FN(or_solve)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, in
     else if (st.flags & OR_SPD) method = OR_M_CHOL;
     else method = OR_M_LU;
     if (method == OR_M_BAND || (o.flags & OR_OPT_FULLSCAN)) { rep->kl = st.kl; rep->ku = st.ku; }
+    /* Z28: with CHECK_FINITE a NaN/Inf anywhere in A or B is rejected before
+     * any factorization (the detection verdicts are still reported). */
+    if ((o.flags & OR_OPT_CHECK_FINITE) &&
+        !(FN(all_finite)(A, lda, n, n) && FN(all_finite)(B, ldb, n, nrhs))) {
+        rep->rcond = 0.0;
+        rep->flags = flags | OR_F_NONFINITE;
+        return OR_ERR_NONFINITE;
+    }
 
     int singular = 0, factored = 0;
     T rcond = 0, anorm = 0;
@@ -720,13 +743,20 @@ int FN(or_solve)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, in
             if (singular) ret = OR_ERR_SINGULAR_NO_FALLBACK;
             else flags |= OR_F_POORLY_COND;
         } else {
-            int sweeps = 0, conv = 0;
-            int64_t rank = FN(lsq_svd)(A, lda, n, B, ldb, nrhs, X, ldx, cut, max_sweeps, sigma_out, &sweeps, &conv);
+            int sweeps = 0, conv = 0, nonfinite = 0;
+            int64_t rank = FN(lsq_svd)(A, lda, n, B, ldb, nrhs, X, ldx, cut, max_sweeps, sigma_out, &sweeps, &conv,
+                                       &nonfinite);
             rep->rank = rank; rep->sweeps = sweeps;
             flags |= OR_F_FALLBACK;
             method = OR_M_SVD;
-            if (rank < n) flags |= OR_F_RANK_DEF;
-            if (!conv) { flags |= OR_F_SVD_NOCONV; ret = OR_ERR_SVD_NOT_CONVERGED; }
+            if (nonfinite) {          /* Z29: min-norm solution undefined, X unspecified */
+                flags |= OR_F_NONFINITE;
+                rep->rank = -1;
+                ret = OR_ERR_NONFINITE;
+            } else {
+                if (rank < n) flags |= OR_F_RANK_DEF;
+                if (!conv) { flags |= OR_F_SVD_NOCONV; ret = OR_ERR_SVD_NOT_CONVERGED; }
+            }
         }
     }
     rep->method = method;

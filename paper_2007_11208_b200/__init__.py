@@ -19,6 +19,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libadaptsolve.so")
+# the same sources built with -DAS_DEBUG: adds the test-only as_debug_* exports (loaded on demand by
+# the reconstruction tests and the diagnostic tools, never by the solve, the bench or smoke())
+DEBUG_LIB_PATH = os.path.join(_HERE, "libadaptsolve_debug.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libadaptsolve.so not found at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'`"
@@ -30,16 +33,17 @@ AS_F64, AS_F32 = 0, 1
 FLAG_BANDED, FLAG_LOWER, FLAG_UPPER, FLAG_SPD = 0x1, 0x2, 0x4, 0x8
 FLAG_CHOL_FAILED, FLAG_SINGULAR, FLAG_RCOND_LOW, FLAG_FALLBACK = 1 << 8, 1 << 9, 1 << 10, 1 << 11
 FLAG_POORLY_COND, FLAG_SVD_NOCONV, FLAG_RANK_DEF = 1 << 12, 1 << 14, 1 << 15
+FLAG_NONFINITE = 1 << 13
 METHOD_BAND, METHOD_TRI_LOWER, METHOD_TRI_UPPER, METHOD_CHOL, METHOD_LU, METHOD_SVD = 1, 2, 3, 4, 5, 6
 OPT_NO_FALLBACK, OPT_FORCE_METHOD, OPT_FULLSCAN = 0x1, 0x2, 0x8
-OPT_SKIP_DETECT = 0x10
-ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
+OPT_SKIP_DETECT, OPT_CHECK_FINITE = 0x10, 0x4
+ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED, ERR_NONFINITE = 1, 2, 3
 
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
-           "as_detect", "as_debug_factor", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
+           "as_detect", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
            "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
-           "as_set_exec_mode", "as_debug_timestamps", "as_debug_lu_trace", "as_bench_gemm",
-           "as_debug_panel_time")
+           "as_set_exec_mode", "as_bench_gemm")
+DEBUG_EXPORTS = ("as_debug_factor", "as_debug_timestamps", "as_debug_lu_trace", "as_debug_panel_time")
 
 
 class Options(C.Structure):
@@ -58,7 +62,7 @@ class Report(C.Structure):
 
 class Structure(C.Structure):
     _fields_ = [("flags", C.c_uint32), ("method", C.c_int32), ("kl", C.c_int64), ("ku", C.c_int64),
-                ("max_diag", C.c_double)]
+                ("max_diag", C.c_double), ("nonfinite_seen", C.c_int32), ("reserved", C.c_int32)]
 
 
 P, I64, D, U32, I32 = C.c_void_p, C.c_int64, C.c_double, C.c_uint32, C.c_int32
@@ -72,7 +76,7 @@ _lib.as_solve_host.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P]
 _lib.as_solve_host.restype = C.c_int
 _lib.as_detect.argtypes = [I32, P, I64, I64, U32, P, P]
 _lib.as_detect.restype = C.c_int
-_lib.as_workspace_bytes.argtypes = [I32, I64, I64]
+_lib.as_workspace_bytes.argtypes = [I32, I64, I64, U32]
 _lib.as_workspace_bytes.restype = I64
 _lib.as_strerror.argtypes = [C.c_int]
 _lib.as_strerror.restype = C.c_char_p
@@ -140,10 +144,11 @@ def to_host(t) -> np.ndarray:
 
 
 def make_options(no_fallback=False, force_method=None, fullscan=False, rcond_threshold=-1.0, lsq_cutoff=-1.0,
-                 max_sweeps=30, skip_detect=False) -> Options:
+                 max_sweeps=30, skip_detect=False, check_finite=False) -> Options:
     o = Options()
     o.flags = (OPT_NO_FALLBACK if no_fallback else 0) | (OPT_FORCE_METHOD if force_method else 0) | \
-        (OPT_FULLSCAN if fullscan else 0) | (OPT_SKIP_DETECT if skip_detect else 0)
+        (OPT_FULLSCAN if fullscan else 0) | (OPT_SKIP_DETECT if skip_detect else 0) | \
+        (OPT_CHECK_FINITE if check_finite else 0)
     o.force_method = int(force_method or 0)
     o.rcond_threshold = float(rcond_threshold)
     o.lsq_cutoff = float(lsq_cutoff)
@@ -195,15 +200,39 @@ def as_solve_host(A: np.ndarray, B: np.ndarray, options: Options | None = None, 
     return ret, X, rep.as_dict()
 
 
-def as_detect(A, fullscan=False, stream=None):
+def as_detect(A, fullscan=False, stream=None, check_finite=False):
     st = Structure()
-    ret = _lib.as_detect(_dt(A), A.data_ptr(), _ld(A), A.shape[0], OPT_FULLSCAN if fullscan else 0, C.byref(st),
-                         _stream_ptr(stream))
+    fl = (OPT_FULLSCAN if fullscan else 0) | (OPT_CHECK_FINITE if check_finite else 0)
+    ret = _lib.as_detect(_dt(A), A.data_ptr(), _ld(A), A.shape[0], fl, C.byref(st), _stream_ptr(stream))
     return ret, {k: getattr(st, k) for k, _ in st._fields_}
 
 
-_lib.as_debug_factor.argtypes = [I32, I32, P, I64, I64, I64, I64, P, P, P]
-_lib.as_debug_factor.restype = I64
+_dbg = None
+
+
+def debug_lib():
+    """libadaptsolve_debug.so (the -DAS_DEBUG build with the as_debug_* exports), loaded on demand."""
+    global _dbg
+    if _dbg is None:
+        if not os.path.exists(DEBUG_LIB_PATH):
+            raise ImportError(f"{DEBUG_LIB_PATH} not found (built with libadaptsolve.so by build())")
+        d = C.CDLL(DEBUG_LIB_PATH)
+        d.as_debug_factor.argtypes = [I32, I32, P, I64, I64, I64, I64, P, P, P]
+        d.as_debug_factor.restype = I64
+        d.as_debug_timestamps.argtypes = [P]
+        d.as_debug_timestamps.restype = C.c_int
+        d.as_debug_panel_time.argtypes = [C.c_int, C.c_int, P, C.c_int64, C.c_int64, C.c_int64, C.c_int, P, C.c_int,
+                                          C.c_int]
+        d.as_debug_panel_time.restype = C.c_double
+        d.as_debug_lu_trace.argtypes = [P, P, C.c_int]
+        d.as_debug_lu_trace.restype = C.c_int
+        d.as_solve_ex.argtypes = _lib.as_solve_ex.argtypes
+        d.as_solve_ex.restype = C.c_int
+        d.as_set_instrumentation.argtypes = [C.c_int]
+        d.as_set_exec_mode.argtypes = [C.c_int]
+        _dbg = d
+    return _dbg
+
 
 
 def as_debug_factor(A, method: int, stream=None):
@@ -213,7 +242,7 @@ def as_debug_factor(A, method: int, stream=None):
     n = A.shape[0]
     Wt = empty_colmajor(n, n, A.dtype, device=A.device)
     ipiv = torch.empty(n, dtype=torch.int64, device=A.device)
-    info = _lib.as_debug_factor(_dt(A), method, A.data_ptr(), _ld(A), n, 0, 0, Wt.data_ptr(), ipiv.data_ptr(),
+    info = debug_lib().as_debug_factor(_dt(A), method, A.data_ptr(), _ld(A), n, 0, 0, Wt.data_ptr(), ipiv.data_ptr(),
                                 _stream_ptr(stream))
     return int(info), Wt, ipiv
 
@@ -240,10 +269,6 @@ _lib.as_bench_gemm.restype = C.c_double
 def bench_gemm(M, N, K, dtype_code=AS_F64, trans_b=False, iters=5) -> float:
     """TFLOP/s of the library's trailing-update GEMM kernel."""
     return float(_lib.as_bench_gemm(dtype_code, M, N, K, int(trans_b), iters))
-_lib.as_debug_timestamps.argtypes = [P]
-_lib.as_debug_timestamps.restype = C.c_int
-_lib.as_debug_panel_time.argtypes = [C.c_int, C.c_int, P, C.c_int64, C.c_int64, C.c_int64, C.c_int, P, C.c_int, C.c_int]
-_lib.as_debug_panel_time.restype = C.c_double
 
 
 def debug_panel_time(W, k0, nbp, kind=0, iters=5, dbg=0):
@@ -252,19 +277,17 @@ def debug_panel_time(W, k0, nbp, kind=0, iters=5, dbg=0):
     n = W.shape[0]
     Wc = W.clone()
     src = W.clone()
-    return _lib.as_debug_panel_time(_dt(W), kind, Wc.data_ptr(), W.stride(1), n, k0, nbp, src.data_ptr(),
+    return debug_lib().as_debug_panel_time(_dt(W), kind, Wc.data_ptr(), W.stride(1), n, k0, nbp, src.data_ptr(),
                                     iters, dbg)
 
 
-_lib.as_debug_lu_trace.argtypes = [P, P, C.c_int]
-_lib.as_debug_lu_trace.restype = C.c_int
 
 
 def debug_lu_trace():
     """[(kind, block, start_us, end_us)] of the last LU factorization (AS_LU_TRACE=1), or None."""
     cap = 2048
     lo, hi = (C.c_ulonglong * cap)(), (C.c_ulonglong * cap)()
-    cnt = _lib.as_debug_lu_trace(lo, hi, cap)
+    cnt = debug_lib().as_debug_lu_trace(lo, hi, cap)
     if cnt <= 0:
         return None
     starts = [lo[i] for i in range(cnt) if lo[i] != 0xFFFFFFFFFFFFFFFF]
@@ -282,7 +305,7 @@ def debug_lu_trace():
 def debug_timestamps(raw: bool = False):
     """Phase stamps (ns, %globaltimer) of the last call, relative to the first stamp."""
     out = (C.c_ulonglong * 16)()
-    if _lib.as_debug_timestamps(out) != 0:
+    if debug_lib().as_debug_timestamps(out) != 0:
         return None
     v = list(out)
     if raw:
@@ -314,8 +337,8 @@ def last_kernel_nodes() -> int:
     return int(_lib.as_last_kernel_nodes())
 
 
-def workspace_bytes(dtype_code: int, n: int, nrhs: int) -> int:
-    return int(_lib.as_workspace_bytes(dtype_code, n, nrhs))
+def workspace_bytes(dtype_code: int, n: int, nrhs: int, opts: int = 0) -> int:
+    return int(_lib.as_workspace_bytes(dtype_code, n, nrhs, opts))
 
 
 def release_all() -> None:

@@ -10,6 +10,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libadaptsolve.so")
+# the same sources with -DAS_DEBUG: adds the test-only / diagnostic exports (as_debug_*) of
+# include/adaptsolve.h; loaded only by tests and tools, never by the solve, the bench or smoke()
+OUT_DEBUG = os.path.join(HERE, "libadaptsolve_debug.so")
+DEBUG_ONLY = {"api.cu"}   # the only translation unit whose exports change under AS_DEBUG
 BUILD = os.path.join(HERE, "build_obj")
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
@@ -28,9 +32,14 @@ def _deps_mtime():
     return max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC)) if os.path.isdir(CSRC) else 0
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    cmd = [NVCC] + COMMON + PER_FILE.get(src, []) + ["-c", os.path.join(CSRC, src), "-o", obj]
+def _obj(src: str, debug: bool = False) -> str:
+    return os.path.join(BUILD, src.replace(".cu", "_debug.o" if debug else ".o"))
+
+
+def _compile(src: str, verbose: bool, debug: bool = False) -> str:
+    obj = _obj(src, debug)
+    cmd = [NVCC] + COMMON + PER_FILE.get(src, []) + (["-DAS_DEBUG"] if debug else []) + \
+        ["-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -42,30 +51,36 @@ def _compile(src: str, verbose: bool) -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     hdr = os.path.join(HERE, "..", "include", "adaptsolve.h")
     newest = max(_deps_mtime(), os.path.getmtime(hdr))
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
+    if not force and all(os.path.exists(o) and os.path.getmtime(o) >= newest for o in (OUT, OUT_DEBUG)):
         return OUT
     os.makedirs(BUILD, exist_ok=True)
     # a source is recompiled when it, or any header, is newer than its object
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + [hdr]
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
 
-    def need(src: str) -> bool:
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    def need(src: str, debug: bool) -> bool:
+        obj = _obj(src, debug)
         if force or verbose or not os.path.exists(obj):
             return True
         return os.path.getmtime(obj) < max(newest_hdr, os.path.getmtime(os.path.join(CSRC, src)))
 
-    def one(src: str) -> str:
-        return _compile(src, verbose) if need(src) else os.path.join(BUILD, src.replace(".cu", ".o"))
+    def one(job) -> str:
+        src, debug = job
+        return _compile(src, verbose, debug) if need(src, debug) else _obj(src, debug)
 
-    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(one, sources()))
-    tmp = OUT + ".tmp"
-    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-lcuda"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
+    jobs = [(s, False) for s in sources()] + [(s, True) for s in sources() if s in DEBUG_ONLY]
+    # the largest translation units first (they bound the wall time)
+    jobs.sort(key=lambda j: -os.path.getsize(os.path.join(CSRC, j[0])))
+    with cf.ThreadPoolExecutor(max_workers=min(10, (os.cpu_count() or 4) + 2)) as ex:
+        objs = dict(zip(jobs, ex.map(one, jobs)))
+    for out, debug in ((OUT, False), (OUT_DEBUG, True)):
+        lst = [objs[(s, debug and s in DEBUG_ONLY)] for s in sources()]
+        tmp = out + ".tmp"
+        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + lst + ["-lcudart", "-lcuda"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, out)
     return OUT
 
 

@@ -69,6 +69,11 @@ __global__ void tri_prep_kernel(const DevArgs* args, int64_t lda, int64_t n, Dev
 
 __global__ void gate_kernel(DevState* st, cudaGraphConditionalHandle h_post) {
     if (threadIdx.x != 0) return;
+    if (st->flags & AS_FLAG_NONFINITE) {   // AS_OPT_CHECK_FINITE rejected the input (Z28): nothing runs
+        st->post = 0;
+        if (h_post) cudaGraphSetConditional(h_post, 0u);
+        return;
+    }
     const bool singular = st->info != ~0ull;
     if (singular) { st->flags |= AS_FLAG_SINGULAR; st->rcond = 0.0; }
     const double r = st->rcond;
@@ -270,6 +275,7 @@ static void body_solve(const Work& w, int m, SyncAlloc& sa, cudaStream_t s) {
 
 // ------------------------------------------------------------------ plans
 struct PlanKey {
+    uintptr_t stream;    // plans (and their workspaces) are per stream: concurrent streams never share one
     int dev, dtype;
     int64_t n, nrhs, lda, ldb;
     uint32_t opts;
@@ -279,8 +285,8 @@ struct PlanKey {
     int instrumented;
     int eager;
     bool operator<(const PlanKey& o) const {
-        return std::tie(dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps, instrumented, eager) <
-               std::tie(o.dev, o.dtype, o.n, o.nrhs, o.lda, o.ldb, o.opts, o.force, o.thr, o.cut, o.sweeps,
+        return std::tie(stream, dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps, instrumented, eager) <
+               std::tie(o.stream, o.dev, o.dtype, o.n, o.nrhs, o.lda, o.ldb, o.opts, o.force, o.thr, o.cut, o.sweeps,
                         o.instrumented, o.eager);
     }
 };
@@ -381,7 +387,8 @@ static int build_graph(Plan& P) {
         launch_state_init(w, s0, k.opts, k.force, k.thr, k.cut, k.sweeps);
         cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s0);
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[0], s0, cudaEventRecordExternal);
-        if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
+        if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0,
+                                                          (k.opts & AS_OPT_CHECK_FINITE) != 0);
         cudaGraphConditionalHandle h_method = make_handle(s0, 0);
         launch_dispatch(w, s0, h_method);
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[1], s0, cudaEventRecordExternal);
@@ -503,7 +510,8 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
     launch_state_init(w, s, k.opts, k.force, k.thr, k.cut, k.sweeps);
     cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s);
     if (k.instrumented) cudaEventRecord(P.ev[0], s);
-    if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0);
+    if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0,
+                                                      (k.opts & AS_OPT_CHECK_FINITE) != 0);
     launch_dispatch(w, s, 0);
     if (k.instrumented) cudaEventRecord(P.ev[1], s);
     int err = rd();
@@ -586,6 +594,7 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     if (!is_device_ptr(B)) return -5;
     if (!is_device_ptr(X)) return -8;
     PlanKey key{};
+    key.stream = (uintptr_t)stream;
     key.dev = dev; key.dtype = dt; key.n = n; key.nrhs = nrhs; key.lda = lda; key.ldb = ldb;
     const double eps = dt == AS_F64 ? 2.220446049250313080847e-16 : 1.1920928955078125e-07;
     key.opts = opt ? opt->flags : 0u;
@@ -594,6 +603,8 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
         if (key.force < AS_METHOD_BAND || key.force > AS_METHOD_LU) return -9;
     }
     if ((key.opts & AS_OPT_SKIP_DETECT) && (!(key.opts & AS_OPT_FORCE_METHOD) || key.force == AS_METHOD_BAND)) return -9;
+    // the finite check rides on the detection pass, which SKIP_DETECT removes
+    if ((key.opts & AS_OPT_SKIP_DETECT) && (key.opts & AS_OPT_CHECK_FINITE)) return -9;
     key.thr = (opt && opt->rcond_threshold >= 0) ? opt->rcond_threshold : 0.5 * eps;
     if (dt == AS_F32) key.thr = (double)(float)key.thr;
     key.cut = (opt && opt->lsq_cutoff >= 0) ? opt->lsq_cutoff : (double)n * eps;
@@ -633,9 +644,11 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     if (rep_host) *rep_host = P->rep_pinned->rep;
     {
         const as_report& r = P->rep_pinned->rep;
-        int64_t c = P->nodes_top + P->nodes_method[r.primary_method & 7];
+        // a Cholesky failure runs the LU body inside the CHOL body's IF branch (primary_method is then LU)
+        int64_t c = P->nodes_top;
         if (r.flags & AS_FLAG_CHOL_FAILED) c += P->nodes_method[AS_METHOD_CHOL] + P->nodes_chol_lu;
-        else if (r.primary_method == AS_METHOD_CHOL) c += P->nodes_chol_ok;
+        else if (r.primary_method == AS_METHOD_CHOL) c += P->nodes_method[AS_METHOD_CHOL] + P->nodes_chol_ok;
+        else c += P->nodes_method[r.primary_method & 7];
         if (r.flags & AS_FLAG_FALLBACK) c += P->nodes_fallback + (int64_t)r.sweeps * P->nodes_sweep;
         else if (!(P->rep_pinned->ret)) c += P->nodes_solve_hdr + P->nodes_solve[r.primary_method & 7];
         t_last_nodes = c;
@@ -655,6 +668,10 @@ __global__ void det_out_kernel(const DevState* st, as_structure* out, int fullsc
     if (threadIdx.x != 0) return;
     as_structure o;
     o.flags = st->alive;
+    // BANDED alive at the end means every tile was read: kl/ku are final, re-check the 25% rule on the pair
+    if ((o.flags & AS_FLAG_BANDED) && !band_density_ok(st->n, st->kl, st->ku)) o.flags &= ~AS_FLAG_BANDED;
+    o.nonfinite_seen = (st->flags & AS_FLAG_NONFINITE) ? 1 : 0;
+    o.reserved = 0;
     int m;
     if (o.flags & AS_FLAG_BANDED) m = AS_METHOD_BAND;
     else if (o.flags & AS_FLAG_LOWER) m = AS_METHOD_TRI_LOWER;
@@ -668,6 +685,11 @@ __global__ void det_out_kernel(const DevState* st, as_structure* out, int fullsc
     o.max_diag = dfrom(st->max_diag);
     *out = o;
 }
+
+// device staging for as_solve_host's A, B and X (X separate from B: an in-place solve would
+// exclude the speculative partitioned band path); freed by as_release_all
+static std::mutex g_host_mu;
+static std::map<std::tuple<int, int, int64_t, int64_t>, std::tuple<void*, void*, void*>> g_host_staging;
 
 }  // namespace as
 
@@ -719,13 +741,10 @@ int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void
     if (!X) return -8;
     const size_t es = dt == AS_F64 ? 8 : 4;
     cudaStream_t s = (cudaStream_t)stream;
-    static std::mutex mu;
-    // device staging for A, B and X (X separate from B: an in-place solve would exclude the
-    // speculative partitioned band path)
-    static std::map<std::tuple<int, int, int64_t, int64_t>, std::tuple<void*, void*, void*>> bufs;
+    auto& bufs = g_host_staging;
     int dev = 0;
     cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
+    std::lock_guard<std::mutex> lk(g_host_mu);
     auto key = std::make_tuple(dev, (int)dt, n, nrhs);
     auto it = bufs.find(key);
     if (it == bufs.end()) {
@@ -789,8 +808,9 @@ int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detec
     a.A = A;
     set_args_kernel2<<<1, 1, 0, s>>>(a, w.args);
     launch_state_init(w, s, detect_flags, 0, 0.0, 0.0, 30);
-    const bool fullscan = (detect_flags & AS_OPT_FULLSCAN) != 0;
-    launch_detect(w, s, fullscan);
+    const bool check_finite = (detect_flags & AS_OPT_CHECK_FINITE) != 0;
+    const bool fullscan = (detect_flags & AS_OPT_FULLSCAN) != 0 || check_finite;
+    launch_detect(w, s, fullscan, check_finite);
     det_out_kernel<<<1, 32, 0, s>>>(w.st, (as_structure*)w.cand, fullscan);
     as_structure h;
     int err = check(cudaMemcpyAsync(&h, w.cand, sizeof(h), cudaMemcpyDeviceToHost, s), "D2H structure");
@@ -800,6 +820,7 @@ int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detec
     return 0;
 }
 
+#ifdef AS_DEBUG
 // Test-only: the primary factorization alone (the same launchers the solve uses), eagerly on a
 // private workspace, factors copied out for the PA = LU / L L^T = A reconstruction tests.
 int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda, int64_t n, int64_t kl, int64_t ku,
@@ -842,10 +863,17 @@ int64_t as_debug_factor(as_dtype dt, int32_t method, const void* A, int64_t lda,
     return h.chol_failed ? h.chol_fail_col + 1 : 0;
 }
 
-int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs) {
+#endif  // AS_DEBUG
+
+int64_t as_workspace_bytes(as_dtype dt, int64_t n, int64_t nrhs, uint32_t opts) {
+    if ((dt != AS_F64 && dt != AS_F32) || n < 0 || nrhs < 0) return -1;
     Work w{};
     w.dtype = dt; w.n = n; w.nrhs = nrhs;
-    return (int64_t)layout(w, 0, nullptr);
+    int dev = 0;
+    w.num_sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    else cudaGetLastError();
+    return (int64_t)layout(w, opts, nullptr);
 }
 
 int64_t as_last_kernel_nodes(void) { return t_last_nodes; }
@@ -886,6 +914,7 @@ double as_bench_gemm(int dtype, int64_t M, int64_t N, int64_t K, int trans_b, in
     return 2.0 * (double)M * N * K * iters / (ms * 1e-3) / 1e12;
 }
 
+#ifdef AS_DEBUG
 double as_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n, int64_t k0, int nbp, const void* Wsrc,
                            int iters, int dbg) {
     if (!W || !Wsrc || n <= 0 || k0 < 0 || k0 >= n || nbp <= 0 || ldw < n || iters <= 0) return -1.0;
@@ -910,6 +939,8 @@ int as_debug_timestamps(unsigned long long* out16) {
     return 0;
 }
 
+#endif  // AS_DEBUG
+
 double as_measure_fp64_peak(int iters, void* stream) {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
@@ -929,9 +960,18 @@ int as_last_stage_ms(double* out4) {
 }
 
 void as_release_all(void) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    g_plans.clear();
-    g_det.clear();
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_plans.clear();
+        g_det.clear();
+    }
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    for (auto& kv : g_host_staging) {
+        cudaFree(std::get<0>(kv.second));
+        cudaFree(std::get<1>(kv.second));
+        cudaFree(std::get<2>(kv.second));
+    }
+    g_host_staging.clear();
 }
 
 const char* as_strerror(int code) {
@@ -940,6 +980,7 @@ const char* as_strerror(int code) {
     switch (code) {
     case AS_ERR_SINGULAR_NO_FALLBACK: return "matrix is exactly singular and the SVD fallback is disabled";
     case AS_ERR_SVD_NOT_CONVERGED: return "one-sided Jacobi SVD did not converge within max_sweeps";
+    case AS_ERR_NONFINITE: return "non-finite (NaN or Inf) input";
     case AS_ERR_NOT_IMPLEMENTED: return "not implemented";
     case AS_ERR_NO_DEVICE: return "no CUDA device";
     default: break;

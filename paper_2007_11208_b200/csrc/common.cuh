@@ -72,6 +72,18 @@ struct DevState {
     uint32_t pad3;
 };
 
+// The 25% rule of P:339 on the band capacity count(n,kl,ku) = n(kl+ku+1) - kl(kl+1)/2 - ku(ku+1)/2:
+// banded <=> 4 count <= n^2, exact in 64-bit integers (Z2, Z3)
+AS_HD bool band_density_ok(long long n, long long kl, long long ku) {
+    unsigned long long un = (unsigned long long)n;
+    unsigned long long cnt = un * (unsigned long long)(kl + ku + 1) - (unsigned long long)(kl * (kl + 1) / 2) -
+                             (unsigned long long)(ku * (ku + 1) / 2);
+    return 4ull * cnt <= un * un;
+}
+
+// IEEE finiteness without a library call: x - x is 0 for every finite x, NaN for NaN and +-Inf
+template <typename T> AS_HD bool is_finite_val(T x) { return x - x == T(0); }
+
 // orderable bits for non-negative doubles (IEEE bit pattern is monotone)
 AS_DEV unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
 AS_DEV double dfrom(unsigned long long b) { return __longlong_as_double((long long)b); }

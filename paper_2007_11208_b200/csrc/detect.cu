@@ -17,9 +17,6 @@
 
 namespace as {
 
-// ------------------------------------------------------------------ per-call args
-__global__ void set_args_kernel(DevArgs a, DevArgs* dst) { *dst = a; }
-
 // ------------------------------------------------------------------ state init
 __global__ void state_init_kernel(DevState* st, int64_t n, uint32_t opts, int force_method, double thr, double cut,
                                   int max_sweeps) {
@@ -43,8 +40,6 @@ __global__ void state_init_kernel(DevState* st, int64_t n, uint32_t opts, int fo
     s.band_dom = 3u;
     *st = s;
 }
-
-AS_DEV bool band_density_ok(long long n, long long kl, long long ku);
 
 // The far corner tile pair, (rows n-64.., cols 0..63) and its mirror, checked ahead of the pair
 // pass with every verdict that needs no diagonal value: non-zeros (UPPER / LOWER, kl / ku and the
@@ -93,8 +88,8 @@ __device__ void corner_pair(const T* A, int64_t lda, int64_t n, DevState* st) {
                           (__any_sync(0xffffffffu, unz) ? AS_FLAG_LOWER : 0u) |
                           (__any_sync(0xffffffffu, asym) ? AS_FLAG_SPD_CANDIDATE : 0u);
     if ((threadIdx.x & 31) == 0) {
-        int gkl = kl ? max(kl, atomicMax(&st->kl, kl)) : 0;
-        int gku = ku ? max(ku, atomicMax(&st->ku, ku)) : 0;
+        int gkl = kl ? max(kl, atomicMax(&st->kl, kl)) : *(volatile int*)&st->kl;
+        int gku = ku ? max(ku, atomicMax(&st->ku, ku)) : *(volatile int*)&st->ku;
         unsigned k2 = kill;
         if ((kl || ku) && !band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
         if (k2) atomicAnd(&st->alive, ~k2);
@@ -133,169 +128,10 @@ __global__ void detect_diag_kernel(const DevArgs* args, int64_t lda, int64_t n, 
     }
 }
 
-AS_DEV bool band_density_ok(long long n, long long kl, long long ku) {
-    unsigned long long un = (unsigned long long)n;
-    unsigned long long cnt = un * (unsigned long long)(kl + ku + 1) - (unsigned long long)(kl * (kl + 1) / 2) -
-                             (unsigned long long)(ku * (ku + 1) / 2);
-    return 4ull * cnt <= un * un;
-}
 
-// ------------------------------------------------------------------ pass 2: tile pairs
-// CTA = 256 threads = 8 warps.  Tile 64x64.  Lane l of warp w holds rows l and
-// l+32 of columns w, w+8, ..., w+56 of the lower tile (I,J) in registers; the
-// mirror tile (J,I) is staged in shared memory (padded, conflict-free
-// transposed reads).  Diagonal tiles (I==J) pair with themselves.
 constexpr int kDetThreads = 256;
-constexpr int kLD = kTile + 1;
 
-template <typename T>
-__global__ void __launch_bounds__(kDetThreads) detect_pairs_kernel(const DevArgs* args, int64_t lda, int64_t n,
-                                                                    DevState* st, const T* diag, int fullscan) {
-    __shared__ T up[kTile * kLD];
-    __shared__ unsigned s_pair;
-    __shared__ unsigned s_alive;
-    __shared__ int s_kl, s_ku;
-    __shared__ unsigned s_kill;
-    const T* A = (const T*)args->A;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long nt = (n + kTile - 1) / kTile;
-    const unsigned long long total = (unsigned long long)(nt * (nt + 1) / 2);
-    const T tol = T(100) * Eps<T>::v;                       // Fig. 4 line 5
-    const double maxd = dfrom(st->max_diag);                 // final after pass 1
-    const T max_diag = (T)maxd;                              // exact (it was a T value)
-    int my_kl = 0, my_ku = 0;                                // CTA-cached global maxima
-
-    for (;;) {
-        if (threadIdx.x == 0) {
-            unsigned al = *(volatile unsigned*)&st->alive;
-            s_alive = al;
-            s_pair = (fullscan || al) ? atomicAdd(&st->pair_ticket, 1u) : 0xffffffffu;
-            s_kl = 0; s_ku = 0; s_kill = 0;
-        }
-        __syncthreads();
-        const unsigned p = s_pair;
-        const unsigned alive = fullscan ? 0xFu : s_alive;
-        if (p >= total) break;
-        // pair index -> (I, J): distance-major, far pairs first
-        long long q = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5) + 1;
-        while (q * (q - 1) / 2 > (long long)p) --q;
-        while (q * (q + 1) / 2 <= (long long)p) ++q;
-        const long long D = nt - q;
-        const long long J = (long long)p - q * (q - 1) / 2;
-        const long long I = J + D;
-        const bool diag_tile = (D == 0);
-        const bool need_lower = fullscan || (alive & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
-        const bool need_upper = fullscan || diag_tile || (alive & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
-        const long long r0 = I * kTile, c0 = J * kTile;     // lower tile origin (rows I, cols J)
-        const int rows_lo = (int)min<long long>(kTile, n - r0), cols_lo = (int)min<long long>(kTile, n - c0);
-
-        // ---- stage the mirror tile (rows J, cols I) into smem: up[c' * kLD + r']
-        if (need_upper) {
-            const int rows_up = cols_lo, cols_up = rows_lo;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int c = warp + 8 * k;
-                if (c < cols_up) {
-                    const T* col = A + (c0) + (r0 + c) * lda;     // column (I*64 + c), rows J*64..
-                    up[c * kLD + lane] = lane < rows_up ? col[lane] : T(0);
-                    up[c * kLD + lane + 32] = lane + 32 < rows_up ? col[lane + 32] : T(0);
-                }
-            }
-        }
-        // ---- lower tile into registers
-        T lo0[8], lo1[8];
-        if (need_lower || diag_tile) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int c = warp + 8 * k;
-                const T* col = A + r0 + (c0 + c) * lda;
-                const bool cv = c < cols_lo;
-                lo0[k] = (cv && lane < rows_lo) ? col[lane] : T(0);
-                lo1[k] = (cv && lane + 32 < rows_lo) ? col[lane + 32] : T(0);
-            }
-        }
-        __syncthreads();
-
-        int kl_loc = 0, ku_loc = 0;
-        bool lower_nz = false, upper_nz = false, spd_dead = false;
-        const bool chk_spd = (alive & AS_FLAG_SPD_CANDIDATE) != 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int c = warp + 8 * k;
-            if (c >= cols_lo) continue;
-            const long long gj = c0 + c;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = lane + 32 * h;
-                if (r >= rows_lo) continue;
-                const long long gi = r0 + r;
-                const T a = h ? lo1[k] : lo0[k];   // A(gi, gj)
-                if (gi > gj) {
-                    // mirror b = A(gj, gi) = up tile element (row r' = c, col c' = r)
-                    const T b = need_upper ? up[r * kLD + c] : T(0);
-                    const int dist = (int)(gi - gj);
-                    if (a != T(0)) { lower_nz = true; kl_loc = max(kl_loc, dist); }
-                    if (b != T(0)) { upper_nz = true; ku_loc = max(ku_loc, dist); }
-                    if (chk_spd) {
-                        const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
-                        const T delta = (a - b) < T(0) ? -(a - b) : (a - b);          // line 12
-                        const T m = aa > ab ? aa : ab;
-                        if (delta > tol && delta > tol * m) spd_dead = true;           // lines 13-14
-                        if (aa >= max_diag) spd_dead = true;                            // line 15
-                        const T lhs = aa + ab;
-                        const T rhs = diag[gi] + diag[gj];
-                        if (lhs >= rhs) spd_dead = true;                                // line 16
-                    }
-                } else if (gi < gj && diag_tile) {
-                    // strictly-upper element of a diagonal tile (its pair is handled from the lower side)
-                    if (a != T(0)) { upper_nz = true; ku_loc = max(ku_loc, (int)(gj - gi)); }
-                }
-            }
-        }
-        // ---- reduce within the CTA
-        kl_loc = __reduce_max_sync(0xffffffffu, kl_loc);
-        ku_loc = __reduce_max_sync(0xffffffffu, ku_loc);
-        const unsigned kill = (__any_sync(0xffffffffu, lower_nz) ? AS_FLAG_UPPER : 0u) |
-                              (__any_sync(0xffffffffu, upper_nz) ? AS_FLAG_LOWER : 0u) |
-                              (__any_sync(0xffffffffu, spd_dead) ? AS_FLAG_SPD_CANDIDATE : 0u);
-        if (lane == 0) {
-            if (kl_loc) atomicMax(&s_kl, kl_loc);
-            if (ku_loc) atomicMax(&s_ku, ku_loc);
-            if (kill) atomicOr(&s_kill, kill);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int gkl = my_kl, gku = my_ku;
-            if (s_kl > my_kl) gkl = max(s_kl, atomicMax(&st->kl, s_kl));
-            if (s_ku > my_ku) gku = max(s_ku, atomicMax(&st->ku, s_ku));
-            my_kl = gkl; my_ku = gku;
-            unsigned k2 = s_kill;
-            if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
-            if (k2 & alive) atomicAnd(&st->alive, ~k2);
-        }
-        // (thread 0 is the only reader of my_kl/my_ku)
-        __syncthreads();
-    }
-}
-
-// ------------------------------------------------------------------ pass 2 (v2): pipelined tile pairs
-// Persistent CTAs (one per SM) stream tile pairs through a 2-stage cp.async
-// pipeline into padded shared memory; while pair k is checked, pair k+G is in
-// flight.  Elements are visited along skewed diagonals (lane l, step d:
-// row l, column (l+d) mod 64) so that both the tile read and the transposed
-// mirror read are shared-memory bank-conflict free with a 16-byte aligned
-// padded leading dimension (66 doubles / 68 floats).
-template <typename T> struct DetLD;
-template <> struct DetLD<double> { static constexpr int v = 66; };
-template <> struct DetLD<float> { static constexpr int v = 68; };
-
-AS_DEV void cp_async_bytes(void* smem, const void* gmem, int chunk, int src_bytes) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    if (chunk == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
-    else if (chunk == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
-    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
-}
-
+// pair index -> (I, J): distance-major, far-from-diagonal pairs first
 AS_DEV void pair_of(unsigned p, long long nt, long long& I, long long& J) {
     long long q = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5) + 1;
     while (q * (q - 1) / 2 > (long long)p) --q;
@@ -303,146 +139,6 @@ AS_DEV void pair_of(unsigned p, long long nt, long long& I, long long& J) {
     const long long D = nt - q;
     J = (long long)p - q * (q - 1) / 2;
     I = J + D;
-}
-
-// stage a 64x64 tile (rows rr.., cols cc..) into smem column-major with leading dimension LD
-template <typename T>
-AS_DEV void stage_tile(T* dst, const T* A, int64_t lda, int64_t n, long long rr, long long cc, int chunk_bytes) {
-    constexpr int LD = DetLD<T>::v;
-    const int per = chunk_bytes / (int)sizeof(T);          // elements per chunk
-    const int cpc = kTile / per;                            // chunks per column
-    for (int e = threadIdx.x; e < kTile * cpc; e += blockDim.x) {
-        const int c = e / cpc, r = (e % cpc) * per;
-        const long long gr = rr + r, gc = cc + c;
-        int bytes = 0;
-        if (gc < n && gr < n) bytes = (int)(min<long long>(per, n - gr) * sizeof(T));
-        const T* src = bytes ? A + gr + gc * lda : A;
-        cp_async_bytes(dst + c * LD + r, src, chunk_bytes, bytes);
-    }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kDetThreads, 1) detect_pairs_v2(const DevArgs* args, int64_t lda, int64_t n,
-                                                                   DevState* st, const T* diag, int fullscan) {
-    constexpr int LD = DetLD<T>::v;
-    constexpr int TILE = kTile * LD;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* buf = (T*)smem_raw;                 // [stage][lower, upper][TILE]
-    __shared__ unsigned s_alive[2];
-    __shared__ int s_kl, s_ku;
-    __shared__ unsigned s_kill;
-    const T* A = (const T*)args->A;
-    // 16-byte chunks when every column start is 16-byte aligned, else element-wise
-    const int chunk_bytes = (((uintptr_t)A & 15) == 0 && ((lda * (int64_t)sizeof(T)) & 15) == 0) ? 16 : (int)sizeof(T);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long nt = (n + kTile - 1) / kTile;
-    const unsigned total = (unsigned)(nt * (nt + 1) / 2);
-    const T tol = T(100) * Eps<T>::v;                       // Fig. 4 line 5
-    const T max_diag = (T)dfrom(st->max_diag);
-    const unsigned G = gridDim.x;
-    int my_kl = 0, my_ku = 0;
-
-    auto issue = [&](int stage, unsigned p, unsigned alive) {
-        long long I, J;
-        pair_of(p, nt, I, J);
-        const bool diag_tile = (I == J);
-        const bool need_lower = diag_tile || (alive & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
-        const bool need_upper = !diag_tile && (alive & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
-        T* lo = buf + (stage * 2 + 0) * TILE;
-        T* up = buf + (stage * 2 + 1) * TILE;
-        if (need_lower) stage_tile<T>(lo, A, lda, n, I * kTile, J * kTile, chunk_bytes);
-        if (need_upper) stage_tile<T>(up, A, lda, n, J * kTile, I * kTile, chunk_bytes);
-    };
-
-    unsigned p = blockIdx.x;
-    if (threadIdx.x == 0) s_alive[0] = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
-    __syncthreads();
-    if (p >= total || s_alive[0] == 0) return;
-    issue(0, p, s_alive[0]);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    int cur = 0;
-    for (;;) {
-        // decide and issue the next pair
-        if (threadIdx.x == 0) {
-            s_alive[cur ^ 1] = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
-            s_kl = 0; s_ku = 0; s_kill = 0;
-        }
-        __syncthreads();
-        const unsigned pn = p + G;
-        const bool next_ok = pn < total && s_alive[cur ^ 1] != 0;
-        if (next_ok) issue(cur ^ 1, pn, s_alive[cur ^ 1]);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-        // ---- check pair p on stage cur
-        {
-            const unsigned alive = s_alive[cur];
-            long long I, J;
-            pair_of(p, nt, I, J);
-            const bool diag_tile = (I == J);
-            const bool have_lower = diag_tile || (alive & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
-            const bool have_upper = !diag_tile && (alive & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
-            const bool chk_spd = (alive & AS_FLAG_SPD_CANDIDATE) != 0;
-            const T* lo = buf + (cur * 2 + 0) * TILE;
-            const T* up = diag_tile ? lo : buf + (cur * 2 + 1) * TILE;
-            const long long r0 = I * kTile, c0 = J * kTile;
-            const int r = 32 * (warp & 1) + lane;
-            const int dbase = 16 * (warp >> 1);
-            int kl_loc = 0, ku_loc = 0;
-            bool lower_nz = false, upper_nz = false, spd_dead = false;
-            const long long gi = r0 + r;
-            const T di = (chk_spd && gi < n) ? diag[gi] : T(0);
-#pragma unroll 4
-            for (int dd = 0; dd < 16; ++dd) {
-                const int c = (r + dbase + dd) & (kTile - 1);
-                const long long gj = c0 + c;
-                if (gi >= n || gj >= n) continue;
-                const T a = have_lower ? lo[c * LD + r] : T(0);          // A(gi, gj)
-                if (gi > gj) {
-                    const T b = have_upper || diag_tile ? up[r * LD + c] : T(0);   // A(gj, gi)
-                    const int dist = (int)(gi - gj);
-                    if (a != T(0)) { lower_nz = true; kl_loc = max(kl_loc, dist); }
-                    if (b != T(0)) { upper_nz = true; ku_loc = max(ku_loc, dist); }
-                    if (chk_spd) {
-                        const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
-                        const T df = a - b;
-                        const T delta = df < T(0) ? -df : df;                        // line 12
-                        const T m = aa > ab ? aa : ab;
-                        if (delta > tol && delta > tol * m) spd_dead = true;         // lines 13-14
-                        if (aa >= max_diag) spd_dead = true;                          // line 15
-                        if (aa + ab >= di + diag[gj]) spd_dead = true;               // line 16
-                    }
-                } else if (gi < gj && diag_tile) {
-                    if (a != T(0)) { upper_nz = true; ku_loc = max(ku_loc, (int)(gj - gi)); }
-                }
-            }
-            kl_loc = __reduce_max_sync(0xffffffffu, kl_loc);
-            ku_loc = __reduce_max_sync(0xffffffffu, ku_loc);
-            const unsigned kill = (__any_sync(0xffffffffu, lower_nz) ? AS_FLAG_UPPER : 0u) |
-                                  (__any_sync(0xffffffffu, upper_nz) ? AS_FLAG_LOWER : 0u) |
-                                  (__any_sync(0xffffffffu, spd_dead) ? AS_FLAG_SPD_CANDIDATE : 0u);
-            if (lane == 0) {
-                if (kl_loc) atomicMax(&s_kl, kl_loc);
-                if (ku_loc) atomicMax(&s_ku, ku_loc);
-                if (kill) atomicOr(&s_kill, kill);
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int gkl = my_kl, gku = my_ku;
-                if (s_kl > my_kl) gkl = max(s_kl, atomicMax(&st->kl, s_kl));
-                if (s_ku > my_ku) gku = max(s_ku, atomicMax(&st->ku, s_ku));
-                my_kl = gkl; my_ku = gku;
-                unsigned k2 = s_kill;
-                if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
-                if (k2 & alive) atomicAnd(&st->alive, ~k2);
-            }
-        }
-        __syncthreads();   // stage cur is free again
-        if (!next_ok) break;
-        p = pn;
-        cur ^= 1;
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ pass 2 (v3): register-direct tile pairs
@@ -491,7 +187,8 @@ AS_DEV void load_tile_regs(T (&v)[16], const T* A, int64_t lda, int64_t n, long 
 
 template <typename T>
 __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs* args, int64_t lda, int64_t n,
-                                                                DevState* st, const T* diag, int fullscan) {
+                                                                DevState* st, const T* diag, int fullscan,
+                                                                int check_finite) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* lo_s = (T*)smem_raw;            // kTile x kLD3 (only used for the sympd pass)
     T* up_s = lo_s + kTile * kLD3;
@@ -531,7 +228,9 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
                 const unsigned pn = p + gridDim.x;
                 const bool has_next = pn < total;
                 if (has_next) load(pn, nxt);
-                if (threadIdx.x == 0) s_alive = *(volatile unsigned*)&st->alive;
+                // the early-exit decision travels through the barrier's reduction itself (no shared
+                // word that the next iteration's write could race with a slow warp's read)
+                const bool gone = threadIdx.x == 0 && *(volatile unsigned*)&st->alive == 0u;
                 long long I, J;
                 pair_of(p, nt, I, J);
                 bool nz = false;
@@ -541,11 +240,12 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
                     // diagonal tile: only the strict lower (UPPER candidate) / strict upper part counts
                     nz |= cur[i] != T(0) && (I != J || (up_only ? r > c : c > r));
                 }
-                if (__syncthreads_or(nz)) {
+                const int v = __syncthreads_or((nz ? 1 : 0) | (gone ? 2 : 0));
+                if (v & 1) {
                     if (threadIdx.x == 0) atomicAnd(&st->alive, ~known);
                     return;
                 }
-                if (s_alive == 0u || !has_next) return;
+                if ((v & 2) || !has_next) return;
                 p = pn;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
@@ -581,6 +281,14 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
         else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) up[i] = T(0);
+        }
+        if (check_finite) {
+            // AS_OPT_CHECK_FINITE (Z28): every element of A passes through here exactly once in the full
+            // scan (out-of-range lanes hold 0); one flag, no effect on the four verdicts
+            bool bad = false;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) bad |= !is_finite_val(lo[i]) || !is_finite_val(up[i]);
+            if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&st->flags, AS_FLAG_NONFINITE);
         }
         if (threadIdx.x == 0) {
             s_alive = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
@@ -672,6 +380,12 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
             int gkl = my_kl, gku = my_ku;
             if (s_kl > my_kl) gkl = max(s_kl, atomicMax(&st->kl, s_kl));
             if (s_ku > my_ku) gku = max(s_ku, atomicMax(&st->ku, s_ku));
+            // the other CTAs' extents count too (the 25% rule is on the pair (kl, ku)); the final
+            // verdict is re-checked on the exact extents by the dispatch
+            if (s_kl > 0 || s_ku > 0) {
+                gkl = max(gkl, *(volatile int*)&st->kl);
+                gku = max(gku, *(volatile int*)&st->ku);
+            }
             my_kl = gkl; my_ku = gku;
             unsigned k2 = s_kill;
             if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
@@ -686,10 +400,14 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
 // else general LU; or the forced method.  Sets the SWITCH handle.
 __global__ void dispatch_kernel(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
     if (threadIdx.x != 0) return;
-    const unsigned f = (st->opts & AS_OPT_SKIP_DETECT) ? 0u : st->alive;   // detection skipped: no verdicts
+    unsigned f = (st->opts & AS_OPT_SKIP_DETECT) ? 0u : st->alive;   // detection skipped: no verdicts
+    // BANDED still alive means no CTA exited early, so kl/ku are the exact extents: the 25% rule on the
+    // final pair (two extents raised by different CTAs may each pass alone, Z2/Z3)
+    if ((f & AS_FLAG_BANDED) && !band_density_ok(st->n, st->kl, st->ku)) f &= ~AS_FLAG_BANDED;
     st->det_flags = f;
     int m;
-    if (st->opts & AS_OPT_FORCE_METHOD) m = st->force_method;
+    if (st->flags & AS_FLAG_NONFINITE) { m = AS_METHOD_NONE; st->ret = AS_ERR_NONFINITE; }   // Z28
+    else if (st->opts & AS_OPT_FORCE_METHOD) m = st->force_method;
     else if (f & AS_FLAG_BANDED) m = AS_METHOD_BAND;
     else if (f & AS_FLAG_LOWER) m = AS_METHOD_TRI_LOWER;
     else if (f & AS_FLAG_UPPER) m = AS_METHOD_TRI_UPPER;
@@ -707,7 +425,19 @@ void launch_state_init(const Work& w, cudaStream_t s, uint32_t opts, int force_m
     cudaMemsetAsync(w.bars, 0, sizeof(unsigned) * w.bars_len, s);
 }
 
-void launch_detect(const Work& w, cudaStream_t s, bool fullscan) {
+// AS_OPT_CHECK_FINITE: B (n x nrhs, ld ldb) scanned once for NaN/Inf (Z28)
+template <typename T>
+__global__ void finite_b_kernel(const DevArgs* args, int64_t ldb, int64_t n, int64_t nrhs, DevState* st) {
+    const T* B = (const T*)args->B;
+    if (!B) return;                       // as_detect: no right-hand sides
+    bool bad = false;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * nrhs; e += (int64_t)gridDim.x * blockDim.x)
+        bad |= !is_finite_val(B[e % n + (e / n) * ldb]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&st->flags, AS_FLAG_NONFINITE);
+}
+
+void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite) {
+    fullscan = fullscan || check_finite;
     const int dthreads = 256;
     const int dblocks = (int)std::min<int64_t>((w.n + dthreads - 1) / dthreads, 4 * w.num_sms);
     const long long nt = (w.n + kTile - 1) / kTile;
@@ -718,14 +448,20 @@ void launch_detect(const Work& w, cudaStream_t s, bool fullscan) {
         cudaFuncSetAttribute(detect_pairs_v3<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<double><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (double*)w.diag);
         detect_pairs_v3<double><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
-                                                                              (const double*)w.diag, fullscan);
+                                                                              (const double*)w.diag, fullscan,
+                                                                              check_finite);
+        if (check_finite && w.nrhs > 0 && w.ldb >= w.n)
+            finite_b_kernel<double><<<w.num_sms * 2, 256, 0, s>>>(w.args, w.ldb, w.n, w.nrhs, w.st);
     } else {
         const int smem = (int)(sizeof(float) * 2 * kTile * kLD3);
         const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 4);
         cudaFuncSetAttribute(detect_pairs_v3<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<float><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (float*)w.diag);
         detect_pairs_v3<float><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
-                                                                             (const float*)w.diag, fullscan);
+                                                                             (const float*)w.diag, fullscan,
+                                                                             check_finite);
+        if (check_finite && w.nrhs > 0 && w.ldb >= w.n)
+            finite_b_kernel<float><<<w.num_sms * 2, 256, 0, s>>>(w.args, w.ldb, w.n, w.nrhs, w.st);
     }
 }
 

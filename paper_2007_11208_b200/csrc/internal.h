@@ -47,7 +47,7 @@ struct Work {
 // launchers (each enqueues on `s`; used while capturing the plan's graph)
 void launch_state_init(const Work& w, cudaStream_t s, uint32_t opts, int force_method, double thr, double cut,
                        int max_sweeps);
-void launch_detect(const Work& w, cudaStream_t s, bool fullscan);
+void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite = false);
 void launch_dispatch(const Work& w, cudaStream_t s, cudaGraphConditionalHandle h_method);
 void launch_copy_b_to_x(const Work& w, cudaStream_t s);   // band.cu
 

@@ -379,6 +379,7 @@ __global__ void sigma_kernel(const T* M, int64_t ldw, int64_t n, T* sig, DevStat
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     double best = 0.0;
+    bool bad = false;
     for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n; k += warps) {
         T s = T(0);
         for (int64_t i = lane; i < n; i += 32) { const T x = M[i + k * ldw]; s += x * x; }
@@ -386,8 +387,11 @@ __global__ void sigma_kernel(const T* M, int64_t ldw, int64_t n, T* sig, DevStat
         const T sg = sqrt(s);
         if (lane == 0) sig[k] = sg;
         if ((double)sg > best) best = (double)sg;
+        bad |= !is_finite_val(sg);
     }
     if (lane == 0 && best > 0.0) atomicMax(&st->smax_bits, dbits(best));
+    // non-finite input reached the SVD: the minimum-norm solution is undefined (Z29)
+    if (lane == 0 && bad) atomicOr(&st->flags, AS_FLAG_NONFINITE);
 }
 
 // rank and the optional descending copy of sigma (rank-based placement, stable)
@@ -435,6 +439,7 @@ __global__ void svd_done_kernel(DevState* st) {
     if (threadIdx.x != 0) return;
     st->flags |= AS_FLAG_FALLBACK;
     st->method = AS_METHOD_SVD;
+    if (st->flags & AS_FLAG_NONFINITE) { st->rank = -1; st->ret = AS_ERR_NONFINITE; return; }   // Z29
     if (st->rank < 0) st->rank = 0;
     if (st->rank < st->n) st->flags |= AS_FLAG_RANK_DEF;
     if (!st->svd_conv) { st->flags |= AS_FLAG_SVD_NOCONV; st->ret = AS_ERR_SVD_NOT_CONVERGED; }

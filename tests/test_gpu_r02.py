@@ -1,0 +1,177 @@
+"""GPU parity, round 2: the LU paths the large configs really take, full-size references for
+C4 / C5 / C5f (committed oracle results, tools/oracle_refs.py), non-finite input, the 25% rule on
+two far extents, and the Jacobi sweep cap.
+
+Bars as in test_gpu_parity.py (north star, Z18-Z21, Z28-Z29)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from helpers import backward_error, forward_diff
+from test_gpu_parity import check_parity, gpu_solve
+
+pytestmark = pytest.mark.gpu
+
+AS = pytest.importorskip("paper_2007_11208_b200") if torch.cuda.is_available() else None
+REFS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "refs")
+MASK = 0xFF | oracle.F_CHOL_FAILED | oracle.F_SINGULAR | oracle.F_RCOND_LOW | oracle.F_FALLBACK | \
+    oracle.F_POORLY_COND | oracle.F_NONFINITE | oracle.F_SVD_NOCONV
+
+
+def _ref(tag):
+    p = os.path.join(REFS, f"{tag}.npz")
+    if not os.path.exists(p):
+        pytest.fail(f"missing {p}: run tools/oracle_refs.py {tag}")
+    return np.load(p)
+
+
+# ------------------------------------------------------------------ LU: cooperative panel + look-ahead sizes
+@pytest.mark.parametrize("n,nrhs", [(1600, 8), (2048, 17), (3000, 33), (4096, 32)])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_lu_mid_sizes_vs_oracle(n, nrhs, fp32):
+    """n > 1536 runs the cooperative panel (lu.cu) and n >= 2048 the look-ahead stream: graded
+    element-wise against the oracle (phi <= 1e-15 cond_1, fp32: 1e-6 cond_1 vs the fp64 oracle on
+    the promoted data), plus the gate bit."""
+    A, B = W.make("C5", n=n, nrhs=nrhs, seed=n)
+    if fp32:
+        A, B = np.asfortranarray(A.astype(np.float32)), np.asfortranarray(B.astype(np.float32))
+    rep, orep = check_parity(A, B, fp32=fp32, no_fallback=True)
+    assert rep["primary_method"] == oracle.M_LU
+
+
+# ------------------------------------------------------------------ full-size configs against committed references
+def test_config_c5_full_size_vs_oracle():
+    """C5 (n=16384, 32 RHS): X against the oracle's X (computed once per input hash by
+    tools/oracle_refs.py, which calls only oracle/): eta <= 1e-13, phi <= 1e-15 cond_1, flags."""
+    ref = _ref("C5")
+    A, B = W.make("C5")
+    assert W.sha256(A, B) == str(ref["sha256"])
+    ret, X, rep = gpu_solve(A, B)
+    assert ret == int(ref["ret"]) == 0
+    assert (rep["flags"] & MASK) == (int(ref["flags"]) & MASK), (hex(rep["flags"]), hex(int(ref["flags"])))
+    assert rep["method"] == int(ref["method"]) == oracle.M_LU
+    cond = float(ref["anorm"]) / float(ref["rcond"])
+    assert abs(np.log2(rep["rcond"] / float(ref["rcond"]))) <= 1.0
+    assert backward_error(A, X, B) <= 1e-13
+    assert forward_diff(X, ref["X"]) <= 1e-15 * cond, (forward_diff(X, ref["X"]), cond)
+
+
+def test_config_c5f_full_size_vs_oracle():
+    """C5f (C5 rounded to fp32, NO_FALLBACK, Z21): gate-bit parity with the fp32 oracle unless either
+    rcond is within 10% of the threshold; X against the fp64 oracle on the promoted data:
+    eta <= 1e-5, phi <= 1e-6 cond_1."""
+    ref = _ref("C5f")
+    A, B = W.make("C5f")
+    assert W.sha256(A, B) == str(ref["sha256"])
+    ret, X, rep = gpu_solve(A, B, no_fallback=True)
+    assert ret == 0 == int(ref["ret32"])
+    assert (rep["flags"] & 0xFF) == (int(ref["flags32"]) & 0xFF)
+    thr = 2.0 ** -24
+    knife = any(abs(r / thr - 1.0) <= 0.1 for r in (rep["rcond"], float(ref["rcond32"])))
+    if not knife:
+        assert (rep["flags"] & oracle.F_RCOND_LOW) == (int(ref["flags32"]) & oracle.F_RCOND_LOW)
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    cond = float(ref["anorm"]) / float(ref["rcond"])
+    assert backward_error(A64, X, B64) <= 1e-5
+    assert forward_diff(X, ref["X"]) <= 1e-6 * cond
+
+
+def test_config_c4_full_size_vs_oracle():
+    """C4 (n=1024): gate + fallback bits, singular values against the oracle's (same A, so the
+    rounding of A's formation cancels) and against the closed form (both <= 1e-13), rank = oracle's
+    +-1, residual rho within 1% of the oracle's."""
+    ref = _ref("C4")
+    n = 1024
+    A, B, U, sigma, V = W.illcond_c4(n=n)
+    assert W.sha256(A, B) == str(ref["sha256"])
+    sig = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ret, Xd, rep = AS.as_solve_ex(AS.to_device(A), AS.to_device(B), sigma_out=sig)
+    torch.cuda.synchronize()
+    X = AS.to_host(Xd)
+    assert ret == int(ref["ret"]) == 0
+    assert (rep["flags"] & MASK) == (int(ref["flags"]) & MASK)
+    assert rep["method"] == oracle.M_SVD and rep["primary_method"] == oracle.M_LU
+    s = sig.cpu().numpy()
+    assert np.abs(s - ref["sigma"]).max() <= 1e-13, np.abs(s - ref["sigma"]).max()
+    assert np.abs(s - sigma).max() <= 1e-13, np.abs(s - sigma).max()
+    assert abs(rep["rank"] - int(ref["rank"])) <= 1
+    b = B[:, 0]
+    rho = np.linalg.norm(b - A @ X[:, 0]) / np.linalg.norm(b)
+    rho_or = np.linalg.norm(b - A @ ref["X"][:, 0]) / np.linalg.norm(b)
+    assert abs(rho - rho_or) <= 1e-2 * rho_or, (rho, rho_or)
+
+
+def test_svd_sweep_cap_not_converged():
+    """max_sweeps = 1 on an ill-conditioned system: both sides report SVD_NOT_CONVERGED (+2) after
+    exactly one sweep (the cap of Z16)."""
+    A, B, *_ = W.illcond_c4(n=96)
+    ret, X, rep = gpu_solve(A, B, max_sweeps=1)
+    oret, Xo, orep, _ = oracle.solve(A, B, max_sweeps=1)
+    assert ret == oret == oracle.ERR_SVD_NOT_CONVERGED
+    assert (rep["flags"] & MASK) == (orep["flags"] & MASK)
+    assert rep["flags"] & oracle.F_SVD_NOCONV and rep["sweeps"] == orep["sweeps"] == 1
+
+
+# ------------------------------------------------------------------ non-finite input (Z28, Z29)
+@pytest.mark.parametrize("where", ["A", "B"])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_check_finite(where, bad, fp32):
+    for n, i, j in ((40, 7, 31), (300, 299, 0), (300, 150, 151)):
+        A, B = W.make("C1", n=n, nrhs=2, seed=n)
+        if fp32:
+            A, B = np.asfortranarray(A.astype(np.float32)), np.asfortranarray(B.astype(np.float32))
+        (A if where == "A" else B)[i, j % B.shape[1] if where == "B" else j] = bad
+        ret, _, rep = gpu_solve(A, B, check_finite=True)
+        oret, _, orep, _ = oracle.solve(A, B, check_finite=True)
+        assert ret == oret == AS.ERR_NONFINITE
+        assert (rep["flags"] & MASK) == (orep["flags"] & MASK), (hex(rep["flags"]), hex(orep["flags"]))
+        assert rep["method"] == 0
+        if where == "A":
+            _, st = AS.as_detect(AS.to_device(A), check_finite=True)
+            assert st["nonfinite_seen"] == 1
+
+
+def test_check_finite_clean_input_unchanged():
+    """A finite input solves identically with and without CHECK_FINITE (same flags, same X bits)."""
+    for tag, kw in (("C1", {}), ("C2", dict(n=2000, nrhs=2)), ("C3a", dict(n=300, nrhs=3))):
+        A, B = W.make(tag, **kw)
+        r0, X0, rep0 = gpu_solve(A, B)
+        r1, X1, rep1 = gpu_solve(A, B, check_finite=True)
+        assert r0 == r1 == 0 and rep0["flags"] == rep1["flags"]
+        assert np.array_equal(X0, X1)
+        _, st = AS.as_detect(AS.to_device(A), check_finite=True)
+        assert st["nonfinite_seen"] == 0
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_nonfinite_reaching_svd(bad):
+    A = np.asfortranarray(np.array([[4.0, 1.0, 0.5], [1.0, bad, 2.0], [0.5, 1.0, 3.0]]))
+    B = np.asfortranarray(np.array([[1.0], [2.0], [3.0]]))
+    ret, _, rep = gpu_solve(A, B)
+    oret, _, orep, _ = oracle.solve(A, B)
+    assert ret == oret == AS.ERR_NONFINITE
+    assert (rep["flags"] & MASK) == (orep["flags"] & MASK)
+    assert rep["rank"] == orep["rank"] == -1
+
+
+# ------------------------------------------------------------------ 25% rule on extents raised by different tile pairs
+@pytest.mark.parametrize("n,far", [(1024, (300, 20, 10, 210)), (2000, (1500, 1000, 0, 400)), (700, (600, 450, 5, 105))])
+def test_density_two_far_extents(n, far):
+    """A lone far sub-diagonal and a lone far super-diagonal element in different tile pairs: each
+    extent alone passes the 25% rule, together they do not (Z2/Z3) -> not banded."""
+    i1, j1, i2, j2 = far
+    A = np.asfortranarray(np.eye(n) * 3.0)
+    A[i1, j1] = 0.5
+    A[i2, j2] = 0.25
+    d = oracle.detect(A)
+    assert not d.banded and d.kl == max(i1 - j1, 0) and d.ku == max(j2 - i2, 0)
+    for fullscan in (False, True):
+        _, st = AS.as_detect(AS.to_device(A), fullscan=fullscan)
+        assert st["flags"] == d.flags, (st, d.flags)
+    B = np.asfortranarray(np.ones((n, 1)))
+    check_parity(A, B)

@@ -9,11 +9,25 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HDR = os.path.join(ROOT, "include", "adaptsolve.h")
 LIB = os.path.join(ROOT, "paper_2007_11208_b200", "libadaptsolve.so")
+DEBUG_LIB = os.path.join(ROOT, "paper_2007_11208_b200", "libadaptsolve_debug.so")
+_DECL = r"^\s*(?:int|int64_t|void|double|const char\*)\s+\**(as_\w+)\s*\("
+
+
+def _split_header():
+    src = open(HDR).read()
+    a = src.index("#ifdef AS_DEBUG")
+    b = src.index("#endif /* AS_DEBUG */")
+    return src[:a] + src[b:], src[a:b]
 
 
 def declared():
-    src = open(HDR).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+\**(as_\w+)\s*\(", src, re.M)))
+    """Symbols of the release boundary (outside the AS_DEBUG block)."""
+    return sorted(set(re.findall(_DECL, _split_header()[0], re.M)))
+
+
+def declared_debug():
+    """Test-only symbols declared inside #ifdef AS_DEBUG."""
+    return sorted(set(re.findall(_DECL, _split_header()[1], re.M)))
 
 
 def test_header_declares_boundary():
@@ -39,6 +53,21 @@ def test_binding_names_match_header():
     import paper_2007_11208_b200 as AS
     for name in declared():
         assert name in AS.EXPORTS
+    assert sorted(AS.DEBUG_EXPORTS) == declared_debug()
+
+
+def test_debug_exports_only_in_debug_build():
+    """the test-only exports exist only in the -DAS_DEBUG build."""
+    if not os.path.exists(DEBUG_LIB):
+        import __graft_entry__
+        __graft_entry__.build()
+    rel, dbg = ctypes.CDLL(LIB), ctypes.CDLL(DEBUG_LIB)
+    assert declared_debug(), "no AS_DEBUG block in the header"
+    for name in declared_debug():
+        assert not hasattr(rel, name), name
+        assert hasattr(dbg, name), name
+    for name in declared():
+        assert hasattr(dbg, name), name
 
 
 def test_sm100a_sass_present():
@@ -57,3 +86,6 @@ def test_workspace_bytes_cpu():
     import paper_2007_11208_b200 as AS
     b = AS.workspace_bytes(0, 1024, 1)
     assert b > 8 * 1024 * 1024
+    # FORCE_METHOD reserves a band factor of any width (3n rows of W)
+    assert AS.workspace_bytes(0, 1024, 1, AS.OPT_FORCE_METHOD) > b
+    assert AS.workspace_bytes(0, -1, 1) == -1 and AS.workspace_bytes(7, 8, 1) == -1

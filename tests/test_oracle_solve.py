@@ -392,3 +392,54 @@ def test_float32_solve():
     assert backward_error(A32, X, B32) < 1e-6
     _, X64, _, _ = oracle.solve(A32.astype(np.float64), B32.astype(np.float64))
     assert forward_diff(X, X64) < 1e-6 / rep["rcond"]
+
+
+# ------------------------------------------------------------------ non-finite input (Z28/Z29)
+@pytest.mark.parametrize("seed", range(8))
+def test_check_finite_matches_isfinite(seed):
+    """CHECK_FINITE rejects exactly the inputs numpy's isfinite() rejects (NaN, +Inf, -Inf anywhere in A
+    or B); finite inputs solve bit-identically to the default path."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(3, 40))
+    A = np.asfortranarray(rng.standard_normal((n, n)) + 4 * np.eye(n))
+    B = np.asfortranarray(rng.standard_normal((n, 2)))
+    r0, X0, rep0, _ = oracle.solve(A, B)
+    r1, X1, rep1, _ = oracle.solve(A, B, check_finite=True)
+    assert r0 == r1 == 0 and np.array_equal(X0, X1) and rep0["flags"] == rep1["flags"]
+    bad = [np.nan, np.inf, -np.inf][seed % 3]
+    tgt = A if seed % 2 == 0 else B
+    i, j = int(rng.integers(0, n)), int(rng.integers(0, tgt.shape[1]))
+    A2, B2 = A.copy(order="F"), B.copy(order="F")
+    (A2 if tgt is A else B2)[i, j] = bad
+    assert not (np.isfinite(A2).all() and np.isfinite(B2).all())
+    r, _, rep, _ = oracle.solve(A2, B2, check_finite=True)
+    assert r == oracle.ERR_NONFINITE
+    assert rep["flags"] & oracle.F_NONFINITE
+    assert (rep["flags"] >> 4) & 0xF == 0 and rep["rcond"] == 0.0      # no method ran
+    # detection verdicts are still the literal ones
+    assert (rep["flags"] & 0xF) == oracle.detect(A2).flags
+
+
+def test_nonfinite_reaching_svd_is_an_error():
+    """Without CHECK_FINITE a NaN/Inf in A makes the rcond estimate non-finite or 0, the gate sends the
+    call to the SVD, whose singular values are then non-finite: the min-norm solution is undefined
+    (Z29) -> AS_ERR_NONFINITE, never a silent 'rank 0' answer."""
+    for bad in (np.nan, np.inf):
+        A = F([[4.0, 1.0, 0.5], [1.0, bad, 2.0], [0.5, 1.0, 3.0]])
+        B = F([[1.0], [2.0], [3.0]])
+        r, _, rep, _ = oracle.solve(A, B)
+        assert r == oracle.ERR_NONFINITE, (bad, r, rep)
+        assert rep["flags"] & oracle.F_NONFINITE and rep["flags"] & oracle.F_FALLBACK
+        assert rep["rank"] == -1 and not rep["flags"] & oracle.F_RANK_DEF
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_band_pack_anorm_is_the_1norm(seed):
+    """band_pack's band 1-norm: every non-zero of a banded matrix lies in the band, so it equals the
+    plain max column sum of |A| (numpy), independent of the packing code."""
+    rng = np.random.default_rng(100 + seed)
+    n, kl, ku = 60 + seed, 1 + seed, 3 - seed % 3
+    A = W.random_banded(n, kl, ku, seed=seed)
+    A[int(rng.integers(0, n)), :] *= 7.0    # a heavy row (stays inside the band) so no column sum is typical
+    _, anorm = oracle.band_pack(A, kl, ku)
+    assert anorm == pytest.approx(np.abs(A).sum(axis=0).max(), rel=4 * n * 2.2e-16)
