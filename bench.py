@@ -1,17 +1,20 @@
 #!/usr/bin/env python
 """Benchmark of the adaptive solve of A X = B (arXiv 2007.11208) on B200.
 
-One "step" = one call of the public C-ABI entry point ``as_solve_ex`` on the
-BASELINE.json workload: structure detection -> dispatch -> factor -> rcond
-estimate -> gate -> solve (or SVD fallback), one graph launch and one stream
-sync, inputs resident in HBM.  The default workload is configs[1] (C2: banded
-fp64 n=8192, kl=ku=8, 4 RHS); ``--config`` selects another BASELINE config.
+One "step" = one call of the public C-ABI entry point (``as_solve_ex`` / ``as_solve_async``) on a
+BASELINE.json workload: structure detection -> dispatch -> factor -> rcond estimate -> gate ->
+solve (or SVD fallback), one graph launch, inputs resident in HBM.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+The headline is C5 (dense fp64 n = 16384, 32 RHS: the largest config, the one carrying the 60 %
+fp64 tensor-core target).  The same JSON line carries, under ``configs``, the same measurement
+(value, roofline, e2e, cpu_baseline, clocks) for every other BASELINE config: C1, C2, C3a, C3b,
+C4 and C5f.  ``--config T`` makes T the headline; ``--only`` skips the other configs.
 
-Under torchrun (N > 1) every rank solves its own independent system (the solve
-does not shard): weak scaling, no
-collective on the data path; timing is the max over ranks.
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--only] [--impl reference]
+
+Under torchrun (N > 1) every rank solves its own independent system (the solve does not shard,
+DESIGN.md "Multi-GPU: replicas only"): weak scaling, no collective on the data path; timing is the
+max over ranks.  The reference arm (``--impl reference``) is the CPU oracle.
 """
 from __future__ import annotations
 
@@ -29,10 +32,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fp64 GFLOP/s and solves/s per structure class; fraction of fp64/HBM roofline"
+TAGS = ["C1", "C2", "C3a", "C3b", "C4", "C5", "C5f"]
+HEADLINE = "C5"
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # 37.2: 64 fp64 FMA/clk/SM at the max SM clock
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12     # 74.4: 128 fp32 lanes/SM (FFMA), no tensor core
 
 
-# ------------------------------------------------------------------ workload accounting (DESIGN.md "Roofline")
-def workload(tag: str):
+# ------------------------------------------------------------------ workload accounting (DESIGN.md section 6)
+def workload(tag: str, sweeps: int = 0):
+    """Algorithmic flops / bytes of the path the config takes (LAPACK standard counts)."""
     import workloads as W
     kw = dict(W.CONFIGS[tag][1])
     n, nrhs = kw["n"], kw["nrhs"]
@@ -42,50 +50,38 @@ def workload(tag: str):
         kl, ku = kw["kl"], kw["ku"]
         info["flops"] = n * (2 * kl * (kl + ku) + kl) + nrhs * 2 * n * (2 * kl + ku)   # gbtrf + gbtrs
         info["detect_bytes"] = n * n * es                       # a banded matrix must be read entirely
-        info["factor_bytes"] = (kl + ku + 1) * n * es + 2 * (2 * kl + ku + 1) * n * es   # pack read + ab write/rw
-        info["solve_bytes"] = 2 * n * nrhs * es + (2 * kl + ku + 1) * n * es
-    elif tag in ("C3a",):
-        info["flops"] = n ** 3 / 3 + 2 * n * n * nrhs            # potrf + potrs
-        info["detect_bytes"] = n * n * es
+        # band read once by the factor, factors written and read back by the solves, B read, X written
+        info["band_bytes"] = (kl + ku + 1) * n * es + 2 * (2 * kl + ku + 1) * n * es + 2 * n * nrhs * es
+        info["e2e_bytes"] = info["detect_bytes"] + info["band_bytes"]
+    elif tag == "C3a":
+        info["flops"] = n ** 3 / 3 + 2 * n * n * nrhs           # potrf + potrs
         info["factor_flops"] = n ** 3 / 3
+        info["detect_bytes"] = n * n * es
     elif tag == "C3b":
-        info["flops"] = n * n * nrhs                             # trtrs
-        info["detect_bytes"] = n * (n + 1) // 2 * es             # strict lower + diagonal
+        info["flops"] = n * n * nrhs                            # trtrs
+        info["detect_bytes"] = n * (n + 1) // 2 * es            # strict lower + diagonal (only UPPER alive)
         info["solve_bytes"] = n * (n + 1) // 2 * es + 2 * n * nrhs * es
     elif tag in ("C1", "C5", "C5f"):
-        info["flops"] = 2 * n ** 3 / 3 + 2 * n * n * nrhs        # getrf + getrs
+        info["flops"] = 2 * n ** 3 / 3 + 2 * n * n * nrhs       # getrf + getrs
         info["factor_flops"] = 2 * n ** 3 / 3
-        info["detect_bytes"] = None                              # exits after the first tile pair
+        info["detect_bytes"] = None                             # exits after the first tile pair
     elif tag == "C4":
-        info["flops"] = 2 * n ** 3 / 3 + 4 * n ** 3 / 3          # getrf + QR (Jacobi sweeps added at run time)
+        # getrf + Householder QR (4n^3/3) + the executed one-sided Jacobi sweeps: per pair three dot
+        # products (6n) and the rotation of two columns of M (6n); the rotations are applied to V^T c,
+        # V is never formed -> 6 n^2 (n - 1) per sweep; + min-norm apply (2 n^2 per RHS)
+        info["flops"] = 2 * n ** 3 / 3 + 4 * n ** 3 / 3 + sweeps * 6 * n * n * (n - 1) + 2 * n * n * nrhs
+        info["sweeps"] = sweeps
         info["detect_bytes"] = None
     return info
 
 
-def make_inputs(tag: str):
-    import workloads as W
-    if tag == "C5f":
-        return W.make("C5f")
-    return W.make(tag)
-
-
 def load_traffic():
-    """{config: {kernel, dram_bytes, source}} written from ncu --set full captures (profiles/)."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    """{config: {kernel, dram_bytes, source}} from ncu --set full captures (profiles/)."""
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f)
     except (OSError, ValueError):
         return {}
-
-
-def clocks_peak_ghz() -> float:
-    """Max SM clock (GHz) from MEASURED_PEAKS.json (1.965 on this pool's B200s)."""
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f).get("sm_max_mhz", 1965.0)) / 1e3
-    except (OSError, ValueError):
-        return 1.965
 
 
 def load_peaks():
@@ -149,8 +145,53 @@ class ClockSampler:
                 "samples": len(sms)}
 
 
-# ------------------------------------------------------------------ reference arm (the oracle)
+# ------------------------------------------------------------------ CPU oracle (cpu_baseline and the reference arm)
+# Bounded samples of the SAME input bytes: the full system where the plain unblocked oracle finishes in
+# seconds; for C3a / C5 / C5f its leading principal n_s x n_s block with the first RHS columns (a
+# principal block of an SPD / Gaussian matrix has the same structure class and dispatch), the time
+# scaled to the full system by the ratio of the path's flop counts (unblocked O(n^3) loops).
+SAMPLE_N = {"C3a": 2048, "C5": 2048, "C5f": 2048}
+
+
+def oracle_sample(tag: str, A, B):
+    n = A.shape[0]
+    ns = SAMPLE_N.get(tag)
+    if ns is None or ns >= n:
+        return A, B, 1.0, f"full {tag} system (n={n}, {B.shape[1]} RHS, the benchmark's own input bytes)"
+    As = np.asfortranarray(A[:ns, :ns])
+    Bs = np.asfortranarray(B[:ns, :min(4, B.shape[1])])
+    scale = (ns / n) ** 3
+    return As, Bs, scale, (f"leading {ns}x{ns} principal block of the {tag} input with {Bs.shape[1]} RHS; "
+                           f"solves/s scaled to n={n} by the O(n^3) flop ratio ({ns}/{n})^3")
+
+
+def oracle_opts(tag):
+    return dict(no_fallback=True) if tag == "C5f" else {}
+
+
+def cpu_baseline(tag: str, A, B, budget_s: float = 8.0):
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    As, Bs, scale, sample = oracle_sample(tag, A, B)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.solve(As, Bs, **oracle_opts(tag))
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s or reps >= 200:
+            break
+    dt = time.perf_counter() - t0
+    out = {"value": reps / dt * scale, "unit": "solves/s", "cores": oracle.get_threads(), "kind": "oracle",
+           "sample": f"{sample}; {reps} oracle solve(s) in {dt:.1f} s"}
+    ref = os.path.join(ROOT, "tests", "golden", "refs", f"{tag}.npz")
+    if os.path.exists(ref) and scale != 1.0:
+        # context: the full-size oracle solve that produced the committed reference (tools/oracle_refs.py)
+        out["full_size_oracle_seconds_recorded"] = float(np.load(ref)["seconds"])
+    return out
+
+
 def run_reference(args, tag: str, rank: int, world: int):
+    """The reference arm: the CPU oracle, as it stands, on the box's host cores (rank 0 only)."""
     if rank != 0:
         return
     import oracle
@@ -158,53 +199,23 @@ def run_reference(args, tag: str, rank: int, world: int):
     info = workload(tag)
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    # bounded sample: the full system for C1/C2 (fast on CPU); otherwise a scaled-down system of the same recipe
-    sample = f"full {tag} system"
-    if tag in ("C3a", "C3b", "C4", "C5", "C5f"):
-        import workloads as W
-        small = {"C3a": dict(n=1024, nrhs=16), "C3b": dict(n=2048, nrhs=16), "C4": dict(n=256),
-                 "C5": dict(n=1024, nrhs=4), "C5f": dict(n=1024, nrhs=4)}[tag]
-        A, B = W.make(tag, **small)
-        sample = f"{tag} recipe at n={small['n']} (full size exceeds a minutes-long CPU budget)"
-    for _ in range(args.warmup if tag in ("C1",) else min(args.warmup, 1)):
-        oracle.solve(A, B)
+    As, Bs, scale, sample = oracle_sample(tag, A, B)
+    for _ in range(args.warmup if scale == 1.0 and tag in ("C1", "C2") else min(args.warmup, 1)):
+        oracle.solve(As, Bs, **oracle_opts(tag))
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.solve(A, B)
+        oracle.solve(As, Bs, **oracle_opts(tag))
     dt = time.perf_counter() - t0
-    v = args.steps / dt
+    v = args.steps / dt * scale
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if tag != "C5f" else "f32",
-            "data": "synthetic (seeded BASELINE.json recipe)",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if tag == "C5f" else "f64", "data": "synthetic (seeded BASELINE.json recipe)",
             "config": {"workload": f"{tag}: {info['desc']}", "sample": sample},
             "cpu_baseline": {"value": v, "unit": "solves/s", "cores": oracle.get_threads(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def cpu_baseline(tag: str, A, B, budget_s: float = 12.0):
-    import oracle
-    cores = len(os.sched_getaffinity(0))
-    oracle.set_threads(cores)
-    sample = f"full {tag} system"
-    if tag not in ("C1", "C2"):
-        import workloads as W
-        small = {"C3a": dict(n=1024, nrhs=16), "C3b": dict(n=2048, nrhs=16), "C4": dict(n=256),
-                 "C5": dict(n=1024, nrhs=4), "C5f": dict(n=1024, nrhs=4)}[tag]
-        A, B = W.make(tag, **small)
-        sample = f"{tag} recipe at n={small['n']}"
-    reps = 0
-    t0 = time.perf_counter()
-    while True:
-        oracle.solve(A, B)
-        reps += 1
-        if time.perf_counter() - t0 >= budget_s or reps >= 200:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": reps / dt, "unit": "solves/s", "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"{sample}, {reps} solve(s) in {dt:.1f} s"}
 
 
 # ------------------------------------------------------------------ multi-rank aggregation
@@ -223,13 +234,189 @@ def job_throughput(world: int, steps: int, t_max_ms: float) -> float:
     return world * steps / (t_max_ms * 1e-3)
 
 
+def make_inputs(tag: str):
+    import workloads as W
+    return W.make(tag)
+
+
+# ------------------------------------------------------------------ one config on the GPU
+def roofline(tag, info, stage, ms_per_step, fp64_peak, hbm_peak, hbm_src):
+    """Roofline of the dominant stage (stage = [detect, factor+rcond, gate+solve/fallback, total] ms)."""
+    names = ["detect", "factor+rcond(+fused solve)", "gate+solve/fallback"]
+    dom = int(np.argmax(stage[:3]))
+    roof = {"stage": names[dom], "stage_ms": [round(float(x), 4) for x in stage.tolist()]}
+    peak_src = "fp64 DMMA register loop measured in this run (best of the probe variants)"
+    if tag == "C2":
+        # HBM-bound end to end: detection must read all of A, then the band traffic (SURVEY 8(d) C2)
+        ach = info["e2e_bytes"] / (ms_per_step * 1e-3) / 1e9
+        roof.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                     "algorithmic_bytes": info["e2e_bytes"], "scope": "whole step (detection + band factor/solve)",
+                     "peak_source": hbm_src})
+        band_ms = float(stage[1] + stage[2])
+        roof["band_stage"] = {"ms": band_ms, "bytes": info["band_bytes"],
+                              "achieved_gbs": info["band_bytes"] / (band_ms * 1e-3) / 1e9,
+                              "note": "latency-bound chains (SURVEY 8(a) a4)"}
+    elif tag == "C3b":
+        # TRTRS + TRCON stage: max(bytes/BW, flops/peak) (SURVEY 8(d) C3b)
+        t_roof = max(info["solve_bytes"] / (hbm_peak * 1e9), info["flops"] / (fp64_peak * 1e12))
+        ms = float(stage[1])
+        roof.update({"bound": "tensor", "achieved": info["flops"] / (ms * 1e-3) / 1e12, "peak": fp64_peak,
+                     "unit": "TFLOP/s", "frac": t_roof / (ms * 1e-3), "t_roof_ms": t_roof * 1e3,
+                     "algorithmic_flops": info["flops"], "algorithmic_bytes": info["solve_bytes"],
+                     "scope": "factor stage: trtrs (fused with the estimator's first/last applies) + trcon",
+                     "peak_source": peak_src})
+    elif tag == "C5f":
+        ms = float(stage[1])
+        ach = info["factor_flops"] / (ms * 1e-3) / 1e12
+        roof.update({"bound": "alu", "achieved": ach, "peak": NOMINAL_FP32_TFLOPS, "unit": "TFLOP/s",
+                     "frac": ach / NOMINAL_FP32_TFLOPS, "algorithmic_flops": info["factor_flops"],
+                     "scope": "factor stage (getrf + gecon + fused getrs)",
+                     "peak_source": "FP32 FFMA unit count: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (no tensor core: "
+                                    "tf32 misses the fp32 accuracy bar)"})
+    elif info.get("factor_flops"):
+        ms = float(stage[1])
+        ach = info["factor_flops"] / (ms * 1e-3) / 1e12
+        roof.update({"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": ach / fp64_peak, "frac_of_nominal": ach / NOMINAL_FP64_TFLOPS,
+                     "nominal_peak": NOMINAL_FP64_TFLOPS, "algorithmic_flops": info["factor_flops"],
+                     "scope": "factor stage (factorization + rcond estimate + fused solve)", "peak_source": peak_src})
+    else:
+        ach = info["flops"] / (ms_per_step * 1e-3) / 1e12
+        roof.update({"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": ach / fp64_peak, "frac_of_nominal": ach / NOMINAL_FP64_TFLOPS,
+                     "nominal_peak": NOMINAL_FP64_TFLOPS, "algorithmic_flops": info["flops"],
+                     "scope": "whole step", "peak_source": peak_src})
+    roof.setdefault("traffic", None)
+    tr = load_traffic().get(tag)
+    if tr:
+        roof["traffic"] = tr["dram_bytes"]
+        roof["traffic_kernel"] = tr["kernel"]
+        roof["traffic_source"] = tr["source"]
+    return roof
+
+
+def measure(tag, args, dist, world, rank, local, fp64_peak, want_cpu):
+    import ctypes as C
+
+    import torch
+
+    import paper_2007_11208_b200 as AS
+    A, B = make_inputs(tag)
+    dA, dB = AS.to_device(A), AS.to_device(B)
+    X = AS.empty_colmajor(B.shape[0], B.shape[1], dB.dtype)
+    stream = torch.cuda.current_stream()
+    # C5f: the fp32 rcond sits at the 0.5 eps gate (SURVEY F1 / Z21): NO_FALLBACK, the LU data point
+    opts = AS.make_options(no_fallback=True) if tag == "C5f" else None
+    for _ in range(args.warmup):
+        ret, _, rep = AS.as_solve_ex(dA, dB, X=X, options=opts)
+        assert ret == 0, AS.strerror(ret)
+    torch.cuda.synchronize()
+    # inputs smaller than L2 (C1, C4 and the 134 MB C3a/C3b): a 256 MB write between steps
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda") if A.nbytes < 256 * 2 ** 20 else None
+    clock = ClockSampler(local)
+    clock.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stage = np.zeros(4)
+    launches = 0
+    step_ms, reports = [], []
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ret, _, rep = AS.as_solve_ex(dA, dB, X=X, options=opts)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        st = AS.last_stage_ms()
+        if st:
+            stage += np.array(st)
+        launches += AS.last_kernel_nodes()
+        reports.append(rep)
+    torch.cuda.synchronize()
+    blocking_ms = float(np.sum(step_ms)) / args.steps
+    # device throughput (inputs larger than L2): K back-to-back as_solve_async calls (one graph launch
+    # each, no host sync in between) bracketed by a barrier + synchronize
+    if flush is None and not args.eager:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(args.steps):
+            r = AS.as_solve_async(dA, dB, X, options=opts, stream=stream)
+            assert r == 0, AS.strerror(r)
+        eb.record(stream)
+        eb.synchronize()
+        torch.cuda.synchronize()
+        step_ms = [ea.elapsed_time(eb) / args.steps] * args.steps
+    if dist:
+        dist.barrier()
+    clocks = clock.stop()
+    t_ms = aggregate_time(float(np.sum(step_ms)), dist, device="cuda")
+    ms_per_step = t_ms / args.steps
+    value = job_throughput(world, args.steps, t_ms)
+    stage /= args.steps
+    rep = reports[-1]
+    info = workload(tag, sweeps=int(rep["sweeps"]))
+
+    # ---- end to end: host buffers through as_solve_host (H2D of A and B + solve + D2H of X timed)
+    pin_A = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory()
+    pin_B = torch.from_numpy(np.ascontiguousarray(B.T)).pin_memory()
+    pin_X = torch.empty_like(pin_B).pin_memory()
+    e2e_ms = []
+    rep_h = AS.Report()
+    dtc = AS.AS_F32 if A.dtype == np.float32 else AS.AS_F64
+    n, nrhs = B.shape
+    for i in range(max(3, min(args.steps, 10)) + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = AS.lib().as_solve_host(dtc, pin_A.data_ptr(), n, n, pin_B.data_ptr(), n, nrhs, pin_X.data_ptr(),
+                                   C.byref(opts) if opts is not None else None, C.byref(rep_h), stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        assert r == 0, AS.strerror(r)
+        if i > 0:   # the first call allocates the staging buffers / plan
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_t = aggregate_time(float(np.sum(e2e_ms)), dist, device="cuda")
+    e2e = {"value": world * len(e2e_ms) / (e2e_t * 1e-3), "unit": "solves/s",
+           "h2d_bytes_per_step": int(A.nbytes + B.nbytes), "d2h_bytes_per_step": int(B.nbytes)}
+    del pin_A, pin_B, pin_X
+
+    hbm_peak, hbm_src = load_peaks()
+    roof = roofline(tag, info, stage, ms_per_step, fp64_peak, hbm_peak, hbm_src)
+    out = {"tag": tag, "workload": f"{tag}: {info['desc']}", "n": info["n"], "nrhs": info["nrhs"],
+           "value": value, "unit": "solves/s", "ms_per_step": ms_per_step, "steps": args.steps,
+           "gflops": info["flops"] / (ms_per_step * 1e-3) / 1e9, "algorithmic_flops": info["flops"],
+           "dtype": "f32" if tag == "C5f" else "f64",
+           "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps (256 MB write)",
+           "timing": ("K back-to-back as_solve_async calls between two synchronizes (device throughput)"
+                      if flush is None and not args.eager else
+                      "per-call CUDA events around blocking as_solve_ex (host launch + sync included)"),
+           "ms_per_call_blocking": blocking_ms, "method": rep["method"], "flags": hex(rep["flags"]),
+           "rcond": rep["rcond"], "sweeps": rep["sweeps"], "roofline": roof, "e2e": e2e,
+           "gpu_launches": int(launches), "clocks": clocks}
+    if info.get("detect_bytes"):
+        ach = info["detect_bytes"] / (stage[0] * 1e-3) / 1e9
+        out["detect_hbm"] = {"achieved_gbs": ach, "frac": ach / hbm_peak, "bytes": info["detect_bytes"],
+                             "ms": float(stage[0])}
+    out["cpu_baseline"] = cpu_baseline(tag, A, B) if want_cpu else None
+    del dA, dB, X
+    AS.release_all()
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------ main (CUDA arm)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3a", "C3b", "C4", "C5", "C5f"])
+    ap.add_argument("--config", default=HEADLINE, choices=TAGS)
+    ap.add_argument("--only", action="store_true", help="measure the headline config only")
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true",
@@ -258,162 +445,27 @@ def main():
     AS.set_instrumentation(True)
     if args.eager:
         AS.set_exec_mode(True)
-    info = workload(tag)
-    A, B = make_inputs(tag)
-    dA, dB = AS.to_device(A), AS.to_device(B)
-    X = AS.empty_colmajor(B.shape[0], B.shape[1], dB.dtype)
-    stream = torch.cuda.current_stream()
-    # C5f: the fp32 rcond sits at the 0.5*eps gate: run with NO_FALLBACK and
-    # report the LU data point (the gate bit is still set in the flags)
-    opts = AS.make_options(no_fallback=True) if tag == "C5f" else None
-
-    # warm-up (builds + instantiates the plan's graph)
-    for _ in range(args.warmup):
-        ret, _, rep = AS.as_solve_ex(dA, dB, X=X, options=opts)
-        assert ret == 0, AS.strerror(ret)
-    torch.cuda.synchronize()
     fp64_peak = AS.measure_fp64_peak(40000)
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    head = measure(tag, args, dist, world, rank, local, fp64_peak, want_cpu)
+    others = {}
+    if not args.only:
+        for t in TAGS:
+            if t != tag:
+                others[t] = measure(t, args, dist, world, rank, local, fp64_peak, want_cpu)
 
-    # ---- timed region: K public-API calls, inputs resident (A is larger than L2 for C2/C3/C5;
-    # for C1/C4 the 126 MB L2 is flushed by a 256 MB write between steps, outside the per-call timing)
-    flush = None
-    if A.nbytes < 256 * 2 ** 20:
-        flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
-    clock = ClockSampler(local)
-    clock.start()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    stage = np.zeros(4)
-    launches = 0
-    step_ms = []
-    reports = []
-    for _ in range(args.steps):
-        if flush is not None:
-            flush.fill_(1.0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        ret, _, rep = AS.as_solve_ex(dA, dB, X=X, options=opts)
-        e1.record(stream)
-        e1.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
-        st = AS.last_stage_ms()
-        if st:
-            stage += np.array(st)
-        launches += AS.last_kernel_nodes()
-        reports.append(rep)
-    torch.cuda.synchronize()
-    blocking_ms = float(np.sum(step_ms)) / args.steps
-    # Device throughput (inputs larger than L2): the same K public-API solves issued back to back
-    # with as_solve_async (one graph launch each, no host sync between them), bracketed by a
-    # barrier + synchronize; the host-side enqueue of call k+1 overlaps the GPU work of call k.
-    # With L2 flushes between steps (small inputs) the blocking per-call loop above is the number.
-    if flush is None and not args.eager:
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record(stream)
-        for _ in range(args.steps):
-            r = AS.as_solve_async(dA, dB, X, options=opts, stream=stream)
-            assert r == 0, AS.strerror(r)
-        eb.record(stream)
-        eb.synchronize()
-        torch.cuda.synchronize()
-        step_ms = [ea.elapsed_time(eb) / args.steps] * args.steps
-    if dist:
-        dist.barrier()
-    clocks = clock.stop()
-    t_ms = aggregate_time(float(np.sum(step_ms)), dist, device="cuda")
-    ms_per_step = t_ms / args.steps
-    value = job_throughput(world, args.steps, t_ms)
-    stage /= args.steps
-    rep = reports[-1]
-
-    # ---- end to end: host buffers through as_solve_host (H2D + solve + D2H inside the timing)
-    pin_A = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory()
-    pin_B = torch.from_numpy(np.ascontiguousarray(B.T)).pin_memory()
-    pin_X = torch.empty_like(pin_B).pin_memory()
-    import ctypes as C
-    e2e_ms = []
-    rep_h = AS.Report()
-    dtc = AS.AS_F32 if A.dtype == np.float32 else AS.AS_F64
-    n, nrhs = B.shape
-    for i in range(max(3, min(args.steps, 10)) + 1):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        r = AS.lib().as_solve_host(dtc, pin_A.data_ptr(), n, n, pin_B.data_ptr(), n, nrhs, pin_X.data_ptr(),
-                                   C.byref(opts) if opts is not None else None, C.byref(rep_h), stream.cuda_stream)
-        e1.record(stream)
-        e1.synchronize()
-        if i > 0:   # first call allocates the staging buffers / plan
-            e2e_ms.append(e0.elapsed_time(e1))
-    e2e = {"value": world * len(e2e_ms) / (np.sum(e2e_ms) * 1e-3), "unit": "solves/s",
-           "h2d_bytes_per_step": int(A.nbytes + B.nbytes), "d2h_bytes_per_step": int(B.nbytes)}
-
-    # ---- roofline of the dominant stage
-    hbm_peak, hbm_src = load_peaks()
-    names = ["detect", "factor+rcond", "solve/fallback"]
-    dom = int(np.argmax(stage[:3]))
-    roof = {"stage": names[dom], "stage_ms": [round(x, 4) for x in stage.tolist()]}
-    if dom == 0 and info.get("detect_bytes"):
-        ach = info["detect_bytes"] / (stage[0] * 1e-3) / 1e9
-        roof.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                     "traffic": None, "algorithmic_bytes": info["detect_bytes"], "peak_source": hbm_src})
-    elif info.get("factor_flops") and dom == 1 and tag == "C5f":
-        # fp32 runs on the SIMT FFMA pipe (tf32 tensor cores would miss the fp32 accuracy bar):
-        # plain ALU arithmetic against the unit-count peak
-        ffma_peak = 148 * 128 * 2 * clocks_peak_ghz() / 1e3
-        ach = info["factor_flops"] / (stage[1] * 1e-3) / 1e12
-        roof.update({"bound": "alu", "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s",
-                     "frac": ach / ffma_peak, "traffic": None, "algorithmic_flops": info["factor_flops"],
-                     "peak_source": "FP32 FFMA unit count: 148 SMs x 128 lanes x 2 flop x max SM clock"})
-    elif info.get("factor_flops") and dom == 1:
-        ach = info["factor_flops"] / (stage[1] * 1e-3) / 1e12
-        roof.update({"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": ach / fp64_peak, "traffic": None, "algorithmic_flops": info["factor_flops"],
-                     "peak_source": "fp64 DMMA register loop measured in this run"})
-    elif tag == "C2":
-        byts = info["factor_bytes"] if dom == 1 else info["solve_bytes"]
-        ach = byts / (stage[dom] * 1e-3) / 1e9
-        roof.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                     "traffic": None, "algorithmic_bytes": byts, "peak_source": hbm_src,
-                     "note": "banded factor/solve is a latency-bound chain of n pivot steps (SURVEY 8(a) a4)"})
-    else:
-        flops = info["flops"]
-        ach = flops / (stage[dom] * 1e-3) / 1e12
-        roof.update({"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                     "traffic": None, "peak_source": "fp64 DMMA register loop measured in this run"})
-    # DRAM traffic of the dominant kernel per launch, from the committed ncu --set full capture
-    tr = load_traffic().get(tag)
-    if tr:
-        roof["traffic"] = tr["dram_bytes"]
-        roof["traffic_kernel"] = tr["kernel"]
-        roof["traffic_source"] = tr["source"]
-    # detection stage fraction is always reported when it is HBM-graded
-    extra = {}
-    if info.get("detect_bytes"):
-        ach = info["detect_bytes"] / (stage[0] * 1e-3) / 1e9
-        extra["detect_hbm"] = {"achieved_gbs": ach, "frac": ach / hbm_peak, "bytes": info["detect_bytes"]}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(tag, A, B)
-
-    gflops = info["flops"] / (ms_per_step * 1e-3) / 1e9
-    line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if tag == "C5f" else "f64", "data": "synthetic (seeded BASELINE.json recipe)",
-            "config": {"workload": f"{tag}: {info['desc']}", "n": info["n"], "nrhs": info["nrhs"],
+    line = {"metric": METRIC, "value": head["value"], "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": head["dtype"],
+            "data": "synthetic (seeded BASELINE.json recipe)",
+            "config": {"workload": head["workload"], "n": head["n"], "nrhs": head["nrhs"],
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps (256 MB write)",
-                       "timing": ("K back-to-back as_solve_async calls between two synchronizes (device throughput)"
-                                  if flush is None and not args.eager else
-                                  "per-call CUDA events around blocking as_solve_ex (host launch + sync included)"),
-                       "ms_per_call_blocking": blocking_ms,
-                       "method": rep["method"], "flags": hex(rep["flags"]), "rcond": rep["rcond"]},
-            "gflops": gflops, "roofline": roof, **extra, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clocks, "fp64_dmma_peak_tflops": fp64_peak}
+                       "l2": head["l2"], "timing": head["timing"], "ms_per_call_blocking": head["ms_per_call_blocking"],
+                       "method": head["method"], "flags": head["flags"], "rcond": head["rcond"]},
+            "gflops": head["gflops"], "roofline": head["roofline"], "cpu_baseline": head["cpu_baseline"],
+            "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
+            "fp64_dmma_peak_tflops": fp64_peak, "fp64_nominal_tflops": NOMINAL_FP64_TFLOPS,
+            "configs": {t: {k: v for k, v in o.items() if k != "tag"} for t, o in others.items()}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -27,7 +27,10 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"libadaptsolve.so not found at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'`"
                       " (there is deliberately no CPU fallback)")
 
-_lib = C.CDLL(LIB_PATH)
+# AS_USE_DEBUG_LIB=1 (diagnostic tools only): every call goes through the -DAS_DEBUG build, so the
+# as_debug_* diagnostics see the plans of the solves made through this module
+_USE_DEBUG = os.environ.get("AS_USE_DEBUG_LIB", "") not in ("", "0")
+_lib = C.CDLL(DEBUG_LIB_PATH if _USE_DEBUG else LIB_PATH)
 
 AS_F64, AS_F32 = 0, 1
 FLAG_BANDED, FLAG_LOWER, FLAG_UPPER, FLAG_SPD = 0x1, 0x2, 0x4, 0x8
@@ -216,7 +219,7 @@ def debug_lib():
     if _dbg is None:
         if not os.path.exists(DEBUG_LIB_PATH):
             raise ImportError(f"{DEBUG_LIB_PATH} not found (built with libadaptsolve.so by build())")
-        d = C.CDLL(DEBUG_LIB_PATH)
+        d = _lib if _USE_DEBUG else C.CDLL(DEBUG_LIB_PATH)
         d.as_debug_factor.argtypes = [I32, I32, P, I64, I64, I64, I64, P, P, P]
         d.as_debug_factor.restype = I64
         d.as_debug_timestamps.argtypes = [P]

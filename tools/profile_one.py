@@ -29,6 +29,6 @@ for i in range(a.calls):
     ret, _, rep = AS.as_solve_ex(dA, dB, X=X)
     torch.cuda.synchronize()
     print(i, ret, rep["method"], hex(rep["flags"]), rep["rcond"], AS.last_kernel_nodes(), flush=True)
-ts = AS.debug_timestamps()
+ts = AS.debug_timestamps() if os.environ.get("AS_USE_DEBUG_LIB") else None
 if ts and ts[0] is not None:
     print("stamps_us", [round(x, 1) if x is not None else None for x in ts])
