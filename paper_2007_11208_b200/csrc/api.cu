@@ -352,6 +352,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.bars_len = 8 + nblk + 8;
     w.bars = (unsigned*)take(4 * w.bars_len);
     w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * 128 + es * 2 * 128);   // LU panel slots, rowbuf, diagbuf (128-wide)
+    w.lfbuf = take(lu_lfbuf_bytes(n, w.dtype));
     return off;
 }
 

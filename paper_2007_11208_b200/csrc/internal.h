@@ -41,6 +41,7 @@ struct Work {
     unsigned* bars;      // cooperative-kernel barrier counters (zeroed per solve)
     int64_t bars_len;
     void* cand;          // LU panel candidates
+    void* lfbuf;         // leaf LU panel: counters, exchange slots, candidate rows, row-move staging
     int num_sms;
 };
 

@@ -496,383 +496,307 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
     if (threadIdx.x == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
 }
 
-// ------------------------------------------------------------------ panel (leaf-blocked, one cluster)
-// The panel's m rows are split over the P <= 16 CTAs of one thread-block cluster, RPT rows per
-// thread (row tid + 256 i of the CTA's chunk).  The columns are factored in leaves of KLW columns
-// held in REGISTERS (RPT x KLW = 64 values per thread); the rest of the panel stays in global
-// memory (L2) and receives one deferred rank-KLW update per leaf.  Rows are kept ROTATED: at leaf
-// step jj, a[i][k] holds leaf column (jj + k) mod KLW, so the current column is a[i][0], every
-// register index is a compile-time constant and the column loop stays compact (not unrolled).
-// Per column (first-max tie-break, Z15; a NaN diagonal keeps its row, as the serial sweep does):
-//   warp argmax = fmax shuffle + ballot + integer min-reduction of the row index; the winning
-//   lane stores its (rotated) row, the owner of row g its row g; ONE CTA barrier; every thread
-//   merges the 8 warp results.  P > 1: each CTA's winner (value, index, row) -- and row g from
-//   its owner -- is pushed into every CTA with st.async, which completes the receiver's mbarrier
-//   transaction count: data and signal arrive together, no cluster barrier, no fence.
-//   Then: swap of rows g and p (their owners), multipliers, rank-1 update in registers.
-// Per leaf: the leaf's interchanges composed into one permutation of <= 2 KLW rows and applied to
-// the panel's other columns; U12 = L11^{-1} A12 for the leaf's pivot rows; A22 -= L21 U12 for the
-// rows below.  Result (rows interchanged within the panel, ipiv): the unblocked column sweep's up
-// to rounding.
-constexpr int kLfMaxP = 16;
+// ------------------------------------------------------------------ panel (leaf-blocked, few CTAs)
+// For tall panels (m > the cluster panel's reach) beside a running trailing GEMM.  The panel's m
+// rows are split over P = ceil(m / kLfRows) CTAs (<= 16 at n = 16384, so the GEMM keeps the other
+// ~132 SMs; the CTAs are an ordinary launch that is scheduled as GEMM tiles retire -- no cluster
+// placement, no gang scheduling).  Rows stay where they are in W during the panel ("original
+// order"); every CTA tracks the CURRENT position of each of its rows (pos[]) and all CTAs track which
+// row sits at each of the panel's nbp positions (row_at[]), so a row interchange of xGETF2 is pure
+// bookkeeping and the first-max tie-break is decided on positions exactly as in the serial sweep
+// (Z15).  Columns are factored in leaves of LW columns held in shared memory:
+//   per column j of the leaf: local first-max of |a| over the unpivoted rows (key |a|, then the
+//     smaller position; a NaN at position g keeps g), published with the candidate's leaf row into a
+//     sequence-numbered global slot; every CTA polls the P slots (barrier and data in one) and
+//     merges them; bookkeeping of the interchange; multipliers and the rank-1 update of the leaf's
+//     later columns, fused with the next column's local argmax;
+//   per leaf: the leaf written back; U12 = L11^{-1} A12 for the leaf's pivot rows (L11 = the
+//     published pivot rows, identical in every CTA); A22 -= L21 U12 for the CTA's unpivoted rows.
+// At the end the <= 2 nbp rows whose position changed are moved to their final positions (two grid
+// barriers around a staging copy).  ipiv is LAPACK's (position swapped with g at step g).
+// Result: the unblocked column sweep's L\U and interchanges, up to rounding.
+constexpr int kLfRows = 1024;          // rows per CTA
+constexpr int kLfMaxP = 64;            // CTAs (slots per parity)
+template <typename T> struct LfLeaf;
+template <> struct LfLeaf<double> { static constexpr int v = 16; };
+template <> struct LfLeaf<float> { static constexpr int v = 32; };
 
-template <typename T, int KLW>
-struct LeafSmem {
-    T rowbuf[2][1][KLW];                 // the CTA winner's row (rotated)
-    T gbuf[2][KLW];                      // row g (rotated), CTA-local
-    T crow[2][kLfMaxP][KLW];             // cluster: every CTA's candidate row
-    T cgrow[2][KLW];                     // cluster: row g
-    T Ub[KLW][KLW];                      // pivot rows of the leaf, natural column order
-    T U12[KLW][kPW - KLW + 17];          // + padding (vector reads past the last column); odd row
-                                         // stride: column accesses are bank-conflict free
-    unsigned long long cvi[2][kLfMaxP][2];   // cluster: (value bits, index) per CTA
-    unsigned long long mbar[2];
-    T wval[2][kPT / 32];
-    int widx[2][kPT / 32];
-    int64_t s_piv[kPW];
-    int64_t s_src[2 * KLW], s_dst[2 * KLW];
-    int s_np;
+struct __align__(32) LfSlot {
+    double v;                  // |a| of the candidate (-1: none)
+    long long pos;             // its current position
+    long long row;             // its row in W (original order)
+    unsigned long long seq;    // sequence number (published last, with release)
 };
 
-template <typename T> AS_DEV unsigned long long t_bits(T v);
-template <> AS_DEV unsigned long long t_bits<double>(double v) { return (unsigned long long)__double_as_longlong(v); }
-template <> AS_DEV unsigned long long t_bits<float>(float v) { return (unsigned long long)__float_as_uint(v); }
-template <typename T> AS_DEV T t_from(unsigned long long b);
-template <> AS_DEV double t_from<double>(unsigned long long b) { return __longlong_as_double((long long)b); }
-template <> AS_DEV float t_from<float>(unsigned long long b) { return __uint_as_float((unsigned)b); }
-template <typename T>
-AS_DEV void push_elem(const T* local_dst, unsigned rank, T v, unsigned rbar) {
-    const unsigned ra = mapa_u32(smem_u32(local_dst), rank);
-    if (sizeof(T) == 8) st_async_b64(ra, t_bits<T>(v), rbar);
-    else st_async_b32(ra, (unsigned)t_bits<T>(v), rbar);
-}
+template <typename T, int LW>
+struct LfSmem {
+    T S[kLfRows * LW];                 // leaf columns of my rows, column-major (stride kLfRows)
+    T U12[LW * kPW];                   // [k][c] leaf rows of U12 for the panel's later columns
+    T LU11[LW * LW];                   // [jj][c] published pivot rows of the leaf (L11 \ U11)
+    T ubuf[LW];
+    int pos[kLfRows];                  // current position of my row (>= 0) or -(final position) - 1
+    int row_at[kPW];                   // row in W at panel position k0 + i
+    int pivrow[LW];
+    double cv[8];
+    int cpos[8], crow[8];
+    double wv;
+    int wpos, wrow, wown, nmoved;
+};
 
-template <typename T, int RPT, int KLW>
-__global__ void __launch_bounds__(kPT, 1) lu_panel_fast_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
-                                                                int64_t* ipiv, DevState* st, unsigned long long* tr_min,
-                                                                unsigned long long* tr_max, int dbg) {
-    cg::cluster_group cl = cg::this_cluster();
-    if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
-    const int P = (int)cl.num_blocks(), cta = (int)cl.block_rank();
-    const int64_t m = n - k0;
-    const int64_t chunk = (m + P - 1) / P;
-    const int64_t rbeg = k0 + (int64_t)cta * chunk;
-    const int64_t rend = min(n, rbeg + chunk);
+// lexicographic candidate order: larger |a| first, then the smaller position
+template <typename T>
+AS_DEV bool lf_better(T v2, int p2, T v, int p) { return v2 > v || (v2 == v && p2 < p); }
+
+template <typename T, int LW>
+__global__ void __launch_bounds__(kPT, 1) lu_panel_lf_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+                                                             int64_t* ipiv, DevState* st, LfSlot* slots, T* xrow,
+                                                             T* stage, int* stage_dst, unsigned* ctr,
+                                                             unsigned long long seq_base,
+                                                             unsigned long long* tr_min, unsigned long long* tr_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    LeafSmem<T, KLW>& S = *reinterpret_cast<LeafSmem<T, KLW>*>(smem_raw);
-    constexpr int URW = kPW - KLW + 17;
+    LfSmem<T, LW>& sm = *(LfSmem<T, LW>*)smem_raw;
+    if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
+    const int P = gridDim.x, cta = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int kNone = 0x7fffffff;        // row positions fit in int (n <= 2^31 - 1)
-    int gr[RPT];
+    const int64_t m = n - k0;
+    const int chunk = (int)((m + P - 1) / P);
+    const int64_t rbeg = k0 + (int64_t)cta * chunk;             // my rows of W: rbeg .. rbeg + nr
+    const int nr = (int)max<int64_t>(0, min<int64_t>(n, rbeg + chunk) - rbeg);
+    constexpr int RPT = kLfRows / kPT;
+    for (int r = tid; r < nr; r += kPT) sm.pos[r] = (int)(rbeg + r);
+    for (int i = tid; i < nbp; i += kPT) sm.row_at[i] = (int)(k0 + i);
+    unsigned long long info = ~0ull;
+    T bv = T(-1);                      // this thread's candidate for the next column
+    int bp = 0x7fffffff, br = -1;
+    bool bnan = false;                 // the row at position g holds a NaN
+
+    // thread candidate -> CTA candidate (sm.cv[0] / cpos / crow); one barrier
+    auto cta_argmax = [&](int64_t g) {
+        unsigned kh = 0u, kl = 0u;
+        if (br >= 0) cand_key<T>(bv, kh, kl);
+        const unsigned mh = __reduce_max_sync(0xffffffffu, kh);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, kh == mh ? kl : 0u);
+        const unsigned mp = __reduce_min_sync(0xffffffffu, (mh != 0u && kh == mh && kl == ml) ? (unsigned)bp : 0xffffffffu);
+        const unsigned wl = __ballot_sync(0xffffffffu, mh != 0u && kh == mh && kl == ml && (unsigned)bp == mp);
+        const int src = wl ? __ffs(wl) - 1 : 0;
+        const T wv = __shfl_sync(0xffffffffu, bv, src);
+        const int wr = __shfl_sync(0xffffffffu, br, src);
+        const bool dn = __any_sync(0xffffffffu, bnan);
+        if (lane == 0) {
+            sm.cv[warp] = dn ? (double)INFINITY : (wl ? (double)wv : -1.0);
+            sm.cpos[warp] = dn ? (int)g : (wl ? (int)mp : 0x7fffffff);
+            sm.crow[warp] = dn ? -2 : (wl ? wr : -1);       // -2: the row at g (found below)
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double v = lane < 8 ? sm.cv[lane] : -1.0;
+            int pp = lane < 8 ? sm.cpos[lane] : 0x7fffffff;
+            int rr = lane < 8 ? sm.crow[lane] : -1;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) gr[i] = (rbeg + tid + (int64_t)kPT * i < rend) ? (int)(rbeg + tid + (int64_t)kPT * i) : -1;
-    T a[RPT][KLW];
-    auto cbar = [&]() {
-        if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        else __syncthreads();
+            for (int o = 4; o > 0; o >>= 1) {
+                const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                const int p2 = __shfl_xor_sync(0xffffffffu, pp, o);
+                const int r2 = __shfl_xor_sync(0xffffffffu, rr, o);
+                if (lf_better(v2, p2, v, pp)) { v = v2; pp = p2; rr = r2; }
+            }
+            if (lane == 0) { sm.cv[0] = v; sm.cpos[0] = pp; sm.crow[0] = rr; }
+        }
     };
-    if (P > 1) {
-        if (tid == 0) { mbar_init(&S.mbar[0], 1); mbar_init(&S.mbar[1], 1); mbar_fence_init_cluster(); }
-        cbar();
-    }
-    // local first-max over my rows at positions >= gmin for the current (rotated) column
-    auto local_cand = [&](int gmin, T& lv, int& li) {
-        lv = T(-1);
-        li = kNone;
-        bool dn = false;
+    // local candidate of column jj (leaf-local) from scratch over my unpivoted rows
+    auto scan = [&](int jj, int64_t g) {
+        bv = T(-1); bp = 0x7fffffff; br = -1; bnan = false;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            if (gr[i] >= gmin) {
-                T x = a[i][0];
-                x = x < T(0) ? -x : x;
-                if (gr[i] == gmin && x != x) dn = true;
-                if (x > lv) { lv = x; li = gr[i]; }      // rows increase with i: strict > keeps the first
+            const int r = tid + kPT * i;
+            if (r < nr && sm.pos[r] >= 0) {
+                T a = sm.S[r + jj * kLfRows];
+                a = a < T(0) ? -a : a;
+                if (a != a) { if (sm.pos[r] == g) bnan = true; continue; }
+                if (lf_better(a == T(0) ? T(0) : a, sm.pos[r], bv, bp)) { bv = a == T(0) ? T(0) : a; bp = sm.pos[r]; br = r; }
             }
         }
-        if (dn) { lv = T(INFINITY); li = gmin; }
     };
 
-    unsigned long long info = ~0ull;
-    int uses = 0;                             // columns processed (mbarrier phase bookkeeping)
-    for (int c0 = 0; c0 < nbp; c0 += KLW) {
-        const int w = min(KLW, nbp - c0);
-        const int g0 = (int)(k0 + c0);
-#pragma unroll
-        for (int c = 0; c < KLW; ++c)
-#pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                a[i][c] = (gr[i] >= g0 && c < w) ? W[gr[i] + (k0 + c0 + c) * ldw] : T(0);
-        T lv;
-        int li;
-        local_cand(g0, lv, li);
-        if ((dbg & 8) && tid < w) S.s_piv[c0 + tid] = g0 + tid;   // ablation: no interchanges
-        for (int jj = 0; jj < (dbg & 8 ? 0 : w); ++jj, ++uses) {
-            const int c = c0 + jj;
-            const int g = (int)(k0 + c);
-            const int par = uses & 1;
-            // ---- warp argmax: value by fmax shuffles, index by ballot + min-reduction
-            T wm = lv;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-            const unsigned wi = __reduce_min_sync(0xffffffffu, (lv == wm && li != kNone) ? (unsigned)li : (unsigned)kNone);
-            if (lane == 0) { S.wval[par][warp] = wi == (unsigned)kNone ? T(-1) : wm; S.widx[par][warp] = (int)wi; }
+    for (int L = 0; L < nbp; L += LW) {
+        const int lw = min(LW, nbp - L);
+        // ---- load the leaf columns of my rows (W is in original row order during the panel)
+        batched<8, T>(
+            nr * lw, [&](int e) -> T { const int c = e / nr, r = e - c * nr; return __ldcg(&W[(rbeg + r) + (k0 + L + c) * ldw]); },
+            [&](int e, T v) { const int c = e / nr, r = e - c * nr; sm.S[r + c * kLfRows] = v; });
+        __syncthreads();
+        scan(0, k0 + L);
+        for (int jj = 0; jj < lw; ++jj) {
+            const int j = L + jj;
+            const int64_t g = k0 + j;
+            const int par = j & 1;
+            cta_argmax(g);
             __syncthreads();
-            // ---- CTA winner (every thread); its owner stores the row, the owner of g row g
-            // (warp-uniform branches: only the owners' warps execute the row copies)
-            T cv = T(-1);
-            int ci = kNone;
-#pragma unroll
-            for (int q = 0; q < kPT / 32; ++q) {
-                const T v = S.wval[par][q];
-                const int ix = S.widx[par][q];
-                if (v > cv || (v == cv && ix < ci)) { cv = v; ci = ix; }
-            }
-            const int cw = 0;
-            {
-                const int wc = (ci != kNone) ? (int)(((int64_t)ci - rbeg) & (kPT - 1)) >> 5 : -1;
-                const int wg = (g >= rbeg && g < rend) ? (int)(((int64_t)g - rbeg) & (kPT - 1)) >> 5 : -1;
-                if (warp == wc) {
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i)
-                        if (gr[i] == ci)
-#pragma unroll
-                            for (int k = 0; k < KLW; ++k) S.rowbuf[par][0][k] = a[i][k];
+            // ---- publish my candidate (its leaf row) and poll everyone's
+            if (warp == 0) {
+                int crow = sm.crow[0];
+                if (crow == -2) {                     // NaN at position g: that row (mine) wins by rule
+                    for (int r = 0; r < nr; ++r) if (sm.pos[r] == (int)g) { crow = r; break; }
                 }
-                if (warp == wg) {
+                if (P > 1) {
+                    if (crow >= 0 && lane < lw) xrow[((int64_t)par * kLfMaxP + cta) * LW + lane] = sm.S[crow + lane * kLfRows];
+                    __syncwarp();
+                    if (lane == 0) {
+                        LfSlot* sl = slots + par * kLfMaxP + cta;
+                        sl->v = sm.cv[0];
+                        sl->pos = sm.cpos[0];
+                        sl->row = crow >= 0 ? rbeg + crow : -1;
+                        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq),
+                                     "l"(seq_base + (unsigned long long)j + 1ull) : "memory");
+                    }
+                    const unsigned long long want = seq_base + (unsigned long long)j + 1ull;
+                    bool ready = lane >= P;
+                    bool ready2 = lane + 32 >= P;
+                    for (;;) {
+                        if (!ready) ready = ld_relaxed64(&slots[par * kLfMaxP + lane].seq) >= want;
+                        if (!ready2) ready2 = ld_relaxed64(&slots[par * kLfMaxP + lane + 32].seq) >= want;
+                        if (__all_sync(0xffffffffu, ready && ready2)) break;
+                    }
+                    fence_acq_rel();
+                    double v = -1.0;
+                    int pp = 0x7fffffff, ow = 0;
+                    long long rw = -1;
+                    for (int q = lane; q < P; q += 32) {
+                        const double v2 = __ldcg(&slots[par * kLfMaxP + q].v);
+                        const int p2 = (int)__ldcg(&slots[par * kLfMaxP + q].pos);
+                        if (lf_better(v2, p2, v, pp)) { v = v2; pp = p2; ow = q; rw = __ldcg(&slots[par * kLfMaxP + q].row); }
+                    }
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i)
-                        if (gr[i] == g)
-#pragma unroll
-                            for (int k = 0; k < KLW; ++k) S.gbuf[par][k] = a[i][k];
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                        const int p2 = __shfl_xor_sync(0xffffffffu, pp, o);
+                        const int o2 = __shfl_xor_sync(0xffffffffu, ow, o);
+                        const long long r2 = __shfl_xor_sync(0xffffffffu, rw, o);
+                        if (lf_better(v2, p2, v, pp)) { v = v2; pp = p2; ow = o2; rw = r2; }
+                    }
+                    if (lane < lw) sm.ubuf[lane] = __ldcg(&xrow[((int64_t)par * kLfMaxP + ow) * LW + lane]);
+                    if (lane == 0) { sm.wpos = pp; sm.wrow = (int)rw; sm.wown = ow; }
+                } else {
+                    if (lane < lw) sm.ubuf[lane] = sm.S[crow + lane * kLfRows];
+                    if (lane == 0) { sm.wpos = sm.cpos[0]; sm.wrow = (int)(rbeg + crow); sm.wown = 0; }
                 }
             }
             __syncthreads();
-            int p = ci;
-            const T* prow = &S.rowbuf[par][cw][0];
-            const T* grw = &S.gbuf[par][0];
-            if (P > 1) {
-                // ---- cluster exchange: push (value, index, row) and row g into every CTA
-                const unsigned bar_l = smem_u32(&S.mbar[par]);
-                if (warp == 0) {
-                    for (int e = lane; e < P * (KLW + 2); e += 32) {
-                        const int q = e / (KLW + 2), k = e - q * (KLW + 2);
-                        const unsigned rb = mapa_u32(bar_l, q);
-                        if (k < KLW) push_elem<T>(&S.crow[par][cta][k], q, S.rowbuf[par][cw][k], rb);
-                        else if (k == KLW) st_async_b64(mapa_u32(smem_u32(&S.cvi[par][cta][0]), q), t_bits<double>((double)cv), rb);
-                        else st_async_b64(mapa_u32(smem_u32(&S.cvi[par][cta][1]), q), (unsigned long long)(unsigned)ci, rb);
-                    }
-                } else if (warp == 1 && g >= rbeg && g < rend) {
-                    for (int e = lane; e < P * KLW; e += 32) {
-                        const int q = e / KLW, k = e - q * KLW;
-                        push_elem<T>(&S.cgrow[par][k], q, S.gbuf[par][k], mapa_u32(bar_l, q));
-                    }
-                }
-                if (tid == 0) mbar_arrive_expect_tx(&S.mbar[par], (unsigned)(P * (KLW * sizeof(T) + 16) + KLW * sizeof(T)));
-                const unsigned ph = (unsigned)((uses >> 1) & 1);
-                while (!mbar_try_wait_cluster(&S.mbar[par], ph)) {}
-                T bv = T(-1);
-                int bi = kNone, bo = 0;
-                for (int q = 0; q < P; ++q) {
-                    const T v = (T)t_from<double>(S.cvi[par][q][0]);
-                    const int ix = (int)(unsigned)S.cvi[par][q][1];
-                    if (v > bv || (v == bv && ix < bi)) { bv = v; bi = ix; bo = q; }
-                }
-                p = bi;
-                prow = &S.crow[par][bo][0];
-                grw = &S.cgrow[par][0];
-            }
-            const T piv = prow[0];
+            // ---- the interchange (bookkeeping only) and the pivot row
+            const T piv = sm.ubuf[jj];
+            const int p = sm.wpos, rs = sm.wrow;
             const bool elim = piv != T(0);
-            if (tid < KLW) S.Ub[jj][(jj + tid) % KLW] = prow[tid];
-            if (tid == 0) S.s_piv[c] = (p == kNone) ? g : p;
-            if (!elim) {
-                if (info == ~0ull) info = (unsigned long long)(g + 1);
-            } else if (p != g) {
-                const int wg = (g >= rbeg && g < rend) ? (int)(((int64_t)g - rbeg) & (kPT - 1)) >> 5 : -1;
-                const int wp = (p >= rbeg && p < rend) ? (int)(((int64_t)p - rbeg) & (kPT - 1)) >> 5 : -1;
-                if (warp == wg || warp == wp) {
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        if (gr[i] == g) {
-#pragma unroll
-                            for (int k = 0; k < KLW; ++k) a[i][k] = prow[k];
-                        } else if (gr[i] == p) {
-#pragma unroll
-                            for (int k = 0; k < KLW; ++k) a[i][k] = grw[k];
-                        }
-                    }
-                }
+            if (tid == 0) {
+                const int q = sm.row_at[j];            // the row currently at position g
+                if (cta == 0) ipiv[g] = elim ? p : g;
+                if (!elim && info == ~0ull) info = (unsigned long long)(g + 1);
+                const int ps = elim ? p : (int)g;
+                const int rpiv = elim ? rs : q;        // zero pivot: no interchange (the serial sweep's rule)
+                sm.row_at[j] = rpiv;
+                if (elim && ps - k0 < nbp && ps != g) sm.row_at[ps - k0] = q;
+                if (elim && q != rpiv && q >= rbeg && q < rbeg + nr) sm.pos[q - rbeg] = ps;
+                if (rpiv >= rbeg && rpiv < rbeg + nr) sm.pos[rpiv - rbeg] = -(int)g - 1;
+                sm.pivrow[jj] = rpiv;
             }
-            // ---- multipliers, rank-1 update (registers), rotation, next column's local candidate
-            const int nlive = KLW - jj;
-            T l[RPT];
+            if (tid < lw) sm.LU11[jj * LW + tid] = sm.ubuf[tid];
+            __syncthreads();
+            // ---- multipliers, rank-1 update of the leaf's later columns, next column's candidate
+            bv = T(-1); bp = 0x7fffffff; br = -1; bnan = false;
+            const bool more = jj + 1 < lw;
 #pragma unroll
             for (int i = 0; i < RPT; ++i) {
-                const bool below = gr[i] > g && elim;
-                l[i] = below ? a[i][0] / piv : T(0);
-                if (below) a[i][0] = l[i];
-            }
-#pragma unroll
-            for (int k = 1; k < KLW; ++k) {
-                if (k < nlive) {
-                    const T uk = prow[k];
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i) a[i][k] -= l[i] * uk;
+                const int r = tid + kPT * i;
+                if (r >= nr || sm.pos[r] < 0) continue;
+                T* Sr = sm.S + r;
+                if (elim) {
+                    const T l = Sr[jj * kLfRows] / piv;
+                    Sr[jj * kLfRows] = l;
+                    for (int c = jj + 1; c < lw; ++c) Sr[c * kLfRows] -= l * sm.ubuf[c];
+                }
+                if (more) {
+                    T a = Sr[(jj + 1) * kLfRows];
+                    a = a < T(0) ? -a : a;
+                    if (a != a) { if (sm.pos[r] == g + 1) bnan = true; continue; }
+                    if (a == T(0)) a = T(0);
+                    if (lf_better(a, sm.pos[r], bv, bp)) { bv = a; bp = sm.pos[r]; br = r; }
                 }
             }
+        }
+        __syncthreads();
+        // ---- leaf done: write it back (original row order)
+        batched<8, T>(
+            nr * lw, [&](int e) -> T { const int c = e / nr, r = e - c * nr; return sm.S[r + c * kLfRows]; },
+            [&](int e, T v) { const int c = e / nr, r = e - c * nr; W[(rbeg + r) + (k0 + L + c) * ldw] = v; });
+        const int c0 = L + lw, rest = nbp - c0;
+        if (rest > 0) {
+            // U12 = L11^{-1} A12 on the leaf's pivot rows (their owners updated them before publishing
+            // this leaf's candidates, so the acquire of the slots made them visible)
+            for (int c = tid; c < rest; c += kPT) {
+                T u[LW];
 #pragma unroll
+                for (int k = 0; k < LW; ++k)
+                    if (k < lw) u[k] = __ldcg(&W[(int64_t)sm.pivrow[k] + (k0 + c0 + c) * ldw]);
+#pragma unroll
+                for (int k = 0; k < LW; ++k) {
+                    if (k >= lw) break;
+#pragma unroll
+                    for (int i2 = 0; i2 < k; ++i2) u[k] -= sm.LU11[k * LW + i2] * u[i2];
+                    sm.U12[k * kPW + c] = u[k];
+                }
+            }
+            __syncthreads();
+            // my pivot rows of this leaf get their U12 row; my unpivoted rows A22 -= L21 U12
+            for (int e = tid; e < lw * rest; e += kPT) {
+                const int k = e / rest, c = e - k * rest;
+                const int rw = sm.pivrow[k];
+                if (rw >= rbeg && rw < rbeg + nr) W[(int64_t)rw + (k0 + c0 + c) * ldw] = sm.U12[k * kPW + c];
+            }
+#pragma unroll 1
             for (int i = 0; i < RPT; ++i) {
-                const T x0 = a[i][0];
+                const int r = tid + kPT * i;
+                const bool act = r < nr && sm.pos[r] >= 0;
+                if (!__syncthreads_or(act)) continue;
+                T l[LW];
 #pragma unroll
-                for (int k = 0; k < KLW - 1; ++k) a[i][k] = a[i][k + 1];
-                a[i][KLW - 1] = x0;
-            }
-            local_cand(g + 1, lv, li);
-        }
-        // short leaf: finish the rotation so that a[.][c] is leaf column c again
-        if (w < KLW && !(dbg & 8))
-            for (int r = w; r < KLW; ++r)
+                for (int k = 0; k < LW; ++k) l[k] = (act && k < lw) ? sm.S[r + k * kLfRows] : T(0);
+                T* Wr = W + (rbeg + r) + (k0 + c0) * ldw;
+                for (int c = 0; c < rest; c += 4) {
+                    T a[4];
 #pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                    const T x0 = a[i][0];
+                    for (int q = 0; q < 4; ++q) a[q] = (act && c + q < rest) ? __ldcg(&Wr[(int64_t)(c + q) * ldw]) : T(0);
 #pragma unroll
-                    for (int k = 0; k < KLW - 1; ++k) a[i][k] = a[i][k + 1];
-                    a[i][KLW - 1] = x0;
-                }
-        // ---- leaf end: write back, pivots, the leaf's interchanges on the panel's other columns
+                    for (int k = 0; k < LW; ++k)
 #pragma unroll
-        for (int cc = 0; cc < KLW; ++cc)
+                        for (int q = 0; q < 4; ++q) a[q] -= l[k] * sm.U12[k * kPW + min(c + q, kPW - 1)];
 #pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                if (gr[i] >= g0 && cc < w) W[gr[i] + (k0 + c0 + cc) * ldw] = a[i][cc];
-        __syncthreads();
-        if (cta == 0 && tid < w) ipiv[g0 + tid] = S.s_piv[c0 + tid];
-        if (tid == 0) S.s_np = 0;
-        __syncthreads();
-        if (tid < 2 * w) {
-            const int t = tid;
-            int64_t x = 0;
-            bool go = true;
-            if (t < w) x = g0 + t;
-            else {
-                x = S.s_piv[c0 + t - w];
-                if (x < g0 + w) go = false;
-                for (int q = 0; q < t - w && go; ++q) go = S.s_piv[c0 + q] != x;
-            }
-            if (go) {
-                int64_t pos = x;
-                for (int q = 0; q < w; ++q) {
-                    const int64_t r = g0 + q, tq = S.s_piv[c0 + q];
-                    if (pos == r) pos = tq;
-                    else if (pos == tq) pos = r;
-                }
-                if (pos != x) {
-                    const int k = atomicAdd(&S.s_np, 1);
-                    S.s_dst[k] = pos;
-                    S.s_src[k] = x;
+                    for (int q = 0; q < 4; ++q)
+                        if (act && c + q < rest) Wr[(int64_t)(c + q) * ldw] = a[q];
                 }
             }
         }
         __syncthreads();
-        {
-            // a warp per column, every gather issued before any scatter; <= 2 KLW moved rows
-            const int np = S.s_np;
-            const int nother = nbp - w;
-            constexpr int kPer = (2 * KLW + 31) / 32;
-            int64_t src[kPer], dst[kPer];
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int k = lane + 32 * u;
-                src[u] = k < np ? S.s_src[k] : 0;
-                dst[u] = k < np ? S.s_dst[k] : 0;
-            }
-            constexpr int kCW = kPer > 2 ? 4 : 8;
-            const int nw = P * (kPT / 32), w0 = cta * (kPT / 32) + warp;
-            for (int t0 = 0; t0 < (dbg & 1 ? 0 : nother); t0 += nw * kCW) {
-                T vv[kCW][kPer];
-#pragma unroll
-                for (int uu = 0; uu < kCW; ++uu) {
-                    const int t = t0 + w0 + uu * nw;
-                    const int col = t < c0 ? t : t + w;
-#pragma unroll
-                    for (int u = 0; u < kPer; ++u)
-                        vv[uu][u] = (lane + 32 * u < np && t < nother) ? W[src[u] + (k0 + col) * ldw] : T(0);
-                }
-#pragma unroll
-                for (int uu = 0; uu < kCW; ++uu) {
-                    const int t = t0 + w0 + uu * nw;
-                    const int col = t < c0 ? t : t + w;
-#pragma unroll
-                    for (int u = 0; u < kPer; ++u)
-                        if (lane + 32 * u < np && t < nother) W[dst[u] + (k0 + col) * ldw] = vv[uu][u];
-                }
-            }
-        }
-        cbar();
-        // ---- deferred update of the rest of the panel
-        if (c0 + w < nbp && !(dbg & 2)) {
-            const int c1 = c0 + w, rw = nbp - c1;
-            batched<8, T>(
-                KLW * rw, [&](int e) -> T { const int k = e % KLW, cc = e / KLW; return __ldcg(&W[(g0 + k) + (k0 + c1 + cc) * ldw]); },
-                [&](int e, T v) { const int k = e % KLW, cc = e / KLW; S.U12[k][cc] = v; });
-            __syncthreads();
-            // U12 = L11^{-1} A12 (unit lower L11 = Ub) in column-oriented (axpy) form: step k
-            // updates rows k+1.. of every column in parallel (a per-column serial sweep would be a
-            // chain of KLW^2/2 dependent shared-memory loads)
-            for (int k = 0; k + 1 < KLW; ++k) {
-                const int nrow = KLW - 1 - k;
-                for (int e = tid; e < nrow * rw; e += kPT) {
-                    const int i2 = k + 1 + e % nrow, cc = e / nrow;
-                    S.U12[i2][cc] -= S.Ub[i2][k] * S.U12[k][cc];
-                }
-                __syncthreads();
-            }
-            for (int e = tid; e < KLW * rw; e += kPT) {
-                const int k = e % KLW, cc = e / KLW;
-                const int64_t rk = g0 + k;
-                if (rk >= rbeg && rk < rend) W[rk + (k0 + c1 + cc) * ldw] = S.U12[k][cc];
-            }
-            // A22 -= L21 U12 on my rows below the leaf (L21 = the leaf values in registers); batches
-            // of kQ columns with the next batch's loads in flight
-            constexpr int kQ = RPT >= 4 ? 2 : RPT >= 2 ? 4 : 4;
-            const int lim = g0 + w;
-            T nx[RPT][kQ];
-            auto load = [&](int cb) {
-#pragma unroll
-                for (int q = 0; q < kQ; ++q)
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i)
-                        nx[i][q] = (gr[i] >= lim && cb + q < rw) ? W[gr[i] + (k0 + c1 + cb + q) * ldw] : T(0);
-            };
-            load(0);
-            for (int cb = 0; cb < rw; cb += kQ) {
-                T acc[RPT][kQ];
-#pragma unroll
-                for (int q = 0; q < kQ; ++q)
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i) acc[i][q] = nx[i][q];
-                if (cb + kQ < rw) load(cb + kQ);
-#pragma unroll
-                for (int k = 0; k < KLW; ++k) {
-                    T uu[kQ];
-#pragma unroll
-                    for (int q = 0; q < kQ; ++q) uu[q] = S.U12[k][cb + q];
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i)
-#pragma unroll
-                        for (int q = 0; q < kQ; ++q) acc[i][q] -= a[i][k] * uu[q];
-                }
-#pragma unroll
-                for (int q = 0; q < kQ; ++q)
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i)
-                        if (gr[i] >= lim && cb + q < rw) W[gr[i] + (k0 + c1 + cb + q) * ldw] = acc[i][q];
-            }
-            __syncthreads();
-        }
     }
-    (void)URW;
-    if (P > 1) cbar();                       // no CTA leaves while remote stores may target it
+    // ---- rows whose position changed go to their final position: stage every moved row (all
+    // panel columns), grid barrier, scatter
+    unsigned gen = 0;
+    if (P > 1) grid_barrier(ctr, ++gen, (unsigned)P);
+    else __syncthreads();
+    for (int r = warp; r < nr; r += kPT / 32) {
+        const int ps = sm.pos[r];
+        const int fin = ps >= 0 ? ps : -ps - 1;
+        if (fin == (int)(rbeg + r)) continue;
+        int slot = 0;
+        if (lane == 0) slot = (int)atomicAdd(ctr + 1, 1u);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        for (int c = lane; c < nbp; c += 32) stage[(int64_t)slot * kPW + c] = W[(rbeg + r) + (k0 + c) * ldw];
+        if (lane == 0) stage_dst[slot] = fin;
+    }
+    if (P > 1) grid_barrier(ctr, ++gen, (unsigned)P);
+    else __syncthreads();
+    const int nmv = (int)__ldcg(ctr + 1);
+    for (int e = cta * kPT + tid; e < nmv * nbp; e += P * kPT) {
+        const int sl = e / nbp, c = e - sl * nbp;
+        W[(int64_t)__ldcg(&stage_dst[sl]) + (k0 + c) * ldw] = __ldcg(&stage[(int64_t)sl * kPW + c]);
+    }
     if (tid == 0 && cta == 0 && info != ~0ull) atomicMin(&st->info, info);
     if (tr_max && tid == 0) atomicMax(tr_max, gtimer());
 }
@@ -1454,81 +1378,76 @@ static LuStreams& lu_streams() {
     return L;
 }
 
-static int g_panel_dbg = 0;   // diagnostics: ablation mask of the register panel (lu_debug_panel_time)
+static int g_panel_dbg = 0;   // diagnostics: phase counters of the cluster panel (lu_debug_panel_time)
 
-// Cluster size and rows per thread of the fast panel: one CTA up to 1024 rows (RPT = 1, 2, 4
-// with leaves of 64, 32, 16 columns), then up to 16 CTAs of <= 1024 rows; larger panels use the
-// cooperative kernel.
+// lfbuf layout (Work::lfbuf, lf_layout): per-block counters, exchange slots, candidate rows,
+// staging for the final row moves
+struct LfBufs {
+    unsigned* ctr;       // [2 * nblk]: grid barrier, staging count (zeroed per factorization)
+    LfSlot* slots;       // [2][kLfMaxP]
+    void* xrow;          // [2][kLfMaxP][LW]
+    int* stage_dst;      // [2 * kPW]
+    void* stage;         // [2 * kPW][kPW]
+    size_t zero_bytes;   // ctr + slots
+};
+static LfBufs lf_layout(void* base, int64_t n, size_t es) {
+    LfBufs b{};
+    const int64_t nblk = (n + kBW - 1) / kBW;
+    char* p = (char*)base;
+    auto take = [&](size_t bytes) { char* q = p; p += (bytes + 255) & ~(size_t)255; return q; };
+    b.ctr = (unsigned*)take(sizeof(unsigned) * 2 * (size_t)nblk);
+    b.slots = (LfSlot*)take(sizeof(LfSlot) * 2 * kLfMaxP);
+    b.zero_bytes = (size_t)(p - (char*)base);
+    b.xrow = take(es * 2 * kLfMaxP * 32);
+    b.stage_dst = (int*)take(sizeof(int) * 2 * kPW);
+    b.stage = take(es * 2 * kPW * kPW);
+    return b;
+}
+size_t lu_lfbuf_bytes(int64_t n, int dtype) { return (size_t)(lf_layout(nullptr, n, dtype == AS_F64 ? 8 : 4).stage) +
+                                                     (dtype == AS_F64 ? 8 : 4) * 2 * kPW * kPW; }
+
+// The leaf panel: P = ceil(m / kLfRows) CTAs of one ordinary launch (see lu_panel_lf_kernel).
 template <typename T>
-static bool leaf_panel_launch(const Work& w, int64_t k0, int nbp, int prio, cudaStream_t s) {
+static bool lf_panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long seq_base, int prio, cudaStream_t s) {
     const int64_t n = w.n, m = n - k0;
-    static const int rows_env = getenv("AS_LU_LEAF_ROWS") ? atoi(getenv("AS_LU_LEAF_ROWS")) : 1024;
-    static int pmax = kLfMaxP;
-    if (nbp > kPW) return false;
-    for (;;) {
-        int P = 1;
-        while (P < pmax && (m + P - 1) / P > rows_env) P *= 2;
-        const int64_t chunk = (m + P - 1) / P;
-        const int rpt = (int)((chunk + kPT - 1) / kPT);
-        if (rpt > 4) return false;
-        void* kern;
-        size_t smem;
-        if (rpt <= 1) { kern = (void*)lu_panel_fast_kernel<T, 1, 64>; smem = sizeof(LeafSmem<T, 64>); }
-        else if (rpt <= 2) { kern = (void*)lu_panel_fast_kernel<T, 2, 32>; smem = sizeof(LeafSmem<T, 32>); }
-        else { kern = (void*)lu_panel_fast_kernel<T, 4, 16>; smem = sizeof(LeafSmem<T, 16>); }
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(P);
-        cfg.blockDim = dim3(kPT);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute at[2];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-        at[1].id = cudaLaunchAttributePriority; at[1].val.priority = prio;
-        cfg.attrs = at;
-        cfg.numAttrs = 2;
-        LuTrace& tr = lu_trace();
-        const int slot = (int)(k0 / kBW) * 4 + ((k0 % kBW) ? 2 : 1);
-        unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
-        unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
-        // the cluster shape must be schedulable (checked outside the stream: a failing launch
-        // would invalidate a graph capture)
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0) {
-            T* Wp = (T*)w.W;
-            int64_t ldw = w.ldw;
-            int64_t* ip = w.ipiv;
-            DevState* stp = w.st;
-            int dbg = g_panel_dbg;
-            void* args[] = {&Wp, &ldw, (void*)&n, &k0, &nbp, &ip, &stp, &tmn, &tmx, &dbg};
-            const cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
-            if (e == cudaSuccess) return true;
-        }
-        cudaGetLastError();
-        if (pmax <= 1) return false;
-        pmax /= 2;                          // e.g. 16-CTA clusters not available: retry with 8
-    }
+    const int P = (int)((m + kLfRows - 1) / kLfRows);
+    if (P > kLfMaxP || P > w.num_sms || nbp > kPW || !w.lfbuf) return false;
+    constexpr int LW = LfLeaf<T>::v;
+    auto kern = lu_panel_lf_kernel<T, LW>;
+    const size_t smem = sizeof(LfSmem<T, LW>);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    LfBufs b = lf_layout(w.lfbuf, n, sizeof(T));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(kPT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority; at[0].val.priority = prio;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LuTrace& tr = lu_trace();
+    const int slot = (int)(k0 / kBW) * 4 + 1;
+    unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
+    unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, b.slots, (T*)b.xrow,
+                                             (T*)b.stage, b.stage_dst, b.ctr + 2 * (k0 / kBW), seq_base, tmn, tmx);
+    if (e != cudaSuccess) { cudaGetLastError(); return false; }
+    return true;
 }
 
 template <typename T>
 static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long seq_base, int prio, cudaStream_t s) {
     const int64_t n = w.n, m = n - k0;
-    // register/cluster panel: opt-in (AS_LU_PANEL=reg) until it beats the cooperative panel
-    // Panel policy.  The cluster panel occupies <= 16 SMs but is slower per column than the
-    // cooperative panel (which occupies ~m/128 SMs); measured on C5 (n = 16384) the cooperative
-    // panel everywhere wins (196 ms) over the cluster panel for m >= 12288 / 10240 / 8192
-    // (209 / 218 / 227 ms), so the cluster panel is opt-in: AS_LU_PANEL=reg (everywhere) or
-    // AS_LU_FAST_MIN_M=<m> (where the panel has >= m rows).
-    static const char* pol = getenv("AS_LU_PANEL");
-    static const int64_t fast_min_m = getenv("AS_LU_FAST_MIN_M") ? atoll(getenv("AS_LU_FAST_MIN_M")) : (int64_t)1 << 62;
-    const bool want_fast = pol && strcmp(pol, "reg") == 0 ? true : (pol && strcmp(pol, "coop") == 0) ? false : m >= fast_min_m;
-    if (want_fast && getenv("AS_LU_PANEL_OLD") == nullptr && leaf_panel_launch<T>(w, k0, nbp, prio, s)) return;
+    // Panel policy: rows that fit in <= kClMax CTAs' shared memory -> one cluster (DSMEM exchange);
+    // taller panels -> the leaf panel on ceil(m / 1024) CTAs (the trailing GEMM keeps the other
+    // SMs); AS_LU_PANEL=coop forces the cooperative panel (m / 128 CTAs, measured slower on C5).
+    const char* pol = getenv("AS_LU_PANEL");
+    const bool coop = pol && strcmp(pol, "coop") == 0;
     static const int rows_per_cta = getenv("AS_LU_PANEL_ROWS") ? atoi(getenv("AS_LU_PANEL_ROWS")) : 128;
     int P = (int)std::min<int64_t>(w.num_sms, (m + rows_per_cta - 1) / rows_per_cta);
     P = std::max(P, 1);
-    if (getenv("AS_LU_NO_CLUSTER") == nullptr) {
+    if (!coop && getenv("AS_LU_NO_CLUSTER") == nullptr) {
         // cluster panel when the rows fit in <= kClMax CTAs' shared memory (~200 KB each)
         int pc = 1;
         while (pc < kClMax && (size_t)((m + pc - 1) / pc) * nbp * sizeof(T) > 192 * 1024) pc *= 2;
@@ -1553,6 +1472,7 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
             cudaGetLastError();
         }
     }
+    if (!coop && lf_panel_launch<T>(w, k0, nbp, seq_base, prio, s)) return;
     const int64_t chunk = (m + P - 1) / P;
     size_t smem = sizeof(T) * ((chunk | 1) * nbp + nbp);
     int use_smem = 1;
@@ -1649,6 +1569,7 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         return;
     }
     cudaMemsetAsync(w.cand, 0, sizeof(PSlot) * 1024, s);       // panel exchange slots (sequence numbers)
+    if (w.lfbuf) cudaMemsetAsync(w.lfbuf, 0, lf_layout(w.lfbuf, n, sizeof(T)).zero_bytes, s);   // leaf panel counters + slots
     if (lu_trace().tmin) {
         cudaMemsetAsync(lu_trace().tmin, 0xFF, sizeof(unsigned long long) * 4 * kTraceBlocks, s);
         cudaMemsetAsync(lu_trace().tmax, 0, sizeof(unsigned long long) * 4 * kTraceBlocks, s);
@@ -1737,6 +1658,8 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
     cudaMalloc(&w.ipiv, 8 * n);
     cudaMalloc(&w.st, sizeof(DevState));
     cudaMalloc(&w.cand, 16 * 2 * 1024 + 8 * 2 * 1024 * 128 + 8 * 2 * 128);
+    const size_t lfb = lu_lfbuf_bytes(n, dtype);
+    cudaMalloc(&w.lfbuf, lfb);
     cudaMemset(w.st, 0, sizeof(DevState));
     cudaMemset(&w.st->info, 0xFF, 8);
     cudaEvent_t e0, e1;
@@ -1748,20 +1671,13 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
     for (int it = 0; it < iters; ++it) {
         cudaMemcpy(W, Wsrc, es * ldw * n, cudaMemcpyDeviceToDevice);
         cudaMemset(w.cand, 0, 16 * 2 * 1024);
+        cudaMemset(w.lfbuf, 0, lf_layout(w.lfbuf, n, es).zero_bytes);
         cudaEventRecord(e0, 0);
-        if (dtype == AS_F64) {
-            if (kind != 0 || !leaf_panel_launch<double>(w, k0, nbp, 0, 0)) {
-                setenv("AS_LU_PANEL_OLD", "1", 1);
-                panel_launch<double>(w, k0, nbp, 0, 0, 0);
-                unsetenv("AS_LU_PANEL_OLD");
-            }
-        } else {
-            if (kind != 0 || !leaf_panel_launch<float>(w, k0, nbp, 0, 0)) {
-                setenv("AS_LU_PANEL_OLD", "1", 1);
-                panel_launch<float>(w, k0, nbp, 0, 0, 0);
-                unsetenv("AS_LU_PANEL_OLD");
-            }
-        }
+        // kind 0: the launch the factorization makes; kind 1: the cooperative panel
+        if (kind == 1) setenv("AS_LU_PANEL", "coop", 1);
+        if (dtype == AS_F64) panel_launch<double>(w, k0, nbp, 0, 0, 0);
+        else panel_launch<float>(w, k0, nbp, 0, 0, 0);
+        if (kind == 1) unsetenv("AS_LU_PANEL");
         cudaEventRecord(e1, 0);
         cudaEventSynchronize(e1);
         float ms = 0.f;
@@ -1781,6 +1697,7 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
     cudaFree(w.ipiv);
     cudaFree(w.st);
     cudaFree(w.cand);
+    cudaFree(w.lfbuf);
     if (err != cudaSuccess) return -(double)err;
     return 1000.0 * tot / (iters > 1 ? iters - 1 : 1);
 }
