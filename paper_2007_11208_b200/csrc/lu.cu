@@ -498,9 +498,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
 
 // ------------------------------------------------------------------ panel (leaf-blocked, few CTAs)
 // For tall panels (m > the cluster panel's reach) beside a running trailing GEMM.  The panel's m
-// rows are split over P = ceil(m / kLfRows) CTAs (<= 16 at n = 16384, so the GEMM keeps the other
-// ~132 SMs; the CTAs are an ordinary launch that is scheduled as GEMM tiles retire -- no cluster
-// placement, no gang scheduling).  Rows stay where they are in W during the panel ("original
+// rows are split over P = ceil(m / kLfRows) CTAs (32 at n = 16384).  A CTA is small enough (<= 128
+// registers per thread, ~85 KB of shared memory) to share an SM with one CTA of the trailing GEMM,
+// so the launch (ordinary, high priority) is placed as GEMM tiles retire -- no cluster placement,
+// no gang scheduling, and the GEMM keeps every SM.  Rows stay where they are in W during the panel ("original
 // order"); every CTA tracks the CURRENT position of each of its rows (pos[]) and all CTAs track which
 // row sits at each of the panel's nbp positions (row_at[]), so a row interchange of xGETF2 is pure
 // bookkeeping and the first-max tie-break is decided on positions exactly as in the serial sweep
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
 // At the end the <= 2 nbp rows whose position changed are moved to their final positions (two grid
 // barriers around a staging copy).  ipiv is LAPACK's (position swapped with g at step g).
 // Result: the unblocked column sweep's L\U and interchanges, up to rounding.
-constexpr int kLfRows = 1024;          // rows per CTA
+constexpr int kLfRows = 512;           // rows per CTA
 constexpr int kLfMaxP = 64;            // CTAs (slots per parity)
 template <typename T> struct LfLeaf;
 template <> struct LfLeaf<double> { static constexpr int v = 16; };
@@ -548,7 +549,7 @@ template <typename T>
 AS_DEV bool lf_better(T v2, int p2, T v, int p) { return v2 > v || (v2 == v && p2 < p); }
 
 template <typename T, int LW>
-__global__ void __launch_bounds__(kPT, 1) lu_panel_lf_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+__global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
                                                              int64_t* ipiv, DevState* st, LfSlot* slots, T* xrow,
                                                              T* stage, int* stage_dst, unsigned* ctr,
                                                              unsigned long long seq_base,
@@ -750,26 +751,28 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_lf_kernel(T* W, int64_t ldw, 
                 const int rw = sm.pivrow[k];
                 if (rw >= rbeg && rw < rbeg + nr) W[(int64_t)rw + (k0 + c0 + c) * ldw] = sm.U12[k * kPW + c];
             }
+            // (one row at a time, 16 columns per batch: 16 independent loads in flight per thread)
+            constexpr int CB = 16;
 #pragma unroll 1
             for (int i = 0; i < RPT; ++i) {
                 const int r = tid + kPT * i;
-                const bool act = r < nr && sm.pos[r] >= 0;
-                if (!__syncthreads_or(act)) continue;
+                if (r >= nr || sm.pos[r] < 0) continue;
                 T l[LW];
 #pragma unroll
-                for (int k = 0; k < LW; ++k) l[k] = (act && k < lw) ? sm.S[r + k * kLfRows] : T(0);
+                for (int k = 0; k < LW; ++k) l[k] = k < lw ? sm.S[r + k * kLfRows] : T(0);
                 T* Wr = W + (rbeg + r) + (k0 + c0) * ldw;
-                for (int c = 0; c < rest; c += 4) {
-                    T a[4];
+#pragma unroll 1
+                for (int c = 0; c < rest; c += CB) {
+                    T a[CB];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) a[q] = (act && c + q < rest) ? __ldcg(&Wr[(int64_t)(c + q) * ldw]) : T(0);
+                    for (int q = 0; q < CB; ++q) a[q] = c + q < rest ? __ldcg(&Wr[(int64_t)(c + q) * ldw]) : T(0);
 #pragma unroll
                     for (int k = 0; k < LW; ++k)
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) a[q] -= l[k] * sm.U12[k * kPW + min(c + q, kPW - 1)];
+                        for (int q = 0; q < CB; ++q) a[q] -= l[k] * sm.U12[k * kPW + min(c + q, kPW - 1)];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (act && c + q < rest) Wr[(int64_t)(c + q) * ldw] = a[q];
+                    for (int q = 0; q < CB; ++q)
+                        if (c + q < rest) Wr[(int64_t)(c + q) * ldw] = a[q];
                 }
             }
         }
@@ -1601,23 +1604,25 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         if (kn >= n) break;
         // trailing columns: interchanges + U12 = L11^{-1} A12 in one kernel
         (void)p1;
-        swap_u12_launch<T>(w, k0, bw, kn, n, s);
         const int64_t M = n - kn;
         const int nbw = (int)std::min<int64_t>(kBW, n - kn);
         if (lookahead && n - kn > nbw) {
-            // next block's columns first (high priority), then its panels; the rest of the GEMM
-            // concurrently on the main stream
+            // the next block's columns first (high priority: its swap + U12, its GEMM, its panels);
+            // the other columns' swap + U12 and the bulk of the GEMM concurrently on the main stream
+            swap_u12_launch<T>(w, k0, bw, kn, kn + nbw, s);
             cudaEvent_t e0 = ev();
             cudaEventRecord(e0, s);
             cudaStreamWaitEvent(LS.hi, e0, 0);
             gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
             block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
+            swap_u12_launch<T>(w, k0, bw, kn + nbw, n, s);
             gemm_launch<T>(w, kn, kn + nbw, k0, M, n - kn - nbw, bw, s, 0, getenv("AS_LU_ONE_PER_SM") != nullptr,
                            (int)(k0 / kBW) * 4 + 0);
             cudaEvent_t e1 = ev();
             cudaEventRecord(e1, LS.hi);
             cudaStreamWaitEvent(s, e1, 0);
         } else {
+            swap_u12_launch<T>(w, k0, bw, kn, n, s);
             gemm_launch<T>(w, kn, kn, k0, M, n - kn, bw, s, 0);
             block_panels<T>(w, kn, nbw, LS.prio_hi, s);
         }
