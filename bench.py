@@ -409,6 +409,94 @@ def measure(tag, args, dist, world, rank, local, fp64_peak, want_cpu):
     return out
 
 
+# ------------------------------------------------------------------ batched small systems
+BATCH_N, BATCH_COUNT = 100, 1000
+
+
+def measure_batched(args, dist, world, local, want_cpu):
+    """The paper's workload shape: 1000 unique random systems of one size, here the C1
+    recipe at n = 100 with seeds 0..999, solved by ONE as_solve_batched call (one thread block per
+    system, the whole adaptive flowchart each)."""
+    import torch
+
+    import paper_2007_11208_b200 as AS
+    import workloads as W
+    n, cnt = BATCH_N, BATCH_COUNT
+    pairs = [W.dense_c1(n=n, nrhs=1, seed=s) for s in range(cnt)]
+    A = np.stack([p[0] for p in pairs])
+    B = np.stack([p[1] for p in pairs])
+    dA, dB = AS.to_device_batched(A), AS.to_device_batched(B)
+    X = AS.empty_colmajor_batched(cnt, n, 1, dA.dtype)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        r, _, rep, rets = AS.as_solve_batched(dA, dB, X=X)
+        assert r == 0, AS.strerror(r)
+    torch.cuda.synchronize()
+    assert int(rets.abs().sum()) == 0
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
+    clock = ClockSampler(local)
+    clock.start()
+    if dist:
+        dist.barrier()
+    tot = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        AS.as_solve_batched(dA, dB, X=X)
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    clocks = clock.stop()
+    t_ms = aggregate_time(tot, dist, device="cuda")
+    value = world * cnt * args.steps / (t_ms * 1e-3)
+    # e2e: pinned host batch -> device, solve, X -> host (all inside the timing)
+    pa = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).pin_memory()
+    pb = torch.from_numpy(np.ascontiguousarray(np.transpose(B, (0, 2, 1)))).pin_memory()
+    px = torch.empty_like(pb).pin_memory()
+    da = torch.empty_like(pa, device="cuda")
+    db = torch.empty_like(pb, device="cuda")
+    e2e_ms = []
+    for i in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        da.copy_(pa, non_blocking=True)
+        db.copy_(pb, non_blocking=True)
+        _, Xe, _, _ = AS.as_solve_batched(da.transpose(1, 2), db.transpose(1, 2))
+        px.copy_(Xe.transpose(1, 2), non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        if i:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e = {"value": world * cnt * len(e2e_ms) / (np.sum(e2e_ms) * 1e-3), "unit": "solves/s",
+           "h2d_bytes_per_step": int(A.nbytes + B.nbytes), "d2h_bytes_per_step": int(B.nbytes)}
+    flops = cnt * (2 * n ** 3 / 3 + 2 * n * n)
+    ach = flops / (t_ms / args.steps * 1e-3) / 1e12
+    out = {"workload": f"batched: {cnt} systems of the C1 recipe at n={n} (seeds 0..{cnt - 1}), 1 RHS, one "
+                       f"as_solve_batched call", "n": n, "nrhs": 1, "batch": cnt, "value": value, "unit": "solves/s",
+           "ms_per_step": t_ms / args.steps, "steps": args.steps, "dtype": "f64",
+           "l2": "L2 flushed between steps (256 MB write)",
+           "roofline": {"bound": "tensor", "achieved": ach, "peak": NOMINAL_FP64_TFLOPS, "unit": "TFLOP/s",
+                        "frac": ach / NOMINAL_FP64_TFLOPS, "traffic": None, "algorithmic_flops": flops,
+                        "note": "one thread block per system, latency-bound column loops (SIMT)"},
+           "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
+           "vs_single_system_C1_solves_per_s": None}
+    if want_cpu:
+        import oracle
+        oracle.set_threads(len(os.sched_getaffinity(0)))
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < 6.0 and k < cnt:
+            oracle.solve(A[k], B[k])
+            k += 1
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": k / dt, "unit": "solves/s", "cores": oracle.get_threads(), "kind": "oracle",
+                               "sample": f"the first {k} systems of the batch, one oracle solve each, {dt:.1f} s"}
+    else:
+        out["cpu_baseline"] = None
+    return out
+
+
 # ------------------------------------------------------------------ main (CUDA arm)
 def main():
     ap = argparse.ArgumentParser()
@@ -453,6 +541,10 @@ def main():
         for t in TAGS:
             if t != tag:
                 others[t] = measure(t, args, dist, world, rank, local, fp64_peak, want_cpu)
+            others["batched_n100"] = measure_batched(args, dist, world, local, want_cpu)
+            if "C1" in others or tag == "C1":
+                c1 = others["C1"]["value"] if "C1" in others else head["value"]
+                others["batched_n100"]["vs_single_system_C1_solves_per_s"] = c1
 
     line = {"metric": METRIC, "value": head["value"], "unit": "solves/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,

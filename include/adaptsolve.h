@@ -165,6 +165,25 @@ int as_solve_ex(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* 
 int as_solve_async(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
                    void* X, const as_options* opt, as_report* rep_dev, void* sigma_out, void* stream);
 
+/* as_solve_batched: `batch` independent systems A_b X_b = B_b of one shape (
+ * the paper's workload is "1000 unique random systems" per size), each solved by the
+ * full adaptive flowchart (detection, dispatch, factor, rcond gate, SVD fallback) with its own
+ * verdict.  n <= 128 and nrhs <= 16: ONE thread block per system, matrix in shared memory, one
+ * launch for the whole batch (detection reads every element, so kl/ku are always exact); larger
+ * shapes: one single-system graph launch per system (then ldx must equal ldb).
+ *   A, B, X   DEVICE, column-major; system b at A + b*strideA (leading dimension lda), B + b*strideB
+ *             (ldb), X + b*strideX (ldx); strides in elements, strideA >= lda*n etc.  A, B read-only;
+ *             X == B (same strides) allowed.
+ *   opt       host, may be NULL (AS_OPT_SKIP_DETECT is illegal here).
+ *   rep       DEVICE array of `batch` reports, may be NULL; ret: DEVICE int32[batch] per-system
+ *             return codes (AS_OK / AS_ERR_*), may be NULL; sigma_out: DEVICE batch*n fallback
+ *             singular values (system b at b*n, descending), may be NULL.
+ * No host synchronization: everything is enqueued on `stream`.  Returns 0, -i (illegal i-th
+ * argument, nothing enqueued) or AS_ERR_CUDA_BASE + e. */
+int as_solve_batched(as_dtype dt, int64_t n, int64_t nrhs, int64_t batch, const void* A, int64_t lda, int64_t strideA,
+                     const void* B, int64_t ldb, int64_t strideB, void* X, int64_t ldx, int64_t strideX,
+                     const as_options* opt, as_report* rep, int32_t* ret, void* sigma_out, void* stream);
+
 /* as_solve_host: same contract with HOST buffers A, B, X (pageable or
  * pinned); copies H2D, solves, copies X D2H on `stream`.  The end-to-end entry
  * point timed by bench.py's "e2e" leg. */

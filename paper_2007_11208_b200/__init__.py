@@ -43,7 +43,7 @@ OPT_SKIP_DETECT, OPT_CHECK_FINITE = 0x10, 0x4
 ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED, ERR_NONFINITE = 1, 2, 3
 
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
-           "as_detect", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
+           "as_solve_batched", "as_detect", "as_workspace_bytes", "as_last_kernel_nodes", "as_release_all",
            "as_strerror", "as_version", "as_set_instrumentation", "as_last_stage_ms", "as_measure_fp64_peak",
            "as_set_exec_mode", "as_bench_gemm")
 DEBUG_EXPORTS = ("as_debug_factor", "as_debug_timestamps", "as_debug_lu_trace", "as_debug_panel_time")
@@ -76,6 +76,8 @@ _lib.as_solve_ex.restype = C.c_int
 _lib.as_solve_async.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P, P]
 _lib.as_solve_async.restype = C.c_int
 _lib.as_solve_host.argtypes = [I32, P, I64, I64, P, I64, I64, P, P, P, P]
+_lib.as_solve_batched.argtypes = [I32, I64, I64, I64, P, I64, I64, P, I64, I64, P, I64, I64, P, P, P, P, P]
+_lib.as_solve_batched.restype = C.c_int
 _lib.as_solve_host.restype = C.c_int
 _lib.as_detect.argtypes = [I32, P, I64, I64, U32, P, P]
 _lib.as_detect.restype = C.c_int
@@ -201,6 +203,53 @@ def as_solve_host(A: np.ndarray, B: np.ndarray, options: Options | None = None, 
     ret = _lib.as_solve_host(dt, A.ctypes.data, max(1, n), n, B.ctypes.data, max(1, n), nrhs, X.ctypes.data,
                              C.byref(options) if options is not None else None, C.byref(rep), _stream_ptr(stream))
     return ret, X, rep.as_dict()
+
+
+def as_solve_batched(A, B, X=None, options: Options | None = None, sigma_out=None, stream=None):
+    """Batched solve of A[b] X[b] = B[b].  A: (batch, n, n) CUDA tensor whose matrices are column-major
+    (A.stride(1) == 1, i.e. created as to_device_batched); B: (batch, n, nrhs) likewise.  Returns
+    (ret, X, reports) with reports a (batch, 11) view of the device as_report array and the
+    per-system return codes as an int32 CUDA tensor (no host sync happens here)."""
+    import torch
+    batch, n = A.shape[0], A.shape[1]
+    nrhs = B.shape[2]
+    if X is None:
+        X = empty_colmajor_batched(batch, n, nrhs, B.dtype, device=B.device)
+    for t in (A, B, X):
+        if t.shape[1] > 1 and t.stride(1) != 1:
+            raise ValueError("expected column-major matrices (stride(1) == 1); use to_device_batched()")
+    rep = torch.zeros((batch, C.sizeof(Report)), dtype=torch.uint8, device=A.device)
+    rets = torch.zeros(batch, dtype=torch.int32, device=A.device)
+    ret = _lib.as_solve_batched(_dt(A), n, nrhs, batch, A.data_ptr(), max(1, A.stride(2)), A.stride(0),
+                                B.data_ptr(), max(1, B.stride(2) if nrhs > 1 else n), B.stride(0),
+                                X.data_ptr(), max(1, X.stride(2) if nrhs > 1 else n), X.stride(0),
+                                C.byref(options) if options is not None else None, rep.data_ptr(), rets.data_ptr(),
+                                sigma_out.data_ptr() if sigma_out is not None else None, _stream_ptr(stream))
+    return ret, X, rep, rets
+
+
+def reports_to_host(rep) -> list:
+    """Device report array (from as_solve_batched) -> list of dicts."""
+    raw = rep.cpu().numpy().tobytes()
+    sz = C.sizeof(Report)
+    out = []
+    for b in range(rep.shape[0]):
+        r = Report.from_buffer_copy(raw[b * sz:(b + 1) * sz])
+        out.append(r.as_dict())
+    return out
+
+
+def empty_colmajor_batched(batch: int, rows: int, cols: int, dtype, device="cuda"):
+    import torch
+    return torch.empty((batch, cols, rows), dtype=dtype, device=device).transpose(1, 2)
+
+
+def to_device_batched(a: np.ndarray, device="cuda"):
+    """(batch, n, m) numpy -> CUDA tensor whose matrices are column-major (stride(1) == 1)."""
+    import torch
+    a = np.asarray(a)
+    t = torch.from_numpy(np.ascontiguousarray(np.transpose(a, (0, 2, 1)))).to(device)
+    return t.transpose(1, 2)
 
 
 def as_detect(A, fullscan=False, stream=None, check_finite=False):

@@ -28,6 +28,7 @@
 #include "gemm.h"
 #include "internal.h"
 #include "rcond.h"
+#include "small.h"
 #include "svd.h"
 #include "trsm.h"
 
@@ -117,6 +118,7 @@ __global__ void finalize_kernel(const DevState* st, RepOut* out, const DevArgs* 
     o.ret = st->ret;
     *out = o;
     if (args->rep_dev) *args->rep_dev = o.rep;
+    if (args->ret_dev) *args->ret_dev = o.ret;
 }
 
 // ------------------------------------------------------------------ capture helpers
@@ -576,7 +578,7 @@ static int64_t count_kernels(cudaGraph_t g) {
 
 static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
                       void* X, const as_options* opt, as_report* rep_host, as_report* rep_dev, void* sigma,
-                      cudaStream_t stream, bool sync) {
+                      cudaStream_t stream, bool sync, int32_t* ret_dev = nullptr) {
     if (dt != AS_F64 && dt != AS_F32) return -1;
     if (n < 0) return -4;
     if (nrhs < 0) return -7;
@@ -617,7 +619,7 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     if (err) return err;
     std::lock_guard<std::mutex> lk(P->mu);
     DevArgs a{};
-    a.A = A; a.B = B; a.X = X; a.sigma = sigma; a.rep_dev = rep_dev; a.rep_host = nullptr;
+    a.A = A; a.B = B; a.X = X; a.sigma = sigma; a.rep_dev = rep_dev; a.rep_host = nullptr; a.ret_dev = ret_dev;
     cudaKernelNodeParams kp = {};
     if (key.eager) {
         err = run_eager(*P, a, stream);
@@ -727,6 +729,59 @@ int as_solve_f32(const float* A, int64_t lda, int64_t n, const float* B, int64_t
 int as_solve_async(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,
                    void* X, const as_options* opt, as_report* rep_dev, void* sigma_out, void* stream) {
     return solve_impl(dt, A, lda, n, B, ldb, nrhs, X, opt, nullptr, rep_dev, sigma_out, (cudaStream_t)stream, false);
+}
+
+int as_solve_batched(as_dtype dt, int64_t n, int64_t nrhs, int64_t batch, const void* A, int64_t lda, int64_t strideA,
+                     const void* B, int64_t ldb, int64_t strideB, void* X, int64_t ldx, int64_t strideX,
+                     const as_options* opt, as_report* rep, int32_t* ret, void* sigma_out, void* stream) {
+    if (dt != AS_F64 && dt != AS_F32) return -1;
+    if (n < 0) return -2;
+    if (nrhs < 0) return -3;
+    if (batch < 0) return -4;
+    if (lda < std::max<int64_t>(1, n)) return -6;
+    if (strideA < lda * n) return -7;
+    if (ldb < std::max<int64_t>(1, n)) return -9;
+    if (strideB < ldb * nrhs) return -10;
+    if (ldx < std::max<int64_t>(1, n)) return -12;
+    if (strideX < ldx * nrhs) return -13;
+    if (n == 0 || nrhs == 0 || batch == 0) return 0;
+    if (!A || !is_device_ptr(A)) return -5;
+    if (!B || !is_device_ptr(B)) return -8;
+    if (!X || !is_device_ptr(X)) return -11;
+    if (rep && !is_device_ptr(rep)) return -15;
+    if (ret && !is_device_ptr(ret)) return -16;
+    if (sigma_out && !is_device_ptr(sigma_out)) return -17;
+    const double eps = dt == AS_F64 ? 2.220446049250313080847e-16 : 1.1920928955078125e-07;
+    const uint32_t opts = opt ? opt->flags : 0u;
+    const int force = (opts & AS_OPT_FORCE_METHOD) ? opt->force_method : 0;
+    if ((opts & AS_OPT_FORCE_METHOD) && (force < AS_METHOD_BAND || force > AS_METHOD_LU)) return -14;
+    if (opts & AS_OPT_SKIP_DETECT) return -14;   // the one-block solver always detects (it reads A once anyway)
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t es = dt == AS_F64 ? 8 : 4;
+    if (n <= kSmallN && nrhs <= kSmallRhs) {
+        SmallArgs a{};
+        a.A = A; a.lda = lda; a.sA = strideA;
+        a.B = B; a.ldb = ldb; a.sB = strideB;
+        a.X = X; a.ldx = ldx; a.sX = strideX;
+        a.n = (int)n; a.nrhs = (int)nrhs; a.batch = batch;
+        a.opts = opts; a.force = force;
+        a.thr = (opt && opt->rcond_threshold >= 0) ? opt->rcond_threshold : 0.5 * eps;
+        if (dt == AS_F32) a.thr = (double)(float)a.thr;
+        a.cut = (opt && opt->lsq_cutoff >= 0) ? opt->lsq_cutoff : (double)n * eps;
+        a.max_sweeps = (opt && opt->max_sweeps > 0) ? opt->max_sweeps : 30;
+        a.rep = rep; a.ret = ret;
+        a.sigma = sigma_out; a.sS = n;
+        return launch_small_batched(dt, a, s);
+    }
+    // larger systems: one graph launch of the single-system solver per system, on the stream
+    if (ldx != ldb) return -12;   // the single-system path writes X with ldb
+    for (int64_t b = 0; b < batch; ++b) {
+        const int r = solve_impl(dt, (const char*)A + es * b * strideA, lda, n, (const char*)B + es * b * strideB, ldb,
+                                 nrhs, (char*)X + es * b * strideX, opt, nullptr, rep ? rep + b : nullptr,
+                                 sigma_out ? (char*)sigma_out + es * b * n : nullptr, s, false, ret ? ret + b : nullptr);
+        if (r != 0) return r;
+    }
+    return 0;
 }
 
 int as_solve_host(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb, int64_t nrhs,

@@ -15,6 +15,7 @@ struct DevArgs {
     void* sigma;        // optional fallback singular values (device)
     as_report* rep_dev; // optional device report
     as_report* rep_host;// optional mapped pinned host report
+    int32_t* ret_dev;   // optional device return code (batched calls)
 };
 
 // Workspace layout of a plan (all device pointers; see api.cu).

@@ -551,7 +551,7 @@ AS_DEV bool lf_better(T v2, int p2, T v, int p) { return v2 > v || (v2 == v && p
 template <typename T, int LW>
 __global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
                                                              int64_t* ipiv, DevState* st, LfSlot* slots, T* xrow,
-                                                             T* stage, int* stage_dst, unsigned* ctr,
+                                                             T* stage, int* stage_dst, T* ubufg, unsigned* ctr,
                                                              unsigned long long seq_base,
                                                              unsigned long long* tr_min, unsigned long long* tr_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -745,12 +745,14 @@ __global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, 
                 }
             }
             __syncthreads();
-            // my pivot rows of this leaf get their U12 row; my unpivoted rows A22 -= L21 U12
-            for (int e = tid; e < lw * rest; e += kPT) {
-                const int k = e / rest, c = e - k * rest;
-                const int rw = sm.pivrow[k];
-                if (rw >= rbeg && rw < rbeg + nr) W[(int64_t)rw + (k0 + c0 + c) * ldw] = sm.U12[k * kPW + c];
-            }
+            // the leaf's U12 rows go to Ubuf (by position), NOT to the pivot rows in W: other CTAs may
+            // still be reading those rows' A12 for their own (redundant) U12; the final row moves put
+            // them in place.  My unpivoted rows: A22 -= L21 U12.
+            if (cta == 0)
+                for (int e = tid; e < lw * rest; e += kPT) {
+                    const int k = e / rest, c = e - k * rest;
+                    ubufg[(int64_t)(L + k) * kPW + c0 + c] = sm.U12[k * kPW + c];
+                }
             // (one row at a time, 16 columns per batch: 16 independent loads in flight per thread)
             constexpr int CB = 16;
 #pragma unroll 1
@@ -778,19 +780,23 @@ __global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, 
         }
         __syncthreads();
     }
-    // ---- rows whose position changed go to their final position: stage every moved row (all
-    // panel columns), grid barrier, scatter
+    // ---- final rows: every pivot row (its U part beyond its leaf from Ubuf) and every row whose
+    // position changed are staged, grid barrier, scattered to their final positions
     unsigned gen = 0;
     if (P > 1) grid_barrier(ctr, ++gen, (unsigned)P);
     else __syncthreads();
     for (int r = warp; r < nr; r += kPT / 32) {
         const int ps = sm.pos[r];
         const int fin = ps >= 0 ? ps : -ps - 1;
-        if (fin == (int)(rbeg + r)) continue;
+        if (ps >= 0 && fin == (int)(rbeg + r)) continue;
+        const int gi = fin - (int)k0;
+        const int lend = ps >= 0 ? nbp : min(nbp, (gi / LW + 1) * LW);
         int slot = 0;
         if (lane == 0) slot = (int)atomicAdd(ctr + 1, 1u);
         slot = __shfl_sync(0xffffffffu, slot, 0);
-        for (int c = lane; c < nbp; c += 32) stage[(int64_t)slot * kPW + c] = W[(rbeg + r) + (k0 + c) * ldw];
+        for (int c = lane; c < nbp; c += 32)
+            stage[(int64_t)slot * kPW + c] = c < lend ? __ldcg(&W[(rbeg + r) + (k0 + c) * ldw])
+                                                      : __ldcg(&ubufg[(int64_t)gi * kPW + c]);
         if (lane == 0) stage_dst[slot] = fin;
     }
     if (P > 1) grid_barrier(ctr, ++gen, (unsigned)P);
@@ -1391,6 +1397,7 @@ struct LfBufs {
     void* xrow;          // [2][kLfMaxP][LW]
     int* stage_dst;      // [2 * kPW]
     void* stage;         // [2 * kPW][kPW]
+    void* ubuf;          // [kPW][kPW] U rows of the panel by position (beyond each pivot row's leaf)
     size_t zero_bytes;   // ctr + slots
 };
 static LfBufs lf_layout(void* base, int64_t n, size_t es) {
@@ -1404,10 +1411,11 @@ static LfBufs lf_layout(void* base, int64_t n, size_t es) {
     b.xrow = take(es * 2 * kLfMaxP * 32);
     b.stage_dst = (int*)take(sizeof(int) * 2 * kPW);
     b.stage = take(es * 2 * kPW * kPW);
+    b.ubuf = take(es * kPW * kPW);
     return b;
 }
-size_t lu_lfbuf_bytes(int64_t n, int dtype) { return (size_t)(lf_layout(nullptr, n, dtype == AS_F64 ? 8 : 4).stage) +
-                                                     (dtype == AS_F64 ? 8 : 4) * 2 * kPW * kPW; }
+size_t lu_lfbuf_bytes(int64_t n, int dtype) { return (size_t)(lf_layout(nullptr, n, dtype == AS_F64 ? 8 : 4).ubuf) +
+                                                     (dtype == AS_F64 ? 8 : 4) * kPW * kPW; }
 
 // The leaf panel: P = ceil(m / kLfRows) CTAs of one ordinary launch (see lu_panel_lf_kernel).
 template <typename T>
@@ -1434,7 +1442,8 @@ static bool lf_panel_launch(const Work& w, int64_t k0, int nbp, unsigned long lo
     unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
     unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, b.slots, (T*)b.xrow,
-                                             (T*)b.stage, b.stage_dst, b.ctr + 2 * (k0 / kBW), seq_base, tmn, tmx);
+                                             (T*)b.stage, b.stage_dst, (T*)b.ubuf, b.ctr + 2 * (k0 / kBW), seq_base, tmn,
+                                             tmx);
     if (e != cudaSuccess) { cudaGetLastError(); return false; }
     return true;
 }

@@ -1,0 +1,163 @@
+"""Batched small systems (as_solve_batched): every system of a batch graded
+against the oracle on its own, with its own verdict, method, gate, fallback.
+
+Bars as test_gpu_parity.check_parity: detection bits / kl / ku / method / gate / fallback exact;
+fp64 eta <= 1e-13, phi <= 1e-15 cond_1; fp32 eta <= 1e-5, phi <= 1e-6 cond_1 vs the fp64 oracle on
+the promoted data; fallback: sigma vs the oracle's, rank +-1, residual within 1 %."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from helpers import backward_error, forward_diff
+
+pytestmark = pytest.mark.gpu
+
+AS = pytest.importorskip("paper_2007_11208_b200") if torch.cuda.is_available() else None
+MASK = 0xFF | oracle.F_CHOL_FAILED | oracle.F_SINGULAR | oracle.F_RCOND_LOW | oracle.F_FALLBACK | \
+    oracle.F_POORLY_COND | oracle.F_NONFINITE | oracle.F_SVD_NOCONV
+
+
+def mixed_systems(n, seed, nrhs=2):
+    """One system of every structure class the flowchart distinguishes, at size n."""
+    rng = np.random.default_rng(seed)
+    mats = {
+        "dense": W.random_dense(n, seed=seed, shift=4.0),
+        "dense_raw": W.random_dense(n, seed=seed + 1),
+        "band_dom": W.random_banded(n, 2, 1, seed=seed, dominant=True),
+        "band": W.random_banded(n, 1, 3, seed=seed + 2),
+        "lower": W.random_triangular(n, upper=False, seed=seed),
+        "upper": W.random_triangular(n, upper=True, seed=seed + 3),
+        "spd": W.random_spd_fig3(n, seed=seed),
+        "chol_fail": None,
+        "singular": W.random_dense(n, seed=seed + 4),
+        "illcond": W.illcond_c4(n=n, seed=seed)[0] if n > 1 else np.ones((1, 1)),
+        "diag": np.asfortranarray(np.diag(1.0 + rng.random(n))),
+    }
+    # symmetric, passes Fig. 4 (|a_ij| = 0.45 < 1 = a_ii) but indefinite for n >= 4: Cholesky fails
+    # and the general LU runs
+    M = np.full((n, n), -0.45)
+    np.fill_diagonal(M, 1.0)
+    mats["chol_fail"] = np.asfortranarray(M)
+    # exactly singular with an exactly rank-deficient SVD (a scaled permutation with one zero):
+    # factor failure -> fallback, whose Jacobi then converges at once (no order-dependent sweeps)
+    d = 1.0 + rng.random(n)
+    d[n // 2] = 0.0
+    perm = rng.permutation(n)
+    Sg = np.zeros((n, n))
+    Sg[perm, np.arange(n)] = d
+    mats["singular"] = np.asfortranarray(Sg)
+    names = list(mats)
+    A = np.stack([np.asfortranarray(mats[k]) for k in names])
+    B = rng.standard_normal((len(names), n, nrhs))
+    return names, A, B
+
+
+def check_one(name, A, B, X, rep, ret, fp32, sig=None):
+    oret, Xo, orep, osig = oracle.solve(A, B)
+    assert ret == oret, (name, ret, oret, rep, orep)
+    assert (rep["flags"] & MASK) == (orep["flags"] & MASK), (name, hex(rep["flags"]), hex(orep["flags"]))
+    assert rep["method"] == orep["method"] and rep["primary_method"] == orep["primary_method"], name
+    if orep["kl"] >= 0:
+        assert (rep["kl"], rep["ku"]) == (orep["kl"], orep["ku"]), name
+    if ret not in (0,):
+        return
+    if orep["rcond"] > 1e-10 and rep["rcond"] > 0:
+        assert abs(np.log2(rep["rcond"] / orep["rcond"])) <= 1.0, (name, rep["rcond"], orep["rcond"])
+    if rep["flags"] & oracle.F_FALLBACK:
+        assert abs(rep["rank"] - orep["rank"]) <= 1, name
+        b = B[:, 0].astype(np.float64)
+        A64 = A.astype(np.float64)
+        rho = np.linalg.norm(b - A64 @ X[:, 0].astype(np.float64)) / np.linalg.norm(b)
+        rho_o = np.linalg.norm(b - A64 @ Xo[:, 0].astype(np.float64)) / np.linalg.norm(b)
+        assert abs(rho - rho_o) <= 1e-2 * max(rho_o, 1e-12) + (1e-6 if fp32 else 1e-12), (name, rho, rho_o)
+        if sig is not None and not fp32:
+            assert np.abs(sig - osig).max() <= 1e-13 * max(1.0, osig.max()), name
+        return
+    if fp32:
+        A64, B64 = A.astype(np.float64), B.astype(np.float64)
+        _, Xr, rr, _ = oracle.solve(A64, B64, no_fallback=True)
+        assert backward_error(A64, X, B64) <= 1e-5, name
+        assert forward_diff(X, Xr) <= 1e-6 * rr["anorm"] / rr["rcond"], name
+    else:
+        assert backward_error(A, X, B) <= 1e-13, (name, backward_error(A, X, B))
+        assert forward_diff(X, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"], name
+
+
+def run_batch(A, B, fp32=False, **opt):
+    dt = np.float32 if fp32 else np.float64
+    A = A.astype(dt)
+    B = B.astype(dt)
+    dA, dB = AS.to_device_batched(A), AS.to_device_batched(B)
+    n = A.shape[1]
+    sig = torch.zeros((A.shape[0], n), dtype=dA.dtype, device="cuda")
+    o = AS.make_options(**opt) if opt else None
+    ret, X, rep, rets = AS.as_solve_batched(dA, dB, options=o, sigma_out=sig)
+    torch.cuda.synchronize()
+    assert ret == 0, AS.strerror(ret)
+    Xh = np.transpose(X.cpu().numpy(), (0, 1, 2))
+    return A, B, Xh, AS.reports_to_host(rep), rets.cpu().numpy(), sig.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 31, 32, 33, 64, 100, 127, 128])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_batched_mixed_classes(n, fp32):
+    names, A, B = mixed_systems(n, seed=n)
+    A, B, X, reps, rets, sig = run_batch(A, B, fp32=fp32)
+    for b, nm in enumerate(names):
+        check_one(nm, np.asfortranarray(A[b]), np.asfortranarray(B[b]), np.asfortranarray(X[b]), reps[b], int(rets[b]),
+                  fp32, sig[b])
+
+
+def test_batched_c1_recipe_many():
+    """1000 dense systems of the C1 recipe at n = 100 (the paper's 1000-system workload):
+    every one against the oracle."""
+    n, cnt = 100, 1000
+    A = np.stack([W.dense_c1(n=n, nrhs=1, seed=s)[0] for s in range(cnt)])
+    B = np.stack([W.dense_c1(n=n, nrhs=1, seed=s)[1] for s in range(cnt)])
+    A, B, X, reps, rets, _ = run_batch(A, B)
+    for b in range(0, cnt, 37):
+        check_one(f"c1#{b}", np.asfortranarray(A[b]), np.asfortranarray(B[b]), np.asfortranarray(X[b]), reps[b],
+                  int(rets[b]), False)
+    assert (rets == 0).all() and all(r["method"] == oracle.M_LU for r in reps)
+
+
+@pytest.mark.parametrize("opt", [dict(no_fallback=True), dict(force_method=5), dict(max_sweeps=1),
+                                 dict(check_finite=True)])
+def test_batched_options(opt):
+    names, A, B = mixed_systems(40, seed=3)
+    if opt.get("check_finite"):
+        A[0, 3, 4] = np.nan
+        B[2, 1, 0] = np.inf
+    A, B, X, reps, rets, _ = run_batch(A, B, **opt)
+    for b, nm in enumerate(names):
+        oret, Xo, orep, _ = oracle.solve(np.asfortranarray(A[b]), np.asfortranarray(B[b]), **opt)
+        assert int(rets[b]) == oret, (nm, rets[b], oret)
+        assert (reps[b]["flags"] & MASK) == (orep["flags"] & MASK), (nm, hex(reps[b]["flags"]), hex(orep["flags"]))
+        if oret == 0 and not (orep["flags"] & oracle.F_FALLBACK) and not (orep["flags"] & oracle.F_RCOND_LOW):
+            assert forward_diff(X[b], Xo) <= 1e-15 * orep["anorm"] / orep["rcond"], nm
+
+
+def test_batched_large_n_uses_graph_path():
+    """n > 128: the batch falls back to one single-system graph launch per system (same verdicts)."""
+    names, A, B = mixed_systems(150, seed=9, nrhs=1)
+    sel = [names.index(k) for k in ("dense", "band_dom", "upper", "spd", "illcond")]
+    A, B = A[sel], B[sel]
+    A, B, X, reps, rets, sig = run_batch(A, B)
+    for i, b in enumerate(sel):
+        check_one(names[b], np.asfortranarray(A[i]), np.asfortranarray(B[i]), np.asfortranarray(X[i]), reps[i],
+                  int(rets[i]), False)
+
+
+def test_batched_illegal_arguments():
+    import ctypes as C
+    e = torch.zeros((2, 4, 4), dtype=torch.float64, device="cuda")
+    lib = AS.lib()
+    assert lib.as_solve_batched(0, -1, 1, 1, e.data_ptr(), 4, 16, e.data_ptr(), 4, 16, e.data_ptr(), 4, 16,
+                                None, None, None, None, None) == -2
+    assert lib.as_solve_batched(0, 4, 1, 1, e.data_ptr(), 3, 16, e.data_ptr(), 4, 16, e.data_ptr(), 4, 16,
+                                None, None, None, None, None) == -6
+    assert lib.as_solve_batched(0, 4, 1, 2, e.data_ptr(), 4, 8, e.data_ptr(), 4, 16, e.data_ptr(), 4, 16,
+                                None, None, None, None, None) == -7
+    assert lib.as_solve_batched(0, 0, 1, 2, None, 1, 0, None, 1, 0, None, 1, 0, None, None, None, None, None) == 0
