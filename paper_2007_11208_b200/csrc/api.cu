@@ -355,6 +355,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.bars = (unsigned*)take(4 * w.bars_len);
     w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * 128 + es * 2 * 128);   // LU panel slots, rowbuf, diagbuf (128-wide)
     w.lfbuf = take(lu_lfbuf_bytes(n, w.dtype));
+    w.linv = take(es * (size_t)((n + 127) / 128) * 128 * 128);
     return off;
 }
 
@@ -403,11 +404,13 @@ static int build_graph(Plan& P) {
             launch_band_norm(w, s);
             cudaGraphConditionalHandle h_bm = make_handle(s, 0);
             launch_band_dominance(w, h_bm, s);
-            // SWITCH: 0 sequential GBTRF path, 1 + c partitioned path with K class 2^c
-            cudaGraph_t* bb = add_cond(s, h_bm, cudaGraphCondTypeSwitch, 5);
+            // SWITCH: 0 sequential GBTRF path, 1 + c partitioned path with K class 2^c, 5 the
+            // register chain for kl, ku <= 3
+            cudaGraph_t* bb = add_cond(s, h_bm, cudaGraphCondTypeSwitch, 6);
             B.body(bb[0], [&](cudaStream_t s2) { body_factor(w, AS_METHOD_BAND, B.sa, s2); });
             for (int c = 0; c < 4; ++c)
                 B.body(bb[1 + c], [&](cudaStream_t s2) { body_factor(w, kBandSpike + c, B.sa, s2); });
+            B.body(bb[5], [&](cudaStream_t s2) { launch_band_chain(w, s2); });
         });
         B.body(mb[AS_METHOD_CHOL], [&](cudaStream_t s) {
             launch_chol_factor(w, s);
@@ -528,7 +531,8 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
         launch_band_norm(w, s);
         launch_band_dominance(w, 0, s);
         if ((err = rd())) return err;
-        body_factor(w, h.band_use_spike ? kBandSpike + h.band_use_spike - 1 : AS_METHOD_BAND, sa, s);
+        if (h.band_chain) launch_band_chain(w, s);
+        else body_factor(w, h.band_use_spike ? kBandSpike + h.band_use_spike - 1 : AS_METHOD_BAND, sa, s);
     } else {
         body_factor(w, h.method, sa, s);
     }

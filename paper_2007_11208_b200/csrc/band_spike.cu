@@ -837,7 +837,12 @@ __global__ void band_mode_kernel(const DevArgs* args, DevState* st, cudaGraphCon
                     (const void*)args->X != args->B;
     st->band_fast = 0;
     st->band_use_spike = use ? 1 + cbit : 0;      // 1 + K class index (SWITCH value; 0 = sequential)
-    if (h) cudaGraphSetConditional(h, use ? (unsigned)(1 + cbit) : 0u);
+    // not partitioned, kl, ku <= 3 (tridiagonal, the paper's 5-diagonal class): the register chain
+    // (band_chain.cu, SWITCH value 5); it writes X before the gate, so not for X == B either
+    const int chain = !use && st->kl <= 3 && st->ku <= 3 && st->primary == AS_METHOD_BAND &&
+                      (const void*)args->X != args->B ? 1 + 4 * st->kl + st->ku : 0;
+    st->band_chain = chain;
+    if (h) cudaGraphSetConditional(h, use ? (unsigned)(1 + cbit) : chain ? 5u : 0u);
 }
 
 // ------------------------------------------------------------------ host side

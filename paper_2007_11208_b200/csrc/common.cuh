@@ -64,7 +64,7 @@ struct DevState {
     unsigned band_dom;            // bit0: strictly row dominant, bit1: strictly column dominant
     int32_t band_use_spike;       // partitioned solver selected
     int32_t band_fast;            // partitioned solver already produced X
-    int32_t pad2;
+    int32_t band_chain;           // narrow-band chain path selected: 1 + 4 kl + ku (kl, ku <= 3), else 0
     unsigned long long dbg_t[16]; // %globaltimer phase stamps (diagnostics)
     // ---- barriers / counters (zeroed per solve)
     uint32_t bar[4];

@@ -43,6 +43,7 @@ struct Work {
     int64_t bars_len;
     void* cand;          // LU panel candidates
     void* lfbuf;         // leaf LU panel: counters, exchange slots, candidate rows, row-move staging
+    void* linv;          // LU: full 128 x 128 inverse of each block's unit-lower L11 (n/128 blocks)
     int num_sms;
 };
 
@@ -52,5 +53,6 @@ void launch_state_init(const Work& w, cudaStream_t s, uint32_t opts, int force_m
 void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite = false);
 void launch_dispatch(const Work& w, cudaStream_t s, cudaGraphConditionalHandle h_method);
 void launch_copy_b_to_x(const Work& w, cudaStream_t s);   // band.cu
+void launch_band_chain(const Work& w, cudaStream_t s);    // band_chain.cu: kl, ku <= 3 (factor + rcond + X)
 
 }  // namespace as

@@ -1024,6 +1024,134 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
         W[(k0 + row) + (cc0 + c) * ldw] = Bn[c * kSULD + row];
     }
 }
+// ------------------------------------------------------------------ fused interchanges + U12 (v2)
+// The block's full 128 x 128 inverse L11^{-1} = [La^{-1} 0; -Lc^{-1} Lb La^{-1}  Lc^{-1}] is formed once
+// per block (linv128_kernel, after the panel) so that U12 = L11^{-1} A12 is ONE product per column
+// tile; a CTA takes 64 trailing columns: the interchanges composed into one permutation (as above),
+// every moved value gathered before any store, then U12 = L11^{-1} Bn with L11^{-1} streamed through
+// L1 (4 rows x 8 columns per thread).
+constexpr int kSU2C = 64;
+constexpr int kSU2LD = kBW + 1;
+template <typename T>
+__global__ void __launch_bounds__(256) linv128_kernel(const T* W, int64_t ldw, int64_t k0, int bw, const T* Dinv,
+                                                      T* Linv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Ai = (T*)smem_raw;
+    T* Ci = Ai + kB64 * kB64;
+    T* Lb = Ci + kB64 * kB64;
+    T* T1 = Lb + kB64 * kB64;
+    const int p1 = min(kB64, bw), p2 = bw - p1;
+    const T* Da = Dinv + (k0 / kB64) * (int64_t)kB64 * kB64;
+    for (int e = threadIdx.x; e < kB64 * kB64; e += 256) {
+        const int r = e & 63, c = e >> 6;
+        Ai[e] = Da[e];
+        Ci[e] = p2 > 0 ? Da[kB64 * kB64 + e] : T(0);
+        Lb[e] = (p2 > 0 && r < p2 && c < p1) ? W[(k0 + kB64 + r) + (k0 + c) * ldw] : T(0);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kB64 * kB64; e += 256) {          // T1 = Lb La^{-1}
+        const int r = e & 63, c = e >> 6;
+        T acc = T(0);
+        for (int k = 0; k < kB64; ++k) acc += Lb[r + k * kB64] * Ai[k + c * kB64];
+        T1[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kBW * kBW; e += 256) {
+        const int r = e & (kBW - 1), c = e >> 7;
+        T v;
+        if (r < kB64) v = c < kB64 ? (r == c ? T(1) : Ai[r + c * kB64]) : T(0);
+        else if (c >= kB64) v = r == c ? T(1) : Ci[(r - kB64) + (c - kB64) * kB64];
+        else {                                                        // -Lc^{-1} (Lb La^{-1})
+            T acc = T(0);
+            for (int k = 0; k < kB64; ++k) acc += Ci[(r - kB64) + k * kB64] * T1[k + c * kB64];
+            v = -acc;
+        }
+        if (r >= bw || c >= bw) v = r == c ? T(1) : T(0);
+        Linv[e] = v;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) swap_u12v2_kernel(T* W, int64_t ldw, int64_t k0, int bw, int64_t c0, int64_t c1,
+                                                        const int64_t* ipiv, const T* __restrict__ Linv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Bn = (T*)smem_raw;                // [kSU2C][kSU2LD]: column c of the block rows after the interchanges
+    T* Ex = Bn + kSU2C * kSU2LD;         // [kSU2C][kSU2LD]: values for the rows leaving the block
+    __shared__ int64_t piv[kBW];
+    __shared__ int64_t srow[2 * kBW];
+    __shared__ int64_t edst[kBW];
+    __shared__ int s_ne;
+    const int64_t cc0 = c0 + (int64_t)blockIdx.x * kSU2C;
+    const int nc = (int)min<int64_t>(kSU2C, c1 - cc0);
+    if (nc <= 0) return;
+    if (threadIdx.x == 0) s_ne = 0;
+    for (int q = threadIdx.x; q < bw; q += blockDim.x) piv[q] = ipiv[k0 + q];
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * bw; t += blockDim.x) {
+        int64_t x;
+        if (t < bw) x = k0 + t;
+        else {
+            x = piv[t - bw];
+            if (x < k0 + bw) continue;
+            bool first = true;
+            for (int q = 0; q < t - bw; ++q) first = first && (piv[q] != x);
+            if (!first) continue;
+        }
+        int64_t pos = x;
+        for (int q = 0; q < bw; ++q) {
+            const int64_t r = k0 + q, tq = piv[q];
+            if (pos == r) pos = tq;
+            else if (pos == tq) pos = r;
+        }
+        if (pos < k0 + bw) srow[pos - k0] = x;
+        else { const int e = atomicAdd(&s_ne, 1); edst[e] = pos; srow[bw + e] = x; }
+    }
+    __syncthreads();
+    const int ne = s_ne, R = bw + ne;
+    batched<16, T>(
+        R * nc, [&](int e) -> T { const int c = e / R, row = e - c * R; return W[srow[row] + (cc0 + c) * ldw]; },
+        [&](int e, T v) {
+            const int c = e / R, row = e - c * R;
+            if (row < bw) Bn[c * kSU2LD + row] = v;
+            else Ex[c * kSU2LD + row - bw] = v;
+        });
+    __syncthreads();
+    for (int e = threadIdx.x; e < ne * nc; e += blockDim.x) {
+        const int c = e / ne, row = e - c * ne;
+        W[edst[row] + (cc0 + c) * ldw] = Ex[c * kSU2LD + row];
+    }
+    // U12 = L11^{-1} Bn: lane -> rows lane + 32 i, warp -> columns 8 warp .. 8 warp + 7
+    const int lane = threadIdx.x & 31, cg = (threadIdx.x >> 5) * 8;
+    T acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[i][u] = T(0);
+    const int kmax = min(bw, 96 + lane + 1);            // L11^{-1} is lower triangular: k <= row
+    for (int k = 0; k < kmax; ++k) {
+        T l[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) l[i] = __ldg(&Linv[(lane + 32 * i) + k * kBW]);
+        T bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bv[u] = Bn[(cg + u) * kSU2LD + k];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[i][u] += l[i] * bv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int c = cg + u;
+        if (c >= nc) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = lane + 32 * i;
+            if (r < bw) W[(k0 + r) + (cc0 + c) * ldw] = acc[i][u];
+        }
+    }
+}
+
 // ------------------------------------------------------------------ small n: one-cluster LU
 // xGETRF for n <= kSmN (C1) in ONE launch: a cluster of P = ceil(n/64) CTAs, CTA c owns the
 // column block [64c, 64c+64).  512 threads: thread (r, h) = row r, columns 32h .. 32h+31 of the
@@ -1527,11 +1655,25 @@ static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
     const int smem = (int)(sizeof(T) * (2 * kB64 * kB64LD + 3 * 256));
     cudaFuncSetAttribute(lu_linv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     lu_linv_kernel<T><<<(nbp + kB64 - 1) / kB64, 256, smem, s>>>((const T*)w.W, w.ldw, k0, nbp, (T*)w.Dinv0);
+    if (w.linv && k0 + nbp < w.n) {      // the full block inverse for the fused interchanges + U12
+        const int sm2 = (int)(sizeof(T) * 4 * kB64 * kB64);
+        cudaFuncSetAttribute(linv128_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+        linv128_kernel<T><<<1, 256, sm2, s>>>((const T*)w.W, w.ldw, k0, nbp, (const T*)w.Dinv0,
+                                             (T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW);
+    }
 }
 
 template <typename T>
 static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s) {
     if (c1 <= c0) return;
+    static const bool v1 = getenv("AS_LU_SWAP_V1") != nullptr;
+    if (w.linv && !v1) {
+        const int smem = (int)(sizeof(T) * 2 * kSU2C * kSU2LD);
+        cudaFuncSetAttribute(swap_u12v2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        swap_u12v2_kernel<T><<<(unsigned)((c1 - c0 + kSU2C - 1) / kSU2C), 256, smem, s>>>(
+            (T*)w.W, w.ldw, k0, bw, c0, c1, w.ipiv, (const T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW);
+        return;
+    }
     const int smem = (int)(sizeof(T) * (2 * kSUC * kSULD + 3 * kB64 * kB64));
     cudaFuncSetAttribute(swap_u12_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     swap_u12_kernel<T><<<(unsigned)((c1 - c0 + kSUC - 1) / kSUC), 256, smem, s>>>((T*)w.W, w.ldw, k0, bw, c0, c1, w.ipiv,

