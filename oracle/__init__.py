@@ -28,6 +28,9 @@ F_POORLY_COND, F_NONFINITE, F_SVD_NOCONV, F_RANK_DEF = 1 << 12, 1 << 13, 1 << 14
 M_BAND, M_TRI_LOWER, M_TRI_UPPER, M_CHOL, M_LU, M_SVD = 1, 2, 3, 4, 5, 6
 OPT_NO_FALLBACK, OPT_FORCE_METHOD, OPT_FULLSCAN = 0x1, 0x2, 0x8
 OPT_CHECK_FINITE = 0x4
+OPT_SYM_INDEF = 0x20
+M_LDLT = 7
+F_SYMMETRIC = 1 << 16
 ERR_NONFINITE = 3
 F_NONFINITE = 1 << 13
 ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED = 1, 2
@@ -79,6 +82,8 @@ def lib():
             g("or_getrf").argtypes = [P, I64, I64, P]; g("or_getrf").restype = I64
             g("or_getrs").argtypes = [P, I64, I64, P, P, I64, I64]
             g("or_potrf").argtypes = [P, I64, I64]; g("or_potrf").restype = I64
+            g("or_sytrf").argtypes = [P, I64, I64, P]; g("or_sytrf").restype = I64
+            g("or_sytrs").argtypes = [P, I64, I64, P, P, I64, I64]
             g("or_trsv").argtypes = [P, I64, I64, I, I, I, P]
             g("or_band_pack").argtypes = [P, I64, I64, I64, I64, P, I64]; g("or_band_pack").restype = D
             g("or_gbtrf").argtypes = [I64, I64, I64, P, I64, P]; g("or_gbtrf").restype = I64
@@ -194,6 +199,24 @@ def potrf(A):
     return np.tril(L), int(info)
 
 
+def sytrf(A):
+    """Bunch-Kaufman L D L^T (lower) of the oracle: (W, ipiv 0-based with -(kp+1) for 2x2 blocks, info)."""
+    W = _fortran(A).copy(order="F")
+    n = W.shape[0]
+    ipiv = np.zeros(n, dtype=np.int64)
+    info = _fn("or_sytrf", W)(_ptr(W), max(1, n), n, _ptr(ipiv))
+    return W, ipiv, int(info)
+
+
+def sytrs(W, ipiv, B):
+    W = _fortran(W)
+    X = _fortran(B).astype(W.dtype, copy=True).reshape(W.shape[0], -1, order="F")
+    n = W.shape[0]
+    _fn("or_sytrs", W)(_ptr(W), max(1, n), n, _ptr(np.ascontiguousarray(ipiv, dtype=np.int64)), _ptr(X), max(1, n),
+                       X.shape[1])
+    return X
+
+
 def trsv(A, b, upper: bool, trans: bool = False, unit: bool = False):
     A = _fortran(A)
     x = np.array(b, dtype=A.dtype, copy=True).reshape(-1)
@@ -278,7 +301,7 @@ def lsq_svd(A, B, cut=None, max_sweeps=30):
 
 # ---------------------------------------------------------------- solve
 def solve(A, B, *, no_fallback=False, force_method=None, fullscan=False, rcond_threshold=-1.0,
-          lsq_cutoff=-1.0, max_sweeps=30, check_finite=False):
+          lsq_cutoff=-1.0, max_sweeps=30, check_finite=False, sym_indef=False):
     """The adaptive solve (oracle_impl.h: or_solve).  Returns (ret, X, report dict, sigma)."""
     A = _fortran(A)
     B = _fortran(B).astype(A.dtype, copy=False)
@@ -287,7 +310,8 @@ def solve(A, B, *, no_fallback=False, force_method=None, fullscan=False, rcond_t
     sig = np.zeros(max(n, 1), dtype=A.dtype)
     o = Options()
     o.flags = (OPT_NO_FALLBACK if no_fallback else 0) | (OPT_FORCE_METHOD if force_method else 0) | \
-        (OPT_FULLSCAN if fullscan else 0) | (OPT_CHECK_FINITE if check_finite else 0)
+        (OPT_FULLSCAN if fullscan else 0) | (OPT_CHECK_FINITE if check_finite else 0) | \
+        (OPT_SYM_INDEF if sym_indef else 0)
     o.force_method = int(force_method or 0)
     o.rcond_threshold = rcond_threshold
     o.lsq_cutoff = lsq_cutoff

@@ -22,6 +22,7 @@
 #define OR_F_NONFINITE     (1u << 13)
 #define OR_F_SVD_NOCONV    (1u << 14)
 #define OR_F_RANK_DEF      (1u << 15)
+#define OR_F_SYMMETRIC     (1u << 16)   /* exact symmetry (only with OR_OPT_SYM_INDEF) */
 /* methods */
 #define OR_M_BAND 1
 #define OR_M_TRI_LOWER 2
@@ -29,11 +30,13 @@
 #define OR_M_CHOL 4
 #define OR_M_LU 5
 #define OR_M_SVD 6
+#define OR_M_LDLT 7   /* symmetric indefinite LDL^T, Bunch-Kaufman (OR_OPT_SYM_INDEF) */
 /* options */
 #define OR_OPT_NO_FALLBACK  0x1u
 #define OR_OPT_FORCE_METHOD 0x2u
 #define OR_OPT_CHECK_FINITE 0x4u
 #define OR_OPT_FULLSCAN     0x8u
+#define OR_OPT_SYM_INDEF    0x20u  /* exactly symmetric, not (or failed) sympd -> LDL^T (Z30) */
 /* errors */
 #define OR_ERR_SINGULAR_NO_FALLBACK 1
 #define OR_ERR_SVD_NOT_CONVERGED    2

@@ -96,6 +96,17 @@ static int FN(is_upper)(const T* A, int64_t lda, int64_t n)
     return 1;
 }
 
+/* Exact symmetry, A_ij == A_ji for every pair (IEEE compare: a NaN breaks it).  Evaluated only
+ * for the symmetric-indefinite specialisation the paper names as future work, which
+ * is an option (OR_OPT_SYM_INDEF, Z30). */
+static int FN(is_symmetric)(const T* A, int64_t lda, int64_t n)
+{
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = j + 1; i < n; ++i)
+            if (!(A[i + j * lda] == A[j + i * lda])) return 0;
+    return 1;
+}
+
 /* Band capacity count(n,kl,ku) = n(kl+ku+1) - kl(kl+1)/2 - ku(ku+1)/2 and
  * the 25% rule of P:339 ("more than 25% ... non-zero" -> non-banded):
  * banded <=> 4*count <= n^2, exact integer arithmetic (Z2, Z3). */
@@ -333,13 +344,151 @@ static void FN(getrs_vec)(const T* W, int64_t ld, int64_t n, const int64_t* ipiv
 }
 
 /* ------------------------------------------------------------------ */
+/* Symmetric indefinite LDL^T with Bunch-Kaufman pivoting (P:741-743,   */
+/* "plain symmetric matrices" as future work; the xSYTF2 algorithm,    */
+/* lower triangle, Z30)                                      */
+/* ------------------------------------------------------------------ */
+/* P A P^T = L D L^T with 1x1 and 2x2 diagonal blocks; only the lower
+ * triangle of W is read and overwritten (D on the block diagonal, the
+ * multipliers below).  ipiv (0-based): 1x1 block at k: ipiv[k] = kp (rows
+ * and columns k and kp interchanged); 2x2 block at k, k+1: ipiv[k] =
+ * ipiv[k+1] = -(kp + 1) (k+1 and kp interchanged).  alpha = (1+sqrt(17))/8.
+ * Returns 0, or 1+k for the first exactly zero (or NaN) pivot column. */
+static int64_t FN(sytrf)(T* W, int64_t ld, int64_t n, int64_t* ipiv)
+{
+#define WL(i, j) W[(i) + (j) * ld]
+    const T alpha = ((T)1 + SQRT((T)17)) / (T)8;
+    int64_t info = 0, k = 0;
+    while (k < n) {
+        int kstep = 1;
+        int64_t kp = k, imax = k;
+        const T absakk = ABS(WL(k, k));
+        T colmax = (T)0;
+        if (k < n - 1) {
+            imax = k + 1;
+            colmax = ABS(WL(k + 1, k));
+            for (int64_t i = k + 2; i < n; ++i) if (ABS(WL(i, k)) > colmax) { colmax = ABS(WL(i, k)); imax = i; }
+        }
+        if ((absakk > colmax ? absakk : colmax) == (T)0 || absakk != absakk) {
+            if (info == 0) info = k + 1;
+            kp = k;
+        } else {
+            if (absakk >= alpha * colmax) {
+                kp = k;
+            } else {
+                /* largest off-diagonal |.| in row imax: A(imax, k..imax-1), then column imax below */
+                int64_t jmax = k;
+                T rowmax = ABS(WL(imax, k));
+                for (int64_t j = k + 1; j < imax; ++j) if (ABS(WL(imax, j)) > rowmax) { rowmax = ABS(WL(imax, j)); jmax = j; }
+                if (imax < n - 1) {
+                    int64_t j2 = imax + 1;
+                    T m2 = ABS(WL(imax + 1, imax));
+                    for (int64_t i = imax + 2; i < n; ++i) if (ABS(WL(i, imax)) > m2) { m2 = ABS(WL(i, imax)); j2 = i; }
+                    if (m2 > rowmax) rowmax = m2;
+                    (void)j2;
+                }
+                (void)jmax;
+                if (absakk >= alpha * colmax * (colmax / rowmax)) kp = k;
+                else if (ABS(WL(imax, imax)) >= alpha * rowmax) kp = imax;
+                else { kp = imax; kstep = 2; }
+            }
+            const int64_t kk = k + kstep - 1;
+            if (kp != kk) {        /* interchange rows and columns kk and kp of A(k:n, k:n) */
+                for (int64_t i = kp + 1; i < n; ++i) { T t = WL(i, kk); WL(i, kk) = WL(i, kp); WL(i, kp) = t; }
+                for (int64_t j = kk + 1; j < kp; ++j) { T t = WL(j, kk); WL(j, kk) = WL(kp, j); WL(kp, j) = t; }
+                { T t = WL(kk, kk); WL(kk, kk) = WL(kp, kp); WL(kp, kp) = t; }
+                if (kstep == 2) { T t = WL(k + 1, k); WL(k + 1, k) = WL(kp, k); WL(kp, k) = t; }
+            }
+            if (kstep == 1) {
+                if (k < n - 1) {   /* A := A - d11 x x^T (xSYR), x = A(k+1:n, k); then x *= d11 */
+                    const T d11 = (T)1 / WL(k, k);
+                    #pragma omp parallel for schedule(static)
+                    for (int64_t j = k + 1; j < n; ++j) {
+                        const T temp = -d11 * WL(j, k);
+                        for (int64_t i = j; i < n; ++i) WL(i, j) = WL(i, j) + WL(i, k) * temp;
+                    }
+                    for (int64_t i = k + 1; i < n; ++i) WL(i, k) = d11 * WL(i, k);
+                }
+            } else if (k < n - 2) {
+                T d21 = WL(k + 1, k);
+                const T d11 = WL(k + 1, k + 1) / d21;
+                const T d22 = WL(k, k) / d21;
+                const T t = (T)1 / (d11 * d22 - (T)1);
+                d21 = t / d21;
+                for (int64_t j = k + 2; j < n; ++j) {
+                    const T wk = d21 * (d11 * WL(j, k) - WL(j, k + 1));
+                    const T wkp1 = d21 * (d22 * WL(j, k + 1) - WL(j, k));
+                    for (int64_t i = j; i < n; ++i) WL(i, j) = WL(i, j) - WL(i, k) * wk - WL(i, k + 1) * wkp1;
+                    WL(j, k) = wk;
+                    WL(j, k + 1) = wkp1;
+                }
+            }
+        }
+        if (kstep == 1) ipiv[k] = kp;
+        else { ipiv[k] = -(kp + 1); ipiv[k + 1] = -(kp + 1); }
+        k += kstep;
+    }
+    return info;
+#undef WL
+}
+
+/* xSYTRS (lower): b <- A^{-1} b from sytrf's factors (L D L^T with the interchanges). */
+static void FN(sytrs_vec)(const T* W, int64_t ld, int64_t n, const int64_t* ipiv, T* b)
+{
+#define WL(i, j) W[(i) + (j) * ld]
+    int64_t k = 0;
+    while (k < n) {                       /* solve L D y = P b */
+        if (ipiv[k] >= 0) {
+            const int64_t kp = ipiv[k];
+            if (kp != k) { T t = b[k]; b[k] = b[kp]; b[kp] = t; }
+            for (int64_t i = k + 1; i < n; ++i) b[i] = b[i] - WL(i, k) * b[k];
+            b[k] = b[k] / WL(k, k);
+            k += 1;
+        } else {
+            const int64_t kp = -ipiv[k] - 1;
+            if (kp != k + 1) { T t = b[k + 1]; b[k + 1] = b[kp]; b[kp] = t; }
+            for (int64_t i = k + 2; i < n; ++i) b[i] = b[i] - WL(i, k) * b[k] - WL(i, k + 1) * b[k + 1];
+            const T akm1k = WL(k + 1, k);
+            const T akm1 = WL(k, k) / akm1k;
+            const T ak = WL(k + 1, k + 1) / akm1k;
+            const T denom = akm1 * ak - (T)1;
+            const T bkm1 = b[k] / akm1k;
+            const T bk = b[k + 1] / akm1k;
+            b[k] = (ak * bkm1 - bk) / denom;
+            b[k + 1] = (akm1 * bk - bkm1) / denom;
+            k += 2;
+        }
+    }
+    k = n - 1;
+    while (k >= 0) {                      /* solve L^T P x = y */
+        if (ipiv[k] >= 0) {
+            T s = b[k];
+            for (int64_t i = k + 1; i < n; ++i) s = s - WL(i, k) * b[i];
+            b[k] = s;
+            const int64_t kp = ipiv[k];
+            if (kp != k) { T t = b[k]; b[k] = b[kp]; b[kp] = t; }
+            k -= 1;
+        } else {
+            T s = b[k], s1 = b[k - 1];
+            for (int64_t i = k + 1; i < n; ++i) { s = s - WL(i, k) * b[i]; s1 = s1 - WL(i, k - 1) * b[i]; }
+            b[k] = s;
+            b[k - 1] = s1;
+            const int64_t kp = -ipiv[k] - 1;
+            if (kp != k) { T t = b[k]; b[k] = b[kp]; b[kp] = t; }
+            k -= 2;
+        }
+    }
+#undef WL
+}
+
+/* ------------------------------------------------------------------ */
 /* Reciprocal condition estimate (the xxCON family P:350,     */
 /* P:386): 1-norm estimate of ||A^-1||_1 by the Hager-Higham */
 /* procedure in the form LAPACK's xLACN2 uses (Z13b), with M = A^-1 and    */
 /* M^T applied through the path's factors.                               */
 /* ------------------------------------------------------------------ */
 typedef struct {
-    int kind;               /* 0 LU, 1 band LU, 2 triangular, 3 Cholesky */
+    int kind;               /* 0 LU, 1 band LU, 2 triangular, 3 Cholesky, 4 LDL^T (ipiv = sytrf's) */
     const T* F; int64_t ldf; int64_t n;
     int64_t kl, ku; const int64_t* ipiv;
     int upper;
@@ -364,6 +513,9 @@ static void FN(applyM)(const FN(opM)* op, int trans, T* y)
     case 3:   /* xPOCON: inv(L^T) * inv(L), symmetric */
         FN(trsv)(op->F, op->ldf, n, 0, 0, 0, y);
         FN(trsv)(op->F, op->ldf, n, 0, 1, 0, y);
+        break;
+    case 4:   /* xSYCON: A^{-1} through xSYTRS, symmetric (both kases the same) */
+        FN(sytrs_vec)(op->F, op->ldf, n, op->ipiv, y);
         break;
     }
 }
@@ -603,6 +755,9 @@ int64_t FN(or_getrf)(T* W, int64_t ld, int64_t n, int64_t* ipiv) { return FN(get
 void FN(or_getrs)(const T* W, int64_t ld, int64_t n, const int64_t* ipiv, T* B, int64_t ldb, int64_t nrhs)
 { for (int64_t r = 0; r < nrhs; ++r) FN(getrs_vec)(W, ld, n, ipiv, B + r * ldb); }
 int64_t FN(or_potrf)(T* L, int64_t ld, int64_t n) { return FN(potrf)(L, ld, n); }
+int64_t FN(or_sytrf)(T* W, int64_t ld, int64_t n, int64_t* ipiv) { return FN(sytrf)(W, ld, n, ipiv); }
+void FN(or_sytrs)(const T* W, int64_t ld, int64_t n, const int64_t* ipiv, T* B, int64_t ldb, int64_t nrhs)
+{ for (int64_t r = 0; r < nrhs; ++r) FN(sytrs_vec)(W, ld, n, ipiv, B + r * ldb); }
 void FN(or_trsv)(const T* A, int64_t lda, int64_t n, int upper, int trans, int unit, T* b) { FN(trsv)(A, lda, n, upper, trans, unit, b); }
 double FN(or_band_pack)(const T* A, int64_t lda, int64_t n, int64_t kl, int64_t ku, T* ab, int64_t ldab)
 { return (double)FN(band_pack)(A, lda, n, kl, ku, ab, ldab); }
@@ -610,7 +765,8 @@ int64_t FN(or_gbtrf)(int64_t n, int64_t kl, int64_t ku, T* ab, int64_t ldab, int
 void FN(or_gbtrs)(int64_t n, int64_t kl, int64_t ku, const T* ab, int64_t ldab, const int64_t* ipiv, T* B, int64_t ldb, int64_t nrhs, int trans)
 { for (int64_t r = 0; r < nrhs; ++r) { if (trans) FN(gbtrs_vec_t)(n, kl, ku, ab, ldab, ipiv, B + r * ldb); else FN(gbtrs_vec)(n, kl, ku, ab, ldab, ipiv, B + r * ldb); } }
 double FN(or_norm1)(const T* A, int64_t lda, int64_t n) { return (double)FN(norm1_full)(A, lda, n); }
-/* rcond estimators from factors: kind 0 LU (F=W), 1 band (F=ab), 2 tri (F=A), 3 Cholesky (F=L). */
+/* rcond estimators from factors: kind 0 LU (F=W), 1 band (F=ab), 2 tri (F=A), 3 Cholesky (F=L),
+ * 4 LDL^T (F=W, ipiv = sytrf's). */
 double FN(or_rcond)(int kind, const T* F, int64_t ldf, int64_t n, int64_t kl, int64_t ku, const int64_t* ipiv, int upper, double anorm, int* nsolves)
 {
     FN(opM) op = { kind, F, ldf, n, kl, ku, ipiv, upper };
@@ -647,12 +803,18 @@ int FN(or_solve)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, in
     or_structure st;
     FN(or_detect)(A, lda, n, &st);
     uint32_t flags = st.flags;
+    /* Z30: with SYM_INDEF the exact symmetry is evaluated; a symmetric matrix that is not likely
+     * sympd (or whose Cholesky fails) takes LDL^T instead of the general LU */
+    const int symind = (o.flags & OR_OPT_SYM_INDEF) != 0;
+    const int sym = symind && FN(is_symmetric)(A, lda, n);
+    if (sym) flags |= OR_F_SYMMETRIC;
     int method;
     if (o.flags & OR_OPT_FORCE_METHOD) method = o.force_method;
     else if (st.flags & OR_BANDED) method = OR_M_BAND;
     else if (st.flags & OR_LOWER) method = OR_M_TRI_LOWER;
     else if (st.flags & OR_UPPER) method = OR_M_TRI_UPPER;
     else if (st.flags & OR_SPD) method = OR_M_CHOL;
+    else if (sym) method = OR_M_LDLT;
     else method = OR_M_LU;
     if (method == OR_M_BAND || (o.flags & OR_OPT_FULLSCAN)) { rep->kl = st.kl; rep->ku = st.ku; }
     /* Z28: with CHECK_FINITE a NaN/Inf anywhere in A or B is rejected before
@@ -700,11 +862,11 @@ int FN(or_solve)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, in
         for (int64_t j = 0; j < n; ++j) for (int64_t i = 0; i < n; ++i) W[i + j * n] = A[i + j * lda];
         if (method == OR_M_CHOL) {
             info = FN(potrf)(W, n, n);
-            if (info) {              /* not actually sympd -> generic solver */
+            if (info) {              /* not actually sympd -> generic solver (Z30: LDL^T if symmetric) */
                 flags |= OR_F_CHOL_FAILED;
                 rep->chol_fail_col = info - 1;
                 info = 0;
-                method = OR_M_LU;
+                method = sym ? OR_M_LDLT : OR_M_LU;
                 for (int64_t j = 0; j < n; ++j) for (int64_t i = 0; i < n; ++i) W[i + j * n] = A[i + j * lda];
             } else {
                 anorm = FN(norm1_full)(A, lda, n);
@@ -713,6 +875,19 @@ int FN(or_solve)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, in
                 factored = 1;
                 for (int64_t r = 0; r < nrhs; ++r) { FN(trsv)(W, n, n, 0, 0, 0, X + r * ldx); FN(trsv)(W, n, n, 0, 1, 0, X + r * ldx); }
             }
+        }
+        if (method == OR_M_LDLT) {   /* xSYTRF / xSYCON / xSYTRS, lower (Z30) */
+            int64_t* ipiv = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+            anorm = FN(norm1_full)(A, lda, n);
+            info = FN(sytrf)(W, n, n, ipiv);
+            if (info) singular = 1;
+            else {
+                FN(opM) op = { 4, W, n, n, 0, 0, ipiv, 0 };
+                rcond = FN(rcond_from)(anorm, FN(lacn2)(&op, NULL));
+                factored = 1;
+                for (int64_t r = 0; r < nrhs; ++r) FN(sytrs_vec)(W, n, n, ipiv, X + r * ldx);
+            }
+            free(ipiv);
         }
         if (method == OR_M_LU) {
             int64_t* ipiv = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);

@@ -443,3 +443,70 @@ def test_band_pack_anorm_is_the_1norm(seed):
     A[int(rng.integers(0, n)), :] *= 7.0    # a heavy row (stays inside the band) so no column sum is typical
     _, anorm = oracle.band_pack(A, kl, ku)
     assert anorm == pytest.approx(np.abs(A).sum(axis=0).max(), rel=4 * n * 2.2e-16)
+
+
+# ------------------------------------------------------------------ LDL^T, Bunch-Kaufman (Z30)
+def _sym_indef(n, seed):
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, n))
+    return np.asfortranarray((M + M.T) / 2)
+
+
+@pytest.mark.parametrize("n,seed", [(1, 0), (2, 1), (5, 2), (17, 3), (40, 4), (60, 5), (60, 6)])
+def test_sytrf_matches_lapack_dsytf2(n, seed):
+    """For n below LAPACK's block size dsytrf is the unblocked dsytf2: the oracle's pivots must be
+    LAPACK's exactly (1-based kp, negative for 2x2 blocks) and its factors equal up to rounding."""
+    A = _sym_indef(n, seed)
+    if n >= 5:
+        A[2, 2] = 0.0                       # forces interchanges / 2x2 blocks early
+    W, ipiv, info = oracle.sytrf(A)
+    lu, piv, linfo = lapack.dsytrf(A, lower=1)
+    assert info == linfo == 0
+    lp = np.where(ipiv >= 0, ipiv + 1, ipiv)
+    assert np.array_equal(lp, piv), (lp, piv)
+    L = np.tril(W)
+    assert np.allclose(L, np.tril(lu), rtol=1e-12, atol=1e-12 * np.abs(A).max())
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_sytrs_solves(seed):
+    """x = A^{-1} b through the LDL^T factors equals the exact rational solution (n <= 8)."""
+    rng = np.random.default_rng(40 + seed)
+    n = 3 + seed
+    A = rng.integers(-4, 5, (n, n)).astype(np.float64)
+    A = np.asfortranarray(A + A.T)
+    b = rng.integers(-5, 6, n).astype(np.float64)
+    if abs(np.linalg.det(A)) < 1e-6:
+        A[np.arange(n), np.arange(n)] += 7.0
+    W, ipiv, info = oracle.sytrf(A)
+    assert info == 0
+    x = oracle.sytrs(W, ipiv, b)[:, 0]
+    xe = np.array([float(v) for v in exact_solve(A, b)])
+    assert np.abs(x - xe).max() <= 1e-12 * max(1.0, np.abs(xe).max())
+
+
+def test_sym_indef_dispatch_and_rcond():
+    """SYM_INDEF: an exactly symmetric indefinite matrix takes LDL^T (method 7, SYMMETRIC bit), its
+    rcond equals LAPACK's dsycon on the same factors, the solution is the linear solve; without the
+    option the paper's flowchart is unchanged (general LU); a likely-sympd matrix whose Cholesky fails
+    takes LDL^T when exactly symmetric."""
+    A = _sym_indef(50, 9)
+    B = np.asfortranarray(np.random.default_rng(9).standard_normal((50, 2)))
+    r, X, rep, _ = oracle.solve(A, B, sym_indef=True)
+    assert r == 0 and rep["method"] == oracle.M_LDLT and rep["flags"] & oracle.F_SYMMETRIC
+    assert np.abs(X - np.linalg.solve(A, B)).max() <= 1e-10 * np.abs(X).max()
+    lu, piv, _ = lapack.dsytrf(A, lower=1)
+    anorm = np.abs(A).sum(axis=0).max()
+    rc, _ = lapack.dsycon(lu, piv, anorm, lower=1)
+    assert rep["rcond"] == pytest.approx(rc, rel=1e-12)
+    r2, _, rep2, _ = oracle.solve(A, B)
+    assert rep2["method"] == oracle.M_LU and not rep2["flags"] & oracle.F_SYMMETRIC
+    M = np.full((20, 20), -0.45)
+    np.fill_diagonal(M, 1.0)
+    r3, X3, rep3, _ = oracle.solve(np.asfortranarray(M), B[:20].copy(order="F"), sym_indef=True)
+    assert rep3["flags"] & oracle.F_CHOL_FAILED and rep3["method"] == oracle.M_LDLT
+    assert np.abs(M @ X3 - B[:20]).max() <= 1e-12 * np.abs(B).max() * 20
+    # asymmetric by one ulp: not exactly symmetric -> LU
+    A4 = A.copy(order="F")
+    A4[3, 7] = np.nextafter(A4[3, 7], 10.0)
+    assert oracle.solve(A4, B, sym_indef=True)[2]["method"] == oracle.M_LU
