@@ -69,6 +69,7 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
                                              (robustness to floating-point limits), Z28/Z29 */
 #define AS_FLAG_SVD_NOCONV    (1u << 14)  /* Jacobi hit max_sweeps */
 #define AS_FLAG_RANK_DEF      (1u << 15)  /* fallback effective rank < n */
+#define AS_FLAG_SYMMETRIC     (1u << 16)  /* A is exactly symmetric (evaluated only with AS_OPT_SYM_INDEF, n <= 128) */
 
 /* ---- methods ------------------------------------------------------------- */
 #define AS_METHOD_NONE      0
@@ -78,6 +79,8 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
 #define AS_METHOD_CHOL      4   /* POTRF/POCON/POTRS */
 #define AS_METHOD_LU        5   /* GETRF/GECON/GETRS */
 #define AS_METHOD_SVD       6   /* QR + one-sided Jacobi min-norm */
+#define AS_METHOD_LDLT      7   /* symmetric indefinite L D L^T, Bunch-Kaufman (xSYTRF/xSYCON/xSYTRS; the paper's
+                                   future work P:741-743; AS_OPT_SYM_INDEF, n <= 128) */
 
 /* ---- options ------------------------------------------------------------- */
 #define AS_OPT_NO_FALLBACK  0x1u   /* disable the SVD fallback */
@@ -86,6 +89,10 @@ typedef enum { AS_F64 = 0, AS_F32 = 1 } as_dtype;
                                       the detection pass then reads every element of A (no early exit) and B is
                                       scanned once; off by default (the paper is silent on non-finite input, Z28) */
 #define AS_OPT_FULLSCAN     0x8u   /* detection never exits early; kl/ku always exact */
+#define AS_OPT_SYM_INDEF    0x20u  /* the symmetric-indefinite specialisation (Z30): for
+                                      n <= 128 an exactly symmetric matrix that is not likely-sympd (or whose
+                                      Cholesky fails) is solved by Bunch-Kaufman L D L^T on the one-block
+                                      solver; larger systems ignore the option */
 #define AS_OPT_SKIP_DETECT  0x10u  /* with AS_OPT_FORCE_METHOD (LU, CHOL, TRI_*): no structure detection at all --
                                       the "standard solver" of the paper's comparison; report bits
                                       0..3 are 0.  Illegal (-9) without FORCE_METHOD or with AS_METHOD_BAND,

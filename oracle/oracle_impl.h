@@ -805,7 +805,7 @@ int FN(or_solve)(const T* A, int64_t lda, int64_t n, const T* B, int64_t ldb, in
     uint32_t flags = st.flags;
     /* Z30: with SYM_INDEF the exact symmetry is evaluated; a symmetric matrix that is not likely
      * sympd (or whose Cholesky fails) takes LDL^T instead of the general LU */
-    const int symind = (o.flags & OR_OPT_SYM_INDEF) != 0;
+    const int symind = (o.flags & OR_OPT_SYM_INDEF) != 0 && n <= 128;   /* Z30: larger systems ignore it */
     const int sym = symind && FN(is_symmetric)(A, lda, n);
     if (sym) flags |= OR_F_SYMMETRIC;
     int method;

@@ -39,7 +39,8 @@ FLAG_POORLY_COND, FLAG_SVD_NOCONV, FLAG_RANK_DEF = 1 << 12, 1 << 14, 1 << 15
 FLAG_NONFINITE = 1 << 13
 METHOD_BAND, METHOD_TRI_LOWER, METHOD_TRI_UPPER, METHOD_CHOL, METHOD_LU, METHOD_SVD = 1, 2, 3, 4, 5, 6
 OPT_NO_FALLBACK, OPT_FORCE_METHOD, OPT_FULLSCAN = 0x1, 0x2, 0x8
-OPT_SKIP_DETECT, OPT_CHECK_FINITE = 0x10, 0x4
+OPT_SKIP_DETECT, OPT_CHECK_FINITE, OPT_SYM_INDEF = 0x10, 0x4, 0x20
+METHOD_LDLT, FLAG_SYMMETRIC = 7, 1 << 16
 ERR_SINGULAR_NO_FALLBACK, ERR_SVD_NOT_CONVERGED, ERR_NONFINITE = 1, 2, 3
 
 EXPORTS = ("as_solve", "as_solve_f64", "as_solve_f32", "as_solve_ex", "as_solve_async", "as_solve_host",
@@ -149,11 +150,11 @@ def to_host(t) -> np.ndarray:
 
 
 def make_options(no_fallback=False, force_method=None, fullscan=False, rcond_threshold=-1.0, lsq_cutoff=-1.0,
-                 max_sweeps=30, skip_detect=False, check_finite=False) -> Options:
+                 max_sweeps=30, skip_detect=False, check_finite=False, sym_indef=False) -> Options:
     o = Options()
     o.flags = (OPT_NO_FALLBACK if no_fallback else 0) | (OPT_FORCE_METHOD if force_method else 0) | \
         (OPT_FULLSCAN if fullscan else 0) | (OPT_SKIP_DETECT if skip_detect else 0) | \
-        (OPT_CHECK_FINITE if check_finite else 0)
+        (OPT_CHECK_FINITE if check_finite else 0) | (OPT_SYM_INDEF if sym_indef else 0)
     o.force_method = int(force_method or 0)
     o.rcond_threshold = float(rcond_threshold)
     o.lsq_cutoff = float(lsq_cutoff)

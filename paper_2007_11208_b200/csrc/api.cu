@@ -563,6 +563,51 @@ static bool is_device_ptr(const void* p) {
 }
 
 static thread_local int64_t t_last_nodes = 0;
+
+// The symmetric-indefinite specialisation (Z30) lives in the one-block solver (small.cu): a single
+// system with AS_OPT_SYM_INDEF and n <= kSmallN runs there as a batch of one.
+struct SmallOut { as_report rep; int32_t ret; int32_t pad; };
+static std::mutex g_small_mu;
+static std::map<std::pair<int, uintptr_t>, std::pair<SmallOut*, SmallOut*>> g_small_out;   // (device, stream) -> (dev, pinned)
+
+static int solve_small_single(as_dtype dt, const void* A, int64_t lda, int64_t n, const void* B, int64_t ldb,
+                              int64_t nrhs, void* X, const PlanKey& key, as_report* rep_host, as_report* rep_dev,
+                              void* sigma, cudaStream_t stream, bool sync, int32_t* ret_dev) {
+    SmallOut *d = nullptr, *h = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_small_mu);
+        auto& slot = g_small_out[{key.dev, (uintptr_t)stream}];
+        if (!slot.first) {
+            if (cudaMalloc(&slot.first, sizeof(SmallOut)) != cudaSuccess ||
+                cudaMallocHost(&slot.second, sizeof(SmallOut)) != cudaSuccess) {
+                cudaGetLastError();
+                return AS_ERR_CUDA_BASE + (int)cudaErrorMemoryAllocation;
+            }
+        }
+        d = slot.first;
+        h = slot.second;
+    }
+    SmallArgs a{};
+    a.A = A; a.lda = lda; a.sA = lda * n;
+    a.B = B; a.ldb = ldb; a.sB = ldb * nrhs;
+    a.X = X; a.ldx = ldb; a.sX = ldb * nrhs;
+    a.n = (int)n; a.nrhs = (int)nrhs; a.batch = 1;
+    a.opts = key.opts; a.force = key.force;
+    a.thr = key.thr; a.cut = key.cut; a.max_sweeps = key.sweeps;
+    a.rep = rep_dev ? rep_dev : &d->rep;
+    a.ret = ret_dev ? ret_dev : &d->ret;
+    a.sigma = sigma; a.sS = n;
+    int err = launch_small_batched(dt, a, stream);
+    if (err || !sync) return err;
+    if (rep_dev) cudaMemcpyAsync(&d->rep, rep_dev, sizeof(as_report), cudaMemcpyDeviceToDevice, stream);
+    if (ret_dev) cudaMemcpyAsync(&d->ret, ret_dev, sizeof(int32_t), cudaMemcpyDeviceToDevice, stream);
+    cudaMemcpyAsync(h, d, sizeof(SmallOut), cudaMemcpyDeviceToHost, stream);
+    err = check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    if (err) return err;
+    if (rep_host) *rep_host = h->rep;
+    t_last_nodes = 1;
+    return h->ret;
+}
 static thread_local Plan* t_last_plan = nullptr;
 
 // kernel nodes of a graph; recursing into conditional bodies per `pick`
@@ -607,7 +652,8 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     key.opts = opt ? opt->flags : 0u;
     key.force = (opt && (opt->flags & AS_OPT_FORCE_METHOD)) ? opt->force_method : 0;
     if (key.opts & AS_OPT_FORCE_METHOD) {
-        if (key.force < AS_METHOD_BAND || key.force > AS_METHOD_LU) return -9;
+        if (key.force < AS_METHOD_BAND || (key.force > AS_METHOD_LU && key.force != AS_METHOD_LDLT)) return -9;
+        if (key.force == AS_METHOD_LDLT && !((key.opts & AS_OPT_SYM_INDEF) && n <= kSmallN && nrhs <= kSmallRhs)) return -9;
     }
     if ((key.opts & AS_OPT_SKIP_DETECT) && (!(key.opts & AS_OPT_FORCE_METHOD) || key.force == AS_METHOD_BAND)) return -9;
     // the finite check rides on the detection pass, which SKIP_DETECT removes
@@ -618,6 +664,8 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     key.sweeps = (opt && opt->max_sweeps > 0) ? opt->max_sweeps : 30;
     key.instrumented = g_instrument;
     key.eager = g_eager;
+    if ((key.opts & AS_OPT_SYM_INDEF) && n <= kSmallN && nrhs <= kSmallRhs && !(key.opts & AS_OPT_SKIP_DETECT))
+        return solve_small_single(dt, A, lda, n, B, ldb, nrhs, X, key, rep_host, rep_dev, sigma, stream, sync, ret_dev);
     Plan* P = nullptr;
     int err = get_plan(key, &P);
     if (err) return err;
@@ -758,7 +806,9 @@ int as_solve_batched(as_dtype dt, int64_t n, int64_t nrhs, int64_t batch, const 
     const double eps = dt == AS_F64 ? 2.220446049250313080847e-16 : 1.1920928955078125e-07;
     const uint32_t opts = opt ? opt->flags : 0u;
     const int force = (opts & AS_OPT_FORCE_METHOD) ? opt->force_method : 0;
-    if ((opts & AS_OPT_FORCE_METHOD) && (force < AS_METHOD_BAND || force > AS_METHOD_LU)) return -14;
+    if ((opts & AS_OPT_FORCE_METHOD) && (force < AS_METHOD_BAND || (force > AS_METHOD_LU && force != AS_METHOD_LDLT))) return -14;
+    if ((opts & AS_OPT_FORCE_METHOD) && force == AS_METHOD_LDLT && !((opts & AS_OPT_SYM_INDEF) && n <= kSmallN && nrhs <= kSmallRhs))
+        return -14;
     if (opts & AS_OPT_SKIP_DETECT) return -14;   // the one-block solver always detects (it reads A once anyway)
     cudaStream_t s = (cudaStream_t)stream;
     const size_t es = dt == AS_F64 ? 8 : 4;

@@ -522,12 +522,26 @@ template <typename T> struct LfLeaf;
 template <> struct LfLeaf<double> { static constexpr int v = 16; };
 template <> struct LfLeaf<float> { static constexpr int v = 32; };
 
-struct __align__(32) LfSlot {
-    double v;                  // |a| of the candidate (-1: none)
-    long long pos;             // its current position
-    long long row;             // its row in W (original order)
-    unsigned long long seq;    // sequence number (published last, with release)
-};
+// self-validating exchange words of the leaf panel: (seq32 << 32) | 32-bit payload
+constexpr int kLlSlot = 64;                       // words per slot
+constexpr int kLlWords = 4 + 32;                  // header + 32 payload words (16 doubles / 32 floats)
+template <typename T> struct LlPer;
+template <> struct LlPer<double> { static constexpr int v = 2; };
+template <> struct LlPer<float> { static constexpr int v = 1; };
+AS_DEV unsigned ll_half(double x, int h) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return h == 0 ? (unsigned)(b >> 32) : (unsigned)b;
+}
+AS_DEV unsigned ll_half(float x, int) { return __float_as_uint(x); }
+template <typename T> AS_DEV T ll_join(unsigned a, unsigned b);
+template <> AS_DEV double ll_join<double>(unsigned a, unsigned b) {
+    return __longlong_as_double((long long)(((unsigned long long)a << 32) | b));
+}
+template <> AS_DEV float ll_join<float>(unsigned a, unsigned) { return __uint_as_float(a); }
+AS_DEV void st_relaxed64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 
 template <typename T, int LW>
 struct LfSmem {
@@ -550,12 +564,14 @@ AS_DEV bool lf_better(T v2, int p2, T v, int p) { return v2 > v || (v2 == v && p
 
 template <typename T, int LW>
 __global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
-                                                             int64_t* ipiv, DevState* st, LfSlot* slots, T* xrow,
+                                                             int64_t* ipiv, DevState* st, unsigned long long* llx,
                                                              T* stage, int* stage_dst, T* ubufg, unsigned* ctr,
                                                              unsigned long long seq_base,
                                                              unsigned long long* tr_min, unsigned long long* tr_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LfSmem<T, LW>& sm = *(LfSmem<T, LW>*)smem_raw;
+    constexpr int kLlPer = LlPer<T>::v;
+    static_assert(LW * kLlPer == kLlWords - 4, "a leaf row is 32 exchange words");
     if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
     const int P = gridDim.x, cta = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -639,32 +655,60 @@ __global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, 
                     for (int r = 0; r < nr; ++r) if (sm.pos[r] == (int)g) { crow = r; break; }
                 }
                 if (P > 1) {
-                    if (crow >= 0 && lane < lw) xrow[((int64_t)par * kLfMaxP + cta) * LW + lane] = sm.S[crow + lane * kLfRows];
-                    __syncwarp();
-                    if (lane == 0) {
-                        LfSlot* sl = slots + par * kLfMaxP + cta;
-                        sl->v = sm.cv[0];
-                        sl->pos = sm.cpos[0];
-                        sl->row = crow >= 0 ? rbeg + crow : -1;
-                        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq),
-                                     "l"(seq_base + (unsigned long long)j + 1ull) : "memory");
+                    // self-validating exchange words (seq32 << 32 | payload32): no flag + data round
+                    // trips, no fences per column.  Slot = [|v| hi, |v| lo, pos, row, leaf row values]
+                    const unsigned sq = (unsigned)(seq_base + (unsigned long long)j + 1ull);
+                    unsigned long long* mine = llx + ((int64_t)par * kLfMaxP + cta) * kLlSlot;
+                    if (jj == 0) fence_acq_rel();     // my last trailing update before my first word of the leaf
+                    {
+                        const unsigned long long vb = (unsigned long long)__double_as_longlong(sm.cv[0]);
+                        const long long rowg = crow >= 0 ? rbeg + crow : -1;
+                        for (int w = lane; w < kLlWords; w += 32) {
+                            unsigned pl;
+                            if (w == 0) pl = (unsigned)(vb >> 32);
+                            else if (w == 1) pl = (unsigned)vb;
+                            else if (w == 2) pl = (unsigned)sm.cpos[0];
+                            else if (w == 3) pl = (unsigned)rowg;
+                            else {
+                                const int e = (w - 4) / kLlPer, h = (w - 4) % kLlPer;
+                                const T x = (crow >= 0 && e < lw) ? sm.S[crow + e * kLfRows] : T(0);
+                                pl = ll_half(x, h);
+                            }
+                            st_relaxed64(mine + w, ((unsigned long long)sq << 32) | pl);
+                        }
                     }
-                    const unsigned long long want = seq_base + (unsigned long long)j + 1ull;
-                    bool ready = lane >= P;
-                    bool ready2 = lane + 32 >= P;
+                    // phase 1: the 4 header words of every slot (lane l: word l & 3 of slots l/4 + 8k)
+                    unsigned long long hw[kLfMaxP / 8];
+                    bool ok[kLfMaxP / 8];
+#pragma unroll
+                    for (int k = 0; k < kLfMaxP / 8; ++k) ok[k] = (lane >> 2) + 8 * k >= P;
                     for (;;) {
-                        if (!ready) ready = ld_relaxed64(&slots[par * kLfMaxP + lane].seq) >= want;
-                        if (!ready2) ready2 = ld_relaxed64(&slots[par * kLfMaxP + lane + 32].seq) >= want;
-                        if (__all_sync(0xffffffffu, ready && ready2)) break;
+                        bool all = true;
+#pragma unroll
+                        for (int k = 0; k < kLfMaxP / 8; ++k)
+                            if (!ok[k]) {
+                                const int q = (lane >> 2) + 8 * k;
+                                hw[k] = ld_relaxed64(llx + ((int64_t)par * kLfMaxP + q) * kLlSlot + (lane & 3));
+                                ok[k] = (unsigned)(hw[k] >> 32) == sq;
+                                all = all && ok[k];
+                            }
+                        if (__all_sync(0xffffffffu, all)) break;
                     }
-                    fence_acq_rel();
                     double v = -1.0;
                     int pp = 0x7fffffff, ow = 0;
                     long long rw = -1;
-                    for (int q = lane; q < P; q += 32) {
-                        const double v2 = __ldcg(&slots[par * kLfMaxP + q].v);
-                        const int p2 = (int)__ldcg(&slots[par * kLfMaxP + q].pos);
-                        if (lf_better(v2, p2, v, pp)) { v = v2; pp = p2; ow = q; rw = __ldcg(&slots[par * kLfMaxP + q].row); }
+                    const int gb = lane & ~3;
+#pragma unroll
+                    for (int k = 0; k < kLfMaxP / 8; ++k) {
+                        const unsigned w0 = __shfl_sync(0xffffffffu, (unsigned)hw[k], gb + 0);
+                        const unsigned w1 = __shfl_sync(0xffffffffu, (unsigned)hw[k], gb + 1);
+                        const unsigned w2 = __shfl_sync(0xffffffffu, (unsigned)hw[k], gb + 2);
+                        const unsigned w3 = __shfl_sync(0xffffffffu, (unsigned)hw[k], gb + 3);
+                        const int q = (lane >> 2) + 8 * k;
+                        if (q >= P) continue;
+                        const double v2 = __longlong_as_double((long long)(((unsigned long long)w0 << 32) | w1));
+                        const int p2 = (int)w2;
+                        if (lf_better(v2, p2, v, pp)) { v = v2; pp = p2; ow = q; rw = (long long)(int)w3; }
                     }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
@@ -674,7 +718,18 @@ __global__ void __launch_bounds__(kPT, 2) lu_panel_lf_kernel(T* W, int64_t ldw, 
                         const long long r2 = __shfl_xor_sync(0xffffffffu, rw, o);
                         if (lf_better(v2, p2, v, pp)) { v = v2; pp = p2; ow = o2; rw = r2; }
                     }
-                    if (lane < lw) sm.ubuf[lane] = __ldcg(&xrow[((int64_t)par * kLfMaxP + ow) * LW + lane]);
+                    // phase 2: the winner's leaf row (one word per lane)
+                    {
+                        const unsigned long long* src = llx + ((int64_t)par * kLfMaxP + ow) * kLlSlot + 4;
+                        unsigned long long x = 0;
+                        if (lane < kLlWords - 4) {
+                            do { x = ld_relaxed64(src + lane); } while ((unsigned)(x >> 32) != sq);
+                        }
+                        const T val = ll_join<T>((unsigned)x, __shfl_down_sync(0xffffffffu, (unsigned)x, 1));
+                        const int e = lane / kLlPer;
+                        if (lane % kLlPer == 0 && e < lw) sm.ubuf[e] = val;
+                    }
+                    if (jj == lw - 1) fence_acq_rel();  // the leaf's pivot rows (A12) are read next
                     if (lane == 0) { sm.wpos = pp; sm.wrow = (int)rw; sm.wown = ow; }
                 } else {
                     if (lane < lw) sm.ubuf[lane] = sm.S[crow + lane * kLfRows];
@@ -1521,12 +1576,11 @@ static int g_panel_dbg = 0;   // diagnostics: phase counters of the cluster pane
 // staging for the final row moves
 struct LfBufs {
     unsigned* ctr;       // [2 * nblk]: grid barrier, staging count (zeroed per factorization)
-    LfSlot* slots;       // [2][kLfMaxP]
-    void* xrow;          // [2][kLfMaxP][LW]
+    unsigned long long* llx;   // [2][kLfMaxP][kLlSlot] self-validating exchange words
     int* stage_dst;      // [2 * kPW]
     void* stage;         // [2 * kPW][kPW]
     void* ubuf;          // [kPW][kPW] U rows of the panel by position (beyond each pivot row's leaf)
-    size_t zero_bytes;   // ctr + slots
+    size_t zero_bytes;   // ctr + llx (zeroed per factorization: stale words of an earlier call never match)
 };
 static LfBufs lf_layout(void* base, int64_t n, size_t es) {
     LfBufs b{};
@@ -1534,9 +1588,8 @@ static LfBufs lf_layout(void* base, int64_t n, size_t es) {
     char* p = (char*)base;
     auto take = [&](size_t bytes) { char* q = p; p += (bytes + 255) & ~(size_t)255; return q; };
     b.ctr = (unsigned*)take(sizeof(unsigned) * 2 * (size_t)nblk);
-    b.slots = (LfSlot*)take(sizeof(LfSlot) * 2 * kLfMaxP);
+    b.llx = (unsigned long long*)take(sizeof(unsigned long long) * 2 * kLfMaxP * kLlSlot);
     b.zero_bytes = (size_t)(p - (char*)base);
-    b.xrow = take(es * 2 * kLfMaxP * 32);
     b.stage_dst = (int*)take(sizeof(int) * 2 * kPW);
     b.stage = take(es * 2 * kPW * kPW);
     b.ubuf = take(es * kPW * kPW);
@@ -1569,7 +1622,7 @@ static bool lf_panel_launch(const Work& w, int64_t k0, int nbp, unsigned long lo
     const int slot = (int)(k0 / kBW) * 4 + 1;
     unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
     unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, b.slots, (T*)b.xrow,
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, b.llx,
                                              (T*)b.stage, b.stage_dst, (T*)b.ubuf, b.ctr + 2 * (k0 / kBW), seq_base, tmn,
                                              tmx);
     if (e != cudaSuccess) { cudaGetLastError(); return false; }

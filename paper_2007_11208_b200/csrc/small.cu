@@ -34,6 +34,7 @@ template <typename T> AS_DEV T tabs(T x);
 template <> AS_DEV double tabs<double>(double x) { return fabs(x); }
 template <> AS_DEV float tabs<float>(float x) { return fabsf(x); }
 
+constexpr int KIND_LDLT = 4;      // one-block solver only: Bunch-Kaufman L D L^T (Z30)
 constexpr int kSmallT = 256;
 constexpr int kSmallWarps = kSmallT / 32;
 constexpr int kRows = kSmallN / 32;      // rows per lane in the warp substitutions
@@ -48,7 +49,7 @@ struct SmallSmem {
     int ipiv[kSmallN];
     int isgn[kSmallN];
     int ired[32];
-    int kl, ku, flags, nonfinite, spd_dead, rot;
+    int kl, ku, flags, nonfinite, spd_dead, rot, asym;
     T max_diag;
 };
 
@@ -118,6 +119,65 @@ AS_DEV void warp_trsv(const T* W, int ld, int n, bool upper, bool trans, bool un
     __syncwarp();
 }
 
+// xSYTRS (lower) on one warp: v <- A^{-1} v from the Bunch-Kaufman factors in W (the oracle's
+// sytrs_vec: L D forward with the interleaved interchanges, then L^T backward)
+template <typename T>
+AS_DEV void warp_sytrs(const T* W, int ld, int n, const int* ipiv, T* v) {
+    const int lane = threadIdx.x & 31;
+    int k = 0;
+    while (k < n) {
+        if (ipiv[k] >= 0) {
+            const int kp = ipiv[k];
+            if (lane == 0 && kp != k) { const T t = v[k]; v[k] = v[kp]; v[kp] = t; }
+            __syncwarp();
+            const T bk = v[k];
+            for (int i = k + 1 + lane; i < n; i += 32) v[i] = v[i] - W[i + k * ld] * bk;
+            __syncwarp();
+            if (lane == 0) v[k] = bk / W[k + k * ld];
+            __syncwarp();
+            k += 1;
+        } else {
+            const int kp = -ipiv[k] - 1;
+            if (lane == 0 && kp != k + 1) { const T t = v[k + 1]; v[k + 1] = v[kp]; v[kp] = t; }
+            __syncwarp();
+            const T b0 = v[k], b1 = v[k + 1];
+            for (int i = k + 2 + lane; i < n; i += 32) v[i] = v[i] - W[i + k * ld] * b0 - W[i + (k + 1) * ld] * b1;
+            __syncwarp();
+            if (lane == 0) {
+                const T akm1k = W[(k + 1) + k * ld];
+                const T akm1 = W[k + k * ld] / akm1k;
+                const T ak = W[(k + 1) + (k + 1) * ld] / akm1k;
+                const T denom = akm1 * ak - T(1);
+                const T bkm1 = b0 / akm1k;
+                const T bk = b1 / akm1k;
+                v[k] = (ak * bkm1 - bk) / denom;
+                v[k + 1] = (akm1 * bk - bkm1) / denom;
+            }
+            __syncwarp();
+            k += 2;
+        }
+    }
+    k = n - 1;
+    while (k >= 0) {
+        const bool one = ipiv[k] >= 0;
+        T s = T(0), s1 = T(0);
+        for (int i = k + 1 + lane; i < n; i += 32) {
+            s += W[i + k * ld] * v[i];
+            if (!one) s1 += W[i + (k - 1) * ld] * v[i];
+        }
+        s = warp_sum(s);
+        s1 = warp_sum(s1);
+        if (lane == 0) {
+            v[k] = v[k] - s;
+            if (!one) v[k - 1] = v[k - 1] - s1;
+            const int kp = one ? ipiv[k] : -ipiv[k] - 1;
+            if (kp != k) { const T t = v[k]; v[k] = v[kp]; v[kp] = t; }
+        }
+        __syncwarp();
+        k -= one ? 1 : 2;
+    }
+}
+
 // y <- M y or M^T y, M = A^{-1} through the path's factors (the oracle's applyM); warp 0 only.
 template <typename T>
 AS_DEV void small_apply(SmallSmem<T>& sm, int n, int kind, bool upper, bool trans, T* v) {
@@ -144,6 +204,9 @@ AS_DEV void small_apply(SmallSmem<T>& sm, int n, int kind, bool upper, bool tran
         break;
     case KIND_TRI:
         warp_trsv(sm.W, ld, n, upper, trans, false, v);
+        break;
+    case KIND_LDLT:                         // xSYCON: symmetric, both kases through xSYTRS
+        warp_sytrs(sm.W, ld, n, sm.ipiv, v);
         break;
     default:                                // KIND_CHOL: inv(L^T) inv(L)
         warp_trsv(sm.W, ld, n, false, false, false, v);
@@ -262,6 +325,107 @@ AS_DEV int small_getrf(SmallSmem<T>& sm, int n) {
     return info;
 }
 
+// Bunch-Kaufman xSYTF2 (lower) on W, the oracle's sytrf step by step; returns info (1 + first zero
+// pivot column); ipiv as the oracle (1x1: kp; 2x2 at k, k+1: -(kp + 1) twice)
+template <typename T>
+AS_DEV int small_sytrf(SmallSmem<T>& sm, int n) {
+    const int ld = n + 1;
+    const T alpha = (T(1) + sqrt(T(17))) / T(8);
+    int info = 0, k = 0;
+    while (k < n) {
+        int kstep = 1, kp = k;
+        const T absakk = tabs(sm.W[k + k * ld]);
+        T colmax = T(0);
+        int imax = k;
+        if (k < n - 1) {
+            T key = T(-1);
+            int idx = 0x7fffffff;
+            for (int i = k + 1 + threadIdx.x; i < n; i += kSmallT) {
+                const T v = tabs(sm.W[i + k * ld]);
+                if (v == v && v > key) { key = v; idx = i; }
+            }
+            imax = block_argmax(key, idx, sm.red, sm.ired);
+            if (imax == 0x7fffffff) imax = k + 1;
+            colmax = tabs(sm.W[imax + k * ld]);
+        }
+        if ((absakk > colmax ? absakk : colmax) == T(0) || absakk != absakk) {
+            if (info == 0) info = k + 1;
+            kp = k;
+        } else {
+            if (absakk >= alpha * colmax) {
+                kp = k;
+            } else {
+                T rm = T(0);
+                for (int j = k + threadIdx.x; j < imax; j += kSmallT) rm = fmax(rm, tabs(sm.W[imax + j * ld]));
+                for (int i = imax + 1 + threadIdx.x; i < n; i += kSmallT) rm = fmax(rm, tabs(sm.W[i + imax * ld]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+                __syncthreads();
+                if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = rm;
+                __syncthreads();
+                T rowmax = T(0);
+                for (int w = 0; w < kSmallWarps; ++w) rowmax = fmax(rowmax, sm.red[w]);
+                if (absakk >= alpha * colmax * (colmax / rowmax)) kp = k;
+                else if (tabs(sm.W[imax + imax * ld]) >= alpha * rowmax) kp = imax;
+                else { kp = imax; kstep = 2; }
+            }
+            const int kk = k + kstep - 1;
+            __syncthreads();
+            if (kp != kk) {                 // interchange rows and columns kk and kp of A(k:n, k:n)
+                for (int i = kp + 1 + threadIdx.x; i < n; i += kSmallT) {
+                    const T t = sm.W[i + kk * ld]; sm.W[i + kk * ld] = sm.W[i + kp * ld]; sm.W[i + kp * ld] = t;
+                }
+                for (int j = kk + 1 + threadIdx.x; j < kp; j += kSmallT) {
+                    const T t = sm.W[j + kk * ld]; sm.W[j + kk * ld] = sm.W[kp + j * ld]; sm.W[kp + j * ld] = t;
+                }
+                if (threadIdx.x == 0) {
+                    T t = sm.W[kk + kk * ld]; sm.W[kk + kk * ld] = sm.W[kp + kp * ld]; sm.W[kp + kp * ld] = t;
+                    if (kstep == 2) { t = sm.W[(k + 1) + k * ld]; sm.W[(k + 1) + k * ld] = sm.W[kp + k * ld]; sm.W[kp + k * ld] = t; }
+                }
+            }
+            __syncthreads();
+            if (kstep == 1) {
+                if (k < n - 1) {            // A := A - d11 x x^T (lower), x *= d11
+                    const T d11 = T(1) / sm.W[k + k * ld];
+                    const int m = n - k - 1;
+                    for (int e = threadIdx.x; e < m * m; e += kSmallT) {
+                        const int i = k + 1 + e % m, j = k + 1 + e / m;
+                        if (i >= j) sm.W[i + j * ld] = sm.W[i + j * ld] + sm.W[i + k * ld] * (-d11 * sm.W[j + k * ld]);
+                    }
+                    __syncthreads();
+                    for (int i = k + 1 + threadIdx.x; i < n; i += kSmallT) sm.W[i + k * ld] = d11 * sm.W[i + k * ld];
+                }
+            } else if (k < n - 2) {
+                T d21 = sm.W[(k + 1) + k * ld];
+                const T d11 = sm.W[(k + 1) + (k + 1) * ld] / d21;
+                const T d22 = sm.W[k + k * ld] / d21;
+                const T t = T(1) / (d11 * d22 - T(1));
+                d21 = t / d21;
+                for (int j = k + 2 + threadIdx.x; j < n; j += kSmallT) {
+                    sm.x[j] = d21 * (d11 * sm.W[j + k * ld] - sm.W[j + (k + 1) * ld]);
+                    sm.y[j] = d21 * (d22 * sm.W[j + (k + 1) * ld] - sm.W[j + k * ld]);
+                }
+                __syncthreads();
+                const int m = n - k - 2;
+                for (int e = threadIdx.x; e < m * m; e += kSmallT) {
+                    const int i = k + 2 + e % m, j = k + 2 + e / m;
+                    if (i >= j) sm.W[i + j * ld] = sm.W[i + j * ld] - sm.W[i + k * ld] * sm.x[j] - sm.W[i + (k + 1) * ld] * sm.y[j];
+                }
+                __syncthreads();
+                for (int j = k + 2 + threadIdx.x; j < n; j += kSmallT) { sm.W[j + k * ld] = sm.x[j]; sm.W[j + (k + 1) * ld] = sm.y[j]; }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (kstep == 1) sm.ipiv[k] = kp;
+            else { sm.ipiv[k] = -(kp + 1); sm.ipiv[k + 1] = -(kp + 1); }
+        }
+        __syncthreads();
+        k += kstep;
+    }
+    return info;
+}
+
 // xPOTF2 (lower, right-looking) on W; returns 1 + failing column, 0 on success
 template <typename T>
 AS_DEV int small_potrf(SmallSmem<T>& sm, int n) {
@@ -298,7 +462,7 @@ __global__ void __launch_bounds__(kSmallT, 1) small_solve_kernel(SmallArgs a) {
     const T eps = Eps<T>::v;
 
     // ---- detection: every element is read here anyway -> exact kl / ku
-    if (tid == 0) { sm.kl = 0; sm.ku = 0; sm.flags = 0; sm.nonfinite = 0; sm.spd_dead = 0; sm.rot = 0; }
+    if (tid == 0) { sm.kl = 0; sm.ku = 0; sm.flags = 0; sm.nonfinite = 0; sm.spd_dead = 0; sm.rot = 0; sm.asym = 0; }
     __syncthreads();
     {
         int kl = 0, ku = 0, f = 0;
@@ -361,9 +525,19 @@ __global__ void __launch_bounds__(kSmallT, 1) small_solve_kernel(SmallArgs a) {
             }
         dead = __any_sync(0xffffffffu, dead);
         if (lane == 0 && dead) sm.spd_dead = 1;
+        if (a.opts & AS_OPT_SYM_INDEF) {                                  // exact symmetry (Z30)
+            bool asym = false;
+            for (int e = tid; e < n * n; e += kSmallT) {
+                const int i = e % n, j = e / n;
+                if (i > j && !(sm.W[i + j * ld] == sm.W[j + i * ld])) asym = true;
+            }
+            asym = __any_sync(0xffffffffu, asym);
+            if (lane == 0 && asym) sm.asym = 1;
+        }
     }
     __syncthreads();
     const int kl = sm.kl, ku = sm.ku;
+    const bool sym = (a.opts & AS_OPT_SYM_INDEF) && !sm.asym;
     unsigned det = 0;
     if (band_density_ok(n, kl, ku)) det |= AS_FLAG_BANDED;                // P:339, Z2/Z3
     if (!(sm.flags & 2)) det |= AS_FLAG_LOWER;
@@ -375,10 +549,11 @@ __global__ void __launch_bounds__(kSmallT, 1) small_solve_kernel(SmallArgs a) {
     else if (det & AS_FLAG_LOWER) method = AS_METHOD_TRI_LOWER;
     else if (det & AS_FLAG_UPPER) method = AS_METHOD_TRI_UPPER;
     else if (det & AS_FLAG_SPD_CANDIDATE) method = AS_METHOD_CHOL;
+    else if (sym) method = AS_METHOD_LDLT;
     else method = AS_METHOD_LU;
     const bool fullscan = (a.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0;
 
-    uint32_t flags = det;
+    uint32_t flags = det | (sym ? AS_FLAG_SYMMETRIC : 0u);
     int32_t ret = AS_OK;
     int primary = method;
     double rcond = 0.0, anorm_out = 0.0;
@@ -419,14 +594,19 @@ __global__ void __launch_bounds__(kSmallT, 1) small_solve_kernel(SmallArgs a) {
         } else if (method == AS_METHOD_CHOL) {
             const int f = small_potrf(sm, n);
             if (f) {                                                      // general LU
-                flags |= AS_FLAG_CHOL_FAILED;
+                flags |= AS_FLAG_CHOL_FAILED;                             // (Z30: LDL^T if exactly symmetric)
                 chol_col = f - 1;
-                method = primary = AS_METHOD_LU;
+                method = primary = sym ? AS_METHOD_LDLT : AS_METHOD_LU;
                 __syncthreads();
                 load_w(sm, A, a.lda, n);
             } else {
                 kind = KIND_CHOL;
             }
+        }
+        if (method == AS_METHOD_LDLT) {
+            kind = KIND_LDLT;
+            info = small_sytrf(sm, n);
+            singular = info != 0;
         }
         if (method == AS_METHOD_LU || method == AS_METHOD_BAND) {
             kind = method == AS_METHOD_BAND ? KIND_BAND : KIND_LU;

@@ -169,3 +169,75 @@ def test_batched_illegal_arguments():
     assert lib.as_solve_batched(0, 4, 1, 2, e.data_ptr(), 4, 8, e.data_ptr(), 4, 16, e.data_ptr(), 4, 16,
                                 None, None, None, None, None) == -7
     assert lib.as_solve_batched(0, 0, 1, 2, None, 1, 0, None, 1, 1, None, 1, 1, None, None, None, None, None) == 0
+
+
+# ------------------------------------------------------------------ symmetric indefinite: L D L^T (Z30)
+def sym_systems(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    M = rng.standard_normal((n, n))
+    out.append(("sym_indef", (M + M.T) / 2))
+    S = (M + M.T) / 2
+    if n >= 3:
+        np.fill_diagonal(S, 0.0)           # zero diagonal: 2x2 pivots from the first column
+    out.append(("sym_zero_diag", S))
+    C = np.full((n, n), -0.45)
+    np.fill_diagonal(C, 1.0)
+    out.append(("sym_chol_fail", C))       # likely-sympd by Fig. 4, indefinite for n >= 4
+    K = np.zeros((n, n))
+    if n >= 2:
+        K[0, 1] = K[1, 0] = 1.0
+        K[np.arange(2, n), np.arange(2, n)] = 1.0 + rng.random(n - 2)
+    out.append(("sym_2x2_block", K))
+    out.append(("spd", W.random_spd_fig3(n, seed=seed)))
+    out.append(("asym", W.random_dense(n, seed=seed)))
+    return [(a, np.asfortranarray(b)) for a, b in out]
+
+
+@pytest.mark.parametrize("n", [2, 3, 17, 64, 100, 128])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_batched_ldlt(n, fp32):
+    systems = sym_systems(n, seed=100 + n)
+    names = [s[0] for s in systems]
+    A = np.stack([s[1] for s in systems])
+    B = np.random.default_rng(n).standard_normal((len(names), n, 2))
+    A, B, X, reps, rets, _ = run_batch(A, B, fp32=fp32, sym_indef=True)
+    for b, nm in enumerate(names):
+        Ab, Bb = np.asfortranarray(A[b]), np.asfortranarray(B[b])
+        oret, Xo, orep, _ = oracle.solve(Ab, Bb, sym_indef=True)
+        assert int(rets[b]) == oret, (nm, rets[b], oret)
+        m = MASK | oracle.F_SYMMETRIC
+        assert (reps[b]["flags"] & m) == (orep["flags"] & m), (nm, hex(reps[b]["flags"]), hex(orep["flags"]))
+        assert reps[b]["method"] == orep["method"], nm
+        if nm.startswith("sym") and n >= 4:
+            assert orep["method"] == oracle.M_LDLT or orep["flags"] & oracle.F_FALLBACK, (nm, orep)
+        if oret == 0 and not orep["flags"] & (oracle.F_FALLBACK | oracle.F_RCOND_LOW):
+            assert abs(np.log2(reps[b]["rcond"] / orep["rcond"])) <= 1.0, nm
+            if fp32:
+                _, Xr, rr, _ = oracle.solve(Ab.astype(np.float64), Bb.astype(np.float64), sym_indef=True, no_fallback=True)
+                assert backward_error(Ab.astype(np.float64), X[b], Bb.astype(np.float64)) <= 1e-5, nm
+                assert forward_diff(X[b], Xr) <= 1e-6 * rr["anorm"] / rr["rcond"], nm
+            else:
+                assert backward_error(Ab, X[b], Bb) <= 1e-13, nm
+                assert forward_diff(X[b], Xo) <= 1e-15 * orep["anorm"] / orep["rcond"], nm
+
+
+def test_single_system_ldlt_and_size_gate():
+    """as_solve_ex with SYM_INDEF: n <= 128 runs the one-block LDL^T; n > 128 ignores the option (the
+    paper's LU), exactly as the oracle's Z30 rule; FORCE_METHOD=LDLT outside the gate is illegal."""
+    for n in (90, 200):
+        M = np.random.default_rng(n).standard_normal((n, n))
+        A = np.asfortranarray((M + M.T) / 2)
+        B = np.asfortranarray(np.random.default_rng(1).standard_normal((n, 3)))
+        o = AS.make_options(sym_indef=True)
+        ret, Xd, rep = AS.as_solve_ex(AS.to_device(A), AS.to_device(B), options=o)
+        torch.cuda.synchronize()
+        oret, Xo, orep, _ = oracle.solve(A, B, sym_indef=True)
+        assert ret == oret == 0
+        assert rep["method"] == orep["method"] == (oracle.M_LDLT if n <= 128 else oracle.M_LU)
+        assert (rep["flags"] & (MASK | oracle.F_SYMMETRIC)) == (orep["flags"] & (MASK | oracle.F_SYMMETRIC))
+        X = AS.to_host(Xd)
+        assert forward_diff(X, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"]
+    o = AS.make_options(force_method=AS.METHOD_LDLT)
+    ret, _, _ = AS.as_solve_ex(AS.to_device(A), AS.to_device(B), options=o)
+    assert ret == -9
