@@ -199,142 +199,6 @@ __global__ void __launch_bounds__(256) l21_kernel(T* W, int64_t ldw, int64_t n, 
     }
 }
 
-// ------------------------------------------------------------------ Cholesky panel (one cluster)
-// The whole block column (rows k0 .. n, columns k0 .. k0+nbp) factored in one kernel: the m rows
-// are split over the P <= 16 CTAs of a cluster, one row per thread, the row's nbp <= 64 values in
-// registers.  Deferred scaling: step j subtracts a_ij a_kj / d_j (d_j = a_jj, all unscaled), so a
-// column step needs only the diagonal block's column j (pushed by its owners into every CTA's
-// shared memory) and ONE cluster barrier; at the end l_ij = a_ij / sqrt(d_j).  The first !(d_j > 0)
-// stops the factorization (Z23).  This is POTF2 + L21 = A21 L11^{-T} in one pass.
-constexpr int kChMaxP = 16;
-template <int B, int E, class F>
-AS_DEV void static_for(F&& f) {
-    if constexpr (B < E) {
-        f(std::integral_constant<int, B>{});
-        static_for<B + 1, E>(f);
-    }
-}
-template <typename T>
-__global__ void __launch_bounds__(256, 1) chol_panel_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp, DevState* st) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    if (ld_volatile_i32(&st->chol_failed)) return;
-    const int P = (int)cl.num_blocks(), cta = (int)cl.block_rank();
-    const int64_t m = n - k0;
-    const int64_t chunk = (m + P - 1) / P;          // >= nbp: the diagonal block is in CTA 0
-    const int64_t rbeg = k0 + (int64_t)cta * chunk;
-    const int64_t rend = min(n, rbeg + chunk);
-    const int tid = threadIdx.x;
-    const int64_t gr = rbeg + tid;
-    const bool live = gr < rend;
-    const int dr = (int)(gr - k0);                   // diagonal index of my row (< nbp: diagonal block)
-    __shared__ T colv[2][kNB];
-    __shared__ T dsave[kNB];
-    __shared__ int s_fail;
-    T a[kNB];
-    {
-        const T* src = W + (live ? gr : k0) + k0 * ldw;
-#pragma unroll
-        for (int c = 0; c < kNB; ++c) {
-            a[c] = (live && c < nbp && (dr >= nbp || c <= dr)) ? *src : T(0);
-            src += ldw;
-        }
-    }
-    if (tid == 0) s_fail = -1;
-    int fail = -1;
-    // Column loop NOT unrolled (64 unrolled steps are instruction-cache bound); the row is kept
-    // rotated in registers: at step j, a[k] holds column (j + k) mod 64, so the current column is
-    // a[0] and every register index is a compile-time constant.
-    for (int j = 0; j < nbp; ++j) {
-        const int par = j & 1;
-        // owners of the diagonal block's rows j .. nbp-1 push their column-j value
-        if (live && cta == 0 && dr >= j && dr < nbp) {
-            for (int q = 0; q < P; ++q) {
-                T* cv = cl.map_shared_rank(&colv[par][0], q);
-                cv[dr] = a[0];
-            }
-        }
-        if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        else __syncthreads();
-        const T d = colv[par][j];
-        if (!(d > T(0))) { fail = j; break; }             // uniform
-        if (tid == 0) dsave[j] = d;
-        const int nlive = nbp - j;                         // a[k], k < nlive: columns j .. nbp-1
-        if (live && dr > j) {
-            const T f = a[0] / d;
-            // chunks of 16 with a compiler barrier between them: bounds the loads in flight
-            // (register pressure: a[] already takes 128 registers)
-#pragma unroll
-            for (int kc = 0; kc < kNB; kc += 16) {
-                T cv[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) cv[k] = (kc + k >= 1 && kc + k < nlive) ? colv[par][j + kc + k] : T(0);
-#pragma unroll
-                for (int k = 0; k < 16; ++k) a[kc + k] -= f * cv[k];
-                asm volatile("" ::: "memory");
-            }
-        }
-        const T x0 = a[0];
-#pragma unroll
-        for (int k = 0; k < kNB - 1; ++k) a[k] = a[k + 1];
-        a[kNB - 1] = x0;
-    }
-    // finish the rotation (nbp < 64) so that a[c] is column c again
-    if (fail < 0)
-        for (int r = nbp; r < kNB; ++r) {
-            const T x0 = a[0];
-#pragma unroll
-            for (int k = 0; k < kNB - 1; ++k) a[k] = a[k + 1];
-            a[kNB - 1] = x0;
-        }
-    if (fail >= 0) {
-        if (cta == 0 && tid == 0) {
-            st->chol_failed = 1;
-            st->chol_fail_col = k0 + fail;
-        }
-        return;
-    }
-    __syncthreads();
-    if (live) {
-        T* dst = W + gr + k0 * ldw;
-#pragma unroll
-        for (int c = 0; c < kNB; ++c) {
-            if (c < nbp && (dr >= nbp || c <= dr)) {
-                const T sq = sqrt(dsave[c]);
-                *dst = (c == dr) ? sq : a[c] / sq;
-            }
-            dst += ldw;
-        }
-    }
-    // keep every CTA's shared memory alive until the last remote push has landed
-    if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-template <typename T>
-static bool chol_panel_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s, bool force = false) {
-    const int64_t m = w.n - k0;
-    // cluster panel: opt-in (AS_CHOL_PANEL=cluster) until it beats POTF2 + L21
-    if (!force && (!getenv("AS_CHOL_PANEL") || strcmp(getenv("AS_CHOL_PANEL"), "cluster") != 0)) return false;
-    int P = 1;
-    while (P < kChMaxP && (m + P - 1) / P > 256) P *= 2;
-    if ((m + P - 1) / P > 256) return false;                 // rows do not fit one per thread
-    while (P > 1 && (m + P - 1) / P < nbp) P /= 2;           // the diagonal block stays in CTA 0
-    auto kern = chol_panel_kernel<T>;
-    if (P > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P);
-    cfg.blockDim = dim3(256);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) != cudaSuccess || ncl <= 0) { cudaGetLastError(); return false; }
-    return cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, w.n, k0, nbp, w.st) == cudaSuccess;
-}
-
 // Right-looking with look-ahead: after block k's panel, the next block column is updated first
 // (M = rest, N = 64, K = 64) and the next panel (POTF2 + inverse, L21) starts on a
 // high-priority stream while the bulk SYRK of block k runs on the main stream.
@@ -363,10 +227,8 @@ static void chol_factor_t(const Work& w, cudaStream_t s) {
     const int sm2 = (int)(sizeof(T) * 2 * kNB * kL21LD);
     cudaFuncSetAttribute(potf2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
     cudaFuncSetAttribute(l21_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-    bool reg_panels = false;
     auto panel = [&](int64_t k0, cudaStream_t st) {
         const int nbp = (int)std::min<int64_t>(kNB, n - k0);
-        if (chol_panel_launch<T>(w, k0, nbp, st)) { reg_panels = true; return; }
         potf2_kernel<T><<<1, 256, sm1, st>>>(W, ldw, n, k0, nbp, w.st, Dinv);
         const int64_t rest = n - k0 - nbp;
         if (rest > 0) l21_kernel<T><<<(unsigned)((rest + kNB - 1) / kNB), 256, sm2, st>>>(W, ldw, n, k0, nbp, w.st, Dinv);
@@ -408,7 +270,6 @@ static void chol_factor_t(const Work& w, cudaStream_t s) {
         }
     }
     // the register panels do not form L11^{-1}: all diagonal-block inverses (POTRS / POCON) at once
-    if (reg_panels) launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv0, false, false, w.st, false, w.args, s);
 }
 
 // Diagnostics: average time (us) of one Cholesky panel of W (restored from Wsrc before each
@@ -433,7 +294,6 @@ double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t 
         cudaEventRecord(e0, 0);
         auto run = [&](auto tag) {
             using T = decltype(tag);
-            if (kind == 0 && chol_panel_launch<T>(w, k0, nbp, 0, true)) return;
             const int sm1 = (int)(sizeof(T) * (2 * kNB * kChLD + 3 * 256));
             const int sm2 = (int)(sizeof(T) * 2 * kNB * kL21LD);
             cudaFuncSetAttribute(potf2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);

@@ -89,89 +89,7 @@ AS_DEV void gemm_stage(T* As, T* Bs, const T* A, int64_t lda, const T* B, int64_
     }
 }
 
-template <bool TA>
-AS_DEV double lds_a(const double* As, int m, int k) { return TA ? As[m * LDKM + k] : As[k * LDMK + m]; }
-template <bool TB>
-AS_DEV double lds_b(const double* Bs, int k, int n) { return TB ? Bs[k * LDMK + n] : Bs[n * LDKM + k]; }
 
-constexpr int kStageElems = (GBK * LDMK > GBM * LDKM ? GBK * LDMK : GBM * LDKM);
-
-// ------------------------------------------------------------------ fp64 DMMA kernel
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(GTHREADS, 1) gemm_dmma_kernel(GemmArgs g) {
-    if (g.skip && *g.skip) return;
-    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
-    if (g.lower_only && n0 > m0 + GBM - 1) return;   // tile strictly above the diagonal (SYRK)
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* As = (double*)smem_raw;
-    double* Bs = As + GSTAGES * kStageElems;
-    const double* A = (const double*)g.A;
-    const double* B = (const double*)g.B;
-    double* C = (double*)g.C;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
-    const int gid = lane >> 2, tig = lane & 3;
-
-    double acc[8][4][2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const int nk = (int)((g.K + GBK - 1) / GBK);
-#pragma unroll
-    for (int s = 0; s < GSTAGES - 1; ++s) {
-        if (s < nk)
-            gemm_stage<double, TA, TB>(As + s * kStageElems, Bs + s * kStageElems, A, g.lda, B, g.ldb, g.M, g.N, g.K,
-                                       m0, n0, (int64_t)s * GBK);
-        cp_async_commit();
-    }
-    for (int kt = 0; kt < nk; ++kt) {
-        cp_async_wait<GSTAGES - 2>();
-        __syncthreads();
-        {
-            const int nxt = kt + GSTAGES - 1;
-            if (nxt < nk) {
-                const int s = nxt % GSTAGES;
-                gemm_stage<double, TA, TB>(As + s * kStageElems, Bs + s * kStageElems, A, g.lda, B, g.ldb, g.M, g.N,
-                                           g.K, m0, n0, (int64_t)nxt * GBK);
-            }
-            cp_async_commit();
-        }
-        const double* as = As + (kt % GSTAGES) * kStageElems;
-        const double* bs = Bs + (kt % GSTAGES) * kStageElems;
-#pragma unroll
-        for (int ks = 0; ks < GBK / 4; ++ks) {
-            double af[8], bf[4];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = lds_a<TA>(as, wm + 8 * i + gid, ks * 4 + tig);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = lds_b<TB>(bs, ks * 4 + tig, wn + 8 * j + gid);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        }
-    }
-    cp_async_wait<0>();
-    // epilogue: C -= acc
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t r = m0 + wm + 8 * i + gid;
-        if (r >= g.M) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
-                if (c < g.N) {
-                    double* p = C + r + c * g.ldc;
-                    *p = *p - acc[i][j][h];
-                }
-            }
-        }
-    }
-}
 
 // ------------------------------------------------------------------ fp32 SIMT kernel
 // Thread (ty, tx) of a 16x16 grid owns rows {ty*4..+3, 64+ty*4..+3} and
