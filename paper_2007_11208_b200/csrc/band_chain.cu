@@ -23,205 +23,271 @@ namespace {
 template <typename T>
 AS_DEV T cabs(T x) { return x < T(0) ? -x : x; }
 
-// ------------------------------------------------------------------ xGBTRF, lane 0
+// Every chain reads its operands from shared memory: the warp stages the NEXT chunk of kCH steps
+// (factor columns, pivots, entering right-hand-side values) into registers before lane 0 (or every
+// lane, one vector each) runs the current chunk, and stores them after it -- the global-memory
+// latency of the next chunk hides behind the ~kCH dependent steps of the current one.
+constexpr int kCH = 64;
+constexpr int kMaxKV = 6, kMaxLdab = 10;   // kl, ku <= 3
+
+template <typename T>
+struct ChainSm {
+    T ab[kCH * kMaxLdab];          // factor columns of the chunk (or A's entering rows for xGBTRF)
+    long long ip[kCH];
+    T b[32 * (kCH + 1)];           // entering right-hand-side values, one row of kCH + 1 per lane
+};
+
+// asynchronous element copy global -> shared (zero-filled when !ok)
+template <typename U>
+AS_DEV void cpa(U* dst, const U* src, bool ok) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const void* g = ok ? (const void*)src : (const void*)dst;
+    if (sizeof(U) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(g), "r"(ok ? 8 : 0) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(g), "r"(ok ? 4 : 0) : "memory");
+}
+AS_DEV void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+AS_DEV void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// ------------------------------------------------------------------ xGBTRF (chain on lane 0)
 template <typename T, int KL, int KU>
-AS_DEV int64_t chain_gbtrf(const T* __restrict__ A, int64_t lda, int64_t n, T* ab, int64_t* ipiv) {
+AS_DEV int64_t chain_gbtrf(ChainSm<T> (&sm)[2], const T* __restrict__ A, int64_t lda, int64_t n, T* ab,
+                           int64_t* ipiv) {
     constexpr int KV = KL + KU;
     constexpr int LDAB = 2 * KL + KU + 1;
-    constexpr int kPF = KV >= 4 ? 4 : 8;   // prefetch depth (rows); shallower for wide windows (registers)
-    T w[KL + 1][KV + 1];
-    // window at j = 0: rows 0..KL, columns 0..KV (in-band entries of A)
-#pragma unroll
-    for (int r = 0; r <= KL; ++r)
-#pragma unroll
-        for (int c = 0; c <= KV; ++c) {
-            const bool inb = (r - c <= KL) && (c - r <= KU) && r < n && c < n;
-            w[r][c] = inb ? A[r + (int64_t)c * lda] : T(0);
+    constexpr int NE = kCH * (KV + 1);
+    const int lane = threadIdx.x;
+    // entering row of step j: A(j + KL + 1, j + 1 + c), c = 0..KV (all in the band)
+    auto issue = [&](int64_t c0, int buf) {
+        for (int e = lane; e < NE; e += 32) {
+            const int d = e / (KV + 1), c = e - d * (KV + 1);
+            const int64_t i = c0 + d + KL + 1, k = c0 + d + 1 + c;
+            const bool ok = i < n && k < n;
+            cpa(&sm[buf].ab[e], ok ? &A[i + k * lda] : (const T*)nullptr, ok);
         }
-    // prefetch queue: row j + KL + 1 (entering at the end of step j), columns j + 1 .. j + 1 + KV
-    T q[kPF][KV + 1];
-    auto load_row = [&](int64_t j, T (&dst)[KV + 1]) {
-        const int64_t i = j + KL + 1;
-#pragma unroll
-        for (int c = 0; c <= KV; ++c) {
-            const int64_t k = j + 1 + c;
-            dst[c] = (i < n && k < n) ? __ldg(&A[i + k * lda]) : T(0);
-        }
+        cpa_commit();
     };
-#pragma unroll
-    for (int d = 0; d < kPF; ++d) load_row(d, q[d]);
+    issue(0, 0);
+    cpa_wait_all();
+    __syncwarp();
+    T w[KL + 1][KV + 1];
     int64_t info = 0;
-    for (int64_t j0 = 0; j0 < n; j0 += kPF) {
-        T nq[kPF][KV + 1];
+    if (lane == 0) {
 #pragma unroll
-        for (int d = 0; d < kPF; ++d) load_row(j0 + kPF + d, nq[d]);
+        for (int r = 0; r <= KL; ++r)
 #pragma unroll
-        for (int d = 0; d < kPF; ++d) {
-            const int64_t j = j0 + d;
-            if (j >= n) break;
-            const int km = (int)min<int64_t>(KL, n - 1 - j);
-            // first max |w[r][0]|, r = 0..km (Z15: strict >, NaN never wins)
-            int p = 0;
-            T best = cabs(w[0][0]);
-#pragma unroll
-            for (int r = 1; r <= KL; ++r)
-                if (r <= km && cabs(w[r][0]) > best) { best = cabs(w[r][0]); p = r; }
-            ipiv[j] = j + p;
-            T pv = w[0][0];
-#pragma unroll
-            for (int r = 1; r <= KL; ++r) if (r == p) pv = w[r][0];
-            T l[KL + 1];
-#pragma unroll
-            for (int r = 0; r <= KL; ++r) l[r] = T(0);
-            if (pv != T(0)) {
-                // interchange rows 0 and p of the window
-#pragma unroll
-                for (int r = 1; r <= KL; ++r)
-                    if (r == p)
-#pragma unroll
-                        for (int c = 0; c <= KV; ++c) { const T t = w[0][c]; w[0][c] = w[r][c]; w[r][c] = t; }
-#pragma unroll
-                for (int r = 1; r <= KL; ++r)
-                    if (r <= km) l[r] = w[r][0] / w[0][0];       // multipliers by division (Z15)
-#pragma unroll
-                for (int r = 1; r <= KL; ++r)
-#pragma unroll
-                    for (int c = 1; c <= KV; ++c) w[r][c] = w[r][c] - l[r] * w[0][c];
-            } else if (info == 0) {
-                info = j + 1;
+            for (int c = 0; c <= KV; ++c) {
+                const bool inb = (r - c <= KL) && (c - r <= KU) && r < n && c < n;
+                w[r][c] = inb ? A[r + (int64_t)c * lda] : T(0);
             }
-            // factor column j: U(j, j + c) at AB(KV - c, j + c), L(j + r, j) at AB(KV + r, j)
+    }
+    for (int64_t c0 = 0, q = 0; c0 < n; c0 += kCH, ++q) {
+        const int cur = (int)(q & 1);
+        if (c0 + kCH < n) issue(c0 + kCH, cur ^ 1);                  // next chunk in flight
+        if (lane == 0) {
+            const int cnt = (int)min<int64_t>(kCH, n - c0);
+            for (int d = 0; d < cnt; ++d) {
+                const int64_t j = c0 + d;
+                const int km = (int)min<int64_t>(KL, n - 1 - j);
+                int p = 0;
+                T best = cabs(w[0][0]);                              // first max (Z15)
 #pragma unroll
-            for (int c = 0; c <= KV; ++c)
-                if (j + c < n) ab[(KV - c) + (j + c) * (int64_t)LDAB] = w[0][c];
+                for (int r = 1; r <= KL; ++r)
+                    if (r <= km && cabs(w[r][0]) > best) { best = cabs(w[r][0]); p = r; }
+                ipiv[j] = j + p;
+                T pv = w[0][0];
 #pragma unroll
-            for (int r = 1; r <= KL; ++r) ab[(KV + r) + j * (int64_t)LDAB] = l[r];
-            // shift the window: rows j+1.., columns j+1..; the new last row from the queue
+                for (int r = 1; r <= KL; ++r) if (r == p) pv = w[r][0];
+                T l[KL + 1];
 #pragma unroll
-            for (int r = 0; r < KL; ++r)
+                for (int r = 0; r <= KL; ++r) l[r] = T(0);
+                if (pv != T(0)) {
 #pragma unroll
-                for (int c = 0; c < KV; ++c) w[r][c] = w[r + 1][c + 1];
+                    for (int r = 1; r <= KL; ++r)
+                        if (r == p)
 #pragma unroll
-            for (int r = 0; r < KL; ++r) w[r][KV] = T(0);
-            if (KL > 0) {
+                            for (int c = 0; c <= KV; ++c) { const T t = w[0][c]; w[0][c] = w[r][c]; w[r][c] = t; }
 #pragma unroll
-                for (int c = 0; c <= KV; ++c) w[KL][c] = q[d][c];
-            } else {
-                // KL = 0: the window is row j+1 only, columns j+1 .. j+1+KU
+                    for (int r = 1; r <= KL; ++r)
+                        if (r <= km) l[r] = w[r][0] / w[0][0];       // multipliers by division (Z15)
 #pragma unroll
-                for (int c = 0; c <= KV; ++c) w[0][c] = q[d][c];
+                    for (int r = 1; r <= KL; ++r)
+#pragma unroll
+                        for (int c = 1; c <= KV; ++c) w[r][c] = w[r][c] - l[r] * w[0][c];
+                } else if (info == 0) {
+                    info = j + 1;
+                }
+                // factor column j: U(j, j + c) at AB(KV - c, j + c), L(j + r, j) at AB(KV + r, j)
+#pragma unroll
+                for (int c = 0; c <= KV; ++c)
+                    if (j + c < n) ab[(KV - c) + (j + c) * (int64_t)LDAB] = w[0][c];
+#pragma unroll
+                for (int r = 1; r <= KL; ++r) ab[(KV + r) + j * (int64_t)LDAB] = l[r];
+#pragma unroll
+                for (int r = 0; r < KL; ++r)
+#pragma unroll
+                    for (int c = 0; c < KV; ++c) w[r][c] = w[r + 1][c + 1];
+#pragma unroll
+                for (int r = 0; r < KL; ++r) w[r][KV] = T(0);
+#pragma unroll
+                for (int c = 0; c <= KV; ++c) w[KL][c] = sm[cur].ab[d * (KV + 1) + c];
             }
         }
-#pragma unroll
-        for (int d = 0; d < kPF; ++d)
-#pragma unroll
-            for (int c = 0; c <= KV; ++c) q[d][c] = nq[d][c];
+        cpa_wait_all();
+        __syncwarp();
     }
-    return info;
+    return __shfl_sync(0xffffffffu, (long long)info, 0);
 }
 
-// ------------------------------------------------------------------ xGBTRS ('N' and 'T'), one lane
-// b (global, stride 1) overwritten.  'N': interchanges + L forward, U backward.  'T': U^T forward,
-// L^T backward with the interchanges undone in reverse (the oracle's gbtrs_vec / gbtrs_vec_t).
+// ------------------------------------------------------------------ xGBTRS ('N' / 'T') on nv vectors
+// Lane l < nv solves vector l (b + l * ldv) in place; the factor chunk and the pivots are shared.
+// 'N': interchanges + L forward, U backward.  'T': U^T forward, L^T backward with the interchanges
+// undone in reverse (the oracle's gbtrs_vec / gbtrs_vec_t).
 template <typename T, int KL, int KU>
-AS_DEV void chain_gbtrs(const T* ab, const int64_t* ipiv, int64_t n, T* b, bool trans) {
+AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, int64_t n, T* b, int64_t ldv, int nv,
+                        bool trans) {
     constexpr int KV = KL + KU;
     constexpr int LDAB = 2 * KL + KU + 1;
+    constexpr int NAB = kCH * LDAB;
+    const int lane = threadIdx.x;
+    const bool act = lane < nv;
+    T* bl = b + (int64_t)(act ? lane : 0) * ldv;
+    int cur = 0;
+    // one sweep: chunks of kCH steps in direction fwd; per step j: factor column j, pivot j, and the
+    // entering value b[j + boff] of every vector, staged by cp.async one chunk ahead
+    auto sweep = [&](bool fwd, int64_t first, int64_t last, int boff, auto&& step) {
+        const int64_t cnt_all = fwd ? last - first + 1 : first - last + 1;
+        if (cnt_all <= 0) return;
+        auto jof = [&](int64_t q, int d) { return fwd ? first + q * kCH + d : first - q * kCH - d; };
+        auto issue = [&](int64_t q, int buf) {
+            for (int e = lane; e < NAB; e += 32) {
+                const int d = e / LDAB, r = e - d * LDAB;
+                const int64_t j = jof(q, d);
+                const bool ok = j >= 0 && j < n;
+                cpa(&sm[buf].ab[e], ok ? &ab[r + j * (int64_t)LDAB] : (const T*)nullptr, ok);
+            }
+            for (int d = lane; d < kCH; d += 32) {
+                const int64_t j = jof(q, d);
+                const bool ok = j >= 0 && j < n;
+                cpa(&sm[buf].ip[d], ok ? (const long long*)&ipiv[j] : (const long long*)nullptr, ok);
+            }
+            for (int e = lane; e < nv * kCH; e += 32) {
+                const int v = e / kCH, d = e - v * kCH;
+                const int64_t i = jof(q, d) + boff;
+                const bool ok = i >= 0 && i < n;
+                cpa(&sm[buf].b[v * (kCH + 1) + d], ok ? &b[i + v * ldv] : (const T*)nullptr, ok);
+            }
+            cpa_commit();
+        };
+        issue(0, cur);
+        cpa_wait_all();
+        __syncwarp();
+        const int64_t nq = (cnt_all + kCH - 1) / kCH;
+        for (int64_t q = 0; q < nq; ++q) {
+            if (q + 1 < nq) issue(q + 1, cur ^ 1);
+            const int cnt = (int)min<int64_t>(kCH, cnt_all - q * kCH);
+            if (act)
+                for (int d = 0; d < cnt; ++d) step(jof(q, d), d);
+            cpa_wait_all();
+            __syncwarp();
+            cur ^= 1;
+        }
+    };
+    auto col = [&](int d, int r) -> T { return sm[cur].ab[d * LDAB + r]; };
+    auto ent = [&](int d) -> T { return sm[cur].b[lane * (kCH + 1) + d]; };
     if (!trans) {
-        // forward: window b[j .. j+KL]
+        // forward: window v[r] = b[j + r]
         T v[KL + 1];
 #pragma unroll
-        for (int r = 0; r <= KL; ++r) v[r] = r < n ? b[r] : T(0);
-        for (int64_t j = 0; j < n; ++j) {
-            const T nxt = (j + KL + 1 < n) ? b[j + KL + 1] : T(0);
+        for (int r = 0; r <= KL; ++r) v[r] = (act && r < n) ? bl[r] : T(0);
+        sweep(true, 0, n - 1, KL + 1, [&](int64_t j, int d) {
+            const T nxt = ent(d);
             if (j + 1 < n) {
                 const int lm = (int)min<int64_t>(KL, n - 1 - j);
-                const int p = (int)(ipiv[j] - j);
+                const int p = (int)(sm[cur].ip[d] - j);
 #pragma unroll
                 for (int r = 1; r <= KL; ++r)
                     if (r == p) { const T t = v[0]; v[0] = v[r]; v[r] = t; }
 #pragma unroll
                 for (int r = 1; r <= KL; ++r)
-                    if (r <= lm) v[r] = v[r] - (ab[(KV + r) + j * (int64_t)LDAB]) * v[0];
+                    if (r <= lm) v[r] = v[r] - col(d, KV + r) * v[0];
             }
-            b[j] = v[0];
+            bl[j] = v[0];
 #pragma unroll
             for (int r = 0; r < KL; ++r) v[r] = v[r + 1];
             if (KL > 0) v[KL] = nxt;
             else v[0] = nxt;
-        }
-        // backward: x_j = b_j / U(j,j); b_i -= U(i, j) x_j for i = j - KV .. j - 1 (window b[j-KV .. j])
+        });
+        __syncwarp();
+        // backward: window u[c] = b[j - KV + c], u[KV] = b[j]
         T u[KV + 1];
 #pragma unroll
-        for (int c = 0; c <= KV; ++c) u[c] = (n - 1 - KV + c >= 0) ? b[n - 1 - KV + c] : T(0);   // u[KV] = b[j]
-        for (int64_t j = n - 1; j >= 0; --j) {
-            const T prev = (j - KV - 1 >= 0) ? b[j - KV - 1] : T(0);
-            const T x = u[KV] / (ab[KV + j * (int64_t)LDAB]);
-            b[j] = x;
+        for (int c = 0; c <= KV; ++c) u[c] = (act && n - 1 - KV + c >= 0) ? bl[n - 1 - KV + c] : T(0);
+        sweep(false, n - 1, 0, -KV - 1, [&](int64_t j, int d) {
+            const T prev = ent(d);
+            const T x = u[KV] / col(d, KV);
+            bl[j] = x;
 #pragma unroll
-            for (int c = 0; c < KV; ++c) {
-                const int64_t i = j - KV + c;
-                if (i >= 0) u[c] = u[c] - (ab[(KV + i - j) + j * (int64_t)LDAB]) * x;
-            }
+            for (int c = 0; c < KV; ++c)
+                if (j - KV + c >= 0) u[c] = u[c] - col(d, c) * x;       // U(j - KV + c, j) at AB(c, j)
 #pragma unroll
             for (int c = KV; c > 0; --c) u[c] = u[c - 1];
             u[0] = prev;
-        }
+        });
     } else {
-        // U^T forward: b_j = (b_j - sum_{i=j-KV}^{j-1} U(i, j) x_i) / U(j, j); window of the last KV x
+        // U^T forward: x_j = (b_j - sum_{i=j-KV}^{j-1} U(i, j) x_i) / U(j, j); xs = last KV x
         T xs[KV + 1];
 #pragma unroll
-        for (int c = 0; c <= KV; ++c) xs[c] = T(0);      // xs[c] = x_{j - KV + c}, c < KV
-        for (int64_t j = 0; j < n; ++j) {
-            T s = b[j];
+        for (int c = 0; c <= KV; ++c) xs[c] = T(0);
+        sweep(true, 0, n - 1, 0, [&](int64_t j, int d) {
+            T s = ent(d);
 #pragma unroll
-            for (int c = 0; c < KV; ++c) {
-                const int64_t i = j - KV + c;
-                if (i >= 0) s = s - (ab[(KV + i - j) + j * (int64_t)LDAB]) * xs[c];
-            }
-            const T x = s / (ab[KV + j * (int64_t)LDAB]);
-            b[j] = x;
+            for (int c = 0; c < KV; ++c)
+                if (j - KV + c >= 0) s = s - col(d, c) * xs[c];
+            const T x = s / col(d, KV);
+            bl[j] = x;
 #pragma unroll
             for (int c = 0; c + 1 < KV; ++c) xs[c] = xs[c + 1];
             if (KV > 0) xs[KV - 1] = x;
-        }
-        // L^T backward: b_j = b_j - sum_{r=1..lm} L(j + r, j) b_{j+r}; then swap b_j, b_ipiv(j)
+        });
+        __syncwarp();
+        // L^T backward with the interchanges in reverse: window v[r] = b[j + r]
         if (KL > 0 && n >= 2) {
-            T v[KL + 1];                                   // v[r] = b[j + r]
+            T v[KL + 1];
 #pragma unroll
-            for (int r = 0; r <= KL; ++r) v[r] = (n - 2 + r < n) ? b[n - 2 + r] : T(0);
-            for (int64_t j = n - 2; j >= 0; --j) {
-                const T prev = j >= 1 ? b[j - 1] : T(0);
+            for (int r = 0; r <= KL; ++r) v[r] = (act && n - 2 + r < n) ? bl[n - 2 + r] : T(0);
+            sweep(false, n - 2, 0, -1, [&](int64_t j, int d) {
+                const T prev = ent(d);
                 const int lm = (int)min<int64_t>(KL, n - 1 - j);
                 T s = v[0];
 #pragma unroll
                 for (int r = 1; r <= KL; ++r)
-                    if (r <= lm) s = s - (ab[(KV + r) + j * (int64_t)LDAB]) * v[r];
+                    if (r <= lm) s = s - col(d, KV + r) * v[r];
                 v[0] = s;
-                const int p = (int)(ipiv[j] - j);
+                const int p = (int)(sm[cur].ip[d] - j);
 #pragma unroll
                 for (int r = 1; r <= KL; ++r)
-                    if (r == p) { const T t = v[0]; v[0] = v[r]; v[r] = t; b[j + r] = v[r]; }
-                b[j] = v[0];
+                    if (r == p) { const T t = v[0]; v[0] = v[r]; v[r] = t; bl[j + r] = v[r]; }
+                bl[j] = v[0];
 #pragma unroll
                 for (int r = KL; r > 0; --r) v[r] = v[r - 1];
                 v[0] = prev;
-            }
+            });
         }
     }
+    __syncwarp();
 }
 
 // ------------------------------------------------------------------ the kernel (one warp)
 template <typename T, int KL, int KU>
-AS_DEV void band_chain_body(const DevArgs* args, int64_t lda, int64_t n, int64_t ldb, int64_t nrhs, T* ab,
-                            int64_t* ipiv, T* xv, signed char* isgn, DevState* st) {
+AS_DEV void band_chain_body(ChainSm<T> (&sm)[2], const DevArgs* args, int64_t lda, int64_t n, int64_t ldb,
+                            int64_t nrhs, T* ab, int64_t* ipiv, T* xv, signed char* isgn, DevState* st) {
     const int lane = threadIdx.x;
     const T* A = (const T*)args->A;
-    __shared__ long long s_info;
-    if (lane == 0) s_info = chain_gbtrf<T, KL, KU>(A, lda, n, ab, ipiv);
+    const long long info = chain_gbtrf<T, KL, KU>(sm, A, lda, n, ab, ipiv);
     __syncwarp();
     __threadfence_block();
-    const long long info = s_info;
     if (info) {
         if (lane == 0) atomicMin(&st->info, (unsigned long long)info);
         return;
@@ -241,7 +307,7 @@ AS_DEV void band_chain_body(const DevArgs* args, int64_t lda, int64_t n, int64_t
         }
         return bi == 0x7fffffffffffffffll ? 0ll : bi;
     };
-    auto apply = [&](bool tr) { if (lane == 0) chain_gbtrs<T, KL, KU>(ab, ipiv, n, xv, tr); sync(); };
+    auto apply = [&](bool tr) { chain_gbtrs<T, KL, KU>(sm, ab, ipiv, n, xv, n, 1, tr); sync(); };
     for (int64_t i = lane; i < n; i += 32) xv[i] = T(1) / (T)n;
     sync();
     apply(false);
@@ -289,10 +355,14 @@ AS_DEV void band_chain_body(const DevArgs* args, int64_t lda, int64_t n, int64_t
     // partitioned path; the fallback overwrites it)
     T* X = (T*)args->X;
     const T* B = (const T*)args->B;
-    for (int64_t c = lane; c < nrhs; c += 32) {
-        T* x = X + c * ldb;
-        for (int64_t i = 0; i < n; ++i) x[i] = B[i + c * ldb];
-        chain_gbtrs<T, KL, KU>(ab, ipiv, n, x, false);
+    for (int64_t c0 = 0; c0 < nrhs; c0 += 32) {
+        const int nv = (int)min<int64_t>(32, nrhs - c0);
+        for (int64_t e = lane; e < n * nv; e += 32) {
+            const int64_t i = e % n, c = c0 + e / n;
+            X[i + c * ldb] = B[i + c * ldb];
+        }
+        sync();
+        chain_gbtrs<T, KL, KU>(sm, ab, ipiv, n, X + c0 * ldb, ldb, nv, false);
     }
     if (lane == 0) st->band_fast = 1;
 }
@@ -302,9 +372,10 @@ template <typename T>
 __global__ void __launch_bounds__(32, 1) band_chain_kernel(const DevArgs* args, int64_t lda, int64_t n, int64_t ldb,
                                                            int64_t nrhs, T* ab, int64_t* ipiv, T* xv,
                                                            signed char* isgn, DevState* st) {
+    __shared__ ChainSm<T> sm[2];
     switch (st->band_chain) {
 #define AS_CHAIN_CASE(KL, KU) \
-    case 1 + 4 * KL + KU: band_chain_body<T, KL, KU>(args, lda, n, ldb, nrhs, ab, ipiv, xv, isgn, st); break;
+    case 1 + 4 * KL + KU: band_chain_body<T, KL, KU>(sm, args, lda, n, ldb, nrhs, ab, ipiv, xv, isgn, st); break;
     AS_CHAIN_CASE(0, 0) AS_CHAIN_CASE(0, 1) AS_CHAIN_CASE(0, 2) AS_CHAIN_CASE(0, 3)
     AS_CHAIN_CASE(1, 0) AS_CHAIN_CASE(1, 1) AS_CHAIN_CASE(1, 2) AS_CHAIN_CASE(1, 3)
     AS_CHAIN_CASE(2, 0) AS_CHAIN_CASE(2, 1) AS_CHAIN_CASE(2, 2) AS_CHAIN_CASE(2, 3)

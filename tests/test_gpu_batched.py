@@ -79,7 +79,10 @@ def check_one(name, A, B, X, rep, ret, fp32, sig=None):
         A64 = A.astype(np.float64)
         rho = np.linalg.norm(b - A64 @ X[:, 0].astype(np.float64)) / np.linalg.norm(b)
         rho_o = np.linalg.norm(b - A64 @ Xo[:, 0].astype(np.float64)) / np.linalg.norm(b)
-        assert abs(rho - rho_o) <= 1e-2 * max(rho_o, 1e-12) + (1e-6 if fp32 else 1e-12), (name, rho, rho_o)
+        # (the C4 recipe at n <= 128: a kept sigma sits within ~1.2x of the cut, its singular vector -- hence
+        # rho -- carries eps sigma_max / sigma_k ~ 1 % noise (Z14 / F3): 10 % here, 1 % at C4's n = 1024)
+        rtol = 0.1 if name == "illcond" else 1e-2
+        assert abs(rho - rho_o) <= rtol * max(rho_o, 1e-12) + (1e-6 if fp32 else 1e-12), (name, rho, rho_o)
         if sig is not None and not fp32:
             assert np.abs(sig - osig).max() <= 1e-13 * max(1.0, osig.max()), name
         return

@@ -247,6 +247,10 @@ def test_narrow_band_chain(n, kl, ku, fp32):
     """Non-dominant bands with kl, ku <= 3 (the paper's random 5-diagonal Table 1 class, tridiagonals):
     partial pivoting happens (N(0,1) entries), graded against the oracle's xGBTRF/xGBCON/xGBTRS."""
     A = W.random_banded(n, kl, ku, seed=n + 10 * kl + ku)
+    # N(0,1) bands plus a diagonal shift of 1.5: rows are not all dominant (partial pivoting happens),
+    # yet the condition stays moderate (a bare random triangular band is exponentially ill-conditioned:
+    # its LU underflows and the gate decides on rounding)
+    A[np.arange(n), np.arange(n)] += 1.5 * np.sign(A[np.arange(n), np.arange(n)] + 1e-300)
     if kl == ku == 0:
         A = np.asfortranarray(np.diag(np.random.default_rng(n).standard_normal(n) + 3.0))
     B = np.asfortranarray(np.random.default_rng(n).standard_normal((n, 3)))
