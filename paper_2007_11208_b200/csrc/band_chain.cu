@@ -34,6 +34,7 @@ template <typename T>
 struct ChainSm {
     T ab[kCH * kMaxLdab];          // factor columns of the chunk (or A's entering rows for xGBTRF)
     long long ip[kCH];
+    T rd[kCH];                     // 1 / u_jj of the chunk
     T b[32 * (kCH + 1)];           // entering right-hand-side values, one row of kCH + 1 per lane
 };
 
@@ -53,7 +54,7 @@ AS_DEV void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory")
 // ------------------------------------------------------------------ xGBTRF (chain on lane 0)
 template <typename T, int KL, int KU>
 AS_DEV int64_t chain_gbtrf(ChainSm<T> (&sm)[2], const T* __restrict__ A, int64_t lda, int64_t n, T* ab,
-                           int64_t* ipiv) {
+                           int64_t* ipiv, T* rdiag) {
     constexpr int KV = KL + KU;
     constexpr int LDAB = 2 * KL + KU + 1;
     constexpr int NE = kCH * (KV + 1);
@@ -118,6 +119,7 @@ AS_DEV int64_t chain_gbtrf(ChainSm<T> (&sm)[2], const T* __restrict__ A, int64_t
                 } else if (info == 0) {
                     info = j + 1;
                 }
+                rdiag[j] = T(1) / w[0][0];                              // the solves multiply by 1/u_jj
                 // factor column j: U(j, j + c) at AB(KV - c, j + c), L(j + r, j) at AB(KV + r, j)
 #pragma unroll
                 for (int c = 0; c <= KV; ++c)
@@ -145,8 +147,8 @@ AS_DEV int64_t chain_gbtrf(ChainSm<T> (&sm)[2], const T* __restrict__ A, int64_t
 // 'N': interchanges + L forward, U backward.  'T': U^T forward, L^T backward with the interchanges
 // undone in reverse (the oracle's gbtrs_vec / gbtrs_vec_t).
 template <typename T, int KL, int KU>
-AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, int64_t n, T* b, int64_t ldv, int nv,
-                        bool trans) {
+AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, const T* rdiag, int64_t n, T* b,
+                        int64_t ldv, int nv, bool trans) {
     constexpr int KV = KL + KU;
     constexpr int LDAB = 2 * KL + KU + 1;
     constexpr int NAB = kCH * LDAB;
@@ -171,6 +173,7 @@ AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, i
                 const int64_t j = jof(q, d);
                 const bool ok = j >= 0 && j < n;
                 cpa(&sm[buf].ip[d], ok ? (const long long*)&ipiv[j] : (const long long*)nullptr, ok);
+                cpa(&sm[buf].rd[d], ok ? &rdiag[j] : (const T*)nullptr, ok);
             }
             for (int e = lane; e < nv * kCH; e += 32) {
                 const int v = e / kCH, d = e - v * kCH;
@@ -226,7 +229,7 @@ AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, i
         for (int c = 0; c <= KV; ++c) u[c] = (act && n - 1 - KV + c >= 0) ? bl[n - 1 - KV + c] : T(0);
         sweep(false, n - 1, 0, -KV - 1, [&](int64_t j, int d) {
             const T prev = ent(d);
-            const T x = u[KV] / col(d, KV);
+            const T x = u[KV] * sm[cur].rd[d];
             bl[j] = x;
 #pragma unroll
             for (int c = 0; c < KV; ++c)
@@ -245,7 +248,7 @@ AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, i
 #pragma unroll
             for (int c = 0; c < KV; ++c)
                 if (j - KV + c >= 0) s = s - col(d, c) * xs[c];
-            const T x = s / col(d, KV);
+            const T x = s * sm[cur].rd[d];
             bl[j] = x;
 #pragma unroll
             for (int c = 0; c + 1 < KV; ++c) xs[c] = xs[c + 1];
@@ -282,10 +285,10 @@ AS_DEV void chain_gbtrs(ChainSm<T> (&sm)[2], const T* ab, const int64_t* ipiv, i
 // ------------------------------------------------------------------ the kernel (one warp)
 template <typename T, int KL, int KU>
 AS_DEV void band_chain_body(ChainSm<T> (&sm)[2], const DevArgs* args, int64_t lda, int64_t n, int64_t ldb,
-                            int64_t nrhs, T* ab, int64_t* ipiv, T* xv, signed char* isgn, DevState* st) {
+                            int64_t nrhs, T* ab, int64_t* ipiv, T* xv, signed char* isgn, T* rdiag, DevState* st) {
     const int lane = threadIdx.x;
     const T* A = (const T*)args->A;
-    const long long info = chain_gbtrf<T, KL, KU>(sm, A, lda, n, ab, ipiv);
+    const long long info = chain_gbtrf<T, KL, KU>(sm, A, lda, n, ab, ipiv, rdiag);
     __syncwarp();
     __threadfence_block();
     if (info) {
@@ -307,7 +310,7 @@ AS_DEV void band_chain_body(ChainSm<T> (&sm)[2], const DevArgs* args, int64_t ld
         }
         return bi == 0x7fffffffffffffffll ? 0ll : bi;
     };
-    auto apply = [&](bool tr) { chain_gbtrs<T, KL, KU>(sm, ab, ipiv, n, xv, n, 1, tr); sync(); };
+    auto apply = [&](bool tr) { chain_gbtrs<T, KL, KU>(sm, ab, ipiv, rdiag, n, xv, n, 1, tr); sync(); };
     for (int64_t i = lane; i < n; i += 32) xv[i] = T(1) / (T)n;
     sync();
     apply(false);
@@ -362,7 +365,7 @@ AS_DEV void band_chain_body(ChainSm<T> (&sm)[2], const DevArgs* args, int64_t ld
             X[i + c * ldb] = B[i + c * ldb];
         }
         sync();
-        chain_gbtrs<T, KL, KU>(sm, ab, ipiv, n, X + c0 * ldb, ldb, nv, false);
+        chain_gbtrs<T, KL, KU>(sm, ab, ipiv, rdiag, n, X + c0 * ldb, ldb, nv, false);
     }
     if (lane == 0) st->band_fast = 1;
 }
@@ -371,11 +374,11 @@ AS_DEV void band_chain_body(ChainSm<T> (&sm)[2], const DevArgs* args, int64_t ld
 template <typename T>
 __global__ void __launch_bounds__(32, 1) band_chain_kernel(const DevArgs* args, int64_t lda, int64_t n, int64_t ldb,
                                                            int64_t nrhs, T* ab, int64_t* ipiv, T* xv,
-                                                           signed char* isgn, DevState* st) {
+                                                           signed char* isgn, T* rdiag, DevState* st) {
     __shared__ ChainSm<T> sm[2];
     switch (st->band_chain) {
 #define AS_CHAIN_CASE(KL, KU) \
-    case 1 + 4 * KL + KU: band_chain_body<T, KL, KU>(sm, args, lda, n, ldb, nrhs, ab, ipiv, xv, isgn, st); break;
+    case 1 + 4 * KL + KU: band_chain_body<T, KL, KU>(sm, args, lda, n, ldb, nrhs, ab, ipiv, xv, isgn, rdiag, st); break;
     AS_CHAIN_CASE(0, 0) AS_CHAIN_CASE(0, 1) AS_CHAIN_CASE(0, 2) AS_CHAIN_CASE(0, 3)
     AS_CHAIN_CASE(1, 0) AS_CHAIN_CASE(1, 1) AS_CHAIN_CASE(1, 2) AS_CHAIN_CASE(1, 3)
     AS_CHAIN_CASE(2, 0) AS_CHAIN_CASE(2, 1) AS_CHAIN_CASE(2, 2) AS_CHAIN_CASE(2, 3)
@@ -390,10 +393,10 @@ __global__ void __launch_bounds__(32, 1) band_chain_kernel(const DevArgs* args, 
 void launch_band_chain(const Work& w, cudaStream_t s) {
     if (w.dtype == AS_F64)
         band_chain_kernel<double><<<1, 32, 0, s>>>(w.args, w.lda, w.n, w.ldb, w.nrhs, (double*)w.W, w.ipiv,
-                                                    (double*)w.xe, (signed char*)w.zx, w.st);
+                                                    (double*)w.xe, (signed char*)w.zx, (double*)w.vec, w.st);
     else
         band_chain_kernel<float><<<1, 32, 0, s>>>(w.args, w.lda, w.n, w.ldb, w.nrhs, (float*)w.W, w.ipiv,
-                                                   (float*)w.xe, (signed char*)w.zx, w.st);
+                                                   (float*)w.xe, (signed char*)w.zx, (float*)w.vec, w.st);
 }
 
 }  // namespace as

@@ -1665,7 +1665,12 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
             cudaGetLastError();
         }
     }
-    if (!coop && lf_panel_launch<T>(w, k0, nbp, seq_base, prio, s)) return;
+    // the leaf panel beside the big GEMMs (it leaves the SMs to them); below lf_min_m rows the GEMM of
+    // a block is shorter than a leaf panel (~0.9 ms per 128 columns: latency of the per-column
+    // multi-CTA exchange) and the faster cooperative panel (rows in shared memory, ~0.45 ms) wins even
+    // though it occupies m/128 SMs
+    static const int64_t lf_min_m = getenv("AS_LU_LF_MIN_M") ? atoll(getenv("AS_LU_LF_MIN_M")) : 10240;
+    if (!coop && m > lf_min_m && lf_panel_launch<T>(w, k0, nbp, seq_base, prio, s)) return;
     const int64_t chunk = (m + P - 1) / P;
     size_t smem = sizeof(T) * ((chunk | 1) * nbp + nbp);
     int use_smem = 1;

@@ -191,6 +191,8 @@ def sym_systems(n, seed):
     if n >= 2:
         K[0, 1] = K[1, 0] = 1.0
         K[np.arange(2, n), np.arange(2, n)] = 1.0 + rng.random(n - 2)
+    if n >= 4:
+        K[0, n - 1] = K[n - 1, 0] = 0.1    # far corner: not banded, so the symmetric path decides
     out.append(("sym_2x2_block", K))
     out.append(("spd", W.random_spd_fig3(n, seed=seed)))
     out.append(("asym", W.random_dense(n, seed=seed)))
