@@ -1090,39 +1090,45 @@ constexpr int kSU2LD = kBW + 1;
 template <typename T>
 __global__ void __launch_bounds__(256) linv128_kernel(const T* W, int64_t ldw, int64_t k0, int bw, const T* Dinv,
                                                       T* Linv) {
+    // CTA c writes columns [16 c, 16 c + 16) of the 128 x 128 inverse; CTAs 0..3 form their slice of
+    // the off-diagonal block C = -Lc^{-1} (Lb La^{-1}) (two 64 x 64 x 16 products)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* Ai = (T*)smem_raw;
-    T* Ci = Ai + kB64 * kB64;
-    T* Lb = Ci + kB64 * kB64;
-    T* T1 = Lb + kB64 * kB64;
+    T* Ci = (T*)smem_raw;                // 64 x 64
+    T* Lb = Ci + kB64 * kB64;            // 64 x 64
+    T* Aic = Lb + kB64 * kB64;           // 64 x 16 (La^{-1} columns of the slice)
+    T* T1 = Aic + kB64 * 16;             // 64 x 16
     const int p1 = min(kB64, bw), p2 = bw - p1;
     const T* Da = Dinv + (k0 / kB64) * (int64_t)kB64 * kB64;
-    for (int e = threadIdx.x; e < kB64 * kB64; e += 256) {
-        const int r = e & 63, c = e >> 6;
-        Ai[e] = Da[e];
-        Ci[e] = p2 > 0 ? Da[kB64 * kB64 + e] : T(0);
-        Lb[e] = (p2 > 0 && r < p2 && c < p1) ? W[(k0 + kB64 + r) + (k0 + c) * ldw] : T(0);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < kB64 * kB64; e += 256) {          // T1 = Lb La^{-1}
-        const int r = e & 63, c = e >> 6;
-        T acc = T(0);
-        for (int k = 0; k < kB64; ++k) acc += Lb[r + k * kB64] * Ai[k + c * kB64];
-        T1[e] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < kBW * kBW; e += 256) {
-        const int r = e & (kBW - 1), c = e >> 7;
-        T v;
-        if (r < kB64) v = c < kB64 ? (r == c ? T(1) : Ai[r + c * kB64]) : T(0);
-        else if (c >= kB64) v = r == c ? T(1) : Ci[(r - kB64) + (c - kB64) * kB64];
-        else {                                                        // -Lc^{-1} (Lb La^{-1})
-            T acc = T(0);
-            for (int k = 0; k < kB64; ++k) acc += Ci[(r - kB64) + k * kB64] * T1[k + c * kB64];
-            v = -acc;
+    const int cb = blockIdx.x * 16;      // first output column
+    const bool left = cb < kB64;
+    if (left && p2 > 0) {
+        for (int e = threadIdx.x; e < kB64 * kB64; e += 256) {
+            const int r = e & 63, c = e >> 6;
+            Ci[e] = Da[kB64 * kB64 + e];
+            Lb[e] = (r < p2 && c < p1) ? W[(k0 + kB64 + r) + (k0 + c) * ldw] : T(0);
         }
+        for (int e = threadIdx.x; e < kB64 * 16; e += 256) Aic[e] = Da[(e & 63) + (cb + (e >> 6)) * kB64];
+        __syncthreads();
+        for (int e = threadIdx.x; e < kB64 * 16; e += 256) {      // T1 = Lb La^{-1}(:, slice)
+            const int r = e & 63, c = e >> 6;
+            T acc = T(0);
+            for (int k = 0; k < kB64; ++k) acc += Lb[r + k * kB64] * Aic[k + c * kB64];
+            T1[e] = acc;
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < kBW * 16; e += 256) {
+        const int r = e & (kBW - 1), c = cb + (e >> 7);
+        T v;
+        if (r < kB64) v = c < kB64 ? (r == c ? T(1) : Da[r + c * kB64]) : T(0);
+        else if (c >= kB64) v = r == c ? T(1) : (p2 > 0 ? Da[kB64 * kB64 + (r - kB64) + (c - kB64) * kB64] : T(0));
+        else if (p2 > 0) {                                          // -Lc^{-1} (Lb La^{-1})
+            T acc = T(0);
+            for (int k = 0; k < kB64; ++k) acc += Ci[(r - kB64) + k * kB64] * T1[k + (c - cb) * kB64];
+            v = -acc;
+        } else v = T(0);
         if (r >= bw || c >= bw) v = r == c ? T(1) : T(0);
-        Linv[e] = v;
+        Linv[r + (int64_t)c * kBW] = v;
     }
 }
 
@@ -1552,6 +1558,7 @@ static bool small_lu_launch(const Work& w, cudaStream_t s) {
 struct LuStreams {
     cudaStream_t hi = nullptr;
     cudaStream_t side = nullptr;   // interchanges into the finished L columns (off the critical path)
+    cudaStream_t aux = nullptr;    // second stream of the chunked swap + U12 / trailing GEMM
     cudaEvent_t ev[64];
     int next = 0;
     int prio_hi = 0;
@@ -1565,6 +1572,7 @@ static LuStreams& lu_streams() {
         L.prio_hi = hi;
         cudaStreamCreateWithPriority(&L.hi, cudaStreamNonBlocking, hi);
         cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, lo);
+        cudaStreamCreateWithPriority(&L.aux, cudaStreamNonBlocking, lo);
         for (auto& e : L.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     }
     return L;
@@ -1714,9 +1722,9 @@ static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
     cudaFuncSetAttribute(lu_linv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     lu_linv_kernel<T><<<(nbp + kB64 - 1) / kB64, 256, smem, s>>>((const T*)w.W, w.ldw, k0, nbp, (T*)w.Dinv0);
     if (w.linv && k0 + nbp < w.n) {      // the full block inverse for the fused interchanges + U12
-        const int sm2 = (int)(sizeof(T) * 4 * kB64 * kB64);
+        const int sm2 = (int)(sizeof(T) * (2 * kB64 * kB64 + 2 * kB64 * 16));
         cudaFuncSetAttribute(linv128_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-        linv128_kernel<T><<<1, 256, sm2, s>>>((const T*)w.W, w.ldw, k0, nbp, (const T*)w.Dinv0,
+        linv128_kernel<T><<<kBW / 16, 256, sm2, s>>>((const T*)w.W, w.ldw, k0, nbp, (const T*)w.Dinv0,
                                              (T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW);
     }
 }
@@ -1824,9 +1832,29 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
             cudaStreamWaitEvent(LS.hi, e0, 0);
             gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
             block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
-            swap_u12_launch<T>(w, k0, bw, kn + nbw, n, s);
-            gemm_launch<T>(w, kn, kn + nbw, k0, M, n - kn - nbw, bw, s, 0, getenv("AS_LU_ONE_PER_SM") != nullptr,
-                           (int)(k0 / kBW) * 4 + 0);
+            // the other columns: swap + U12, then the bulk GEMM, in column chunks alternating between
+            // two streams, so that chunk i's GEMM overlaps chunk i+1's (memory-bound) swap + U12
+            const int64_t c0r = kn + nbw, rn = n - c0r;
+            static const int nch_env = getenv("AS_LU_SWAP_CHUNKS") ? atoi(getenv("AS_LU_SWAP_CHUNKS")) : 4;
+            const int nch = rn >= 4096 ? nch_env : rn >= 1024 ? std::min(nch_env, 2) : 1;
+            if (nch <= 1) {
+                swap_u12_launch<T>(w, k0, bw, c0r, n, s);
+                gemm_launch<T>(w, kn, c0r, k0, M, rn, bw, s, 0, false, (int)(k0 / kBW) * 4 + 0);
+            } else {
+                cudaEvent_t ea = ev();
+                cudaEventRecord(ea, s);
+                cudaStreamWaitEvent(LS.aux, ea, 0);
+                for (int i = 0; i < nch; ++i) {
+                    auto bnd = [&](int q) { return q >= nch ? n : c0r + (rn * q / nch + 63) / 64 * 64; };
+                    const int64_t a0 = bnd(i), a1 = bnd(i + 1);
+                    cudaStream_t st = (i & 1) ? LS.aux : s;
+                    swap_u12_launch<T>(w, k0, bw, a0, a1, st);
+                    gemm_launch<T>(w, kn, a0, k0, M, a1 - a0, bw, st, 0, false, (int)(k0 / kBW) * 4 + 0);
+                }
+                cudaEvent_t eb = ev();
+                cudaEventRecord(eb, LS.aux);
+                cudaStreamWaitEvent(s, eb, 0);
+            }
             cudaEvent_t e1 = ev();
             cudaEventRecord(e1, LS.hi);
             cudaStreamWaitEvent(s, e1, 0);
