@@ -294,20 +294,26 @@ __global__ void __launch_bounds__(s2::NT, 2) gemm_sgemm_nn_kernel(GemmArgs g) {
 // CTA tile 128 x 64 x 16, 4 warps (2 x 2, warp tile 64 x 32 = 8 x 4 DMMA tiles),
 // 3-stage cp.async pipeline, 2 CTAs per SM so one CTA's C read-modify-write
 // epilogue overlaps the other's MMA main loop.
-namespace d2 {
-constexpr int BM = 128, BN = 64, BK = 16, ST = 2, NT = 128;
-constexpr int LDA_KM = BM + 4;   // A as [k][m]
-constexpr int LDA_MK = BK + 4;   // A as [m][k]
-constexpr int LDB_NK = BK + 4;   // B as [n][k]
-constexpr int LDB_KN = BN + 4;   // B as [k][n]
-constexpr int AEL = (BK * LDA_KM > BM * LDA_MK) ? BK * LDA_KM : BM * LDA_MK;
-constexpr int BEL = (BN * LDB_NK > BK * LDB_KN) ? BN * LDB_NK : BK * LDB_KN;
-}  // namespace d2
+constexpr int kGemmCfgDefault = 0;
+// tile configuration of the DMMA GEMM: k-tile BK_ and pipeline depth ST_ (the launcher's choice,
+// measured in tools/gemm_bench.py); BM x BN = 128 x 64, 4 warps of 64 x 32
+template <int BK_, int ST_>
+struct D2 {
+    static constexpr int BM = 128, BN = 64, BK = BK_, ST = ST_, NT = 128;
+    static constexpr int LDA_KM = BM + 4;   // A as [k][m]
+    static constexpr int LDA_MK = BK + 4;   // A as [m][k]
+    static constexpr int LDB_NK = BK + 4;   // B as [n][k]
+    static constexpr int LDB_KN = BN + 4;   // B as [k][n]
+    static constexpr int AEL = (BK * LDA_KM > BM * LDA_MK) ? BK * LDA_KM : BM * LDA_MK;
+    static constexpr int BEL = (BN * LDB_NK > BK * LDB_KN) ? BN * LDB_NK : BK * LDB_KN;
+};
+using d2 = D2<16, 2>;
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, class d2>
 AS_DEV void stage_d2(double* As, double* Bs, const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M,
                      int64_t N, int64_t K, int64_t m0, int64_t n0, int64_t k0) {
-    using namespace d2;
+    constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK, NT = d2::NT;
+    constexpr int LDA_KM = d2::LDA_KM, LDA_MK = d2::LDA_MK, LDB_NK = d2::LDB_NK, LDB_KN = d2::LDB_KN;
     if (!TA) {      // BK columns x BM contiguous m: chunk = 2 doubles
         for (int e = threadIdx.x; e < BK * (BM / 2); e += NT) {
             const int kk = e / (BM / 2), mm = (e % (BM / 2)) * 2;
@@ -344,9 +350,11 @@ AS_DEV void stage_d2(double* As, double* Bs, const double* A, int64_t lda, const
     }
 }
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, class d2>
 __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
-    using namespace d2;
+    constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK, ST = d2::ST;
+    constexpr int LDA_KM = d2::LDA_KM, LDA_MK = d2::LDA_MK, LDB_NK = d2::LDB_NK, LDB_KN = d2::LDB_KN;
+    constexpr int AEL = d2::AEL, BEL = d2::BEL;
     if (g.skip && *g.skip) return;
     if (g.trace_min && threadIdx.x == 0) atomicMin(g.trace_min, gtimer());
     const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     const int nk = (int)((g.K + BK - 1) / BK);
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
-        if (s < nk) stage_d2<TA, TB>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)s * BK);
+        if (s < nk) stage_d2<TA, TB, d2>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)s * BK);
         cp_async_commit();
     }
     // acc starts as C (all loads in flight together, overlapping the prologue);
@@ -386,7 +394,7 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
         const int nxt = kt + ST - 1;
         if (nxt < nk) {
             const int s = nxt % ST;
-            stage_d2<TA, TB>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)nxt * BK);
+            stage_d2<TA, TB, d2>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)nxt * BK);
         }
         cp_async_commit();
         const double* as = As + (kt % ST) * AEL;
@@ -488,16 +496,28 @@ static void launch_k(K kern, const GemmArgs& g, size_t smem, cudaStream_t s) {
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
     if (dtype == AS_F64) {
-        const size_t smem = g.one_per_sm ? (size_t)116 * 1024 : sizeof(double) * d2::ST * (d2::AEL + d2::BEL);
-        auto go = [&](auto kern) {
-            dim3 grid((unsigned)((g.M + d2::BM - 1) / d2::BM), (unsigned)((g.N + d2::BN - 1) / d2::BN));
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            kern<<<grid, d2::NT, smem, s>>>(g);
+        // AS_GEMM_CFG (A/B measurements): 0 BK 16 x 2 stages (default), 1: 16 x 3, 2: 32 x 2, 3: 32 x 3
+        const char* ce = getenv("AS_GEMM_CFG");
+        const int cfg = ce ? atoi(ce) : kGemmCfgDefault;
+        auto run = [&](auto cfgtag) {
+            using C = decltype(cfgtag);
+            const size_t smem = sizeof(double) * C::ST * (C::AEL + C::BEL);
+            auto go = [&](auto kern) {
+                dim3 grid((unsigned)((g.M + C::BM - 1) / C::BM), (unsigned)((g.N + C::BN - 1) / C::BN));
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kern<<<grid, C::NT, smem, s>>>(g);
+            };
+            if (!g.TA && !g.TB) go(gemm_dmma2_kernel<false, false, C>);
+            else if (!g.TA && g.TB) go(gemm_dmma2_kernel<false, true, C>);
+            else if (g.TA && !g.TB) go(gemm_dmma2_kernel<true, false, C>);
+            else go(gemm_dmma2_kernel<true, true, C>);
         };
-        if (!g.TA && !g.TB) go(gemm_dmma2_kernel<false, false>);
-        else if (!g.TA && g.TB) go(gemm_dmma2_kernel<false, true>);
-        else if (g.TA && !g.TB) go(gemm_dmma2_kernel<true, false>);
-        else go(gemm_dmma2_kernel<true, true>);
+        switch (cfg) {
+        case 1: run(D2<16, 3>{}); break;
+        case 2: run(D2<32, 2>{}); break;
+        case 3: run(D2<32, 3>{}); break;
+        default: run(D2<16, 2>{}); break;
+        }
     } else {
         // NN with 16-byte aligned operands (the LU trailing update): the v2 kernel
         const bool al = (((uintptr_t)g.A | (uintptr_t)g.B | (uintptr_t)g.C) & 15) == 0 && g.lda % 4 == 0 &&
