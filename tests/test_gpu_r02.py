@@ -279,3 +279,37 @@ def test_narrow_band_chain_pivots_and_singular():
     A2[600, :] = 0.0
     rep, orep = check_parity(A2, B[:, :2].copy(order="F"))
     assert rep["flags"] & oracle.F_SINGULAR
+
+
+# ------------------------------------------------------------------ race evidence (compute-sanitizer is closed on this pool)
+@pytest.mark.parametrize("case", ["lu_leaf", "lu_coop", "lu_cluster", "upper", "spd", "band_spike", "band_chain", "svd"])
+def test_repeat_bitwise_deterministic(case):
+    """Every path with cross-CTA exchanges (sync-free epoch-tagged TRSM words, sequence-numbered and
+    self-validating panel slots, spin grid barriers) solves the same input 25 times: X, flags and
+    rcond must be bitwise identical every time (no floating-point atomics on numeric paths, so any
+    difference is a race), and equal the oracle's within the parity bars."""
+    mats = {
+        "lu_leaf": lambda: W.make("C5", n=11000, nrhs=2, seed=3),      # first blocks: leaf panel (m > 10240)
+        "lu_coop": lambda: W.make("C5", n=3000, nrhs=2, seed=4),
+        "lu_cluster": lambda: W.make("C5", n=1000, nrhs=2, seed=5),
+        "upper": lambda: (W.random_triangular(2500, upper=True, seed=6), np.ones((2500, 3))),
+        "spd": lambda: (W.random_spd_fig3(1500, seed=7), np.ones((1500, 3))),
+        "band_spike": lambda: W.make("C2", n=5000, nrhs=3),
+        "band_chain": lambda: (W.random_banded(3000, 2, 2, seed=8), np.ones((3000, 2))),
+        "svd": lambda: W.illcond_c4(n=160, seed=9)[:2],
+    }
+    A, B = mats[case]()
+    A, B = np.asfortranarray(A), np.asfortranarray(B)
+    dA, dB = AS.to_device(A), AS.to_device(B)
+    X = AS.empty_colmajor(B.shape[0], B.shape[1], dB.dtype)
+    ref = None
+    for _ in range(25 if A.shape[0] < 8000 else 6):
+        ret, _, rep = AS.as_solve_ex(dA, dB, X=X)
+        torch.cuda.synchronize()
+        cur = (ret, rep["flags"], rep["rcond"], X.cpu().numpy().tobytes())
+        if ref is None:
+            ref = cur
+        else:
+            assert cur == ref, case
+    if A.shape[0] <= 3000:
+        check_parity(A, B)
