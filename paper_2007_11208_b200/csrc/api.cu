@@ -722,7 +722,7 @@ static std::map<std::tuple<int, int, int64_t, int64_t>, std::unique_ptr<DetPlan>
 __global__ void det_out_kernel(const DevState* st, as_structure* out, int fullscan) {
     if (threadIdx.x != 0) return;
     as_structure o;
-    o.flags = st->alive;
+    o.flags = st->alive & ~st->pair_kill;
     // BANDED alive at the end means every tile was read: kl/ku are final, re-check the 25% rule on the pair
     if ((o.flags & AS_FLAG_BANDED) && !band_density_ok(st->n, st->kl, st->ku)) o.flags &= ~AS_FLAG_BANDED;
     o.nonfinite_seen = (st->flags & AS_FLAG_NONFINITE) ? 1 : 0;

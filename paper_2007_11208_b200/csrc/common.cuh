@@ -29,6 +29,7 @@ struct DevState {
     int32_t kl, ku;               // running max (atomicMax)
     unsigned long long max_diag;  // ordered bits of (double)max positive diagonal
     uint32_t pair_ticket;         // detection work queue
+    uint32_t pair_kill;           // candidates killed by the tile-pair pass (alive keeps the diagonal pass's)
     uint32_t opts;                // AS_OPT_* of this plan
     int32_t force_method;
     int32_t method;               // dispatch method (after Cholesky failure: LU)

@@ -207,49 +207,45 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
     const int r_loc = 2 * lane;
     // candidates only die, so the alive mask seen at the previous pair's barrier is a safe
     // (conservative) guide for which tiles to load: no L2 round trip before the loads
-    unsigned known = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+    // Kills of this pass go to st->pair_kill; st->alive keeps the diagonal pass's verdicts for the
+    // whole kernel, so every CTA takes the same mode (streaming vs tile pairs) from it; the current
+    // state is alive & ~pair_kill.
+    auto cur_alive = [&]() { return *(volatile unsigned*)&st->alive & ~*(volatile unsigned*)&st->pair_kill; };
+    const unsigned alive0 = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+    unsigned known = fullscan ? 0xFu : cur_alive();
 
     for (unsigned p = blockIdx.x; p < total; p += gridDim.x) {
-        if (!fullscan && (known == AS_FLAG_UPPER || known == AS_FLAG_LOWER)) {
-            // ---- only one triangular candidate left: one tile per pair decides (UPPER: the lower
-            // tile must be zero; LOWER: the mirror tile), so the next pair's tile is loaded into
-            // the second register buffer before the current one is checked (loads stay in flight)
-            const bool up_only = known == AS_FLAG_UPPER;
-            auto load = [&](unsigned q, T (&v)[16]) {
-                long long I2, J2;
-                pair_of(q, nt, I2, J2);
-                const bool inter = (I2 * kTile + kTile <= n) && (J2 * kTile + kTile <= n);
-                if (up_only) load_tile_regs<T>(v, A, lda, n, I2 * kTile, J2 * kTile, vec, inter);
-                else load_tile_regs<T>(v, A, lda, n, J2 * kTile, I2 * kTile, vec, inter);
-            };
-            T cur[16], nxt[16];
-            load(p, cur);
-            for (;;) {
-                const unsigned pn = p + gridDim.x;
-                const bool has_next = pn < total;
-                if (has_next) load(pn, nxt);
-                // the early-exit decision travels through the barrier's reduction itself (no shared
-                // word that the next iteration's write could race with a slow warp's read)
-                const bool gone = threadIdx.x == 0 && *(volatile unsigned*)&st->alive == 0u;
-                long long I, J;
-                pair_of(p, nt, I, J);
-                bool nz = false;
+        if (!fullscan && (alive0 == AS_FLAG_UPPER || alive0 == AS_FLAG_LOWER)) {
+            // ---- only one triangular candidate left (C3b after the corner pair): the question is
+            // only "is the other strict triangle all zero?".  In column-major storage
+            // the strict lower (upper) part of column j is ONE contiguous run, rows j+1..n-1 (0..j-1),
+            // so it is streamed, not tiled: a warp takes the column pair (u, n-1-u) (n-1 elements
+            // together, balanced), 16 independent loads in flight per lane, no block barriers; a
+            // non-zero kills the candidate (the verdict is an AND over elements, Z8) and every warp
+            // stops at its next check of the alive mask.
+            const bool up_only = alive0 == AS_FLAG_UPPER;
+            const long long gw = (long long)blockIdx.x * (kDetThreads / 32) + warp;
+            const long long nw = (long long)gridDim.x * (kDetThreads / 32);
+            bool nz = false;
+            for (long long u = gw; u < (n + 1) / 2 && !nz; u += nw) {
+                for (int h = 0; h < 2 && !nz; ++h) {
+                    const long long j = h ? n - 1 - u : u;
+                    if (h && j == u) break;
+                    const long long r0 = up_only ? j + 1 : 0, r1 = up_only ? n : j;
+                    const T* col = A + j * lda;
+                    for (long long r = r0 + lane; r < r1; r += 32 * 16) {
+                        T v[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
-                    // diagonal tile: only the strict lower (UPPER candidate) / strict upper part counts
-                    nz |= cur[i] != T(0) && (I != J || (up_only ? r > c : c > r));
-                }
-                const int v = __syncthreads_or((nz ? 1 : 0) | (gone ? 2 : 0));
-                if (v & 1) {
-                    if (threadIdx.x == 0) atomicAnd(&st->alive, ~known);
-                    return;
-                }
-                if ((v & 2) || !has_next) return;
-                p = pn;
+                        for (int k = 0; k < 16; ++k) v[k] = r + 32 * k < r1 ? __ldcs(col + r + 32 * k) : T(0);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+                        for (int k = 0; k < 16; ++k) nz |= v[k] != T(0);
+                    }
+                    nz = __any_sync(0xffffffffu, nz);
+                }
+                if (!nz && cur_alive() == 0u) break;   // another warp found one
             }
+            if (nz && lane == 0) atomicOr(&st->pair_kill, alive0);
+            return;
         }
         long long I, J;
         pair_of(p, nt, I, J);
@@ -291,7 +287,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
             if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&st->flags, AS_FLAG_NONFINITE);
         }
         if (threadIdx.x == 0) {
-            s_alive = fullscan ? 0xFu : *(volatile unsigned*)&st->alive;
+            s_alive = fullscan ? 0xFu : cur_alive();
             s_kl = 0; s_ku = 0; s_kill = 0; s_nz = 0;
         }
         __syncthreads();
@@ -389,7 +385,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
             my_kl = gkl; my_ku = gku;
             unsigned k2 = s_kill;
             if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
-            if (k2 & alive) atomicAnd(&st->alive, ~k2);
+            if (k2 & alive) atomicOr(&st->pair_kill, k2);
         }
         __syncthreads();
     }
@@ -400,7 +396,7 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
 // else general LU; or the forced method.  Sets the SWITCH handle.
 __global__ void dispatch_kernel(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
     if (threadIdx.x != 0) return;
-    unsigned f = (st->opts & AS_OPT_SKIP_DETECT) ? 0u : st->alive;   // detection skipped: no verdicts
+    unsigned f = (st->opts & AS_OPT_SKIP_DETECT) ? 0u : (st->alive & ~st->pair_kill);   // skipped: no verdicts
     // BANDED still alive means no CTA exited early, so kl/ku are the exact extents: the 25% rule on the
     // final pair (two extents raised by different CTAs may each pass alone, Z2/Z3)
     if ((f & AS_FLAG_BANDED) && !band_density_ok(st->n, st->kl, st->ku)) f &= ~AS_FLAG_BANDED;
