@@ -247,6 +247,65 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
             if (nz && lane == 0) atomicOr(&st->pair_kill, alive0);
             return;
         }
+        if (!fullscan && alive0 == AS_FLAG_SPD_CANDIDATE) {
+            // ---- only the sympd candidate left after the diagonal pass (C3a): Fig. 4 lines 12-16 on
+            // every pair, nothing else.  The mirror tile goes through shared memory (double-buffered
+            // by pair parity), the lower tile stays in registers, and ONE barrier per pair both
+            // publishes this pair's mirror tile and reduces the previous pair's verdict.
+            bool dead = false;
+            int par = 0;
+            for (unsigned q = p; q < total; q += gridDim.x, par ^= 1) {
+                long long I, J;
+                pair_of(q, nt, I, J);
+                const long long D = I - J, r0 = I * kTile, c0 = J * kTile;
+                const bool inter = (r0 + kTile <= n) && (c0 + kTile <= n);
+                T lo[16], up[16], drow[2], dcol[8];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) drow[h] = (r0 + r_loc + h < n) ? diag[r0 + r_loc + h] : T(0);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) dcol[k] = (c0 + warp + 8 * k < n) ? diag[c0 + warp + 8 * k] : T(0);
+                load_tile_regs<T>(lo, A, lda, n, r0, c0, vec, inter);
+                if (D != 0) load_tile_regs<T>(up, A, lda, n, c0, r0, vec, inter);
+                T* us = par ? up_s : lo_s;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                    us[c * kLD3 + r] = (D != 0) ? up[i] : lo[i];
+                }
+                const bool gone = threadIdx.x == 0 && cur_alive() == 0u;
+                const int v = __syncthreads_or((dead ? 1 : 0) | (gone ? 2 : 0));
+                if (v & 1) { if (threadIdx.x == 0) atomicOr(&st->pair_kill, (unsigned)AS_FLAG_SPD_CANDIDATE); return; }
+                if (v & 2) return;
+                if (inter && D > 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                        const T a = lo[i], b = us[r * kLD3 + c];
+                        const T aa = fabs(a), ab = fabs(b), delta = fabs(a - b);
+                        dead |= ((delta > tol) & (delta > tol * aa) & (delta > tol * ab)) | (aa >= max_diag) |
+                                (aa + ab >= drow[i & 1] + dcol[i >> 1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int c = warp + 8 * (i >> 1), r = r_loc + (i & 1);
+                        const long long gi = r0 + r, gj = c0 + c;
+                        if (gi >= n || gj >= n || gi <= gj) continue;
+                        const T a = lo[i], b = us[r * kLD3 + c];
+                        const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
+                        const T df = a - b;
+                        const T delta = df < T(0) ? -df : df;                        // line 12
+                        const T m = aa > ab ? aa : ab;
+                        if (delta > tol && delta > tol * m) dead = true;             // lines 13-14
+                        if (aa >= max_diag) dead = true;                             // line 15
+                        if (aa + ab >= drow[i & 1] + dcol[i >> 1]) dead = true;      // line 16
+                    }
+                }
+            }
+            if (__syncthreads_or(dead ? 1 : 0) && threadIdx.x == 0)
+                atomicOr(&st->pair_kill, (unsigned)AS_FLAG_SPD_CANDIDATE);
+            return;
+        }
         long long I, J;
         pair_of(p, nt, I, J);
         const long long D = I - J;
