@@ -356,6 +356,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * 128 + es * 2 * 128);   // LU panel slots, rowbuf, diagbuf (128-wide)
     w.lfbuf = take(lu_lfbuf_bytes(n, w.dtype));
     w.linv = take(es * (size_t)((n + 127) / 128) * 128 * 128);
+    w.swplan = take(lu_swplan_bytes(n));
     return off;
 }
 

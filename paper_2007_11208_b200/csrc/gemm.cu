@@ -350,6 +350,37 @@ AS_DEV void stage_d2(double* As, double* Bs, const double* A, int64_t lda, const
     }
 }
 
+// Interior tiles (the whole BM x BN x BK slab inside the operands): the per-thread source pointers
+// are formed once per tile (stage_d2_ptrs) and every chunk is base + q * (compile-time stride) * ld,
+// advanced by one k-tile per call -- ~3 instructions per 16-byte chunk instead of the ~30 of the
+// bounds-checked path (r01 ncu: the staging code issued more warp instructions than the DMMAs).
+template <bool TA, bool TB, class d2>
+AS_DEV void stage_d2_ptrs(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m0, int64_t n0,
+                          const double*& pa, const double*& pb, int& sa, int& sb) {
+    constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK;
+    const int t = threadIdx.x;
+    if (!TA) { const int kk = t / (BM / 2), mm = (t % (BM / 2)) * 2; pa = A + m0 + mm + kk * lda; sa = kk * d2::LDA_KM + mm; }
+    else     { const int mm = t / (BK / 2), kk = (t % (BK / 2)) * 2; pa = A + kk + (m0 + mm) * lda; sa = mm * d2::LDA_MK + kk; }
+    if (!TB) { const int nn = t / (BK / 2), kk = (t % (BK / 2)) * 2; pb = B + kk + (n0 + nn) * ldb; sb = nn * d2::LDB_NK + kk; }
+    else     { const int kk = t / (BN / 2), nn = (t % (BN / 2)) * 2; pb = B + n0 + nn + kk * ldb; sb = kk * d2::LDB_KN + nn; }
+}
+template <bool TA, bool TB, class d2>
+AS_DEV void stage_d2_fast(double* As, double* Bs, const double* pa, int64_t lda, const double* pb, int64_t ldb, int sa,
+                          int sb) {
+    constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK, NT = d2::NT;
+    constexpr int QA = BK * (BM / 2) / NT, QB = BN * (BK / 2) / NT;
+    static_assert(BK * (BM / 2) % NT == 0 && BN * (BK / 2) % NT == 0, "chunks per thread");
+    // rows of the chunk grid covered by one pass of NT threads
+    constexpr int RA = TA ? NT / (BK / 2) : NT / (BM / 2);      // A: m rows (TA) or k columns (!TA) per pass
+    constexpr int RB = TB ? NT / (BN / 2) : NT / (BK / 2);      // B: k rows (TB) or n columns (!TB) per pass
+#pragma unroll
+    for (int q = 0; q < QA; ++q)
+        cp_async16(As + sa + q * RA * (TA ? d2::LDA_MK : d2::LDA_KM), pa + (int64_t)(q * RA) * lda, 16);
+#pragma unroll
+    for (int q = 0; q < QB; ++q)
+        cp_async16(Bs + sb + q * RB * (TB ? d2::LDB_KN : d2::LDB_NK), pb + (int64_t)(q * RB) * ldb, 16);
+}
+
 template <bool TA, bool TB, class d2>
 __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK, ST = d2::ST;
@@ -369,33 +400,52 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
     const int gid = lane >> 2, tig = lane & 3;
     const int nk = (int)((g.K + BK - 1) / BK);
+    const bool full = (m0 + BM <= g.M) && (n0 + BN <= g.N);
+    const int nkf = full ? (int)(g.K / BK) : 0;        // k-tiles [0, nkf) take the pointer-increment staging
+    const double *pa, *pb;
+    int sa, sb;
+    stage_d2_ptrs<TA, TB, d2>(A, g.lda, B, g.ldb, m0, n0, pa, pb, sa, sb);
+    const int64_t ka = TA ? (int64_t)BK : (int64_t)BK * g.lda, kb = TB ? (int64_t)BK * g.ldb : (int64_t)BK;
+    auto stage = [&](int kt) {
+        const int s = kt % ST;
+        if (kt < nkf) {
+            stage_d2_fast<TA, TB, d2>(As + s * AEL, Bs + s * BEL, pa, g.lda, pb, g.ldb, sa, sb);
+            pa += ka; pb += kb;
+        } else {
+            stage_d2<TA, TB, d2>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)kt * BK);
+        }
+    };
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
-        if (s < nk) stage_d2<TA, TB, d2>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)s * BK);
+        if (s < nk) stage(s);
         cp_async_commit();
     }
     // acc starts as C (all loads in flight together, overlapping the prologue);
     // the MMAs then accumulate acc += A (-B), so the epilogue is a plain store.
+    // The MMA runs on the transposed tile (first operand = B^T fragment, second = A^T fragment), so
+    // a thread's two accumulator values are C(r, c), C(r + 1, c) with r = .. + 2 tig, c = .. + gid:
+    // adjacent in the column-major C -> one 16-byte load / store per DMMA tile.
     double acc[8][4][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int64_t r = m0 + wm + 8 * i + gid;
+        const int64_t r = m0 + wm + 8 * i + 2 * tig;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+            const int64_t c = n0 + wn + 8 * j + gid;
+            if (full) {
+                const double2 v = __ldcg((const double2*)(C + r + c * g.ldc));
+                acc[i][j][0] = v.x; acc[i][j][1] = v.y;
+            } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
-                acc[i][j][h] = (r < g.M && c < g.N) ? __ldcg(C + r + c * g.ldc) : 0.0;
+                for (int h = 0; h < 2; ++h) acc[i][j][h] = (r + h < g.M && c < g.N) ? __ldcg(C + r + h + c * g.ldc) : 0.0;
             }
+        }
     }
     for (int kt = 0; kt < nk; ++kt) {
         cp_async_wait<ST - 2>();
         __syncthreads();
         const int nxt = kt + ST - 1;
-        if (nxt < nk) {
-            const int s = nxt % ST;
-            stage_d2<TA, TB, d2>(As + s * AEL, Bs + s * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0, (int64_t)nxt * BK);
-        }
+        if (nxt < nk) stage(nxt);
         cp_async_commit();
         const double* as = As + (kt % ST) * AEL;
         const double* bs = Bs + (kt % ST) * BEL;
@@ -415,20 +465,22 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], bf[j], af[i]);
         }
     }
     cp_async_wait<0>();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int64_t r = m0 + wm + 8 * i + gid;
-        if (r >= g.M) continue;
+        const int64_t r = m0 + wm + 8 * i + 2 * tig;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+            const int64_t c = n0 + wn + 8 * j + gid;
+            if (full) {
+                *(double2*)(C + r + c * g.ldc) = make_double2(acc[i][j][0], acc[i][j][1]);
+            } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
-                if (c < g.N) C[r + c * g.ldc] = acc[i][j][h];
+                for (int h = 0; h < 2; ++h)
+                    if (r + h < g.M && c < g.N) C[r + h + c * g.ldc] = acc[i][j][h];
             }
         }
     }

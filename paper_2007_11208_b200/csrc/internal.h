@@ -44,6 +44,7 @@ struct Work {
     void* cand;          // LU panel candidates
     void* lfbuf;         // leaf LU panel: counters, exchange slots, candidate rows, row-move staging
     void* linv;          // LU: full 128 x 128 inverse of each block's unit-lower L11 (n/128 blocks)
+    void* swplan;        // LU: per block, the composed row interchanges (lu.cu SwapPlan)
     int num_sms;
 };
 

@@ -1085,11 +1085,51 @@ __global__ void __launch_bounds__(256) swap_u12_kernel(T* W, int64_t ldw, int64_
 // tile; a CTA takes 64 trailing columns: the interchanges composed into one permutation (as above),
 // every moved value gathered before any store, then U12 = L11^{-1} Bn with L11^{-1} streamed through
 // L1 (4 rows x 8 columns per thread).
+struct SwapPlan {
+    int64_t srow[2 * kBW];   // [0, bw): source row of block position q; [bw, bw + ne): rows leaving the block
+    int64_t edst[kBW];       // destination row of leaving value e
+    int ne;
+    int pad;
+};
+constexpr int kSU3C = 16;
+constexpr int kSU3LD = kBW + 1;
+
+template <typename T>
+__device__ void swap_plan_build(const int64_t* ipiv, int64_t k0, int bw, SwapPlan* plan) {
+    __shared__ int64_t piv[kBW];
+    __shared__ int s_ne;
+    if (threadIdx.x == 0) s_ne = 0;
+    for (int q = threadIdx.x; q < bw; q += blockDim.x) piv[q] = ipiv[k0 + q];
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * bw; t += blockDim.x) {
+        int64_t x;
+        if (t < bw) x = k0 + t;
+        else {
+            x = piv[t - bw];
+            if (x < k0 + bw) continue;
+            bool first = true;
+            for (int q = 0; q < t - bw; ++q) first = first && (piv[q] != x);
+            if (!first) continue;
+        }
+        int64_t pos = x;
+        for (int q = 0; q < bw; ++q) {
+            const int64_t r = k0 + q, tq = piv[q];
+            if (pos == r) pos = tq;
+            else if (pos == tq) pos = r;
+        }
+        if (pos < k0 + bw) plan->srow[pos - k0] = x;
+        else { const int e = atomicAdd(&s_ne, 1); plan->edst[e] = pos; plan->srow[bw + e] = x; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) plan->ne = s_ne;
+}
+
 constexpr int kSU2C = 64;
 constexpr int kSU2LD = kBW + 1;
 template <typename T>
 __global__ void __launch_bounds__(256) linv128_kernel(const T* W, int64_t ldw, int64_t k0, int bw, const T* Dinv,
-                                                      T* Linv) {
+                                                      T* Linv, const int64_t* ipiv, SwapPlan* plan) {
+    if (blockIdx.x == kBW / 16) { swap_plan_build<T>(ipiv, k0, bw, plan); return; }   // the extra CTA
     // CTA c writes columns [16 c, 16 c + 16) of the 128 x 128 inverse; CTAs 0..3 form their slice of
     // the off-diagonal block C = -Lc^{-1} (Lb La^{-1}) (two 64 x 64 x 16 products)
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1203,6 +1243,76 @@ __global__ void __launch_bounds__(256) swap_u12v2_kernel(T* W, int64_t ldw, int6
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
+        const int c = cg + u;
+        if (c >= nc) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = lane + 32 * i;
+            if (r < bw) W[(k0 + r) + (cc0 + c) * ldw] = acc[i][u];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ fused interchanges + U12, v3
+// The composed permutation of a block's interchanges depends only on ipiv: it is formed once per
+// block (the extra CTA of linv128_kernel) into a SwapPlan instead of by every CTA of every launch,
+// and a CTA takes NC = 16 trailing columns (33 KB of shared memory, 6 CTAs per SM, 4x the CTAs of
+// the 64-column kernel: the r02 launch list showed 57 us per launch at 64 CTAs x 132 KB, one CTA per
+// SM, against ~2 us of fp64 work).  L11^{-1} is lower triangular: the product visits k in four
+// blocks of 32 and row group i (rows lane + 32 i) only for i >= k / 32 (62.5 % of the FMAs).
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) swap_u12v3_kernel(T* W, int64_t ldw, int64_t k0, int bw, int64_t c0, int64_t c1,
+                                                        const SwapPlan* __restrict__ plan, const T* __restrict__ Linv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Bn = (T*)smem_raw;                // [NC][kSU3LD]: column c of the block rows after the interchanges
+    T* Ex = Bn + NC * kSU3LD;            // [NC][kSU3LD]: values for the rows leaving the block
+    __shared__ int64_t srow[2 * kBW];
+    __shared__ int64_t edst[kBW];
+    const int64_t cc0 = c0 + (int64_t)blockIdx.x * NC;
+    const int nc = (int)min<int64_t>(NC, c1 - cc0);
+    if (nc <= 0) return;
+    const int ne = plan->ne, R = bw + ne;
+    for (int t = threadIdx.x; t < R; t += blockDim.x) srow[t] = plan->srow[t];
+    for (int t = threadIdx.x; t < ne; t += blockDim.x) edst[t] = plan->edst[t];
+    __syncthreads();
+    batched<16, T>(
+        R * nc, [&](int e) -> T { const int c = e / R, row = e - c * R; return W[srow[row] + (cc0 + c) * ldw]; },
+        [&](int e, T v) {
+            const int c = e / R, row = e - c * R;
+            if (row < bw) Bn[c * kSU3LD + row] = v;
+            else Ex[c * kSU3LD + row - bw] = v;
+        });
+    __syncthreads();
+    for (int e = threadIdx.x; e < ne * nc; e += blockDim.x) {
+        const int c = e / ne, row = e - c * ne;
+        W[edst[row] + (cc0 + c) * ldw] = Ex[c * kSU3LD + row];
+    }
+    // U12 = L11^{-1} Bn: lane -> rows lane + 32 i, warp -> columns CW warp .. CW warp + CW - 1
+    constexpr int CW = NC / 8;
+    const int lane = threadIdx.x & 31, cg = (threadIdx.x >> 5) * CW;
+    T acc[4][CW];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int u = 0; u < CW; ++u) acc[i][u] = T(0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int kend = min(32 * j + 32, bw);
+#pragma unroll 4
+        for (int k = 32 * j; k < kend; ++k) {
+            T l[4], bv[CW];
+#pragma unroll
+            for (int i = j; i < 4; ++i) l[i] = __ldg(&Linv[(lane + 32 * i) + k * kBW]);
+#pragma unroll
+            for (int u = 0; u < CW; ++u) bv[u] = Bn[(cg + u) * kSU3LD + k];
+#pragma unroll
+            for (int i = j; i < 4; ++i)
+#pragma unroll
+                for (int u = 0; u < CW; ++u) acc[i][u] += l[i] * bv[u];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
         const int c = cg + u;
         if (c >= nc) continue;
 #pragma unroll
@@ -1559,7 +1669,10 @@ struct LuStreams {
     cudaStream_t hi = nullptr;
     cudaStream_t side = nullptr;   // interchanges into the finished L columns (off the critical path)
     cudaStream_t aux = nullptr;    // second stream of the chunked swap + U12 / trailing GEMM
+    cudaStream_t ch[3] = {nullptr, nullptr, nullptr};   // column-chunk streams 1..3 (chunk 0 runs on the caller's stream)
     cudaEvent_t ev[64];
+    cudaEvent_t evl[2];            // dataflow schedule: "block k's panel is ready" (by step parity)
+    cudaEvent_t evc[4][2];         // dataflow schedule: chunk q finished step k (by step parity)
     int next = 0;
     int prio_hi = 0;
 };
@@ -1573,7 +1686,10 @@ static LuStreams& lu_streams() {
         cudaStreamCreateWithPriority(&L.hi, cudaStreamNonBlocking, hi);
         cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, lo);
         cudaStreamCreateWithPriority(&L.aux, cudaStreamNonBlocking, lo);
+        for (auto& c : L.ch) cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, lo);
         for (auto& e : L.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        for (auto& e : L.evl) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        for (auto& r : L.evc) for (auto& e : r) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     }
     return L;
 }
@@ -1603,6 +1719,7 @@ static LfBufs lf_layout(void* base, int64_t n, size_t es) {
     b.ubuf = take(es * kPW * kPW);
     return b;
 }
+size_t lu_swplan_bytes(int64_t n) { return sizeof(SwapPlan) * (size_t)((n + kBW - 1) / kBW); }
 size_t lu_lfbuf_bytes(int64_t n, int dtype) { return (size_t)(lf_layout(nullptr, n, dtype == AS_F64 ? 8 : 4).ubuf) +
                                                      (dtype == AS_F64 ? 8 : 4) * kPW * kPW; }
 
@@ -1724,8 +1841,9 @@ static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
     if (w.linv && k0 + nbp < w.n) {      // the full block inverse for the fused interchanges + U12
         const int sm2 = (int)(sizeof(T) * (2 * kB64 * kB64 + 2 * kB64 * 16));
         cudaFuncSetAttribute(linv128_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
-        linv128_kernel<T><<<kBW / 16, 256, sm2, s>>>((const T*)w.W, w.ldw, k0, nbp, (const T*)w.Dinv0,
-                                             (T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW);
+        linv128_kernel<T><<<kBW / 16 + (w.swplan ? 1 : 0), 256, sm2, s>>>(
+            (const T*)w.W, w.ldw, k0, nbp, (const T*)w.Dinv0, (T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW, w.ipiv,
+            w.swplan ? (SwapPlan*)w.swplan + k0 / kBW : nullptr);
     }
 }
 
@@ -1733,6 +1851,14 @@ template <typename T>
 static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s) {
     if (c1 <= c0) return;
     static const bool v1 = getenv("AS_LU_SWAP_V1") != nullptr;
+    static const bool v2 = getenv("AS_LU_SWAP_V2") != nullptr;
+    if (w.linv && w.swplan && !v1 && !v2) {
+        const int smem = (int)(sizeof(T) * 2 * kSU3C * kSU3LD);
+        swap_u12v3_kernel<T, kSU3C><<<(unsigned)((c1 - c0 + kSU3C - 1) / kSU3C), 256, smem, s>>>(
+            (T*)w.W, w.ldw, k0, bw, c0, c1, (const SwapPlan*)w.swplan + k0 / kBW,
+            (const T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW);
+        return;
+    }
     if (w.linv && !v1) {
         const int smem = (int)(sizeof(T) * 2 * kSU2C * kSU2LD);
         cudaFuncSetAttribute(swap_u12v2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1795,22 +1921,86 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         cudaMemsetAsync(lu_trace().tmax, 0, sizeof(unsigned long long) * 4 * kTraceBlocks, s);
     }
     LuStreams& LS = lu_streams();
-    // Look-ahead: next block's panels on a high-priority stream beside the bulk GEMM (measured
-    // ~10% on C5; the gang-scheduled cooperative panel only partly overlaps).
     const bool lookahead = n >= 2048 && getenv("AS_LU_NO_LOOKAHEAD") == nullptr;
     int evi = 0;
     auto ev = [&]() { return LS.ev[(evi++) % 64]; };
+    static const bool old_sched = getenv("AS_LU_OLD_SCHED") != nullptr;
+    if (lookahead && !old_sched) {
+        // Dataflow schedule.  The trailing columns are split into nch FIXED column chunks (boundaries
+        // multiples of the block width), each with its own stream: chunk q at step k runs
+        // swap + U12 then the GEMM of its columns as soon as (a) block k's panel, inverses and swap
+        // plan exist (ev_linv, from the high-priority stream) and (b) its own step k-1 is done (stream
+        // order).  The high-priority stream carries the critical chain panel(k) -> swap + U12 and GEMM
+        // of block k+1's columns -> panel(k+1); it waits only for the chunk that owns those columns.
+        // No join of all streams per block: the r02 trace showed a 335 us gap between consecutive
+        // bulk GEMMs (42 ms over C5) while the next block's swap + U12 ran alone.
+        // The interchanges into the finished L columns (side stream) wait for every chunk's previous
+        // step: a lagging GEMM(k-1) still reads L21 of block k-1 in the row order of step k-1.
+        const int nch = (int)std::min<int64_t>(4, std::max<int64_t>(1, n / 4096));
+        int64_t Cq[5];
+        for (int q = 0; q <= nch; ++q) Cq[q] = q == nch ? n : (n * q / nch + kBW - 1) / kBW * kBW;
+        cudaStream_t chs[4] = {s, LS.ch[0], LS.ch[1], LS.ch[2]};
+        cudaEvent_t last_ch[4] = {nullptr, nullptr, nullptr, nullptr};
+        cudaEvent_t e_start = ev();
+        cudaEventRecord(e_start, s);
+        cudaStreamWaitEvent(LS.hi, e_start, 0);
+        cudaStreamWaitEvent(LS.side, e_start, 0);
+        for (int q = 1; q < nch; ++q) cudaStreamWaitEvent(chs[q], e_start, 0);
+        block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, LS.hi);
+        // dedicated events, double-buffered by step parity: every wait on an event is issued before
+        // its next record two steps later
+        cudaEvent_t ev_linv = LS.evl[0];
+        cudaEventRecord(ev_linv, LS.hi);
+        int step = 0;
+        for (int64_t k0 = 0; k0 < n; k0 += kBW, ++step) {
+            const int bw = (int)std::min<int64_t>(kBW, n - k0);
+            const int64_t kn = k0 + bw;
+            cudaStreamWaitEvent(LS.side, ev_linv, 0);
+            for (int q = 0; q < nch; ++q)
+                if (last_ch[q]) cudaStreamWaitEvent(LS.side, last_ch[q], 0);
+            laswp_launch<T>(w, k0, bw, 0, k0, 0, 0, true, LS.side);   // L columns + row permutation
+            if (kn >= n) break;
+            const int64_t M = n - kn;
+            const int nbw = (int)std::min<int64_t>(kBW, n - kn);
+            const cudaEvent_t ev_cur = ev_linv;       // block k's panel / inverses / swap plan
+            // critical chain (high priority): block k+1's columns, then its panel
+            int q0 = 0;
+            while (q0 + 1 < nch && kn >= Cq[q0 + 1]) ++q0;
+            if (last_ch[q0]) cudaStreamWaitEvent(LS.hi, last_ch[q0], 0);
+            swap_u12_launch<T>(w, k0, bw, kn, kn + nbw, LS.hi);
+            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
+            block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
+            ev_linv = LS.evl[(step + 1) & 1];
+            cudaEventRecord(ev_linv, LS.hi);
+            // the other columns, chunk by chunk
+            for (int q = 0; q < nch; ++q) {
+                const int64_t a0 = std::max<int64_t>(Cq[q], kn + nbw), a1 = Cq[q + 1];
+                if (a0 >= a1) continue;
+                cudaStreamWaitEvent(chs[q], ev_cur, 0);
+                swap_u12_launch<T>(w, k0, bw, a0, a1, chs[q]);
+                gemm_launch<T>(w, kn, a0, k0, M, a1 - a0, bw, chs[q], 0, false, q == q0 ? (int)(k0 / kBW) * 4 + 0 : -1);
+                last_ch[q] = LS.evc[q][step & 1];
+                cudaEventRecord(last_ch[q], chs[q]);
+            }
+        }
+        cudaStreamWaitEvent(s, ev_linv, 0);
+        for (int q = 1; q < nch; ++q)
+            if (last_ch[q]) cudaStreamWaitEvent(s, last_ch[q], 0);
+        cudaEvent_t ej = ev();
+        cudaEventRecord(ej, LS.side);
+        cudaStreamWaitEvent(s, ej, 0);
+        // streams that joined the capture without work since must still rejoin s
+        for (int q = 1; q < nch; ++q)
+            if (!last_ch[q]) { cudaEvent_t e = ev(); cudaEventRecord(e, chs[q]); cudaStreamWaitEvent(s, e, 0); }
+        launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
+        return;
+    }
     bool side_used = false;
     // first block's panels
     block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, s);
     for (int64_t k0 = 0; k0 < n; k0 += kBW) {
         const int bw = (int)std::min<int64_t>(kBW, n - k0);
-        const int p1 = std::min(kHalf, bw);
         const int64_t kn = k0 + bw;             // next block start
-        // the block's interchanges into all other columns (the panel already swapped its own):
-        // the finished L columns [0, k0) on the side stream (nothing reads them before the
-        // solve; the side stream keeps the blocks' order), the trailing columns [kn, n) and
-        // the row permutation on the critical path
         {
             cudaEvent_t el = ev();
             cudaEventRecord(el, s);
@@ -1819,50 +2009,11 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
             side_used = true;
         }
         if (kn >= n) break;
-        // trailing columns: interchanges + U12 = L11^{-1} A12 in one kernel
-        (void)p1;
         const int64_t M = n - kn;
         const int nbw = (int)std::min<int64_t>(kBW, n - kn);
-        if (lookahead && n - kn > nbw) {
-            // the next block's columns first (high priority: its swap + U12, its GEMM, its panels);
-            // the other columns' swap + U12 and the bulk of the GEMM concurrently on the main stream
-            swap_u12_launch<T>(w, k0, bw, kn, kn + nbw, s);
-            cudaEvent_t e0 = ev();
-            cudaEventRecord(e0, s);
-            cudaStreamWaitEvent(LS.hi, e0, 0);
-            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
-            block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
-            // the other columns: swap + U12, then the bulk GEMM, in column chunks alternating between
-            // two streams, so that chunk i's GEMM overlaps chunk i+1's (memory-bound) swap + U12
-            const int64_t c0r = kn + nbw, rn = n - c0r;
-            static const int nch_env = getenv("AS_LU_SWAP_CHUNKS") ? atoi(getenv("AS_LU_SWAP_CHUNKS")) : 4;
-            const int nch = rn >= 4096 ? nch_env : rn >= 1024 ? std::min(nch_env, 2) : 1;
-            if (nch <= 1) {
-                swap_u12_launch<T>(w, k0, bw, c0r, n, s);
-                gemm_launch<T>(w, kn, c0r, k0, M, rn, bw, s, 0, false, (int)(k0 / kBW) * 4 + 0);
-            } else {
-                cudaEvent_t ea = ev();
-                cudaEventRecord(ea, s);
-                cudaStreamWaitEvent(LS.aux, ea, 0);
-                for (int i = 0; i < nch; ++i) {
-                    auto bnd = [&](int q) { return q >= nch ? n : c0r + (rn * q / nch + 63) / 64 * 64; };
-                    const int64_t a0 = bnd(i), a1 = bnd(i + 1);
-                    cudaStream_t st = (i & 1) ? LS.aux : s;
-                    swap_u12_launch<T>(w, k0, bw, a0, a1, st);
-                    gemm_launch<T>(w, kn, a0, k0, M, a1 - a0, bw, st, 0, false, (int)(k0 / kBW) * 4 + 0);
-                }
-                cudaEvent_t eb = ev();
-                cudaEventRecord(eb, LS.aux);
-                cudaStreamWaitEvent(s, eb, 0);
-            }
-            cudaEvent_t e1 = ev();
-            cudaEventRecord(e1, LS.hi);
-            cudaStreamWaitEvent(s, e1, 0);
-        } else {
-            swap_u12_launch<T>(w, k0, bw, kn, n, s);
-            gemm_launch<T>(w, kn, kn, k0, M, n - kn, bw, s, 0);
-            block_panels<T>(w, kn, nbw, LS.prio_hi, s);
-        }
+        swap_u12_launch<T>(w, k0, bw, kn, n, s);
+        gemm_launch<T>(w, kn, kn, k0, M, n - kn, bw, s, 0);
+        block_panels<T>(w, kn, nbw, LS.prio_hi, s);
     }
     if (side_used) {
         cudaEvent_t ej = ev();
