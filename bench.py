@@ -286,6 +286,17 @@ def roofline(tag, info, stage, ms_per_step, fp64_peak, hbm_peak, hbm_src):
                      "frac": ach / fp64_peak, "frac_of_nominal": ach / NOMINAL_FP64_TFLOPS,
                      "nominal_peak": NOMINAL_FP64_TFLOPS, "algorithmic_flops": info["flops"],
                      "scope": "whole step", "peak_source": peak_src})
+    if tag in ("C5", "C5f"):
+        # the dominant kernel alone (the trailing-update GEMM, K = 128, at the flop-weighted median
+        # trailing size of the factorization), timed live with CUDA events on its launch stream
+        import paper_2007_11208_b200 as AS
+        dt = AS.AS_F64 if tag == "C5" else AS.AS_F32
+        pk = fp64_peak if tag == "C5" else NOMINAL_FP32_TFLOPS
+        tf = AS.bench_gemm(12288, 12288, 128, dt, False, 5)
+        roof["dominant_kernel"] = {"name": "gemm_dmma2_kernel<NN>" if tag == "C5" else "gemm_sgemm_nn_kernel",
+                                   "shape": [12288, 12288, 128], "achieved": tf, "peak": pk, "unit": "TFLOP/s",
+                                   "frac": tf / pk, "flops_per_launch": 2.0 * 12288 * 12288 * 128,
+                                   "share_of_step": "profiles/r02: launch list of the same configuration"}
     roof.setdefault("traffic", None)
     tr = load_traffic().get(tag)
     if tr:

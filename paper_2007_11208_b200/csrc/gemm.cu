@@ -297,9 +297,13 @@ __global__ void __launch_bounds__(s2::NT, 2) gemm_sgemm_nn_kernel(GemmArgs g) {
 constexpr int kGemmCfgDefault = 0;
 // tile configuration of the DMMA GEMM: k-tile BK_ and pipeline depth ST_ (the launcher's choice,
 // measured in tools/gemm_bench.py); BM x BN = 128 x 64, 4 warps of 64 x 32
-template <int BK_, int ST_>
+template <int BK_, int ST_, int NT_ = 128>
 struct D2 {
-    static constexpr int BM = 128, BN = 64, BK = BK_, ST = ST_, NT = 128;
+    static constexpr int BM = 128, BN = 64, BK = BK_, ST = ST_, NT = NT_;
+    // warp tile: MI x 4 DMMA tiles (64 x 32 with 4 warps, 32 x 32 with 8 warps: four warps per
+    // scheduler instead of two to cover each other's barrier waits and C prologues)
+    static constexpr int MI = NT_ == 128 ? 8 : 4;
+    static constexpr int WARPS_M = BM / (8 * MI);
     static constexpr int LDA_KM = BM + 4;   // A as [k][m]
     static constexpr int LDA_MK = BK + 4;   // A as [m][k]
     static constexpr int LDB_NK = BK + 4;   // B as [n][k]
@@ -383,7 +387,7 @@ AS_DEV void stage_d2_fast(double* As, double* Bs, const double* pa, int64_t lda,
 
 template <bool TA, bool TB, class d2>
 __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
-    constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK, ST = d2::ST;
+    constexpr int BM = d2::BM, BN = d2::BN, BK = d2::BK, ST = d2::ST, MI = d2::MI;
     constexpr int LDA_KM = d2::LDA_KM, LDA_MK = d2::LDA_MK, LDB_NK = d2::LDB_NK, LDB_KN = d2::LDB_KN;
     constexpr int AEL = d2::AEL, BEL = d2::BEL;
     if (g.skip && *g.skip) return;
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     const double* B = (const double*)g.B;
     double* C = (double*)g.C;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+    const int wm = (warp % d2::WARPS_M) * 8 * MI, wn = (warp / d2::WARPS_M) * 32;
     const int gid = lane >> 2, tig = lane & 3;
     const int nk = (int)((g.K + BK - 1) / BK);
     const bool full = (m0 + BM <= g.M) && (n0 + BN <= g.N);
@@ -425,9 +429,9 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     // The MMA runs on the transposed tile (first operand = B^T fragment, second = A^T fragment), so
     // a thread's two accumulator values are C(r, c), C(r + 1, c) with r = .. + 2 tig, c = .. + gid:
     // adjacent in the column-major C -> one 16-byte load / store per DMMA tile.
-    double acc[8][4][2];
+    double acc[MI][4][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < MI; ++i) {
         const int64_t r = m0 + wm + 8 * i + 2 * tig;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -451,9 +455,9 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
         const double* bs = Bs + (kt % ST) * BEL;
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
-            double af[8], bf[4];
+            double af[MI], bf[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < MI; ++i) {
                 const int m = wm + 8 * i + gid, k = ks * 4 + tig;
                 af[i] = TA ? as[m * LDA_MK + k] : as[k * LDA_KM + m];
             }
@@ -463,14 +467,14 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
                 bf[j] = -(TB ? bs[k * LDB_KN + n] : bs[n * LDB_NK + k]);
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], bf[j], af[i]);
         }
     }
     cp_async_wait<0>();
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < MI; ++i) {
         const int64_t r = m0 + wm + 8 * i + 2 * tig;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -701,6 +705,9 @@ void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
         case 1: run(D2<16, 3>{}); break;
         case 2: run(D2<32, 2>{}); break;
         case 3: run(D2<32, 3>{}); break;
+        case 5: run(D2<16, 2, 256>{}); break;
+        case 6: run(D2<16, 3, 256>{}); break;
+        case 7: run(D2<32, 2, 256>{}); break;
         default: run(D2<16, 2>{}); break;
         }
     } else {

@@ -89,23 +89,12 @@ template <> AS_DEV void cand_key<float>(float x, unsigned& hi, unsigned& lo) {
 // candidate can be published before the bulk of the rank-1 update -- the other CTAs' exchange
 // latency then overlaps this CTA's update.
 template <typename T>
-AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, int64_t g, int col, T& v, long long& idx,
-                               T* sv, long long* si, int* sdn) {
-    // first max |a(r, col)| over local rows at positions >= g; NaN never wins, a NaN at row g keeps
-    // g (the serial sweep's semantics).  Warp level: fmax shuffles + ballot + integer min of the
-    // row; CTA level: every warp merges the 8 warp results the same way (one barrier).
+AS_DEV void panel_argmax_reduce(T bv, unsigned br, int dnan, int64_t rbeg, int64_t g, T& v, long long& idx, T* sv,
+                                long long* si, int* sdn) {
+    // per-thread candidate (bv = |a|, br = local row or 0xffffffff, dnan = "the row at g holds a NaN")
+    // -> CTA candidate.  Warp level: integer reductions on the order-preserving key + the smallest
+    // row among the maxima; CTA level: every warp merges the 8 warp results the same way (one barrier).
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    T bv = T(-1);
-    unsigned br = 0xffffffffu;
-    int dnan = 0;
-    for (int r = threadIdx.x; r < nr; r += blockDim.x) {
-        const int64_t gr = rbeg + r;
-        if (gr < g) continue;
-        T a = Ps[r + col * cp];
-        a = a < T(0) ? -a : a;
-        if (gr == g && a != a) dnan = 1;
-        if (a > bv) { bv = a; br = (unsigned)r; }     // rows increase: strict > keeps the first
-    }
     unsigned kh = 0u, kl = 0u;
     if (br != 0xffffffffu) cand_key<T>(bv == T(0) ? T(0) : bv, kh, kl);   // (-0 -> +0)
     unsigned mh = __reduce_max_sync(0xffffffffu, kh);
@@ -129,6 +118,25 @@ AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, in
     v = (rmin == 0xffffffffu) ? T(-1) : m8;
     idx = (rmin == 0xffffffffu) ? 0x7fffffffffffffffll : (long long)(rbeg + rmin);
     if (dn) { v = T(INFINITY); idx = g; }
+}
+
+template <typename T>
+AS_DEV void panel_local_argmax(const T* Ps, int64_t cp, int nr, int64_t rbeg, int64_t g, int col, T& v, long long& idx,
+                               T* sv, long long* si, int* sdn) {
+    // first max |a(r, col)| over local rows at positions >= g; NaN never wins, a NaN at row g keeps
+    // g (the serial sweep's semantics).
+    T bv = T(-1);
+    unsigned br = 0xffffffffu;
+    int dnan = 0;
+    for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+        const int64_t gr = rbeg + r;
+        if (gr < g) continue;
+        T a = Ps[r + col * cp];
+        a = a < T(0) ? -a : a;
+        if (gr == g && a != a) dnan = 1;
+        if (a > bv) { bv = a; br = (unsigned)r; }     // rows increase: strict > keeps the first
+    }
+    panel_argmax_reduce<T>(bv, br, dnan, rbeg, g, v, idx, sv, si, sdn);
 }
 
 // Bulk rank-1 update of the panel rows r0 .. nr-1 (local), columns j+2 .. nbp-1:
@@ -229,6 +237,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         publish(0, v, idx);
     }
     unsigned long long info = ~0ull;
+    // Column step, four CTA barriers (r02: was nine): [poll] B1 [pivot row -> ubuf, the interchange's
+    // two row writes] B2 [multipliers, column j+1 and each thread's candidate for it] B3 (inside the
+    // reduction) [rows rc / g+1 finished and copied out] B4 [publish] [bulk update].  The next step's
+    // B1 orders the bulk update before anything that overwrites what it reads.
     for (int j = 0; j < nbp; ++j) {
         const int64_t g = k0 + j;
         const int par = j & 1;
@@ -274,61 +286,91 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
             }
             if (lane == 0) { s_p = bi; s_owner = bo; }
         }
-        __syncthreads();
+        __syncthreads();                                                      // B1
         const long long p = s_p;
         const int owner = s_owner;
         const bool own_p = p != g && p >= rbeg && p < rend;
-        // the pivot row into ubuf; the owner of p takes the old row g (both loads in flight together)
+        const int g_loc = (g >= rbeg && g < rend) ? (int)(g - rbeg) : -1;
+        // the pivot row into ubuf; the pivot itself first (same line, one broadcast load): an exact
+        // zero pivot means no interchange and no elimination (singular column)
+        const T* prow = rowbuf + ((int64_t)par * P + owner) * nbp;
+        const T piv = __ldcg(&prow[j]);
+        const bool elim = piv != T(0);
         T* dst_p = own_p ? Ps + (p - rbeg) : nullptr;
         for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
-            const T u = __ldcg(&rowbuf[((int64_t)par * P + owner) * nbp + c]);
-            const T dg = own_p ? __ldcg(&diagbuf[par * nbp + c]) : T(0);
+            const T u = __ldcg(&prow[c]);
+            const T dg = (own_p && elim) ? __ldcg(&diagbuf[par * nbp + c]) : T(0);
             ubuf[c] = u;
-            if (own_p) dst_p[c * cp] = dg;
-        }
-        __syncthreads();
-        const T piv = ubuf[j];
-        if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
-        const bool elim = piv != T(0);
-        if (!elim) {                             // exact zero pivot: singular column (no swap, no elimination)
-            if (info == ~0ull) info = (unsigned long long)(g + 1);
-            if (own_p)                           // undo: row p keeps its own values
-                for (int c = threadIdx.x; c < nbp; c += blockDim.x) dst_p[c * cp] = ubuf[c];
-        } else if (g >= rbeg && g < rend) {
-            const int r = (int)(g - rbeg);
-            for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = ubuf[c];
-        }
-        __syncthreads();
-        const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
-        // ---- multipliers and column j+1 of my rows > g
-        if (elim) {
-            const T u1 = (j + 1 < nbp) ? ubuf[j + 1] : T(0);
-            for (int r = (int)r0 + threadIdx.x; r < nr; r += blockDim.x) {
-                const T l = Ps[r + j * cp] / piv;
-                Ps[r + j * cp] = l;
-                if (j + 1 < nbp) Ps[r + (j + 1) * cp] -= l * u1;
+            if (elim) {
+                if (own_p) dst_p[c * cp] = dg;               // the owner of p takes the old row g
+                if (g_loc >= 0) Ps[g_loc + c * cp] = u;      // the pivot row at position g
             }
         }
-        __syncthreads();
+        if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
+        if (!elim && info == ~0ull) info = (unsigned long long)(g + 1);
+        __syncthreads();                                                      // B2
+        const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
+        // ---- multipliers, column j+1 of my rows > g, and each thread's candidate for column j+1
+        T cbv = T(-1);
+        unsigned cbr = 0xffffffffu;
+        int cdn = 0;
+        {
+            const bool more = j + 1 < nbp;
+            const T u1 = more ? ubuf[j + 1] : T(0);
+            for (int r = (int)r0 + threadIdx.x; r < nr; r += blockDim.x) {
+                T a1 = more ? Ps[r + (j + 1) * cp] : T(0);
+                if (elim) {
+                    const T l = Ps[r + j * cp] / piv;
+                    Ps[r + j * cp] = l;
+                    if (more) { a1 -= l * u1; Ps[r + (j + 1) * cp] = a1; }
+                }
+                if (more) {
+                    const T aa = a1 < T(0) ? -a1 : a1;
+                    if (rbeg + r == g + 1 && aa != aa) cdn = 1;
+                    if (aa > cbv) { cbv = aa; cbr = (unsigned)r; }   // rows increase: strict > keeps the first
+                }
+            }
+        }
         if (j + 1 >= nbp) break;
-        // ---- column j+1's candidate: finish its row (and row g+1) first, publish, then the bulk
         T v;
         long long idx;
-        panel_local_argmax(Ps, cp, nr, rbeg, g + 1, j + 1, v, idx, sv, si, sdn);
+        panel_argmax_reduce<T>(cbv, cbr, cdn, rbeg, g + 1, v, idx, sv, si, sdn);   // B3 inside
         const int rc = (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) ? (int)(idx - rbeg) : -1;
         const int rg = (g + 1 >= rbeg && g + 1 < rend) ? (int)(g + 1 - rbeg) : -1;
-        if (elim) {
-            for (int c = j + 2 + threadIdx.x; c < nbp; c += blockDim.x) {
-                if (rc >= 0) Ps[rc + c * cp] -= Ps[rc + j * cp] * ubuf[c];
-                if (rg >= 0 && rg != rc) Ps[rg + c * cp] -= Ps[rg + j * cp] * ubuf[c];
+        // ---- the candidate row and row g+1: finish their update (columns j+2..) while copying them out
+        {
+            const int par1 = (j + 1) & 1;
+            const T lc = (rc >= 0 && elim) ? Ps[rc + j * cp] : T(0);
+            const T lg = (rg >= 0 && elim) ? Ps[rg + j * cp] : T(0);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
+                const T uc = ubuf[c];
+                if (rc >= 0) {
+                    T a = Ps[rc + c * cp];
+                    if (elim && c >= j + 2) { a -= lc * uc; Ps[rc + c * cp] = a; }
+                    rowbuf[((int64_t)par1 * P + cta) * nbp + c] = a;
+                    if (rg == rc) diagbuf[par1 * nbp + c] = a;
+                }
+                if (rg >= 0 && rg != rc) {
+                    T a = Ps[rg + c * cp];
+                    if (elim && c >= j + 2) { a -= lg * uc; Ps[rg + c * cp] = a; }
+                    diagbuf[par1 * nbp + c] = a;
+                }
             }
         }
-        __syncthreads();
-        publish(j + 1, v, idx);
+        __syncthreads();                                                      // B4
+        if (threadIdx.x == 0) {
+            // slots are double-buffered by column parity like rowbuf: a CTA one column ahead must
+            // not overwrite a candidate another CTA has not read yet
+            PSlot* sl = slots + ((j + 1) & 1) * 512 + cta;
+            sl->v = (double)v;
+            sl->idx = idx;
+            // release is cumulative: the CTA's rowbuf writes (ordered by the barrier above) are published too
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq), "l"(seq_base + (unsigned long long)j + 2ull) : "memory");
+        }
         // ---- bulk rank-1 update of the remaining rows, columns j+2.. (thread = row, column phase)
         if (elim) panel_bulk_update<T>(Ps, cp, ubuf, (int)r0, nr, j, nbp, rc, rg);
-        __syncthreads();
     }
+    __syncthreads();
     if (use_smem) {
         for (int e = threadIdx.x; e < nr * nbp; e += blockDim.x) {
             const int c = e / nr, r = e - c * nr;
@@ -401,6 +443,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
         publish(0, v, idx);
     }
     unsigned long long info = ~0ull;
+    // Column step: one cluster barrier and two CTA barriers (r02: was one + seven): [cluster barrier:
+    // every candidate visible, the previous bulk update finished] [every warp merges the P candidates;
+    // pivot row -> ubuf, the interchange's two row writes] B2 [multipliers, column j+1, candidates]
+    // B3 (inside the reduction) [rows rc / g+1 finished and copied to the exchange buffers] [bulk update]
     for (int j = 0; j < nbp; ++j) {
         const int64_t g = k0 + j;
         const int par = j & 1;
@@ -408,7 +454,9 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
         if (P > 1) cl.sync();                            // every candidate of column j is visible
         else __syncthreads();
         PHC(1);
-        if (warp == 0) {
+        long long p;
+        int owner;
+        {
             T bv = T(-1);
             long long bi = 0x7fffffffffffffffll;
             int bo = 0;
@@ -424,66 +472,84 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
                 const int o2 = __shfl_xor_sync(0xffffffffu, bo, o);
                 if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; bo = o2; }
             }
-            if (lane == 0) { s_p = bi; s_owner = bo; }
+            p = bi; owner = bo;                          // identical in every lane of every warp
         }
-        __syncthreads();
-        const long long p = s_p;
-        const int owner = s_owner;
         const int gown = (int)((g - k0) / chunk);
         const bool own_p = p != g && p >= rbeg && p < rend;
+        const int g_loc = (g >= rbeg && g < rend) ? (int)(g - rbeg) : -1;
         const T* rc = cl.map_shared_rank(candb + par * nbp, owner);
         const T* rd = cl.map_shared_rank(diagb + par * nbp, gown);
+        const T piv = rc[j];
+        const bool elim = piv != T(0);                   // exact zero pivot: no interchange, no elimination
         T* dst_p = own_p ? Ps + (p - rbeg) : nullptr;
         for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
             const T u = rc[c];
-            const T dg = own_p ? rd[c] : T(0);
+            const T dg = (own_p && elim) ? rd[c] : T(0);
             ubuf[c] = u;
-            if (own_p) dst_p[c * cp] = dg;
-        }
-        __syncthreads();
-        PHC(2);
-        const T piv = ubuf[j];
-        if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
-        const bool elim = piv != T(0);
-        if (!elim) {
-            if (info == ~0ull) info = (unsigned long long)(g + 1);
-            if (own_p)
-                for (int c = threadIdx.x; c < nbp; c += blockDim.x) dst_p[c * cp] = ubuf[c];
-        } else if (g >= rbeg && g < rend) {
-            const int r = (int)(g - rbeg);
-            for (int c = threadIdx.x; c < nbp; c += blockDim.x) Ps[r + c * cp] = ubuf[c];
-        }
-        __syncthreads();
-        const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
-        if (elim) {
-            const T u1 = (j + 1 < nbp) ? ubuf[j + 1] : T(0);
-            for (int r = (int)r0 + threadIdx.x; r < nr; r += blockDim.x) {
-                const T l = Ps[r + j * cp] / piv;
-                Ps[r + j * cp] = l;
-                if (j + 1 < nbp) Ps[r + (j + 1) * cp] -= l * u1;
+            if (elim) {
+                if (own_p) dst_p[c * cp] = dg;
+                if (g_loc >= 0) Ps[g_loc + c * cp] = u;
             }
         }
-        __syncthreads();
+        if (cta == 0 && threadIdx.x == 0) ipiv[g] = (p == 0x7fffffffffffffffll) ? g : p;
+        if (!elim && info == ~0ull) info = (unsigned long long)(g + 1);
+        __syncthreads();                                                      // B2
+        PHC(2);
+        const int64_t r0 = max<int64_t>(0, g + 1 - rbeg);
+        T cbv = T(-1);
+        unsigned cbr = 0xffffffffu;
+        int cdn = 0;
+        {
+            const bool more = j + 1 < nbp;
+            const T u1 = more ? ubuf[j + 1] : T(0);
+            for (int r = (int)r0 + threadIdx.x; r < nr; r += blockDim.x) {
+                T a1 = more ? Ps[r + (j + 1) * cp] : T(0);
+                if (elim) {
+                    const T l = Ps[r + j * cp] / piv;
+                    Ps[r + j * cp] = l;
+                    if (more) { a1 -= l * u1; Ps[r + (j + 1) * cp] = a1; }
+                }
+                if (more) {
+                    const T aa = a1 < T(0) ? -a1 : a1;
+                    if (rbeg + r == g + 1 && aa != aa) cdn = 1;
+                    if (aa > cbv) { cbv = aa; cbr = (unsigned)r; }
+                }
+            }
+        }
         PHC(3);
         if (j + 1 >= nbp) break;
         T v;
         long long idx;
-        panel_local_argmax(Ps, cp, nr, rbeg, g + 1, j + 1, v, idx, sv, si, sdn);
+        panel_argmax_reduce<T>(cbv, cbr, cdn, rbeg, g + 1, v, idx, sv, si, sdn);   // B3 inside
         PHC(4);
         const int rcn = (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) ? (int)(idx - rbeg) : -1;
         const int rg = (g + 1 >= rbeg && g + 1 < rend) ? (int)(g + 1 - rbeg) : -1;
-        if (elim) {
-            for (int c = j + 2 + threadIdx.x; c < nbp; c += blockDim.x) {
-                if (rcn >= 0) Ps[rcn + c * cp] -= Ps[rcn + j * cp] * ubuf[c];
-                if (rg >= 0 && rg != rcn) Ps[rg + c * cp] -= Ps[rg + j * cp] * ubuf[c];
+        {
+            const int par1 = (j + 1) & 1;
+            const T lc = (rcn >= 0 && elim) ? Ps[rcn + j * cp] : T(0);
+            const T lg = (rg >= 0 && elim) ? Ps[rg + j * cp] : T(0);
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
+                const T uc = ubuf[c];
+                if (rcn >= 0) {
+                    T a = Ps[rcn + c * cp];
+                    if (elim && c >= j + 2) { a -= lc * uc; Ps[rcn + c * cp] = a; }
+                    candb[par1 * nbp + c] = a;
+                    if (rg == rcn) diagb[par1 * nbp + c] = a;
+                }
+                if (rg >= 0 && rg != rcn) {
+                    T a = Ps[rg + c * cp];
+                    if (elim && c >= j + 2) { a -= lg * uc; Ps[rg + c * cp] = a; }
+                    diagb[par1 * nbp + c] = a;
+                }
             }
+            if (threadIdx.x == 0) { s_cv[par1] = v; s_ci[par1] = idx; }
         }
-        __syncthreads();
-        publish(j + 1, v, idx);
         PHC(5);
+        // (the multipliers of rows rcn / rg were read above by every thread before any of its bulk
+        // writes; the bulk update skips those two rows and reads only ubuf and column j)
         if (elim) panel_bulk_update<T>(Ps, cp, ubuf, (int)r0, nr, j, nbp, rcn, rg);
-        __syncthreads();
     }
+    __syncthreads();
     PHC(6);
 #undef PHC
     if (prof)
@@ -1851,8 +1917,10 @@ template <typename T>
 static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s) {
     if (c1 <= c0) return;
     static const bool v1 = getenv("AS_LU_SWAP_V1") != nullptr;
-    static const bool v2 = getenv("AS_LU_SWAP_V2") != nullptr;
-    if (w.linv && w.swplan && !v1 && !v2) {
+    // the 16-column kernel (r02o, C5, same run: 163.3 ms against 170.3 with the 64-column kernel
+    // everywhere and 167.2 with it on the bulk only; AS_LU_SWAP_V3_MAXC=c keeps it to launches of <= c columns)
+    static const int64_t v3_maxc = getenv("AS_LU_SWAP_V3_MAXC") ? atoll(getenv("AS_LU_SWAP_V3_MAXC")) : (int64_t)1 << 40;
+    if (w.linv && w.swplan && !v1 && c1 - c0 <= v3_maxc) {
         const int smem = (int)(sizeof(T) * 2 * kSU3C * kSU3LD);
         swap_u12v3_kernel<T, kSU3C><<<(unsigned)((c1 - c0 + kSU3C - 1) / kSU3C), 256, smem, s>>>(
             (T*)w.W, w.ldw, k0, bw, c0, c1, (const SwapPlan*)w.swplan + k0 / kBW,
@@ -1924,8 +1992,10 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
     const bool lookahead = n >= 2048 && getenv("AS_LU_NO_LOOKAHEAD") == nullptr;
     int evi = 0;
     auto ev = [&]() { return LS.ev[(evi++) % 64]; };
-    static const bool old_sched = getenv("AS_LU_OLD_SCHED") != nullptr;
-    if (lookahead && !old_sched) {
+    // AS_LU_SCHED=1: the dataflow schedule below (measured slower on C5 in r02n: 188 vs 170 ms with the
+    // same kernels); default: the block-synchronous look-ahead schedule further down
+    static const int sched = getenv("AS_LU_SCHED") ? atoi(getenv("AS_LU_SCHED")) : 0;
+    if (lookahead && sched == 1) {
         // Dataflow schedule.  The trailing columns are split into nch FIXED column chunks (boundaries
         // multiples of the block width), each with its own stream: chunk q at step k runs
         // swap + U12 then the GEMM of its columns as soon as (a) block k's panel, inverses and swap
@@ -1995,12 +2065,19 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
         return;
     }
+    // Look-ahead: next block's panels on a high-priority stream beside the bulk GEMM (measured
+    // ~10% on C5; the gang-scheduled cooperative panel only partly overlaps).
     bool side_used = false;
     // first block's panels
     block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, s);
     for (int64_t k0 = 0; k0 < n; k0 += kBW) {
         const int bw = (int)std::min<int64_t>(kBW, n - k0);
+        const int p1 = std::min(kHalf, bw);
         const int64_t kn = k0 + bw;             // next block start
+        // the block's interchanges into all other columns (the panel already swapped its own):
+        // the finished L columns [0, k0) on the side stream (nothing reads them before the
+        // solve; the side stream keeps the blocks' order), the trailing columns [kn, n) and
+        // the row permutation on the critical path
         {
             cudaEvent_t el = ev();
             cudaEventRecord(el, s);
@@ -2009,11 +2086,51 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
             side_used = true;
         }
         if (kn >= n) break;
+        // trailing columns: interchanges + U12 = L11^{-1} A12 in one kernel
+        (void)p1;
         const int64_t M = n - kn;
         const int nbw = (int)std::min<int64_t>(kBW, n - kn);
-        swap_u12_launch<T>(w, k0, bw, kn, n, s);
-        gemm_launch<T>(w, kn, kn, k0, M, n - kn, bw, s, 0);
-        block_panels<T>(w, kn, nbw, LS.prio_hi, s);
+        if (lookahead && n - kn > nbw) {
+            // the next block's columns first (high priority: its swap + U12, its GEMM, its panels);
+            // the other columns' swap + U12 and the bulk of the GEMM concurrently on the main stream
+            // (its swap + U12 on the high-priority stream too: the bulk's first chunk does not wait for it)
+            cudaEvent_t e0 = ev();
+            cudaEventRecord(e0, s);
+            cudaStreamWaitEvent(LS.hi, e0, 0);
+            swap_u12_launch<T>(w, k0, bw, kn, kn + nbw, LS.hi);
+            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
+            block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
+            // the other columns: swap + U12, then the bulk GEMM, in column chunks alternating between
+            // two streams, so that chunk i's GEMM overlaps chunk i+1's (memory-bound) swap + U12
+            const int64_t c0r = kn + nbw, rn = n - c0r;
+            static const int nch_env = getenv("AS_LU_SWAP_CHUNKS") ? atoi(getenv("AS_LU_SWAP_CHUNKS")) : 4;
+            const int nch = rn >= 4096 ? nch_env : rn >= 1024 ? std::min(nch_env, 2) : 1;
+            if (nch <= 1) {
+                swap_u12_launch<T>(w, k0, bw, c0r, n, s);
+                gemm_launch<T>(w, kn, c0r, k0, M, rn, bw, s, 0, false, (int)(k0 / kBW) * 4 + 0);
+            } else {
+                cudaEvent_t ea = ev();
+                cudaEventRecord(ea, s);
+                cudaStreamWaitEvent(LS.aux, ea, 0);
+                for (int i = 0; i < nch; ++i) {
+                    auto bnd = [&](int q) { return q >= nch ? n : c0r + (rn * q / nch + 63) / 64 * 64; };
+                    const int64_t a0 = bnd(i), a1 = bnd(i + 1);
+                    cudaStream_t st = (i & 1) ? LS.aux : s;
+                    swap_u12_launch<T>(w, k0, bw, a0, a1, st);
+                    gemm_launch<T>(w, kn, a0, k0, M, a1 - a0, bw, st, 0, false, (int)(k0 / kBW) * 4 + 0);
+                }
+                cudaEvent_t eb = ev();
+                cudaEventRecord(eb, LS.aux);
+                cudaStreamWaitEvent(s, eb, 0);
+            }
+            cudaEvent_t e1 = ev();
+            cudaEventRecord(e1, LS.hi);
+            cudaStreamWaitEvent(s, e1, 0);
+        } else {
+            swap_u12_launch<T>(w, k0, bw, kn, n, s);
+            gemm_launch<T>(w, kn, kn, k0, M, n - kn, bw, s, 0);
+            block_panels<T>(w, kn, nbw, LS.prio_hi, s);
+        }
     }
     if (side_used) {
         cudaEvent_t ej = ev();

@@ -313,3 +313,29 @@ def test_repeat_bitwise_deterministic(case):
             assert cur == ref, case
     if A.shape[0] <= 3000:
         check_parity(A, B)
+
+
+# ------------------------------------------------------------------ one-CTA estimator (n <= 512)
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 200, 384, 512])
+@pytest.mark.parametrize("kind", ["lu", "spd", "lower", "upper"])
+def test_small_estimator_rcond_tight(kind, n):
+    """n <= 512: xLACN2 runs in one CTA (rcond.cu est_small_kernel) through the same factors and the
+    same steps as the oracle's estimator (Z13b).  Same iteration, same vectors: the estimate
+    agrees to rounding (1e-8 relative), not only within the soft factor-of-two bar."""
+    rng = np.random.default_rng(1000 * n + len(kind))
+    if kind == "lu":
+        A = rng.standard_normal((n, n)) + 4.0 * np.eye(n)
+    elif kind == "spd":
+        A = W.random_spd_fig3(n, seed=n) if n > 1 else np.array([[2.5]])
+    else:
+        T = np.tril(rng.standard_normal((n, n)) / 8.0, -1) + np.diag(1.0 + rng.random(n))
+        A = T if kind == "lower" else T.T
+    A = np.asfortranarray(A)
+    B = np.asfortranarray(rng.standard_normal((n, 3)))
+    ret, X, rep = gpu_solve(A, B)
+    oret, Xo, orep, _ = oracle.solve(A, B)
+    assert ret == oret == 0
+    assert rep["primary_method"] == orep["primary_method"]
+    assert (rep["flags"] & MASK) == (orep["flags"] & MASK)
+    assert orep["rcond"] > 0
+    assert abs(rep["rcond"] / orep["rcond"] - 1.0) <= 1e-8, (rep["rcond"], orep["rcond"])

@@ -1,0 +1,16 @@
+# r02p: LU panels with merged barriers (coop 9 -> 4, cluster 8 -> 3 per column), swapLA on the hi stream
+set -x
+O=gpurun_out/r02p
+mkdir -p $O
+timeout 1500 python -m pytest tests/test_gpu_r02.py tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -x -k "(lu or LU or debug_factor or determin or c4 or C4 or fallback or singular) and not narrow" > $O/pytest_lu.txt 2>&1; echo "rc=$?"
+b() { cfg=$1; name=$2; shift 2; env "$@" timeout 600 python bench.py --config $cfg --only --steps 5 --no-cpu-baseline > $O/bench_${cfg}_$name.json 2> $O/bench_${cfg}_$name.err; }
+b C5 default AS_X=0
+b C5 sched1 AS_LU_SCHED=1
+b C5 lf8192 AS_LU_LF_MIN_M=8192
+b C5 lf6144 AS_LU_LF_MIN_M=6144
+b C5f default AS_X=0
+b C4 default AS_X=0
+AS_USE_DEBUG_LIB=1 timeout 600 python tools/lu_trace.py C5 > $O/lu_trace_C5.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C5.csv python tools/profile_one.py --config C5 --eager --calls 1 > /dev/null 2>&1
+python tools/launches.py $O/launches_C5.csv > $O/launches_C5.txt 2>&1; gzip -f $O/launches_C5.csv
+python tools/std_vs_adaptive.py --out $O/std_vs_adaptive.json > $O/std_vs_adaptive.txt 2>&1
