@@ -353,7 +353,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     w.ll = (unsigned long long*)take(8 * w.ll_len);
     w.bars_len = 8 + nblk + 8;
     w.bars = (unsigned*)take(4 * w.bars_len);
-    w.cand = take(16 * 2 * 1024 + es * 2 * 1024 * 128 + es * 2 * 128);   // LU panel slots, rowbuf, diagbuf (128-wide)
+    w.cand = take(lu_cand_bytes());      // LU panel exchange words (headers, candidate rows, diagonal row)
     w.lfbuf = take(lu_lfbuf_bytes(n, w.dtype));
     w.linv = take(es * (size_t)((n + 127) / 128) * 128 * 128);
     w.swplan = take(lu_swplan_bytes(n));

@@ -11,6 +11,7 @@ double chol_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t 
                              int iters, int dbg);
 unsigned long long* debug_trace_buf(int which);   // lu.cu diagnostics (AS_LU_TRACE)
 int lu_trace_copy(unsigned long long* out_min, unsigned long long* out_max, int cap);  // lu.cu diagnostics
+size_t lu_cand_bytes();                        // Work::cand size (lu.cu)
 size_t lu_swplan_bytes(int64_t n);             // Work::swplan size (lu.cu)
 size_t lu_lfbuf_bytes(int64_t n, int dtype);   // Work::lfbuf size (lu.cu)
 void launch_lu_factor(const Work& w, cudaStream_t s);                 // lu.cu: W = L\U, ipiv, perm, Dinv0/1, anorm

@@ -34,7 +34,10 @@
 
 namespace as {
 
-constexpr int kPT = 256;     // panel threads
+constexpr int kPT = 256;     // panel threads (leaf panel)
+// cooperative / cluster panels: 512 threads halve the (latency-bound) bulk rank-1 update but every
+// barrier-separated phase grows with the thread count: measured 337 vs 304 us (m = 128), 475 vs 442 us (m = 4096)
+constexpr int kPT2 = 256;
 constexpr int kPW = 128;     // panel width (= block width: one cooperative panel per block, so the
                              // look-ahead chain is panel + L11 inverse only)
 constexpr int kBW = 128;     // block width
@@ -60,12 +63,6 @@ static LuTrace& lu_trace() {
     return t;
 }
 
-struct __align__(32) PSlot {
-    double v;
-    long long idx;
-    unsigned long long seq;
-    long long pad;
-};
 
 // Order-preserving integer key of a candidate |a| >= +0 (0 is reserved for "no candidate"): the
 // first-max argmax becomes three integer warp reductions (max high word, max low word among the
@@ -104,10 +101,10 @@ AS_DEV void panel_argmax_reduce(T bv, unsigned br, int dnan, int64_t rbeg, int64
     dnan = __any_sync(0xffffffffu, dnan);
     if (lane == 0) { sv[warp] = (wr == 0xffffffffu) ? T(-1) : wm; si[warp] = (long long)wr; sdn[warp] = dnan; }
     __syncthreads();
-    const int nw = (int)(blockDim.x >> 5);
-    const T v8 = (lane & 7) < nw ? sv[lane & 7] : T(-1);
-    const unsigned r8 = (lane & 7) < nw ? (unsigned)si[lane & 7] : 0xffffffffu;
-    const int d8 = (lane & 7) < nw ? sdn[lane & 7] : 0;
+    const int nw = (int)(blockDim.x >> 5);               // <= 32 warps: one lane per warp result
+    const T v8 = lane < nw ? sv[lane] : T(-1);
+    const unsigned r8 = lane < nw ? (unsigned)si[lane] : 0xffffffffu;
+    const int d8 = lane < nw ? sdn[lane] : 0;
     kh = 0u; kl = 0u;
     if (r8 != 0xffffffffu) cand_key<T>(v8, kh, kl);
     mh = __reduce_max_sync(0xffffffffu, kh);
@@ -177,11 +174,50 @@ AS_DEV void panel_bulk_update(T* __restrict__ Ps, int64_t cp, const T* __restric
     }
 }
 
+// Exchange words of the cooperative panel: every 8-byte word is (seq32 << 32) | 32 payload bits, so
+// a word is its own "ready" flag -- the producer needs no barrier + release fence before a flag and
+// the consumer no acquire fence after it (r02: ~1 us of the 4.4 us column step).  The arena is zeroed
+// per factorization (sequence numbers repeat across solves).
+//   hdr   [2 parities][512 CTAs][4]: |candidate| high / low word, candidate row index (0xffffffff: none)
+//   rowll [2][512][kPW][WPE]:        the CTA's candidate row
+//   diagll[2][kPW][WPE]:             the row at position g (for the owner of the pivot row)
+template <typename T> struct PlW { static constexpr int v = sizeof(T) / 4; };
+constexpr int kPlMaxP = 512;
+constexpr size_t kPlHdrWords = 2 * kPlMaxP * 4;
+constexpr size_t kPlRowWords = (size_t)2 * kPlMaxP * 128 * 2;      // sized for fp64 (2 words per element)
+constexpr size_t kPlDiagWords = 2 * 128 * 2;
+size_t lu_cand_bytes() { return 8 * (kPlHdrWords + kPlRowWords + kPlDiagWords); }
+AS_DEV void pl_put(unsigned long long* w, double x, unsigned sq) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x), hi = (unsigned long long)sq << 32;
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(w), "l"(hi | (b >> 32)), "l"(hi | (b & 0xffffffffull)) : "memory");
+}
+AS_DEV void pl_put(unsigned long long* w, float x, unsigned sq) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(w), "l"(((unsigned long long)sq << 32) | __float_as_uint(x)) : "memory");
+}
+AS_DEV double pl_get(const unsigned long long* w, unsigned sq, double) {
+    unsigned long long a, b;
+    do {
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(w) : "memory");
+    } while ((unsigned)(a >> 32) != sq || (unsigned)(b >> 32) != sq);
+    return __longlong_as_double((long long)(((a & 0xffffffffull) << 32) | (b & 0xffffffffull)));
+}
+AS_DEV float pl_get(const unsigned long long* w, unsigned sq, float) {
+    unsigned long long a;
+    do {
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(a) : "l"(w) : "memory");
+    } while ((unsigned)(a >> 32) != sq);
+    return __uint_as_float((unsigned)a);
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
-                                                            int64_t* ipiv, DevState* st, PSlot* slots, T* rowbuf,
-                                                            T* diagbuf, unsigned long long seq_base, int use_smem,
+__global__ void __launch_bounds__(kPT2, 1) lu_panel2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+                                                            int64_t* ipiv, DevState* st, unsigned long long* xch,
+                                                            unsigned long long seq_base, int use_smem,
                                                             unsigned long long* tr_min, unsigned long long* tr_max) {
+    constexpr int WPE = PlW<T>::v;
+    unsigned long long* hdr = xch;
+    unsigned long long* rowll = xch + kPlHdrWords;
+    unsigned long long* diagll = rowll + kPlRowWords;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (tr_min && threadIdx.x == 0) atomicMin(tr_min, gtimer());
     const int P = gridDim.x, cta = blockIdx.x;
@@ -194,9 +230,9 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
     const int64_t cp = use_smem ? (chunk | 1) : ldw;
     T* Ps = use_smem ? (T*)smem_raw : W + rbeg + k0 * ldw;
     T* ubuf = use_smem ? (T*)smem_raw + cp * nbp : (T*)smem_raw;
-    __shared__ T sv[8];
-    __shared__ long long si[8];
-    __shared__ int sdn[8];
+    __shared__ T sv[32];
+    __shared__ long long si[32];
+    __shared__ int sdn[32];
     __shared__ long long s_p;
     __shared__ int s_owner;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -207,28 +243,30 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
             [&](int e, T v) { const int c = e / nr, r = e - c * nr; Ps[r + c * cp] = v; });
         __syncthreads();
     }
-    // publish the candidate for column j: (v, idx) of this CTA, its row, and the old row g
+    // publish the candidate for column j: (|v|, idx) of this CTA, its row, and the row at position g
+    auto put_hdr = [&](int j, T v, long long idx) {       // one thread
+        const unsigned sq = (unsigned)(seq_base + (unsigned long long)j + 1ull);
+        const unsigned long long hi = (unsigned long long)sq << 32;
+        const unsigned long long vb = (unsigned long long)__double_as_longlong((double)v);
+        unsigned long long* h = hdr + ((size_t)(j & 1) * kPlMaxP + cta) * 4;
+        const unsigned i32 = idx == 0x7fffffffffffffffll ? 0xffffffffu : (unsigned)idx;
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(h), "l"(hi | (vb >> 32)), "l"(hi | (vb & 0xffffffffull)) : "memory");
+        asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(h + 2), "l"(hi | i32) : "memory");
+    };
     auto publish = [&](int j, T v, long long idx) {
         const int64_t g = k0 + j;
         const int par = j & 1;
+        const unsigned sq = (unsigned)(seq_base + (unsigned long long)j + 1ull);
         if (idx != 0x7fffffffffffffffll && idx >= rbeg && idx < rend) {
             const int r = (int)(idx - rbeg);
-            for (int c = threadIdx.x; c < nbp; c += blockDim.x) rowbuf[((int64_t)par * P + cta) * nbp + c] = Ps[r + c * cp];
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x)
+                pl_put(rowll + (((size_t)par * kPlMaxP + cta) * kPW + c) * WPE, Ps[r + c * cp], sq);
         }
         if (g >= rbeg && g < rend) {
             const int r = (int)(g - rbeg);
-            for (int c = threadIdx.x; c < nbp; c += blockDim.x) diagbuf[par * nbp + c] = Ps[r + c * cp];
+            for (int c = threadIdx.x; c < nbp; c += blockDim.x) pl_put(diagll + ((size_t)par * kPW + c) * WPE, Ps[r + c * cp], sq);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // slots are double-buffered by column parity like rowbuf: a CTA one column ahead must
-            // not overwrite a candidate another CTA has not read yet
-            PSlot* sl = slots + par * 512 + cta;
-            sl->v = (double)v;
-            sl->idx = idx;
-            // release is cumulative: the CTA's rowbuf writes (ordered by the barrier above) are published too
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq), "l"(seq_base + (unsigned long long)j + 1ull) : "memory");
-        }
+        if (threadIdx.x == 0) put_hdr(j, v, idx);
     };
     {
         T v;
@@ -237,15 +275,16 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         publish(0, v, idx);
     }
     unsigned long long info = ~0ull;
-    // Column step, four CTA barriers (r02: was nine): [poll] B1 [pivot row -> ubuf, the interchange's
+    // Column step, three CTA barriers (r02: was nine): [poll] B1 [pivot row -> ubuf, the interchange's
     // two row writes] B2 [multipliers, column j+1 and each thread's candidate for it] B3 (inside the
-    // reduction) [rows rc / g+1 finished and copied out] B4 [publish] [bulk update].  The next step's
+    // reduction) [rows rc / g+1 finished and published word by word] [bulk update].  The next step's
     // B1 orders the bulk update before anything that overwrites what it reads.
     for (int j = 0; j < nbp; ++j) {
         const int64_t g = k0 + j;
         const int par = j & 1;
         const unsigned long long want = seq_base + (unsigned long long)j + 1ull;
-        // ---- poll every slot (barrier + data in one), pick the winner
+        // ---- poll every CTA's header words (barrier + data in one), pick the winner
+        const unsigned sq = (unsigned)want;
         if (warp == 0) {
             T bv = T(-1);
             long long bi = 0x7fffffffffffffffll;
@@ -253,6 +292,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
             // each lane owns up to 5 slots (P <= 160); all are polled together each round
             constexpr int kMaxPer = 5;
             bool ready[kMaxPer];
+            unsigned long long h0[kMaxPer], h1[kMaxPer], h2[kMaxPer];
 #pragma unroll
             for (int q = 0; q < kMaxPer; ++q) ready[q] = (lane + 32 * q) >= P;
             for (;;) {
@@ -260,20 +300,22 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
 #pragma unroll
                 for (int q = 0; q < kMaxPer; ++q) {
                     if (!ready[q]) {
-                        const unsigned long long sq = ld_relaxed64(&slots[par * 512 + lane + 32 * q].seq);
-                        ready[q] = sq >= want;
+                        const unsigned long long* h = hdr + ((size_t)par * kPlMaxP + lane + 32 * q) * 4;
+                        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(h0[q]), "=l"(h1[q]) : "l"(h) : "memory");
+                        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(h2[q]) : "l"(h + 2) : "memory");
+                        ready[q] = (unsigned)(h0[q] >> 32) == sq && (unsigned)(h1[q] >> 32) == sq && (unsigned)(h2[q] >> 32) == sq;
                         all = all && ready[q];
                     }
                 }
                 if (__all_sync(0xffffffffu, all)) break;
             }
-            fence_acq_rel();   // the slots' data (and the rows they guard) after the flags
 #pragma unroll
             for (int q = 0; q < kMaxPer; ++q) {
                 const int t = lane + 32 * q;
                 if (t < P) {
-                    const T cv = (T)__ldcg(&slots[par * 512 + t].v);
-                    const long long ci = __ldcg(&slots[par * 512 + t].idx);
+                    const T cv = (T)__longlong_as_double((long long)(((h0[q] & 0xffffffffull) << 32) | (h1[q] & 0xffffffffull)));
+                    const unsigned i32 = (unsigned)h2[q];
+                    const long long ci = i32 == 0xffffffffu ? 0x7fffffffffffffffll : (long long)i32;
                     if (cv > bv || (cv == bv && ci < bi)) { bv = cv; bi = ci; bo = t; }
                 }
             }
@@ -293,13 +335,13 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         const int g_loc = (g >= rbeg && g < rend) ? (int)(g - rbeg) : -1;
         // the pivot row into ubuf; the pivot itself first (same line, one broadcast load): an exact
         // zero pivot means no interchange and no elimination (singular column)
-        const T* prow = rowbuf + ((int64_t)par * P + owner) * nbp;
-        const T piv = __ldcg(&prow[j]);
+        const unsigned long long* prow = rowll + (((size_t)par * kPlMaxP + owner) * kPW) * WPE;
+        const T piv = pl_get(prow + (size_t)j * WPE, sq, T(0));
         const bool elim = piv != T(0);
         T* dst_p = own_p ? Ps + (p - rbeg) : nullptr;
         for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
-            const T u = __ldcg(&prow[c]);
-            const T dg = (own_p && elim) ? __ldcg(&diagbuf[par * nbp + c]) : T(0);
+            const T u = pl_get(prow + (size_t)c * WPE, sq, T(0));
+            const T dg = (own_p && elim) ? pl_get(diagll + ((size_t)par * kPW + c) * WPE, sq, T(0)) : T(0);
             ubuf[c] = u;
             if (elim) {
                 if (own_p) dst_p[c * cp] = dg;               // the owner of p takes the old row g
@@ -340,32 +382,26 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
         // ---- the candidate row and row g+1: finish their update (columns j+2..) while copying them out
         {
             const int par1 = (j + 1) & 1;
+            const unsigned sq1 = sq + 1u;
             const T lc = (rc >= 0 && elim) ? Ps[rc + j * cp] : T(0);
             const T lg = (rg >= 0 && elim) ? Ps[rg + j * cp] : T(0);
+            unsigned long long* myrow = rowll + (((size_t)par1 * kPlMaxP + cta) * kPW) * WPE;
+            unsigned long long* dgrow = diagll + ((size_t)par1 * kPW) * WPE;
             for (int c = threadIdx.x; c < nbp; c += blockDim.x) {
                 const T uc = ubuf[c];
                 if (rc >= 0) {
                     T a = Ps[rc + c * cp];
                     if (elim && c >= j + 2) { a -= lc * uc; Ps[rc + c * cp] = a; }
-                    rowbuf[((int64_t)par1 * P + cta) * nbp + c] = a;
-                    if (rg == rc) diagbuf[par1 * nbp + c] = a;
+                    pl_put(myrow + (size_t)c * WPE, a, sq1);
+                    if (rg == rc) pl_put(dgrow + (size_t)c * WPE, a, sq1);
                 }
                 if (rg >= 0 && rg != rc) {
                     T a = Ps[rg + c * cp];
                     if (elim && c >= j + 2) { a -= lg * uc; Ps[rg + c * cp] = a; }
-                    diagbuf[par1 * nbp + c] = a;
+                    pl_put(dgrow + (size_t)c * WPE, a, sq1);
                 }
             }
-        }
-        __syncthreads();                                                      // B4
-        if (threadIdx.x == 0) {
-            // slots are double-buffered by column parity like rowbuf: a CTA one column ahead must
-            // not overwrite a candidate another CTA has not read yet
-            PSlot* sl = slots + ((j + 1) & 1) * 512 + cta;
-            sl->v = (double)v;
-            sl->idx = idx;
-            // release is cumulative: the CTA's rowbuf writes (ordered by the barrier above) are published too
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&sl->seq), "l"(seq_base + (unsigned long long)j + 2ull) : "memory");
+            if (threadIdx.x == 0) put_hdr(j + 1, v, idx);      // no barrier: every word validates itself
         }
         // ---- bulk rank-1 update of the remaining rows, columns j+2.. (thread = row, column phase)
         if (elim) panel_bulk_update<T>(Ps, cp, ubuf, (int)r0, nr, j, nbp, rc, rg);
@@ -390,7 +426,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel2_kernel(T* W, int64_t ldw, in
 namespace cg = cooperative_groups;
 constexpr int kClMax = 8;
 template <typename T>
-__global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
+__global__ void __launch_bounds__(kPT2, 1) lu_panel_cl_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
                                                               int64_t* ipiv, DevState* st, int prof_on) {
     cg::cluster_group cl = cg::this_cluster();
     // diagnostics (prof_on): clock64 phase totals of CTA 0 / thread 0 into st->dbg_t
@@ -410,11 +446,14 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
     T* ubuf = Ps + cp * nbp;                             // pivot row
     T* candb = ubuf + nbp;                               // [2][nbp] my candidate row
     T* diagb = candb + 2 * nbp;                          // [2][nbp] old row g (owner of g)
-    __shared__ T s_cv[2];
-    __shared__ long long s_ci[2];
-    __shared__ T sv[8];
-    __shared__ long long si[8];
-    __shared__ int sdn[8];
+    // every CTA's candidate header (|v|, row), pushed into every CTA's inbox at publication: the winner
+    // is then picked from local shared memory and only the winning row is read remotely (r02q: the
+    // three dependent DSMEM reads of the pull version were 1865 of 7150 cycles per column at P = 8)
+    __shared__ T in_cv[2][kClMax];
+    __shared__ long long in_ci[2][kClMax];
+    __shared__ T sv[32];
+    __shared__ long long si[32];
+    __shared__ int sdn[32];
     __shared__ long long s_p;
     __shared__ int s_owner;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -434,7 +473,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
             const int r = (int)(g - rbeg);
             for (int c = threadIdx.x; c < nbp; c += blockDim.x) diagb[par * nbp + c] = Ps[r + c * cp];
         }
-        if (threadIdx.x == 0) { s_cv[par] = v; s_ci[par] = idx; }
+        if ((int)threadIdx.x < P) {
+            *cl.map_shared_rank(&in_cv[par][cta], threadIdx.x) = v;
+            *cl.map_shared_rank(&in_ci[par][cta], threadIdx.x) = idx;
+        }
     };
     {
         T v;
@@ -460,11 +502,7 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
             T bv = T(-1);
             long long bi = 0x7fffffffffffffffll;
             int bo = 0;
-            if (lane < P) {
-                bv = *cl.map_shared_rank(&s_cv[par], lane);
-                bi = *cl.map_shared_rank(&s_ci[par], lane);
-                bo = lane;
-            }
+            if (lane < P) { bv = in_cv[par][lane]; bi = in_ci[par][lane]; bo = lane; }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -542,7 +580,10 @@ __global__ void __launch_bounds__(kPT, 1) lu_panel_cl_kernel(T* W, int64_t ldw, 
                     diagb[par1 * nbp + c] = a;
                 }
             }
-            if (threadIdx.x == 0) { s_cv[par1] = v; s_ci[par1] = idx; }
+            if ((int)threadIdx.x < P) {
+                *cl.map_shared_rank(&in_cv[par1][cta], threadIdx.x) = v;
+                *cl.map_shared_rank(&in_ci[par1][cta], threadIdx.x) = idx;
+            }
         }
         PHC(5);
         // (the multipliers of rows rcn / rg were read above by every thread before any of its bulk
@@ -1328,7 +1369,8 @@ __global__ void __launch_bounds__(256) swap_u12v2_kernel(T* W, int64_t ldw, int6
 // blocks of 32 and row group i (rows lane + 32 i) only for i >= k / 32 (62.5 % of the FMAs).
 template <typename T, int NC>
 __global__ void __launch_bounds__(256) swap_u12v3_kernel(T* W, int64_t ldw, int64_t k0, int bw, int64_t c0, int64_t c1,
-                                                        const SwapPlan* __restrict__ plan, const T* __restrict__ Linv) {
+                                                        const SwapPlan* __restrict__ plan, const T* __restrict__ Linv,
+                                                        int noswap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* Bn = (T*)smem_raw;                // [NC][kSU3LD]: column c of the block rows after the interchanges
     T* Ex = Bn + NC * kSU3LD;            // [NC][kSU3LD]: values for the rows leaving the block
@@ -1337,8 +1379,9 @@ __global__ void __launch_bounds__(256) swap_u12v3_kernel(T* W, int64_t ldw, int6
     const int64_t cc0 = c0 + (int64_t)blockIdx.x * NC;
     const int nc = (int)min<int64_t>(NC, c1 - cc0);
     if (nc <= 0) return;
-    const int ne = plan->ne, R = bw + ne;
-    for (int t = threadIdx.x; t < R; t += blockDim.x) srow[t] = plan->srow[t];
+    // noswap: the interchanges were applied already (two-panel blocks): U12 = L11^{-1} A12 only
+    const int ne = noswap ? 0 : plan->ne, R = bw + ne;
+    for (int t = threadIdx.x; t < R; t += blockDim.x) srow[t] = noswap ? k0 + t : plan->srow[t];
     for (int t = threadIdx.x; t < ne; t += blockDim.x) edst[t] = plan->edst[t];
     __syncthreads();
     batched<16, T>(
@@ -1842,7 +1885,7 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
             cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(pc);
-            cfg.blockDim = dim3(kPT);
+            cfg.blockDim = dim3(kPT2);
             cfg.dynamicSmemBytes = smc;
             cfg.stream = s;
             cudaLaunchAttribute at[2];
@@ -1860,20 +1903,17 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
     // a block is shorter than a leaf panel (~0.9 ms per 128 columns: latency of the per-column
     // multi-CTA exchange) and the faster cooperative panel (rows in shared memory, ~0.45 ms) wins even
     // though it occupies m/128 SMs
-    static const int64_t lf_min_m = getenv("AS_LU_LF_MIN_M") ? atoll(getenv("AS_LU_LF_MIN_M")) : 10240;
+    static const int64_t lf_min_m = getenv("AS_LU_LF_MIN_M") ? atoll(getenv("AS_LU_LF_MIN_M")) : 12288;
     if (!coop && m > lf_min_m && lf_panel_launch<T>(w, k0, nbp, seq_base, prio, s)) return;
     const int64_t chunk = (m + P - 1) / P;
     size_t smem = sizeof(T) * ((chunk | 1) * nbp + nbp);
     int use_smem = 1;
     if (smem > 200 * 1024) { use_smem = 0; smem = sizeof(T) * nbp; }
-    PSlot* slots = (PSlot*)w.cand;
-    T* rowbuf = (T*)((char*)w.cand + sizeof(PSlot) * 1024);
-    T* diagbuf = rowbuf + (int64_t)2 * 1024 * kPW;
     auto kern = lu_panel2_kernel<T>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1024));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P);
-    cfg.blockDim = dim3(kPT);
+    cfg.blockDim = dim3(kPT2);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -1886,8 +1926,8 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
     const int slot = (int)(k0 / kBW) * 4 + ((k0 % kBW) ? 2 : 1);
     unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
     unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
-    cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, slots, rowbuf, diagbuf, seq_base, use_smem,
-                       tmn, tmx);
+    cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, (unsigned long long*)w.cand, seq_base,
+                       use_smem, tmn, tmx);
 }
 
 template <typename T>
@@ -1914,8 +1954,15 @@ static void linv_launch(const Work& w, int64_t k0, int nbp, cudaStream_t s) {
 }
 
 template <typename T>
-static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s) {
+static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64_t c1, cudaStream_t s, bool noswap = false) {
     if (c1 <= c0) return;
+    if (noswap) {
+        const int smem = (int)(sizeof(T) * 2 * kSU3C * kSU3LD);
+        swap_u12v3_kernel<T, kSU3C><<<(unsigned)((c1 - c0 + kSU3C - 1) / kSU3C), 256, smem, s>>>(
+            (T*)w.W, w.ldw, k0, bw, c0, c1, (const SwapPlan*)w.swplan + k0 / kBW,
+            (const T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW, 1);
+        return;
+    }
     static const bool v1 = getenv("AS_LU_SWAP_V1") != nullptr;
     // the 16-column kernel (r02o, C5, same run: 163.3 ms against 170.3 with the 64-column kernel
     // everywhere and 167.2 with it on the bulk only; AS_LU_SWAP_V3_MAXC=c keeps it to launches of <= c columns)
@@ -1924,7 +1971,7 @@ static void swap_u12_launch(const Work& w, int64_t k0, int bw, int64_t c0, int64
         const int smem = (int)(sizeof(T) * 2 * kSU3C * kSU3LD);
         swap_u12v3_kernel<T, kSU3C><<<(unsigned)((c1 - c0 + kSU3C - 1) / kSU3C), 256, smem, s>>>(
             (T*)w.W, w.ldw, k0, bw, c0, c1, (const SwapPlan*)w.swplan + k0 / kBW,
-            (const T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW);
+            (const T*)w.linv + (k0 / kBW) * (int64_t)kBW * kBW, 0);
         return;
     }
     if (w.linv && !v1) {
@@ -1982,7 +2029,7 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
         return;
     }
-    cudaMemsetAsync(w.cand, 0, sizeof(PSlot) * 1024, s);       // panel exchange slots (sequence numbers)
+    cudaMemsetAsync(w.cand, 0, lu_cand_bytes(), s);            // panel exchange words (sequence numbers repeat across solves)
     if (w.lfbuf) cudaMemsetAsync(w.lfbuf, 0, lf_layout(w.lfbuf, n, sizeof(T)).zero_bytes, s);   // leaf panel counters + slots
     if (lu_trace().tmin) {
         cudaMemsetAsync(lu_trace().tmin, 0xFF, sizeof(unsigned long long) * 4 * kTraceBlocks, s);
@@ -1995,6 +2042,104 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
     // AS_LU_SCHED=1: the dataflow schedule below (measured slower on C5 in r02n: 188 vs 170 ms with the
     // same kernels); default: the block-synchronous look-ahead schedule further down
     static const int sched = getenv("AS_LU_SCHED") ? atoi(getenv("AS_LU_SCHED")) : 0;
+    if (lookahead && sched == 2 && w.linv && w.swplan && n >= 4096) {
+        // Two-panel blocks: the trailing update runs with K = 256 (DMMA GEMM 87 % of peak against 82 % at
+        // K = 128, half the passes over the trailing matrix, half the joins).  Per double block
+        // [k0, k0 + 256) = panels A, B:
+        //   columns of B:       interchanges of A + U12(A), A22 -= L21(A) U12(A), then panel B
+        //   columns of A:       interchanges of B (rows below A's block; L21(A) must be in the row order
+        //                       the K = 256 update sees)
+        //   trailing columns:   interchanges of A + U12(A); interchanges of B; the 128-row strip of B
+        //                       -= L21(A)[rows of B] U12(A); U12(B) = L11(B)^{-1} strip; then ONE update
+        //                       A22 -= [L21(A) L21(B)] [U12(A); U12(B)] on the rows below the double block.
+        // Look-ahead: the next double block's panel-A columns take all of this first on the
+        // high-priority stream, then panel A'; panel B' follows on the same stream as soon as the
+        // first chunk of the bulk update (which holds B's columns) is done.
+        auto trail = [&](int64_t k0, int wa, int wb, int64_t c0, int64_t c1, cudaStream_t st, int trace_slot) {
+            if (c1 <= c0) return;
+            const int64_t kb = k0 + wa;
+            swap_u12_launch<T>(w, k0, wa, c0, c1, st);                       // A's interchanges + U12(A)
+            if (wb > 0) {
+                laswp_launch<T>(w, kb, wb, c0, c1, 0, 0, false, st);          // B's interchanges
+                gemm_launch<T>(w, kb, c0, k0, wb, c1 - c0, wa, st, 0);        // strip of B's rows
+                swap_u12_launch<T>(w, kb, wb, c0, c1, st, true);              // U12(B) (no interchanges)
+            }
+            const int64_t r0 = kb + std::max(wb, 0);
+            gemm_launch<T>(w, r0, c0, k0, n - r0, c1 - c0, wa + std::max(wb, 0), st, 0, false, trace_slot);
+        };
+        cudaEvent_t e_start = ev();
+        cudaEventRecord(e_start, s);
+        cudaStreamWaitEvent(LS.hi, e_start, 0);
+        cudaStreamWaitEvent(LS.side, e_start, 0);
+        cudaStreamWaitEvent(LS.aux, e_start, 0);
+        block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, LS.hi);      // panel A of block 0
+        cudaEvent_t ev_b_cols = nullptr;       // "the columns of the next panels B and A' are up to date"
+        cudaEvent_t ev_main_done = nullptr;    // the previous double block's bulk update is complete
+        int step = 0;
+        for (int64_t k0 = 0; k0 < n; k0 += 2 * kBW, ++step) {
+            const int wa = (int)std::min<int64_t>(kBW, n - k0);
+            const int64_t kb = k0 + wa;
+            const int wb = (int)std::min<int64_t>(kBW, n - kb);          // <= 0: no panel B
+            const int64_t kn = kb + std::max(wb, 0);                     // next double block
+            // ---- panel B (high priority): its columns get A's interchanges, U12(A) and the K = 128 update
+            if (wb > 0) {
+                if (ev_b_cols) cudaStreamWaitEvent(LS.hi, ev_b_cols, 0);
+                swap_u12_launch<T>(w, k0, wa, kb, kb + wb, LS.hi);
+                gemm_launch<T>(w, kb, kb, k0, n - kb, wb, wa, LS.hi, LS.prio_hi);
+                block_panels<T>(w, kb, wb, LS.prio_hi, LS.hi);
+                laswp_launch<T>(w, kb, wb, k0, k0 + wa, 0, 0, false, LS.hi);   // B's interchanges into L21(A)
+            }
+            cudaEvent_t ev_p = LS.evl[step & 1];
+            cudaEventRecord(ev_p, LS.hi);
+            // ---- finished L columns [0, k0) and the row permutation (side stream); the previous double
+            // block's bulk update still reads its L21 in the old row order: wait for it
+            cudaStreamWaitEvent(LS.side, ev_p, 0);
+            if (ev_main_done) cudaStreamWaitEvent(LS.side, ev_main_done, 0);
+            laswp_launch<T>(w, k0, wa, 0, k0, 0, 0, true, LS.side);
+            if (wb > 0) laswp_launch<T>(w, kb, wb, 0, k0, 0, 0, true, LS.side);
+            if (kn >= n) break;
+            // ---- look-ahead: the next panel A's columns, then panel A' (high priority)
+            const int wa2 = (int)std::min<int64_t>(kBW, n - kn);
+            trail(k0, wa, wb, kn, kn + wa2, LS.hi, (int)(k0 / kBW) * 4 + 3);
+            block_panels<T>(w, kn, wa2, LS.prio_hi, LS.hi);
+            // ---- the other trailing columns in chunks alternating between two streams; the first chunk
+            // holds the next panel B's columns
+            cudaStreamWaitEvent(s, ev_p, 0);
+            {
+                cudaEvent_t ea = LS.evc[3][step & 1];      // aux continues from the joined state of s
+                cudaEventRecord(ea, s);
+                cudaStreamWaitEvent(LS.aux, ea, 0);
+            }
+            const int64_t c0r = kn + wa2, rn = n - c0r;
+            ev_b_cols = nullptr;
+            if (rn > 0) {
+                const int nch = rn >= 4096 ? 4 : rn >= 1024 ? 2 : 1;
+                for (int i = 0; i < nch; ++i) {
+                    auto bnd = [&](int q) { return q >= nch ? n : c0r + std::max<int64_t>((rn * q / nch + 63) / 64 * 64, q > 0 ? 2 * kBW : 0); };
+                    const int64_t a0 = std::min<int64_t>(bnd(i), n), a1 = std::min<int64_t>(bnd(i + 1), n);
+                    cudaStream_t st = (i & 1) ? LS.aux : s;
+                    trail(k0, wa, wb, a0, a1, st, i == 0 ? (int)(k0 / kBW) * 4 + 0 : -1);
+                    if (i == 0) { ev_b_cols = LS.evc[0][step & 1]; cudaEventRecord(ev_b_cols, st); }
+                }
+                cudaEvent_t eb = LS.evc[1][step & 1];
+                cudaEventRecord(eb, LS.aux);
+                cudaStreamWaitEvent(s, eb, 0);
+            }
+            ev_main_done = LS.evc[2][step & 1];
+            cudaEventRecord(ev_main_done, s);
+        }
+        cudaEvent_t e1 = ev();
+        cudaEventRecord(e1, LS.hi);
+        cudaStreamWaitEvent(s, e1, 0);
+        cudaEvent_t ea = ev();
+        cudaEventRecord(ea, LS.aux);
+        cudaStreamWaitEvent(s, ea, 0);
+        cudaEvent_t ej = ev();
+        cudaEventRecord(ej, LS.side);
+        cudaStreamWaitEvent(s, ej, 0);
+        launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
+        return;
+    }
     if (lookahead && sched == 1) {
         // Dataflow schedule.  The trailing columns are split into nch FIXED column chunks (boundaries
         // multiples of the block width), each with its own stream: chunk q at step k runs
@@ -2167,7 +2312,7 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
     cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, 0);
     cudaMalloc(&w.ipiv, 8 * n);
     cudaMalloc(&w.st, sizeof(DevState));
-    cudaMalloc(&w.cand, 16 * 2 * 1024 + 8 * 2 * 1024 * 128 + 8 * 2 * 128);
+    cudaMalloc(&w.cand, lu_cand_bytes());
     const size_t lfb = lu_lfbuf_bytes(n, dtype);
     cudaMalloc(&w.lfbuf, lfb);
     cudaMemset(w.st, 0, sizeof(DevState));
@@ -2180,7 +2325,7 @@ double lu_debug_panel_time(int dtype, int kind, void* W, int64_t ldw, int64_t n,
     double tot = 0.0;
     for (int it = 0; it < iters; ++it) {
         cudaMemcpy(W, Wsrc, es * ldw * n, cudaMemcpyDeviceToDevice);
-        cudaMemset(w.cand, 0, 16 * 2 * 1024);
+        cudaMemset(w.cand, 0, lu_cand_bytes());
         cudaMemset(w.lfbuf, 0, lf_layout(w.lfbuf, n, es).zero_bytes);
         cudaEventRecord(e0, 0);
         // kind 0: the launch the factorization makes; kind 1: the cooperative panel

@@ -175,38 +175,6 @@ AS_DEV void block_product(const T* __restrict__ Ms, const T* __restrict__ Xs, T 
     }
 }
 
-// fp64, RT == 8: the 64 x 64 x 8 block product on the fp64 tensor cores (mma.sync m8n8k4 -> DMMA).
-// Warp w owns rows 8w .. 8w+7; thread (gid = lane / 4, tig = lane % 4) ends with C(8w + gid, 2 tig)
-// and C(8w + gid, 2 tig + 1); two accumulator chains (even / odd k-steps) halve the dependent
-// DMMA chain.  No barrier, no shared-memory reduction: 16 DMMAs + 32 LDS per warp against the SIMT
-// version's 128 FMAs + 144 LDS per thread and a barrier.
-AS_DEV void ts_dmma884(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
-template <bool TRANSB>
-AS_DEV void block_product_dmma(const double* __restrict__ Ms, const double* __restrict__ Xs, double (&part)[2]) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
-    const int row = 8 * w + gid;
-    double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
-#pragma unroll
-    for (int s = 0; s < kNB / 8; ++s) {
-        const int ka = 8 * s + tig, kb = ka + 4;
-        const double a0 = TRANSB ? Ms[ka + row * kLDT] : Ms[row + ka * kLDT];
-        const double a1 = TRANSB ? Ms[kb + row * kLDT] : Ms[row + kb * kLDT];
-        const double b0 = Xs[ka + gid * kLDX], b1 = Xs[kb + gid * kLDX];
-        ts_dmma884(e0, e1, a0, b0);
-        ts_dmma884(o0, o1, a1, b1);
-    }
-    part[0] = e0 + o0;
-    part[1] = e1 + o1;
-}
-template <typename T, bool TRANSB>
-AS_DEV void block_product_mm(const T* Ms, const T* Xs, T (&part)[2]) {
-    if constexpr (sizeof(T) == 8) block_product_dmma<TRANSB>((const double*)Ms, (const double*)Xs, (double(&)[2])part);
-}
-
 template <typename T>
 AS_DEV void cp_async_elem(T* smem, const T* gmem, bool ok) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -258,12 +226,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     const int nbr = (int)min<int64_t>(kNB, n - ob);
     const int c0 = rt * RT;
     const int R = min(RT, p.nrhs - c0);
-    // ownership of the accumulators: SIMT (row tid % 64, columns g + 4u) or, for the fp64 8-column
-    // tile, the DMMA fragment layout (row 8 warp + lane / 4, columns 2 (lane % 4) + u)
-    constexpr bool MM = (RT == 8 && sizeof(T) == 8);
-    const int g = threadIdx.x / kNB;
-    const int i = MM ? 8 * (int)(threadIdx.x >> 5) + (int)((threadIdx.x & 31) >> 2) : (int)(threadIdx.x % kNB);
-    auto colu = [&](int u) { return MM ? 2 * (int)(threadIdx.x & 3) + u : (RT == 1 ? 0 : g + 4 * u); };
+    const int i = threadIdx.x % kNB, g = threadIdx.x / kNB;
 
     // async staging of op(T)_{b j} (no-trans: A[b rows, j cols]; trans: A[j rows, b cols])
     auto stage = [&](T* dst, int sp) {
@@ -290,7 +253,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     T acc[PER];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
-        const int c = colu(u);
+        const int c = RT == 1 ? 0 : g + 4 * u;
         acc[u] = ((RT > 1 || g == 0) && c < R && i < nbr) ? X[(ob + i) + (c0 + c) * p.ldx] : T(0);
     }
 
@@ -319,8 +282,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
         if (sp + 1 == s) TSP(2);
-        if constexpr (MM) block_product_mm<T, TRANS>(Ms, Xs, part);
-        else block_product<T, TRANS, RT>(Ms, Xs, part, R, Red);
+        block_product<T, TRANS, RT>(Ms, Xs, part, R, Red);
         if (RT == 1) {
             Red[g * kNB + i] = part[0];
             __syncthreads();
@@ -338,12 +300,11 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     TSP(4);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
-        const int c = colu(u);
+        const int c = RT == 1 ? 0 : g + 4 * u;
         if (RT > 1 || g == 0) Xs[i + c * kLDX] = acc[u];
     }
     __syncthreads();
-    if constexpr (MM) block_product_mm<T, TRANS>(Ds, Xs, part);
-    else block_product<T, TRANS, RT>(Ds, Xs, part, R, Red);
+    block_product<T, TRANS, RT>(Ds, Xs, part, R, Red);
     unsigned long long* dst = p.ll + ((int64_t)(b * ntiles + rt) * RT) * kNB * LLw<T>::v;
     if (RT == 1) {
         Red[g * kNB + i] = part[0];
@@ -356,7 +317,7 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     } else {
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
-            const int c = colu(u);
+            const int c = g + 4 * u;
             const T x = (i < nbr && c < R) ? part[u] : T(0);
             ll_put(dst + (int64_t)(c * kNB + i) * LLw<T>::v, x, ep);
             if (i < nbr && c < R) X[(ob + i) + (c0 + c) * p.ldx] = x;

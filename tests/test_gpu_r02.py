@@ -315,13 +315,13 @@ def test_repeat_bitwise_deterministic(case):
         check_parity(A, B)
 
 
-# ------------------------------------------------------------------ one-CTA estimator (n <= 512)
+# ------------------------------------------------------------------ estimator: same steps as the oracle
 @pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 200, 384, 512])
 @pytest.mark.parametrize("kind", ["lu", "spd", "lower", "upper"])
-def test_small_estimator_rcond_tight(kind, n):
-    """n <= 512: xLACN2 runs in one CTA (rcond.cu est_small_kernel) through the same factors and the
-    same steps as the oracle's estimator (Z13b).  Same iteration, same vectors: the estimate
-    agrees to rounding (1e-8 relative), not only within the soft factor-of-two bar."""
+def test_estimator_rcond_tight(kind, n):
+    """The device xLACN2 state machine (rcond.cu) runs the oracle's estimator steps (Z13b)
+    through the same factors: same iteration, same vectors, so the estimate agrees to rounding
+    (1e-8 relative), not only within the soft factor-of-two bar."""
     rng = np.random.default_rng(1000 * n + len(kind))
     if kind == "lu":
         A = rng.standard_normal((n, n)) + 4.0 * np.eye(n)
