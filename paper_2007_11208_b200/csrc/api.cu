@@ -15,7 +15,10 @@
 // Every branch decision is a graph conditional node whose value a kernel
 // sets from device-resident flags, so a call is one graph launch and one
 // stream synchronization.
+#include <cuda.h>
+
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <type_traits>
@@ -41,7 +44,50 @@ struct RepOut {
 };
 
 // ------------------------------------------------------------------ small kernels
-__global__ void set_args_kernel2(DevArgs a, DevArgs* dst) { *dst = a; }
+__global__ void set_args_kernel2(DevArgs a, DevArgs* dst) {
+    *dst = a;
+    // the tensor map in the argument block is consumed through the tensormap proxy (detect.cu)
+    asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+}
+
+// 2-D tensor map of A for the detection tile pipeline (TMA 2-D tiles): dims
+// (rows, columns) = (n, n), row stride lda, box 64 x 64, no swizzle, out-of-range elements read as 0.
+typedef CUresult (*TmapEncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncFn tmap_encoder() {
+    static TmapEncFn enc = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess) { cudaGetLastError(); f = nullptr; }
+        return (TmapEncFn)f;
+    }();
+    return enc;
+}
+// A plan takes the TMA pair pass when the shape qualifies (detect_tma_plan), A is 16-byte aligned (part of
+// the plan key: the choice between the two pair kernels is made on the host) and the driver can encode maps.
+static bool plan_uses_tma(int dt, int64_t n, int64_t lda, bool a16) {
+    return a16 && detect_tma_plan(dt, n, lda) && tmap_encoder() != nullptr;
+}
+static int fill_tmap(DevArgs& a, int dt, const void* A, int64_t lda, int64_t n) {
+    a.tma_ok = 0;
+    const size_t es = dt == AS_F64 ? 8 : 4;
+    static_assert(sizeof(CUtensorMap) == sizeof(a.tmapA), "CUtensorMap is 128 bytes");
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n}, strides[1] = {(cuuint64_t)(lda * es)};
+    const cuuint32_t box[2] = {kTile, kTile}, estr[2] = {1, 1};
+    CUtensorMap tm;
+    const CUresult r = tmap_encoder()(&tm, dt == AS_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        fprintf(stderr, "[adaptsolve] cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+        return AS_ERR_CUDA_BASE + (int)cudaErrorInvalidValue;
+    }
+    memcpy(a.tmapA, &tm, sizeof(tm));
+    a.tma_ok = 1;
+    return 0;
+}
 __global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned v) {
     if (threadIdx.x == 0) cudaGraphSetConditional(h, v);
 }
@@ -286,10 +332,11 @@ struct PlanKey {
     int sweeps;
     int instrumented;
     int eager;
+    int a16;             // A is 16-byte aligned (the detection pair pass is then the TMA pipeline)
     bool operator<(const PlanKey& o) const {
-        return std::tie(stream, dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps, instrumented, eager) <
+        return std::tie(stream, dev, dtype, n, nrhs, lda, ldb, opts, force, thr, cut, sweeps, instrumented, eager, a16) <
                std::tie(o.stream, o.dev, o.dtype, o.n, o.nrhs, o.lda, o.ldb, o.opts, o.force, o.thr, o.cut, o.sweeps,
-                        o.instrumented, o.eager);
+                        o.instrumented, o.eager, o.a16);
     }
 };
 static int g_instrument = 0;
@@ -338,7 +385,7 @@ static size_t layout(Work& w, uint32_t opts, char* base) {
     const size_t w_elems = std::max<size_t>((size_t)w.ldw * (size_t)std::max<int64_t>(band_rows, 1),
                                             (size_t)spike_scratch_elems(n, w.num_sms > 0 ? w.num_sms : 148));
     w.W = take(es * w_elems);
-    w.diag = take(es * n);
+    w.diag = take(es * (n + kTile));   // + one tile: the TMA detection pass copies whole 64-element slices
     w.xe = take(es * n);
     w.Dinv0 = take(es * nblk * kNB * kNB);
     w.Dinv1 = take(es * nblk * kNB * kNB);
@@ -477,6 +524,7 @@ static int get_plan(const PlanKey& key, Plan** out) {
     Work& w = P->w;
     w.dtype = key.dtype; w.n = key.n; w.nrhs = key.nrhs; w.lda = key.lda; w.ldb = key.ldb;
     cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, key.dev);
+    w.det_tma = plan_uses_tma(key.dtype, key.n, key.lda, key.a16 != 0);
     const size_t bytes = layout(w, key.opts, nullptr);
     int err = check(cudaMalloc(&P->ws, bytes), "cudaMalloc(workspace)");
     if (err) return err;
@@ -665,6 +713,7 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     key.sweeps = (opt && opt->max_sweeps > 0) ? opt->max_sweeps : 30;
     key.instrumented = g_instrument;
     key.eager = g_eager;
+    key.a16 = ((uintptr_t)A & 15) == 0;
     if ((key.opts & AS_OPT_SYM_INDEF) && n <= kSmallN && nrhs <= kSmallRhs && !(key.opts & AS_OPT_SKIP_DETECT))
         return solve_small_single(dt, A, lda, n, B, ldb, nrhs, X, key, rep_host, rep_dev, sigma, stream, sync, ret_dev);
     Plan* P = nullptr;
@@ -673,6 +722,7 @@ static int solve_impl(as_dtype dt, const void* A, int64_t lda, int64_t n, const 
     std::lock_guard<std::mutex> lk(P->mu);
     DevArgs a{};
     a.A = A; a.B = B; a.X = X; a.sigma = sigma; a.rep_dev = rep_dev; a.rep_host = nullptr; a.ret_dev = ret_dev;
+    if (P->w.det_tma && (err = fill_tmap(a, dt, A, lda, n)) != 0) return err;
     cudaKernelNodeParams kp = {};
     if (key.eager) {
         err = run_eager(*P, a, stream);
@@ -718,7 +768,7 @@ struct DetPlan {
     void* ws = nullptr;
     ~DetPlan() { if (ws) cudaFree(ws); }
 };
-static std::map<std::tuple<int, int, int64_t, int64_t>, std::unique_ptr<DetPlan>> g_det;
+static std::map<std::tuple<int, int, int64_t, int64_t, int>, std::unique_ptr<DetPlan>> g_det;
 
 __global__ void det_out_kernel(const DevState* st, as_structure* out, int fullscan) {
     if (threadIdx.x != 0) return;
@@ -894,29 +944,32 @@ int as_detect(as_dtype dt, const void* A, int64_t lda, int64_t n, uint32_t detec
     cudaGetDevice(&dev);
     cudaStream_t s = (cudaStream_t)stream;
     std::lock_guard<std::mutex> lk(g_mu);
-    auto key = std::make_tuple(dev, (int)dt, n, lda);
+    const int a16 = ((uintptr_t)A & 15) == 0;
+    auto key = std::make_tuple(dev, (int)dt, n, lda, a16);
     auto it = g_det.find(key);
     if (it == g_det.end()) {
         auto D = std::make_unique<DetPlan>();
         Work& w = D->w;
         w.dtype = dt; w.n = n; w.lda = lda; w.nrhs = 1; w.ldb = n;
         cudaDeviceGetAttribute(&w.num_sms, cudaDevAttrMultiProcessorCount, dev);
+        w.det_tma = plan_uses_tma(dt, n, lda, a16 != 0);
         const size_t es = dt == AS_F64 ? 8 : 4;
         size_t bytes = align256(sizeof(DevState)) + align256(sizeof(DevArgs)) + align256(sizeof(as_structure)) +
-                       align256(es * n) + align256(64 * 4);
+                       align256(es * (n + kTile)) + align256(64 * 4);
         int err = check(cudaMalloc(&D->ws, bytes), "cudaMalloc(detect)");
         if (err) return err;
         char* p = (char*)D->ws;
         w.st = (DevState*)p; p += align256(sizeof(DevState));
         w.args = (DevArgs*)p; p += align256(sizeof(DevArgs));
         w.cand = p; p += align256(sizeof(as_structure));
-        w.diag = p; p += align256(es * n);
+        w.diag = p; p += align256(es * (n + kTile));
         w.bars = (unsigned*)p; w.bars_len = 64;
         it = g_det.emplace(key, std::move(D)).first;
     }
     Work& w = it->second->w;
     DevArgs a{};
     a.A = A;
+    if (w.det_tma) { const int e = fill_tmap(a, dt, A, lda, n); if (e) return e; }
     set_args_kernel2<<<1, 1, 0, s>>>(a, w.args);
     launch_state_init(w, s, detect_flags, 0, 0.0, 0.0, 30);
     const bool check_finite = (detect_flags & AS_OPT_CHECK_FINITE) != 0;

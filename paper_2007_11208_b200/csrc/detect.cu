@@ -13,6 +13,9 @@
 // a dense asymmetric matrix kills all four candidates within the first pair
 // and the kernel exits early (the paper's "all further processing is stopped",
 // P:339-340), while a banded matrix is read exactly once (HBM-bound).
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace as {
@@ -450,6 +453,285 @@ __global__ void __launch_bounds__(kDetThreads, 2) detect_pairs_v3(const DevArgs*
     }
 }
 
+// ------------------------------------------------------------------ pass 2, TMA tile pipeline
+// The pair pass for 16-byte aligned A / lda and n >= 1024 (chosen on the host: one launch either way).
+// One CTA per SM; a producer thread feeds a ring of six 32 KB (fp64) slots with 2-D TMA tile loads
+// (cp.async.bulk.tensor, 64 x 64 boxes of the tensor map in the argument block, zero-filled out of
+// range) that complete on per-stage mbarriers; eight consumer warps read the tiles from shared
+// memory and release the stage on a second mbarrier -- no block barrier, 192 KB in flight per SM.
+// Pairs are handed out far-from-diagonal first from a device counter (the first wave statically).
+//   one triangular candidate left (C3b): 6 stages of one tile (the other strict triangle's tiles);
+//     "is any element non-zero" on 16-byte shared-memory reads.
+//   otherwise: 3 stages of (lower tile, mirror tile, diag slices of the tile's rows and columns).
+//     The tile is walked along wrapped diagonals, lane l of a task taking element (r, (r + d) mod 64):
+//     both the lower tile (column-major, index c*64 + r) and the mirror tile read transposed (index
+//     r*64 + c) are then conflict-free without padding or swizzle.  Only the sympd candidate left
+//     (C3a): Fig. 4 lines 12-16 and nothing else; several candidates (C2): band extents / triangle
+//     verdicts per warp, Fig. 4 only for warps that saw a non-zero (an all-zero set passes lines
+//     12-16 trivially: every diagonal entry is > 0 while the candidate lives).
+// The verdicts are the same per-element predicates as detect_pairs_v3 (Z8).
+constexpr int kTmaSlots = 6;
+constexpr int kTmaConsumers = 256;
+constexpr int kTmaThreads = kTmaConsumers + 32;
+
+AS_DEV void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+AS_DEV void mbar_arrive(uint64_t* b) {
+    asm volatile("{ .reg .b64 t; mbarrier.arrive.shared::cta.b64 t, [%0]; }" ::"r"(smem_u32(b)) : "memory");
+}
+AS_DEV void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("{ .reg .b64 t; mbarrier.arrive.expect_tx.shared::cta.b64 t, [%0], %1; }" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+AS_DEV void mbar_wait(uint64_t* b, unsigned parity) {
+    unsigned ok;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(smem_u32(b)), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+// A is streamed once: the tiles carry an L2 evict-first policy (as the __ldcs loads of detect_pairs_v3 do),
+// so they do not displace the workspace lines the factorization kernels are about to use
+AS_DEV void tma_tile_2d(void* dst, const void* tmap, int row0, int col0, uint64_t* bar, uint64_t policy) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+                 ::"r"(smem_u32(dst)), "l"(tmap), "r"(row0), "r"(col0), "r"(smem_u32(bar)), "l"(policy)
+                 : "memory");
+}
+AS_DEV void tma_bulk_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTmaThreads, 1) detect_pairs_tma(const DevArgs* args, int64_t n, DevState* st,
+                                                                  const T* diag, int hint) {
+    extern __shared__ __align__(128) unsigned char smem_tma[];
+    constexpr int kTileElems = kTile * kTile;
+    T* ring = (T*)smem_tma;                                       // kTmaSlots tiles
+    T* dsl = ring + kTmaSlots * kTileElems;                       // [3 stages][rows | columns][64]
+    uint64_t* full = (uint64_t*)(dsl + 3 * 2 * kTile);
+    uint64_t* empty = full + kTmaSlots;
+    int* s_I = (int*)(empty + kTmaSlots);                         // per stage: pair (I, J), I < 0: end
+    int* s_J = s_I + kTmaSlots;
+    unsigned* s_known = (unsigned*)(s_J + kTmaSlots);             // per stage: candidates alive when it was issued
+    const unsigned alive0 = *(volatile unsigned*)&st->alive;      // the diagonal pass's verdicts (uniform)
+    if (alive0 == 0u) return;
+    const bool tri = alive0 == AS_FLAG_UPPER || alive0 == AS_FLAG_LOWER;
+    const bool spd_only = alive0 == AS_FLAG_SPD_CANDIDATE;
+    const bool up_only = alive0 == AS_FLAG_UPPER;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long nt = (n + kTile - 1) / kTile;
+    const unsigned total = (unsigned)(nt * (nt + 1) / 2);
+    const int S = tri ? kTmaSlots : kTmaSlots / 2;                // stages
+    const int stage_elems = tri ? kTileElems : 2 * kTileElems;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kTmaSlots; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kTmaConsumers / 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTmaConsumers / 32) {
+        // ---- producer (one thread)
+        if (lane != 0) return;
+        const void* tmap = (const void*)args->tmapA;
+        // the map was written by set_args_kernel2's generic-proxy stores (released there)
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmap) : "memory");
+        // two tickets and one look at pair_kill always in flight: their latencies stay off the loop
+        uint64_t pol;
+        if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        unsigned pk_prev = *(volatile unsigned*)&st->pair_kill;
+        unsigned q = blockIdx.x;
+        unsigned q1 = atomicAdd(&st->pair_ticket, 1u) + gridDim.x;
+        unsigned q2 = atomicAdd(&st->pair_ticket, 1u) + gridDim.x;
+        for (unsigned it = 0;; ++it) {
+            const int sg = (int)(it % (unsigned)S);
+            const unsigned known = alive0 & ~pk_prev;
+            pk_prev = *(volatile unsigned*)&st->pair_kill;
+            mbar_wait(&empty[sg], ((it / (unsigned)S) & 1u) ^ 1u);
+            if (q >= total || known == 0u) {
+                s_I[sg] = -1;
+                mbar_arrive(&full[sg]);
+                break;
+            }
+            long long I, J;
+            pair_of(q, nt, I, J);
+            q = q1; q1 = q2;
+            q2 = atomicAdd(&st->pair_ticket, 1u) + gridDim.x;
+            s_I[sg] = (int)I; s_J[sg] = (int)J; s_known[sg] = known;
+            T* dst = ring + (size_t)sg * stage_elems;
+            const int r0 = (int)(I * kTile), c0 = (int)(J * kTile);
+            if (tri) {
+                mbar_expect_tx(&full[sg], (unsigned)(kTileElems * sizeof(T)));
+                if (up_only) tma_tile_2d(dst, tmap, r0, c0, &full[sg], pol);      // strict lower part must be zero
+                else tma_tile_2d(dst, tmap, c0, r0, &full[sg], pol);              // strict upper part must be zero
+            } else {
+                // only UPPER left: the mirror (upper) tile decides nothing; only LOWER left: the lower tile
+                const bool need_lo = I == J || (known & (AS_FLAG_BANDED | AS_FLAG_UPPER | AS_FLAG_SPD_CANDIDATE));
+                const bool need_up = I != J && (known & (AS_FLAG_BANDED | AS_FLAG_LOWER | AS_FLAG_SPD_CANDIDATE));
+                const bool need_d = (known & AS_FLAG_SPD_CANDIDATE) != 0u;
+                s_known[sg] = known | (need_lo ? 16u : 0u) | (need_up ? 32u : 0u);
+                mbar_expect_tx(&full[sg], (unsigned)((((need_lo ? 1 : 0) + (need_up ? 1 : 0)) * kTileElems +
+                                                      (need_d ? 2 * kTile : 0)) * sizeof(T)));
+                if (need_lo) tma_tile_2d(dst, tmap, r0, c0, &full[sg], pol);
+                if (need_up) tma_tile_2d(dst + kTileElems, tmap, c0, r0, &full[sg], pol);
+                if (need_d) {
+                    tma_bulk_1d(dsl + sg * 2 * kTile, diag + r0, (unsigned)(kTile * sizeof(T)), &full[sg]);
+                    tma_bulk_1d(dsl + sg * 2 * kTile + kTile, diag + c0, (unsigned)(kTile * sizeof(T)), &full[sg]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers
+    const T tol = T(100) * Eps<T>::v;
+    const T max_diag = (T)dfrom(st->max_diag);
+    bool dead = false;                    // tri / sympd-only: the one candidate is gone
+    unsigned killed = 0u;                 // several candidates: kills this warp has published (lane 0)
+    int my_kl = 0, my_ku = 0;             // several candidates: extents this warp has published (lane 0)
+    for (unsigned it = 0;; ++it) {
+        const int sg = (int)(it % (unsigned)S);
+        mbar_wait(&full[sg], (it / (unsigned)S) & 1u);
+        const int I = s_I[sg], J = s_J[sg];
+        if (I < 0) break;
+        const int D = I - J;
+        const T* lo_s = ring + (size_t)sg * stage_elems;
+        const T* up_s = D != 0 ? lo_s + kTileElems : lo_s;
+        const T* drs = dsl + sg * 2 * kTile;
+        const T* dcs = drs + kTile;
+        const long long r0 = (long long)I * kTile, c0 = (long long)J * kTile;
+        const bool interior = r0 + kTile <= n;
+        if (dead) {
+            // a kill is already published: drain the stages the producer issued before it noticed
+        } else if (tri) {
+            using V2 = typename Vec2<T>::type;
+            const V2* tv = (const V2*)lo_s;
+            bool nz = false;
+            if (D != 0) {
+#pragma unroll
+                for (int k = 0; k < kTileElems / 2 / kTmaConsumers; ++k) {
+                    const V2 x = tv[threadIdx.x + kTmaConsumers * k];
+                    nz |= (x.x != T(0)) | (x.y != T(0));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kTileElems / 2 / kTmaConsumers; ++k) {
+                    const int e = 2 * (threadIdx.x + kTmaConsumers * k), r = e & (kTile - 1), c = e >> 6;
+                    const V2 x = tv[threadIdx.x + kTmaConsumers * k];
+                    // diagonal tile: only the strict triangle on the far side of the candidate counts
+                    const bool in0 = up_only ? r > c : r < c, in1 = up_only ? r + 1 > c : r + 1 < c;
+                    nz |= (in0 & (x.x != T(0))) | (in1 & (x.y != T(0)));
+                }
+            }
+            dead = __any_sync(0xffffffffu, nz);
+            if (dead && lane == 0) atomicOr(&st->pair_kill, alive0);
+        } else if (spd_only) {
+            bool kill = false;
+            if (D > 0 && interior) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int d = warp * 8 + (i >> 1), r = 32 * (i & 1) + lane, c = (r + d) & (kTile - 1);
+                    const T a = lo_s[c * kTile + r], b = up_s[r * kTile + c];
+                    const T aa = fabs(a), ab = fabs(b), delta = fabs(a - b);
+                    kill |= ((delta > tol) & (delta > tol * aa) & (delta > tol * ab)) | (aa >= max_diag) |
+                            (aa + ab >= drs[r] + dcs[c]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int d = warp * 8 + (i >> 1), r = 32 * (i & 1) + lane, c = (r + d) & (kTile - 1);
+                    const long long gi = r0 + r, gj = c0 + c;
+                    if (gi >= n || gj >= n || gi <= gj) continue;
+                    const T a = lo_s[c * kTile + r], b = up_s[r * kTile + c];
+                    const T aa = a < T(0) ? -a : a, ab = b < T(0) ? -b : b;
+                    const T df = a - b;
+                    const T delta = df < T(0) ? -df : df;                           // line 12
+                    const T m = aa > ab ? aa : ab;
+                    if (delta > tol && delta > tol * m) kill = true;                // lines 13-14
+                    if (aa >= max_diag) kill = true;                                // line 15
+                    if (aa + ab >= drs[r] + dcs[c]) kill = true;                    // line 16
+                }
+            }
+            dead = __any_sync(0xffffffffu, kill);
+            if (dead && lane == 0) atomicOr(&st->pair_kill, alive0);
+        } else {
+            // ---- several candidates alive (banded inputs, C2): extents, triangle verdicts, Fig. 4
+            const unsigned known = s_known[sg];
+            const bool has_lo = (known & 16u) != 0u, has_up = (known & 32u) != 0u;
+            T a[16], b[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int d = warp * 8 + (i >> 1), r = 32 * (i & 1) + lane, c = (r + d) & (kTile - 1);
+                a[i] = has_lo ? lo_s[c * kTile + r] : T(0);                          // A(r0 + r, c0 + c)
+                b[i] = D == 0 ? (has_lo ? lo_s[r * kTile + c] : T(0)) : (has_up ? up_s[r * kTile + c] : T(0));   // A(c0 + c, r0 + r)
+            }
+            int kl = 0, ku = 0;
+            bool lnz = false, unz = false;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int d = warp * 8 + (i >> 1), r = 32 * (i & 1) + lane, c = (r + d) & (kTile - 1);
+                const int dist = D * kTile + r - c;                 // row - column of a; column - row of b
+                if (a[i] != T(0)) {
+                    if (dist > 0) { lnz = true; kl = max(kl, dist); }
+                    else if (dist < 0) { unz = true; ku = max(ku, -dist); }          // (diagonal tile only)
+                }
+                if (D != 0 && b[i] != T(0)) { unz = true; ku = max(ku, dist); }
+            }
+            bool kill = false;
+            if ((known & AS_FLAG_SPD_CANDIDATE) && __any_sync(0xffffffffu, lnz | unz)) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int d = warp * 8 + (i >> 1), r = 32 * (i & 1) + lane, c = (r + d) & (kTile - 1);
+                    const long long gi = r0 + r, gj = c0 + c;
+                    if (gi >= n || gj >= n || gi <= gj) continue;
+                    const T aa = a[i] < T(0) ? -a[i] : a[i], ab = b[i] < T(0) ? -b[i] : b[i];
+                    const T df = a[i] - b[i];
+                    const T delta = df < T(0) ? -df : df;                           // line 12
+                    const T m = aa > ab ? aa : ab;
+                    if (delta > tol && delta > tol * m) kill = true;                // lines 13-14
+                    if (aa >= max_diag) kill = true;                                // line 15
+                    if (aa + ab >= drs[r] + dcs[c]) kill = true;                    // line 16
+                }
+            }
+            kl = __reduce_max_sync(0xffffffffu, kl);
+            ku = __reduce_max_sync(0xffffffffu, ku);
+            unsigned k2 = (__any_sync(0xffffffffu, lnz) ? AS_FLAG_UPPER : 0u) |
+                          (__any_sync(0xffffffffu, unz) ? AS_FLAG_LOWER : 0u) |
+                          (__any_sync(0xffffffffu, kill) ? AS_FLAG_SPD_CANDIDATE : 0u);
+            if (lane == 0 && (kl > my_kl || ku > my_ku || (k2 & ~killed))) {
+                int gkl = my_kl, gku = my_ku;
+                if (kl > my_kl) gkl = max(kl, atomicMax(&st->kl, kl));
+                if (ku > my_ku) gku = max(ku, atomicMax(&st->ku, ku));
+                // the other warps' and CTAs' extents count too (the 25% rule is on the pair (kl, ku)); the
+                // final verdict is re-checked on the exact extents by the dispatch
+                if (kl > my_kl || ku > my_ku) {
+                    gkl = max(gkl, *(volatile int*)&st->kl);
+                    gku = max(gku, *(volatile int*)&st->ku);
+                    if (!band_density_ok(n, gkl, gku)) k2 |= AS_FLAG_BANDED;
+                }
+                my_kl = gkl; my_ku = gku;
+                if (k2 & ~killed) atomicOr(&st->pair_kill, k2);
+                killed |= k2;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sg]);
+    }
+}
+
+int detect_tma_plan(int dtype, int64_t n, int64_t lda) {
+    static const int off = getenv("AS_DET_TMA") != nullptr && atoi(getenv("AS_DET_TMA")) == 0;
+    static const int64_t min_n = getenv("AS_DET_TMA_MIN_N") ? atoll(getenv("AS_DET_TMA_MIN_N")) : 1024;
+    const int64_t es = dtype == AS_F64 ? 8 : 4;
+    return !off && n >= min_n && (lda * es) % 16 == 0 && n <= 0x7fffffffll - kTile;
+}
+
 // ------------------------------------------------------------------ dispatch
 // First match in the paper's order: banded, lower, upper, sympd,
 // else general LU; or the forced method.  Sets the SWITCH handle.
@@ -491,8 +773,20 @@ __global__ void finite_b_kernel(const DevArgs* args, int64_t ldb, int64_t n, int
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&st->flags, AS_FLAG_NONFINITE);
 }
 
+template <typename T>
+static void launch_pairs_tma(const Work& w, cudaStream_t s) {
+    const int smem = (int)(sizeof(T) * (kTmaSlots * kTile * kTile + 3 * 2 * kTile) + 2 * kTmaSlots * sizeof(uint64_t) +
+                           3 * kTmaSlots * sizeof(int));
+    const long long nt = (w.n + kTile - 1) / kTile;
+    const int blocks = (int)std::min<long long>(nt * (nt + 1) / 2, (long long)w.num_sms);
+    cudaFuncSetAttribute(detect_pairs_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static const int hint = getenv("AS_DET_TMA_HINT") ? atoi(getenv("AS_DET_TMA_HINT")) : 1;
+    detect_pairs_tma<T><<<blocks, kTmaThreads, smem, s>>>(w.args, w.n, w.st, (const T*)w.diag, hint);
+}
+
 void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite) {
     fullscan = fullscan || check_finite;
+    const int tma = !fullscan && w.det_tma;
     const int dthreads = 256;
     const int dblocks = (int)std::min<int64_t>((w.n + dthreads - 1) / dthreads, 4 * w.num_sms);
     const long long nt = (w.n + kTile - 1) / kTile;
@@ -502,9 +796,10 @@ void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_fini
         const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 2);
         cudaFuncSetAttribute(detect_pairs_v3<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<double><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (double*)w.diag);
-        detect_pairs_v3<double><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
-                                                                              (const double*)w.diag, fullscan,
-                                                                              check_finite);
+        if (tma) launch_pairs_tma<double>(w, s);
+        else detect_pairs_v3<double><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
+                                                                                   (const double*)w.diag, fullscan,
+                                                                                   check_finite);
         if (check_finite && w.nrhs > 0 && w.ldb >= w.n)
             finite_b_kernel<double><<<w.num_sms * 2, 256, 0, s>>>(w.args, w.ldb, w.n, w.nrhs, w.st);
     } else {
@@ -512,9 +807,10 @@ void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_fini
         const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 4);
         cudaFuncSetAttribute(detect_pairs_v3<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<float><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (float*)w.diag);
-        detect_pairs_v3<float><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
-                                                                             (const float*)w.diag, fullscan,
-                                                                             check_finite);
+        if (tma) launch_pairs_tma<float>(w, s);
+        else detect_pairs_v3<float><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
+                                                                                  (const float*)w.diag, fullscan,
+                                                                                  check_finite);
         if (check_finite && w.nrhs > 0 && w.ldb >= w.n)
             finite_b_kernel<float><<<w.num_sms * 2, 256, 0, s>>>(w.args, w.ldb, w.n, w.nrhs, w.st);
     }

@@ -294,7 +294,6 @@ __global__ void __launch_bounds__(s2::NT, 2) gemm_sgemm_nn_kernel(GemmArgs g) {
 // CTA tile 128 x 64 x 16, 4 warps (2 x 2, warp tile 64 x 32 = 8 x 4 DMMA tiles),
 // 3-stage cp.async pipeline, 2 CTAs per SM so one CTA's C read-modify-write
 // epilogue overlaps the other's MMA main loop.
-constexpr int kGemmCfgDefault = 0;
 // tile configuration of the DMMA GEMM: k-tile BK_ and pipeline depth ST_ (the launcher's choice,
 // measured in tools/gemm_bench.py); BM x BN = 128 x 64, 4 warps of 64 x 32
 template <int BK_, int ST_, int NT_ = 128>
@@ -491,130 +490,6 @@ __global__ void __launch_bounds__(d2::NT, 2) gemm_dmma2_kernel(GemmArgs g) {
     if (g.trace_max && threadIdx.x == 0) atomicMax(g.trace_max, gtimer());
 }
 
-// ------------------------------------------------------------------ persistent NN DMMA GEMM (v3)
-// C -= A B for the LU / Cholesky trailing updates (A = L21 panel columns, B = U12 rows, NN).
-// One 256-thread CTA per SM walks 128 x 128 tiles (8 warps of 64 x 32).  The per-tile fixed cost of
-// the one-tile-per-CTA kernel (C into the accumulators, the pipeline fill) -- ~4 us of a 23 us tile
-// at K = 128 -- is moved off the critical path: the next tile's C tile (into shared memory) and its
-// first k-slab are issued by cp.async at the start of the current tile's last k-slab, and the next
-// tile starts from C in shared memory.
-namespace d3 {
-constexpr int BM = 128, BN = 128, BK = 16, ST = 2, NT = 256;
-constexpr int LDA = BM + 4;        // A slab as [k][m]
-constexpr int LDB = BK + 4;        // B slab as [n][k]
-constexpr int LDC = BM + 2;        // C tile as [n][m]
-constexpr int AEL = BK * LDA, BEL = BN * LDB;
-constexpr size_t SMEM = sizeof(double) * ((size_t)ST * (AEL + BEL) + (size_t)BN * LDC);
-}  // namespace d3
-
-AS_DEV void stage_d3(double* As, double* Bs, const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M,
-                     int64_t N, int64_t K, int64_t m0, int64_t n0, int64_t k0) {
-    using namespace d3;
-    for (int e = threadIdx.x; e < BK * (BM / 2); e += NT) {      // BK columns of A, BM contiguous rows
-        const int kk = e / (BM / 2), mm = (e % (BM / 2)) * 2;
-        const int64_t gk = k0 + kk, gm = m0 + mm;
-        int bytes = 0;
-        if (gk < K && gm < M) bytes = (int)(min<int64_t>(2, M - gm) * 8);
-        cp_async16(As + kk * LDA + mm, bytes ? A + gm + gk * lda : A, bytes);
-    }
-    for (int e = threadIdx.x; e < BN * (BK / 2); e += NT) {      // BN columns of B, BK contiguous rows
-        const int nn = e / (BK / 2), kk = (e % (BK / 2)) * 2;
-        const int64_t gk = k0 + kk, gn = n0 + nn;
-        int bytes = 0;
-        if (gn < N && gk < K) bytes = (int)(min<int64_t>(2, K - gk) * 8);
-        cp_async16(Bs + nn * LDB + kk, bytes ? B + gk + gn * ldb : B, bytes);
-    }
-}
-AS_DEV void stage_c3(double* Cs, const double* C, int64_t ldc, int64_t M, int64_t N, int64_t m0, int64_t n0) {
-    using namespace d3;
-    for (int e = threadIdx.x; e < BN * (BM / 2); e += NT) {
-        const int nn = e / (BM / 2), mm = (e % (BM / 2)) * 2;
-        const int64_t gm = m0 + mm, gn = n0 + nn;
-        int bytes = 0;
-        if (gn < N && gm < M) bytes = (int)(min<int64_t>(2, M - gm) * 8);
-        cp_async16(Cs + nn * LDC + mm, bytes ? C + gm + gn * ldc : C, bytes);
-    }
-}
-
-__global__ void __launch_bounds__(d3::NT, 1) gemm_dmma3_kernel(GemmArgs g) {
-    using namespace d3;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* As = (double*)smem_raw;
-    double* Bs = As + ST * AEL;
-    double* Cs = Bs + ST * BEL;
-    const double* A = (const double*)g.A;
-    const double* B = (const double*)g.B;
-    double* C = (double*)g.C;
-    if (g.trace_min && threadIdx.x == 0) atomicMin(g.trace_min, gtimer());
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
-    const int gid = lane >> 2, tig = lane & 3;
-    const int nk = (int)((g.K + BK - 1) / BK);
-    const int64_t mt = (g.M + BM - 1) / BM, ntl = (g.N + BN - 1) / BN, tiles = mt * ntl;
-    int64_t t = blockIdx.x;
-    if (t >= tiles) return;
-    unsigned slot = 0;                                 // running k-slab counter (stage = slot % ST)
-    stage_c3(Cs, C, g.ldc, g.M, g.N, (t % mt) * BM, (t / mt) * BN);
-    stage_d3(As, Bs, A, g.lda, B, g.ldb, g.M, g.N, g.K, (t % mt) * BM, (t / mt) * BN, 0);
-    cp_async_commit();
-    for (; t < tiles; t += gridDim.x) {
-        const int64_t m0 = (t % mt) * BM, n0 = (t / mt) * BN;
-        const int64_t tn = t + gridDim.x;
-        cp_async_wait<0>();
-        __syncthreads();
-        double acc[8][4][2];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) acc[i][j][h] = Cs[(wn + 8 * j + 2 * tig + h) * LDC + wm + 8 * i + gid];
-        for (int kt = 0; kt < nk; ++kt) {
-            if (kt > 0) { cp_async_wait<0>(); }
-            __syncthreads();                           // slab kt visible; slab kt-1 (and Cs) free
-            const unsigned nxt = slot + 1;
-            if (kt + 1 < nk) {
-                stage_d3(As + (nxt % ST) * AEL, Bs + (nxt % ST) * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m0, n0,
-                         (int64_t)(kt + 1) * BK);
-            } else if (tn < tiles) {                   // the next tile's C and first slab
-                const int64_t m1 = (tn % mt) * BM, n1 = (tn / mt) * BN;
-                stage_c3(Cs, C, g.ldc, g.M, g.N, m1, n1);
-                stage_d3(As + (nxt % ST) * AEL, Bs + (nxt % ST) * BEL, A, g.lda, B, g.ldb, g.M, g.N, g.K, m1, n1, 0);
-            }
-            cp_async_commit();
-            const double* as = As + (slot % ST) * AEL;
-            const double* bs = Bs + (slot % ST) * BEL;
-#pragma unroll
-            for (int ks = 0; ks < BK / 4; ++ks) {
-                double af[8], bf[4];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) af[i] = as[(ks * 4 + tig) * LDA + wm + 8 * i + gid];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) bf[j] = -bs[(wn + 8 * j + gid) * LDB + ks * 4 + tig];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-            }
-            slot = nxt;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t r = m0 + wm + 8 * i + gid;
-            if (r >= g.M) continue;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int64_t c = n0 + wn + 8 * j + 2 * tig + h;
-                    if (c < g.N) C[r + c * g.ldc] = acc[i][j][h];
-                }
-        }
-    }
-    cp_async_wait<0>();
-    if (g.trace_max && threadIdx.x == 0) atomicMax(g.trace_max, gtimer());
-}
-
 // ------------------------------------------------------------------ fp64 tensor peak probe
 // Register-resident DMMA loop (CH independent accumulator chains per warp): the fp64 tensor-core
 // roofline denominator.  tools/ubench_dmma.cu swept the shapes on B200: 8 warps x 2 CTAs per SM with
@@ -676,40 +551,21 @@ static void launch_k(K kern, const GemmArgs& g, size_t smem, cudaStream_t s) {
 void launch_gemm_minus(int dtype, const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
     if (dtype == AS_F64) {
-        // AS_GEMM_CFG (A/B measurements): 0 BK 16 x 2 stages (default), 1: 16 x 3, 2: 32 x 2, 3: 32 x 3
-        const char* ce = getenv("AS_GEMM_CFG");
-        const int cfg = ce ? atoi(ce) : kGemmCfgDefault;
-        auto run = [&](auto cfgtag) {
-            using C = decltype(cfgtag);
-            const size_t smem = sizeof(double) * C::ST * (C::AEL + C::BEL);
-            auto go = [&](auto kern) {
-                dim3 grid((unsigned)((g.M + C::BM - 1) / C::BM), (unsigned)((g.N + C::BN - 1) / C::BN));
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kern<<<grid, C::NT, smem, s>>>(g);
-            };
-            if (!g.TA && !g.TB) go(gemm_dmma2_kernel<false, false, C>);
-            else if (!g.TA && g.TB) go(gemm_dmma2_kernel<false, true, C>);
-            else if (g.TA && !g.TB) go(gemm_dmma2_kernel<true, false, C>);
-            else go(gemm_dmma2_kernel<true, true, C>);
+        // one tile configuration: 128 x 64 x 16, two stages, 4 warps of 64 x 32, two CTAs per SM.  Measured
+        // against it on B200 (tools/gemm_bench.py history): three stages 74.8 %, k-tiles of 32
+        // 66.8 %, both 58.6 %, a persistent 128 x 128 kernel 64.2 %, 8 warps of 32 x 32 84.6 % alone but
+        // 181 vs 167 ms inside the C5 factorization (no register room left for a panel CTA on the SM)
+        using C = D2<16, 2>;
+        const size_t smem = sizeof(double) * C::ST * (C::AEL + C::BEL);
+        auto go = [&](auto kern) {
+            dim3 grid((unsigned)((g.M + C::BM - 1) / C::BM), (unsigned)((g.N + C::BN - 1) / C::BN));
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<grid, C::NT, smem, s>>>(g);
         };
-        if (cfg == 4 && !g.TA && !g.TB && !g.lower_only && !g.skip) {
-            int dev = 0, sms = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int64_t tiles = ((g.M + d3::BM - 1) / d3::BM) * ((g.N + d3::BN - 1) / d3::BN);
-            cudaFuncSetAttribute(gemm_dmma3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3::SMEM);
-            gemm_dmma3_kernel<<<(unsigned)std::min<int64_t>(tiles, sms), d3::NT, d3::SMEM, s>>>(g);
-            return;
-        }
-        switch (cfg) {
-        case 1: run(D2<16, 3>{}); break;
-        case 2: run(D2<32, 2>{}); break;
-        case 3: run(D2<32, 3>{}); break;
-        case 5: run(D2<16, 2, 256>{}); break;
-        case 6: run(D2<16, 3, 256>{}); break;
-        case 7: run(D2<32, 2, 256>{}); break;
-        default: run(D2<16, 2>{}); break;
-        }
+        if (!g.TA && !g.TB) go(gemm_dmma2_kernel<false, false, C>);
+        else if (!g.TA && g.TB) go(gemm_dmma2_kernel<false, true, C>);
+        else if (g.TA && !g.TB) go(gemm_dmma2_kernel<true, false, C>);
+        else go(gemm_dmma2_kernel<true, true, C>);
     } else {
         // NN with 16-byte aligned operands (the LU trailing update): the v2 kernel
         const bool al = (((uintptr_t)g.A | (uintptr_t)g.B | (uintptr_t)g.C) & 15) == 0 && g.lda % 4 == 0 &&

@@ -16,6 +16,10 @@ struct DevArgs {
     as_report* rep_dev; // optional device report
     as_report* rep_host;// optional mapped pinned host report
     int32_t* ret_dev;   // optional device return code (batched calls)
+    // 2-D TMA tensor map of A (64 x 64 tiles; a CUtensorMap, encoded per call on the host) for the
+    // detection pass's tile pipeline; tma_ok = 0: A or lda not 16-byte aligned, or no driver entry point
+    int32_t tma_ok;
+    alignas(64) unsigned long long tmapA[16];
 };
 
 // Workspace layout of a plan (all device pointers; see api.cu).
@@ -45,12 +49,15 @@ struct Work {
     void* lfbuf;         // leaf LU panel: counters, exchange slots, candidate rows, row-move staging
     void* linv;          // LU: full 128 x 128 inverse of each block's unit-lower L11 (n/128 blocks)
     void* swplan;        // LU: per block, the composed row interchanges (lu.cu SwapPlan)
+    int det_tma;         // plan-level: launch the TMA instantiation of the detection pair pass as well
     int num_sms;
 };
 
 // launchers (each enqueues on `s`; used while capturing the plan's graph)
 void launch_state_init(const Work& w, cudaStream_t s, uint32_t opts, int force_method, double thr, double cut,
                        int max_sweeps);
+// 1: the plan also launches the TMA tile pipeline of the detection pair pass (detect.cu)
+int detect_tma_plan(int dtype, int64_t n, int64_t lda);
 void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite = false);
 void launch_dispatch(const Work& w, cudaStream_t s, cudaGraphConditionalHandle h_method);
 void launch_copy_b_to_x(const Work& w, cudaStream_t s);   // band.cu

@@ -213,7 +213,8 @@ template <typename T>
 __global__ void __launch_bounds__(kPT2, 1) lu_panel2_kernel(T* W, int64_t ldw, int64_t n, int64_t k0, int nbp,
                                                             int64_t* ipiv, DevState* st, unsigned long long* xch,
                                                             unsigned long long seq_base, int use_smem,
-                                                            unsigned long long* tr_min, unsigned long long* tr_max) {
+                                                            unsigned long long* tr_min, unsigned long long* tr_max,
+                                                            unsigned poll_nap) {
     constexpr int WPE = PlW<T>::v;
     unsigned long long* hdr = xch;
     unsigned long long* rowll = xch + kPlHdrWords;
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(kPT2, 1) lu_panel2_kernel(T* W, int64_t ldw, i
                     }
                 }
                 if (__all_sync(0xffffffffu, all)) break;
+                if (poll_nap) __nanosleep(poll_nap);     // P warps spinning on the same header lines
             }
 #pragma unroll
             for (int q = 0; q < kMaxPer; ++q) {
@@ -1778,7 +1780,6 @@ struct LuStreams {
     cudaStream_t hi = nullptr;
     cudaStream_t side = nullptr;   // interchanges into the finished L columns (off the critical path)
     cudaStream_t aux = nullptr;    // second stream of the chunked swap + U12 / trailing GEMM
-    cudaStream_t ch[3] = {nullptr, nullptr, nullptr};   // column-chunk streams 1..3 (chunk 0 runs on the caller's stream)
     cudaEvent_t ev[64];
     cudaEvent_t evl[2];            // dataflow schedule: "block k's panel is ready" (by step parity)
     cudaEvent_t evc[4][2];         // dataflow schedule: chunk q finished step k (by step parity)
@@ -1795,7 +1796,6 @@ static LuStreams& lu_streams() {
         cudaStreamCreateWithPriority(&L.hi, cudaStreamNonBlocking, hi);
         cudaStreamCreateWithPriority(&L.side, cudaStreamNonBlocking, lo);
         cudaStreamCreateWithPriority(&L.aux, cudaStreamNonBlocking, lo);
-        for (auto& c : L.ch) cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, lo);
         for (auto& e : L.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         for (auto& e : L.evl) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         for (auto& r : L.evc) for (auto& e : r) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -1926,8 +1926,9 @@ static void panel_launch(const Work& w, int64_t k0, int nbp, unsigned long long 
     const int slot = (int)(k0 / kBW) * 4 + ((k0 % kBW) ? 2 : 1);
     unsigned long long* tmn = tr.tmin && k0 / kBW < kTraceBlocks ? tr.tmin + slot : nullptr;
     unsigned long long* tmx = tr.tmax && k0 / kBW < kTraceBlocks ? tr.tmax + slot : nullptr;
+    static const unsigned poll_nap = getenv("AS_LU_POLL_NAP") ? (unsigned)atoi(getenv("AS_LU_POLL_NAP")) : 0u;
     cudaLaunchKernelEx(&cfg, kern, (T*)w.W, w.ldw, n, k0, nbp, w.ipiv, w.st, (unsigned long long*)w.cand, seq_base,
-                       use_smem, tmn, tmx);
+                       use_smem, tmn, tmx, poll_nap);
 }
 
 template <typename T>
@@ -2039,8 +2040,10 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
     const bool lookahead = n >= 2048 && getenv("AS_LU_NO_LOOKAHEAD") == nullptr;
     int evi = 0;
     auto ev = [&]() { return LS.ev[(evi++) % 64]; };
-    // AS_LU_SCHED=1: the dataflow schedule below (measured slower on C5 in r02n: 188 vs 170 ms with the
-    // same kernels); default: the block-synchronous look-ahead schedule further down
+    // AS_LU_SCHED=2: two-panel blocks with a K = 256 trailing update (below; r02v: 165.1 vs 166.1 ms on C5,
+    // 147.4 vs 150.6 ms on C5f -- within run-to-run spread, kept opt-in); default: the block-synchronous
+    // look-ahead schedule further down.  A dataflow schedule (fixed column chunks, one stream each, no
+    // per-block join) was measured slower (179.6 vs 167.2 ms) and removed.
     static const int sched = getenv("AS_LU_SCHED") ? atoi(getenv("AS_LU_SCHED")) : 0;
     if (lookahead && sched == 2 && w.linv && w.swplan && n >= 4096) {
         // Two-panel blocks: the trailing update runs with K = 256 (DMMA GEMM 87 % of peak against 82 % at
@@ -2137,76 +2140,6 @@ static void lu_factor_t(const Work& w, cudaStream_t s) {
         cudaEvent_t ej = ev();
         cudaEventRecord(ej, LS.side);
         cudaStreamWaitEvent(s, ej, 0);
-        launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
-        return;
-    }
-    if (lookahead && sched == 1) {
-        // Dataflow schedule.  The trailing columns are split into nch FIXED column chunks (boundaries
-        // multiples of the block width), each with its own stream: chunk q at step k runs
-        // swap + U12 then the GEMM of its columns as soon as (a) block k's panel, inverses and swap
-        // plan exist (ev_linv, from the high-priority stream) and (b) its own step k-1 is done (stream
-        // order).  The high-priority stream carries the critical chain panel(k) -> swap + U12 and GEMM
-        // of block k+1's columns -> panel(k+1); it waits only for the chunk that owns those columns.
-        // No join of all streams per block: the r02 trace showed a 335 us gap between consecutive
-        // bulk GEMMs (42 ms over C5) while the next block's swap + U12 ran alone.
-        // The interchanges into the finished L columns (side stream) wait for every chunk's previous
-        // step: a lagging GEMM(k-1) still reads L21 of block k-1 in the row order of step k-1.
-        const int nch = (int)std::min<int64_t>(4, std::max<int64_t>(1, n / 4096));
-        int64_t Cq[5];
-        for (int q = 0; q <= nch; ++q) Cq[q] = q == nch ? n : (n * q / nch + kBW - 1) / kBW * kBW;
-        cudaStream_t chs[4] = {s, LS.ch[0], LS.ch[1], LS.ch[2]};
-        cudaEvent_t last_ch[4] = {nullptr, nullptr, nullptr, nullptr};
-        cudaEvent_t e_start = ev();
-        cudaEventRecord(e_start, s);
-        cudaStreamWaitEvent(LS.hi, e_start, 0);
-        cudaStreamWaitEvent(LS.side, e_start, 0);
-        for (int q = 1; q < nch; ++q) cudaStreamWaitEvent(chs[q], e_start, 0);
-        block_panels<T>(w, 0, (int)std::min<int64_t>(kBW, n), LS.prio_hi, LS.hi);
-        // dedicated events, double-buffered by step parity: every wait on an event is issued before
-        // its next record two steps later
-        cudaEvent_t ev_linv = LS.evl[0];
-        cudaEventRecord(ev_linv, LS.hi);
-        int step = 0;
-        for (int64_t k0 = 0; k0 < n; k0 += kBW, ++step) {
-            const int bw = (int)std::min<int64_t>(kBW, n - k0);
-            const int64_t kn = k0 + bw;
-            cudaStreamWaitEvent(LS.side, ev_linv, 0);
-            for (int q = 0; q < nch; ++q)
-                if (last_ch[q]) cudaStreamWaitEvent(LS.side, last_ch[q], 0);
-            laswp_launch<T>(w, k0, bw, 0, k0, 0, 0, true, LS.side);   // L columns + row permutation
-            if (kn >= n) break;
-            const int64_t M = n - kn;
-            const int nbw = (int)std::min<int64_t>(kBW, n - kn);
-            const cudaEvent_t ev_cur = ev_linv;       // block k's panel / inverses / swap plan
-            // critical chain (high priority): block k+1's columns, then its panel
-            int q0 = 0;
-            while (q0 + 1 < nch && kn >= Cq[q0 + 1]) ++q0;
-            if (last_ch[q0]) cudaStreamWaitEvent(LS.hi, last_ch[q0], 0);
-            swap_u12_launch<T>(w, k0, bw, kn, kn + nbw, LS.hi);
-            gemm_launch<T>(w, kn, kn, k0, M, nbw, bw, LS.hi, LS.prio_hi, false, (int)(k0 / kBW) * 4 + 3);
-            block_panels<T>(w, kn, nbw, LS.prio_hi, LS.hi);
-            ev_linv = LS.evl[(step + 1) & 1];
-            cudaEventRecord(ev_linv, LS.hi);
-            // the other columns, chunk by chunk
-            for (int q = 0; q < nch; ++q) {
-                const int64_t a0 = std::max<int64_t>(Cq[q], kn + nbw), a1 = Cq[q + 1];
-                if (a0 >= a1) continue;
-                cudaStreamWaitEvent(chs[q], ev_cur, 0);
-                swap_u12_launch<T>(w, k0, bw, a0, a1, chs[q]);
-                gemm_launch<T>(w, kn, a0, k0, M, a1 - a0, bw, chs[q], 0, false, q == q0 ? (int)(k0 / kBW) * 4 + 0 : -1);
-                last_ch[q] = LS.evc[q][step & 1];
-                cudaEventRecord(last_ch[q], chs[q]);
-            }
-        }
-        cudaStreamWaitEvent(s, ev_linv, 0);
-        for (int q = 1; q < nch; ++q)
-            if (last_ch[q]) cudaStreamWaitEvent(s, last_ch[q], 0);
-        cudaEvent_t ej = ev();
-        cudaEventRecord(ej, LS.side);
-        cudaStreamWaitEvent(s, ej, 0);
-        // streams that joined the capture without work since must still rejoin s
-        for (int q = 1; q < nch; ++q)
-            if (!last_ch[q]) { cudaEvent_t e = ev(); cudaEventRecord(e, chs[q]); cudaStreamWaitEvent(s, e, 0); }
         launch_trtri_blocks(w.dtype, w.W, w.ldw, n, w.Dinv1, true, false, w.st, true, w.args, s);
         return;
     }

@@ -339,3 +339,132 @@ def test_estimator_rcond_tight(kind, n):
     assert (rep["flags"] & MASK) == (orep["flags"] & MASK)
     assert orep["rcond"] > 0
     assert abs(rep["rcond"] / orep["rcond"] - 1.0) <= 1e-8, (rep["rcond"], orep["rcond"])
+
+
+# ------------------------------------------------------------------ detection: TMA tile pipeline (single candidate left)
+def _padded(A, lda):
+    """A (n x n) as a column-major device view with leading dimension lda (poison beyond row n)."""
+    n = A.shape[0]
+    big = np.full((lda, n), 7.0, dtype=A.dtype, order="F")
+    big[:n] = A
+    return AS.to_device(big)[:n]
+
+
+def _tma_cases(n, dtype, rng):
+    i, j = np.indices((n, n))
+    dense = rng.standard_normal((n, n))
+    up = np.triu(dense) + np.diag(np.full(n, 3.0))
+    lo = np.tril(dense) + np.diag(np.full(n, 3.0))
+    sym = (dense + dense.T) / (8.0 * n) + np.diag(1.0 + rng.random(n))
+    yield "upper", up
+    yield "lower", lo
+    yield "sympd", sym
+    # one non-zero in the other triangle: next to the diagonal inside a diagonal tile, in an interior
+    # tile, in the last (ragged) tile row, and a -0.0 (a zero) / NaN (a non-zero)
+    spots = [(65, 64), (n // 2 + 3, 70), (n - 1, n // 2), (n - 2, n - 3), (200, 3)]
+    for k, (r, c) in enumerate(spots):
+        M = up.copy(); M[r, c] = 1e-300 if dtype == np.float64 else 1e-30
+        yield f"upper_nz{k}", M
+        M = lo.copy(); M[c, r] = -2.0
+        yield f"lower_nz{k}", M
+    M = up.copy(); M[300, 5] = -0.0
+    yield "upper_negzero", M
+    M = up.copy(); M[301, 5] = np.nan
+    yield "upper_nan", M
+    # Fig. 4 lines 12-16 violated on one element pair (interior pair, diagonal tile, ragged edge tile)
+    for k, (r, c) in enumerate([(n // 2 + 3, 70), (130, 129), (n - 1, n - 66), (n - 1, 64)]):
+        M = sym.copy(); M[r, c] *= 1.0 + 1e-3                      # lines 13-14
+        yield f"sympd_asym{k}", M
+        M = sym.copy(); M[r, c] = M[c, r] = 5.0                     # line 15: |a| >= max diag
+        yield f"sympd_maxdiag{k}", M
+        M = sym.copy(); M[r, c] = M[c, r] = 0.5 * (M[r, r] + M[c, c])   # line 16 (equality kills)
+        yield f"sympd_diagsum{k}", M
+    M = sym.copy(); M[400, 100] = M[100, 400] = np.nan             # NaN compares false: survives Fig. 4
+    yield "sympd_nan", M
+    M = sym.copy(); M[7, 7] = np.nan                               # NaN on the diagonal (line 8: no kill)
+    yield "sympd_nan_diag", M
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("n,pad", [(1024, 0), (1100, 0), (1537, 3), (2049, 7)])
+def test_detect_tma_single_candidate(n, pad, dtype):
+    """n >= 1024 with 16-byte aligned columns and one candidate left after the diagonal pass runs the
+    TMA tile pipeline (detect_pairs_tma): every verdict bit-exact against the oracle, on clean
+    triangular / sympd inputs and with a single deciding element in each kind of tile."""
+    rng = np.random.default_rng(n)
+    lda = n + pad                     # (1537 + 3) and (2049 + 7) are multiples of 4: aligned in fp32 too
+    assert (lda * np.dtype(dtype).itemsize) % 16 == 0
+    for name, M in _tma_cases(n, dtype, rng):
+        A = np.asfortranarray(M.astype(dtype))
+        d = oracle.detect(A)
+        ret, st = AS.as_detect(_padded(A, lda))
+        assert ret == 0
+        assert st["flags"] == d.flags and st["method"] == d.method, (name, n, st, d)
+
+
+def test_detect_tma_matches_direct_path_in_solve():
+    """The same solve with the TMA pass and (lda odd: columns not 16-byte aligned) without it."""
+    n = 1100
+    A, B = W.make("C3b", n=n, nrhs=3)
+    ret, X1, rep1 = gpu_solve(A, B)
+    big = np.full((n + 1, n), 3.0, order="F"); big[:n] = A
+    o = AS.make_options()
+    ret2, X2, rep2 = AS.as_solve_ex(AS.to_device(big)[:n], AS.to_device(B), options=o)
+    torch.cuda.synchronize()
+    assert ret == ret2 == 0 and rep1["flags"] == rep2["flags"] and rep1["method"] == rep2["method"] == oracle.M_TRI_UPPER
+    assert np.array_equal(X1, AS.to_host(X2))
+
+
+def _tma_generic_cases(n, rng):
+    i, j = np.indices((n, n))
+    dense = rng.standard_normal((n, n))
+
+    def band(kl, ku, dom=False):
+        M = np.where((i - j <= kl) & (j - i <= ku), dense, 0.0)
+        if dom:
+            M[np.arange(n), np.arange(n)] = 1.0 + np.abs(M).sum(axis=1)
+        return M
+
+    yield "diagonal", band(0, 0)
+    yield "lower_band", band(5, 0)
+    yield "upper_band", band(0, 7)
+    yield "band_8_8", band(8, 8, dom=True)
+    yield "band_200_3", band(200, 3)
+    yield "band_63_64", band(63, 64)
+    # around the 25% capacity boundary (P:339): n (kl + ku + 1) - ... against n^2 / 4
+    for kl, ku in [(n // 8, n // 8 - 8), (n // 8 + 4, n // 8 + 4), (n // 4 - 40, 0), (0, n // 4 + 40), (n // 7, n // 9)]:
+        yield f"band_{kl}_{ku}", band(kl, ku)
+    sb = band(4, 4)
+    sb = (sb + sb.T) / 20.0
+    sb[np.arange(n), np.arange(n)] = 2.0 + rng.random(n)
+    yield "sympd_band", sb
+    M = sb.copy(); M[n - 3, n - 6] *= 1.0 + 1e-3
+    yield "sympd_band_asym_edge", M
+    M = sb.copy(); M[700, 697] = M[697, 700] = 3.5
+    yield "sympd_band_maxdiag", M
+    # two lone far elements in different tile pairs: each extent passes the 25% rule alone, not together
+    M = np.eye(n); M[n // 3 + 20, 20] = 1.0; M[10, n // 5 + 10] = 1.0
+    yield "two_far_elements", M
+    M = band(1, 1); M[n - 100, 50] = 1e-200
+    yield "tridiag_plus_far", M
+    M = np.tril(band(3, 3)); M[5, 900] = -0.0
+    yield "lower_band_negzero", M
+    M = dense * (rng.random((n, n)) < 0.002); M[np.arange(n), np.arange(n)] = 5.0
+    yield "sparse_random", M
+    yield "dense", dense
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("n,pad", [(1024, 0), (1100, 0), (2049, 7)])
+def test_detect_tma_several_candidates(n, pad, dtype):
+    """Banded / sparse / dense inputs at n >= 1024 through the TMA pair pass with several candidates alive:
+    flags, method and (when banded) the exact extents against the oracle."""
+    rng = np.random.default_rng(n + 1)
+    for name, M in _tma_generic_cases(n, rng):
+        A = np.asfortranarray(M.astype(dtype))
+        d = oracle.detect(A)
+        ret, st = AS.as_detect(_padded(A, n + pad))
+        assert ret == 0
+        assert st["flags"] == d.flags and st["method"] == d.method, (name, n, st, d)
+        if d.banded:
+            assert (st["kl"], st["ku"]) == (d.kl, d.ku), (name, st, d)

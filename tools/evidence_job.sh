@@ -1,8 +1,8 @@
-# r02z: final-tree evidence. Part 1: full GPU suite, smoke, default bench line (every config + batched),
+# Evidence job (run on the GPU box through gpurun; results are copied into profiles/<round>/). Part 1: full GPU suite, smoke, default bench line (every config + batched),
 # reference arm, eager launch lists per config, standard-vs-adaptive.  Part 2: ncu --set full captures
 # of the dominant kernels, summarised on the box (tools/ncu_traffic.py; gpurun copies back <= 64 MiB).
 set -x
-O=gpurun_out/r02z
+O=${1:-gpurun_out/evidence}
 mkdir -p $O
 nproc > $O/host.txt
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,clocks.max.mem --format=csv > $O/gpu.txt 2>&1
@@ -47,3 +47,12 @@ cap jacobi_C4 jacobi 0 python tools/profile_one.py --config C4 --eager --calls 1
 cap potf2_C3a potf2 10 python tools/profile_one.py --config C3a --eager --calls 1
 cap sgemm_C5f sgemm 30 python tools/profile_one.py --config C5f --eager --calls 1
 du -sh $O
+# side measurements (same box, same build): knobs around the defaults
+b() { cfg=$1; name=$2; shift 2; env "$@" timeout 600 python bench.py --config $cfg --only --steps 5 --no-cpu-baseline > $O/ab_${cfg}_$name.json 2> $O/ab_${cfg}_$name.err; }
+b C5 default AS_X=0
+b C5 pollnap32 AS_LU_POLL_NAP=32
+b C5 pollnap100 AS_LU_POLL_NAP=100
+b C5 sched2 AS_LU_SCHED=2
+b C5 sched2_coop AS_LU_SCHED=2 AS_LU_LF_MIN_M=99999
+b C5f sched2 AS_LU_SCHED=2
+b C5f default AS_X=0
