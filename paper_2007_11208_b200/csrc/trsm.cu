@@ -121,6 +121,7 @@ AS_DEV bool ll_get(const unsigned long long* w, unsigned ep, float& x) {
 // (the four quarters are summed through shared memory).  RT >= 4: thread (row i, column
 // group g) owns columns g, g+4, ... over the full k range -> part[0 .. RT/4).
 constexpr int kLDX = kNB + 1;
+template <int RT> struct TsBufs { static constexpr int v = RT == 1 ? 3 : 2; };
 template <int RT> struct TsPer { static constexpr int v = RT == 1 ? 1 : RT / 4; };
 // RT = 4, 8: thread (row i, k-quarter g) accumulates ALL RT columns over its 16 k values (every
 // block element is read once from shared memory, RT independent FMA chains), then the four
@@ -184,12 +185,13 @@ AS_DEV void cp_async_elem(T* smem, const T* gmem, bool ok) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(ok ? 4 : 0) : "memory");
 }
 
-// Shared memory: two T-block buffers (the second one receives Dinv_b during the last step, off
-// the critical path), the X_j tile, and for RT == 1 the k-quarter partials: <= 83 KB, so two
-// or three CTAs fit per SM and every block of an n <= 16384 solve is resident at once.
+// Shared memory: the ring of T-block buffers (Dinv_b is staged as the last entry, off the critical
+// path), the X_j tile and the k-quarter partials: 87 KB (RT = 8) / 101 KB (RT = 1), two CTAs per SM, so
+// every block of an n <= 16384 solve is resident at once.
 template <typename T, int RT>
 constexpr size_t ts_smem() {
-    return sizeof(T) * (2 * kNB * kLDT + (size_t)kLDX * RT + (RT == 1 ? 4 * kNB : RT <= 8 ? (size_t)4 * RT * kNB : 0));
+    return sizeof(T) * ((size_t)TsBufs<RT>::v * kNB * kLDT + (size_t)kLDX * RT +
+                        (RT == 1 ? 4 * kNB : RT <= 8 ? (size_t)4 * RT * kNB : 0));
 }
 
 template <typename T, bool UPPER, bool TRANS, int RT>
@@ -198,9 +200,12 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     if (p.skip_if_singular && st->info != ~0ull) return;
     constexpr int PER = TsPer<RT>::v;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* Mb0 = (T*)smem_raw;                      // kNB x kLDT: T block (double buffered: Mb0, Mb1)
-    T* Mb1 = Mb0 + kNB * kLDT;
-    T* Xs = Mb1 + kNB * kLDT;                   // kLDX x RT: X_j tile (column c at c * kLDX)
+    // ring of NBUF T-block buffers (kNB x kLDT each).  A single-RHS solve is bound by the bytes a CTA keeps
+    // in flight (one 32 KB block per L2 / HBM round trip was 0.4-0.8 us per step: r02 launch lists), so it
+    // stages two blocks ahead; the multi-RHS solves stay double-buffered (two CTAs per SM).
+    constexpr int NBUF = TsBufs<RT>::v;
+    T* Mb0 = (T*)smem_raw;
+    T* Xs = Mb0 + NBUF * kNB * kLDT;            // kLDX x RT: X_j tile (column c at c * kLDX)
     T* Red = Xs + kLDX * RT;                    // RT == 1: 4 x kNB partials
     __shared__ unsigned s_ticket;
 
@@ -228,27 +233,57 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     const int R = min(RT, p.nrhs - c0);
     const int i = threadIdx.x % kNB, g = threadIdx.x / kNB;
 
-    // async staging of op(T)_{b j} (no-trans: A[b rows, j cols]; trans: A[j rows, b cols])
+    // async staging of op(T)_{b j} (no-trans: A[b rows, j cols]; trans: A[j rows, b cols]).  Thread (row i,
+    // column group g) copies elements (i, g + 4 q): one pointer increment per element on full blocks (the
+    // generic index arithmetic was ~25 instructions per element, more than the product itself: ncu r02)
     auto stage = [&](T* dst, int sp) {
         const int j = FWD ? sp : nblk - 1 - sp;
         const int64_t oj = (int64_t)j * kNB;
         const int nbj = (int)min<int64_t>(kNB, n - oj);
-        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-            const int r = e % kNB, c = e / kNB;
-            const bool ok = TRANS ? (r < nbj && c < nbr) : (r < nbr && c < nbj);
-            const T* src = !ok ? A : TRANS ? A + (oj + r) + (ob + c) * p.lda : A + (ob + r) + (oj + c) * p.lda;
-            cp_async_elem(dst + r + c * kLDT, src, ok);
+        if (nbr == kNB && nbj == kNB) {
+            const T* src = TRANS ? A + (oj + i) + (ob + g) * p.lda : A + (ob + i) + (oj + g) * p.lda;
+            const unsigned sa = smem_u32(dst + i + g * kLDT);
+            const int64_t step = 4 * p.lda;
+#pragma unroll
+            for (int q = 0; q < kNB / 4; ++q) {
+                if (sizeof(T) == 8)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + (unsigned)(q * 4 * kLDT * sizeof(T))), "l"(src) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa + (unsigned)(q * 4 * kLDT * sizeof(T))), "l"(src) : "memory");
+                src += step;
+            }
+        } else {
+            for (int e = threadIdx.x; e < kNB * kNB; e += kTsThreads) {
+                const int r = e % kNB, c = e / kNB;
+                const bool ok = TRANS ? (r < nbj && c < nbr) : (r < nbr && c < nbj);
+                const T* src = !ok ? A : TRANS ? A + (oj + r) + (ob + c) * p.lda : A + (ob + r) + (oj + c) * p.lda;
+                cp_async_elem(dst + r + c * kLDT, src, ok);
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto stage_dinv = [&](T* dst) {
-        const T* D = Dinv + (int64_t)b * kNB * kNB;
-        for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) cp_async_elem(dst + (e % kNB) + (e / kNB) * kLDT, D + e, true);
+        const T* D = Dinv + (int64_t)b * kNB * kNB + i + g * kNB;
+        const unsigned sa = smem_u32(dst + i + g * kLDT);
+#pragma unroll
+        for (int q = 0; q < kNB / 4; ++q) {
+            if (sizeof(T) == 8)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + (unsigned)(q * 4 * kLDT * sizeof(T))), "l"(D + q * 4 * kNB) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa + (unsigned)(q * 4 * kLDT * sizeof(T))), "l"(D + q * 4 * kNB) : "memory");
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    T* Ds = (s & 1) ? Mb1 : Mb0;               // the buffer step s would use (free after step s-1)
-    if (s > 0) stage(Mb0, 0);
-    else stage_dinv(Ds);
+    // the staged sequence: op(T) blocks of steps 0 .. s-1, then Dinv_b as "step s"; one commit group per index
+    auto buf = [&](int idx) { return Mb0 + (size_t)(idx % NBUF) * kNB * kLDT; };
+    auto stage_idx = [&](int idx) {
+        if (idx < s) stage(buf(idx), idx);
+        else if (idx == s) stage_dinv(buf(idx));
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    T* Ds = buf(s);
+#pragma unroll
+    for (int q = 0; q < NBUF - 1; ++q) stage_idx(q);
     // acc = B_b for my (row, columns)
     T acc[PER];
 #pragma unroll
@@ -258,28 +293,50 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
     }
 
     T part[PER];
+    constexpr int NE = (kNB * RT + kTsThreads - 1) / kTsThreads;   // published words a thread fetches per step
+    T xv[NE];
+    bool xk[NE];
+    auto spec = [&](int sp2) {
+        const int j2 = FWD ? sp2 : nblk - 1 - sp2;
+        const unsigned long long* src = p.ll + ((int64_t)(j2 * ntiles + rt) * RT) * kNB * LLw<T>::v;
+#pragma unroll
+        for (int q = 0; q < NE; ++q) {
+            const int e = threadIdx.x + q * kTsThreads;
+            xk[q] = e < kNB * RT && ll_get(src + (int64_t)e * LLw<T>::v, ep, xv[q]);
+        }
+    };
+#pragma unroll
+    for (int q = 0; q < NE; ++q) { xv[q] = T(0); xk[q] = false; }
+    if (RT > 1 && s > 0) spec(0);   // (single RHS: measured slower, 232 vs 197 us over C3b's five transposed applies)
     for (int sp = 0; sp < s; ++sp) {
         const int j = FWD ? sp : nblk - 1 - sp;
         const int64_t oj = (int64_t)j * kNB;
         const int nbj = (int)min<int64_t>(kNB, n - oj);
-        T* Ms = (sp & 1) ? Mb1 : Mb0;
-        if (sp + 1 < s) stage((sp & 1) ? Mb0 : Mb1, sp + 1);
-        else stage_dinv(Ds);                    // last step: Dinv_b into the free buffer
-        // X_j (tile rt): each thread spins on its own tagged words until the producer's epoch shows
+        T* Ms = buf(sp);
+        stage_idx(sp + NBUF - 1);               // into the buffer step sp - 1 has just released
+        // X_j (tile rt): each thread spins on its own tagged words until the producer's epoch shows.  The
+        // words of step sp + 1 are read speculatively one step ahead (early blocks are long published: their
+        // L2 round trip then overlaps this step's barrier and product); a stale tag falls back to the spin.
         (void)oj; (void)nbj;
         if (sp + 1 == s) TSP(0);
         {
             const unsigned long long* src = p.ll + ((int64_t)(j * ntiles + rt) * RT) * kNB * LLw<T>::v;
-            for (int e = threadIdx.x; e < kNB * RT; e += blockDim.x) {
-                const int r = e % kNB, c = e / kNB;
-                T x;
-                while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x))
-                    if (RT > 1) __nanosleep(ts_backoff_ns);   // single RHS: few pollers, latency first
-                Xs[r + c * kLDX] = x;
+#pragma unroll
+            for (int q = 0; q < NE; ++q) {
+                const int e = threadIdx.x + q * kTsThreads;
+                if (e < kNB * RT) {
+                    const int r = e % kNB, c = e / kNB;
+                    T x = xv[q];
+                    if (!xk[q])
+                        while (!ll_get(src + (int64_t)e * LLw<T>::v, ep, x))
+                            if (RT > 1) __nanosleep(ts_backoff_ns);   // single RHS: few pollers, latency first
+                    Xs[r + c * kLDX] = x;
+                }
             }
         }
+        if (RT > 1 && sp + 1 < s) spec(sp + 1);
         if (sp + 1 == s) TSP(1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(NBUF - 1) : "memory");
         __syncthreads();
         if (sp + 1 == s) TSP(2);
         block_product<T, TRANS, RT>(Ms, Xs, part, R, Red);

@@ -468,3 +468,46 @@ def test_detect_tma_several_candidates(n, pad, dtype):
         assert st["flags"] == d.flags and st["method"] == d.method, (name, n, st, d)
         if d.banded:
             assert (st["kl"], st["ku"]) == (d.kl, d.ku), (name, st, d)
+
+
+# ------------------------------------------------------------------ Cholesky: two panels per step (K = 128 bulk update)
+_PAIRS_SNIPPET = r"""
+import sys
+import numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import oracle, workloads as W
+import paper_2007_11208_b200 as AS
+from helpers import backward_error, forward_diff
+for n, nrhs in [(640, 3), (1100, 5), (2112, 9)]:
+    A, B = W.make("C3a", n=n, nrhs=nrhs, seed=n)
+    ret, X, rep = AS.as_solve_ex(AS.to_device(A), AS.to_device(B))
+    torch.cuda.synchronize()
+    oret, Xo, orep, _ = oracle.solve(A, B)
+    X = AS.to_host(X)
+    assert ret == oret == 0 and rep["method"] == orep["method"] == oracle.M_CHOL, (ret, rep, orep)
+    assert (rep["flags"] & 0xFFFF) == (orep["flags"] & 0xFFFF)
+    assert backward_error(A, X, B) <= 1e-13
+    assert forward_diff(X, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"]
+    assert abs(np.log2(rep["rcond"] / orep["rcond"])) <= 1.0
+# not positive definite in the second panel of a pair: falls back to LU exactly like the oracle
+A, B = W.make("C3a", n=700, nrhs=2, seed=5)
+A[100, 100] = 0.01
+A = np.asfortranarray(A)
+ret, X, rep = AS.as_solve_ex(AS.to_device(A), AS.to_device(B))
+torch.cuda.synchronize()
+oret, Xo, orep, _ = oracle.solve(A, B)
+assert ret == oret and (rep["flags"] & 0xFFFF) == (orep["flags"] & 0xFFFF) and rep["method"] == orep["method"], (rep, orep)
+print("pairs ok")
+"""
+
+
+def test_chol_paired_panels_small_n():
+    """The paired-panel Cholesky schedule (default for n >= 6144) forced down to n >= 512 in a child
+    process (the threshold is read once per process): oracle parity incl. the failure -> LU branch."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AS_CHOL_PAIRS_MIN_N="512")
+    r = subprocess.run([sys.executable, "-c", _PAIRS_SNIPPET.format(root=root, tests=os.path.join(root, "tests"))],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "pairs ok" in r.stdout, r.stdout + r.stderr
