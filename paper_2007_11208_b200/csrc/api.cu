@@ -92,23 +92,53 @@ __global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned v) {
     if (threadIdx.x == 0) cudaGraphSetConditional(h, v);
 }
 
-// triangular path prep: first exact-zero diagonal (singular), triangle 1-norm
+// triangular path prep: first exact-zero diagonal (singular), triangle 1-norm.  One CTA per column pair
+// (u, n-1-u): n + 1 elements together whatever u, every load of a column in flight at once (a warp per
+// column left the longest column, n / 32 dependent rounds on one warp, as the kernel's critical path);
+// the eight warp sums of a column are added in a fixed order (no floating-point atomics: Z25).
 template <typename T>
-__global__ void tri_prep_kernel(const DevArgs* args, int64_t lda, int64_t n, DevState* st, int upper) {
+__global__ void __launch_bounds__(256) tri_prep_kernel(const DevArgs* args, int64_t lda, int64_t n, DevState* st, int upper) {
     const T* A = (const T*)args->A;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ T wsum[2][8];
     double best = 0.0;
     unsigned long long info = ~0ull;
-    for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += warps) {
-        const int64_t i0 = upper ? 0 : j, i1 = upper ? j : n - 1;
-        T s = T(0);
-        for (int64_t i = i0 + lane; i <= i1; i += 32) { const T a = A[i + j * lda]; s += a < T(0) ? -a : a; }
-        s = warp_sum(s);
-        if ((double)s > best || s != s) best = (double)s;
-        if (lane == 0 && A[j + j * lda] == T(0) && (unsigned long long)(j + 1) < info) info = (unsigned long long)(j + 1);
+    for (int64_t u = blockIdx.x; u < (n + 1) / 2; u += gridDim.x) {
+        T s[2] = {T(0), T(0)};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j = h ? n - 1 - u : u;
+            if (h && j == u) break;
+            const int64_t i0 = upper ? 0 : j, i1 = upper ? j : n - 1;
+            const T* col = A + j * lda;
+            T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+            for (int64_t i = i0 + threadIdx.x; i <= i1; i += 4 * 256) {
+                const T v0 = col[i];
+                const T v1 = i + 256 <= i1 ? col[i + 256] : T(0);
+                const T v2 = i + 512 <= i1 ? col[i + 512] : T(0);
+                const T v3 = i + 768 <= i1 ? col[i + 768] : T(0);
+                a0 += v0 < T(0) ? -v0 : v0; a1 += v1 < T(0) ? -v1 : v1;
+                a2 += v2 < T(0) ? -v2 : v2; a3 += v3 < T(0) ? -v3 : v3;
+            }
+            s[h] = warp_sum((a0 + a1) + (a2 + a3));
+        }
+        __syncthreads();                 // the previous pair's sums have been read
+        if (lane == 0) { wsum[0][warp] = s[0]; wsum[1][warp] = s[1]; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = h ? n - 1 - u : u;
+                if (h && j == u) break;
+                T t = T(0);
+#pragma unroll
+                for (int w = 0; w < 8; ++w) t += wsum[h][w];
+                if ((double)t > best || t != t) best = (double)t;
+                if (A[j + j * lda] == T(0) && (unsigned long long)(j + 1) < info) info = (unsigned long long)(j + 1);
+            }
+        }
     }
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         if (best > 0.0) atomicMax(&st->anorm_bits, dbits(best));
         if (info != ~0ull) atomicMin(&st->info, info);
     }
@@ -230,8 +260,9 @@ struct Builder {
 };
 
 static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
-    if (w.dtype == AS_F64) tri_prep_kernel<double><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
-    else tri_prep_kernel<float><<<w.num_sms * 4, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((w.n + 1) / 2, (int64_t)w.num_sms * 16));
+    if (w.dtype == AS_F64) tri_prep_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
+    else tri_prep_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
     launch_trtri_blocks(w.dtype, nullptr, w.lda, w.n, w.Dinv0, upper, false, w.st, true, w.args, s);
 }
 

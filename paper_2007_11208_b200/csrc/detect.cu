@@ -107,18 +107,23 @@ __global__ void detect_diag_kernel(const DevArgs* args, int64_t lda, int64_t n, 
     const T* A = (const T*)args->A;
     double local = 0.0;
     bool kill = false;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        T a = A[j + j * lda];
+    // block reduce
+    __shared__ double smax[32];
+    __shared__ int skill;
+    const int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, jstep = (int64_t)gridDim.x * blockDim.x;
+    // the first diagonal element is requested before the corner check, whose own loads and barrier then
+    // overlap its latency (block 0 used to pay the two DRAM round trips one after the other)
+    T a_next = j0 < n ? A[j0 + j0 * lda] : T(1);
+    if (threadIdx.x == 0) skill = 0;
+    __syncthreads();
+    if (blockIdx.x == 0 && blockDim.x == 256 && n >= 2 * kTile) corner_pair<T>(A, lda, n, st);
+    for (int64_t j = j0; j < n; j += jstep) {
+        const T a = a_next;
+        if (j + jstep < n) a_next = A[(j + jstep) + (j + jstep) * lda];
         diag[j] = a;
         if (a <= T(0)) kill = true;                 // line 8 (NaN: false -> no kill)
         if (a > T(0) && (double)a > local) local = (double)a;   // line 9
     }
-    // block reduce
-    __shared__ double smax[32];
-    __shared__ int skill;
-    if (threadIdx.x == 0) skill = 0;
-    __syncthreads();
-    if (blockIdx.x == 0 && blockDim.x == 256 && n >= 2 * kTile) corner_pair<T>(A, lda, n, st);
     for (int o = 16; o > 0; o >>= 1) local = fmax(local, __shfl_xor_sync(0xffffffffu, local, o));
     if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = local;
     if (kill) skill = 1;

@@ -511,3 +511,31 @@ def test_chol_paired_panels_small_n():
     r = subprocess.run([sys.executable, "-c", _PAIRS_SNIPPET.format(root=root, tests=os.path.join(root, "tests"))],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "pairs ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_detect_tma_alignment_is_part_of_the_plan():
+    """Same n and lda, A 16-byte aligned (TMA pair pass) and offset by one element (register-direct pass),
+    alternating on one stream: two plans, identical verdicts and solutions."""
+    n, nrhs = 1100, 2
+    A, B = W.make("C3a", n=n, nrhs=nrhs, seed=3)
+    flat = torch.empty(n * n + 1, dtype=torch.float64, device="cuda")
+    views = []
+    for off in (0, 1):
+        v = flat[off:off + n * n].view(n, n).t()
+        assert (v.data_ptr() % 16 == 0) == (off == 0)
+        views.append(v)
+    dB = AS.to_device(B)
+    outs = []
+    for rep_i in range(2):
+        for v in views:
+            v.copy_(torch.from_numpy(A).to("cuda"))
+            ret, st = AS.as_detect(v)
+            assert ret == 0
+            ret2, X, rep = AS.as_solve_ex(v, dB)
+            torch.cuda.synchronize()
+            assert ret2 == 0
+            outs.append((st["flags"], st["method"], rep["flags"], AS.to_host(X)))
+    d = oracle.detect(A)
+    for fl, m, rf, X in outs:
+        assert fl == d.flags and m == d.method and rf == outs[0][2]
+        assert np.array_equal(X, outs[0][3])
