@@ -259,11 +259,32 @@ struct Builder {
     }
 };
 
+// The 1-norm / zero-diagonal pass streams the whole triangle while the diagonal-block inverses touch only
+// n / 64 blocks: the two run side by side (a second captured stream).  The inverses' "skip if singular"
+// test may then miss a zero diagonal found concurrently; their output is unused in that case (every
+// solve checks the flag itself).
+struct TriStreams {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[2];
+};
+static TriStreams& tri_streams() {
+    static thread_local TriStreams S;
+    if (!S.aux) {
+        cudaStreamCreateWithFlags(&S.aux, cudaStreamNonBlocking);
+        for (auto& e : S.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    return S;
+}
 static void tri_prep(const Work& w, bool upper, cudaStream_t s) {
+    TriStreams& TS = tri_streams();
+    cudaEventRecord(TS.ev[0], s);
+    cudaStreamWaitEvent(TS.aux, TS.ev[0], 0);
+    launch_trtri_blocks(w.dtype, nullptr, w.lda, w.n, w.Dinv0, upper, false, w.st, true, w.args, TS.aux);
+    cudaEventRecord(TS.ev[1], TS.aux);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((w.n + 1) / 2, (int64_t)w.num_sms * 16));
     if (w.dtype == AS_F64) tri_prep_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
     else tri_prep_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st, upper);
-    launch_trtri_blocks(w.dtype, nullptr, w.lda, w.n, w.Dinv0, upper, false, w.st, true, w.args, s);
+    cudaStreamWaitEvent(s, TS.ev[1], 0);
 }
 
 // Z = [B | e/n | alt] (ld n): the triangular path solves the primary system together with the two

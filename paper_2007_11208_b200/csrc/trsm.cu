@@ -347,7 +347,10 @@ __global__ void __launch_bounds__(kTsThreads) trsm_sf_kernel(TsArgs p, const Dev
         } else {
 #pragma unroll
             for (int u = 0; u < PER; ++u) acc[u] -= part[u];
-            __syncthreads();                    // Ms / Xs reused by the next step
+            // Ms / Xs are reused by the next step.  RT = 4, 8: the product's own barrier (after the partial
+            // sums are written) already orders every read of Ms / Xs before the next step's writes, and the
+            // partials are rewritten only after the next step's first barrier: no third barrier per step
+            if (RT > 8) __syncthreads();
         }
     }
     // X_b = Dinv_b * acc  (trans: Dinv_b^T)

@@ -489,6 +489,16 @@ for n, nrhs in [(640, 3), (1100, 5), (2112, 9)]:
     assert backward_error(A, X, B) <= 1e-13
     assert forward_diff(X, Xo) <= 1e-15 * orep["anorm"] / orep["rcond"]
     assert abs(np.log2(rep["rcond"] / orep["rcond"])) <= 1.0
+# fp32 through the same schedule, graded against the fp64 oracle on the promoted data
+A, B = W.make("C3a", n=1100, nrhs=4, seed=9)
+A32, B32 = np.asfortranarray(A.astype(np.float32)), np.asfortranarray(B.astype(np.float32))
+ret, X, rep = AS.as_solve_ex(AS.to_device(A32), AS.to_device(B32))
+torch.cuda.synchronize()
+A64, B64 = A32.astype(np.float64), B32.astype(np.float64)
+_, Xr, rr, _ = oracle.solve(A64, B64, no_fallback=True)
+X = AS.to_host(X)
+assert ret == 0 and rep["method"] == oracle.M_CHOL
+assert backward_error(A64, X, B64) <= 1e-5 and forward_diff(X, Xr) <= 1e-6 * rr["anorm"] / rr["rcond"]
 # not positive definite in the second panel of a pair: falls back to LU exactly like the oracle
 A, B = W.make("C3a", n=700, nrhs=2, seed=5)
 A[100, 100] = 0.01
