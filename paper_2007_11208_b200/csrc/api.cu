@@ -491,12 +491,10 @@ static int build_graph(Plan& P) {
         launch_state_init(w, s0, k.opts, k.force, k.thr, k.cut, k.sweeps);
         cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s0);
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[0], s0, cudaEventRecordExternal);
+        if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0,
+                                                          (k.opts & AS_OPT_CHECK_FINITE) != 0);
         cudaGraphConditionalHandle h_method = make_handle(s0, 0);
-        bool dispatched = false;
-        if (!(k.opts & AS_OPT_SKIP_DETECT))
-            dispatched = launch_detect(w, s0, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0,
-                                       (k.opts & AS_OPT_CHECK_FINITE) != 0, true, h_method);
-        if (!dispatched) launch_dispatch(w, s0, h_method);
+        launch_dispatch(w, s0, h_method);
         if (k.instrumented) cudaEventRecordWithFlags(P.ev[1], s0, cudaEventRecordExternal);
         mb = add_cond(s0, h_method, cudaGraphCondTypeSwitch, 6);
         // ---- factor + estimate bodies
@@ -619,11 +617,9 @@ static int run_eager(Plan& P, const DevArgs& a, cudaStream_t s) {
     launch_state_init(w, s, k.opts, k.force, k.thr, k.cut, k.sweeps);
     cudaMemsetAsync(w.flags_ts, 0, 4 * w.flags_ts_len, s);
     if (k.instrumented) cudaEventRecord(P.ev[0], s);
-    bool dispatched = false;
-    if (!(k.opts & AS_OPT_SKIP_DETECT))
-        dispatched = launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0,
-                                   (k.opts & AS_OPT_CHECK_FINITE) != 0, true, 0);
-    if (!dispatched) launch_dispatch(w, s, 0);
+    if (!(k.opts & AS_OPT_SKIP_DETECT)) launch_detect(w, s, (k.opts & (AS_OPT_FULLSCAN | AS_OPT_FORCE_METHOD)) != 0,
+                                                      (k.opts & AS_OPT_CHECK_FINITE) != 0);
+    launch_dispatch(w, s, 0);
     if (k.instrumented) cudaEventRecord(P.ev[1], s);
     int err = rd();
     if (err) return err;

@@ -70,7 +70,7 @@ struct DevState {
     // ---- barriers / counters (zeroed per solve)
     uint32_t bar[4];
     uint32_t epoch;               // solve counter (kept across solves): tags the triangular-solve exchange words
-    uint32_t pair_done;           // CTAs of the TMA pair pass that have finished (the last one dispatches)
+    uint32_t pad3;
 };
 
 // The 25% rule of P:339 on the band capacity count(n,kl,ku) = n(kl+ku+1) - kl(kl+1)/2 - ku(ku+1)/2:

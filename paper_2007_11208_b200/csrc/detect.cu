@@ -511,21 +511,9 @@ AS_DEV void tma_bulk_1d(void* dst, const void* src, unsigned bytes, uint64_t* ba
                  : "memory");
 }
 
-AS_DEV void dispatch_body(DevState* st, cudaGraphConditionalHandle h_method, int use_handle);
-// A CTA of the pair pass is done: the last one of the grid runs the dispatch (one graph node and its launch
-// latency less on the detection stage).  Called by one thread per CTA after its verdict atomics.
-AS_DEV void tma_cta_done(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
-    __threadfence();
-    if (atomicAdd(&st->pair_done, 1u) == gridDim.x - 1u) {
-        __threadfence();
-        dispatch_body(st, h_method, use_handle);
-    }
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kTmaThreads, 1) detect_pairs_tma(const DevArgs* args, int64_t n, DevState* st,
-                                                                  const T* diag, int hint, int fuse_dispatch,
-                                                                  cudaGraphConditionalHandle h_method, int use_handle) {
+                                                                  const T* diag, int hint) {
     extern __shared__ __align__(128) unsigned char smem_tma[];
     constexpr int kTileElems = kTile * kTile;
     T* ring = (T*)smem_tma;                                       // kTmaSlots tiles
@@ -535,12 +523,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) detect_pairs_tma(const DevArgs
     int* s_I = (int*)(empty + kTmaSlots);                         // per stage: pair (I, J), I < 0: end
     int* s_J = s_I + kTmaSlots;
     unsigned* s_known = (unsigned*)(s_J + kTmaSlots);             // per stage: candidates alive when it was issued
-    unsigned* s_done = s_known + kTmaSlots;                       // consumer warps that have left the loop
     const unsigned alive0 = *(volatile unsigned*)&st->alive;      // the diagonal pass's verdicts (uniform)
-    if (alive0 == 0u) {
-        if (fuse_dispatch && threadIdx.x == 0) tma_cta_done(st, h_method, use_handle);
-        return;
-    }
+    if (alive0 == 0u) return;
     const bool tri = alive0 == AS_FLAG_UPPER || alive0 == AS_FLAG_LOWER;
     const bool spd_only = alive0 == AS_FLAG_SPD_CANDIDATE;
     const bool up_only = alive0 == AS_FLAG_UPPER;
@@ -551,7 +535,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) detect_pairs_tma(const DevArgs
     const int stage_elems = tri ? kTileElems : 2 * kTileElems;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kTmaSlots; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kTmaConsumers / 32); }
-        *s_done = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -745,10 +728,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) detect_pairs_tma(const DevArgs
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sg]);
     }
-    if (fuse_dispatch && lane == 0) {
-        __threadfence();                                          // this warp's verdict atomics first
-        if (atomicAdd(s_done, 1u) == kTmaConsumers / 32 - 1) tma_cta_done(st, h_method, use_handle);
-    }
 }
 
 int detect_tma_plan(int dtype, int64_t n, int64_t lda) {
@@ -761,18 +740,16 @@ int detect_tma_plan(int dtype, int64_t n, int64_t lda) {
 // ------------------------------------------------------------------ dispatch
 // First match in the paper's order: banded, lower, upper, sympd,
 // else general LU; or the forced method.  Sets the SWITCH handle.
-AS_DEV void dispatch_body(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
-    // (volatile reads: the TMA pair pass calls this from its last CTA, whose verdict inputs were written by
-    // other CTAs' atomics during the same kernel)
-    const unsigned opts = st->opts;
-    unsigned f = (opts & AS_OPT_SKIP_DETECT) ? 0u : (*(volatile uint32_t*)&st->alive & ~*(volatile uint32_t*)&st->pair_kill);   // skipped: no verdicts
+__global__ void dispatch_kernel(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
+    if (threadIdx.x != 0) return;
+    unsigned f = (st->opts & AS_OPT_SKIP_DETECT) ? 0u : (st->alive & ~st->pair_kill);   // skipped: no verdicts
     // BANDED still alive means no CTA exited early, so kl/ku are the exact extents: the 25% rule on the
     // final pair (two extents raised by different CTAs may each pass alone, Z2/Z3)
-    if ((f & AS_FLAG_BANDED) && !band_density_ok(st->n, *(volatile int32_t*)&st->kl, *(volatile int32_t*)&st->ku)) f &= ~AS_FLAG_BANDED;
+    if ((f & AS_FLAG_BANDED) && !band_density_ok(st->n, st->kl, st->ku)) f &= ~AS_FLAG_BANDED;
     st->det_flags = f;
     int m;
-    if (*(volatile uint32_t*)&st->flags & AS_FLAG_NONFINITE) { m = AS_METHOD_NONE; st->ret = AS_ERR_NONFINITE; }   // Z28
-    else if (opts & AS_OPT_FORCE_METHOD) m = st->force_method;
+    if (st->flags & AS_FLAG_NONFINITE) { m = AS_METHOD_NONE; st->ret = AS_ERR_NONFINITE; }   // Z28
+    else if (st->opts & AS_OPT_FORCE_METHOD) m = st->force_method;
     else if (f & AS_FLAG_BANDED) m = AS_METHOD_BAND;
     else if (f & AS_FLAG_LOWER) m = AS_METHOD_TRI_LOWER;
     else if (f & AS_FLAG_UPPER) m = AS_METHOD_TRI_UPPER;
@@ -781,10 +758,6 @@ AS_DEV void dispatch_body(DevState* st, cudaGraphConditionalHandle h_method, int
     st->method = m;
     st->primary = m;
     if (use_handle) cudaGraphSetConditional(h_method, (unsigned)m);
-}
-__global__ void dispatch_kernel(DevState* st, cudaGraphConditionalHandle h_method, int use_handle) {
-    if (threadIdx.x != 0) return;
-    dispatch_body(st, h_method, use_handle);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -806,23 +779,19 @@ __global__ void finite_b_kernel(const DevArgs* args, int64_t ldb, int64_t n, int
 }
 
 template <typename T>
-static void launch_pairs_tma(const Work& w, cudaStream_t s, int fuse_dispatch, cudaGraphConditionalHandle h_method) {
+static void launch_pairs_tma(const Work& w, cudaStream_t s) {
     const int smem = (int)(sizeof(T) * (kTmaSlots * kTile * kTile + 3 * 2 * kTile) + 2 * kTmaSlots * sizeof(uint64_t) +
-                           3 * kTmaSlots * sizeof(int) + sizeof(unsigned));
+                           3 * kTmaSlots * sizeof(int));
     const long long nt = (w.n + kTile - 1) / kTile;
     const int blocks = (int)std::min<long long>(nt * (nt + 1) / 2, (long long)w.num_sms);
     cudaFuncSetAttribute(detect_pairs_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     static const int hint = getenv("AS_DET_TMA_HINT") ? atoi(getenv("AS_DET_TMA_HINT")) : 1;
-    detect_pairs_tma<T><<<blocks, kTmaThreads, smem, s>>>(w.args, w.n, w.st, (const T*)w.diag, hint, fuse_dispatch, h_method,
-                                                          h_method != 0);
+    detect_pairs_tma<T><<<blocks, kTmaThreads, smem, s>>>(w.args, w.n, w.st, (const T*)w.diag, hint);
 }
 
-bool launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite, bool fuse_dispatch,
-                   cudaGraphConditionalHandle h_method) {
+void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite) {
     fullscan = fullscan || check_finite;
     const int tma = !fullscan && w.det_tma;
-    static const bool fuse_off = getenv("AS_DET_FUSE_DISPATCH") != nullptr && atoi(getenv("AS_DET_FUSE_DISPATCH")) == 0;
-    const int fuse = tma && fuse_dispatch && !fuse_off;
     const int dthreads = 256;
     const int dblocks = (int)std::min<int64_t>((w.n + dthreads - 1) / dthreads, 4 * w.num_sms);
     const long long nt = (w.n + kTile - 1) / kTile;
@@ -832,7 +801,7 @@ bool launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_fini
         const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 2);
         cudaFuncSetAttribute(detect_pairs_v3<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<double><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (double*)w.diag);
-        if (tma) launch_pairs_tma<double>(w, s, fuse, h_method);
+        if (tma) launch_pairs_tma<double>(w, s);
         else detect_pairs_v3<double><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
                                                                                    (const double*)w.diag, fullscan,
                                                                                    check_finite);
@@ -843,14 +812,13 @@ bool launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_fini
         const int pblocks = (int)std::min<long long>(pairs, (long long)w.num_sms * 4);
         cudaFuncSetAttribute(detect_pairs_v3<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         detect_diag_kernel<float><<<std::max(dblocks, 1), dthreads, 0, s>>>(w.args, w.lda, w.n, w.st, (float*)w.diag);
-        if (tma) launch_pairs_tma<float>(w, s, fuse, h_method);
+        if (tma) launch_pairs_tma<float>(w, s);
         else detect_pairs_v3<float><<<std::max(pblocks, 1), kDetThreads, smem, s>>>(w.args, w.lda, w.n, w.st,
                                                                                   (const float*)w.diag, fullscan,
                                                                                   check_finite);
         if (check_finite && w.nrhs > 0 && w.ldb >= w.n)
             finite_b_kernel<float><<<w.num_sms * 2, 256, 0, s>>>(w.args, w.ldb, w.n, w.nrhs, w.st);
     }
-    return fuse != 0;
 }
 
 void launch_dispatch(const Work& w, cudaStream_t s, cudaGraphConditionalHandle h_method) {

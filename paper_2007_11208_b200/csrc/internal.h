@@ -58,9 +58,7 @@ void launch_state_init(const Work& w, cudaStream_t s, uint32_t opts, int force_m
                        int max_sweeps);
 // 1: the plan also launches the TMA tile pipeline of the detection pair pass (detect.cu)
 int detect_tma_plan(int dtype, int64_t n, int64_t lda);
-// returns true when the pair pass also ran the dispatch (fuse_dispatch and the TMA pair pass): no launch_dispatch then
-bool launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite = false, bool fuse_dispatch = false,
-                   cudaGraphConditionalHandle h_method = 0);
+void launch_detect(const Work& w, cudaStream_t s, bool fullscan, bool check_finite = false);
 void launch_dispatch(const Work& w, cudaStream_t s, cudaGraphConditionalHandle h_method);
 void launch_copy_b_to_x(const Work& w, cudaStream_t s);   // band.cu
 void launch_band_chain(const Work& w, cudaStream_t s);    // band_chain.cu: kl, ku <= 3 (factor + rcond + X)
