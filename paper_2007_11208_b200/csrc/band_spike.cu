@@ -799,32 +799,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) band_spike_kernel(SpikeArgs a) 
     if (cta == 0 && threadIdx.x == 0) st->band_fast = 1;
 }
 
-// ------------------------------------------------------------------ dominance check
-// strict diagonal dominance by rows or by columns over the band (flag: st->band_dom)
-template <typename T>
-__global__ void band_dominance_kernel(const DevArgs* args, int64_t lda, int64_t n, DevState* st) {
-    const T* A = (const T*)args->A;
-    const int64_t kl = st->kl, ku = st->ku;
-    int row_ok = 1, col_ok = 1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        T rs = T(0), cs = T(0);
-        const int64_t j0 = i - kl > 0 ? i - kl : 0, j1 = i + ku < n - 1 ? i + ku : n - 1;
-        for (int64_t j = j0; j <= j1; ++j) if (j != i) { const T v = A[i + j * lda]; rs += v < T(0) ? -v : v; }
-        const int64_t r0 = i - ku > 0 ? i - ku : 0, r1 = i + kl < n - 1 ? i + kl : n - 1;
-        for (int64_t r = r0; r <= r1; ++r) if (r != i) { const T v = A[r + i * lda]; cs += v < T(0) ? -v : v; }
-        const T d = A[i + i * lda];
-        const T ad = d < T(0) ? -d : d;
-        if (!(ad > rs)) row_ok = 0;
-        if (!(ad > cs)) col_ok = 0;
-    }
-    row_ok = __syncthreads_and(row_ok);
-    col_ok = __syncthreads_and(col_ok);
-    if (threadIdx.x == 0) {
-        if (!row_ok) atomicAnd(&st->band_dom, ~1u);
-        if (!col_ok) atomicAnd(&st->band_dom, ~2u);
-    }
-}
-
+// ------------------------------------------------------------------ mode selection
+// (strict diagonal dominance by rows or by columns: st->band_dom, set by band_norm_kernel in band.cu)
 // feasible_mask bit c: the K = 2^c variant was captured (fits in shared memory, enough SMs)
 __global__ void band_mode_kernel(const DevArgs* args, DevState* st, cudaGraphConditionalHandle h, int feasible_mask) {
     if (threadIdx.x != 0) return;
@@ -941,10 +917,7 @@ void launch_band_spike(const Work& w, int cls, cudaStream_t s) {
 }
 
 void launch_band_dominance(const Work& w, cudaGraphConditionalHandle h, cudaStream_t s) {
-    const int blocks = w.num_sms * 2;
     const int mask = w.dtype == AS_F64 ? feasible_mask_t<double>(w.n, w.num_sms) : feasible_mask_t<float>(w.n, w.num_sms);
-    if (w.dtype == AS_F64) band_dominance_kernel<double><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
-    else band_dominance_kernel<float><<<blocks, 256, 0, s>>>(w.args, w.lda, w.n, w.st);
     band_mode_kernel<<<1, 32, 0, s>>>(w.args, w.st, h, mask);
 }
 
