@@ -25,7 +25,9 @@
  *    the caller and must hold ldb*nrhs elements; X == B (exact alias, in-place
  *    solve) is allowed, any other overlap is undefined.  Factors live in a
  *    library-owned workspace cached per (device, stream, dtype, n, nrhs, lda,
- *    ldb, options) and released by as_release_all().  Calls on different
+ *    ldb, options, 16-byte alignment of A: aligned matrices with 16-byte
+ *    aligned columns take the TMA detection pass, n >= 1024) and released by
+ *    as_release_all().  Calls on different
  *    streams therefore never share a workspace; calls on one stream are
  *    ordered by the stream.
  *  - Streams: all device work is enqueued on `stream`; the call synchronizes
